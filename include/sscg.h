@@ -1,0 +1,197 @@
+/*
+ * sscg.h -- C ABI of the B200-native adaptive s-step CG hot path
+ * (arXiv 1908.04081, improved adaptive s-step CG, Alg. 4).
+ *
+ * Plain C types only (no torch / no CUDA types), caller-owned HOST buffers,
+ * integer status codes + a thread-local last-error string, an opaque plan
+ * handle.  A plan is not thread-safe; independent plans may be used from
+ * different threads (the reference allows concurrent independent solves,
+ * SPEC.md:490-491).
+ *
+ * The reference has no FFI of its own: its boundary is the Python function
+ * `sstepcg.adaptive.adaptive_solve(problem, cfg)` (adaptive.py:111) and the
+ * helpers it calls.  Each entry point below names the reference interface it
+ * replaces; paper_1908_04081_b200/_lib.py binds them with ctypes and
+ * INTEGRATION.md shows the stub a maintainer of the reference would add.
+ */
+#ifndef SSCG_H
+#define SSCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSCG_ABI_VERSION 1
+#define SSCG_MAX_SIGMA 16 /* 2*sigma+1 <= 33 basis columns */
+
+/* status codes */
+#define SSCG_OK 0
+#define SSCG_EINVAL 1  /* bad argument (reference: ValueError)            */
+#define SSCG_ECUDA 2   /* CUDA runtime / launch failure                   */
+#define SSCG_ENOMEM 3  /* device allocation failed                        */
+#define SSCG_EPARAM 4  /* basis.py:31 ParameterError                      */
+#define SSCG_ENODEV 5  /* no CUDA device: there is no CPU fallback         */
+#define SSCG_EBREAKDOWN 6 /* basis.py:35 BasisBreakdownError (non-finite column) */
+
+/* solve outcome (trace.converged / stagnated / diverged, trace.py:43-45) */
+#define SSCG_RUNNING 0
+#define SSCG_CONVERGED 1
+#define SSCG_STAGNATED 2
+#define SSCG_DIVERGED 3
+
+/* basis kinds (basis.py:166-177) and c strategies (ritz.py:184-203) */
+#define SSCG_BASIS_MONOMIAL 0
+#define SSCG_BASIS_NEWTON 1
+#define SSCG_BASIS_CHEBYSHEV 2
+#define SSCG_C_ADAPTIVE 0
+#define SSCG_C_UNIT 1
+#define SSCG_C_KAPPA 2
+#define SSCG_C_FULLBOUND 3
+
+/* per-outer integer record columns (OuterLoopRecord, adaptive.py:74-86) */
+#define SSCG_REC_K 0
+#define SSCG_REC_SBAR 1
+#define SSCG_REC_STILDE 2
+#define SSCG_REC_SACTUAL 3
+#define SSCG_REC_BREAKJ 4   /* -1 = None */
+#define SSCG_REC_MARK 5     /* trace.outer_marks entry */
+#define SSCG_REC_PKIND 6    /* basis kind of basis_params_used */
+#define SSCG_REC_NI 8
+/* per-outer double record columns */
+#define SSCG_RECD_PHI 0
+#define SSCG_RECD_BLHS 1
+#define SSCG_RECD_BRHS 2
+#define SSCG_RECD_GEN_LO 3  /* basis_params_used.generated_from (NaN = None) */
+#define SSCG_RECD_GEN_HI 4
+#define SSCG_RECD_TRUE 5    /* ||b - A x||/||b|| at the start of this outer loop */
+#define SSCG_RECD_RREL 6    /* ||r||/||b|| used by select_s_tilde */
+#define SSCG_RECD_C 7       /* c_sel used by select_s_tilde */
+#define SSCG_RECD_ND 8
+/* per-iteration double log columns (SolveTrace.record_iteration, trace.py:50-58) */
+#define SSCG_IT_ALPHA 0
+#define SSCG_IT_BETA 1
+#define SSCG_IT_TRUE 2
+#define SSCG_IT_UPD 3
+#define SSCG_IT_GAP 4
+#define SSCG_IT_XI 5      /* c_values (xi_estimate, ritz.py:154-158) */
+#define SSCG_IT_LMIN 6
+#define SSCG_IT_LMAX 7
+#define SSCG_IT_PSI 8
+#define SSCG_IT_EST 9     /* Gram quadrature sqrt(max(0, r'^T G r'))/||b|| */
+#define SSCG_IT_N 10
+
+/* AdaptiveConfig (adaptive.py:36-71) + the problem scalars it consults */
+typedef struct sscg_config {
+  int32_t sigma;
+  int32_t s_bar0;
+  int32_t f;
+  int32_t basis_kind;
+  int32_t c_strategy;
+  int32_t variant;     /* 0 = old, 1 = improved */
+  int32_t max_outer;
+  int32_t leja_grid;
+  int32_t has_bounds;  /* spectral_bounds given (old variant / monomial path) */
+  int32_t trace_full;  /* 1: per-inner-iteration true residual (adaptive.py:205-215) */
+  int32_t n_a;         /* max row population (full-bound c) */
+  int32_t reserved;
+  double eps_star;
+  double bound_lo, bound_hi;
+  double norm_a, norm_abs_a, kappa_a; /* ProblemInstance scalars (adaptive.py:119,153) */
+} sscg_config;
+
+/* Caller-owned host log buffers, filled by sscg_fetch / sscg_solve. */
+typedef struct sscg_logs {
+  int64_t cap_iters;   /* rows of `iters`                        */
+  int64_t cap_outer;   /* rows of rec_i / rec_d / conds / params */
+  double* iters;       /* [cap_iters][SSCG_IT_N]                 */
+  int32_t* rec_i;      /* [cap_outer][SSCG_REC_NI]                */
+  double* rec_d;       /* [cap_outer][SSCG_RECD_ND]               */
+  double* conds;       /* [cap_outer][SSCG_MAX_SIGMA+1] cond_used */
+  double* thetas;      /* [cap_outer][SSCG_MAX_SIGMA] params used */
+  double* gammas;      /* [cap_outer][SSCG_MAX_SIGMA]             */
+  double* mus;         /* [cap_outer][SSCG_MAX_SIGMA]             */
+  double* outer_true;  /* [cap_outer+1] ||b-Ax||/||b|| at each outer boundary */
+  double* first_gram;  /* [(2*sigma+1)^2] first block's G, or NULL */
+  /* outputs */
+  int32_t status;      /* SSCG_CONVERGED / STAGNATED / DIVERGED   */
+  int32_t total_iters;
+  int32_t total_outer;
+  int32_t n_records;   /* len(trace.outer_records)                 */
+  int32_t outer_launched; /* outer iterations enqueued (incl. no-op tail) */
+  int32_t reserved;
+  double device_ms;    /* device time of sscg_run (CUDA events)    */
+} sscg_logs;
+
+typedef struct sscg_plan sscg_plan;
+
+const char* sscg_last_error(void);
+int sscg_abi_version(void);
+int sscg_device_count(int32_t* count);
+
+/* ---- plan: device copy of the CSR operator ---------------------------------
+ * Replaces SparseMatrix.as_csr() caching (matio.py:47-53): the matrix is
+ * uploaded once per plan and reused by every solve.  row_ptr int64[n+1],
+ * col_idx int32[nnz] (sorted per row, as scipy leaves it), values f64[nnz]. */
+int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
+                     const int64_t* row_ptr, const int32_t* col_idx, const double* values);
+int sscg_plan_destroy(sscg_plan* plan);
+/* bytes of device memory the plan holds (matrix + work space) */
+int sscg_plan_device_bytes(const sscg_plan* plan, int64_t* bytes);
+
+/* ---- the solve: adaptive.py:111-268 ---------------------------------------
+ * sscg_solve = sscg_load + sscg_run + sscg_fetch (host in, host out). */
+int sscg_solve(sscg_plan* plan, const sscg_config* cfg, const double* b, const double* x0,
+               double* x_out, sscg_logs* logs);
+/* split form: upload b/x0, run entirely on device (inputs resident in HBM;
+ * logs->device_ms = CUDA-event time of the run), download x and the logs. */
+int sscg_load(sscg_plan* plan, const double* b, const double* x0);
+int sscg_run(sscg_plan* plan, const sscg_config* cfg, sscg_logs* logs);
+int sscg_fetch(sscg_plan* plan, double* x_out, sscg_logs* logs);
+/* per-kernel-class device time of the last sscg_run with profiling enabled:
+ * ms[0] mpk level kernels, ms[1] gram, ms[2] small, ms[3] recovery, ms[4] other;
+ * counts[] launches of each class.  enable=1 makes the next runs record one
+ * event pair per launch (no graph replay). */
+int sscg_set_profiling(sscg_plan* plan, int32_t enable);
+int sscg_get_profile(const sscg_plan* plan, double* ms5, int64_t* counts5);
+
+/* ---- unit entry points (parity tests; one kernel family each) ------------- */
+/* lacore.py:25-34 spmv: y = A x (scipy csr_matvec rounding, bit for bit) */
+int sscg_spmv(sscg_plan* plan, const double* x, double* y);
+/* basis.py:228-248 build_block without the condition estimates: y_colmajor
+ * [(2s+1)][n] (P_0..P_s, R_0..R_{s-1}) and g [(2s+1)^2].  Returns
+ * SSCG_EBREAKDOWN on a non-finite column (BasisBreakdownError). */
+int sscg_build_block(sscg_plan* plan, const double* p, const double* r, int32_t s,
+                     const double* thetas, const double* gammas, const double* mus,
+                     double* y_colmajor, double* g);
+/* lacore.py:37-47 gram: G = Y^T Y of a column-major n x k block, k <= 33 */
+int sscg_gram(int32_t device, int64_t n, int32_t k, const double* y_colmajor, double* g);
+/* sstep.py:37-44 recover_iterates: x = x_base + Y xp, r = Y rp, p = Y pp */
+int sscg_recover(int32_t device, int64_t n, int32_t k, const double* y_colmajor,
+                 const double* xp, const double* rp, const double* pp, const double* x_base,
+                 double* x_out, double* r_out, double* p_out);
+/* lacore.py:135-148 nested_basis_conds (conds[0] = NaN) */
+int sscg_nested_conds(int32_t device, const double* g, int32_t s_bar, double* conds);
+/* adaptive.py:89-104 select_s_tilde */
+int sscg_select_s_tilde(int32_t device, const double* g, int32_t s_bar, double c, double unit,
+                        double eps_star, double r_norm, int32_t* s_tilde, double* conds);
+/* basis.py:91-127 leja_points */
+int sscg_leja_points(int32_t device, double lmin, double lmax, int32_t count, int32_t grid,
+                     double* out);
+/* basis.py:166-177 params_for (kind, s, lmin, lmax; has_interval=0 -> None) */
+int sscg_params_for(int32_t device, int32_t kind, int32_t s, int32_t has_interval, double lmin,
+                    double lmax, int32_t grid, double* thetas, double* gammas, double* mus,
+                    int32_t* kind_out);
+/* ritz.py:136-158 RitzState.absorb_step over a sequence; rec[m][6] =
+ * (lambda_min, lambda_max, psi, c, xi_estimate, count) after each step
+ * (nonpositive pairs are skipped, as the callers' BreakdownSignal handlers do) */
+int sscg_ritz_sequence(int32_t device, int32_t m, const double* alpha, const double* beta,
+                       double* rec);
+/* lacore.py:50-100 sym_eig (ascending eigenvalues of a symmetric n x n, n <= 33) */
+int sscg_sym_eig(int32_t device, int32_t n, const double* m, double* w);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSCG_H */

@@ -1,0 +1,350 @@
+"""Generate tests/golden/*.npz by running the REFERENCE package itself.
+
+Test infrastructure only.  Run in the build container, where the reference is
+importable (it does not exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python oracle/make_golden.py
+
+Every fixture records the reference's outputs for seeded inputs built by
+`paper_1908_04081_b200.problems` (or inline seeded numpy), so that
+  * tests/test_oracle_golden.py pins oracle/sscg_oracle.py to the reference, and
+  * the -m gpu parity tests compare the CUDA path with the reference's own
+    numbers without needing the reference at run time.
+The nos1 / 494_bus fixtures store the *preconditioned* problem exactly as the
+reference's `load_problem` builds it (matio.py:291-307), as input vectors.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+REF_SRC = "/root/reference/pkg/src"
+if REF_SRC not in sys.path:
+    sys.path.insert(0, REF_SRC)
+
+import sstepcg  # noqa: E402  (the reference)
+from sstepcg import adaptive as ref_adaptive  # noqa: E402
+from sstepcg import basis as ref_basis  # noqa: E402
+from sstepcg import lacore as ref_lacore  # noqa: E402
+from sstepcg import ritz as ref_ritz  # noqa: E402
+from sstepcg.matio import ProblemInstance as RefProblem  # noqa: E402
+from sstepcg.matio import SparseMatrix as RefSparse  # noqa: E402
+
+from paper_1908_04081_b200 import problems  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+
+
+def save(name, **arrays):
+    path = os.path.join(OUT, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"  wrote {name}.npz ({os.path.getsize(path) / 1024:.1f} KB)")
+
+
+def to_ref(prob):
+    a = prob.a
+    ra = RefSparse(n=a.n, row_ptr=np.asarray(a.row_ptr), col_idx=np.asarray(a.col_idx),
+                   values=np.asarray(a.values), n_a=a.n_a)
+    return RefProblem(a=ra, b=prob.b.copy(), x0=prob.x0.copy(), norm_a=prob.norm_a,
+                      norm_abs_a=prob.norm_abs_a, kappa_a=prob.kappa_a, label=prob.label)
+
+
+def spd_dense(n, kappa, seed):
+    """tests/conftest.py:49-54 style: QR-rotated geomspace spectrum."""
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    return (q * np.geomspace(1.0, kappa, n)) @ q.T
+
+
+def dense_problem(a_dense, label):
+    from scipy import sparse as sp
+    a_dense = np.asarray(a_dense, dtype=float)
+    n = a_dense.shape[0]
+    rows, cols = np.nonzero(a_dense)
+    m = sp.coo_matrix((a_dense[rows, cols], (rows, cols)), shape=(n, n)).tocsr()
+    m.sum_duplicates()
+    m.sort_indices()
+    w = np.linalg.eigvalsh(a_dense)
+    ra = RefSparse(n=n, row_ptr=m.indptr.copy(), col_idx=m.indices.copy(),
+                   values=m.data.copy(), n_a=int(np.diff(m.indptr).max()))
+    return RefProblem(a=ra, b=np.full(n, 1.0 / np.sqrt(n)), x0=np.zeros(n),
+                      norm_a=float(w[-1]), norm_abs_a=float(np.linalg.norm(np.abs(a_dense), 2)),
+                      kappa_a=float(w[-1] / w[0]), label=label)
+
+
+# ---------------------------------------------------------------------------
+def gen_leja():
+    cases = [(1.0, 3.0, 2, 10000), (1.0, 3.0, 5, 10000), (0.0, 4.0, 4, 10**5),
+             (0.5, 2.5, 5, 20000), (1e-6, 2.0, 10, 10000), (0.25, 1.75, 6, 20000)]
+    rng = np.random.default_rng(7001)
+    for _ in range(40):
+        lo = float(10 ** rng.uniform(-4, 1))
+        hi = lo + float(10 ** rng.uniform(-2, 3))
+        cases.append((lo, hi, int(rng.integers(3, 16)), int(rng.choice([1000, 10000]))))
+    lo_a, hi_a, cnt, grid, pts = [], [], [], [], []
+    for lo, hi, c, g in cases:
+        lo_a.append(lo); hi_a.append(hi); cnt.append(c); grid.append(g)
+        p = np.full(16, np.nan)
+        p[:c] = ref_basis.leja_points(lo, hi, c, g)
+        pts.append(p)
+    save("leja", lo=np.array(lo_a), hi=np.array(hi_a), count=np.array(cnt),
+         grid=np.array(grid), points=np.array(pts))
+
+
+def gen_params():
+    rng = np.random.default_rng(7002)
+    rows = []
+    for kind in ("monomial", "newton", "chebyshev"):
+        for _ in range(6):
+            s = int(rng.integers(1, 13))
+            lo = float(rng.uniform(0.01, 1.0))
+            hi = lo + float(rng.uniform(0.1, 10.0))
+            p = ref_basis.params_for(kind, s, lo, hi)
+            b = ref_basis.assemble_change_of_basis(s, p)
+            rows.append((kind, s, lo, hi, p, b))
+    out = {}
+    for i, (kind, s, lo, hi, p, b) in enumerate(rows):
+        out[f"c{i}_meta"] = np.array([["monomial", "newton", "chebyshev"].index(kind), s, lo, hi])
+        out[f"c{i}_thetas"] = p.thetas
+        out[f"c{i}_gammas"] = p.gammas
+        out[f"c{i}_mus"] = p.mus
+        out[f"c{i}_bmat"] = b
+    out["ncases"] = np.array(len(rows))
+    save("params", **out)
+
+
+def gen_ritz():
+    rng = np.random.default_rng(7003)
+    seqs = []
+    for _ in range(30):
+        m = int(rng.integers(1, 40))
+        al = rng.uniform(1e-3, 1e3, m)
+        be = rng.uniform(1e-3, 1e3, m)
+        if rng.random() < 0.3:
+            k = int(rng.integers(0, m))
+            be[k] = -be[k]  # breakdown entries are skipped by the caller
+        seqs.append((al, be))
+    out = {}
+    for i, (al, be) in enumerate(seqs):
+        st = ref_ritz.RitzState()
+        rec = []
+        for a_, b_ in zip(al, be):
+            try:
+                st.absorb_step(a_, b_)
+            except ref_ritz.BreakdownSignal:
+                pass
+            rec.append([st.lambda_min, st.lambda_max, st.psi, st.c, st.xi_estimate(), st.count])
+        out[f"s{i}_alpha"] = al
+        out[f"s{i}_beta"] = be
+        out[f"s{i}_rec"] = np.array(rec)
+    out["nseq"] = np.array(len(seqs))
+    out["full_bound"] = np.array([ref_ritz.full_bound_c(1, 1, 1.0, 1.0, 1.0),
+                                  ref_ritz.full_bound_c(7, 27, 1.3, 2.5, 1e4)])
+    save("ritz", **out)
+
+
+def gen_gram_conds():
+    rng = np.random.default_rng(7004)
+    out = {}
+    cases = []
+    for t in range(24):
+        n = int(rng.integers(20, 400))
+        s_bar = int(rng.integers(1, 13))
+        y = np.empty((n, 2 * s_bar + 1))
+        d = np.geomspace(1.0, float(rng.uniform(2, 1e6)), n)
+        y[:, 0] = rng.standard_normal(n)
+        for k in range(1, s_bar + 1):
+            y[:, k] = d * y[:, k - 1] / np.linalg.norm(d * y[:, k - 1])
+        y[:, s_bar + 1] = rng.standard_normal(n)
+        for k in range(1, s_bar):
+            y[:, s_bar + 1 + k] = d * y[:, s_bar + k]
+        g = ref_lacore.gram(y)
+        conds = ref_lacore.nested_basis_conds(g, s_bar)
+        c = float(10 ** rng.uniform(0, 8))
+        eps_star = float(10 ** rng.uniform(-12, -4))
+        rn = float(10 ** rng.uniform(-8, 0))
+        st, _ = ref_adaptive.select_s_tilde(g, s_bar, c, ref_ritz.MACHINE_UNIT, eps_star, rn)
+        out[f"t{t}_y"] = y
+        out[f"t{t}_g"] = g
+        out[f"t{t}_conds"] = conds
+        out[f"t{t}_sel"] = np.array([s_bar, c, eps_star, rn, st])
+        cases.append(t)
+    # Jacobi eigensolver (full-bound c path)
+    for t in range(6):
+        m = rng.standard_normal((2 * t + 3, 2 * t + 3))
+        m = m + m.T
+        out[f"j{t}_m"] = m
+        out[f"j{t}_w"] = ref_lacore.sym_eig(m)
+    out["ncases"] = np.array(len(cases))
+    save("gram_conds", **out)
+
+
+def gen_blocks():
+    rng = np.random.default_rng(7005)
+    out = {}
+    nc = 0
+    for kind in ("monomial", "newton", "chebyshev"):
+        for t in range(4):
+            n = int(rng.integers(30, 300))
+            s = int(rng.integers(1, 13))
+            a_dense = spd_dense(n, float(rng.uniform(10, 1e4)), seed=9000 + nc)
+            a_dense[np.abs(a_dense) < 0.05 * np.abs(a_dense).max()] = 0.0
+            a_dense = 0.5 * (a_dense + a_dense.T) + n * 0.01 * np.eye(n)
+            prob = dense_problem(a_dense, "blk")
+            p = rng.standard_normal(n)
+            r = rng.standard_normal(n)
+            prm = ref_basis.params_for(kind, s, 0.5, 2.0)
+            blk = ref_basis.build_block(prob.a, p, r, prm, s)
+            out[f"b{nc}_rowptr"] = prob.a.row_ptr
+            out[f"b{nc}_col"] = prob.a.col_idx
+            out[f"b{nc}_val"] = prob.a.values
+            out[f"b{nc}_p"] = p
+            out[f"b{nc}_r"] = r
+            out[f"b{nc}_thetas"] = prm.thetas
+            out[f"b{nc}_gammas"] = prm.gammas
+            out[f"b{nc}_mus"] = prm.mus
+            out[f"b{nc}_y"] = blk.y
+            out[f"b{nc}_g"] = blk.g
+            out[f"b{nc}_s"] = np.array(s)
+            nc += 1
+    out["ncases"] = np.array(nc)
+    save("blocks", **out)
+
+
+def run_ref(prob, cfg_kwargs, store_x=True):
+    cfg = ref_adaptive.AdaptiveConfig(**cfg_kwargs)
+    first_g = {}
+    orig = ref_basis.gram
+
+    def spy(y):
+        g = orig(y)
+        if "g" not in first_g:
+            first_g["g"] = g.copy()
+        return g
+
+    ref_basis.gram = spy
+    try:
+        t0 = time.perf_counter()
+        x, trace, coeffs = ref_adaptive.adaptive_solve(prob, cfg)
+        dt = time.perf_counter() - t0
+    finally:
+        ref_basis.gram = orig
+    recs = trace.outer_records
+    d = dict(
+        alphas=np.array(coeffs.alphas), betas=np.array(coeffs.betas),
+        s_schedule=np.array(trace.s_schedule), outer_marks=np.array(trace.outer_marks),
+        true_resid=np.array(trace.true_resid), upd_resid=np.array(trace.upd_resid),
+        resid_gap=np.array(trace.resid_gap), c_values=np.array(trace.c_values),
+        psi=np.array(trace.psi), lambda_min=np.array(trace.lambda_min),
+        lambda_max=np.array(trace.lambda_max),
+        flags=np.array([trace.converged, trace.stagnated, trace.diverged,
+                        trace.total_iters, trace.total_outer]),
+        rec_int=np.array([[r.k, r.s_bar, r.s_tilde, r.s_actual,
+                           -1 if r.break_j is None else r.break_j] for r in recs]).reshape(-1, 5),
+        rec_float=np.array([[r.phi, r.break_lhs, r.break_rhs] for r in recs]).reshape(-1, 3),
+        rec_thetas=np.array([np.asarray(r.basis_params_used.thetas) for r in recs]),
+        first_g=first_g.get("g", np.zeros((0, 0))),
+        wall=np.array(dt),
+        cfg=np.array(json.dumps(cfg_kwargs)),
+    )
+    if store_x:
+        d["x"] = x
+    # conds of the first 8 outer loops (ragged -> padded)
+    k8 = min(8, len(recs))
+    if k8:
+        w = max(len(r.cond_used) for r in recs[:k8])
+        cm = np.full((k8, w), np.nan)
+        for i in range(k8):
+            cm[i, : len(recs[i].cond_used)] = recs[i].cond_used
+        d["conds8"] = cm
+    print(f"    {prob.label} {cfg_kwargs}: outer={trace.total_outer} total={trace.total_iters} "
+          f"conv={trace.converged} final={trace.final_true_resid:.3e} ({dt:.2f}s)")
+    return d
+
+
+def problem_arrays(prob):
+    a = prob.a
+    return dict(n=np.array(a.n), row_ptr=np.asarray(a.row_ptr), col_idx=np.asarray(a.col_idx),
+                values=np.asarray(a.values), n_a=np.array(a.n_a), b=prob.b, x0=prob.x0,
+                norms=np.array([prob.norm_a, prob.norm_abs_a, prob.kappa_a]))
+
+
+def gen_solves():
+    # BASELINE configs that the reference finishes quickly (c1, c2) -- inputs are
+    # regenerated from the seed, so only outputs are stored
+    c1 = to_ref(problems.make_problem("c1"))
+    save("solve_c1", **run_ref(c1, dict(sigma=8, eps_star=1e-10, basis_kind="newton")))
+    c2 = to_ref(problems.make_problem("c2"))
+    save("solve_c2_cheb", **run_ref(c2, dict(sigma=10, eps_star=1e-8, basis_kind="chebyshev")))
+    save("solve_c2_newton", **run_ref(c2, dict(sigma=10, eps_star=1e-8, basis_kind="newton")))
+    # small proxies of c3 / c4 / c5 (same generators, reduced edge)
+    c3p = to_ref(problems.make_problem("c3", scale=24))
+    save("solve_c3p", **run_ref(c3p, dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev")))
+    c5p = to_ref(problems.make_problem("c5", scale=24))
+    save("solve_c5p", **run_ref(c5p, dict(sigma=12, eps_star=1e-10, basis_kind="newton")))
+    c4p = to_ref(problems.make_problem("c4", scale=12))
+    save("solve_c4p", **run_ref(c4p, dict(sigma=10, eps_star=1e-8, basis_kind="newton",
+                                           max_outer=400)),
+         **{"in_" + k: v for k, v in problem_arrays(c4p).items()})
+
+    # the reference's own acceptance matrices (preconditioned by its load_problem)
+    from sstepcg.matio import load_problem
+    data = "/root/reference/pkg/data/matrices"
+    nos1 = load_problem(os.path.join(data, "nos1.mtx"), label="nos1")
+    bus = load_problem(os.path.join(data, "494_bus.mtx"), label="494bus")
+    save("problem_nos1", **problem_arrays(nos1))
+    save("problem_494bus", **problem_arrays(bus))
+    for kind in ("newton", "chebyshev"):
+        for strat in ("adaptive", "unit", "kappa-estimate"):
+            save(f"solve_nos1_{kind}_{strat}",
+                 **run_ref(nos1, dict(sigma=10, eps_star=1e-6, basis_kind=kind, c_strategy=strat)))
+        save(f"solve_494bus_s15_{kind}",
+             **run_ref(bus, dict(sigma=15, eps_star=1e-6, basis_kind=kind)))
+    save("solve_494bus_old", **run_ref(bus, dict(sigma=5, eps_star=1e-6, variant="old",
+                                                 basis_kind="monomial", c_strategy="unit")))
+    save("solve_494bus_cheb6", **run_ref(bus, dict(sigma=6, eps_star=1e-8, basis_kind="chebyshev")))
+
+    # tests/test_adaptive.py-style dense problems
+    p44 = dense_problem(spd_dense(50, 1e4, 44), "spd50")
+    for kind in ("newton", "chebyshev"):
+        save(f"solve_spd50_{kind}", **run_ref(p44, dict(sigma=6, eps_star=1e-10, basis_kind=kind)),
+             **{"in_" + k: v for k, v in problem_arrays(p44).items()})
+    p43 = dense_problem(spd_dense(40, 50.0, 43), "spd40")
+    for variant in ("old", "improved"):
+        save(f"solve_spd40_s1_{variant}",
+             **run_ref(p43, dict(sigma=1, eps_star=1e-10, variant=variant, basis_kind="monomial")),
+             **{"in_" + k: v for k, v in problem_arrays(p43).items()})
+    p45 = dense_problem(spd_dense(40, 1e3, 45), "spd40fb")
+    save("solve_spd40_fullbound",
+         **run_ref(p45, dict(sigma=4, eps_star=1e-8, basis_kind="newton", c_strategy="full-bound")),
+         **{"in_" + k: v for k, v in problem_arrays(p45).items()})
+    # HSCG alphas for the sigma = 1 cross-check (classic.py:33-104)
+    from sstepcg.classic import hscg_solve
+    _, _, co = hscg_solve(p43, 1e-10)
+    save("hscg_spd40", alphas=np.array(co.alphas), betas=np.array(co.betas))
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    print("reference:", sstepcg.__file__)
+    which = sys.argv[1:] or ["leja", "params", "ritz", "gram_conds", "blocks", "solves"]
+    for w in which:
+        print(w)
+        globals()["gen_" + w]()
+    meta = dict(numpy=np.__version__, generated_by="oracle/make_golden.py",
+                reference="/root/reference/pkg/src/sstepcg")
+    import scipy
+    meta["scipy"] = scipy.__version__
+    with open(os.path.join(OUT, "META.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,192 @@
+"""ctypes binding of the C ABI declared in include/sscg.h.
+
+The library is loaded on first use from paper_1908_04081_b200/_lib/libsscg.so
+(built in-tree by `paper_1908_04081_b200.build`).  A missing library or a
+machine without a CUDA device is an error: there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libsscg.so")
+
+# keep in sync with include/sscg.h
+ABI_VERSION = 1
+MAX_SIGMA = 16
+OK, EINVAL, ECUDA, ENOMEM, EPARAM, ENODEV, EBREAKDOWN = range(7)
+RUNNING, CONVERGED, STAGNATED, DIVERGED = range(4)
+BASIS = {"monomial": 0, "newton": 1, "chebyshev": 2}
+BASIS_NAMES = {v: k for k, v in BASIS.items()}
+CSTRAT = {"adaptive": 0, "unit": 1, "kappa-estimate": 2, "full-bound": 3}
+REC_K, REC_SBAR, REC_STILDE, REC_SACTUAL, REC_BREAKJ, REC_MARK, REC_PKIND = range(7)
+REC_NI = 8
+RECD_PHI, RECD_BLHS, RECD_BRHS, RECD_GEN_LO, RECD_GEN_HI, RECD_TRUE, RECD_RREL, RECD_C = range(8)
+RECD_ND = 8
+IT_ALPHA, IT_BETA, IT_TRUE, IT_UPD, IT_GAP, IT_XI, IT_LMIN, IT_LMAX, IT_PSI, IT_EST = range(10)
+IT_N = 10
+
+EXPORTS = (
+    "sscg_last_error", "sscg_abi_version", "sscg_device_count", "sscg_plan_create",
+    "sscg_plan_destroy", "sscg_plan_device_bytes", "sscg_solve", "sscg_load", "sscg_run",
+    "sscg_fetch", "sscg_set_profiling", "sscg_get_profile", "sscg_spmv", "sscg_build_block",
+    "sscg_gram", "sscg_recover", "sscg_nested_conds", "sscg_select_s_tilde",
+    "sscg_leja_points", "sscg_params_for", "sscg_ritz_sequence", "sscg_sym_eig",
+)
+
+
+class SscgConfig(C.Structure):
+    _fields_ = [
+        ("sigma", C.c_int32), ("s_bar0", C.c_int32), ("f", C.c_int32),
+        ("basis_kind", C.c_int32), ("c_strategy", C.c_int32), ("variant", C.c_int32),
+        ("max_outer", C.c_int32), ("leja_grid", C.c_int32), ("has_bounds", C.c_int32),
+        ("trace_full", C.c_int32), ("n_a", C.c_int32), ("reserved", C.c_int32),
+        ("eps_star", C.c_double), ("bound_lo", C.c_double), ("bound_hi", C.c_double),
+        ("norm_a", C.c_double), ("norm_abs_a", C.c_double), ("kappa_a", C.c_double),
+    ]
+
+
+_DP = C.POINTER(C.c_double)
+_IP = C.POINTER(C.c_int32)
+
+
+class SscgLogs(C.Structure):
+    _fields_ = [
+        ("cap_iters", C.c_int64), ("cap_outer", C.c_int64),
+        ("iters", _DP), ("rec_i", _IP), ("rec_d", _DP), ("conds", _DP),
+        ("thetas", _DP), ("gammas", _DP), ("mus", _DP), ("outer_true", _DP),
+        ("first_gram", _DP),
+        ("status", C.c_int32), ("total_iters", C.c_int32), ("total_outer", C.c_int32),
+        ("n_records", C.c_int32), ("outer_launched", C.c_int32), ("reserved", C.c_int32),
+        ("device_ms", C.c_double),
+    ]
+
+
+class SscgError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"sscg error {code}: {msg}")
+        self.code = code
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def _declare(lib):
+    vp = C.c_void_p
+    i32, i64, dbl = C.c_int32, C.c_int64, C.c_double
+    sig = {
+        "sscg_last_error": (C.c_char_p, []),
+        "sscg_abi_version": (C.c_int, []),
+        "sscg_device_count": (C.c_int, [_IP]),
+        "sscg_plan_create": (C.c_int, [C.POINTER(vp), i32, i64, i64, C.POINTER(i64), _IP, _DP]),
+        "sscg_plan_destroy": (C.c_int, [vp]),
+        "sscg_plan_device_bytes": (C.c_int, [vp, C.POINTER(i64)]),
+        "sscg_solve": (C.c_int, [vp, C.POINTER(SscgConfig), _DP, _DP, _DP, C.POINTER(SscgLogs)]),
+        "sscg_load": (C.c_int, [vp, _DP, _DP]),
+        "sscg_run": (C.c_int, [vp, C.POINTER(SscgConfig), C.POINTER(SscgLogs)]),
+        "sscg_fetch": (C.c_int, [vp, _DP, C.POINTER(SscgLogs)]),
+        "sscg_set_profiling": (C.c_int, [vp, i32]),
+        "sscg_get_profile": (C.c_int, [vp, _DP, C.POINTER(i64)]),
+        "sscg_spmv": (C.c_int, [vp, _DP, _DP]),
+        "sscg_build_block": (C.c_int, [vp, _DP, _DP, i32, _DP, _DP, _DP, _DP, _DP]),
+        "sscg_gram": (C.c_int, [i32, i64, i32, _DP, _DP]),
+        "sscg_recover": (C.c_int, [i32, i64, i32, _DP, _DP, _DP, _DP, _DP, _DP, _DP, _DP]),
+        "sscg_nested_conds": (C.c_int, [i32, _DP, i32, _DP]),
+        "sscg_select_s_tilde": (C.c_int, [i32, _DP, i32, dbl, dbl, dbl, dbl, _IP, _DP]),
+        "sscg_leja_points": (C.c_int, [i32, dbl, dbl, i32, i32, _DP]),
+        "sscg_params_for": (C.c_int, [i32, i32, i32, i32, dbl, dbl, i32, _DP, _DP, _DP, _IP]),
+        "sscg_ritz_sequence": (C.c_int, [i32, i32, _DP, _DP, _DP]),
+        "sscg_sym_eig": (C.c_int, [i32, i32, _DP, _DP]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def load(path=LIB_PATH):
+    """Load (once) and return the ctypes handle of libsscg.so."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise RuntimeError(
+                    f"{path} is missing: build it with `python -m paper_1908_04081_b200.build` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(path)
+            _declare(lib)
+            if lib.sscg_abi_version() != ABI_VERSION:
+                raise RuntimeError("libsscg ABI version mismatch")
+            _lib = lib
+    return _lib
+
+
+def check(rc):
+    if rc != OK:
+        msg = load().sscg_last_error().decode(errors="replace")
+        raise SscgError(rc, msg)
+
+
+def dptr(a):
+    return a.ctypes.data_as(_DP)
+
+
+def iptr(a):
+    return a.ctypes.data_as(_IP)
+
+
+def f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def device_count():
+    n = C.c_int32(0)
+    rc = load().sscg_device_count(C.byref(n))
+    return n.value if rc == OK else 0
+
+
+def require_device(device=0):
+    n = device_count()
+    if device >= n:
+        raise SscgError(ENODEV, f"no CUDA device {device} ({n} visible); this build has no CPU path")
+
+
+class Plan:
+    """Device copy of one CSR operator (owns the sscg_plan handle)."""
+
+    def __init__(self, n, row_ptr, col_idx, values, device=0):
+        lib = load()
+        require_device(device)
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        va = f64(values)
+        h = C.c_void_p()
+        check(lib.sscg_plan_create(C.byref(h), int(device), int(n), int(len(va)),
+                                   rp.ctypes.data_as(C.POINTER(C.c_int64)), iptr(ci), dptr(va)))
+        self.handle = h
+        self.n = int(n)
+        self.nnz = int(len(va))
+        self.device = int(device)
+        self._lib = lib
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self._lib.sscg_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def device_bytes(self):
+        v = C.c_int64(0)
+        check(self._lib.sscg_plan_device_bytes(self.handle, C.byref(v)))
+        return v.value

@@ -1,0 +1,230 @@
+// gram.cu -- K_gram: G = Y^T Y of the tall-skinny fp64 basis, single pass.
+//
+// Reference: lacore.py:37-47 `gram` (OpenBLAS dgemm `y.T @ y`, lower triangle
+// mirrored so G is exactly symmetric).
+//
+// Y (n x k, k = 2 s + 1 <= 33, column-major, ld a multiple of GT_ROWS with the
+// padding rows zeroed at allocation) streams through shared memory in
+// GT_ROWS-row tiles with a GT_STAGES-deep cp.async pipeline; each warp feeds
+// 4-row slices of the tile to the fp64 tensor core (DMMA, mma.m8n8k4.f64): with
+// the column blocks Y_i (8 columns) the warp accumulates the lower-triangular
+// tiles G_ij += Y_i^T Y_j.  The A and B fragments of m8n8k4 have the same
+// layout for a Gram product (thread (g, t) holds Y[row0 + t, 8 i + g]), so one
+// fragment load per column block serves every tile in its row and column.
+// Per-warp accumulators are combined in a fixed warp order, per-CTA partials
+// are written packed, and the last CTA to finish sums them in CTA order:
+// deterministic, one launch, no atomics on data.
+//
+// Roofline: HBM-bound (8 k bytes/row against k(k+1)/2 FMA/row).
+#include "internal.cuh"
+
+namespace {
+
+constexpr int GT_ROWS = 64;
+constexpr int GT_STAGES = 3;
+constexpr int GT_LD = GT_ROWS + 4;  // LD % 16 == 4: conflict-free fragment loads
+constexpr int GT_THREADS = 256;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int NB>
+__device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t ld, int k,
+                                          double* part, double* out, int* counter) {
+  constexpr int T = NB * (NB + 1) / 2;
+  extern __shared__ __align__(16) double gsm[];
+  double* tiles = gsm;                              // [GT_STAGES][NB*8][GT_LD]
+  double* red = gsm + GT_STAGES * NB * 8 * GT_LD;   // [T][64]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t ntiles = ld / GT_ROWS;
+
+  // zero the padding columns (k .. NB*8-1) of every stage once
+  for (int i = tid; i < GT_STAGES * NB * 8 * GT_LD; i += GT_THREADS) {
+    int cc = (i / GT_LD) % (NB * 8);
+    if (cc >= k) tiles[i] = 0.0;
+  }
+  double acc[T][2];
+#pragma unroll
+  for (int q = 0; q < T; ++q) acc[q][0] = acc[q][1] = 0.0;
+
+  const int chunks = k * (GT_ROWS / 2);  // 16-byte chunks per tile
+  auto issue = [&](int64_t tile, int stage) {
+    if (tile < ntiles) {
+      double* dst = tiles + (size_t)stage * NB * 8 * GT_LD;
+      const double* src = Y + tile * GT_ROWS;
+      for (int i = tid; i < chunks; i += GT_THREADS) {
+        int cc = i / (GT_ROWS / 2), rr = (i % (GT_ROWS / 2)) * 2;
+        cp_async16(dst + cc * GT_LD + rr, src + (int64_t)cc * ld + rr);
+      }
+    }
+    cp_commit();
+  };
+
+  int64_t tile = blockIdx.x;
+#pragma unroll
+  for (int s = 0; s < GT_STAGES - 1; ++s) issue(tile + (int64_t)s * gridDim.x, s);
+  int stage = 0;
+  for (; tile < ntiles; tile += gridDim.x) {
+    issue(tile + (int64_t)(GT_STAGES - 1) * gridDim.x, (stage + GT_STAGES - 1) % GT_STAGES);
+    cp_wait<GT_STAGES - 1>();
+    __syncthreads();
+    const double* ts = tiles + (size_t)stage * NB * 8 * GT_LD;
+    // 8 warps x 8 rows = 64 rows: two k-steps of 4 rows per warp
+#pragma unroll
+    for (int ks = 0; ks < GT_ROWS / 32; ++ks) {
+      const int row0 = warp * (GT_ROWS / 8) + ks * 4;
+      double fr[NB];
+#pragma unroll
+      for (int cb = 0; cb < NB; ++cb) fr[cb] = ts[(cb * 8 + g) * GT_LD + row0 + t4];
+      int q = 0;
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j, ++q) dmma(acc[q][0], acc[q][1], fr[i], fr[j]);
+    }
+    __syncthreads();
+    stage = (stage + 1) % GT_STAGES;
+  }
+  cp_wait<0>();
+
+  // combine warps in fixed order: red[q][g*8 + 2 t4 + e]
+  for (int w = 0; w < GT_THREADS / 32; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int q = 0; q < T; ++q) {
+        double* d = red + q * 64 + g * 8 + 2 * t4;
+        if (w == 0) {
+          d[0] = acc[q][0];
+          d[1] = acc[q][1];
+        } else {
+          d[0] += acc[q][0];
+          d[1] += acc[q][1];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // packed lower triangle of this CTA
+  const int npack = k * (k + 1) / 2;
+  for (int e = tid; e < npack; e += GT_THREADS) {
+    int a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (a * (a + 1) / 2 > e) --a;
+    while ((a + 1) * (a + 2) / 2 <= e) ++a;
+    const int b = e - a * (a + 1) / 2;
+    const int bi = a >> 3, bj = b >> 3;
+    const int q = bi * (bi + 1) / 2 + bj;
+    part[(size_t)blockIdx.x * GPACK + e] = red[q * 64 + (a & 7) * 8 + (b & 7)];
+  }
+  // last CTA: fixed-order sum over CTAs, mirror to a full symmetric matrix
+  __threadfence();
+  __shared__ int ticket;
+  __syncthreads();
+  if (tid == 0) ticket = atomicAdd(counter, 1);
+  __syncthreads();
+  if (ticket != (int)gridDim.x - 1) return;
+  __threadfence();
+  const int nb = gridDim.x;
+  for (int e = tid; e < npack; e += GT_THREADS) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int cta = 0;
+    const volatile double* pp = part + e;
+    for (; cta + 4 <= nb; cta += 4) {
+      s0 += pp[(size_t)(cta + 0) * GPACK];
+      s1 += pp[(size_t)(cta + 1) * GPACK];
+      s2 += pp[(size_t)(cta + 2) * GPACK];
+      s3 += pp[(size_t)(cta + 3) * GPACK];
+    }
+    for (; cta < nb; ++cta) s0 += pp[(size_t)cta * GPACK];
+    const double v = (s0 + s1) + (s2 + s3);
+    int a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (a * (a + 1) / 2 > e) --a;
+    while ((a + 1) * (a + 2) / 2 <= e) ++a;
+    const int b = e - a * (a + 1) / 2;
+    out[a * k + b] = v;
+    out[b * k + a] = v;
+  }
+  if (tid == 0) *counter = 0;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(GT_THREADS) k_gram_state(Ctx c) {
+  if (c.st->done) return;
+  gram_body<NB>(c.Y, c.ld, c.cfg->ncols, c.part_g, c.st->gram, &c.st->gram_count);
+}
+
+template <int NB>
+__global__ void __launch_bounds__(GT_THREADS)
+    k_gram_raw(const double* Y, int64_t ld, int k, double* part, double* out, int* counter) {
+  gram_body<NB>(Y, ld, k, part, out, counter);
+}
+
+template <int NB>
+constexpr size_t gram_smem() {
+  return sizeof(double) * ((size_t)GT_STAGES * NB * 8 * GT_LD + (size_t)(NB * (NB + 1) / 2) * 64);
+}
+
+template <int NB>
+void set_attr() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_gram_state<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)gram_smem<NB>());
+    cudaFuncSetAttribute(k_gram_raw<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)gram_smem<NB>());
+    done = true;
+  }
+}
+
+int gram_grid(int64_t ld) {
+  int64_t t = ld / GT_ROWS;
+  if (t > GRAM_BLOCKS) t = GRAM_BLOCKS;
+  return (int)(t < 1 ? 1 : t);
+}
+
+}  // namespace
+
+int gram_row_multiple() { return GT_ROWS; }
+
+void launch_gram(const Ctx& c, int ncols, cudaStream_t s) {
+  const int nb = (ncols + 7) / 8;
+  const int grid = gram_grid(c.ld);
+  switch (nb) {
+#define G_CASE(N)                                                             \
+  case N:                                                                     \
+    set_attr<N>();                                                            \
+    k_gram_state<N><<<grid, GT_THREADS, gram_smem<N>(), s>>>(c);              \
+    break;
+    G_CASE(1) G_CASE(2) G_CASE(3) G_CASE(4) G_CASE(5)
+#undef G_CASE
+  }
+}
+
+void launch_gram_raw(const double* Y, int64_t n, int64_t ld, int k, double* part, double* out,
+                     int* counter, cudaStream_t s) {
+  (void)n;
+  const int nb = (k + 7) / 8;
+  const int grid = gram_grid(ld);
+  switch (nb) {
+#define G_CASE(N)                                                                      \
+  case N:                                                                              \
+    set_attr<N>();                                                                     \
+    k_gram_raw<N><<<grid, GT_THREADS, gram_smem<N>(), s>>>(Y, ld, k, part, out, counter); \
+    break;
+    G_CASE(1) G_CASE(2) G_CASE(3) G_CASE(4) G_CASE(5)
+#undef G_CASE
+  }
+}

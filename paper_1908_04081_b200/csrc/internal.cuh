@@ -1,0 +1,151 @@
+// internal.cuh -- shared device-side data model of the sm_100a s-step CG path.
+//
+// Memory layout in HBM (one plan = one operator A on one GPU):
+//   CSR       row_ptr int32[n+1], col int32[nnz], val f64[nnz]  (read sigma times/outer)
+//   Y         f64 column-major, ld = n rounded up to 32; column l = P_l (l=0..sigma),
+//             column sigma+1+l = R_l (l=0..sigma-1).  p and r live IN Y: recovery
+//             writes p into column 0 and r into column sigma+1 (row-local, so in place
+//             is safe), removing the reference's hstack / Y_t copies (basis.py:239,
+//             adaptive.py:166).
+//   x, b      f64[n]
+//   partials  per-block reduction slots (deterministic fixed-order sums)
+//   SolverState  all control state of adaptive_solve (adaptive.py:111-268): the
+//             outer loop runs without host round trips; the host only polls `done`.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sscg.h"
+
+#define SMAX SSCG_MAX_SIGMA   // 16
+#define CMAX (2 * SMAX + 1)   // 33 basis columns
+#define NB8 ((CMAX + 7) / 8)  // 5 column blocks of 8 (DMMA tiles)
+#define GPACK (CMAX * (CMAX + 1) / 2)
+
+// fixed launch geometry (B200: 148 SMs)
+#define NUM_SMS 148
+#define ROWS_PER_CTA 256
+#define RED_BLOCKS (NUM_SMS * 4)   // grid of the row-streaming kernels (partials count)
+#define GRAM_BLOCKS NUM_SMS
+#define SMALL_THREADS 512
+
+struct RitzDev {  // ritz.py:28-158
+  double hi_om, hi_h, hi_zeta;
+  double lo_om, lo_a, lo_d, lo_g, lo_h;
+  double psi, c, eta_next;
+  int hi_init, lo_init, count, pad;
+};
+
+struct ParamsDev {  // basis.py:39-55
+  int kind;
+  int has_from;
+  double lo, hi;  // generated_from
+  double th[SMAX], ga[SMAX], mu[SMAX];
+};
+
+struct DevConfig {  // sscg_config + derived constants
+  int sigma, s_bar0, f, basis_kind, c_strategy, variant, max_outer, leja_grid;
+  int has_bounds, trace_full, n_a, ncols;  // ncols = 2 sigma + 1 (physical Y)
+  double eps_star, bound_lo, bound_hi, norm_a, norm_abs_a, kappa_a;
+  double unit;      // 2^-53 (ritz.py:25)
+  double c0;        // MACHINE_UNIT ** -0.5 (ritz.py:124)
+  double nu;        // norm_abs_a / norm_a (adaptive.py:119)
+  int64_t cap_iters, cap_outer;
+};
+
+struct SolverState {
+  int k;          // outer loop index of the block being built
+  int done;       // 1: solve finished, every kernel is a no-op
+  int status;     // SSCG_RUNNING / CONVERGED / STAGNATED / DIVERGED
+  int s_bar;      // degree of the block being built (level kernels read it)
+  int s_tilde;
+  int s_act;      // inner iterations done in the last block
+  int rec_valid;  // recovery applies this outer loop
+  int total_iters, total_outer, n_records;
+  int best_iter;
+  int breakdown;  // non-finite basis column seen (level kernels, atomicOr)
+  int first_saved;
+  int diag_base;  // global iteration index of the block's first inner iteration
+  int gram_count; // last-block-done counter of the Gram kernel
+  int diag_n;     // inner iterations of this block needing full-trace diagnostics
+  double best;
+  double nb;      // ||b||
+  ParamsDev prm;  // parameters of the block being built
+  RitzDev rz;
+  double cx[CMAX], cr[CMAX], cp[CMAX];      // recovery coefficients, physical columns
+  double dx[SMAX][CMAX], dr[SMAX][CMAX];    // per-iteration coords (full trace)
+  double gram[CMAX * CMAX];                 // reduced Gram of the physical block
+};
+
+// everything a kernel may touch; passed by value
+struct Ctx {
+  const int* rp;
+  const int* col;
+  const double* val;
+  int64_t n;
+  int64_t ld;
+  double* Y;
+  double* x;
+  const double* b;
+  double* xj;  // full-trace scratch
+  double* rj;
+  SolverState* st;
+  const DevConfig* cfg;
+  double* part_t;   // [RED_BLOCKS] ||b - A x||^2 partials
+  double* part_r;   // [RED_BLOCKS] ||r||^2 partials
+  double* part_d;   // [3][RED_BLOCKS] full-trace partials
+  double* part_g;   // [GRAM_BLOCKS][GPACK] Gram partials
+  double* leja_obj; // [leja_grid] scratch
+  // logs (device)
+  double* it_log;   // [cap_iters][SSCG_IT_N]
+  int* rec_i;       // [cap_outer][SSCG_REC_NI]
+  double* rec_d;    // [cap_outer][SSCG_RECD_ND]
+  double* rec_conds;   // [cap_outer][SMAX+1]
+  double* rec_th;      // [cap_outer][SMAX]
+  double* rec_ga;
+  double* rec_mu;
+  double* outer_true;  // [cap_outer+1]
+  double* first_gram;  // [CMAX*CMAX]
+};
+
+#define CUDA_OK(expr)                                             \
+  do {                                                            \
+    cudaError_t e__ = (expr);                                     \
+    if (e__ != cudaSuccess) return sscg_fail_cuda(e__, #expr);    \
+  } while (0)
+
+int sscg_fail_cuda(cudaError_t e, const char* what);
+int sscg_fail(int code, const char* fmt, ...);
+
+// ---- launchers (defined in the .cu files) ----
+// mpk.cu
+void launch_init_residual(const Ctx& c, const double* x0, cudaStream_t s);
+void launch_level(const Ctx& c, int level, cudaStream_t s);
+void launch_spmv(const int* rp, const int* col, const double* val, int64_t n, const double* x,
+                 double* y, cudaStream_t s);
+void launch_block_levels(const int* rp, const int* col, const double* val, int64_t n, int64_t ld,
+                         double* Y, int s, const double* th, const double* ga, const double* mu,
+                         int* breakdown, cudaStream_t st);
+void launch_diag_resid(const Ctx& c, int j, cudaStream_t s);
+// gram.cu (ld must be a multiple of gram_row_multiple(); padding rows zero)
+int gram_row_multiple();
+void launch_gram(const Ctx& c, int ncols, cudaStream_t s);
+void launch_gram_raw(const double* Y, int64_t n, int64_t ld, int k, double* part, double* out,
+                     int* counter, cudaStream_t s);
+// rec.cu
+void launch_recover(const Ctx& c, cudaStream_t s);
+void launch_diag_form(const Ctx& c, int j, cudaStream_t s);
+void launch_recover_raw(const double* Y, int64_t n, int64_t ld, int k, const double* coef,
+                        const double* xbase, double* x, double* r, double* p, cudaStream_t s);
+// small.cu
+void launch_state_init(const Ctx& c, cudaStream_t s);
+void launch_small(const Ctx& c, cudaStream_t s);
+void launch_diag_fin(const Ctx& c, int j, cudaStream_t s);
+size_t small_smem_bytes();
+int unit_nested_conds(const double* g_host, int s_bar, double* conds_host, int mode, double c,
+                      double unit, double eps, double rn, int* s_tilde);
+int unit_leja(double lo, double hi, int count, int grid, double* out);
+int unit_params_for(int kind, int s, int has, double lo, double hi, int grid, double* th,
+                    double* ga, double* mu, int* kind_out);
+int unit_ritz(int m, const double* a, const double* b, double* rec);
+int unit_sym_eig(int n, const double* m, double* w);

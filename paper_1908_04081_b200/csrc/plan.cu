@@ -1,0 +1,755 @@
+// plan.cu -- host runtime behind the C ABI (include/sscg.h).
+//
+// A plan owns the device copy of one CSR operator plus every work buffer of the
+// solve.  sscg_run drives adaptive_solve (adaptive.py:111-268) entirely on the
+// device: one CUDA graph per outer loop (sigma matrix-powers levels, the Gram
+// kernel, K_small, [full-trace diagnostics], recovery) is replayed in chunks;
+// the host only polls the device `done` word of the previous chunk while the
+// next one runs, so the GPU never waits on the host.  Once `done` is set every
+// kernel of the remaining replays returns immediately.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+void small_prepare();
+double sscg_host_c0();
+
+namespace {
+thread_local std::string g_err;
+constexpr int CHUNK = 4;
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+}  // namespace
+
+int sscg_fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int sscg_fail_cuda(cudaError_t e, const char* what) {
+  const int code = (e == cudaErrorMemoryAllocation) ? SSCG_ENOMEM
+                   : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) ? SSCG_ENODEV
+                                                                                  : SSCG_ECUDA;
+  return sscg_fail(code, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+struct sscg_plan {
+  int device = 0;
+  int64_t n = 0, nnz = 0, ld = 0;
+  int* d_rp = nullptr;
+  int* d_col = nullptr;
+  double* d_val = nullptr;
+  int sigma_alloc = 0;
+  double* d_Y = nullptr;
+  double* d_x = nullptr;
+  double* d_b = nullptr;
+  double* d_x0 = nullptr;
+  double* d_xj = nullptr;
+  double* d_rj = nullptr;
+  SolverState* d_st = nullptr;
+  DevConfig* d_cfg = nullptr;
+  double* d_part_t = nullptr;
+  double* d_part_r = nullptr;
+  double* d_part_d = nullptr;
+  double* d_part_g = nullptr;
+  double* d_leja = nullptr;
+  int leja_cap = 0;
+  int64_t cap_iters = 0, cap_outer = 0;
+  double* d_it = nullptr;
+  int* d_ri = nullptr;
+  double* d_rd = nullptr;
+  double* d_conds = nullptr;
+  double* d_th = nullptr;
+  double* d_ga = nullptr;
+  double* d_mu = nullptr;
+  double* d_otrue = nullptr;
+  double* d_fg = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int g_sigma = -1, g_full = -1;
+  int* h_done = nullptr;  // pinned [2]
+  cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  sscg_config cfg{};
+  int have_rhs = 0;
+  int32_t last_launched = 0;
+  double last_ms = 0.0;
+  // profiling
+  int profiling = 0;
+  double prof_ms[5] = {0, 0, 0, 0, 0};
+  int64_t prof_cnt[5] = {0, 0, 0, 0, 0};
+  int64_t bytes = 0;
+};
+
+namespace {
+
+template <class T>
+int dalloc(sscg_plan* p, T** ptr, size_t count) {
+  if (*ptr) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+  }
+  const size_t b = sizeof(T) * (count ? count : 1);
+  CUDA_OK(cudaMalloc((void**)ptr, b));
+  p->bytes += (int64_t)b;
+  return SSCG_OK;
+}
+
+#define TRY(expr)                \
+  do {                           \
+    int rc__ = (expr);           \
+    if (rc__ != SSCG_OK) return rc__; \
+  } while (0)
+
+int ensure_work(sscg_plan* p, int sigma, int64_t max_outer, int leja_grid) {
+  if (sigma > p->sigma_alloc) {
+    const int ncols = 2 * sigma + 1;
+    TRY(dalloc(p, &p->d_Y, (size_t)p->ld * ncols));
+    CUDA_OK(cudaMemset(p->d_Y, 0, sizeof(double) * (size_t)p->ld * ncols));
+    p->sigma_alloc = sigma;
+    if (p->gexec) {
+      cudaGraphExecDestroy(p->gexec);
+      p->gexec = nullptr;
+    }
+  }
+  const int64_t co = max_outer + 2;
+  const int64_t ci = (max_outer + 1) * (int64_t)sigma + 1;
+  if (co > p->cap_outer || ci > p->cap_iters) {
+    const int64_t nco = co > p->cap_outer ? co : p->cap_outer;
+    const int64_t nci = ci > p->cap_iters ? ci : p->cap_iters;
+    TRY(dalloc(p, &p->d_it, (size_t)nci * SSCG_IT_N));
+    TRY(dalloc(p, &p->d_ri, (size_t)nco * SSCG_REC_NI));
+    TRY(dalloc(p, &p->d_rd, (size_t)nco * SSCG_RECD_ND));
+    TRY(dalloc(p, &p->d_conds, (size_t)nco * (SMAX + 1)));
+    TRY(dalloc(p, &p->d_th, (size_t)nco * SMAX));
+    TRY(dalloc(p, &p->d_ga, (size_t)nco * SMAX));
+    TRY(dalloc(p, &p->d_mu, (size_t)nco * SMAX));
+    TRY(dalloc(p, &p->d_otrue, (size_t)nco + 1));
+    p->cap_outer = nco;
+    p->cap_iters = nci;
+    if (p->gexec) {
+      cudaGraphExecDestroy(p->gexec);
+      p->gexec = nullptr;
+    }
+  }
+  if (leja_grid > p->leja_cap) {
+    TRY(dalloc(p, &p->d_leja, (size_t)leja_grid));
+    p->leja_cap = leja_grid;
+    if (p->gexec) {
+      cudaGraphExecDestroy(p->gexec);
+      p->gexec = nullptr;
+    }
+  }
+  return SSCG_OK;
+}
+
+Ctx make_ctx(sscg_plan* p) {
+  Ctx c;
+  c.rp = p->d_rp;
+  c.col = p->d_col;
+  c.val = p->d_val;
+  c.n = p->n;
+  c.ld = p->ld;
+  c.Y = p->d_Y;
+  c.x = p->d_x;
+  c.b = p->d_b;
+  c.xj = p->d_xj;
+  c.rj = p->d_rj;
+  c.st = p->d_st;
+  c.cfg = p->d_cfg;
+  c.part_t = p->d_part_t;
+  c.part_r = p->d_part_r;
+  c.part_d = p->d_part_d;
+  c.part_g = p->d_part_g;
+  c.leja_obj = p->d_leja;
+  c.it_log = p->d_it;
+  c.rec_i = p->d_ri;
+  c.rec_d = p->d_rd;
+  c.rec_conds = p->d_conds;
+  c.rec_th = p->d_th;
+  c.rec_ga = p->d_ga;
+  c.rec_mu = p->d_mu;
+  c.outer_true = p->d_otrue;
+  c.first_gram = p->d_fg;
+  return c;
+}
+
+int check_config(const sscg_config* c) {
+  if (!c) return sscg_fail(SSCG_EINVAL, "config is NULL");
+  if (c->sigma < 1) return sscg_fail(SSCG_EINVAL, "sigma must be >= 1");
+  if (c->sigma > SMAX)
+    return sscg_fail(SSCG_EINVAL, "sigma=%d exceeds SSCG_MAX_SIGMA=%d", c->sigma, SMAX);
+  if (c->s_bar0 < 1 || c->s_bar0 > c->sigma) return sscg_fail(SSCG_EINVAL, "need 1 <= s_bar0 <= sigma");
+  if (c->f < 0) return sscg_fail(SSCG_EINVAL, "f must be >= 0");
+  if (!(c->eps_star > 0.0)) return sscg_fail(SSCG_EINVAL, "eps_star must be positive");
+  if (c->variant != 0 && c->variant != 1) return sscg_fail(SSCG_EINVAL, "unknown variant");
+  if (c->basis_kind < 0 || c->basis_kind > 2)
+    return sscg_fail(SSCG_EPARAM, "unknown basis kind %d", c->basis_kind);
+  if (c->c_strategy < 0 || c->c_strategy > 3)
+    return sscg_fail(SSCG_EINVAL, "unknown c strategy %d", c->c_strategy);
+  if (c->max_outer < 0) return sscg_fail(SSCG_EINVAL, "max_outer must be >= 0");
+  if (c->leja_grid < 2) return sscg_fail(SSCG_EINVAL, "leja_grid must be >= 2");
+  return SSCG_OK;
+}
+
+void capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t s) {
+  for (int l = 0; l < sigma; ++l) launch_level(c, l, s);
+  launch_gram(c, 2 * sigma + 1, s);
+  launch_small(c, s);
+  if (full) {
+    for (int j = 0; j < sigma; ++j) {
+      launch_diag_form(c, j, s);
+      launch_diag_resid(c, j, s);
+      launch_diag_fin(c, j, s);
+    }
+  }
+  launch_recover(c, s);
+  (void)p;
+}
+
+int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
+  if (p->gexec && p->g_sigma == sigma && p->g_full == full) return SSCG_OK;
+  if (p->gexec) {
+    cudaGraphExecDestroy(p->gexec);
+    p->gexec = nullptr;
+  }
+  cudaGraph_t g = nullptr;
+  CUDA_OK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+  capture_outer(p, c, sigma, full, p->stream);
+  cudaError_t e = cudaStreamEndCapture(p->stream, &g);
+  if (e != cudaSuccess) return sscg_fail_cuda(e, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&p->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return sscg_fail_cuda(e, "cudaGraphInstantiate");
+  p->g_sigma = sigma;
+  p->g_full = full;
+  return SSCG_OK;
+}
+
+// profiling mode: launch one outer loop kernel by kernel with event pairs
+struct ProfEv {
+  int cls;
+  cudaEvent_t a, b;
+};
+
+int launch_outer_profiled(sscg_plan* p, const Ctx& c, int sigma, int full,
+                          std::vector<ProfEv>& evs) {
+  auto rec = [&](int cls, auto&& fn) -> int {
+    ProfEv e{cls, nullptr, nullptr};
+    CUDA_OK(cudaEventCreate(&e.a));
+    CUDA_OK(cudaEventCreate(&e.b));
+    CUDA_OK(cudaEventRecord(e.a, p->stream));
+    fn();
+    CUDA_OK(cudaEventRecord(e.b, p->stream));
+    evs.push_back(e);
+    return SSCG_OK;
+  };
+  for (int l = 0; l < sigma; ++l) TRY(rec(0, [&] { launch_level(c, l, p->stream); }));
+  TRY(rec(1, [&] { launch_gram(c, 2 * sigma + 1, p->stream); }));
+  TRY(rec(2, [&] { launch_small(c, p->stream); }));
+  if (full) {
+    for (int j = 0; j < sigma; ++j) {
+      TRY(rec(4, [&] { launch_diag_form(c, j, p->stream); }));
+      TRY(rec(4, [&] { launch_diag_resid(c, j, p->stream); }));
+      TRY(rec(4, [&] { launch_diag_fin(c, j, p->stream); }));
+    }
+  }
+  TRY(rec(3, [&] { launch_recover(c, p->stream); }));
+  return SSCG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sscg_last_error(void) { return g_err.c_str(); }
+int sscg_abi_version(void) { return SSCG_ABI_VERSION; }
+
+int sscg_device_count(int32_t* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return sscg_fail_cuda(e, "cudaGetDeviceCount");
+  }
+  *count = n;
+  return SSCG_OK;
+}
+
+int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
+                     const int64_t* row_ptr, const int32_t* col_idx, const double* values) {
+  if (!out) return sscg_fail(SSCG_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 1) return sscg_fail(SSCG_EINVAL, "n must be >= 1");
+  if (nnz < 0 || nnz >= ((int64_t)1 << 31))
+    return sscg_fail(SSCG_EINVAL, "nnz=%lld outside the int32 CSR range", (long long)nnz);
+  if (n >= ((int64_t)1 << 31)) return sscg_fail(SSCG_EINVAL, "n exceeds int32 column indices");
+  if (!row_ptr || (nnz && (!col_idx || !values))) return sscg_fail(SSCG_EINVAL, "NULL CSR array");
+  if (row_ptr[0] != 0 || row_ptr[n] != nnz)
+    return sscg_fail(SSCG_EINVAL, "row_ptr must start at 0 and end at nnz");
+  int ndev = 0;
+  CUDA_OK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return sscg_fail(SSCG_ENODEV, "device %d not present (%d visible)", device, ndev);
+  CUDA_OK(cudaSetDevice(device));
+  sscg_plan* p = new sscg_plan();
+  p->device = device;
+  p->n = n;
+  p->nnz = nnz;
+  p->ld = round_up(n, gram_row_multiple());
+  int rc = SSCG_OK;
+  do {
+    std::vector<int> rp32(n + 1);
+    for (int64_t i = 0; i <= n; ++i) {
+      if (i && row_ptr[i] < row_ptr[i - 1]) {
+        rc = sscg_fail(SSCG_EINVAL, "row_ptr must be nondecreasing");
+        break;
+      }
+      rp32[i] = (int)row_ptr[i];
+    }
+    if (rc) break;
+    if ((rc = dalloc(p, &p->d_rp, n + 1))) break;
+    if ((rc = dalloc(p, &p->d_col, nnz))) break;
+    if ((rc = dalloc(p, &p->d_val, nnz))) break;
+    cudaError_t e;
+    if ((e = cudaMemcpy(p->d_rp, rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice))) {
+      rc = sscg_fail_cuda(e, "upload row_ptr");
+      break;
+    }
+    if (nnz && (e = cudaMemcpy(p->d_col, col_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice))) {
+      rc = sscg_fail_cuda(e, "upload col_idx");
+      break;
+    }
+    if (nnz && (e = cudaMemcpy(p->d_val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice))) {
+      rc = sscg_fail_cuda(e, "upload values");
+      break;
+    }
+    for (double** v : {&p->d_x, &p->d_b, &p->d_x0, &p->d_xj, &p->d_rj}) {
+      if ((rc = dalloc(p, v, p->ld))) break;
+      if ((e = cudaMemset(*v, 0, sizeof(double) * p->ld))) {
+        rc = sscg_fail_cuda(e, "memset");
+        break;
+      }
+    }
+    if (rc) break;
+    if ((rc = dalloc(p, &p->d_st, 1))) break;
+    if ((rc = dalloc(p, &p->d_cfg, 1))) break;
+    if ((rc = dalloc(p, &p->d_part_t, RED_BLOCKS))) break;
+    if ((rc = dalloc(p, &p->d_part_r, RED_BLOCKS))) break;
+    if ((rc = dalloc(p, &p->d_part_d, 3 * RED_BLOCKS))) break;
+    if ((rc = dalloc(p, &p->d_part_g, (size_t)GRAM_BLOCKS * GPACK))) break;
+    if ((rc = dalloc(p, &p->d_fg, CMAX * CMAX))) break;
+    if ((e = cudaMemset(p->d_st, 0, sizeof(SolverState)))) {
+      rc = sscg_fail_cuda(e, "memset state");
+      break;
+    }
+    if ((e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking))) {
+      rc = sscg_fail_cuda(e, "stream");
+      break;
+    }
+    if ((e = cudaHostAlloc((void**)&p->h_done, 2 * sizeof(int), cudaHostAllocDefault))) {
+      rc = sscg_fail_cuda(e, "pinned flag");
+      break;
+    }
+    for (auto* ev : {&p->ev_chunk[0], &p->ev_chunk[1]})
+      if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming))) rc = sscg_fail_cuda(e, "event");
+    if (rc) break;
+    if ((e = cudaEventCreate(&p->ev_start)) || (e = cudaEventCreate(&p->ev_stop))) {
+      rc = sscg_fail_cuda(e, "event");
+      break;
+    }
+    small_prepare();
+  } while (0);
+  if (rc != SSCG_OK) {
+    std::string keep = g_err;
+    sscg_plan_destroy(p);
+    g_err = keep;
+    return rc;
+  }
+  *out = p;
+  return SSCG_OK;
+}
+
+int sscg_plan_destroy(sscg_plan* p) {
+  if (!p) return SSCG_OK;
+  cudaSetDevice(p->device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  void* bufs[] = {p->d_rp, p->d_col, p->d_val, p->d_Y, p->d_x, p->d_b, p->d_x0, p->d_xj,
+                  p->d_rj, p->d_st, p->d_cfg, p->d_part_t, p->d_part_r, p->d_part_d,
+                  p->d_part_g, p->d_leja, p->d_it, p->d_ri, p->d_rd, p->d_conds, p->d_th,
+                  p->d_ga, p->d_mu, p->d_otrue, p->d_fg};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (p->h_done) cudaFreeHost(p->h_done);
+  for (auto ev : {p->ev_chunk[0], p->ev_chunk[1], p->ev_start, p->ev_stop})
+    if (ev) cudaEventDestroy(ev);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+  return SSCG_OK;
+}
+
+int sscg_plan_device_bytes(const sscg_plan* p, int64_t* bytes) {
+  if (!p || !bytes) return sscg_fail(SSCG_EINVAL, "NULL argument");
+  *bytes = p->bytes;
+  return SSCG_OK;
+}
+
+int sscg_load(sscg_plan* p, const double* b, const double* x0) {
+  if (!p || !b) return sscg_fail(SSCG_EINVAL, "NULL argument");
+  CUDA_OK(cudaSetDevice(p->device));
+  CUDA_OK(cudaMemcpyAsync(p->d_b, b, sizeof(double) * p->n, cudaMemcpyHostToDevice, p->stream));
+  if (x0)
+    CUDA_OK(cudaMemcpyAsync(p->d_x0, x0, sizeof(double) * p->n, cudaMemcpyHostToDevice, p->stream));
+  else
+    CUDA_OK(cudaMemsetAsync(p->d_x0, 0, sizeof(double) * p->n, p->stream));
+  p->have_rhs = 1;
+  return SSCG_OK;
+}
+
+int sscg_set_profiling(sscg_plan* p, int32_t enable) {
+  if (!p) return sscg_fail(SSCG_EINVAL, "NULL plan");
+  p->profiling = enable ? 1 : 0;
+  return SSCG_OK;
+}
+
+int sscg_get_profile(const sscg_plan* p, double* ms5, int64_t* counts5) {
+  if (!p || !ms5 || !counts5) return sscg_fail(SSCG_EINVAL, "NULL argument");
+  for (int i = 0; i < 5; ++i) {
+    ms5[i] = p->prof_ms[i];
+    counts5[i] = p->prof_cnt[i];
+  }
+  return SSCG_OK;
+}
+
+int sscg_run(sscg_plan* p, const sscg_config* cfg, sscg_logs* logs) {
+  if (!p) return sscg_fail(SSCG_EINVAL, "NULL plan");
+  TRY(check_config(cfg));
+  if (!p->have_rhs) return sscg_fail(SSCG_EINVAL, "sscg_load must precede sscg_run");
+  CUDA_OK(cudaSetDevice(p->device));
+  TRY(ensure_work(p, cfg->sigma, cfg->max_outer, cfg->leja_grid));
+  p->cfg = *cfg;
+  DevConfig dc;
+  memset(&dc, 0, sizeof(dc));
+  dc.sigma = cfg->sigma;
+  dc.s_bar0 = cfg->s_bar0;
+  dc.f = cfg->f;
+  dc.basis_kind = cfg->basis_kind;
+  dc.c_strategy = cfg->c_strategy;
+  dc.variant = cfg->variant;
+  dc.max_outer = cfg->max_outer;
+  dc.leja_grid = cfg->leja_grid;
+  dc.has_bounds = cfg->has_bounds;
+  dc.trace_full = cfg->trace_full;
+  dc.n_a = cfg->n_a;
+  dc.ncols = 2 * cfg->sigma + 1;
+  dc.eps_star = cfg->eps_star;
+  dc.bound_lo = cfg->bound_lo;
+  dc.bound_hi = cfg->bound_hi;
+  dc.norm_a = cfg->norm_a;
+  dc.norm_abs_a = cfg->norm_abs_a;
+  dc.kappa_a = cfg->kappa_a;
+  dc.unit = std::ldexp(1.0, -53);
+  dc.c0 = sscg_host_c0();
+  dc.nu = cfg->norm_a != 0.0 ? cfg->norm_abs_a / cfg->norm_a : 1.0;
+  dc.cap_iters = p->cap_iters;
+  dc.cap_outer = p->cap_outer - 1;
+  CUDA_OK(cudaMemcpyAsync(p->d_cfg, &dc, sizeof(dc), cudaMemcpyHostToDevice, p->stream));
+  // scrub logs so short runs leave NaN, not stale values
+  CUDA_OK(cudaMemsetAsync(p->d_it, 0xff, sizeof(double) * p->cap_iters * SSCG_IT_N, p->stream));
+  const Ctx c = make_ctx(p);
+  const int sigma = cfg->sigma, full = cfg->trace_full ? 1 : 0;
+  if (!p->profiling) TRY(build_graph(p, c, sigma, full));
+
+  CUDA_OK(cudaEventRecord(p->ev_start, p->stream));
+  launch_init_residual(c, p->d_x0, p->stream);
+  launch_state_init(c, p->stream);
+  CUDA_OK(cudaGetLastError());
+
+  const int64_t total = (int64_t)cfg->max_outer + 1;
+  int64_t launched = 0;
+  int chunk_id = 0;
+  std::vector<ProfEv> evs;
+  bool finished = false;
+  while (launched < total && !finished) {
+    const int64_t m = (total - launched) < CHUNK ? (total - launched) : CHUNK;
+    for (int64_t i = 0; i < m; ++i) {
+      if (p->profiling) {
+        TRY(launch_outer_profiled(p, c, sigma, full, evs));
+      } else {
+        CUDA_OK(cudaGraphLaunch(p->gexec, p->stream));
+      }
+    }
+    launched += m;
+    const int slot = chunk_id & 1;
+    CUDA_OK(cudaMemcpyAsync(p->h_done + slot, &p->d_st->done, sizeof(int), cudaMemcpyDeviceToHost,
+                            p->stream));
+    CUDA_OK(cudaEventRecord(p->ev_chunk[slot], p->stream));
+    if (chunk_id >= 1) {
+      const int prev = slot ^ 1;
+      CUDA_OK(cudaEventSynchronize(p->ev_chunk[prev]));
+      if (p->h_done[prev]) finished = true;
+    }
+    ++chunk_id;
+  }
+  CUDA_OK(cudaEventRecord(p->ev_stop, p->stream));
+  CUDA_OK(cudaStreamSynchronize(p->stream));
+  CUDA_OK(cudaGetLastError());
+  float ms = 0.f;
+  CUDA_OK(cudaEventElapsedTime(&ms, p->ev_start, p->ev_stop));
+  p->last_ms = ms;
+  p->last_launched = (int32_t)launched;
+  if (p->profiling) {
+    for (int i = 0; i < 5; ++i) {
+      p->prof_ms[i] = 0.0;
+      p->prof_cnt[i] = 0;
+    }
+    for (auto& e : evs) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e.a, e.b);
+      p->prof_ms[e.cls] += t;
+      p->prof_cnt[e.cls] += 1;
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+  }
+  if (logs) {
+    logs->device_ms = ms;
+    logs->outer_launched = (int32_t)launched;
+  }
+  return SSCG_OK;
+}
+
+int sscg_fetch(sscg_plan* p, double* x_out, sscg_logs* logs) {
+  if (!p) return sscg_fail(SSCG_EINVAL, "NULL plan");
+  CUDA_OK(cudaSetDevice(p->device));
+  CUDA_OK(cudaStreamSynchronize(p->stream));
+  if (x_out) CUDA_OK(cudaMemcpy(x_out, p->d_x, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
+  if (!logs) return SSCG_OK;
+  SolverState st;
+  CUDA_OK(cudaMemcpy(&st, p->d_st, sizeof(st), cudaMemcpyDeviceToHost));
+  logs->status = st.status;
+  logs->total_iters = st.total_iters;
+  logs->total_outer = st.total_outer;
+  logs->n_records = st.n_records;
+  logs->outer_launched = p->last_launched;
+  logs->device_ms = p->last_ms;
+  const int64_t ni = std::min<int64_t>({(int64_t)st.total_iters, logs->cap_iters, p->cap_iters});
+  const int64_t no = std::min<int64_t>({(int64_t)st.n_records, logs->cap_outer, p->cap_outer});
+  if (logs->iters && ni > 0)
+    CUDA_OK(cudaMemcpy(logs->iters, p->d_it, sizeof(double) * ni * SSCG_IT_N, cudaMemcpyDeviceToHost));
+  if (no > 0) {
+    if (logs->rec_i)
+      CUDA_OK(cudaMemcpy(logs->rec_i, p->d_ri, sizeof(int) * no * SSCG_REC_NI, cudaMemcpyDeviceToHost));
+    if (logs->rec_d)
+      CUDA_OK(cudaMemcpy(logs->rec_d, p->d_rd, sizeof(double) * no * SSCG_RECD_ND, cudaMemcpyDeviceToHost));
+    if (logs->conds)
+      CUDA_OK(cudaMemcpy(logs->conds, p->d_conds, sizeof(double) * no * (SMAX + 1), cudaMemcpyDeviceToHost));
+    if (logs->thetas)
+      CUDA_OK(cudaMemcpy(logs->thetas, p->d_th, sizeof(double) * no * SMAX, cudaMemcpyDeviceToHost));
+    if (logs->gammas)
+      CUDA_OK(cudaMemcpy(logs->gammas, p->d_ga, sizeof(double) * no * SMAX, cudaMemcpyDeviceToHost));
+    if (logs->mus)
+      CUDA_OK(cudaMemcpy(logs->mus, p->d_mu, sizeof(double) * no * SMAX, cudaMemcpyDeviceToHost));
+  }
+  const int64_t nt = std::min<int64_t>({(int64_t)st.k + 1, logs->cap_outer + 1, p->cap_outer});
+  if (logs->outer_true && nt > 0)
+    CUDA_OK(cudaMemcpy(logs->outer_true, p->d_otrue, sizeof(double) * nt, cudaMemcpyDeviceToHost));
+  if (logs->first_gram && st.first_saved) {
+    const int d = 2 * p->cfg.s_bar0 + 1;
+    CUDA_OK(cudaMemcpy(logs->first_gram, p->d_fg, sizeof(double) * d * d, cudaMemcpyDeviceToHost));
+  }
+  return SSCG_OK;
+}
+
+int sscg_solve(sscg_plan* p, const sscg_config* cfg, const double* b, const double* x0,
+               double* x_out, sscg_logs* logs) {
+  TRY(sscg_load(p, b, x0));
+  TRY(sscg_run(p, cfg, logs));
+  return sscg_fetch(p, x_out, logs);
+}
+
+// ---- unit entry points ------------------------------------------------------
+int sscg_spmv(sscg_plan* p, const double* x, double* y) {
+  if (!p || !x || !y) return sscg_fail(SSCG_EINVAL, "NULL argument");
+  CUDA_OK(cudaSetDevice(p->device));
+  CUDA_OK(cudaMemcpyAsync(p->d_xj, x, sizeof(double) * p->n, cudaMemcpyHostToDevice, p->stream));
+  launch_spmv(p->d_rp, p->d_col, p->d_val, p->n, p->d_xj, p->d_rj, p->stream);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaMemcpyAsync(y, p->d_rj, sizeof(double) * p->n, cudaMemcpyDeviceToHost, p->stream));
+  CUDA_OK(cudaStreamSynchronize(p->stream));
+  return SSCG_OK;
+}
+
+int sscg_build_block(sscg_plan* p, const double* pv, const double* rv, int32_t s,
+                     const double* th, const double* ga, const double* mu, double* y_out,
+                     double* g_out) {
+  if (!p || !pv || !rv || !th || !ga || (s > 1 && !mu)) return sscg_fail(SSCG_EINVAL, "NULL argument");
+  if (s < 1 || s > SMAX) return sscg_fail(SSCG_EINVAL, "s=%d outside [1, %d]", s, SMAX);
+  CUDA_OK(cudaSetDevice(p->device));
+  const int k = 2 * s + 1;
+  double *dY = nullptr, *part = nullptr, *dg = nullptr;
+  int* flag = nullptr;
+  int rc = SSCG_OK;
+  cudaError_t e = cudaSuccess;
+  int h_flag = 0;
+  if ((e = cudaMalloc(&dY, sizeof(double) * p->ld * k)) || (e = cudaMalloc(&part, sizeof(double) * GRAM_BLOCKS * GPACK)) ||
+      (e = cudaMalloc(&dg, sizeof(double) * k * k)) || (e = cudaMalloc(&flag, 2 * sizeof(int))) ||
+      (e = cudaMemset(dY, 0, sizeof(double) * p->ld * k)) || (e = cudaMemset(flag, 0, 2 * sizeof(int))) ||
+      (e = cudaMemcpy(dY, pv, sizeof(double) * p->n, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(dY + (size_t)(s + 1) * p->ld, rv, sizeof(double) * p->n, cudaMemcpyHostToDevice))) {
+    rc = sscg_fail_cuda(e, "build_block setup");
+  } else {
+    launch_block_levels(p->d_rp, p->d_col, p->d_val, p->n, p->ld, dY, s, th, ga, mu, flag, p->stream);
+    launch_gram_raw(dY, p->n, p->ld, k, part, dg, flag + 1, p->stream);
+    if ((e = cudaStreamSynchronize(p->stream)) || (e = cudaGetLastError()) ||
+        (e = cudaMemcpy(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost))) {
+      rc = sscg_fail_cuda(e, "build_block");
+    } else if (h_flag) {
+      rc = sscg_fail(SSCG_EBREAKDOWN, "non-finite basis column (BasisBreakdownError)");
+    } else {
+      for (int col = 0; col < k && !rc; ++col)
+        if ((e = cudaMemcpy(y_out + (size_t)col * p->n, dY + (size_t)col * p->ld, sizeof(double) * p->n,
+                            cudaMemcpyDeviceToHost)))
+          rc = sscg_fail_cuda(e, "download Y");
+      if (!rc && g_out && (e = cudaMemcpy(g_out, dg, sizeof(double) * k * k, cudaMemcpyDeviceToHost)))
+        rc = sscg_fail_cuda(e, "download G");
+    }
+  }
+  cudaFree(dY);
+  cudaFree(part);
+  cudaFree(dg);
+  cudaFree(flag);
+  return rc;
+}
+
+int sscg_gram(int32_t device, int64_t n, int32_t k, const double* y, double* g) {
+  if (!y || !g || n < 1 || k < 1 || k > CMAX) return sscg_fail(SSCG_EINVAL, "bad gram arguments");
+  CUDA_OK(cudaSetDevice(device));
+  const int64_t ld = round_up(n, gram_row_multiple());
+  double *dY = nullptr, *part = nullptr, *dg = nullptr;
+  int* cnt = nullptr;
+  int rc = SSCG_OK;
+  cudaError_t e;
+  if ((e = cudaMalloc(&dY, sizeof(double) * ld * k)) || (e = cudaMalloc(&part, sizeof(double) * GRAM_BLOCKS * GPACK)) ||
+      (e = cudaMalloc(&dg, sizeof(double) * k * k)) || (e = cudaMalloc(&cnt, sizeof(int))) ||
+      (e = cudaMemset(dY, 0, sizeof(double) * ld * k)) || (e = cudaMemset(cnt, 0, sizeof(int))) ||
+      (e = cudaMemcpy2D(dY, ld * sizeof(double), y, n * sizeof(double), n * sizeof(double), k,
+                        cudaMemcpyHostToDevice))) {
+    rc = sscg_fail_cuda(e, "gram setup");
+  } else {
+    launch_gram_raw(dY, n, ld, k, part, dg, cnt, 0);
+    if ((e = cudaDeviceSynchronize()) || (e = cudaGetLastError()) ||
+        (e = cudaMemcpy(g, dg, sizeof(double) * k * k, cudaMemcpyDeviceToHost)))
+      rc = sscg_fail_cuda(e, "gram");
+  }
+  cudaFree(dY);
+  cudaFree(part);
+  cudaFree(dg);
+  cudaFree(cnt);
+  return rc;
+}
+
+int sscg_recover(int32_t device, int64_t n, int32_t k, const double* y, const double* xp,
+                 const double* rp, const double* pp, const double* xb, double* x, double* r,
+                 double* pout) {
+  if (!y || !xp || !rp || !pp || !xb || !x || !r || !pout || n < 1 || k < 1 || k > CMAX)
+    return sscg_fail(SSCG_EINVAL, "bad recover arguments");
+  CUDA_OK(cudaSetDevice(device));
+  const int64_t ld = round_up(n, 64);
+  double *dY = nullptr, *coef = nullptr, *dxb = nullptr, *dx = nullptr, *dr = nullptr, *dp = nullptr;
+  int rc = SSCG_OK;
+  cudaError_t e;
+  std::vector<double> hc(3 * k);
+  for (int i = 0; i < k; ++i) {
+    hc[i] = xp[i];
+    hc[k + i] = rp[i];
+    hc[2 * k + i] = pp[i];
+  }
+  if ((e = cudaMalloc(&dY, sizeof(double) * ld * k)) || (e = cudaMalloc(&coef, sizeof(double) * 3 * k)) ||
+      (e = cudaMalloc(&dxb, sizeof(double) * ld)) || (e = cudaMalloc(&dx, sizeof(double) * ld)) ||
+      (e = cudaMalloc(&dr, sizeof(double) * ld)) || (e = cudaMalloc(&dp, sizeof(double) * ld)) ||
+      (e = cudaMemset(dY, 0, sizeof(double) * ld * k)) || (e = cudaMemset(dxb, 0, sizeof(double) * ld)) ||
+      (e = cudaMemcpy2D(dY, ld * sizeof(double), y, n * sizeof(double), n * sizeof(double), k,
+                        cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(coef, hc.data(), sizeof(double) * 3 * k, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(dxb, xb, sizeof(double) * n, cudaMemcpyHostToDevice))) {
+    rc = sscg_fail_cuda(e, "recover setup");
+  } else {
+    launch_recover_raw(dY, n, ld, k, coef, dxb, dx, dr, dp, 0);
+    if ((e = cudaDeviceSynchronize()) || (e = cudaGetLastError()) ||
+        (e = cudaMemcpy(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost)) ||
+        (e = cudaMemcpy(r, dr, sizeof(double) * n, cudaMemcpyDeviceToHost)) ||
+        (e = cudaMemcpy(pout, dp, sizeof(double) * n, cudaMemcpyDeviceToHost)))
+      rc = sscg_fail_cuda(e, "recover");
+  }
+  for (double* b : {dY, coef, dxb, dx, dr, dp}) cudaFree(b);
+  return rc;
+}
+
+int sscg_nested_conds(int32_t device, const double* g, int32_t s_bar, double* conds) {
+  if (!g || !conds || s_bar < 1 || s_bar > SMAX) return sscg_fail(SSCG_EINVAL, "bad arguments");
+  CUDA_OK(cudaSetDevice(device));
+  return unit_nested_conds(g, s_bar, conds, 0, 1.0, 1.0, 1.0, 1.0, nullptr);
+}
+
+int sscg_select_s_tilde(int32_t device, const double* g, int32_t s_bar, double c, double unit,
+                        double eps_star, double r_norm, int32_t* s_tilde, double* conds) {
+  if (!g || !conds || !s_tilde || s_bar < 1 || s_bar > SMAX)
+    return sscg_fail(SSCG_EINVAL, "bad arguments");
+  CUDA_OK(cudaSetDevice(device));
+  int st = 1;
+  TRY(unit_nested_conds(g, s_bar, conds, 1, c, unit, eps_star, r_norm, &st));
+  *s_tilde = st;
+  return SSCG_OK;
+}
+
+int sscg_leja_points(int32_t device, double lmin, double lmax, int32_t count, int32_t grid,
+                     double* out) {
+  if (!out || count < 1 || count > SMAX || grid < 2) return sscg_fail(SSCG_EINVAL, "bad arguments");
+  if (!(0.0 <= lmin && lmin < lmax))
+    return sscg_fail(SSCG_EPARAM, "need 0 <= lmin < lmax, got (%g, %g)", lmin, lmax);
+  CUDA_OK(cudaSetDevice(device));
+  return unit_leja(lmin, lmax, count, grid, out);
+}
+
+int sscg_params_for(int32_t device, int32_t kind, int32_t s, int32_t has, double lmin, double lmax,
+                    int32_t grid, double* th, double* ga, double* mu, int32_t* kind_out) {
+  if (kind < 0 || kind > 2) return sscg_fail(SSCG_EPARAM, "unknown basis kind %d", kind);
+  if (s < 1 || s > SMAX || !th || !ga || !mu || !kind_out || grid < 2)
+    return sscg_fail(SSCG_EINVAL, "bad arguments");
+  CUDA_OK(cudaSetDevice(device));
+  int ko = 0;
+  TRY(unit_params_for(kind, s, has, lmin, lmax, grid, th, ga, mu, &ko));
+  *kind_out = ko;
+  return SSCG_OK;
+}
+
+int sscg_ritz_sequence(int32_t device, int32_t m, const double* alpha, const double* beta,
+                       double* rec) {
+  if (m < 0 || (m && (!alpha || !beta || !rec))) return sscg_fail(SSCG_EINVAL, "bad arguments");
+  if (m == 0) return SSCG_OK;
+  CUDA_OK(cudaSetDevice(device));
+  return unit_ritz(m, alpha, beta, rec);
+}
+
+int sscg_sym_eig(int32_t device, int32_t n, const double* m, double* w) {
+  if (!m || !w || n < 1 || n > CMAX) return sscg_fail(SSCG_EINVAL, "bad arguments");
+  CUDA_OK(cudaSetDevice(device));
+  return unit_sym_eig(n, m, w);
+}
+
+}  // extern "C"

@@ -1,0 +1,1155 @@
+// small.cu -- K_small: all O(s^2) work of one outer loop in ONE single-CTA kernel,
+// so the solve never returns to the host between outer loops.
+//
+// Compiled with -fmad=false: every scalar expression rounds op by op exactly as
+// the reference's Python floats do (no contraction), so the Ritz recurrences,
+// bounds, break tests and basis parameters follow the reference's arithmetic.
+//
+// Reference map (/root/reference/pkg/src/sstepcg):
+//   run classification            sstep.py:61-76, adaptive.py:138-142, 262-266
+//   nested condition estimates    lacore.py:103-117, 135-148 (LAPACK eigvalsh -> a
+//                                  warp-parallel cyclic Jacobi per nested Gram block)
+//   s~ selection                  adaptive.py:89-104
+//   truncated block / B           adaptive.py:107-108, 162-171; basis.py:180-195
+//   coefficient-space inner loop  adaptive.py:173-246 (+ sstep.py:26-34)
+//   Ritz estimates, c             ritz.py:28-203
+//   next-block parameters         adaptive.py:254-258 -> basis.py:58-177 (Leja grid
+//                                  objective in numpy's pairwise-sum order, golden
+//                                  refinement, 1e-12 tie rule; Chebyshev mu = w/8)
+#include <math.h>
+
+#include "internal.cuh"
+
+namespace {
+
+constexpr int NT = SMALL_THREADS;  // 512
+constexpr int NW = NT / 32;        // 16 warps
+constexpr int JLD = CMAX + 1;      // Jacobi work matrix leading dimension
+constexpr int LEJA_CAND_CAP = 256;
+
+// Python's max(a, b) / min(a, b) semantics (first argument wins unless the
+// second compares strictly greater / smaller; NaN never compares)
+__device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
+__device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
+
+// ---------------------------------------------------------------------------
+// Ritz estimates (ritz.py:28-158)
+__device__ void ritz_init(RitzDev& r, double c0) {
+  r.hi_om = 0.0; r.hi_h = 1.0; r.hi_zeta = 0.0; r.hi_init = 0;
+  r.lo_om = 0.0; r.lo_a = 0.0; r.lo_d = 0.0; r.lo_g = 0.0; r.lo_h = 1.0; r.lo_init = 0;
+  r.psi = 1.0; r.c = c0; r.eta_next = 0.0; r.count = 0; r.pad = 0;
+}
+__device__ __forceinline__ double ritz_lmax(const RitzDev& r) {
+  return r.count >= 1 ? r.hi_om : (double)NAN;
+}
+__device__ __forceinline__ double ritz_lmin(const RitzDev& r) {
+  return r.count >= 1 ? 1.0 / r.lo_om : (double)NAN;
+}
+__device__ bool ritz_absorb(RitzDev& r, double alpha, double beta) {
+  if (!(alpha > 0.0 && beta > 0.0)) return false;  // BreakdownSignal, state untouched
+  const double zeta = 1.0 / sqrt(alpha);
+  const double eta = r.eta_next;
+  if (!r.hi_init) {  // LmaxEstimator.absorb
+    r.hi_om = zeta * zeta;
+    r.hi_zeta = zeta;
+    r.hi_init = 1;
+  } else {
+    const double le = r.hi_zeta * eta;
+    const double d = (le * le) * r.hi_h;
+    const double a = eta * eta + zeta * zeta;
+    const double oa = r.hi_om - a;
+    const double chi = sqrt(oa * oa + 4.0 * d);
+    const double h = (chi != 0.0) ? 0.5 * (1.0 - oa / chi) : 0.0;
+    r.hi_om = r.hi_om + chi * h;
+    r.hi_h = h;
+    r.hi_zeta = zeta;
+  }
+  if (!r.lo_init) {  // LminEstimator.absorb
+    r.lo_om = 1.0 / (zeta * zeta);
+    r.lo_a = r.lo_om;
+    r.lo_init = 1;
+  } else {
+    const double dn = -(eta / zeta) * (r.lo_g * r.lo_d + r.lo_h * r.lo_a);
+    const double an = (eta * eta * r.lo_a + 1.0) / (zeta * zeta);
+    const double oa = r.lo_om - an;
+    const double chi = sqrt(oa * oa + 4.0 * dn * dn);
+    double h2;
+    if (chi != 0.0) {
+      h2 = 0.5 * (1.0 - oa / chi);
+      h2 = py_max(h2, 0.0);
+      h2 = py_min(h2, 1.0);
+    } else {
+      h2 = 0.0;
+    }
+    r.lo_om = r.lo_om + chi * h2;
+    r.lo_g = sqrt(1.0 - h2);
+    r.lo_h = copysign(sqrt(h2), dn);
+    r.lo_d = dn;
+    r.lo_a = an;
+  }
+  r.eta_next = sqrt(beta / alpha);
+  r.psi = r.psi / (r.psi + beta);
+  r.count += 1;
+  if (r.count > 1) r.c = py_max(1.0, ritz_lmax(r) * sqrt(r.psi / ritz_lmin(r)));
+  return true;
+}
+__device__ __forceinline__ double ritz_xi(const RitzDev& r) {
+  if (r.count < 1) return 1.0;
+  return py_max(1.0, ritz_lmax(r) * sqrt(r.psi / ritz_lmin(r)));
+}
+
+// ritz.py:164-171
+__device__ double full_bound_c(int s, int n_a, double nu, double tau, double kappa) {
+  const double t = sqrt(2.0 * s + 1.0);
+  const double t3 = t * t * t;
+  return 2.0 * s * (2.0 * (3.0 + n_a) * nu * t + (6.0 + 8.0 * t) * tau + 2.0 * t3 + 3.0) * kappa;
+}
+
+// ritz.py:184-203 for the three state-only strategies
+__device__ double c_from_state(int kind, const RitzDev& r, double c0) {
+  if (kind == SSCG_C_ADAPTIVE) return r.c;
+  if (kind == SSCG_C_UNIT) return 1.0;
+  /* kappa-estimate */
+  return r.count >= 2 ? ritz_lmax(r) / ritz_lmin(r) : c0;
+}
+
+// ---------------------------------------------------------------------------
+// Warp-parallel cyclic Jacobi (round-robin ordering) on a symmetric n x n matrix
+// in shared memory (leading dimension JLD).  Eigenvalues are left on the
+// diagonal.  Replaces LAPACK dsyevd for the nested Gram blocks (<= 33 x 33).
+__device__ void warp_jacobi(double* A, int n, double* rot /* 4*17 */) {
+  const int lane = threadIdx.x & 31;
+  if (n <= 1) return;
+  const int m = n + (n & 1);
+  const int np = m / 2;
+  double fro2 = 0.0;
+  for (int i = lane; i < n * n; i += 32) {
+    const double v = A[(i / n) * JLD + (i % n)];
+    fro2 += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fro2 += __shfl_xor_sync(0xffffffffu, fro2, o);
+  const double floor_abs = sqrt(fro2) * 8.673617379884035e-19;  // 2^-60 ||A||_F
+  double* cs = rot;
+  double* sn = rot + 17;
+  int* pp = reinterpret_cast<int*>(rot + 34);
+  int* qq = pp + 17;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    int any = 0;
+    for (int r = 0; r < m - 1; ++r) {
+      if (lane < np) {
+        int p, q;
+        if (lane == 0) {
+          p = m - 1;
+          q = r;
+        } else {
+          p = (r + lane) % (m - 1);
+          q = (r - lane + (m - 1)) % (m - 1);
+        }
+        if (p > q) {
+          int t = p;
+          p = q;
+          q = t;
+        }
+        double c = 1.0, s = 0.0;
+        int act = 0;
+        if (q < n) {
+          const double apq = A[p * JLD + q];
+          const double app = A[p * JLD + p], aqq = A[q * JLD + q];
+          const double aa = fabs(apq);
+          if (aa > floor_abs && aa > 1.1102230246251565e-16 * sqrt(fabs(app)) * sqrt(fabs(aqq))) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            double t;
+            if (!isfinite(tau) || fabs(tau) > 1e100) {
+              t = isfinite(tau) ? 1.0 / (2.0 * tau) : 0.0;
+            } else if (tau != 0.0) {
+              t = copysign(1.0, tau) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            } else {
+              t = 1.0;
+            }
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            act = 1;
+          }
+        }
+        cs[lane] = c;
+        sn[lane] = s;
+        pp[lane] = act ? p : -1;
+        qq[lane] = q;
+        any |= act;
+      }
+      __syncwarp();
+      // rows: A[p,:], A[q,:]
+      for (int it = lane; it < np * n; it += 32) {
+        const int k = it / n, j = it % n;
+        const int p = pp[k];
+        if (p < 0) continue;
+        const int q = qq[k];
+        const double c = cs[k], s = sn[k];
+        const double ap = A[p * JLD + j], aq = A[q * JLD + j];
+        A[p * JLD + j] = c * ap - s * aq;
+        A[q * JLD + j] = s * ap + c * aq;
+      }
+      __syncwarp();
+      for (int it = lane; it < np * n; it += 32) {
+        const int k = it / n, i = it % n;
+        const int p = pp[k];
+        if (p < 0) continue;
+        const int q = qq[k];
+        const double c = cs[k], s = sn[k];
+        const double ap = A[i * JLD + p], aq = A[i * JLD + q];
+        A[i * JLD + p] = c * ap - s * aq;
+        A[i * JLD + q] = s * ap + c * aq;
+      }
+      __syncwarp();
+      if (lane < np && pp[lane] >= 0) {
+        A[pp[lane] * JLD + qq[lane]] = 0.0;
+        A[qq[lane] * JLD + pp[lane]] = 0.0;
+      }
+      __syncwarp();
+    }
+    any = __any_sync(0xffffffffu, any);
+    if (!any) break;
+  }
+}
+
+// lacore.py:103-117 on the Jacobi diagonal (lane 0 result)
+__device__ double cond_from_diag(const double* A, int n) {
+  double lmax = -INFINITY, smallest = INFINITY;
+  for (int i = 0; i < n; ++i) {
+    const double w = A[i * JLD + i];
+    lmax = (i == 0) ? w : py_max(lmax, w);
+    const double aw = fabs(w);
+    smallest = (i == 0) ? aw : py_min(smallest, aw);
+  }
+  if (!(lmax > 0.0)) return INFINITY;  // `if lmax <= 0.0` (NaN -> sqrt(NaN) below anyway)
+  if (smallest == 0.0) return INFINITY;
+  return sqrt(lmax / smallest);
+}
+
+// block index helper: columns of Y_{k,i} inside an s_bar-block (lacore.py:145)
+__device__ __forceinline__ int nested_col(int s_bar, int i, int q) {
+  return q <= i ? q : s_bar + 1 + (q - i - 1);
+}
+
+// nested_basis_conds: warp w handles i = w+1, w+1+NW, ...  G has leading dim ldg.
+__device__ void cta_nested_conds(const double* G, int ldg, int s_bar, double* conds,
+                                 double* jac /* NW * (CMAX*JLD + 68) */) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* A = jac + (size_t)warp * (CMAX * JLD + 68);
+  double* rot = A + CMAX * JLD;
+  if (threadIdx.x == 0) conds[0] = NAN;
+  for (int i = warp + 1; i <= s_bar; i += NW) {
+    const int n = 2 * i + 1;
+    for (int e = lane; e < n * n; e += 32) {
+      const int a = e / n, b = e % n;
+      A[a * JLD + b] = G[nested_col(s_bar, i, a) * ldg + nested_col(s_bar, i, b)];
+    }
+    __syncwarp();
+    warp_jacobi(A, n, rot);
+    if (lane == 0) conds[i] = cond_from_diag(A, n);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Basis parameters (basis.py:58-177), CTA-wide
+__device__ void set_monomial(ParamsDev& p, int s) {
+  p.kind = SSCG_BASIS_MONOMIAL;
+  p.has_from = 0;
+  p.lo = p.hi = NAN;
+  for (int i = 0; i < SMAX; ++i) {
+    p.th[i] = (i < s) ? 0.0 : NAN;
+    p.ga[i] = (i < s) ? 1.0 : NAN;
+    p.mu[i] = (i < s - 1) ? 0.0 : NAN;
+  }
+}
+__device__ void set_chebyshev(ParamsDev& p, int s, double lo, double hi) {
+  const double w = hi - lo;
+  p.kind = SSCG_BASIS_CHEBYSHEV;
+  p.has_from = 1;
+  p.lo = lo;
+  p.hi = hi;
+  for (int i = 0; i < SMAX; ++i) {
+    p.th[i] = (i < s) ? 0.5 * (lo + hi) : NAN;
+    p.ga[i] = (i == 0) ? w : ((i < s) ? 0.5 * w : NAN);
+    p.mu[i] = (i < s - 1) ? 0.125 * w : NAN;
+  }
+}
+
+// numpy pairwise sum of up to 15 warp-held terms (lane j holds term j), n < 16:
+// n < 8 sequential from 0.0; else 8-way tree then the tail sequentially.
+__device__ __forceinline__ double np_sum_warp(double term, int n) {
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = __shfl_sync(0xffffffffu, term, j);
+  double res;
+  if (n < 8) {
+    res = 0.0;
+    for (int j = 0; j < n; ++j) res += r[j];
+  } else {
+    res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (int j = 8; j < n; ++j) res += __shfl_sync(0xffffffffu, term, j);
+  }
+  return res;
+}
+__device__ __forceinline__ double leja_f(double x, const double* pts, int n) {
+  const int lane = threadIdx.x & 31;
+  const double term = (lane < n) ? log(fabs(x - pts[lane]) + 1e-300) : 0.0;
+  return np_sum_warp(term, n);
+}
+// basis.py:70-88 golden-section maximisation (warp-uniform)
+__device__ void golden_refine(const double* pts, int n, double lo, double hi, double* xo,
+                              double* vo) {
+  const double ratio = (sqrt(5.0) - 1.0) / 2.0;
+  double a = lo, b = hi;
+  double c = b - ratio * (b - a);
+  double d = a + ratio * (b - a);
+  double fc = leja_f(c, pts, n), fd = leja_f(d, pts, n);
+  for (int it = 0; it < 80; ++it) {
+    if (b - a <= 1e-14 * py_max(py_max(fabs(a), fabs(b)), 1.0)) break;
+    if (fc > fd) {
+      b = d;
+      d = c;
+      fd = fc;
+      c = b - ratio * (b - a);
+      fc = leja_f(c, pts, n);
+    } else {
+      a = c;
+      c = d;
+      fc = fd;
+      d = a + ratio * (b - a);
+      fd = leja_f(d, pts, n);
+    }
+  }
+  const double x = 0.5 * (a + b);
+  *xo = x;
+  *vo = leja_f(x, pts, n);
+}
+
+struct LejaShared {
+  double pts[SMAX];
+  double rx[4], rv[4];
+  int cand[LEJA_CAND_CAP];
+  int ncand;
+  int top[4];
+  int ntop;
+};
+
+__device__ __forceinline__ double lin_x(int i, int grid, double lo, double hi, double step,
+                                        bool zero_step) {
+  // numpy.linspace: y = arange * step + start, last point = stop exactly
+  if (i == grid - 1) return hi;
+  if (zero_step) return ((double)i / (double)(grid - 1)) * (hi - lo) + lo;
+  return (double)i * step + lo;
+}
+
+// basis.py:91-127 leja_points, CTA-wide; obj is a global scratch of `grid` doubles
+__device__ void cta_leja(double lo, double hi, int count, int grid, double* out, double* obj,
+                         LejaShared& L) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    L.pts[0] = hi;
+    L.pts[1] = lo;
+  }
+  __syncthreads();
+  if (count <= 2) {
+    if (tid < count) out[tid] = L.pts[tid];
+    __syncthreads();
+    return;
+  }
+  const double step = (hi - lo) / (double)(grid - 1);
+  const bool zero_step = (step == 0.0);
+  for (int n = 2; n < count; ++n) {
+    // grid objective, incrementally in numpy's pairwise order (see np_sum_warp)
+    for (int i = tid; i < grid; i += NT) {
+      const double x = lin_x(i, grid, lo, hi, step, zero_step);
+      double o;
+      if (n == 2) {
+        o = 0.0;
+        o += log(fabs(x - L.pts[0]) + 1e-300);
+        o += log(fabs(x - L.pts[1]) + 1e-300);
+      } else if (n == 8) {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = log(fabs(x - L.pts[j]) + 1e-300);
+        o = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      } else {
+        o = obj[i] + log(fabs(x - L.pts[n - 1]) + 1e-300);
+      }
+      obj[i] = o;
+    }
+    if (tid == 0) L.ncand = 0;
+    __syncthreads();
+    // interior local maxima (>= both neighbours)
+    for (int i = tid + 1; i < grid - 1; i += NT) {
+      const double v = obj[i];
+      if (v >= obj[i - 1] && v >= obj[i + 1]) {
+        const int slot = atomicAdd(&L.ncand, 1);
+        if (slot < LEJA_CAND_CAP) L.cand[slot] = i;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int nc = L.ncand < LEJA_CAND_CAP ? L.ncand : LEJA_CAND_CAP;
+      if (nc == 0) {  // np.argmax: first maximal index
+        int best = 0;
+        double bv = obj[0];
+        for (int i = 1; i < grid; ++i)
+          if (obj[i] > bv) {
+            bv = obj[i];
+            best = i;
+          }
+        L.cand[0] = best;
+        nc = 1;
+      }
+      // np.nonzero order (ascending index), then a stable ascending sort by value
+      for (int a = 1; a < nc; ++a) {
+        const int v = L.cand[a];
+        int b = a - 1;
+        while (b >= 0 && L.cand[b] > v) {
+          L.cand[b + 1] = L.cand[b];
+          --b;
+        }
+        L.cand[b + 1] = v;
+      }
+      for (int a = 1; a < nc; ++a) {
+        const int v = L.cand[a];
+        const double ov = obj[v];
+        int b = a - 1;
+        while (b >= 0 && obj[L.cand[b]] > ov) {
+          L.cand[b + 1] = L.cand[b];
+          --b;
+        }
+        L.cand[b + 1] = v;
+      }
+      const int nt = nc < 4 ? nc : 4;
+      for (int a = 0; a < nt; ++a) L.top[a] = L.cand[nc - nt + a];
+      L.ntop = nt;
+    }
+    __syncthreads();
+    if (warp < L.ntop) {
+      const int i = L.top[warp];
+      const int il = i - 1 > 0 ? i - 1 : 0;
+      const int ih = i + 1 < grid - 1 ? i + 1 : grid - 1;
+      double xr, vr;
+      golden_refine(L.pts, n, lin_x(il, grid, lo, hi, step, zero_step),
+                    lin_x(ih, grid, lo, hi, step, zero_step), &xr, &vr);
+      if ((tid & 31) == 0) {
+        L.rx[warp] = xr;
+        L.rv[warp] = vr;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double vmax = L.rv[0];
+      for (int a = 1; a < L.ntop; ++a) vmax = py_max(vmax, L.rv[a]);
+      const double thr = vmax - 1e-12 * py_max(1.0, fabs(vmax));
+      int have = 0;
+      double best = 0.0;
+      for (int a = 0; a < L.ntop; ++a) {
+        if (L.rv[a] >= thr) {
+          best = have ? py_min(best, L.rx[a]) : L.rx[a];
+          have = 1;
+        }
+      }
+      L.pts[n] = best;
+    }
+    __syncthreads();
+  }
+  if (tid < count) out[tid] = L.pts[tid];
+  __syncthreads();
+}
+
+// basis.py:166-177 params_for (kind checked by the host); returns 0 or SSCG_EPARAM
+__device__ int cta_params_for(int kind, int s, bool has, double lo, double hi, int grid,
+                              ParamsDev* out, double* obj, LejaShared& L) {
+  const bool usable = has && (0.0 < lo) && (lo < hi);
+  if (kind != SSCG_BASIS_MONOMIAL && usable) {
+    if (kind == SSCG_BASIS_NEWTON) {
+      __shared__ double lp[SMAX];
+      cta_leja(lo, hi, s, grid, lp, obj, L);
+      if (threadIdx.x == 0) {
+        out->kind = SSCG_BASIS_NEWTON;
+        out->has_from = 1;
+        out->lo = lo;
+        out->hi = hi;
+        for (int i = 0; i < SMAX; ++i) {
+          out->th[i] = (i < s) ? lp[i] : NAN;
+          out->ga[i] = (i < s) ? 1.0 : NAN;
+          out->mu[i] = (i < s - 1) ? 0.0 : NAN;
+        }
+      }
+      __syncthreads();
+      return 0;
+    }
+    if (threadIdx.x == 0) set_chebyshev(*out, s, lo, hi);
+    __syncthreads();
+    return 0;
+  }
+  if (threadIdx.x == 0) set_monomial(*out, s);
+  __syncthreads();
+  return 0;
+}
+
+// B = assemble_change_of_basis(s, params) into a dense (2s+1)^2 array, ld = ldb
+__device__ void build_bmat(double* B, int ldb, int s, const ParamsDev& p) {
+  const int dim = 2 * s + 1;
+  for (int e = threadIdx.x; e < dim * ldb; e += blockDim.x) B[e] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int blk = 0; blk < 2; ++blk) {
+      const int start = blk == 0 ? 0 : s + 1;
+      const int size = blk == 0 ? s + 1 : s;
+      for (int j = 0; j < size - 1; ++j) {
+        B[(start + j) * ldb + start + j] = p.th[j];
+        B[(start + j + 1) * ldb + start + j] = p.ga[j];
+        if (j >= 1) B[(start + j - 1) * ldb + start + j] = p.mu[j - 1];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// || |B| ||_2 via the warp Jacobi on |B|^T |B| (ritz.py:174-181), warp 0
+__device__ double warp_abs_norm(const double* B, int ldb, int dim, double* jac) {
+  const int lane = threadIdx.x & 31;
+  double* A = jac;
+  double* rot = jac + CMAX * JLD;
+  for (int e = lane; e < dim * dim; e += 32) {
+    const int i = e / dim, j = e % dim;
+    double acc = 0.0;
+    for (int q = 0; q < dim; ++q) acc += fabs(B[q * ldb + i]) * fabs(B[q * ldb + j]);
+    A[i * JLD + j] = acc;
+  }
+  __syncwarp();
+  warp_jacobi(A, dim, rot);
+  double top = A[0];
+  for (int i = 1; i < dim; ++i) top = py_max(top, A[i * JLD + i]);
+  return sqrt(py_max(0.0, top));
+}
+
+// ---------------------------------------------------------------------------
+// warp-0 helpers for the coefficient-space inner loop (dim <= 33)
+__device__ __forceinline__ double warp_dot0(const double* u, const double* v, int dim) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int i = lane; i < dim; i += 32) s = fma(u[i], v[i], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  return __shfl_sync(0xffffffffu, s, 0);
+}
+__device__ __forceinline__ void warp_matvec(const double* M, int ldm, const double* v, double* out,
+                                            int dim) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < dim; i += 32) {
+    double s = 0.0;
+    for (int j = 0; j < dim; ++j) s = fma(M[i * ldm + j], v[j], s);
+    out[i] = s;
+  }
+  __syncwarp();
+}
+
+__device__ double cta_sum(const double* part, int n, double* red) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += NT) s += part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = NT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+struct SmallShared {
+  double G[CMAX * CMAX];   // s_bar-block Gram, ld CMAX
+  double B[CMAX * CMAX];   // B(s_bar) then B_t, ld CMAX
+  double Gt[CMAX * CMAX];  // truncated Gram, ld CMAX
+  double conds[SMAX + 1];
+  double xp[CMAX], rp[CMAX], pp[CMAX], t1[CMAX], t2[CMAX];
+  double red[NT];
+  double sc[16];
+  int si[16];
+  LejaShared L;
+};
+
+constexpr size_t JAC_BYTES = sizeof(double) * (size_t)NW * (CMAX * JLD + 68);
+
+enum { SC_TRUE, SC_UPD, SC_CSEL, SC_RREL, SC_CBLK, SC_PHI };
+enum { SI_FLAG, SI_SBAR, SI_STILDE, SI_JDONE, SI_DIV, SI_BRKJ };
+
+// ---------------------------------------------------------------------------
+// K_small
+__global__ void __launch_bounds__(NT) k_small(Ctx c) {
+  extern __shared__ __align__(16) double dsm[];
+  SmallShared& S = *reinterpret_cast<SmallShared*>(dsm);
+  double* jac = dsm + (sizeof(SmallShared) + 7) / 8;
+  SolverState* st = c.st;
+  const DevConfig& cf = *c.cfg;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (st->done) {  // nothing of this outer loop may apply
+    if (tid == 0) {
+      st->rec_valid = 0;
+      st->diag_n = 0;
+    }
+    return;
+  }
+  const double t2 = cta_sum(c.part_t, RED_BLOCKS, S.red);
+  const double r2 = cta_sum(c.part_r, RED_BLOCKS, S.red);
+
+  // ---- outer boundary: classification (adaptive.py:138-148, sstep.py:61-76)
+  if (tid == 0) {
+    st->rec_valid = 0;
+    st->diag_n = 0;
+    const double nb = st->nb;
+    const double true_rel = sqrt(t2) / nb;
+    const double upd_rel = sqrt(r2) / nb;
+    const int k = st->k;
+    S.sc[SC_TRUE] = true_rel;
+    S.sc[SC_UPD] = upd_rel;
+    if (k <= cf.cap_outer) c.outer_true[k] = true_rel;
+    if (!cf.trace_full && st->total_iters > 0) {  // fast trace: close the last block
+      const int64_t li = st->total_iters - 1;
+      if (li < cf.cap_iters) {
+        double* row = c.it_log + li * SSCG_IT_N;
+        row[SSCG_IT_TRUE] = true_rel;
+        row[SSCG_IT_GAP] = fabs(true_rel - row[SSCG_IT_UPD]);
+      }
+    }
+    int outcome = SSCG_RUNNING;
+    if (k >= cf.max_outer) {  // loop exhausted: adaptive.py:262-266
+      outcome = (true_rel <= cf.eps_star) ? SSCG_CONVERGED : SSCG_STAGNATED;
+    } else if (true_rel <= cf.eps_star) {
+      outcome = SSCG_CONVERGED;
+    } else if (!isfinite(true_rel) || true_rel > 1e5) {
+      outcome = SSCG_DIVERGED;
+    } else if (true_rel < st->best) {
+      st->best = true_rel;
+      st->best_iter = st->total_iters;
+    } else if (st->total_iters - st->best_iter >= 200 && upd_rel <= 0.01 * true_rel) {
+      outcome = SSCG_STAGNATED;
+    }
+    if (outcome == SSCG_RUNNING && st->breakdown) outcome = SSCG_DIVERGED;  // basis.py:220
+    if (outcome != SSCG_RUNNING) {
+      st->status = outcome;
+      st->done = 1;
+    }
+    S.si[SI_FLAG] = st->done;
+    S.si[SI_SBAR] = st->s_bar;
+  }
+  __syncthreads();
+  if (S.si[SI_FLAG]) return;
+
+  const int sbar = S.si[SI_SBAR];
+  const int sigma = cf.sigma, ncols = cf.ncols;
+  const int D = 2 * sbar + 1;
+  const double nb = st->nb, u = cf.unit, eps = cf.eps_star;
+
+  // ---- s_bar-block Gram (physical columns P_0..P_sbar, R_0..R_{sbar-1})
+  for (int e = tid; e < D * D; e += NT) {
+    const int i = e / D, j = e % D;
+    const int pi = i <= sbar ? i : sigma + 1 + (i - sbar - 1);
+    const int pj = j <= sbar ? j : sigma + 1 + (j - sbar - 1);
+    const double v = st->gram[pi * ncols + pj];
+    S.G[i * CMAX + j] = v;
+    if (!st->first_saved) c.first_gram[e] = v;
+  }
+  __syncthreads();
+  if (tid == 0) st->first_saved = 1;
+
+  // ---- c_sel (adaptive.py:150-157)
+  if (cf.c_strategy == SSCG_C_FULLBOUND) {
+    build_bmat(S.B, CMAX, sbar, st->prm);
+    if (warp == 0) {
+      const double an = warp_abs_norm(S.B, CMAX, D, jac);
+      if (lane == 0)
+        S.sc[SC_CSEL] = full_bound_c(sbar, cf.n_a, cf.nu, an / cf.norm_a, cf.kappa_a);
+    }
+  } else if (tid == 0) {
+    S.sc[SC_CSEL] = c_from_state(cf.c_strategy, st->rz, cf.c0);
+  }
+  __syncthreads();
+
+  // ---- nested condition estimates and s~ (adaptive.py:89-104)
+  cta_nested_conds(S.G, CMAX, sbar, S.conds, jac);
+  __syncthreads();
+  if (tid == 0) {
+    const double r_rel = S.sc[SC_UPD];
+    const double bound = eps / (S.sc[SC_CSEL] * u * r_rel);
+    int s_t = 1;
+    for (int i = 1; i <= sbar; ++i)
+      if (S.conds[i] <= bound) s_t = i;
+    S.si[SI_STILDE] = s_t;
+    S.sc[SC_RREL] = r_rel;
+  }
+  __syncthreads();
+  const int s_t = S.si[SI_STILDE];
+  const int dim = 2 * s_t + 1;
+
+  // ---- truncated block: G_t and B_t (adaptive.py:162-171)
+  for (int e = tid; e < dim * dim; e += NT) {
+    const int i = e / dim, j = e % dim;
+    const int gi = i <= s_t ? i : sbar + 1 + (i - s_t - 1);
+    const int gj = j <= s_t ? j : sbar + 1 + (j - s_t - 1);
+    S.Gt[i * CMAX + j] = S.G[gi * CMAX + gj];
+  }
+  build_bmat(S.B, CMAX, s_t, st->prm);  // (syncs)
+
+  // ---- c_block (adaptive.py:175)
+  if (cf.c_strategy == SSCG_C_FULLBOUND) {
+    if (warp == 0) {
+      const double an = warp_abs_norm(S.B, CMAX, dim, jac);
+      if (lane == 0)
+        S.sc[SC_CBLK] = full_bound_c(s_t, cf.n_a, cf.nu, an / cf.norm_a, cf.kappa_a);
+    }
+  } else if (tid == 0) {
+    S.sc[SC_CBLK] = c_from_state(cf.c_strategy, st->rz, cf.c0);
+  }
+  __syncthreads();
+
+  // ---- coefficient-space inner loop (adaptive.py:173-246), warp 0
+  if (warp == 0) {
+    for (int i = lane; i < CMAX; i += 32) {
+      S.xp[i] = 0.0;
+      S.rp[i] = (i == s_t + 1) ? 1.0 : 0.0;
+      S.pp[i] = (i == 0) ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    warp_matvec(S.Gt, CMAX, S.rp, S.t1, dim);
+    const double q0 = warp_dot0(S.rp, S.t1, dim);
+    double phi = sqrt(py_max(0.0, q0)) / nb;
+    const double c_blk = S.sc[SC_CBLK];
+    const int mark = st->total_iters;
+    int it = st->total_iters;
+    int j_done = 0, diverged = 0, brk_j = -1;
+    double brk_l = NAN, brk_r = NAN;
+    RitzDev rz = st->rz;
+    for (int j = 0; j < s_t; ++j) {
+      warp_matvec(S.Gt, CMAX, S.rp, S.t1, dim);
+      const double num = warp_dot0(S.rp, S.t1, dim);
+      warp_matvec(S.B, CMAX, S.pp, S.t1, dim);
+      warp_matvec(S.Gt, CMAX, S.t1, S.t2, dim);
+      const double den = warp_dot0(S.pp, S.t2, dim);
+      if (den <= 0.0 || num < 0.0 || !isfinite(den) || !isfinite(num)) {
+        diverged = 1;
+        break;
+      }
+      const double alpha = num / den;
+      for (int i = lane; i < dim; i += 32) {
+        const double q = alpha * S.pp[i];
+        S.t1[i] = q;
+        S.xp[i] = S.xp[i] + q;
+      }
+      __syncwarp();
+      warp_matvec(S.B, CMAX, S.t1, S.t2, dim);
+      for (int i = lane; i < dim; i += 32) S.rp[i] = S.rp[i] - S.t2[i];
+      __syncwarp();
+      warp_matvec(S.Gt, CMAX, S.rp, S.t1, dim);
+      const double rr = warp_dot0(S.rp, S.t1, dim);
+      const double beta = rr / num;
+      for (int i = lane; i < dim; i += 32) S.pp[i] = S.rp[i] + beta * S.pp[i];
+      __syncwarp();
+      j_done = j + 1;
+      if (alpha > 0.0 && beta > 0.0 && isfinite(alpha) && isfinite(beta))
+        ritz_absorb(rz, alpha, beta);  // identical in every lane
+      const double est = sqrt(py_max(0.0, rr)) / nb;
+      phi = py_max(phi, est);
+      if (lane == 0 && it < cf.cap_iters) {
+        double* row = c.it_log + (int64_t)it * SSCG_IT_N;
+        row[SSCG_IT_ALPHA] = alpha;
+        row[SSCG_IT_BETA] = beta;
+        row[SSCG_IT_XI] = ritz_xi(rz);
+        row[SSCG_IT_LMIN] = ritz_lmin(rz);
+        row[SSCG_IT_LMAX] = ritz_lmax(rz);
+        row[SSCG_IT_PSI] = rz.psi;
+        row[SSCG_IT_EST] = est;
+        if (!cf.trace_full) {
+          row[SSCG_IT_TRUE] = est;
+          row[SSCG_IT_UPD] = est;
+          row[SSCG_IT_GAP] = NAN;
+        }
+      }
+      if (cf.trace_full) {
+        // physical-column coordinates of (x_j - x, r_j)
+        for (int i = lane; i < CMAX; i += 32) {
+          st->dx[j][i] = 0.0;
+          st->dr[j][i] = 0.0;
+        }
+        __syncwarp();
+        for (int i = lane; i < dim; i += 32) {
+          const int ph = (i <= s_t) ? i : sigma + 1 + (i - s_t - 1);
+          st->dx[j][ph] = S.xp[i];
+          st->dr[j][ph] = S.rp[i];
+        }
+      }
+      ++it;
+      if (rr >= 0.0 && est <= eps && j < s_t - 1) break;  // est_hit
+      if (cf.variant == 1) {
+        const double c_now =
+            (cf.c_strategy == SSCG_C_FULLBOUND) ? c_blk : c_from_state(cf.c_strategy, rz, cf.c0);
+        const double thr = eps / (c_now * u * phi);
+        if (j < s_t - 1 && S.conds[j + 2] >= thr) {
+          brk_j = j;
+          brk_l = S.conds[j + 2];
+          brk_r = thr;
+          break;
+        }
+      } else if (est > 0.0) {
+        const double thr = eps / (c_blk * u * est);
+        if (S.conds[s_t] >= thr) {
+          brk_j = j;
+          brk_l = S.conds[s_t];
+          brk_r = thr;
+          break;
+        }
+      }
+    }
+    if (lane == 0) {
+      st->rz = rz;
+      // trace.mark_outer + record (adaptive.py:178, 232-246)
+      const int k = st->k;
+      st->total_outer += 1;
+      st->total_iters = it;
+      st->diag_base = mark;
+      st->diag_n = cf.trace_full ? j_done : 0;
+      st->s_tilde = s_t;
+      const int rk = st->n_records;
+      if (rk < cf.cap_outer) {
+        int* ri = c.rec_i + (int64_t)rk * SSCG_REC_NI;
+        double* rd = c.rec_d + (int64_t)rk * SSCG_RECD_ND;
+        ri[SSCG_REC_K] = k;
+        ri[SSCG_REC_SBAR] = sbar;
+        ri[SSCG_REC_STILDE] = s_t;
+        ri[SSCG_REC_SACTUAL] = j_done;
+        ri[SSCG_REC_BREAKJ] = brk_j;
+        ri[SSCG_REC_MARK] = mark;
+        ri[SSCG_REC_PKIND] = st->prm.kind;
+        rd[SSCG_RECD_PHI] = phi;
+        rd[SSCG_RECD_BLHS] = brk_l;
+        rd[SSCG_RECD_BRHS] = brk_r;
+        rd[SSCG_RECD_GEN_LO] = st->prm.has_from ? st->prm.lo : NAN;
+        rd[SSCG_RECD_GEN_HI] = st->prm.has_from ? st->prm.hi : NAN;
+        rd[SSCG_RECD_TRUE] = S.sc[SC_TRUE];
+        rd[SSCG_RECD_RREL] = S.sc[SC_RREL];
+        rd[SSCG_RECD_C] = S.sc[SC_CSEL];
+        for (int i = 0; i <= SMAX; ++i)
+          c.rec_conds[(int64_t)rk * (SMAX + 1) + i] = (i <= sbar) ? S.conds[i] : NAN;
+        for (int i = 0; i < SMAX; ++i) {
+          c.rec_th[(int64_t)rk * SMAX + i] = st->prm.th[i];
+          c.rec_ga[(int64_t)rk * SMAX + i] = st->prm.ga[i];
+          c.rec_mu[(int64_t)rk * SMAX + i] = st->prm.mu[i];
+        }
+      }
+      st->n_records = rk + 1;
+      if (diverged) {
+        st->status = SSCG_DIVERGED;
+        st->done = 1;
+      } else {
+        st->rec_valid = 1;
+        st->s_act = j_done;
+      }
+      S.si[SI_DIV] = diverged;
+      S.si[SI_JDONE] = j_done;
+    }
+    // recovery coefficients in physical columns (zero elsewhere)
+    __syncwarp();
+    if (!S.si[SI_DIV]) {
+      for (int i = lane; i < CMAX; i += 32) {
+        st->cx[i] = 0.0;
+        st->cr[i] = 0.0;
+        st->cp[i] = 0.0;
+      }
+      __syncwarp();
+      for (int i = lane; i < dim; i += 32) {
+        const int ph = (i <= s_t) ? i : sigma + 1 + (i - s_t - 1);
+        st->cx[ph] = S.xp[i];
+        st->cr[ph] = S.rp[i];
+        st->cp[ph] = S.pp[i];
+      }
+    }
+  }
+  __syncthreads();
+  if (S.si[SI_DIV]) return;
+
+  // ---- next block's parameters (adaptive.py:254-258) and s_bar (adaptive.py:143)
+  if (cf.variant == 1 && cf.basis_kind != SSCG_BASIS_MONOMIAL) {
+    const RitzDev& rz = st->rz;
+    if (st->total_iters > 1 && rz.count >= 2) {
+      const double lmin = ritz_lmin(rz), lmax = ritz_lmax(rz);
+      if (0.0 < lmin && lmin < lmax)
+        cta_params_for(cf.basis_kind, sigma, true, lmin, lmax, cf.leja_grid, &st->prm, c.leja_obj,
+                       S.L);
+    }
+  }
+  if (tid == 0) {
+    const int nxt = S.si[SI_JDONE] + cf.f;
+    st->s_bar = nxt < sigma ? nxt : sigma;
+    st->k = st->k + 1;
+    st->breakdown = 0;
+  }
+}
+
+// full trace: reduce the diag partials of inner iteration j into the log
+__global__ void __launch_bounds__(NT) k_diag_fin(Ctx c, int j) {
+  __shared__ double red[NT];
+  const SolverState* st = c.st;
+  if (j >= st->diag_n) return;
+  const double t = cta_sum(c.part_d, RED_BLOCKS, red);
+  const double r = cta_sum(c.part_d + RED_BLOCKS, RED_BLOCKS, red);
+  const double g = cta_sum(c.part_d + 2 * RED_BLOCKS, RED_BLOCKS, red);
+  if (threadIdx.x == 0) {
+    const int64_t it = st->diag_base + j;
+    if (it < c.cfg->cap_iters) {
+      double* row = c.it_log + it * SSCG_IT_N;
+      row[SSCG_IT_TRUE] = sqrt(t) / st->nb;
+      row[SSCG_IT_UPD] = sqrt(r) / st->nb;
+      row[SSCG_IT_GAP] = sqrt(g);
+    }
+  }
+}
+
+// initial state (adaptive.py:117-135)
+__global__ void __launch_bounds__(NT) k_state_init(Ctx c) {
+  extern __shared__ __align__(16) double dsm[];
+  SmallShared& S = *reinterpret_cast<SmallShared*>(dsm);
+  SolverState* st = c.st;
+  const DevConfig& cf = *c.cfg;
+  const double b2 = cta_sum(c.part_t, RED_BLOCKS, S.red);
+  if (threadIdx.x == 0) {
+    st->k = 0;
+    st->done = 0;
+    st->status = SSCG_RUNNING;
+    st->s_bar = cf.s_bar0;
+    st->s_tilde = 1;
+    st->s_act = 0;
+    st->rec_valid = 0;
+    st->total_iters = 0;
+    st->total_outer = 0;
+    st->n_records = 0;
+    st->best_iter = 0;
+    st->breakdown = 0;
+    st->first_saved = 0;
+    st->diag_base = 0;
+    st->diag_n = 0;
+    st->gram_count = 0;
+    st->best = INFINITY;
+    st->nb = sqrt(b2);
+    ritz_init(st->rz, cf.c0);
+  }
+  __syncthreads();
+  if (cf.variant == 0 || cf.basis_kind == SSCG_BASIS_MONOMIAL)
+    cta_params_for(cf.basis_kind, cf.sigma, cf.has_bounds != 0, cf.bound_lo, cf.bound_hi,
+                   cf.leja_grid, &st->prm, c.leja_obj, S.L);
+  else if (threadIdx.x == 0)
+    set_monomial(st->prm, cf.sigma);
+}
+
+// ---- unit-entry kernels -----------------------------------------------------
+__global__ void __launch_bounds__(NT)
+    k_unit_conds(const double* G, int s_bar, double* conds, double c, double u, double eps,
+                 double rn, int* s_tilde) {
+  extern __shared__ __align__(16) double dsm[];
+  SmallShared& S = *reinterpret_cast<SmallShared*>(dsm);
+  double* jac = dsm + (sizeof(SmallShared) + 7) / 8;
+  const int D = 2 * s_bar + 1;
+  for (int e = threadIdx.x; e < D * D; e += NT) S.G[(e / D) * CMAX + e % D] = G[e];
+  __syncthreads();
+  cta_nested_conds(S.G, CMAX, s_bar, S.conds, jac);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i <= s_bar; ++i) conds[i] = S.conds[i];
+    const double bound = eps / (c * u * rn);
+    int st = 1;
+    for (int i = 1; i <= s_bar; ++i)
+      if (S.conds[i] <= bound) st = i;
+    *s_tilde = st;
+  }
+}
+
+__global__ void __launch_bounds__(NT)
+    k_unit_params(int kind, int s, int has, double lo, double hi, int grid, ParamsDev* out,
+                  double* obj) {
+  extern __shared__ __align__(16) double dsm[];
+  SmallShared& S = *reinterpret_cast<SmallShared*>(dsm);
+  cta_params_for(kind, s, has != 0, lo, hi, grid, out, obj, S.L);
+}
+
+__global__ void __launch_bounds__(NT)
+    k_unit_leja(double lo, double hi, int count, int grid, double* out, double* obj) {
+  extern __shared__ __align__(16) double dsm[];
+  SmallShared& S = *reinterpret_cast<SmallShared*>(dsm);
+  cta_leja(lo, hi, count, grid, out, obj, S.L);
+}
+
+__global__ void k_unit_ritz(int m, const double* a, const double* b, double* rec, double c0) {
+  RitzDev r;
+  ritz_init(r, c0);
+  for (int i = 0; i < m; ++i) {
+    ritz_absorb(r, a[i], b[i]);
+    double* o = rec + (int64_t)i * 6;
+    o[0] = ritz_lmin(r);
+    o[1] = ritz_lmax(r);
+    o[2] = r.psi;
+    o[3] = r.c;
+    o[4] = ritz_xi(r);
+    o[5] = (double)r.count;
+  }
+}
+
+__global__ void k_unit_symeig(int n, const double* M, double* w) {
+  __shared__ double A[CMAX * JLD + 68];
+  const int lane = threadIdx.x;
+  for (int e = lane; e < n * n; e += 32) A[(e / n) * JLD + e % n] = M[e];
+  __syncwarp();
+  warp_jacobi(A, n, A + CMAX * JLD);
+  if (lane == 0) {
+    for (int i = 0; i < n; ++i) w[i] = A[i * JLD + i];
+    for (int a = 1; a < n; ++a) {  // ascending
+      double v = w[a];
+      int b = a - 1;
+      while (b >= 0 && w[b] > v) {
+        w[b + 1] = w[b];
+        --b;
+      }
+      w[b + 1] = v;
+    }
+  }
+}
+
+bool g_attr_set = false;
+void ensure_attr() {
+  if (g_attr_set) return;
+  const int bytes = (int)small_smem_bytes();
+  cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_state_init, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_unit_conds, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_unit_params, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_unit_leja, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  g_attr_set = true;
+}
+
+double host_c0() { return pow(ldexp(1.0, -53), -0.5); }
+
+}  // namespace
+
+size_t small_smem_bytes() { return ((sizeof(SmallShared) + 7) / 8) * 8 + JAC_BYTES; }
+
+void small_prepare() { ensure_attr(); }
+
+void launch_state_init(const Ctx& c, cudaStream_t s) {
+  k_state_init<<<1, NT, small_smem_bytes(), s>>>(c);
+}
+void launch_small(const Ctx& c, cudaStream_t s) { k_small<<<1, NT, small_smem_bytes(), s>>>(c); }
+void launch_diag_fin(const Ctx& c, int j, cudaStream_t s) { k_diag_fin<<<1, NT, 0, s>>>(c, j); }
+
+// ---- unit entry helpers (synchronous, own allocations) ----------------------
+#define U_OK(expr)                                   \
+  do {                                               \
+    cudaError_t e__ = (expr);                        \
+    if (e__ != cudaSuccess) {                        \
+      rc = sscg_fail_cuda(e__, #expr);               \
+      goto done;                                     \
+    }                                                \
+  } while (0)
+
+int unit_nested_conds(const double* g_host, int s_bar, double* conds_host, int mode, double c,
+                      double unit, double eps, double rn, int* s_tilde) {
+  (void)mode;
+  ensure_attr();
+  int rc = SSCG_OK;
+  const int D = 2 * s_bar + 1;
+  double *dg = nullptr, *dc = nullptr;
+  int* ds = nullptr;
+  U_OK(cudaMalloc(&dg, sizeof(double) * D * D));
+  U_OK(cudaMalloc(&dc, sizeof(double) * (s_bar + 1)));
+  U_OK(cudaMalloc(&ds, sizeof(int)));
+  U_OK(cudaMemcpy(dg, g_host, sizeof(double) * D * D, cudaMemcpyHostToDevice));
+  k_unit_conds<<<1, NT, small_smem_bytes()>>>(dg, s_bar, dc, c, unit, eps, rn, ds);
+  U_OK(cudaGetLastError());
+  U_OK(cudaMemcpy(conds_host, dc, sizeof(double) * (s_bar + 1), cudaMemcpyDeviceToHost));
+  if (s_tilde) U_OK(cudaMemcpy(s_tilde, ds, sizeof(int), cudaMemcpyDeviceToHost));
+done:
+  cudaFree(dg);
+  cudaFree(dc);
+  cudaFree(ds);
+  return rc;
+}
+
+int unit_leja(double lo, double hi, int count, int grid, double* out) {
+  ensure_attr();
+  int rc = SSCG_OK;
+  double *dout = nullptr, *obj = nullptr;
+  U_OK(cudaMalloc(&dout, sizeof(double) * SMAX));
+  U_OK(cudaMalloc(&obj, sizeof(double) * (grid > 0 ? grid : 1)));
+  k_unit_leja<<<1, NT, small_smem_bytes()>>>(lo, hi, count, grid, dout, obj);
+  U_OK(cudaGetLastError());
+  U_OK(cudaMemcpy(out, dout, sizeof(double) * count, cudaMemcpyDeviceToHost));
+done:
+  cudaFree(dout);
+  cudaFree(obj);
+  return rc;
+}
+
+int unit_params_for(int kind, int s, int has, double lo, double hi, int grid, double* th,
+                    double* ga, double* mu, int* kind_out) {
+  ensure_attr();
+  int rc = SSCG_OK;
+  ParamsDev* dp = nullptr;
+  double* obj = nullptr;
+  ParamsDev hp;
+  U_OK(cudaMalloc(&dp, sizeof(ParamsDev)));
+  U_OK(cudaMalloc(&obj, sizeof(double) * (grid > 0 ? grid : 1)));
+  k_unit_params<<<1, NT, small_smem_bytes()>>>(kind, s, has, lo, hi, grid, dp, obj);
+  U_OK(cudaGetLastError());
+  U_OK(cudaMemcpy(&hp, dp, sizeof(ParamsDev), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < s; ++i) {
+    th[i] = hp.th[i];
+    ga[i] = hp.ga[i];
+    if (i < s - 1) mu[i] = hp.mu[i];
+  }
+  *kind_out = hp.kind;
+done:
+  cudaFree(dp);
+  cudaFree(obj);
+  return rc;
+}
+
+int unit_ritz(int m, const double* a, const double* b, double* rec) {
+  int rc = SSCG_OK;
+  double *da = nullptr, *db = nullptr, *dr = nullptr;
+  const size_t mm = m > 0 ? m : 1;
+  U_OK(cudaMalloc(&da, sizeof(double) * mm));
+  U_OK(cudaMalloc(&db, sizeof(double) * mm));
+  U_OK(cudaMalloc(&dr, sizeof(double) * mm * 6));
+  U_OK(cudaMemcpy(da, a, sizeof(double) * m, cudaMemcpyHostToDevice));
+  U_OK(cudaMemcpy(db, b, sizeof(double) * m, cudaMemcpyHostToDevice));
+  k_unit_ritz<<<1, 1>>>(m, da, db, dr, host_c0());
+  U_OK(cudaGetLastError());
+  U_OK(cudaMemcpy(rec, dr, sizeof(double) * m * 6, cudaMemcpyDeviceToHost));
+done:
+  cudaFree(da);
+  cudaFree(db);
+  cudaFree(dr);
+  return rc;
+}
+
+int unit_sym_eig(int n, const double* m, double* w) {
+  int rc = SSCG_OK;
+  double *dm = nullptr, *dw = nullptr;
+  U_OK(cudaMalloc(&dm, sizeof(double) * n * n));
+  U_OK(cudaMalloc(&dw, sizeof(double) * n));
+  U_OK(cudaMemcpy(dm, m, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  k_unit_symeig<<<1, 32>>>(n, dm, dw);
+  U_OK(cudaGetLastError());
+  U_OK(cudaMemcpy(w, dw, sizeof(double) * n, cudaMemcpyDeviceToHost));
+done:
+  cudaFree(dm);
+  cudaFree(dw);
+  return rc;
+}
+
+double sscg_host_c0() { return host_c0(); }
