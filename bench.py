@@ -1,0 +1,334 @@
+"""Benchmark: adaptive s-step CG (arXiv 1908.04081) on B200 -- BASELINE.json metric
+"s-step CG iterations/sec & HBM GB/s (frac of peak) at 1/2/4/8 B200; syncs to tol".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5w] [--impl reference]
+
+One step = one full solve to eps* (the hot path: every outer loop's matrix-powers
+levels, Gram, O(s^2) control kernel and recovery, on the device).  Workload at
+N=1: config c5 weak-scaled, a 256^3 7-point Poisson slab per GPU, sigma=12,
+dynamic Newton basis, eps*=1e-10 (BASELINE.json configs[4]); the other configs
+are parity-test cases (tests/), selectable with --config for reference.
+
+value   CG iterations/s of the solve with b, x0 and A resident in HBM, device
+        time (CUDA events on the solver stream) summed over the K timed solves.
+e2e     the same metric through the public drop-in `adaptive_solve(problem, cfg,
+        trace="fast")` with host buffers: H2D of b and x0 and D2H of x and the
+        logs inside the timed region (wall clock, synchronised).
+roofline  dominant kernel = K_mpk (matrix-powers levels): algorithmic bytes
+        (12 nnz + 4 (n+1) per level of A, 16 n per generated
+        column, + x, b on level 0) / its CUDA-event time, from one profiled solve
+        after the timed region, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the CPU oracle port (oracle/sscg_oracle.py: the reference's
+        numpy/scipy arithmetic, diagnostics off) timed on this host for a
+        bounded sample (1 outer loop of the same problem), extrapolated to the
+        solve's outer-loop count.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (problem key, scale override, sigma, basis, eps*, description)
+    "c5w": ("c5w", None, 12, "newton", 1e-10,
+            "c5 weak-scaled: 3D Poisson 7-pt 256^3 per GPU, sigma=12 Newton, eps*=1e-10"),
+    "c3": ("c3", None, 10, "chebyshev", 1e-10, "c3: 3D Poisson 7-pt 128^3, sigma=10 Chebyshev, 1e-10"),
+    "c4": ("c4", None, 10, "newton", 1e-8, "c4: 27-pt var-coef 192^3, sigma=10 Newton, 1e-8"),
+    "c1": ("c1", None, 8, "newton", 1e-10, "c1: 2D Poisson 64^2, sigma=8 Newton, 1e-10"),
+    "c2": ("c2", None, 10, "chebyshev", 1e-8, "c2: Strakos 1e4, sigma=10 Chebyshev, 1e-8"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+def mpk_bytes_per_outer(n, nnz, sigma, mu_nonzero):
+    """Algorithmic bytes of the sigma matrix-powers levels of one outer loop
+    (SURVEY.md 8(d)): A once per level, 16 n per generated column (+8 n for the
+    Chebyshev two-back term), x and b on level 0 (true residual)."""
+    s_a = 12 * nnz + 4 * (n + 1)
+    gen = 2 * sigma - 1
+    two_back = (2 * sigma - 3) if mu_nonzero else 0  # columns with l >= 1
+    return sigma * s_a + 16 * n * gen + 8 * n * two_back + 16 * n + 8 * n  # + r0 norm read
+
+
+def outer_bytes(n, nnz, sigma, s_t, mu_nonzero):
+    return (mpk_bytes_per_outer(n, nnz, sigma, mu_nonzero) + 8 * n * (2 * sigma + 1)
+            + 8 * n * (2 * s_t + 1) + 8 * n + 24 * n)
+
+
+def cpu_sample(prob, cfg_kw, outer_count, total_iters):
+    """Oracle port on this host: 1 outer loop of the same problem (bounded),
+    per-outer time extrapolated to the solve's outer count."""
+    from oracle import sscg_oracle as O
+    t0 = time.perf_counter()
+    O.solve_problem(prob, O.OracleConfig(max_outer=1, **cfg_kw), diagnostics=False)
+    t1 = time.perf_counter() - t0
+    est = t1 * (outer_count + 1)
+    return total_iters / est, t1
+
+
+def run_ours(args, rank, world):
+    from paper_1908_04081_b200 import AdaptiveConfig, _lib as L, adaptive_solve, problems
+    from paper_1908_04081_b200.adaptive import LogBuffers, make_config
+    from paper_1908_04081_b200.kernels import _plan
+
+    key, scale, sigma, basis, eps, desc = CONFIGS[args.config]
+    if world > 1:
+        raise SystemExit("multi-GPU partitioned bench: run with --gpus 1 (see DESIGN.md 8(e))")
+    t0 = time.perf_counter()
+    prob = problems.make_problem(key, scale=args.scale or scale, world=world)
+    t_gen = time.perf_counter() - t0
+    cfg_kw = dict(sigma=sigma, eps_star=eps, basis_kind=basis)
+    cfg = AdaptiveConfig(**cfg_kw)
+    n, nnz = prob.a.n, prob.a.nnz
+    plan = _plan(prob.a, 0)
+    lib = L.load()
+    cfg, ccfg = make_config(cfg, prob, "fast")
+    logs = LogBuffers(cfg)
+    b = L.f64(prob.b)
+    x0 = L.f64(prob.x0)
+    L.check(lib.sscg_load(plan.handle, L.dptr(b), L.dptr(x0)))
+
+    def dev_solve():
+        L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
+        return logs.s.device_ms, int(logs.s.outer_launched)
+
+    for _ in range(args.warmup):
+        dev_solve()
+    # ---- timed region (device time, inputs resident in HBM)
+    ms_list, launches = [], 0
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            ms, ol = dev_solve()
+            ms_list.append(ms)
+            launches += 2 + ol * (sigma + 3)
+    L.check(lib.sscg_fetch(plan.handle, None, logs.s))
+    total_iters, total_outer = int(logs.s.total_iters), int(logs.s.total_outer)
+    converged = int(logs.s.status) == L.CONVERGED
+    x = np.empty(n)
+    L.check(lib.sscg_fetch(plan.handle, L.dptr(x), logs.s))
+    import scipy.sparse as sp
+    a = prob.a
+    rel = float(np.linalg.norm(prob.b - sp.csr_matrix((a.values, a.col_idx, a.row_ptr),
+                                                      shape=(n, n)) @ x) / np.linalg.norm(prob.b))
+    dev_ms = sum(ms_list) / len(ms_list)
+    value = total_iters / (dev_ms / 1e3)
+
+    # ---- profiled solve (per-kernel-class event times), outside the timed region
+    L.check(lib.sscg_set_profiling(plan.handle, 1))
+    dev_solve()
+    L.check(lib.sscg_set_profiling(plan.handle, 0))
+    import ctypes as C
+    pms = np.zeros(5)
+    pcnt = np.zeros(5, dtype=np.int64)
+    L.check(lib.sscg_get_profile(plan.handle, L.dptr(pms),
+                                 pcnt.ctypes.data_as(C.POINTER(C.c_int64))))
+    s_t = [int(v) for v in logs.rec_i[:total_outer, L.REC_STILDE]]
+    mu_nz = basis == "chebyshev"
+    active = total_outer + 1  # outer loops whose levels did real work
+    mpk_bytes = active * mpk_bytes_per_outer(n, nnz, sigma, mu_nz)
+    mpk_ms = float(pms[0])
+    hbm_peak, peak_kind = peaks()
+    mpk_gbs = mpk_bytes / (mpk_ms / 1e3) / 1e9
+    solve_bytes = sum(outer_bytes(n, nnz, sigma, st, mu_nz) for st in s_t) + \
+        mpk_bytes_per_outer(n, nnz, sigma, mu_nz) + 8 * (2 * sigma + 1) * n
+    solve_gbs = solve_bytes / (dev_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config, {}).get("mpk_level_bytes")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the public API (host buffers)
+    e2e_times = []
+    for i in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        xe, tr, co = adaptive_solve(prob, AdaptiveConfig(**cfg_kw), trace="fast")
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_value = tr.total_iters / (sum(e2e_times) / len(e2e_times))
+    log_bytes = int(logs.iters.nbytes + logs.rec_i.nbytes + logs.rec_d.nbytes +
+                    logs.conds.nbytes + 3 * logs.thetas.nbytes + logs.outer_true.nbytes)
+
+    # ---- CPU baseline (oracle port, bounded sample)
+    cpu = None
+    if not args.no_cpu:
+        cpu_v, t1 = cpu_sample(prob, cfg_kw, total_outer, total_iters)
+        cpu = {"value": cpu_v, "unit": "iter/s", "cores": 1, "kind": "port",
+               "sample": f"oracle/sscg_oracle.py (numpy/scipy, as the reference) on the same "
+                         f"{n}-row problem, max_outer=1 took {t1:.2f}s; full solve extrapolated "
+                         f"as (outer+1) x that = {t1 * (total_outer + 1):.1f}s for "
+                         f"{total_iters} iterations",
+               "threads_note": f"os.cpu_count()={os.cpu_count()}; scipy csr_matvec and numpy "
+                               "element-wise work are single-threaded"}
+
+    line = {
+        "metric": "cg_iterations_per_sec", "value": value, "unit": "iter/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, seeded (np.random.default_rng(0)): x*~U[-1,1], b=A x*, x0=0",
+        "config": {"workload": desc, "n": n, "nnz": nnz, "sigma": sigma, "basis": basis,
+                   "eps_star": eps, "syncs_to_tol": total_outer, "total_iters": total_iters,
+                   "converged": converged, "final_true_rel_resid": rel,
+                   "trace": "fast", "l2": "inputs larger than L2 (each vector "
+                   f"{8 * n / 1e6:.0f} MB, Y {8 * n * (2 * sigma + 1) / 1e9:.2f} GB)",
+                   "problem_gen_s": round(t_gen, 2), "parallelism": f"dp{world} (row slabs)"},
+        "hbm": {"solve_gbs": solve_gbs, "frac_of_measured": solve_gbs / hbm_peak,
+                "frac_of_8tbs": solve_gbs / 8000.0, "algorithmic_bytes_per_solve": solve_bytes},
+        "roofline": {"bound": "hbm", "kernel": "k_level (matrix powers + recurrence)",
+                     "achieved": mpk_gbs, "peak": hbm_peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": mpk_gbs / hbm_peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": mpk_bytes / max(1, active * sigma),
+                     "avg_launch_ms": mpk_ms / max(1, active * sigma),
+                     "kernel_ms": {"mpk": pms[0], "gram": pms[1], "small": pms[2],
+                                   "recovery": pms[3], "other": pms[4]},
+                     "kernel_launches": {"mpk": int(pcnt[0]), "gram": int(pcnt[1]),
+                                         "small": int(pcnt[2]), "recovery": int(pcnt[3])},
+                     "share_of_step": {"mpk": pms[0] / max(pms.sum(), 1e-9),
+                                       "gram": pms[1] / max(pms.sum(), 1e-9),
+                                       "small": pms[2] / max(pms.sum(), 1e-9),
+                                       "recovery": pms[3] / max(pms.sum(), 1e-9)}},
+        "e2e": {"value": e2e_value, "unit": "iter/s", "h2d_bytes_per_step": 16 * n,
+                "d2h_bytes_per_step": 8 * n + log_bytes,
+                "note": "adaptive_solve(problem, cfg, trace='fast'); CSR plan cached on the "
+                        "matrix like SparseMatrix._csr"},
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
+def run_reference(args, rank, world):
+    """The reference's CPU path (oracle port of its numpy/scipy arithmetic) on
+    this host, same config / metric; rank 0 only."""
+    if rank != 0:
+        return
+    from paper_1908_04081_b200 import problems
+    from oracle import sscg_oracle as O
+    key, scale, sigma, basis, eps, desc = CONFIGS[args.config]
+    prob = problems.make_problem(key, scale=args.scale or scale, world=world)
+    cfg_kw = dict(sigma=sigma, eps_star=eps, basis_kind=basis)
+    # outer / total counts of the full solve (measured on the GPU, parity-tested)
+    counts = {}
+    cpath = os.path.join(ROOT, "profiles", "counts.json")
+    if os.path.exists(cpath):
+        counts = json.load(open(cpath)).get(f"{args.config}_w{world}", {})
+    outer = counts.get("outer", 90)
+    total = counts.get("total", 1000)
+    small = problems.make_problem(key, scale=32 if key.startswith("c5") else None, world=1) \
+        if key in ("c5w", "c5", "c3", "c4") else prob
+    for _ in range(args.warmup):  # warm imports / allocator on a small instance
+        O.solve_problem(small, O.OracleConfig(max_outer=1, **cfg_kw), diagnostics=False)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.solve_problem(prob, O.OracleConfig(max_outer=1, **cfg_kw), diagnostics=False)
+        times.append(time.perf_counter() - t0)
+    t1 = sum(times) / len(times)
+    value = total / (t1 * (outer + 1))
+    line = {
+        "metric": "cg_iterations_per_sec", "value": value, "unit": "iter/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t1 * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, seeded", "impl": "reference",
+        "config": {"workload": desc, "n": prob.a.n, "nnz": prob.a.nnz},
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "port",
+                         "sample": f"each step = 1 outer loop of the oracle port on the full "
+                                   f"problem ({t1:.2f}s); iters/s = {total} iters / "
+                                   f"(({outer}+1) outer x step time), counts from "
+                                   "profiles/counts.json"},
+        "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5w", choices=sorted(CONFIGS))
+    ap.add_argument("--scale", type=int, default=None, help="override grid edge (testing)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

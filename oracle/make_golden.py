@@ -331,6 +331,109 @@ def gen_solves():
     save("hscg_spd40", alphas=np.array(co.alphas), betas=np.array(co.betas))
 
 
+# ---------------------------------------------------------------------------
+# Rounding-noise floor of the reference itself: the same solve
+# with only the Gram summation order changed.  Counts / s-sequences that move
+# under these perturbations cannot be demanded bit-exactly of any other
+# implementation; tests/test_gpu_parity.py holds the GPU to this floor.
+def _gram_chunked(y):
+    y = np.asarray(y, dtype=float)
+    g = np.zeros((y.shape[1], y.shape[1]))
+    for s0 in range(0, y.shape[0], 512):
+        c = y[s0:s0 + 512]
+        g += c.T @ c
+    il = np.tril_indices(g.shape[0], -1)
+    g[il[1], il[0]] = g[il]
+    return g
+
+
+def _gram_reversed(y):
+    y = np.ascontiguousarray(np.asarray(y, dtype=float)[::-1])
+    g = y.T @ y
+    il = np.tril_indices(g.shape[0], -1)
+    g[il[1], il[0]] = g[il]
+    return g
+
+
+def _gram_einsum(y):
+    y = np.asarray(y, dtype=float)
+    g = np.einsum("ij,ik->jk", y, y, optimize=False)
+    il = np.tril_indices(g.shape[0], -1)
+    g[il[1], il[0]] = g[il]
+    return g
+
+
+PERTURBATIONS = {"chunked512": _gram_chunked, "reversed": _gram_reversed, "einsum": _gram_einsum}
+
+
+def solve_cases():
+    from sstepcg.matio import load_problem
+    data = "/root/reference/pkg/data/matrices"
+    nos1 = load_problem(os.path.join(data, "nos1.mtx"), label="nos1")
+    bus = load_problem(os.path.join(data, "494_bus.mtx"), label="494bus")
+    cases = {
+        "solve_c1": (lambda: to_ref(problems.make_problem("c1")),
+                     dict(sigma=8, eps_star=1e-10, basis_kind="newton")),
+        "solve_c2_cheb": (lambda: to_ref(problems.make_problem("c2")),
+                          dict(sigma=10, eps_star=1e-8, basis_kind="chebyshev")),
+        "solve_c2_newton": (lambda: to_ref(problems.make_problem("c2")),
+                            dict(sigma=10, eps_star=1e-8, basis_kind="newton")),
+        "solve_c3p": (lambda: to_ref(problems.make_problem("c3", scale=24)),
+                      dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev")),
+        "solve_c5p": (lambda: to_ref(problems.make_problem("c5", scale=24)),
+                      dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
+        "solve_c4p": (lambda: to_ref(problems.make_problem("c4", scale=12)),
+                      dict(sigma=10, eps_star=1e-8, basis_kind="newton", max_outer=400)),
+        "solve_494bus_old": (lambda: bus, dict(sigma=5, eps_star=1e-6, variant="old",
+                                               basis_kind="monomial", c_strategy="unit")),
+        "solve_494bus_cheb6": (lambda: bus, dict(sigma=6, eps_star=1e-8, basis_kind="chebyshev")),
+    }
+    for kind in ("newton", "chebyshev"):
+        for strat in ("adaptive", "unit", "kappa-estimate"):
+            cases[f"solve_nos1_{kind}_{strat}"] = (
+                lambda: nos1, dict(sigma=10, eps_star=1e-6, basis_kind=kind, c_strategy=strat))
+        cases[f"solve_494bus_s15_{kind}"] = (lambda: bus, dict(sigma=15, eps_star=1e-6,
+                                                               basis_kind=kind))
+    p44 = dense_problem(spd_dense(50, 1e4, 44), "spd50")
+    for kind in ("newton", "chebyshev"):
+        cases[f"solve_spd50_{kind}"] = (lambda: p44, dict(sigma=6, eps_star=1e-10,
+                                                          basis_kind=kind))
+    p43 = dense_problem(spd_dense(40, 50.0, 43), "spd40")
+    for variant in ("old", "improved"):
+        cases[f"solve_spd40_s1_{variant}"] = (lambda: p43, dict(
+            sigma=1, eps_star=1e-10, variant=variant, basis_kind="monomial"))
+    p45 = dense_problem(spd_dense(40, 1e3, 45), "spd40fb")
+    cases["solve_spd40_fullbound"] = (lambda: p45, dict(sigma=4, eps_star=1e-8,
+                                                        basis_kind="newton",
+                                                        c_strategy="full-bound"))
+    return cases
+
+
+def gen_noise():
+    orig = ref_basis.gram
+    for name, (mk, kw) in solve_cases().items():
+        prob = mk()
+        rows, seqs, lmins, lmaxs = [], [], [], []
+        for pname, fn in PERTURBATIONS.items():
+            ref_basis.gram = fn
+            try:
+                cfg = ref_adaptive.AdaptiveConfig(**kw)
+                _, tr, _ = ref_adaptive.adaptive_solve(prob, cfg)
+            finally:
+                ref_basis.gram = orig
+            rows.append([tr.total_outer, tr.total_iters, tr.converged, tr.final_true_resid])
+            sq = np.zeros((8, 2), dtype=np.int64)
+            for i, r in enumerate(tr.outer_records[:8]):
+                sq[i] = (r.s_tilde, r.s_actual)
+            seqs.append(sq)
+            lmins.append(tr.lambda_min[-1] if tr.lambda_min else np.nan)
+            lmaxs.append(tr.lambda_max[-1] if tr.lambda_max else np.nan)
+        save("noise_" + name, counts=np.array(rows, dtype=float), seq8=np.array(seqs),
+             lmin_end=np.array(lmins), lmax_end=np.array(lmaxs),
+             names=np.array(list(PERTURBATIONS)))
+        print(f"    noise {name}: outer/total {[(int(r[0]), int(r[1])) for r in rows]}")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     print("reference:", sstepcg.__file__)

@@ -242,13 +242,14 @@ int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
 // profiling mode: launch one outer loop kernel by kernel with event pairs
 struct ProfEv {
   int cls;
+  int outer;
   cudaEvent_t a, b;
 };
 
-int launch_outer_profiled(sscg_plan* p, const Ctx& c, int sigma, int full,
+int launch_outer_profiled(sscg_plan* p, const Ctx& c, int sigma, int full, int outer,
                           std::vector<ProfEv>& evs) {
   auto rec = [&](int cls, auto&& fn) -> int {
-    ProfEv e{cls, nullptr, nullptr};
+    ProfEv e{cls, outer, nullptr, nullptr};
     CUDA_OK(cudaEventCreate(&e.a));
     CUDA_OK(cudaEventCreate(&e.b));
     CUDA_OK(cudaEventRecord(e.a, p->stream));
@@ -488,7 +489,7 @@ int sscg_run(sscg_plan* p, const sscg_config* cfg, sscg_logs* logs) {
     const int64_t m = (total - launched) < CHUNK ? (total - launched) : CHUNK;
     for (int64_t i = 0; i < m; ++i) {
       if (p->profiling) {
-        TRY(launch_outer_profiled(p, c, sigma, full, evs));
+        TRY(launch_outer_profiled(p, c, sigma, full, (int)(launched + i), evs));
       } else {
         CUDA_OK(cudaGraphLaunch(p->gexec, p->stream));
       }
@@ -513,6 +514,9 @@ int sscg_run(sscg_plan* p, const sscg_config* cfg, sscg_logs* logs) {
   p->last_ms = ms;
   p->last_launched = (int32_t)launched;
   if (p->profiling) {
+    // only outer loops that did work (0..k; later replays are no-op tails)
+    int k_done = 0;
+    CUDA_OK(cudaMemcpy(&k_done, &p->d_st->k, sizeof(int), cudaMemcpyDeviceToHost));
     for (int i = 0; i < 5; ++i) {
       p->prof_ms[i] = 0.0;
       p->prof_cnt[i] = 0;
@@ -520,8 +524,10 @@ int sscg_run(sscg_plan* p, const sscg_config* cfg, sscg_logs* logs) {
     for (auto& e : evs) {
       float t = 0.f;
       cudaEventElapsedTime(&t, e.a, e.b);
-      p->prof_ms[e.cls] += t;
-      p->prof_cnt[e.cls] += 1;
+      if (e.outer <= k_done) {
+        p->prof_ms[e.cls] += t;
+        p->prof_cnt[e.cls] += 1;
+      }
       cudaEventDestroy(e.a);
       cudaEventDestroy(e.b);
     }
