@@ -168,7 +168,7 @@ def run_ours(args, rank, world):
         for _ in range(args.steps):
             ms, ol = dev_solve()
             ms_list.append(ms)
-            launches += 2 + ol * (sigma + 3)
+            launches += 2 + ol * (2 * sigma + 2)
     L.check(lib.sscg_fetch(plan.handle, None, logs.s))
     total_iters, total_outer = int(logs.s.total_iters), int(logs.s.total_outer)
     converged = int(logs.s.status) == L.CONVERGED
@@ -190,6 +190,12 @@ def run_ours(args, rank, world):
     pcnt = np.zeros(5, dtype=np.int64)
     L.check(lib.sscg_get_profile(plan.handle, L.dptr(pms),
                                  pcnt.ctypes.data_as(C.POINTER(C.c_int64))))
+    ph = np.zeros(8, dtype=np.int64)
+    L.check(lib.sscg_get_small_phases(plan.handle, ph.ctypes.data_as(C.POINTER(C.c_int64))))
+    calls = max(1, int(ph[7]))
+    names = ["classify", "gram_extract_c", "nested_conds", "select_truncate", "inner_loop",
+             "next_params"]
+    small_phases = {nm: round(float(ph[i]) / calls / 1965.0, 2) for i, nm in enumerate(names)}
     s_t = [int(v) for v in logs.rec_i[:total_outer, L.REC_STILDE]]
     mu_nz = basis == "chebyshev"
     active = total_outer + 1  # outer loops whose levels did real work
@@ -250,6 +256,7 @@ def run_ours(args, rank, world):
                      "avg_launch_ms": mpk_ms / max(1, active * sigma),
                      "kernel_ms": {"mpk": pms[0], "gram": pms[1], "small": pms[2],
                                    "recovery": pms[3], "other": pms[4]},
+                     "small_phases_us_per_call": small_phases,
                      "kernel_launches": {"mpk": int(pcnt[0]), "gram": int(pcnt[1]),
                                          "small": int(pcnt[2]), "recovery": int(pcnt[3])},
                      "share_of_step": {"mpk": pms[0] / max(pms.sum(), 1e-9),

@@ -155,6 +155,10 @@ int sscg_fetch(sscg_plan* plan, double* x_out, sscg_logs* logs);
  * event pair per launch (no graph replay). */
 int sscg_set_profiling(sscg_plan* plan, int32_t enable);
 int sscg_get_profile(const sscg_plan* plan, double* ms5, int64_t* counts5);
+/* K_small phase timers of the last run (SM clock cycles, thread 0):
+ * [0] classify [1] Gram extract + c [2] nested conds [3] s~ + truncation
+ * [4] inner loop + record [5] next-block parameters [6] unused [7] calls */
+int sscg_get_small_phases(const sscg_plan* plan, int64_t* cycles8);
 
 /* ---- unit entry points (parity tests; one kernel family each) ------------- */
 /* lacore.py:25-34 spmv: y = A x (scipy csr_matvec rounding, bit for bit) */

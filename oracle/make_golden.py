@@ -363,7 +363,39 @@ def _gram_einsum(y):
     return g
 
 
-PERTURBATIONS = {"chunked512": _gram_chunked, "reversed": _gram_reversed, "einsum": _gram_einsum}
+def _gram_chunk(size):
+    def g(y):
+        y = np.asarray(y, dtype=float)
+        out = np.zeros((y.shape[1], y.shape[1]))
+        for s0 in range(0, y.shape[0], size):
+            c = y[s0:s0 + size]
+            out += c.T @ c
+        il = np.tril_indices(out.shape[0], -1)
+        out[il[1], il[0]] = out[il]
+        return out
+    return g
+
+
+def _conds_jacobi(g, s_bar):
+    """nested_basis_conds with the reference's own cyclic Jacobi instead of LAPACK."""
+    g = np.asarray(g, dtype=float)
+    conds = np.full(s_bar + 1, np.nan)
+    for i in range(1, s_bar + 1):
+        cols = list(range(0, i + 1)) + list(range(s_bar + 1, s_bar + 1 + i))
+        try:
+            w = ref_lacore.sym_eig(g[np.ix_(cols, cols)])
+        except ref_lacore.EigenConvergenceError:
+            w = np.linalg.eigvalsh(g[np.ix_(cols, cols)])
+        conds[i] = ref_lacore._cond_from_eigvals(w)
+    return conds
+
+
+# (Gram summation order, eigensolver) perturbations of the reference
+PERTURBATIONS = {"chunked512": (_gram_chunked, None), "reversed": (_gram_reversed, None),
+                 "einsum": (_gram_einsum, None), "chunked64": (_gram_chunk(64), None),
+                 "chunked4096": (_gram_chunk(4096), None),
+                 "chunked16": (_gram_chunk(16), None), "chunked2": (_gram_chunk(2), None),
+                 "jacobi-eig": (None, _conds_jacobi)}
 
 
 def solve_cases():
@@ -411,16 +443,22 @@ def solve_cases():
 
 def gen_noise():
     orig = ref_basis.gram
+    orig_conds = ref_lacore.nested_basis_conds
+    only = os.environ.get("NOISE_ONLY")
     for name, (mk, kw) in solve_cases().items():
+        if only and only not in name:
+            continue
         prob = mk()
         rows, seqs, lmins, lmaxs = [], [], [], []
-        for pname, fn in PERTURBATIONS.items():
-            ref_basis.gram = fn
+        for pname, (gfn, cfn) in PERTURBATIONS.items():
+            ref_basis.gram = gfn or orig
+            ref_lacore.nested_basis_conds = cfn or orig_conds
             try:
                 cfg = ref_adaptive.AdaptiveConfig(**kw)
                 _, tr, _ = ref_adaptive.adaptive_solve(prob, cfg)
             finally:
                 ref_basis.gram = orig
+                ref_lacore.nested_basis_conds = orig_conds
             rows.append([tr.total_outer, tr.total_iters, tr.converged, tr.final_true_resid])
             sq = np.zeros((8, 2), dtype=np.int64)
             for i, r in enumerate(tr.outer_records[:8]):

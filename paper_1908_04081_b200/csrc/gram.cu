@@ -20,8 +20,8 @@
 
 namespace {
 
-constexpr int GT_ROWS = 64;
-constexpr int GT_STAGES = 3;
+constexpr int GT_ROWS = 128;
+constexpr int GT_STAGES = 4;
 constexpr int GT_LD = GT_ROWS + 4;  // LD % 16 == 4: conflict-free fragment loads
 constexpr int GT_THREADS = 256;
 
@@ -41,30 +41,41 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int NB>
+// NB full 8-column blocks go through DMMA; the REM (<= 2) trailing columns are
+// accumulated on the CUDA cores (padding them to a 9th..16th column would double
+// the tensor work and make the kernel DMMA-bound instead of HBM-bound).
+template <int NB, int REM>
 __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t ld, int k,
                                           double* part, double* out, int* counter) {
   constexpr int T = NB * (NB + 1) / 2;
+  constexpr int NC = NB * 8 + REM;  // columns staged per tile
   extern __shared__ __align__(16) double gsm[];
-  double* tiles = gsm;                              // [GT_STAGES][NB*8][GT_LD]
-  double* red = gsm + GT_STAGES * NB * 8 * GT_LD;   // [T][64]
+  double* tiles = gsm;                              // [GT_STAGES][NC][GT_LD]
+  double* red = gsm + GT_STAGES * NC * GT_LD;       // [T][64] + [REM][NB*8 + REM]
+  double* redr = red + T * 64;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t ntiles = ld / GT_ROWS;
 
-  // zero the padding columns (k .. NB*8-1) of every stage once
-  for (int i = tid; i < GT_STAGES * NB * 8 * GT_LD; i += GT_THREADS) {
-    int cc = (i / GT_LD) % (NB * 8);
+  // zero the padding columns (k .. NC-1) of every stage once
+  for (int i = tid; i < GT_STAGES * NC * GT_LD; i += GT_THREADS) {
+    int cc = (i / GT_LD) % NC;
     if (cc >= k) tiles[i] = 0.0;
   }
-  double acc[T][2];
+  double acc[T > 0 ? T : 1][2];
 #pragma unroll
   for (int q = 0; q < T; ++q) acc[q][0] = acc[q][1] = 0.0;
+  double accr[REM > 0 ? REM : 1][NB + 1];  // remainder column x (block cb column g) / x rem
+#pragma unroll
+  for (int a = 0; a < (REM > 0 ? REM : 1); ++a)
+#pragma unroll
+    for (int cb = 0; cb <= NB; ++cb) accr[a][cb] = 0.0;
 
-  const int chunks = k * (GT_ROWS / 2);  // 16-byte chunks per tile
+  const int kc = k < NC ? k : NC;
+  const int chunks = kc * (GT_ROWS / 2);  // 16-byte chunks per tile
   auto issue = [&](int64_t tile, int stage) {
     if (tile < ntiles) {
-      double* dst = tiles + (size_t)stage * NB * 8 * GT_LD;
+      double* dst = tiles + (size_t)stage * NC * GT_LD;
       const double* src = Y + tile * GT_ROWS;
       for (int i = tid; i < chunks; i += GT_THREADS) {
         int cc = i / (GT_ROWS / 2), rr = (i % (GT_ROWS / 2)) * 2;
@@ -82,12 +93,12 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
     issue(tile + (int64_t)(GT_STAGES - 1) * gridDim.x, (stage + GT_STAGES - 1) % GT_STAGES);
     cp_wait<GT_STAGES - 1>();
     __syncthreads();
-    const double* ts = tiles + (size_t)stage * NB * 8 * GT_LD;
-    // 8 warps x 8 rows = 64 rows: two k-steps of 4 rows per warp
+    const double* ts = tiles + (size_t)stage * NC * GT_LD;
+    // 8 warps x 16 rows = 128 rows: four k-steps of 4 rows per warp
 #pragma unroll
     for (int ks = 0; ks < GT_ROWS / 32; ++ks) {
       const int row0 = warp * (GT_ROWS / 8) + ks * 4;
-      double fr[NB];
+      double fr[NB > 0 ? NB : 1];
 #pragma unroll
       for (int cb = 0; cb < NB; ++cb) fr[cb] = ts[(cb * 8 + g) * GT_LD + row0 + t4];
       int q = 0;
@@ -95,13 +106,38 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
       for (int i = 0; i < NB; ++i)
 #pragma unroll
         for (int j = 0; j <= i; ++j, ++q) dmma(acc[q][0], acc[q][1], fr[i], fr[j]);
+      if (REM > 0) {
+#pragma unroll
+        for (int a = 0; a < REM; ++a) {
+          const double yr = ts[(NB * 8 + a) * GT_LD + row0 + t4];  // broadcast within t4
+#pragma unroll
+          for (int cb = 0; cb < NB; ++cb) accr[a][cb] = fma(yr, fr[cb], accr[a][cb]);
+          // remainder x remainder (columns NB*8 .. NB*8+a), lanes g < REM
+          if (g <= a) {
+            const double yb = ts[(NB * 8 + g) * GT_LD + row0 + t4];
+            accr[a][NB] = fma(yr, yb, accr[a][NB]);
+          }
+        }
+      }
     }
     __syncthreads();
     stage = (stage + 1) % GT_STAGES;
   }
   cp_wait<0>();
 
-  // combine warps in fixed order: red[q][g*8 + 2 t4 + e]
+  // remainder partials: sum over the 4 row lanes (t4) of each g
+  if (REM > 0) {
+#pragma unroll
+    for (int a = 0; a < REM; ++a)
+#pragma unroll
+      for (int cb = 0; cb <= NB; ++cb) {
+        double v = accr[a][cb];
+        v += __shfl_down_sync(0xffffffffu, v, 2);
+        v += __shfl_down_sync(0xffffffffu, v, 1);
+        accr[a][cb] = v;  // valid in lanes with t4 == 0
+      }
+  }
+  // combine warps in fixed order: red[q][g*8 + 2 t4 + e], redr[a][col]
   for (int w = 0; w < GT_THREADS / 32; ++w) {
     if (warp == w) {
 #pragma unroll
@@ -115,6 +151,20 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
           d[1] += acc[q][1];
         }
       }
+      if (REM > 0 && t4 == 0) {
+#pragma unroll
+        for (int a = 0; a < REM; ++a) {
+#pragma unroll
+          for (int cb = 0; cb < NB; ++cb) {
+            double* d = redr + a * NC + cb * 8 + g;
+            *d = (w == 0) ? accr[a][cb] : *d + accr[a][cb];
+          }
+          if (g <= a) {
+            double* d = redr + a * NC + NB * 8 + g;
+            *d = (w == 0) ? accr[a][NB] : *d + accr[a][NB];
+          }
+        }
+      }
     }
     __syncthreads();
   }
@@ -125,9 +175,15 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
     while (a * (a + 1) / 2 > e) --a;
     while ((a + 1) * (a + 2) / 2 <= e) ++a;
     const int b = e - a * (a + 1) / 2;
-    const int bi = a >> 3, bj = b >> 3;
-    const int q = bi * (bi + 1) / 2 + bj;
-    part[(size_t)blockIdx.x * GPACK + e] = red[q * 64 + (a & 7) * 8 + (b & 7)];
+    double v;
+    if (a >= NB * 8) {  // remainder row a, column b <= a
+      v = redr[(a - NB * 8) * NC + b];
+    } else {
+      const int bi = a >> 3, bj = b >> 3;
+      const int q = bi * (bi + 1) / 2 + bj;
+      v = red[q * 64 + (a & 7) * 8 + (b & 7)];
+    }
+    part[(size_t)blockIdx.x * GPACK + e] = v;
   }
   // last CTA: fixed-order sum over CTAs, mirror to a full symmetric matrix
   __threadfence();
@@ -160,31 +216,32 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
   if (tid == 0) *counter = 0;
 }
 
-template <int NB>
+template <int NB, int REM>
 __global__ void __launch_bounds__(GT_THREADS) k_gram_state(Ctx c) {
   if (c.st->done) return;
-  gram_body<NB>(c.Y, c.ld, c.cfg->ncols, c.part_g, c.st->gram, &c.st->gram_count);
+  gram_body<NB, REM>(c.Y, c.ld, c.cfg->ncols, c.part_g, c.st->gram, &c.st->gram_count);
 }
 
-template <int NB>
+template <int NB, int REM>
 __global__ void __launch_bounds__(GT_THREADS)
     k_gram_raw(const double* Y, int64_t ld, int k, double* part, double* out, int* counter) {
-  gram_body<NB>(Y, ld, k, part, out, counter);
+  gram_body<NB, REM>(Y, ld, k, part, out, counter);
 }
 
-template <int NB>
+template <int NB, int REM>
 constexpr size_t gram_smem() {
-  return sizeof(double) * ((size_t)GT_STAGES * NB * 8 * GT_LD + (size_t)(NB * (NB + 1) / 2) * 64);
+  return sizeof(double) * ((size_t)GT_STAGES * (NB * 8 + REM) * GT_LD +
+                           (size_t)(NB * (NB + 1) / 2) * 64 + (size_t)REM * (NB * 8 + REM) + 8);
 }
 
-template <int NB>
+template <int NB, int REM>
 void set_attr() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(k_gram_state<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)gram_smem<NB>());
-    cudaFuncSetAttribute(k_gram_raw<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)gram_smem<NB>());
+    cudaFuncSetAttribute(k_gram_state<NB, REM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)gram_smem<NB, REM>());
+    cudaFuncSetAttribute(k_gram_raw<NB, REM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)gram_smem<NB, REM>());
     done = true;
   }
 }
@@ -199,32 +256,47 @@ int gram_grid(int64_t ld) {
 
 int gram_row_multiple() { return GT_ROWS; }
 
+// k columns -> NB DMMA blocks + REM CUDA-core columns (REM = k mod 8 when <= 2,
+// otherwise the last block is zero-padded for DMMA)
+#define GRAM_DISPATCH(K, LAUNCH)                                      \
+  do {                                                                \
+    const int nb_ = (K) / 8, r_ = (K) % 8;                            \
+    switch (r_ <= 2 ? nb_ * 10 + r_ : (nb_ + 1) * 10) {               \
+      case 1: LAUNCH(0, 1); break;                                    \
+      case 2: LAUNCH(0, 2); break;                                    \
+      case 10: LAUNCH(1, 0); break;                                   \
+      case 11: LAUNCH(1, 1); break;                                   \
+      case 12: LAUNCH(1, 2); break;                                   \
+      case 20: LAUNCH(2, 0); break;                                   \
+      case 21: LAUNCH(2, 1); break;                                   \
+      case 22: LAUNCH(2, 2); break;                                   \
+      case 30: LAUNCH(3, 0); break;                                   \
+      case 31: LAUNCH(3, 1); break;                                   \
+      case 32: LAUNCH(3, 2); break;                                   \
+      case 40: LAUNCH(4, 0); break;                                   \
+      case 41: LAUNCH(4, 1); break;                                   \
+      case 42: LAUNCH(4, 2); break;                                   \
+      case 50: LAUNCH(5, 0); break;                                   \
+      default: break;                                                 \
+    }                                                                 \
+  } while (0)
+
 void launch_gram(const Ctx& c, int ncols, cudaStream_t s) {
-  const int nb = (ncols + 7) / 8;
   const int grid = gram_grid(c.ld);
-  switch (nb) {
-#define G_CASE(N)                                                             \
-  case N:                                                                     \
-    set_attr<N>();                                                            \
-    k_gram_state<N><<<grid, GT_THREADS, gram_smem<N>(), s>>>(c);              \
-    break;
-    G_CASE(1) G_CASE(2) G_CASE(3) G_CASE(4) G_CASE(5)
-#undef G_CASE
-  }
+#define L_STATE(NB, REM)                                                          \
+  set_attr<NB, REM>();                                                            \
+  k_gram_state<NB, REM><<<grid, GT_THREADS, gram_smem<NB, REM>(), s>>>(c)
+  GRAM_DISPATCH(ncols, L_STATE);
+#undef L_STATE
 }
 
 void launch_gram_raw(const double* Y, int64_t n, int64_t ld, int k, double* part, double* out,
                      int* counter, cudaStream_t s) {
   (void)n;
-  const int nb = (k + 7) / 8;
   const int grid = gram_grid(ld);
-  switch (nb) {
-#define G_CASE(N)                                                                      \
-  case N:                                                                              \
-    set_attr<N>();                                                                     \
-    k_gram_raw<N><<<grid, GT_THREADS, gram_smem<N>(), s>>>(Y, ld, k, part, out, counter); \
-    break;
-    G_CASE(1) G_CASE(2) G_CASE(3) G_CASE(4) G_CASE(5)
-#undef G_CASE
-  }
+#define L_RAW(NB, REM)                                                            \
+  set_attr<NB, REM>();                                                            \
+  k_gram_raw<NB, REM><<<grid, GT_THREADS, gram_smem<NB, REM>(), s>>>(Y, ld, k, part, out, counter)
+  GRAM_DISPATCH(k, L_RAW);
+#undef L_RAW
 }

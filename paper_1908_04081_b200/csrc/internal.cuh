@@ -25,7 +25,9 @@
 // fixed launch geometry (B200: 148 SMs)
 #define NUM_SMS 148
 #define ROWS_PER_CTA 256
-#define RED_BLOCKS (NUM_SMS * 4)   // grid of the row-streaming kernels (partials count)
+#define RED_BLOCKS (NUM_SMS * 8)   // capacity of the per-CTA partial-sum arrays
+#define MT_ROWS 256                 // rows per staged CSR tile (= threads per CTA)
+#define MT_STAGES 2                 // TMA double buffering of CSR tiles
 #define GRAM_BLOCKS NUM_SMS
 #define SMALL_THREADS 512
 
@@ -68,6 +70,8 @@ struct SolverState {
   int diag_base;  // global iteration index of the block's first inner iteration
   int gram_count; // last-block-done counter of the Gram kernel
   int diag_n;     // inner iterations of this block needing full-trace diagnostics
+  int leja_on;    // Newton parameters of this block still need Leja points 2..sigma-1
+  int pad1;
   double best;
   double nb;      // ||b||
   ParamsDev prm;  // parameters of the block being built
@@ -75,6 +79,7 @@ struct SolverState {
   double cx[CMAX], cr[CMAX], cp[CMAX];      // recovery coefficients, physical columns
   double dx[SMAX][CMAX], dr[SMAX][CMAX];    // per-iteration coords (full trace)
   double gram[CMAX * CMAX];                 // reduced Gram of the physical block
+  long long phase_cycles[8];                // K_small phase timers (clock64, thread 0)
 };
 
 // everything a kernel may touch; passed by value
@@ -106,6 +111,8 @@ struct Ctx {
   double* rec_mu;
   double* outer_true;  // [cap_outer+1]
   double* first_gram;  // [CMAX*CMAX]
+  int red_n;        // CTAs of the row-streaming kernels = partial-sum slots in use
+  int stage_cap;    // nnz capacity of one staged CSR tile (0: unstaged kernels)
 };
 
 #define CUDA_OK(expr)                                             \
@@ -127,6 +134,9 @@ void launch_block_levels(const int* rp, const int* col, const double* val, int64
                          double* Y, int s, const double* th, const double* ga, const double* mu,
                          int* breakdown, cudaStream_t st);
 void launch_diag_resid(const Ctx& c, int j, cudaStream_t s);
+size_t staged_smem_bytes(int cap);
+void staged_prepare(int cap);
+int staged_ctas_per_sm(int cap);
 // gram.cu (ld must be a multiple of gram_row_multiple(); padding rows zero)
 int gram_row_multiple();
 void launch_gram(const Ctx& c, int ncols, cudaStream_t s);
@@ -141,6 +151,8 @@ void launch_recover_raw(const double* Y, int64_t n, int64_t ld, int k, const dou
 void launch_state_init(const Ctx& c, cudaStream_t s);
 void launch_small(const Ctx& c, cudaStream_t s);
 void launch_diag_fin(const Ctx& c, int j, cudaStream_t s);
+void launch_params_begin(const Ctx& c, cudaStream_t s);
+void launch_leja_point(const Ctx& c, int n, cudaStream_t s);
 size_t small_smem_bytes();
 int unit_nested_conds(const double* g_host, int s_bar, double* conds_host, int mode, double c,
                       double unit, double eps, double rn, int* s_tilde);

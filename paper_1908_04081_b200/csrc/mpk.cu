@@ -86,6 +86,218 @@ __device__ __forceinline__ double recur(double ay, double y, double y2, double t
 __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 
 // ---------------------------------------------------------------------------
+// TMA-staged CSR tiles.  Persistent CTAs walk MT_ROWS-row tiles; the tile's
+// contiguous col/val segment is moved global->shared by cp.async.bulk (one
+// elected thread, mbarrier completion), double-buffered, so the CSR stream is
+// in flight while the previous tile's rows are computed.  Row sums still run
+// sequentially in stored order from shared memory: bit-identical to csr_matvec.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  uint32_t spins = 0;
+  while (!done) {
+    if (++spins > (1u << 26)) __trap();  // a lost transaction must fail, not hang
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+struct TileStage {
+  const double* val;  // shared: val[beg_v ..)
+  const int* col;     // shared: col[beg_c ..)
+  int beg_v, beg_c;
+};
+
+// stage layout: [cap + 2 doubles of val][cap + 4 ints of col], 16-byte aligned
+__host__ __device__ __forceinline__ size_t stage_bytes(int cap) {
+  return ((size_t)(cap + 2) * 8 + (size_t)(cap + 4) * 4 + 15) / 16 * 16;
+}
+
+// Runs fn(row, TileStage&) over every row of every tile of this CTA.
+template <class Fn>
+__device__ __forceinline__ void staged_rows(const Ctx& c, Fn&& fn) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  __shared__ __align__(8) uint64_t bars[MT_STAGES];
+  __shared__ int tb[MT_STAGES][2];
+  const int cap = c.stage_cap;
+  const size_t sb = stage_bytes(cap);
+  const int64_t ntiles = (c.n + MT_ROWS - 1) / MT_ROWS;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < MT_STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t tile, int s) {  // thread 0 only
+    const int64_t r0 = tile * MT_ROWS;
+    const int64_t r1 = r0 + MT_ROWS < c.n ? r0 + MT_ROWS : c.n;
+    const int beg = c.rp[r0], end = c.rp[r1];
+    const int bv = beg & ~1, bc = beg & ~3;
+    const uint32_t nbv = (uint32_t)(((end - bv) * 8 + 15) / 16 * 16);
+    const uint32_t nbc = (uint32_t)(((end - bc) * 4 + 15) / 16 * 16);
+    tb[s][0] = bv;
+    tb[s][1] = bc;
+    unsigned char* base = msm + (size_t)s * sb;
+    mbar_arrive_tx(&bars[s], nbv + nbc);
+    if (nbv) bulk_g2s(base, c.val + bv, nbv, &bars[s]);
+    if (nbc) bulk_g2s(base + (size_t)(cap + 2) * 8, c.col + bc, nbc, &bars[s]);
+  };
+  int64_t k = 0;
+  if (tid == 0)
+    for (int s = 0; s < MT_STAGES; ++s) {
+      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+      if (t < ntiles) issue(t, s);
+    }
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int s = (int)(k % MT_STAGES);
+    mbar_wait(&bars[s], (uint32_t)((k / MT_STAGES) & 1));
+    TileStage ts;
+    unsigned char* base = msm + (size_t)s * sb;
+    ts.val = reinterpret_cast<const double*>(base);
+    ts.col = reinterpret_cast<const int*>(base + (size_t)(cap + 2) * 8);
+    ts.beg_v = tb[s][0];
+    ts.beg_c = tb[s][1];
+    const int64_t i = tile * MT_ROWS + tid;
+    if (i < c.n) fn(i, ts);
+    __syncthreads();  // stage s free again
+    if (tid == 0) {
+      const int64_t t = tile + (int64_t)MT_STAGES * gridDim.x;
+      if (t < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(t, s);
+      }
+    }
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ void row_dot_s(const TileStage& ts, int beg, int end,
+                                          const double* const* __restrict__ xs, double* acc) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  const double* vv = ts.val - ts.beg_v;
+  const int* cc = ts.col - ts.beg_c;
+  int jj = beg;
+  for (; jj + 2 <= end; jj += 2) {
+    const int c0 = cc[jj], c1 = cc[jj + 1];
+    const double v0 = vv[jj], v1 = vv[jj + 1];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const double x0 = __ldg(xs[q] + c0), x1 = __ldg(xs[q] + c1);
+      acc[q] = __dadd_rn(__dadd_rn(acc[q], __dmul_rn(v0, x0)), __dmul_rn(v1, x1));
+    }
+  }
+  if (jj < end) {
+    const int c0 = cc[jj];
+    const double v0 = vv[jj];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v0, __ldg(xs[q] + c0)));
+  }
+}
+
+__global__ void __launch_bounds__(MT_ROWS) k_level0_staged(Ctx c) {
+  __shared__ double sm[MT_ROWS / 32];
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[0], ga = st->prm.ga[0];
+  const bool do_r = sbar >= 2;
+  const double* P0 = c.Y;
+  double* P1 = c.Y + c.ld;
+  const double* R0 = c.Y + (int64_t)(sigma + 1) * c.ld;
+  double* R1 = c.Y + (int64_t)(sigma + 2) * c.ld;
+  double tt = 0.0, rr = 0.0;
+  int bad = 0;
+  staged_rows(c, [&](int64_t i, const TileStage& ts) {
+    const int beg = c.rp[i], end = c.rp[i + 1];
+    const double p = P0[i], r = R0[i];
+    double acc[3];
+    const double* xs[3] = {c.x, P0, R0};
+    if (do_r)
+      row_dot_s<3>(ts, beg, end, xs, acc);
+    else
+      row_dot_s<2>(ts, beg, end, xs, acc);
+    const double t = __dsub_rn(c.b[i], acc[0]);
+    tt = fma(t, t, tt);
+    rr = fma(r, r, rr);
+    const double wp = recur(acc[1], p, 0.0, th, ga, 0.0, false);
+    P1[i] = wp;
+    bad |= !finite(wp);
+    if (do_r) {
+      const double wr = recur(acc[2], r, 0.0, th, ga, 0.0, false);
+      R1[i] = wr;
+      bad |= !finite(wr);
+    }
+  });
+  tt = block_sum<MT_ROWS>(tt, sm);
+  rr = block_sum<MT_ROWS>(rr, sm);
+  if (threadIdx.x == 0) {
+    c.part_t[blockIdx.x] = tt;
+    c.part_r[blockIdx.x] = rr;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+__global__ void __launch_bounds__(MT_ROWS) k_level_staged(Ctx c, int l) {
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  if (l >= sbar) return;
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[l], ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
+  const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
+  const bool do_r = l < sbar - 1;
+  const double* Pl = c.Y + (int64_t)l * c.ld;
+  const double* Pm = Pl - c.ld;
+  double* Pn = c.Y + (int64_t)(l + 1) * c.ld;
+  const double* Rl = c.Y + (int64_t)(sigma + 1 + l) * c.ld;
+  const double* Rm = Rl - c.ld;
+  double* Rn = c.Y + (int64_t)(sigma + 2 + l) * c.ld;
+  int bad = 0;
+  staged_rows(c, [&](int64_t i, const TileStage& ts) {
+    const int beg = c.rp[i], end = c.rp[i + 1];
+    double acc[2];
+    const double* xs[2] = {Pl, Rl};
+    if (do_r)
+      row_dot_s<2>(ts, beg, end, xs, acc);
+    else
+      row_dot_s<1>(ts, beg, end, xs, acc);
+    const double wp = recur(acc[0], Pl[i], use_mu ? Pm[i] : 0.0, th, ga, mu, use_mu);
+    Pn[i] = wp;
+    bad |= !finite(wp);
+    if (do_r) {
+      const double wr = recur(acc[1], Rl[i], use_mu ? Rm[i] : 0.0, th, ga, mu, use_mu);
+      Rn[i] = wr;
+      bad |= !finite(wr);
+    }
+  });
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+// ---------------------------------------------------------------------------
 // Level 0 of an outer loop: t = b - A x (norm partial), ||r0||^2 partial,
 // P_1 and (if s_bar >= 2) R_1.
 __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0(Ctx c) {
@@ -290,14 +502,38 @@ inline int grid_rows(int64_t n) {
 
 // The row-streaming kernels always launch RED_BLOCKS CTAs (grid-stride) so the
 // partial-sum arrays have a fixed length and the reductions a fixed order.
+size_t staged_smem_bytes(int cap) { return MT_STAGES * stage_bytes(cap); }
+
+void staged_prepare(int cap) {
+  const int bytes = (int)staged_smem_bytes(cap);
+  cudaFuncSetAttribute(k_level0_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_level_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+int staged_ctas_per_sm(int cap) {
+  int a = 0, b = 0;
+  const size_t bytes = staged_smem_bytes(cap);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_level0_staged, MT_ROWS, bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_level_staged, MT_ROWS, bytes);
+  return a < b ? a : b;
+}
+
 void launch_init_residual(const Ctx& c, const double* x0, cudaStream_t s) {
-  k_init_residual<<<RED_BLOCKS, ROWS_PER_CTA, 0, s>>>(c, x0);
+  k_init_residual<<<c.red_n, ROWS_PER_CTA, 0, s>>>(c, x0);
 }
 void launch_level(const Ctx& c, int level, cudaStream_t s) {
+  if (c.stage_cap > 0) {
+    const size_t bytes = staged_smem_bytes(c.stage_cap);
+    if (level == 0)
+      k_level0_staged<<<c.red_n, MT_ROWS, bytes, s>>>(c);
+    else
+      k_level_staged<<<c.red_n, MT_ROWS, bytes, s>>>(c, level);
+    return;
+  }
   if (level == 0)
-    k_level0<<<RED_BLOCKS, ROWS_PER_CTA, 0, s>>>(c);
+    k_level0<<<c.red_n, ROWS_PER_CTA, 0, s>>>(c);
   else
-    k_level<<<RED_BLOCKS, ROWS_PER_CTA, 0, s>>>(c, level);
+    k_level<<<c.red_n, ROWS_PER_CTA, 0, s>>>(c, level);
 }
 void launch_spmv(const int* rp, const int* col, const double* val, int64_t n, const double* x,
                  double* y, cudaStream_t s) {
@@ -311,5 +547,5 @@ void launch_block_levels(const int* rp, const int* col, const double* val, int64
                                                           l >= 1 ? mu[l - 1] : 0.0, breakdown);
 }
 void launch_diag_resid(const Ctx& c, int j, cudaStream_t s) {
-  k_diag_resid<<<RED_BLOCKS, ROWS_PER_CTA, 0, s>>>(c, j);
+  k_diag_resid<<<c.red_n, ROWS_PER_CTA, 0, s>>>(c, j);
 }

@@ -78,6 +78,9 @@ struct sscg_plan {
   double* d_otrue = nullptr;
   double* d_fg = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // Leja branch of the outer-loop graph
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_leja[SMAX] = {};
   cudaGraphExec_t gexec = nullptr;
   int g_sigma = -1, g_full = -1;
   int* h_done = nullptr;  // pinned [2]
@@ -92,6 +95,8 @@ struct sscg_plan {
   double prof_ms[5] = {0, 0, 0, 0, 0};
   int64_t prof_cnt[5] = {0, 0, 0, 0, 0};
   int64_t bytes = 0;
+  int red_n = RED_BLOCKS;  // CTAs of the row-streaming kernels
+  int stage_cap = 0;       // staged CSR tile capacity (0: unstaged kernels)
 };
 
 namespace {
@@ -184,6 +189,8 @@ Ctx make_ctx(sscg_plan* p) {
   c.rec_mu = p->d_mu;
   c.outer_true = p->d_otrue;
   c.first_gram = p->d_fg;
+  c.red_n = p->red_n;
+  c.stage_cap = p->stage_cap;
   return c;
 }
 
@@ -206,7 +213,19 @@ int check_config(const sscg_config* c) {
 }
 
 void capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t s) {
-  for (int l = 0; l < sigma; ++l) launch_level(c, l, s);
+  // next-block parameters: endpoints now, Leja points 2.. on the side branch,
+  // each joined right before the matrix-powers level that consumes it
+  launch_params_begin(c, s);
+  cudaEventRecord(p->ev_fork, s);
+  cudaStreamWaitEvent(p->side, p->ev_fork, 0);
+  for (int n = 2; n < sigma; ++n) {
+    launch_leja_point(c, n, p->side);
+    cudaEventRecord(p->ev_leja[n], p->side);
+  }
+  for (int l = 0; l < sigma; ++l) {
+    if (l >= 2) cudaStreamWaitEvent(s, p->ev_leja[l], 0);
+    launch_level(c, l, s);
+  }
   launch_gram(c, 2 * sigma + 1, s);
   launch_small(c, s);
   if (full) {
@@ -258,6 +277,8 @@ int launch_outer_profiled(sscg_plan* p, const Ctx& c, int sigma, int full, int o
     evs.push_back(e);
     return SSCG_OK;
   };
+  TRY(rec(4, [&] { launch_params_begin(c, p->stream); }));
+  for (int n = 2; n < sigma; ++n) TRY(rec(4, [&] { launch_leja_point(c, n, p->stream); }));
   for (int l = 0; l < sigma; ++l) TRY(rec(0, [&] { launch_level(c, l, p->stream); }));
   TRY(rec(1, [&] { launch_gram(c, 2 * sigma + 1, p->stream); }));
   TRY(rec(2, [&] { launch_small(c, p->stream); }));
@@ -323,8 +344,9 @@ int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
     }
     if (rc) break;
     if ((rc = dalloc(p, &p->d_rp, n + 1))) break;
-    if ((rc = dalloc(p, &p->d_col, nnz))) break;
-    if ((rc = dalloc(p, &p->d_val, nnz))) break;
+    // +4 / +2 elements: the staged kernels round bulk copies up to 16 bytes
+    if ((rc = dalloc(p, &p->d_col, nnz + 4))) break;
+    if ((rc = dalloc(p, &p->d_val, nnz + 2))) break;
     cudaError_t e;
     if ((e = cudaMemcpy(p->d_rp, rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice))) {
       rc = sscg_fail_cuda(e, "upload row_ptr");
@@ -357,10 +379,16 @@ int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
       rc = sscg_fail_cuda(e, "memset state");
       break;
     }
-    if ((e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking))) {
+    if ((e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking)) ||
+        (e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking)) ||
+        (e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming))) {
       rc = sscg_fail_cuda(e, "stream");
       break;
     }
+    for (int i = 0; i < SMAX && !rc; ++i)
+      if ((e = cudaEventCreateWithFlags(&p->ev_leja[i], cudaEventDisableTiming)))
+        rc = sscg_fail_cuda(e, "event");
+    if (rc) break;
     if ((e = cudaHostAlloc((void**)&p->h_done, 2 * sizeof(int), cudaHostAllocDefault))) {
       rc = sscg_fail_cuda(e, "pinned flag");
       break;
@@ -373,6 +401,28 @@ int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
       break;
     }
     small_prepare();
+    // launch geometry of the row-streaming kernels: TMA-staged CSR tiles when a
+    // tile's segment fits shared memory (every stencil), else the direct kernels
+    int sms = NUM_SMS;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    int64_t maxt = 0;
+    for (int64_t r0 = 0; r0 < n; r0 += MT_ROWS) {
+      const int64_t r1 = r0 + MT_ROWS < n ? r0 + MT_ROWS : n;
+      maxt = std::max<int64_t>(maxt, row_ptr[r1] - row_ptr[r0]);
+    }
+    const int64_t cap = (maxt + 4 + 3) / 4 * 4;
+    const int64_t ntiles = (n + MT_ROWS - 1) / MT_ROWS;
+    if (staged_smem_bytes((int)cap) <= 200 * 1024) {
+      p->stage_cap = (int)cap;
+      staged_prepare(p->stage_cap);
+      int per_sm = staged_ctas_per_sm(p->stage_cap);
+      if (per_sm < 1) per_sm = 1;
+      p->red_n = (int)std::min<int64_t>({(int64_t)sms * per_sm, (int64_t)RED_BLOCKS, ntiles});
+    } else {
+      p->stage_cap = 0;
+      p->red_n = (int)std::min<int64_t>((int64_t)sms * 4, (n + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
+    }
+    if (p->red_n < 1) p->red_n = 1;
   } while (0);
   if (rc != SSCG_OK) {
     std::string keep = g_err;
@@ -396,9 +446,12 @@ int sscg_plan_destroy(sscg_plan* p) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_done) cudaFreeHost(p->h_done);
-  for (auto ev : {p->ev_chunk[0], p->ev_chunk[1], p->ev_start, p->ev_stop})
+  for (auto ev : {p->ev_chunk[0], p->ev_chunk[1], p->ev_start, p->ev_stop, p->ev_fork})
+    if (ev) cudaEventDestroy(ev);
+  for (auto ev : p->ev_leja)
     if (ev) cudaEventDestroy(ev);
   if (p->stream) cudaStreamDestroy(p->stream);
+  if (p->side) cudaStreamDestroy(p->side);
   delete p;
   return SSCG_OK;
 }
@@ -586,6 +639,15 @@ int sscg_solve(sscg_plan* p, const sscg_config* cfg, const double* b, const doub
   TRY(sscg_load(p, b, x0));
   TRY(sscg_run(p, cfg, logs));
   return sscg_fetch(p, x_out, logs);
+}
+
+int sscg_get_small_phases(const sscg_plan* p, int64_t* cycles8) {
+  if (!p || !cycles8) return sscg_fail(SSCG_EINVAL, "NULL argument");
+  CUDA_OK(cudaSetDevice(p->device));
+  long long h[8];
+  CUDA_OK(cudaMemcpy(h, p->d_st->phase_cycles, sizeof(h), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 8; ++i) cycles8[i] = h[i];
+  return SSCG_OK;
 }
 
 // ---- unit entry points ------------------------------------------------------

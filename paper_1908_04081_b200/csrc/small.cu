@@ -213,16 +213,190 @@ __device__ void warp_jacobi(double* A, int n, double* rot /* 4*17 */) {
   }
 }
 
-// lacore.py:103-117 on the Jacobi diagonal (lane 0 result)
-__device__ double cond_from_diag(const double* A, int n) {
-  double lmax = -INFINITY, smallest = INFINITY;
-  for (int i = 0; i < n; ++i) {
-    const double w = A[i * JLD + i];
-    lmax = (i == 0) ? w : py_max(lmax, w);
-    const double aw = fabs(w);
-    smallest = (i == 0) ? aw : py_min(smallest, aw);
+// ---------------------------------------------------------------------------
+// Nested condition estimates via the LAPACK route numpy's eigvalsh takes
+// (dsyevd, jobz='N', UPLO='L': dsytd2 Householder tridiagonalisation, then the
+// tridiagonal eigenvalues), restated warp-parallel:
+//   * tridiagonalisation: one reflector per column, lanes over rows;
+//   * only the eigenvalues the estimate needs (lacore.py:103-117: lambda_max and
+//     the smallest |lambda|, i.e. the two eigenvalues straddling 0) by Sturm-count
+//     multisection, 32 shifts per step (one per lane).
+// Cost O(n^3/32) per matrix instead of ~10 Jacobi sweeps of O(n^3).
+__device__ __forceinline__ double warp_sum_all(double v) {
+  // fixed-order tree into lane 0, then broadcast: every lane sees the same bits
+  v += __shfl_down_sync(0xffffffffu, v, 16);
+  v += __shfl_down_sync(0xffffffffu, v, 8);
+  v += __shfl_down_sync(0xffffffffu, v, 4);
+  v += __shfl_down_sync(0xffffffffu, v, 2);
+  v += __shfl_down_sync(0xffffffffu, v, 1);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+__device__ __forceinline__ double warp_max_all(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// dsytd2 (lower) on the n x n symmetric matrix A (smem, ld JLD, full storage);
+// d[n], e[n-1], v/p scratch [CMAX] in smem.  Warp-collective.
+__device__ void warp_tridiag(double* A, int n, double* d, double* e, double* v, double* p) {
+  const int lane = threadIdx.x & 31;
+  for (int i = 0; i < n - 1; ++i) {
+    const int m = n - i - 1;  // reflector length (rows i+1 .. n-1)
+    const double alpha = A[(i + 1) * JLD + i];
+    // xnorm = ||A[i+2:n, i]|| with dnrm2-style scaling
+    double amax = 0.0;
+    for (int r = i + 2 + lane; r < n; r += 32) amax = fmax(amax, fabs(A[r * JLD + i]));
+    amax = warp_max_all(amax);
+    double ss = 0.0;
+    if (amax > 0.0)
+      for (int r = i + 2 + lane; r < n; r += 32) {
+        const double t = A[r * JLD + i] / amax;
+        ss = fma(t, t, ss);
+      }
+    const double xnorm = amax > 0.0 ? amax * sqrt(warp_sum_all(ss)) : 0.0;
+    if (xnorm == 0.0) {  // H = I
+      if (lane == 0) e[i] = alpha;
+      __syncwarp();
+      continue;
+    }
+    const double beta = -copysign(hypot(alpha, xnorm), alpha);
+    const double tau = (beta - alpha) / beta;
+    const double scal = 1.0 / (alpha - beta);
+    for (int r = lane; r < m; r += 32) v[r] = (r == 0) ? 1.0 : A[(i + 1 + r) * JLD + i] * scal;
+    if (lane == 0) e[i] = beta;
+    __syncwarp();
+    // p = tau * A22 v   (A22 = A[i+1:, i+1:])
+    for (int r = lane; r < m; r += 32) {
+      const double* row = A + (i + 1 + r) * JLD + (i + 1);
+      double acc = 0.0;
+      for (int c = 0; c < m; ++c) acc = fma(row[c], v[c], acc);
+      p[r] = tau * acc;
+    }
+    __syncwarp();
+    double pv = 0.0;
+    for (int r = lane; r < m; r += 32) pv = fma(p[r], v[r], pv);
+    const double alpha2 = -0.5 * tau * warp_sum_all(pv);
+    for (int r = lane; r < m; r += 32) p[r] = fma(alpha2, v[r], p[r]);  // w
+    __syncwarp();
+    // A22 -= v w^T + w v^T (both triangles, elementwise symmetric)
+    for (int it = lane; it < m * m; it += 32) {
+      const int r = it / m, c = it % m;
+      double* a = A + (i + 1 + r) * JLD + (i + 1 + c);
+      *a = *a - (v[r] * p[c] + p[r] * v[c]);
+    }
+    __syncwarp();
   }
-  if (!(lmax > 0.0)) return INFINITY;  // `if lmax <= 0.0` (NaN -> sqrt(NaN) below anyway)
+  for (int r = lane; r < n; r += 32) d[r] = A[r * JLD + r];
+  __syncwarp();
+}
+
+// number of eigenvalues of the tridiagonal (d, e) below sigma (dstebz-style)
+__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double sig,
+                                           double pivmin) {
+  double q = d[0] - sig;
+  int cnt = q < 0.0;
+  for (int k = 1; k < n; ++k) {
+    if (fabs(q) <= pivmin) q = -pivmin;
+    q = (d[k] - sig) - e2[k - 1] / q;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// Eigenvalue j (ascending, 0-based) of (d, e) inside [lo, hi] by multisection
+// with the G lanes of one lane group (group-uniform control flow).  When the
+// bracket spans many binades and lo >= 0 (or hi <= 0) the shifts are spaced
+// geometrically, so eigenvalues near 0 are located in a few steps; the search
+// stops at 1e-13 relative width.
+template <int G>
+__device__ double group_eig_index(const double* d, const double* e2, int n, int j, double lo,
+                                  double hi, double pivmin, int gl, unsigned gmask) {
+  for (int step = 0; step < 80; ++step) {
+    const double w = hi - lo;
+    if (!(w > 1e-13 * fmax(fabs(lo), fabs(hi))) || w <= pivmin) break;
+    double sig;
+    const double fr = (double)(gl + 1) / (double)(G + 1);
+    const bool pos_geo = lo >= 0.0 && hi > 0.0 && (lo == 0.0 || hi > 16.0 * lo);
+    const bool neg_geo = hi <= 0.0 && lo < 0.0 && (hi == 0.0 || lo < 16.0 * hi);
+    if (pos_geo) {  // log-spaced between max(lo, hi 2^-160) and hi
+      const double l0 = lo > hi * 6.8e-49 ? lo : hi * 6.8e-49;
+      sig = (gl == G - 1 && lo == 0.0) ? l0 : l0 * exp2(log2(hi / l0) * fr);
+      if (lo == 0.0) sig = l0 * exp2(log2(hi / l0) * (double)gl / (double)(G - 1));
+    } else if (neg_geo) {
+      const double h0 = hi < lo * 6.8e-49 ? hi : lo * 6.8e-49;  // (both negative)
+      sig = h0 * exp2(log2(lo / h0) * (1.0 - fr));
+      if (hi == 0.0) sig = h0 * exp2(log2(lo / h0) * (double)(G - 1 - gl) / (double)(G - 1));
+    } else {
+      sig = lo + w * fr;
+    }
+    const int cnt = sturm_count(d, e2, n, sig, pivmin);
+    const unsigned ok = __ballot_sync(gmask, cnt >= j + 1) >> (__ffs(gmask) - 1);  // lambda_j < sig
+    // shifts are increasing in gl: first lane with cnt >= j+1 bounds from above
+    const double s_hi = __shfl_sync(gmask, sig, (__ffs(gmask) - 1) + (ok ? __ffs(ok) - 1 : 0));
+    const int k = ok ? __ffs(ok) - 1 : G;
+    const double s_lo = (k == 0) ? lo : __shfl_sync(gmask, sig, (__ffs(gmask) - 1) + (k - 1));
+    if (ok) hi = s_hi;
+    lo = s_lo;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// cond estimate sqrt(lmax / min|lambda|) of A (lacore.py:103-117), warp-collective;
+// A is destroyed.  scratch: >= 4 * CMAX doubles.
+__device__ double warp_cond_estimate(double* A, int n, double* scratch) {
+  const int lane = threadIdx.x & 31;
+  double* d = scratch;
+  double* e = scratch + CMAX;
+  double* v = scratch + 2 * CMAX;
+  double* p = scratch + 3 * CMAX;
+  if (n == 1) {
+    const double a = A[0];
+    return (a <= 0.0) ? INFINITY : (fabs(a) == 0.0 ? INFINITY : 1.0);
+  }
+  warp_tridiag(A, n, d, e, v, p);
+  // squared off-diagonals and Gershgorin bounds
+  double emax2 = 0.0;
+  for (int k = lane; k < n - 1; k += 32) {
+    v[k] = e[k] * e[k];
+    emax2 = fmax(emax2, v[k]);
+  }
+  emax2 = warp_max_all(emax2);
+  __syncwarp();
+  double gl_ = INFINITY, gu_ = -INFINITY;
+  for (int k = lane; k < n; k += 32) {
+    const double r = (k > 0 ? fabs(e[k - 1]) : 0.0) + (k < n - 1 ? fabs(e[k]) : 0.0);
+    gl_ = fmin(gl_, d[k] - r);
+    gu_ = fmax(gu_, d[k] + r);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    gl_ = fmin(gl_, __shfl_xor_sync(0xffffffffu, gl_, o));
+    gu_ = fmax(gu_, __shfl_xor_sync(0xffffffffu, gu_, o));
+  }
+  const double span = fmax(fabs(gl_), fabs(gu_));
+  gl_ -= 2.220446049250313e-16 * span * n + 1e-300;
+  gu_ += 2.220446049250313e-16 * span * n + 1e-300;
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax2);
+  const double* e2 = v;
+  // three searches at once, 10 lanes each: lambda_max and the eigenvalues
+  // straddling 0 (lacore.py:111-117 needs lambda_max and the smallest |lambda|)
+  const int neg = sturm_count(d, e2, n, 0.0, pivmin);  // eigenvalues < 0
+  const int grp = lane / 10, gl = lane % 10;
+  double res = NAN;
+  if (grp < 3) {
+    const unsigned gmask = 0x3FFu << (10 * grp);
+    if (grp == 0) res = group_eig_index<10>(d, e2, n, n - 1, gl_, gu_, pivmin, gl, gmask);
+    if (grp == 1 && neg < n) res = group_eig_index<10>(d, e2, n, neg, 0.0, gu_, pivmin, gl, gmask);
+    if (grp == 2 && neg > 0) res = group_eig_index<10>(d, e2, n, neg - 1, gl_, 0.0, pivmin, gl, gmask);
+  }
+  const double lmax = __shfl_sync(0xffffffffu, res, 0);
+  const double pos_small = __shfl_sync(0xffffffffu, res, 10);
+  const double neg_small = __shfl_sync(0xffffffffu, res, 20);
+  if (!(lmax > 0.0)) return INFINITY;
+  double smallest = INFINITY;
+  if (neg < n) smallest = pos_small;
+  if (neg > 0) smallest = fmin(smallest, fabs(neg_small));
   if (smallest == 0.0) return INFINITY;
   return sqrt(lmax / smallest);
 }
@@ -236,7 +410,7 @@ __device__ __forceinline__ int nested_col(int s_bar, int i, int q) {
 __device__ void cta_nested_conds(const double* G, int ldg, int s_bar, double* conds,
                                  double* jac /* NW * (CMAX*JLD + 68) */) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* A = jac + (size_t)warp * (CMAX * JLD + 68);
+  double* A = jac + (size_t)warp * (CMAX * JLD + 4 * CMAX);
   double* rot = A + CMAX * JLD;
   if (threadIdx.x == 0) conds[0] = NAN;
   for (int i = warp + 1; i <= s_bar; i += NW) {
@@ -246,8 +420,8 @@ __device__ void cta_nested_conds(const double* G, int ldg, int s_bar, double* co
       A[a * JLD + b] = G[nested_col(s_bar, i, a) * ldg + nested_col(s_bar, i, b)];
     }
     __syncwarp();
-    warp_jacobi(A, n, rot);
-    if (lane == 0) conds[i] = cond_from_diag(A, n);
+    const double cnd = warp_cond_estimate(A, n, rot);
+    if (lane == 0) conds[i] = cnd;
     __syncwarp();
   }
 }
@@ -344,120 +518,122 @@ __device__ __forceinline__ double lin_x(int i, int grid, double lo, double hi, d
   return (double)i * step + lo;
 }
 
+// One greedy Leja step (basis.py:105-126, one pass of the `while` loop): given
+// pts[0..n-1] (in L.pts) and the grid objective of pts[0..n-2] in `obj` (global
+// scratch, carried between calls), append pts[n].  CTA-wide.
+__device__ void cta_leja_point(double lo, double hi, int n, int grid, double* obj,
+                               LejaShared& L) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nt = blockDim.x;
+  const double step = (hi - lo) / (double)(grid - 1);
+  const bool zero_step = (step == 0.0);
+  // grid objective, incrementally in numpy's pairwise order (see np_sum_warp)
+  for (int i = tid; i < grid; i += nt) {
+    const double x = lin_x(i, grid, lo, hi, step, zero_step);
+    double o;
+    if (n == 2) {
+      o = 0.0;
+      o += log(fabs(x - L.pts[0]) + 1e-300);
+      o += log(fabs(x - L.pts[1]) + 1e-300);
+    } else if (n == 8) {
+      double r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = log(fabs(x - L.pts[j]) + 1e-300);
+      o = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    } else {
+      o = obj[i] + log(fabs(x - L.pts[n - 1]) + 1e-300);
+    }
+    obj[i] = o;
+  }
+  if (tid == 0) L.ncand = 0;
+  __syncthreads();
+  // interior local maxima (>= both neighbours)
+  for (int i = tid + 1; i < grid - 1; i += nt) {
+    const double v = obj[i];
+    if (v >= obj[i - 1] && v >= obj[i + 1]) {
+      const int slot = atomicAdd(&L.ncand, 1);
+      if (slot < LEJA_CAND_CAP) L.cand[slot] = i;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int nc = L.ncand < LEJA_CAND_CAP ? L.ncand : LEJA_CAND_CAP;
+    if (nc == 0) {  // np.argmax: first maximal index
+      int best = 0;
+      double bv = obj[0];
+      for (int i = 1; i < grid; ++i)
+        if (obj[i] > bv) {
+          bv = obj[i];
+          best = i;
+        }
+      L.cand[0] = best;
+      nc = 1;
+    }
+    // np.nonzero order (ascending index), then a stable ascending sort by value
+    for (int a = 1; a < nc; ++a) {
+      const int v = L.cand[a];
+      int b = a - 1;
+      while (b >= 0 && L.cand[b] > v) {
+        L.cand[b + 1] = L.cand[b];
+        --b;
+      }
+      L.cand[b + 1] = v;
+    }
+    for (int a = 1; a < nc; ++a) {
+      const int v = L.cand[a];
+      const double ov = obj[v];
+      int b = a - 1;
+      while (b >= 0 && obj[L.cand[b]] > ov) {
+        L.cand[b + 1] = L.cand[b];
+        --b;
+      }
+      L.cand[b + 1] = v;
+    }
+    const int ntop = nc < 4 ? nc : 4;
+    for (int a = 0; a < ntop; ++a) L.top[a] = L.cand[nc - ntop + a];
+    L.ntop = ntop;
+  }
+  __syncthreads();
+  if (warp < L.ntop) {
+    const int i = L.top[warp];
+    const int il = i - 1 > 0 ? i - 1 : 0;
+    const int ih = i + 1 < grid - 1 ? i + 1 : grid - 1;
+    double xr, vr;
+    golden_refine(L.pts, n, lin_x(il, grid, lo, hi, step, zero_step),
+                  lin_x(ih, grid, lo, hi, step, zero_step), &xr, &vr);
+    if ((tid & 31) == 0) {
+      L.rx[warp] = xr;
+      L.rv[warp] = vr;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double vmax = L.rv[0];
+    for (int a = 1; a < L.ntop; ++a) vmax = py_max(vmax, L.rv[a]);
+    const double thr = vmax - 1e-12 * py_max(1.0, fabs(vmax));
+    int have = 0;
+    double best = 0.0;
+    for (int a = 0; a < L.ntop; ++a) {
+      if (L.rv[a] >= thr) {
+        best = have ? py_min(best, L.rx[a]) : L.rx[a];
+        have = 1;
+      }
+    }
+    L.pts[n] = best;
+  }
+  __syncthreads();
+}
+
 // basis.py:91-127 leja_points, CTA-wide; obj is a global scratch of `grid` doubles
 __device__ void cta_leja(double lo, double hi, int count, int grid, double* out, double* obj,
                          LejaShared& L) {
-  const int tid = threadIdx.x, warp = tid >> 5;
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     L.pts[0] = hi;
     L.pts[1] = lo;
   }
   __syncthreads();
-  if (count <= 2) {
-    if (tid < count) out[tid] = L.pts[tid];
-    __syncthreads();
-    return;
-  }
-  const double step = (hi - lo) / (double)(grid - 1);
-  const bool zero_step = (step == 0.0);
-  for (int n = 2; n < count; ++n) {
-    // grid objective, incrementally in numpy's pairwise order (see np_sum_warp)
-    for (int i = tid; i < grid; i += NT) {
-      const double x = lin_x(i, grid, lo, hi, step, zero_step);
-      double o;
-      if (n == 2) {
-        o = 0.0;
-        o += log(fabs(x - L.pts[0]) + 1e-300);
-        o += log(fabs(x - L.pts[1]) + 1e-300);
-      } else if (n == 8) {
-        double r[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = log(fabs(x - L.pts[j]) + 1e-300);
-        o = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-      } else {
-        o = obj[i] + log(fabs(x - L.pts[n - 1]) + 1e-300);
-      }
-      obj[i] = o;
-    }
-    if (tid == 0) L.ncand = 0;
-    __syncthreads();
-    // interior local maxima (>= both neighbours)
-    for (int i = tid + 1; i < grid - 1; i += NT) {
-      const double v = obj[i];
-      if (v >= obj[i - 1] && v >= obj[i + 1]) {
-        const int slot = atomicAdd(&L.ncand, 1);
-        if (slot < LEJA_CAND_CAP) L.cand[slot] = i;
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int nc = L.ncand < LEJA_CAND_CAP ? L.ncand : LEJA_CAND_CAP;
-      if (nc == 0) {  // np.argmax: first maximal index
-        int best = 0;
-        double bv = obj[0];
-        for (int i = 1; i < grid; ++i)
-          if (obj[i] > bv) {
-            bv = obj[i];
-            best = i;
-          }
-        L.cand[0] = best;
-        nc = 1;
-      }
-      // np.nonzero order (ascending index), then a stable ascending sort by value
-      for (int a = 1; a < nc; ++a) {
-        const int v = L.cand[a];
-        int b = a - 1;
-        while (b >= 0 && L.cand[b] > v) {
-          L.cand[b + 1] = L.cand[b];
-          --b;
-        }
-        L.cand[b + 1] = v;
-      }
-      for (int a = 1; a < nc; ++a) {
-        const int v = L.cand[a];
-        const double ov = obj[v];
-        int b = a - 1;
-        while (b >= 0 && obj[L.cand[b]] > ov) {
-          L.cand[b + 1] = L.cand[b];
-          --b;
-        }
-        L.cand[b + 1] = v;
-      }
-      const int nt = nc < 4 ? nc : 4;
-      for (int a = 0; a < nt; ++a) L.top[a] = L.cand[nc - nt + a];
-      L.ntop = nt;
-    }
-    __syncthreads();
-    if (warp < L.ntop) {
-      const int i = L.top[warp];
-      const int il = i - 1 > 0 ? i - 1 : 0;
-      const int ih = i + 1 < grid - 1 ? i + 1 : grid - 1;
-      double xr, vr;
-      golden_refine(L.pts, n, lin_x(il, grid, lo, hi, step, zero_step),
-                    lin_x(ih, grid, lo, hi, step, zero_step), &xr, &vr);
-      if ((tid & 31) == 0) {
-        L.rx[warp] = xr;
-        L.rv[warp] = vr;
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double vmax = L.rv[0];
-      for (int a = 1; a < L.ntop; ++a) vmax = py_max(vmax, L.rv[a]);
-      const double thr = vmax - 1e-12 * py_max(1.0, fabs(vmax));
-      int have = 0;
-      double best = 0.0;
-      for (int a = 0; a < L.ntop; ++a) {
-        if (L.rv[a] >= thr) {
-          best = have ? py_min(best, L.rx[a]) : L.rx[a];
-          have = 1;
-        }
-      }
-      L.pts[n] = best;
-    }
-    __syncthreads();
-  }
-  if (tid < count) out[tid] = L.pts[tid];
+  for (int n = 2; n < count; ++n) cta_leja_point(lo, hi, n, grid, obj, L);
+  if (threadIdx.x < count) out[threadIdx.x] = L.pts[threadIdx.x];
   __syncthreads();
 }
 
@@ -550,6 +726,22 @@ __device__ __forceinline__ void warp_matvec(const double* M, int ldm, const doub
   __syncwarp();
 }
 
+// out = B v for the block-bidiagonal-plus-coupling B (basis.py:180-195): only
+// B[r][r-1], B[r][r], B[r][r+1] can be non-zero, so the dense FMA chain over the
+// row reduces to these three terms in index order (identical result).
+__device__ __forceinline__ void warp_bapply(const double* B, int ldb, const double* v, double* out,
+                                            int dim) {
+  const int lane = threadIdx.x & 31;
+  for (int r = lane; r < dim; r += 32) {
+    double acc = 0.0;
+    if (r > 0) acc = fma(B[r * ldb + r - 1], v[r - 1], acc);
+    acc = fma(B[r * ldb + r], v[r], acc);
+    if (r + 1 < dim) acc = fma(B[r * ldb + r + 1], v[r + 1], acc);
+    out[r] = acc;
+  }
+  __syncwarp();
+}
+
 __device__ double cta_sum(const double* part, int n, double* red) {
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += NT) s += part[i];
@@ -576,9 +768,20 @@ struct SmallShared {
   LejaShared L;
 };
 
-constexpr size_t JAC_BYTES = sizeof(double) * (size_t)NW * (CMAX * JLD + 68);
+constexpr size_t JAC_BYTES = sizeof(double) * (size_t)NW * (CMAX * JLD + 4 * CMAX);
 
 enum { SC_TRUE, SC_UPD, SC_CSEL, SC_RREL, SC_CBLK, SC_PHI };
+
+// K_small phase timers: 0 classify, 1 Gram extract + c_sel, 2 nested conds,
+// 3 s~ + truncation, 4 inner loop + record, 5 next parameters, 7 calls
+#define PHASE(i)                                                        \
+  do {                                                                  \
+    if (threadIdx.x == 0) {                                             \
+      const long long now__ = clock64();                                \
+      st->phase_cycles[i] += now__ - t_prev__;                          \
+      t_prev__ = now__;                                                 \
+    }                                                                   \
+  } while (0)
 enum { SI_FLAG, SI_SBAR, SI_STILDE, SI_JDONE, SI_DIV, SI_BRKJ };
 
 // ---------------------------------------------------------------------------
@@ -588,7 +791,7 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
   SmallShared& S = *reinterpret_cast<SmallShared*>(dsm);
   double* jac = dsm + (sizeof(SmallShared) + 7) / 8;
   SolverState* st = c.st;
-  const DevConfig& cf = *c.cfg;
+  const DevConfig cf = *c.cfg;  // by value: global log stores would force reloads
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (st->done) {  // nothing of this outer loop may apply
@@ -598,8 +801,10 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
     }
     return;
   }
-  const double t2 = cta_sum(c.part_t, RED_BLOCKS, S.red);
-  const double r2 = cta_sum(c.part_r, RED_BLOCKS, S.red);
+  long long t_prev__ = clock64();
+  if (tid == 0) st->phase_cycles[7] += 1;
+  const double t2 = cta_sum(c.part_t, c.red_n, S.red);
+  const double r2 = cta_sum(c.part_r, c.red_n, S.red);
 
   // ---- outer boundary: classification (adaptive.py:138-148, sstep.py:61-76)
   if (tid == 0) {
@@ -642,6 +847,7 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
     S.si[SI_SBAR] = st->s_bar;
   }
   __syncthreads();
+  PHASE(0);
   if (S.si[SI_FLAG]) return;
 
   const int sbar = S.si[SI_SBAR];
@@ -674,9 +880,11 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
   }
   __syncthreads();
 
+  PHASE(1);
   // ---- nested condition estimates and s~ (adaptive.py:89-104)
   cta_nested_conds(S.G, CMAX, sbar, S.conds, jac);
   __syncthreads();
+  PHASE(2);
   if (tid == 0) {
     const double r_rel = S.sc[SC_UPD];
     const double bound = eps / (S.sc[SC_CSEL] * u * r_rel);
@@ -711,6 +919,7 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
   }
   __syncthreads();
 
+  PHASE(3);
   // ---- coefficient-space inner loop (adaptive.py:173-246), warp 0
   if (warp == 0) {
     for (int i = lane; i < CMAX; i += 32) {
@@ -728,10 +937,10 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
     int j_done = 0, diverged = 0, brk_j = -1;
     double brk_l = NAN, brk_r = NAN;
     RitzDev rz = st->rz;
+    // num = r'^T G r' of iteration j equals rr of iteration j-1 (same operands)
+    double num = q0;
     for (int j = 0; j < s_t; ++j) {
-      warp_matvec(S.Gt, CMAX, S.rp, S.t1, dim);
-      const double num = warp_dot0(S.rp, S.t1, dim);
-      warp_matvec(S.B, CMAX, S.pp, S.t1, dim);
+      warp_bapply(S.B, CMAX, S.pp, S.t1, dim);
       warp_matvec(S.Gt, CMAX, S.t1, S.t2, dim);
       const double den = warp_dot0(S.pp, S.t2, dim);
       if (den <= 0.0 || num < 0.0 || !isfinite(den) || !isfinite(num)) {
@@ -745,7 +954,7 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
         S.xp[i] = S.xp[i] + q;
       }
       __syncwarp();
-      warp_matvec(S.B, CMAX, S.t1, S.t2, dim);
+      warp_bapply(S.B, CMAX, S.t1, S.t2, dim);
       for (int i = lane; i < dim; i += 32) S.rp[i] = S.rp[i] - S.t2[i];
       __syncwarp();
       warp_matvec(S.Gt, CMAX, S.rp, S.t1, dim);
@@ -753,6 +962,7 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
       const double beta = rr / num;
       for (int i = lane; i < dim; i += 32) S.pp[i] = S.rp[i] + beta * S.pp[i];
       __syncwarp();
+      num = rr;
       j_done = j + 1;
       if (alpha > 0.0 && beta > 0.0 && isfinite(alpha) && isfinite(beta))
         ritz_absorb(rz, alpha, beta);  // identical in every lane
@@ -873,18 +1083,13 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
     }
   }
   __syncthreads();
+  PHASE(4);
   if (S.si[SI_DIV]) return;
 
-  // ---- next block's parameters (adaptive.py:254-258) and s_bar (adaptive.py:143)
-  if (cf.variant == 1 && cf.basis_kind != SSCG_BASIS_MONOMIAL) {
-    const RitzDev& rz = st->rz;
-    if (st->total_iters > 1 && rz.count >= 2) {
-      const double lmin = ritz_lmin(rz), lmax = ritz_lmax(rz);
-      if (0.0 < lmin && lmin < lmax)
-        cta_params_for(cf.basis_kind, sigma, true, lmin, lmax, cf.leja_grid, &st->prm, c.leja_obj,
-                       S.L);
-    }
-  }
+  // ---- next block's s_bar (adaptive.py:143); its basis parameters are produced by
+  //      k_params_begin / k_leja_point at the start of the next outer loop
+  __syncthreads();
+  PHASE(5);
   if (tid == 0) {
     const int nxt = S.si[SI_JDONE] + cf.f;
     st->s_bar = nxt < sigma ? nxt : sigma;
@@ -893,14 +1098,59 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
   }
 }
 
+// Next-block basis parameters (adaptive.py:254-258 -> basis.py:166-177), run at
+// the start of outer loop k from the Ritz state K_small(k-1) left.  Newton: the
+// two Leja endpoints (theta_0 = lmax, theta_1 = lmin) are set here, every
+// further Leja point by its own k_leja_point launch on a side branch of the
+// outer-loop graph, joined just before the level that consumes it.
+__global__ void k_params_begin(Ctx c) {
+  SolverState* st = c.st;
+  const DevConfig cf = *c.cfg;  // by value: global log stores would force reloads
+  if (threadIdx.x != 0) return;
+  st->leja_on = 0;
+  if (st->done) return;
+  if (!(cf.variant == 1 && cf.basis_kind != SSCG_BASIS_MONOMIAL)) return;
+  const RitzDev& rz = st->rz;
+  if (!(st->total_iters > 1 && rz.count >= 2)) return;
+  const double lmin = ritz_lmin(rz), lmax = ritz_lmax(rz);
+  if (!(0.0 < lmin && lmin < lmax)) return;
+  const int s = cf.sigma;
+  if (cf.basis_kind == SSCG_BASIS_CHEBYSHEV) {
+    set_chebyshev(st->prm, s, lmin, lmax);
+    return;
+  }
+  ParamsDev& p = st->prm;  // Newton: Leja-ordered shifts, unit scaling, no coupling
+  p.kind = SSCG_BASIS_NEWTON;
+  p.has_from = 1;
+  p.lo = lmin;
+  p.hi = lmax;
+  for (int i = 0; i < SMAX; ++i) {
+    p.th[i] = (i < s) ? ((i == 0) ? lmax : (i == 1 ? lmin : NAN)) : NAN;
+    p.ga[i] = (i < s) ? 1.0 : NAN;
+    p.mu[i] = (i < s - 1) ? 0.0 : NAN;
+  }
+  st->leja_on = s > 2;
+}
+
+// Leja point n (2 <= n < sigma) of the next block (basis.py:105-126)
+__global__ void __launch_bounds__(NT) k_leja_point(Ctx c, int n) {
+  __shared__ LejaShared L;
+  SolverState* st = c.st;
+  if (!st->leja_on || n >= c.cfg->sigma) return;
+  if (threadIdx.x < n) L.pts[threadIdx.x] = st->prm.th[threadIdx.x];
+  __syncthreads();
+  cta_leja_point(st->prm.lo, st->prm.hi, n, c.cfg->leja_grid, c.leja_obj, L);
+  if (threadIdx.x == 0) st->prm.th[n] = L.pts[n];
+}
+
 // full trace: reduce the diag partials of inner iteration j into the log
 __global__ void __launch_bounds__(NT) k_diag_fin(Ctx c, int j) {
   __shared__ double red[NT];
   const SolverState* st = c.st;
   if (j >= st->diag_n) return;
-  const double t = cta_sum(c.part_d, RED_BLOCKS, red);
-  const double r = cta_sum(c.part_d + RED_BLOCKS, RED_BLOCKS, red);
-  const double g = cta_sum(c.part_d + 2 * RED_BLOCKS, RED_BLOCKS, red);
+  const double t = cta_sum(c.part_d, c.red_n, red);
+  const double r = cta_sum(c.part_d + RED_BLOCKS, c.red_n, red);
+  const double g = cta_sum(c.part_d + 2 * RED_BLOCKS, c.red_n, red);
   if (threadIdx.x == 0) {
     const int64_t it = st->diag_base + j;
     if (it < c.cfg->cap_iters) {
@@ -917,8 +1167,8 @@ __global__ void __launch_bounds__(NT) k_state_init(Ctx c) {
   extern __shared__ __align__(16) double dsm[];
   SmallShared& S = *reinterpret_cast<SmallShared*>(dsm);
   SolverState* st = c.st;
-  const DevConfig& cf = *c.cfg;
-  const double b2 = cta_sum(c.part_t, RED_BLOCKS, S.red);
+  const DevConfig cf = *c.cfg;  // by value: global log stores would force reloads
+  const double b2 = cta_sum(c.part_t, c.red_n, S.red);
   if (threadIdx.x == 0) {
     st->k = 0;
     st->done = 0;
@@ -936,6 +1186,8 @@ __global__ void __launch_bounds__(NT) k_state_init(Ctx c) {
     st->diag_base = 0;
     st->diag_n = 0;
     st->gram_count = 0;
+    st->leja_on = 0;
+    for (int i = 0; i < 8; ++i) st->phase_cycles[i] = 0;
     st->best = INFINITY;
     st->nb = sqrt(b2);
     ritz_init(st->rz, cf.c0);
@@ -1045,6 +1297,8 @@ void launch_state_init(const Ctx& c, cudaStream_t s) {
 }
 void launch_small(const Ctx& c, cudaStream_t s) { k_small<<<1, NT, small_smem_bytes(), s>>>(c); }
 void launch_diag_fin(const Ctx& c, int j, cudaStream_t s) { k_diag_fin<<<1, NT, 0, s>>>(c, j); }
+void launch_params_begin(const Ctx& c, cudaStream_t s) { k_params_begin<<<1, 32, 0, s>>>(c); }
+void launch_leja_point(const Ctx& c, int n, cudaStream_t s) { k_leja_point<<<1, NT, 0, s>>>(c, n); }
 
 // ---- unit entry helpers (synchronous, own allocations) ----------------------
 #define U_OK(expr)                                   \
