@@ -5,7 +5,8 @@
 //
 // Y (n x k, k = 2 s + 1 <= 33, column-major, ld a multiple of GT_ROWS with the
 // padding rows zeroed at allocation) streams through shared memory in
-// GT_ROWS-row tiles with a GT_STAGES-deep cp.async pipeline; each warp feeds
+// GT_ROWS-row tiles with a GT_STAGES-deep TMA pipeline (one 1 KB cp.async.bulk
+// per column per tile, mbarrier completion, issued by one thread); each warp feeds
 // 4-row slices of the tile to the fp64 tensor core (DMMA, mma.m8n8k4.f64): with
 // the column blocks Y_i (8 columns) the warp accumulates the lower-triangular
 // tiles G_ij += Y_i^T Y_j.  The A and B fragments of m8n8k4 have the same
@@ -25,14 +26,36 @@ constexpr int GT_STAGES = 4;
 constexpr int GT_LD = GT_ROWS + 4;  // LD % 16 == 4: conflict-free fragment loads
 constexpr int GT_THREADS = 256;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0, spins = 0;
+  while (!done) {
+    if (++spins > (1u << 26)) __trap();
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -72,27 +95,29 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
     for (int cb = 0; cb <= NB; ++cb) accr[a][cb] = 0.0;
 
   const int kc = k < NC ? k : NC;
-  const int chunks = kc * (GT_ROWS / 2);  // 16-byte chunks per tile
+  __shared__ __align__(8) uint64_t bars[GT_STAGES];
+  if (tid == 0) {
+    for (int st = 0; st < GT_STAGES; ++st) mbar_init(&bars[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // one elected thread moves a tile: kc bulk copies of GT_ROWS doubles (1 KB)
   auto issue = [&](int64_t tile, int stage) {
-    if (tile < ntiles) {
-      double* dst = tiles + (size_t)stage * NC * GT_LD;
-      const double* src = Y + tile * GT_ROWS;
-      for (int i = tid; i < chunks; i += GT_THREADS) {
-        int cc = i / (GT_ROWS / 2), rr = (i % (GT_ROWS / 2)) * 2;
-        cp_async16(dst + cc * GT_LD + rr, src + (int64_t)cc * ld + rr);
-      }
-    }
-    cp_commit();
+    double* dst = tiles + (size_t)stage * NC * GT_LD;
+    const double* src = Y + tile * GT_ROWS;
+    mbar_arrive_tx(&bars[stage], (uint32_t)(kc * GT_ROWS * sizeof(double)));
+    for (int cc = 0; cc < kc; ++cc)
+      bulk_g2s(dst + cc * GT_LD, src + (int64_t)cc * ld, GT_ROWS * sizeof(double), &bars[stage]);
   };
-
-  int64_t tile = blockIdx.x;
-#pragma unroll
-  for (int s = 0; s < GT_STAGES - 1; ++s) issue(tile + (int64_t)s * gridDim.x, s);
-  int stage = 0;
-  for (; tile < ntiles; tile += gridDim.x) {
-    issue(tile + (int64_t)(GT_STAGES - 1) * gridDim.x, (stage + GT_STAGES - 1) % GT_STAGES);
-    cp_wait<GT_STAGES - 1>();
-    __syncthreads();
+  if (tid == 0)
+    for (int st = 0; st < GT_STAGES; ++st) {
+      const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
+      if (t < ntiles) issue(t, st);
+    }
+  int64_t kk = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++kk) {
+    const int stage = (int)(kk % GT_STAGES);
+    mbar_wait(&bars[stage], (uint32_t)((kk / GT_STAGES) & 1));
     const double* ts = tiles + (size_t)stage * NC * GT_LD;
     // 8 warps x 16 rows = 128 rows: four k-steps of 4 rows per warp
 #pragma unroll
@@ -112,7 +137,7 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
           const double yr = ts[(NB * 8 + a) * GT_LD + row0 + t4];  // broadcast within t4
 #pragma unroll
           for (int cb = 0; cb < NB; ++cb) accr[a][cb] = fma(yr, fr[cb], accr[a][cb]);
-          // remainder x remainder (columns NB*8 .. NB*8+a), lanes g < REM
+          // remainder x remainder (columns NB*8 .. NB*8+a), lanes g <= a
           if (g <= a) {
             const double yb = ts[(NB * 8 + g) * GT_LD + row0 + t4];
             accr[a][NB] = fma(yr, yb, accr[a][NB]);
@@ -120,10 +145,15 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
         }
       }
     }
-    __syncthreads();
-    stage = (stage + 1) % GT_STAGES;
+    __syncthreads();  // stage free again
+    if (tid == 0) {
+      const int64_t t = tile + (int64_t)GT_STAGES * gridDim.x;
+      if (t < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(t, stage);
+      }
+    }
   }
-  cp_wait<0>();
 
   // remainder partials: sum over the 4 row lanes (t4) of each g
   if (REM > 0) {
@@ -248,7 +278,7 @@ void set_attr() {
 
 int gram_grid(int64_t ld) {
   int64_t t = ld / GT_ROWS;
-  if (t > GRAM_BLOCKS) t = GRAM_BLOCKS;
+  if (t > 2 * NUM_SMS) t = 2 * NUM_SMS;  // 2 CTAs per SM (shared-memory bound)
   return (int)(t < 1 ? 1 : t);
 }
 

@@ -28,7 +28,7 @@
 #define RED_BLOCKS (NUM_SMS * 8)   // capacity of the per-CTA partial-sum arrays
 #define MT_ROWS 256                 // rows per staged CSR tile (= threads per CTA)
 #define MT_STAGES 2                 // TMA double buffering of CSR tiles
-#define GRAM_BLOCKS NUM_SMS
+#define GRAM_BLOCKS (2 * NUM_SMS)  // capacity of the Gram partials
 #define SMALL_THREADS 512
 
 struct RitzDev {  // ritz.py:28-158

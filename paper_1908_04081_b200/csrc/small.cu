@@ -24,7 +24,7 @@ namespace {
 
 constexpr int NT = SMALL_THREADS;  // 512
 constexpr int NW = NT / 32;        // 16 warps
-constexpr int JLD = CMAX + 1;      // Jacobi work matrix leading dimension
+constexpr int JLD = CMAX;          // work matrix leading dimension (odd: conflict-free row access)
 constexpr int LEJA_CAND_CAP = 256;
 
 // Python's max(a, b) / min(a, b) semantics (first argument wins unless the
@@ -238,57 +238,70 @@ __device__ __forceinline__ double warp_max_all(double v) {
 }
 
 // dsytd2 (lower) on the n x n symmetric matrix A (smem, ld JLD, full storage);
-// d[n], e[n-1], v/p scratch [CMAX] in smem.  Warp-collective.
+// d[n], e[n-1], v/p scratch [CMAX] in smem.  Warp-collective; lane c owns
+// column c of the trailing block (A is symmetric, so column c = row c).
 __device__ void warp_tridiag(double* A, int n, double* d, double* e, double* v, double* p) {
   const int lane = threadIdx.x & 31;
   for (int i = 0; i < n - 1; ++i) {
     const int m = n - i - 1;  // reflector length (rows i+1 .. n-1)
+    double* A22 = A + (i + 1) * JLD + (i + 1);
     const double alpha = A[(i + 1) * JLD + i];
-    // xnorm = ||A[i+2:n, i]|| with dnrm2-style scaling
-    double amax = 0.0;
-    for (int r = i + 2 + lane; r < n; r += 32) amax = fmax(amax, fabs(A[r * JLD + i]));
-    amax = warp_max_all(amax);
-    double ss = 0.0;
-    if (amax > 0.0)
-      for (int r = i + 2 + lane; r < n; r += 32) {
-        const double t = A[r * JLD + i] / amax;
-        ss = fma(t, t, ss);
-      }
-    const double xnorm = amax > 0.0 ? amax * sqrt(warp_sum_all(ss)) : 0.0;
+    // xnorm = ||A[i+2:n, i]|| (dnrm2; scaled only when squares could over/underflow)
+    const double xr = (lane >= 1 && lane < m) ? A[(i + 1 + lane) * JLD + i] : 0.0;
+    const double amax = warp_max_all(fabs(xr));
+    double xnorm;
+    if (amax > 1e-140 && amax < 1e140) {
+      xnorm = sqrt(warp_sum_all(xr * xr));
+    } else if (amax > 0.0) {
+      const double inv = 1.0 / amax;
+      const double t = xr * inv;
+      xnorm = amax * sqrt(warp_sum_all(t * t));
+    } else {
+      xnorm = 0.0;
+    }
     if (xnorm == 0.0) {  // H = I
       if (lane == 0) e[i] = alpha;
-      __syncwarp();
       continue;
     }
     const double beta = -copysign(hypot(alpha, xnorm), alpha);
     const double tau = (beta - alpha) / beta;
     const double scal = 1.0 / (alpha - beta);
-    for (int r = lane; r < m; r += 32) v[r] = (r == 0) ? 1.0 : A[(i + 1 + r) * JLD + i] * scal;
+    const double vl = (lane == 0) ? 1.0 : xr * scal;  // v[lane], lane < m
+    if (lane < m) v[lane] = vl;
     if (lane == 0) e[i] = beta;
     __syncwarp();
-    // p = tau * A22 v   (A22 = A[i+1:, i+1:])
-    for (int r = lane; r < m; r += 32) {
-      const double* row = A + (i + 1 + r) * JLD + (i + 1);
-      double acc = 0.0;
-      for (int c = 0; c < m; ++c) acc = fma(row[c], v[c], acc);
-      p[r] = tau * acc;
+    // p = tau * A22 v  (lane c: column c of the symmetric A22)
+    double acc = 0.0;
+    if (lane < m) {
+#pragma unroll 4
+      for (int r = 0; r < m; ++r) acc = fma(A22[r * JLD + lane], v[r], acc);
     }
+    const double pl = tau * acc;
+    const double alpha2 = -0.5 * tau * warp_sum_all(lane < m ? pl * vl : 0.0);
+    const double wl = fma(alpha2, vl, pl);  // w[lane]
+    if (lane < m) p[lane] = wl;
     __syncwarp();
-    double pv = 0.0;
-    for (int r = lane; r < m; r += 32) pv = fma(p[r], v[r], pv);
-    const double alpha2 = -0.5 * tau * warp_sum_all(pv);
-    for (int r = lane; r < m; r += 32) p[r] = fma(alpha2, v[r], p[r]);  // w
-    __syncwarp();
-    // A22 -= v w^T + w v^T (both triangles, elementwise symmetric)
-    for (int it = lane; it < m * m; it += 32) {
-      const int r = it / m, c = it % m;
-      double* a = A + (i + 1 + r) * JLD + (i + 1 + c);
-      *a = *a - (v[r] * p[c] + p[r] * v[c]);
+    // A22 -= v w^T + w v^T (column `lane`, rows 0..m-1; elementwise symmetric)
+    if (lane < m) {
+#pragma unroll 4
+      for (int r = 0; r < m; ++r) {
+        double* a = A22 + r * JLD + lane;
+        *a = *a - (v[r] * wl + p[r] * vl);
+      }
     }
     __syncwarp();
   }
   for (int r = lane; r < n; r += 32) d[r] = A[r * JLD + r];
   __syncwarp();
+}
+
+// fast fp64 reciprocal: MUFU approximation + one Newton step (~1 ulp); enough for
+// Sturm sign counts (they only decide which side of a shift an eigenvalue is)
+__device__ __forceinline__ double rcp_fast(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  const double err = fma(-q, r, 1.0);
+  return fma(r, err, r);
 }
 
 // number of eigenvalues of the tridiagonal (d, e) below sigma (dstebz-style)
@@ -298,7 +311,7 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
   int cnt = q < 0.0;
   for (int k = 1; k < n; ++k) {
     if (fabs(q) <= pivmin) q = -pivmin;
-    q = (d[k] - sig) - e2[k - 1] / q;
+    q = (d[k] - sig) - e2[k - 1] * rcp_fast(q);
     cnt += q < 0.0;
   }
   return cnt;
@@ -720,6 +733,7 @@ __device__ __forceinline__ void warp_matvec(const double* M, int ldm, const doub
   const int lane = threadIdx.x & 31;
   for (int i = lane; i < dim; i += 32) {
     double s = 0.0;
+#pragma unroll 4
     for (int j = 0; j < dim; ++j) s = fma(M[i * ldm + j], v[j], s);
     out[i] = s;
   }
