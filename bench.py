@@ -134,14 +134,149 @@ def cpu_sample(prob, cfg_kw, outer_count, total_iters):
     return total_iters / est, t1
 
 
+def run_partitioned(args, rank, world):
+    """One rank of the row-partitioned solve (torchrun, one process per GPU):
+    gloo carries the setup plumbing (ghost requests, the NCCL id, the final
+    max-over-ranks time), NCCL carries the per-outer-loop halo exchange and the
+    one Gram allreduce inside the CUDA graph."""
+    import ctypes as C
+    import types
+
+    import scipy.sparse as sp
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_04081_b200 import AdaptiveConfig, _lib as L
+    from paper_1908_04081_b200.adaptive import LogBuffers
+    from paper_1908_04081_b200.dist import solve_partitioned
+    from paper_1908_04081_b200.partition import Stencil7Rows
+
+    key, scale, sigma, basis, eps, desc = CONFIGS[args.config]
+    if key != "c5w":
+        raise SystemExit("the partitioned bench runs the weak-scaled c5 slabs (--config c5w)")
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    edge = args.scale or 256
+    nx = ny = edge
+    nz = edge * world
+    rows = Stencil7Rows(nx, ny, nz)
+    n = rows.n
+    t0 = time.perf_counter()
+    xs = np.random.default_rng(0).uniform(-1.0, 1.0, n)  # same x* as problems.poisson3d
+    from paper_1908_04081_b200.partition import slab_bounds
+    bnd = slab_bounds(n, world)
+    lo, hi = int(bnd[rank]), int(bnd[rank + 1])
+    ip, cols, vals = rows.rows(np.arange(lo, hi))
+    b_own = sp.csr_matrix((vals, cols, ip), shape=(hi - lo, n)) @ xs
+    b_glob = np.zeros(n)
+    b_glob[lo:hi] = b_own
+    nb2 = torch.tensor([float(b_own @ b_own)], dtype=torch.float64)
+    dist.all_reduce(nb2)
+    lam = [2.0 - 2.0 * math.cos(math.pi / (m + 1)) for m in (nx, ny, nz)]
+    lmax = sum(2.0 + 2.0 * math.cos(math.pi / (m + 1)) for m in (nx, ny, nz)) - 0.0
+    scal = types.SimpleNamespace(a=types.SimpleNamespace(n_a=7), norm_a=lmax, norm_abs_a=lmax,
+                                 kappa_a=lmax / sum(lam))
+    cfg = AdaptiveConfig(sigma=sigma, eps_star=eps, basis_kind=basis)
+
+    def exchange(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    def bcast(b):
+        obj = [b]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    info = {}
+    xo, tr, co, plan = solve_partitioned(rows, scal, b_glob, np.zeros(n), cfg, rank, world, local,
+                                         exchange, bcast, info=info)
+    t_setup = time.perf_counter() - t0
+    lib = L.load()
+    logs, ccfg = info["logs"], info["ccfg"]
+
+    def dev_solve():
+        L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
+        return logs.s.device_ms, int(logs.s.outer_launched)
+
+    for _ in range(args.warmup):
+        dev_solve()
+    dist.barrier()
+    ms_list, launches = [], 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            dist.barrier()
+            ms, ol = dev_solve()
+            ms_list.append(ms)
+            launches += 3 + ol * (2 * sigma + 4)  # init 3; halo pack/unpack, params, Leja, levels, ...
+    dev_ms = sum(ms_list) / len(ms_list)
+    tmax = torch.tensor([dev_ms], dtype=torch.float64)
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    # end to end through the C ABI with host buffers: H2D of b and x0, D2H of x
+    # and the logs inside the timed region, max over ranks
+    b_loc, x0_loc = info["b"], info["x0"]
+    x_host = np.empty(hi - lo)
+    e2e = []
+    for _ in range(max(1, min(args.steps, 3))):
+        dist.barrier()
+        t1 = time.perf_counter()
+        L.check(lib.sscg_solve(plan.handle, ccfg, L.dptr(b_loc), L.dptr(x0_loc), L.dptr(x_host),
+                               logs.s))
+        e2e.append(time.perf_counter() - t1)
+    te = torch.tensor([sum(e2e) / len(e2e)], dtype=torch.float64)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    L.check(lib.sscg_fetch(plan.handle, None, logs.s))
+    total_iters, total_outer = int(logs.s.total_iters), int(logs.s.total_outer)
+    # global true residual from the owned pieces (independent host SpMV)
+    x_glob = torch.zeros(n, dtype=torch.float64)
+    x_glob[lo:hi] = torch.from_numpy(xo)
+    dist.all_reduce(x_glob)
+    resid = sp.csr_matrix((vals, cols, ip), shape=(hi - lo, n)) @ x_glob.numpy() - b_own
+    rr = torch.tensor([float(resid @ resid)], dtype=torch.float64)
+    dist.all_reduce(rr)
+    rel = math.sqrt(rr.item() / nb2.item())
+    ms = tmax.item()
+    value = world * total_iters / (ms / 1e3)
+    if rank == 0:
+        n_own = hi - lo
+        line = {
+            "metric": "cg_iterations_per_sec", "value": value, "unit": "iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic, seeded (np.random.default_rng(0)): x*~U[-1,1], b=A x*, x0=0",
+            "config": {"workload": desc + f" (global {nx}x{ny}x{nz})", "n": n, "n_per_gpu": n_own,
+                       "sigma": sigma, "basis": basis, "eps_star": eps,
+                       "syncs_to_tol": total_outer, "total_iters": total_iters,
+                       "converged": int(logs.s.status) == L.CONVERGED,
+                       "final_true_rel_resid": rel, "trace": "fast",
+                       "parallelism": f"dp{world} (row slabs, ghost depth {sigma}, one NCCL "
+                                      "halo exchange + one NCCL allreduce per outer loop)",
+                       "value_definition": "per-slab CG iterations/s summed over ranks = "
+                                           "world x total_iters / max-over-ranks device time",
+                       "global_iters_per_sec": total_iters / (ms / 1e3),
+                       "setup_s": round(t_setup, 2),
+                       "allreduce_per_outer": 1, "halo_exchanges_per_outer": 1},
+            "e2e": {"value": world * total_iters / te.item(), "unit": "iter/s",
+                    "h2d_bytes_per_step": int(8 * (len(b_loc) + len(x0_loc))),
+                    "d2h_bytes_per_step": int(8 * (hi - lo) + logs.iters.nbytes),
+                    "note": "sscg_solve per rank (host b, x0 -> x, logs), max over ranks"},
+            "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    dist.barrier()
+
+
 def run_ours(args, rank, world):
     from paper_1908_04081_b200 import AdaptiveConfig, _lib as L, adaptive_solve, problems
     from paper_1908_04081_b200.adaptive import LogBuffers, make_config
     from paper_1908_04081_b200.kernels import _plan
 
     key, scale, sigma, basis, eps, desc = CONFIGS[args.config]
-    if world > 1:
-        raise SystemExit("multi-GPU partitioned bench: run with --gpus 1 (see DESIGN.md 8(e))")
+    if world > 1 or args.partitioned:
+        return run_partitioned(args, rank, world)
     t0 = time.perf_counter()
     prob = problems.make_problem(key, scale=args.scale or scale, world=world)
     t_gen = time.perf_counter() - t0
@@ -328,6 +463,8 @@ def main():
     ap.add_argument("--scale", type=int, default=None, help="override grid edge (testing)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="use the row-partitioned NCCL path even at one GPU")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

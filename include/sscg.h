@@ -140,12 +140,52 @@ int sscg_plan_destroy(sscg_plan* plan);
 /* bytes of device memory the plan holds (matrix + work space) */
 int sscg_plan_device_bytes(const sscg_plan* plan, int64_t* bytes);
 
+/* ---- row-partitioned plans (one process per GPU) ----------
+ * Local rows are ordered [owned | ghost depth 1 | ... | ghost depth `depth`]
+ * (each group in global order), so the rows whose recurrence a matrix-powers
+ * level must (redundantly) compute are a prefix: lvl_rows[d] = number of local
+ * rows with depth <= d (lvl_rows[0] = n_own, lvl_rows[depth-1] = n_rows,
+ * lvl_rows[depth] = n_local).  Rows of depth < depth carry CSR rows (local
+ * column indices).  Halo: for peer q (rank peer_rank[q]) the owned local rows
+ * send_idx[send_off[q] .. send_off[q+1]) go out and the ghost local rows
+ * recv_idx[recv_off[q] .. recv_off[q+1]) come in, both in global row order.
+ * Per outer loop: one grouped ncclSend/ncclRecv of p, r, x ghosts and one
+ * ncclAllReduce of the packed Gram + residual norms.  nccl_id == NULL builds a
+ * member of a single-process virtual group (sscg_vgroup_run) instead. */
+typedef struct sscg_part {
+  int64_t n_own, n_rows, n_local, nnz;
+  int32_t depth;       /* ghost depth provided: solves need sigma <= depth */
+  int32_t rank, world;
+  int32_t n_peers;
+  const int64_t* row_ptr;   /* [n_rows + 1] */
+  const int32_t* col_idx;   /* [nnz], local column indices < n_local */
+  const double* values;     /* [nnz] */
+  const int64_t* lvl_rows;  /* [depth + 1] */
+  const int32_t* peer_rank; /* [n_peers] */
+  const int64_t* send_off;  /* [n_peers + 1] */
+  const int64_t* recv_off;  /* [n_peers + 1] */
+  const int32_t* send_idx;  /* [send_off[n_peers]] */
+  const int32_t* recv_idx;  /* [recv_off[n_peers]] */
+  const unsigned char* nccl_id; /* 128-byte ncclUniqueId shared by the world, or NULL */
+  const char* nccl_lib;     /* path of libnccl.so.2 (NULL: default search) */
+} sscg_part;
+
+int sscg_nccl_unique_id(const char* nccl_lib, unsigned char* id128);
+int sscg_plan_create_part(sscg_plan** out, int32_t device, const sscg_part* part);
+/* Run a row-partitioned solve of `nplans` plans that all live in this process
+ * (on one or more devices) in lock step, exchanging halos with device copies
+ * and reducing in fixed order: the multi-rank algorithm without NCCL, for
+ * testing it on one GPU.  b[i]: owned rows of plan i; x0[i]: its local rows. */
+int sscg_vgroup_run(sscg_plan* const* plans, int32_t nplans, const sscg_config* cfg,
+                    const double* const* b, const double* const* x0, sscg_logs* logs0);
+
 /* ---- the solve: adaptive.py:111-268 ---------------------------------------
  * sscg_solve = sscg_load + sscg_run + sscg_fetch (host in, host out). */
 int sscg_solve(sscg_plan* plan, const sscg_config* cfg, const double* b, const double* x0,
                double* x_out, sscg_logs* logs);
 /* split form: upload b/x0, run entirely on device (inputs resident in HBM;
- * logs->device_ms = CUDA-event time of the run), download x and the logs. */
+ * logs->device_ms = CUDA-event time of the run), download x and the logs.
+ * Partitioned plans: b and x_out cover the owned rows, x0 every local row. */
 int sscg_load(sscg_plan* plan, const double* b, const double* x0);
 int sscg_run(sscg_plan* plan, const sscg_config* cfg, sscg_logs* logs);
 int sscg_fetch(sscg_plan* plan, double* x_out, sscg_logs* logs);

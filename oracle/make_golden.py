@@ -390,12 +390,31 @@ def _conds_jacobi(g, s_bar):
     return conds
 
 
-# (Gram summation order, eigensolver) perturbations of the reference
+class _NoisyLogNumpy:
+    """numpy shim for basis.py whose log() is off by up to 1 ulp (seeded): the
+    Leja objective's golden-section maximum is then located differently at the
+    ~sqrt(u) level, as with any other libm (CUDA's log vs numpy's SIMD log)."""
+
+    def __init__(self, seed):
+        self._rng = np.random.default_rng(seed)
+
+    def __getattr__(self, k):
+        return getattr(np, k)
+
+    def log(self, x):
+        y = np.log(x)
+        k = self._rng.integers(-1, 2, size=np.shape(y))
+        return np.where(k == 0, y, np.where(k > 0, np.nextafter(y, np.inf),
+                                            np.nextafter(y, -np.inf)))
+
+
+# (Gram summation order, eigensolver, libm) perturbations of the reference
 PERTURBATIONS = {"chunked512": (_gram_chunked, None), "reversed": (_gram_reversed, None),
                  "einsum": (_gram_einsum, None), "chunked64": (_gram_chunk(64), None),
                  "chunked4096": (_gram_chunk(4096), None),
                  "chunked16": (_gram_chunk(16), None), "chunked2": (_gram_chunk(2), None),
-                 "jacobi-eig": (None, _conds_jacobi)}
+                 "jacobi-eig": (None, _conds_jacobi),
+                 "leja-log-ulp-1": (None, None, 1), "leja-log-ulp-2": (None, None, 2)}
 
 
 def solve_cases():
@@ -450,15 +469,19 @@ def gen_noise():
             continue
         prob = mk()
         rows, seqs, lmins, lmaxs = [], [], [], []
-        for pname, (gfn, cfn) in PERTURBATIONS.items():
+        for pname, spec in PERTURBATIONS.items():
+            gfn, cfn = spec[0], spec[1]
             ref_basis.gram = gfn or orig
             ref_lacore.nested_basis_conds = cfn or orig_conds
+            if len(spec) > 2:
+                ref_basis.np = _NoisyLogNumpy(spec[2])
             try:
                 cfg = ref_adaptive.AdaptiveConfig(**kw)
                 _, tr, _ = ref_adaptive.adaptive_solve(prob, cfg)
             finally:
                 ref_basis.gram = orig
                 ref_lacore.nested_basis_conds = orig_conds
+                ref_basis.np = np
             rows.append([tr.total_outer, tr.total_iters, tr.converged, tr.final_true_resid])
             sq = np.zeros((8, 2), dtype=np.int64)
             for i, r in enumerate(tr.outer_records[:8]):

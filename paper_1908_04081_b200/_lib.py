@@ -38,6 +38,7 @@ EXPORTS = (
     "sscg_spmv", "sscg_build_block",
     "sscg_gram", "sscg_recover", "sscg_nested_conds", "sscg_select_s_tilde",
     "sscg_leja_points", "sscg_params_for", "sscg_ritz_sequence", "sscg_sym_eig",
+    "sscg_nccl_unique_id", "sscg_plan_create_part", "sscg_vgroup_run",
 )
 
 
@@ -65,6 +66,18 @@ class SscgLogs(C.Structure):
         ("status", C.c_int32), ("total_iters", C.c_int32), ("total_outer", C.c_int32),
         ("n_records", C.c_int32), ("outer_launched", C.c_int32), ("reserved", C.c_int32),
         ("device_ms", C.c_double),
+    ]
+
+
+class SscgPart(C.Structure):
+    _fields_ = [
+        ("n_own", C.c_int64), ("n_rows", C.c_int64), ("n_local", C.c_int64), ("nnz", C.c_int64),
+        ("depth", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("n_peers", C.c_int32),
+        ("row_ptr", C.POINTER(C.c_int64)), ("col_idx", C.POINTER(C.c_int32)),
+        ("values", C.POINTER(C.c_double)), ("lvl_rows", C.POINTER(C.c_int64)),
+        ("peer_rank", C.POINTER(C.c_int32)), ("send_off", C.POINTER(C.c_int64)),
+        ("recv_off", C.POINTER(C.c_int64)), ("send_idx", C.POINTER(C.c_int32)),
+        ("recv_idx", C.POINTER(C.c_int32)), ("nccl_id", C.c_void_p), ("nccl_lib", C.c_char_p),
     ]
 
 
@@ -105,6 +118,10 @@ def _declare(lib):
         "sscg_params_for": (C.c_int, [i32, i32, i32, i32, dbl, dbl, i32, _DP, _DP, _DP, _IP]),
         "sscg_ritz_sequence": (C.c_int, [i32, i32, _DP, _DP, _DP]),
         "sscg_sym_eig": (C.c_int, [i32, i32, _DP, _DP]),
+        "sscg_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_void_p]),
+        "sscg_plan_create_part": (C.c_int, [C.POINTER(vp), i32, C.POINTER(SscgPart)]),
+        "sscg_vgroup_run": (C.c_int, [C.POINTER(vp), i32, C.POINTER(SscgConfig),
+                                      C.POINTER(_DP), C.POINTER(_DP), C.POINTER(SscgLogs)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -23,7 +23,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libsscg.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["mpk.cu", "gram.cu", "rec.cu", "small.cu", "plan.cu"]
+SOURCES = ["mpk.cu", "gram.cu", "rec.cu", "small.cu", "dist.cu", "plan.cu"]
 NO_FMAD = {"small.cu"}
 
 
@@ -32,6 +32,32 @@ def nvcc():
         if cand and os.path.exists(cand):
             return cand
     raise RuntimeError("nvcc not found: the CUDA library cannot be built")
+
+
+def nccl_include():
+    """nccl.h for the (dlopen'ed) NCCL types: the torch-bundled one, else the system one."""
+    try:
+        import nvidia.nccl  # noqa: F401
+        for base in nvidia.nccl.__path__:
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    return "/usr/include"
+
+
+def nccl_library():
+    """libnccl.so.2 to dlopen at run time (same copy torch.distributed uses)."""
+    try:
+        import nvidia.nccl  # noqa: F401
+        for base in nvidia.nccl.__path__:
+            lib = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(lib):
+                return lib
+    except Exception:
+        pass
+    return "libnccl.so.2"
 
 
 def _digest():
@@ -57,7 +83,7 @@ def build(force=False, verbose=False):
     cc = nvcc()
     objs = []
     base = [cc, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE,
-            "--expt-relaxed-constexpr"] + ARCH
+            "-I", nccl_include(), "--expt-relaxed-constexpr"] + ARCH
     for src in SOURCES:
         obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
         cmd = base + (["-fmad=false"] if src in NO_FMAD else []) + [
@@ -67,7 +93,8 @@ def build(force=False, verbose=False):
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [cc, "-shared", "-o", tmp] + objs + ARCH + ["-cudart", "static"]
+    cmd = [cc, "-shared", "-o", tmp] + objs + ARCH + ["-cudart", "static", "-ldl",
+                                                       "-Xlinker", "--no-undefined"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

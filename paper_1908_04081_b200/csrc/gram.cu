@@ -67,9 +67,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // NB full 8-column blocks go through DMMA; the REM (<= 2) trailing columns are
 // accumulated on the CUDA cores (padding them to a 9th..16th column would double
 // the tensor work and make the kernel DMMA-bound instead of HBM-bound).
-template <int NB, int REM>
-__device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t ld, int k,
-                                          double* part, double* out, int* counter) {
+// PACKED=false: `out` = full symmetric k x k matrix (unit entry point).
+// PACKED=true:  `out` = [packed lower triangle | sum(norm_t) | sum(norm_r)], the
+//               one buffer an outer loop allreduces (norm_* = level-0 partials).
+template <int NB, int REM, bool PACKED>
+__device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t ld, int64_t nrows,
+                                          int k, double* part, double* out, int* counter,
+                                          const double* norm_t, const double* norm_r, int n_norm) {
   constexpr int T = NB * (NB + 1) / 2;
   constexpr int NC = NB * 8 + REM;  // columns staged per tile
   extern __shared__ __align__(16) double gsm[];
@@ -78,7 +82,7 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
   double* redr = red + T * 64;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int64_t ntiles = ld / GT_ROWS;
+  const int64_t ntiles = (nrows + GT_ROWS - 1) / GT_ROWS;  // rows >= nrows read as 0
 
   // zero the padding columns (k .. NC-1) of every stage once
   for (int i = tid; i < GT_STAGES * NC * GT_LD; i += GT_THREADS) {
@@ -119,13 +123,15 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
     const int stage = (int)(kk % GT_STAGES);
     mbar_wait(&bars[stage], (uint32_t)((kk / GT_STAGES) & 1));
     const double* ts = tiles + (size_t)stage * NC * GT_LD;
+    const int64_t valid = nrows - tile * GT_ROWS;  // rows of this tile below nrows
     // 8 warps x 16 rows = 128 rows: four k-steps of 4 rows per warp
 #pragma unroll
     for (int ks = 0; ks < GT_ROWS / 32; ++ks) {
       const int row0 = warp * (GT_ROWS / 8) + ks * 4;
+      const bool live = row0 + t4 < valid;
       double fr[NB > 0 ? NB : 1];
 #pragma unroll
-      for (int cb = 0; cb < NB; ++cb) fr[cb] = ts[(cb * 8 + g) * GT_LD + row0 + t4];
+      for (int cb = 0; cb < NB; ++cb) fr[cb] = live ? ts[(cb * 8 + g) * GT_LD + row0 + t4] : 0.0;
       int q = 0;
 #pragma unroll
       for (int i = 0; i < NB; ++i)
@@ -134,12 +140,12 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
       if (REM > 0) {
 #pragma unroll
         for (int a = 0; a < REM; ++a) {
-          const double yr = ts[(NB * 8 + a) * GT_LD + row0 + t4];  // broadcast within t4
+          const double yr = live ? ts[(NB * 8 + a) * GT_LD + row0 + t4] : 0.0;
 #pragma unroll
           for (int cb = 0; cb < NB; ++cb) accr[a][cb] = fma(yr, fr[cb], accr[a][cb]);
           // remainder x remainder (columns NB*8 .. NB*8+a), lanes g <= a
           if (g <= a) {
-            const double yb = ts[(NB * 8 + g) * GT_LD + row0 + t4];
+            const double yb = live ? ts[(NB * 8 + g) * GT_LD + row0 + t4] : 0.0;
             accr[a][NB] = fma(yr, yb, accr[a][NB]);
           }
         }
@@ -236,12 +242,32 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
     }
     for (; cta < nb; ++cta) s0 += pp[(size_t)cta * GPACK];
     const double v = (s0 + s1) + (s2 + s3);
-    int a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-    while (a * (a + 1) / 2 > e) --a;
-    while ((a + 1) * (a + 2) / 2 <= e) ++a;
-    const int b = e - a * (a + 1) / 2;
-    out[a * k + b] = v;
-    out[b * k + a] = v;
+    if (PACKED) {
+      out[e] = v;
+    } else {
+      int a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while (a * (a + 1) / 2 > e) --a;
+      while ((a + 1) * (a + 2) / 2 <= e) ++a;
+      const int b = e - a * (a + 1) / 2;
+      out[a * k + b] = v;
+      out[b * k + a] = v;
+    }
+  }
+  if (PACKED && warp == 0) {  // level-0 residual norms, fixed-order tree
+    double st = 0.0, sr = 0.0;
+    for (int i = lane; i < n_norm; i += 32) {
+      st += norm_t[i];
+      sr += norm_r[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      st += __shfl_down_sync(0xffffffffu, st, o);
+      sr += __shfl_down_sync(0xffffffffu, sr, o);
+    }
+    if (lane == 0) {
+      out[npack] = st;
+      out[npack + 1] = sr;
+    }
   }
   if (tid == 0) *counter = 0;
 }
@@ -249,13 +275,15 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
 template <int NB, int REM>
 __global__ void __launch_bounds__(GT_THREADS) k_gram_state(Ctx c) {
   if (c.st->done) return;
-  gram_body<NB, REM>(c.Y, c.ld, c.cfg->ncols, c.part_g, c.st->gram, &c.st->gram_count);
+  gram_body<NB, REM, true>(c.Y, c.ld, c.n_own, c.cfg->ncols, c.part_g, c.red_buf,
+                           &c.st->gram_count, c.part_t, c.part_r, c.red_n);
 }
 
 template <int NB, int REM>
 __global__ void __launch_bounds__(GT_THREADS)
-    k_gram_raw(const double* Y, int64_t ld, int k, double* part, double* out, int* counter) {
-  gram_body<NB, REM>(Y, ld, k, part, out, counter);
+    k_gram_raw(const double* Y, int64_t ld, int64_t n, int k, double* part, double* out,
+               int* counter) {
+  gram_body<NB, REM, false>(Y, ld, n, k, part, out, counter, nullptr, nullptr, 0);
 }
 
 template <int NB, int REM>
@@ -276,8 +304,8 @@ void set_attr() {
   }
 }
 
-int gram_grid(int64_t ld) {
-  int64_t t = ld / GT_ROWS;
+int gram_grid(int64_t rows) {
+  int64_t t = (rows + GT_ROWS - 1) / GT_ROWS;
   if (t > 2 * NUM_SMS) t = 2 * NUM_SMS;  // 2 CTAs per SM (shared-memory bound)
   return (int)(t < 1 ? 1 : t);
 }
@@ -312,7 +340,7 @@ int gram_row_multiple() { return GT_ROWS; }
   } while (0)
 
 void launch_gram(const Ctx& c, int ncols, cudaStream_t s) {
-  const int grid = gram_grid(c.ld);
+  const int grid = gram_grid(c.n_own);
 #define L_STATE(NB, REM)                                                          \
   set_attr<NB, REM>();                                                            \
   k_gram_state<NB, REM><<<grid, GT_THREADS, gram_smem<NB, REM>(), s>>>(c)
@@ -322,11 +350,10 @@ void launch_gram(const Ctx& c, int ncols, cudaStream_t s) {
 
 void launch_gram_raw(const double* Y, int64_t n, int64_t ld, int k, double* part, double* out,
                      int* counter, cudaStream_t s) {
-  (void)n;
-  const int grid = gram_grid(ld);
+  const int grid = gram_grid(n);
 #define L_RAW(NB, REM)                                                            \
   set_attr<NB, REM>();                                                            \
-  k_gram_raw<NB, REM><<<grid, GT_THREADS, gram_smem<NB, REM>(), s>>>(Y, ld, k, part, out, counter)
+  k_gram_raw<NB, REM><<<grid, GT_THREADS, gram_smem<NB, REM>(), s>>>(Y, ld, n, k, part, out, counter)
   GRAM_DISPATCH(k, L_RAW);
 #undef L_RAW
 }

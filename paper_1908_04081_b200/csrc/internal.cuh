@@ -78,7 +78,6 @@ struct SolverState {
   RitzDev rz;
   double cx[CMAX], cr[CMAX], cp[CMAX];      // recovery coefficients, physical columns
   double dx[SMAX][CMAX], dr[SMAX][CMAX];    // per-iteration coords (full trace)
-  double gram[CMAX * CMAX];                 // reduced Gram of the physical block
   long long phase_cycles[8];                // K_small phase timers (clock64, thread 0)
 };
 
@@ -113,6 +112,39 @@ struct Ctx {
   double* first_gram;  // [CMAX*CMAX]
   int red_n;        // CTAs of the row-streaming kernels = partial-sum slots in use
   int stage_cap;    // nnz capacity of one staged CSR tile (0: unstaged kernels)
+  // row-slab partition (CA-MPK): local rows are ordered by ghost depth, so the
+  // rows a level must (re)compute are a prefix.  Single GPU: every entry == n.
+  int64_t n_own;                // owned rows: Gram, recovery, residual norms
+  int64_t lvl_rows[SMAX + 1];   // lvl_rows[d] = local rows with ghost depth <= d
+  double* red_buf;  // [GPACK + 2] packed Gram + ||b-Ax||^2 + ||r||^2 (allreduced)
+};
+
+// rows level l must produce for P (ghost depth <= sigma-1-l) and R (<= sigma-2-l)
+__host__ __device__ inline int64_t lvl_p_rows(const Ctx& c, int sigma, int l) {
+  const int d = sigma - 1 - l;
+  return c.lvl_rows[d < 0 ? 0 : d];
+}
+__host__ __device__ inline int64_t lvl_r_rows(const Ctx& c, int sigma, int l) {
+  const int d = sigma - 2 - l;
+  return c.lvl_rows[d < 0 ? 0 : d];
+}
+
+// halo exchange lists of a row-partitioned plan (dist.cu)
+struct HaloPlan {
+  int n_peers = 0;
+  int* peer_rank = nullptr;     // host [n_peers]
+  int64_t* send_off = nullptr;  // host [n_peers + 1] (rows)
+  int64_t* recv_off = nullptr;  // host [n_peers + 1]
+  int n_send = 0, n_recv = 0;
+  int* d_send_idx = nullptr;    // owned local rows to send, grouped by peer
+  int* d_send_dst = nullptr;    // their offset in the send buffer ([p | r | x] per peer)
+  int* d_send_cnt = nullptr;    // the peer segment's row count
+  int* d_recv_idx = nullptr;    // ghost local rows, grouped by peer
+  int* d_recv_src = nullptr;
+  int* d_recv_cnt = nullptr;
+  double* d_sendbuf = nullptr;  // [3 n_send]
+  double* d_recvbuf = nullptr;  // [3 n_recv]
+  int r_col = 0;                // physical column of R_0 (sigma + 1) of the current run
 };
 
 #define CUDA_OK(expr)                                             \
@@ -154,6 +186,16 @@ void launch_diag_fin(const Ctx& c, int j, cudaStream_t s);
 void launch_params_begin(const Ctx& c, cudaStream_t s);
 void launch_leja_point(const Ctx& c, int n, cudaStream_t s);
 size_t small_smem_bytes();
+// dist.cu
+int nccl_load(const char* path);
+int nccl_unique_id(const char* path, unsigned char* id128);
+int nccl_comm_init(void** comm, const unsigned char* id128, int rank, int world);
+void nccl_comm_destroy(void* comm);
+int halo_exchange(const HaloPlan& h, const Ctx& c, void* comm, cudaStream_t s);
+void halo_unpack(const HaloPlan& h, const Ctx& c, cudaStream_t s);
+int nccl_allreduce(void* comm, double* buf, int64_t count, cudaStream_t s);
+void launch_vsum(double* const* d_bufs, int nb, int len, cudaStream_t s);
+void launch_norm_pack(const Ctx& c, cudaStream_t s);
 int unit_nested_conds(const double* g_host, int s_bar, double* conds_host, int mode, double c,
                       double unit, double eps, double rn, int* s_tilde);
 int unit_leja(double lo, double hi, int count, int grid, double* out);

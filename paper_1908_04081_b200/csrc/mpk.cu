@@ -135,15 +135,15 @@ __host__ __device__ __forceinline__ size_t stage_bytes(int cap) {
   return ((size_t)(cap + 2) * 8 + (size_t)(cap + 4) * 4 + 15) / 16 * 16;
 }
 
-// Runs fn(row, TileStage&) over every row of every tile of this CTA.
+// Runs fn(row, TileStage&) over rows [0, nrows) tile by tile.
 template <class Fn>
-__device__ __forceinline__ void staged_rows(const Ctx& c, Fn&& fn) {
+__device__ __forceinline__ void staged_rows(const Ctx& c, int64_t nrows, Fn&& fn) {
   extern __shared__ __align__(16) unsigned char msm[];
   __shared__ __align__(8) uint64_t bars[MT_STAGES];
   __shared__ int tb[MT_STAGES][2];
   const int cap = c.stage_cap;
   const size_t sb = stage_bytes(cap);
-  const int64_t ntiles = (c.n + MT_ROWS - 1) / MT_ROWS;
+  const int64_t ntiles = (nrows + MT_ROWS - 1) / MT_ROWS;
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int s = 0; s < MT_STAGES; ++s) mbar_init(&bars[s], 1);
@@ -152,7 +152,7 @@ __device__ __forceinline__ void staged_rows(const Ctx& c, Fn&& fn) {
   __syncthreads();
   auto issue = [&](int64_t tile, int s) {  // thread 0 only
     const int64_t r0 = tile * MT_ROWS;
-    const int64_t r1 = r0 + MT_ROWS < c.n ? r0 + MT_ROWS : c.n;
+    const int64_t r1 = r0 + MT_ROWS < nrows ? r0 + MT_ROWS : nrows;
     const int beg = c.rp[r0], end = c.rp[r1];
     const int bv = beg & ~1, bc = beg & ~3;
     const uint32_t nbv = (uint32_t)(((end - bv) * 8 + 15) / 16 * 16);
@@ -180,7 +180,7 @@ __device__ __forceinline__ void staged_rows(const Ctx& c, Fn&& fn) {
     ts.beg_v = tb[s][0];
     ts.beg_c = tb[s][1];
     const int64_t i = tile * MT_ROWS + tid;
-    if (i < c.n) fn(i, ts);
+    if (i < nrows) fn(i, ts);
     __syncthreads();  // stage s free again
     if (tid == 0) {
       const int64_t t = tile + (int64_t)MT_STAGES * gridDim.x;
@@ -231,7 +231,8 @@ __global__ void __launch_bounds__(MT_ROWS) k_level0_staged(Ctx c) {
   double* R1 = c.Y + (int64_t)(sigma + 2) * c.ld;
   double tt = 0.0, rr = 0.0;
   int bad = 0;
-  staged_rows(c, [&](int64_t i, const TileStage& ts) {
+  const int64_t n_own = c.n_own, rlim = lvl_r_rows(c, sigma, 0);
+  staged_rows(c, lvl_p_rows(c, sigma, 0), [&](int64_t i, const TileStage& ts) {
     const int beg = c.rp[i], end = c.rp[i + 1];
     const double p = P0[i], r = R0[i];
     double acc[3];
@@ -240,13 +241,15 @@ __global__ void __launch_bounds__(MT_ROWS) k_level0_staged(Ctx c) {
       row_dot_s<3>(ts, beg, end, xs, acc);
     else
       row_dot_s<2>(ts, beg, end, xs, acc);
-    const double t = __dsub_rn(c.b[i], acc[0]);
-    tt = fma(t, t, tt);
-    rr = fma(r, r, rr);
+    if (i < n_own) {
+      const double t = __dsub_rn(c.b[i], acc[0]);
+      tt = fma(t, t, tt);
+      rr = fma(r, r, rr);
+    }
     const double wp = recur(acc[1], p, 0.0, th, ga, 0.0, false);
     P1[i] = wp;
     bad |= !finite(wp);
-    if (do_r) {
+    if (do_r && i < rlim) {
       const double wr = recur(acc[2], r, 0.0, th, ga, 0.0, false);
       R1[i] = wr;
       bad |= !finite(wr);
@@ -277,18 +280,20 @@ __global__ void __launch_bounds__(MT_ROWS) k_level_staged(Ctx c, int l) {
   const double* Rm = Rl - c.ld;
   double* Rn = c.Y + (int64_t)(sigma + 2 + l) * c.ld;
   int bad = 0;
-  staged_rows(c, [&](int64_t i, const TileStage& ts) {
+  const int64_t rlim = lvl_r_rows(c, sigma, l);
+  staged_rows(c, lvl_p_rows(c, sigma, l), [&](int64_t i, const TileStage& ts) {
     const int beg = c.rp[i], end = c.rp[i + 1];
     double acc[2];
     const double* xs[2] = {Pl, Rl};
-    if (do_r)
+    const bool rr = do_r && i < rlim;
+    if (rr)
       row_dot_s<2>(ts, beg, end, xs, acc);
     else
       row_dot_s<1>(ts, beg, end, xs, acc);
     const double wp = recur(acc[0], Pl[i], use_mu ? Pm[i] : 0.0, th, ga, mu, use_mu);
     Pn[i] = wp;
     bad |= !finite(wp);
-    if (do_r) {
+    if (rr) {
       const double wr = recur(acc[1], Rl[i], use_mu ? Rm[i] : 0.0, th, ga, mu, use_mu);
       Rn[i] = wr;
       bad |= !finite(wr);
@@ -314,8 +319,9 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0(Ctx c) {
   double* R1 = c.Y + (int64_t)(sigma + 2) * c.ld;
   double tt = 0.0, rr = 0.0;
   int bad = 0;
+  const int64_t n_own = c.n_own, plim = lvl_p_rows(c, sigma, 0), rlim = lvl_r_rows(c, sigma, 0);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += stride) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
     const int beg = c.rp[i], end = c.rp[i + 1];
     const double p = P0[i], r = R0[i];
     double acc[3];
@@ -326,13 +332,15 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0(Ctx c) {
       const double* xs[2] = {c.x, P0};
       row_dot<2>(c.col, c.val, beg, end, xs, acc);
     }
-    const double t = __dsub_rn(c.b[i], acc[0]);
-    tt = fma(t, t, tt);
-    rr = fma(r, r, rr);
+    if (i < n_own) {
+      const double t = __dsub_rn(c.b[i], acc[0]);
+      tt = fma(t, t, tt);
+      rr = fma(r, r, rr);
+    }
     const double wp = recur(acc[1], p, 0.0, th, ga, 0.0, false);
     P1[i] = wp;
     bad |= !finite(wp);
-    if (do_r) {
+    if (do_r && i < rlim) {
       const double wr = recur(acc[2], r, 0.0, th, ga, 0.0, false);
       R1[i] = wr;
       bad |= !finite(wr);
@@ -351,6 +359,7 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0(Ctx c) {
 template <bool DO_R>
 __device__ __forceinline__ int level_rows(const Ctx& c, int l, int sigma, double th, double ga,
                                           double mu, bool use_mu) {
+  const int64_t plim = lvl_p_rows(c, sigma, l), rlim = lvl_r_rows(c, sigma, l);
   const double* Pl = c.Y + (int64_t)l * c.ld;
   const double* Pm = Pl - c.ld;
   double* Pn = c.Y + (int64_t)(l + 1) * c.ld;
@@ -359,10 +368,11 @@ __device__ __forceinline__ int level_rows(const Ctx& c, int l, int sigma, double
   double* Rn = c.Y + (int64_t)(sigma + 2 + l) * c.ld;
   int bad = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += stride) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
     const int beg = c.rp[i], end = c.rp[i + 1];
+    const bool rr = DO_R && i < rlim;
     double acc[2];
-    if (DO_R) {
+    if (rr) {
       const double* xs[2] = {Pl, Rl};
       row_dot<2>(c.col, c.val, beg, end, xs, acc);
     } else {
@@ -372,7 +382,7 @@ __device__ __forceinline__ int level_rows(const Ctx& c, int l, int sigma, double
     const double wp = recur(acc[0], Pl[i], use_mu ? Pm[i] : 0.0, th, ga, mu, use_mu);
     Pn[i] = wp;
     bad |= !finite(wp);
-    if (DO_R) {
+    if (rr) {
       const double wr = recur(acc[1], Rl[i], use_mu ? Rm[i] : 0.0, th, ga, mu, use_mu);
       Rn[i] = wr;
       bad |= !finite(wr);
@@ -403,7 +413,11 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_init_residual(Ctx c, const dou
   double* R0 = c.Y + (int64_t)(sigma + 1) * c.ld;
   double bb = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += stride) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.lvl_rows[SMAX]; i += stride) {
+    if (i >= c.n_own) {  // ghost rows: x from x0; p, r arrive with the first halo exchange
+      c.x[i] = x0[i];
+      continue;
+    }
     double acc[1];
     const double* xs[1] = {x0};
     row_dot<1>(c.col, c.val, c.rp[i], c.rp[i + 1], xs, acc);
@@ -425,7 +439,7 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_diag_resid(Ctx c, int j) {
   if (j >= c.st->diag_n) return;
   double s_t = 0.0, s_r = 0.0, s_g = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += stride) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n_own; i += stride) {
     double acc[1];
     const double* xs[1] = {c.xj};
     row_dot<1>(c.col, c.val, c.rp[i], c.rp[i + 1], xs, acc);
@@ -504,8 +518,12 @@ inline int grid_rows(int64_t n) {
 // partial-sum arrays have a fixed length and the reductions a fixed order.
 size_t staged_smem_bytes(int cap) { return MT_STAGES * stage_bytes(cap); }
 
+// The attribute is per kernel and process-wide, and several plans (ranks of a
+// virtual group, different matrices) may coexist: raise it once to the staging
+// ceiling instead of to one plan's tile size.
 void staged_prepare(int cap) {
-  const int bytes = (int)staged_smem_bytes(cap);
+  (void)cap;
+  const int bytes = 200 * 1024;
   cudaFuncSetAttribute(k_level0_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_level_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }

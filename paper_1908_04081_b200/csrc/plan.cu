@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -77,6 +78,7 @@ struct sscg_plan {
   double* d_mu = nullptr;
   double* d_otrue = nullptr;
   double* d_fg = nullptr;
+  double* d_red = nullptr;  // [GPACK + 2] allreduce payload
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // Leja branch of the outer-loop graph
   cudaEvent_t ev_fork = nullptr;
@@ -95,8 +97,17 @@ struct sscg_plan {
   double prof_ms[5] = {0, 0, 0, 0, 0};
   int64_t prof_cnt[5] = {0, 0, 0, 0, 0};
   int64_t bytes = 0;
+  int64_t n_own = 0;               // owned rows (== n on a single-GPU plan)
+  int64_t lvl_rows[SMAX + 1] = {};  // local rows with ghost depth <= d
   int red_n = RED_BLOCKS;  // CTAs of the row-streaming kernels
   int stage_cap = 0;       // staged CSR tile capacity (0: unstaged kernels)
+  // row partition (sscg_plan_create_part)
+  int64_t n_local = 0;     // local rows incl. every ghost depth (vector length)
+  int depth = SMAX;        // ghost depth the partition provides (max sigma)
+  int rank = 0, world = 1;
+  HaloPlan halo;
+  void* comm = nullptr;    // ncclComm_t, or NULL (single GPU / virtual group)
+  int partitioned = 0;
 };
 
 namespace {
@@ -191,6 +202,9 @@ Ctx make_ctx(sscg_plan* p) {
   c.first_gram = p->d_fg;
   c.red_n = p->red_n;
   c.stage_cap = p->stage_cap;
+  c.n_own = p->n_own;
+  for (int d = 0; d <= SMAX; ++d) c.lvl_rows[d] = p->lvl_rows[d];
+  c.red_buf = p->d_red;
   return c;
 }
 
@@ -212,7 +226,12 @@ int check_config(const sscg_config* c) {
   return SSCG_OK;
 }
 
-void capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t s) {
+int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t s) {
+  // halo of p, r, x for the communication-avoiding levels (partitioned plans)
+  if (p->partitioned && p->comm) {
+    TRY(halo_exchange(p->halo, c, p->comm, s));
+    halo_unpack(p->halo, c, s);
+  }
   // next-block parameters: endpoints now, Leja points 2.. on the side branch,
   // each joined right before the matrix-powers level that consumes it
   launch_params_begin(c, s);
@@ -227,6 +246,10 @@ void capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t
     launch_level(c, l, s);
   }
   launch_gram(c, 2 * sigma + 1, s);
+  if (p->comm) {  // the one synchronisation of the outer loop
+    const int k = 2 * sigma + 1;
+    TRY(nccl_allreduce(p->comm, c.red_buf, (int64_t)k * (k + 1) / 2 + 2, s));
+  }
   launch_small(c, s);
   if (full) {
     for (int j = 0; j < sigma; ++j) {
@@ -236,7 +259,7 @@ void capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t
     }
   }
   launch_recover(c, s);
-  (void)p;
+  return SSCG_OK;
 }
 
 int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
@@ -247,8 +270,12 @@ int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
   }
   cudaGraph_t g = nullptr;
   CUDA_OK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-  capture_outer(p, c, sigma, full, p->stream);
+  const int crc = capture_outer(p, c, sigma, full, p->stream);
   cudaError_t e = cudaStreamEndCapture(p->stream, &g);
+  if (crc != SSCG_OK) {
+    if (g) cudaGraphDestroy(g);
+    return crc;
+  }
   if (e != cudaSuccess) return sscg_fail_cuda(e, "cudaStreamEndCapture");
   e = cudaGraphInstantiate(&p->gexec, g, 0);
   cudaGraphDestroy(g);
@@ -277,10 +304,21 @@ int launch_outer_profiled(sscg_plan* p, const Ctx& c, int sigma, int full, int o
     evs.push_back(e);
     return SSCG_OK;
   };
+  if (p->partitioned && p->comm) {
+    int hrc = SSCG_OK;
+    TRY(rec(4, [&] { hrc = halo_exchange(p->halo, c, p->comm, p->stream); halo_unpack(p->halo, c, p->stream); }));
+    TRY(hrc);
+  }
   TRY(rec(4, [&] { launch_params_begin(c, p->stream); }));
   for (int n = 2; n < sigma; ++n) TRY(rec(4, [&] { launch_leja_point(c, n, p->stream); }));
   for (int l = 0; l < sigma; ++l) TRY(rec(0, [&] { launch_level(c, l, p->stream); }));
   TRY(rec(1, [&] { launch_gram(c, 2 * sigma + 1, p->stream); }));
+  if (p->comm) {
+    const int k = 2 * sigma + 1;
+    int arc = SSCG_OK;
+    TRY(rec(4, [&] { arc = nccl_allreduce(p->comm, c.red_buf, (int64_t)k * (k + 1) / 2 + 2, p->stream); }));
+    TRY(arc);
+  }
   TRY(rec(2, [&] { launch_small(c, p->stream); }));
   if (full) {
     for (int j = 0; j < sigma; ++j) {
@@ -311,119 +349,102 @@ int sscg_device_count(int32_t* count) {
   return SSCG_OK;
 }
 
-int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
-                     const int64_t* row_ptr, const int32_t* col_idx, const double* values) {
-  if (!out) return sscg_fail(SSCG_EINVAL, "out is NULL");
-  *out = nullptr;
-  if (n < 1) return sscg_fail(SSCG_EINVAL, "n must be >= 1");
+}  // extern "C"
+
+namespace {
+// shared constructor: n_rows local rows carry matrix rows, n_own of them are
+// owned, n_local rows (>= n_rows) is the vector length; lvl[d] = rows with
+// ghost depth <= d (d = 0..depth)
+int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64_t n_local,
+              int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+              const int64_t* lvl, int depth) {
+  if (n_rows < 1 || n_own < 1 || n_own > n_rows || n_local < n_rows)
+    return sscg_fail(SSCG_EINVAL, "n must be >= 1 (n_own <= n_rows <= n_local)");
   if (nnz < 0 || nnz >= ((int64_t)1 << 31))
     return sscg_fail(SSCG_EINVAL, "nnz=%lld outside the int32 CSR range", (long long)nnz);
-  if (n >= ((int64_t)1 << 31)) return sscg_fail(SSCG_EINVAL, "n exceeds int32 column indices");
+  if (n_local >= ((int64_t)1 << 31)) return sscg_fail(SSCG_EINVAL, "n exceeds int32 column indices");
   if (!row_ptr || (nnz && (!col_idx || !values))) return sscg_fail(SSCG_EINVAL, "NULL CSR array");
-  if (row_ptr[0] != 0 || row_ptr[n] != nnz)
+  if (row_ptr[0] != 0 || row_ptr[n_rows] != nnz)
     return sscg_fail(SSCG_EINVAL, "row_ptr must start at 0 and end at nnz");
   int ndev = 0;
   CUDA_OK(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev)
     return sscg_fail(SSCG_ENODEV, "device %d not present (%d visible)", device, ndev);
   CUDA_OK(cudaSetDevice(device));
-  sscg_plan* p = new sscg_plan();
   p->device = device;
-  p->n = n;
+  p->n = n_rows;
+  p->n_own = n_own;
+  p->n_local = n_local;
   p->nnz = nnz;
-  p->ld = round_up(n, gram_row_multiple());
+  p->depth = depth;
+  p->ld = round_up(n_local, gram_row_multiple());
+  for (int d = 0; d <= SMAX; ++d) p->lvl_rows[d] = lvl[d <= depth ? d : depth];
   int rc = SSCG_OK;
-  do {
-    std::vector<int> rp32(n + 1);
-    for (int64_t i = 0; i <= n; ++i) {
-      if (i && row_ptr[i] < row_ptr[i - 1]) {
-        rc = sscg_fail(SSCG_EINVAL, "row_ptr must be nondecreasing");
-        break;
-      }
-      rp32[i] = (int)row_ptr[i];
-    }
-    if (rc) break;
-    if ((rc = dalloc(p, &p->d_rp, n + 1))) break;
-    // +4 / +2 elements: the staged kernels round bulk copies up to 16 bytes
-    if ((rc = dalloc(p, &p->d_col, nnz + 4))) break;
-    if ((rc = dalloc(p, &p->d_val, nnz + 2))) break;
-    cudaError_t e;
-    if ((e = cudaMemcpy(p->d_rp, rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice))) {
-      rc = sscg_fail_cuda(e, "upload row_ptr");
-      break;
-    }
-    if (nnz && (e = cudaMemcpy(p->d_col, col_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice))) {
-      rc = sscg_fail_cuda(e, "upload col_idx");
-      break;
-    }
-    if (nnz && (e = cudaMemcpy(p->d_val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice))) {
-      rc = sscg_fail_cuda(e, "upload values");
-      break;
-    }
-    for (double** v : {&p->d_x, &p->d_b, &p->d_x0, &p->d_xj, &p->d_rj}) {
-      if ((rc = dalloc(p, v, p->ld))) break;
-      if ((e = cudaMemset(*v, 0, sizeof(double) * p->ld))) {
-        rc = sscg_fail_cuda(e, "memset");
-        break;
-      }
-    }
-    if (rc) break;
-    if ((rc = dalloc(p, &p->d_st, 1))) break;
-    if ((rc = dalloc(p, &p->d_cfg, 1))) break;
-    if ((rc = dalloc(p, &p->d_part_t, RED_BLOCKS))) break;
-    if ((rc = dalloc(p, &p->d_part_r, RED_BLOCKS))) break;
-    if ((rc = dalloc(p, &p->d_part_d, 3 * RED_BLOCKS))) break;
-    if ((rc = dalloc(p, &p->d_part_g, (size_t)GRAM_BLOCKS * GPACK))) break;
-    if ((rc = dalloc(p, &p->d_fg, CMAX * CMAX))) break;
-    if ((e = cudaMemset(p->d_st, 0, sizeof(SolverState)))) {
-      rc = sscg_fail_cuda(e, "memset state");
-      break;
-    }
-    if ((e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking)) ||
-        (e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking)) ||
-        (e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming))) {
-      rc = sscg_fail_cuda(e, "stream");
-      break;
-    }
-    for (int i = 0; i < SMAX && !rc; ++i)
-      if ((e = cudaEventCreateWithFlags(&p->ev_leja[i], cudaEventDisableTiming)))
-        rc = sscg_fail_cuda(e, "event");
-    if (rc) break;
-    if ((e = cudaHostAlloc((void**)&p->h_done, 2 * sizeof(int), cudaHostAllocDefault))) {
-      rc = sscg_fail_cuda(e, "pinned flag");
-      break;
-    }
-    for (auto* ev : {&p->ev_chunk[0], &p->ev_chunk[1]})
-      if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming))) rc = sscg_fail_cuda(e, "event");
-    if (rc) break;
-    if ((e = cudaEventCreate(&p->ev_start)) || (e = cudaEventCreate(&p->ev_stop))) {
-      rc = sscg_fail_cuda(e, "event");
-      break;
-    }
-    small_prepare();
-    // launch geometry of the row-streaming kernels: TMA-staged CSR tiles when a
-    // tile's segment fits shared memory (every stencil), else the direct kernels
-    int sms = NUM_SMS;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    int64_t maxt = 0;
-    for (int64_t r0 = 0; r0 < n; r0 += MT_ROWS) {
-      const int64_t r1 = r0 + MT_ROWS < n ? r0 + MT_ROWS : n;
-      maxt = std::max<int64_t>(maxt, row_ptr[r1] - row_ptr[r0]);
-    }
-    const int64_t cap = (maxt + 4 + 3) / 4 * 4;
-    const int64_t ntiles = (n + MT_ROWS - 1) / MT_ROWS;
-    if (staged_smem_bytes((int)cap) <= 200 * 1024) {
-      p->stage_cap = (int)cap;
-      staged_prepare(p->stage_cap);
-      int per_sm = staged_ctas_per_sm(p->stage_cap);
-      if (per_sm < 1) per_sm = 1;
-      p->red_n = (int)std::min<int64_t>({(int64_t)sms * per_sm, (int64_t)RED_BLOCKS, ntiles});
-    } else {
-      p->stage_cap = 0;
-      p->red_n = (int)std::min<int64_t>((int64_t)sms * 4, (n + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
-    }
-    if (p->red_n < 1) p->red_n = 1;
-  } while (0);
+  std::vector<int> rp32(n_rows + 1);
+  for (int64_t i = 0; i <= n_rows; ++i) {
+    if (i && row_ptr[i] < row_ptr[i - 1]) return sscg_fail(SSCG_EINVAL, "row_ptr must be nondecreasing");
+    rp32[i] = (int)row_ptr[i];
+  }
+  // +4 / +2 elements: the staged kernels round bulk copies up to 16 bytes
+  TRY(dalloc(p, &p->d_rp, n_rows + 1));
+  TRY(dalloc(p, &p->d_col, nnz + 4));
+  TRY(dalloc(p, &p->d_val, nnz + 2));
+  CUDA_OK(cudaMemcpy(p->d_rp, rp32.data(), sizeof(int) * (n_rows + 1), cudaMemcpyHostToDevice));
+  if (nnz) CUDA_OK(cudaMemcpy(p->d_col, col_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice));
+  if (nnz) CUDA_OK(cudaMemcpy(p->d_val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  for (double** v : {&p->d_x, &p->d_b, &p->d_x0, &p->d_xj, &p->d_rj}) {
+    TRY(dalloc(p, v, p->ld));
+    CUDA_OK(cudaMemset(*v, 0, sizeof(double) * p->ld));
+  }
+  TRY(dalloc(p, &p->d_st, 1));
+  TRY(dalloc(p, &p->d_cfg, 1));
+  TRY(dalloc(p, &p->d_part_t, RED_BLOCKS));
+  TRY(dalloc(p, &p->d_part_r, RED_BLOCKS));
+  TRY(dalloc(p, &p->d_part_d, 3 * RED_BLOCKS));
+  TRY(dalloc(p, &p->d_part_g, (size_t)GRAM_BLOCKS * GPACK));
+  TRY(dalloc(p, &p->d_fg, CMAX * CMAX));
+  TRY(dalloc(p, &p->d_red, GPACK + 2));
+  CUDA_OK(cudaMemset(p->d_st, 0, sizeof(SolverState)));
+  CUDA_OK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  CUDA_OK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+  CUDA_OK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  for (int i = 0; i < SMAX; ++i) CUDA_OK(cudaEventCreateWithFlags(&p->ev_leja[i], cudaEventDisableTiming));
+  CUDA_OK(cudaHostAlloc((void**)&p->h_done, 2 * sizeof(int), cudaHostAllocDefault));
+  for (auto* ev : {&p->ev_chunk[0], &p->ev_chunk[1]})
+    CUDA_OK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+  CUDA_OK(cudaEventCreate(&p->ev_start));
+  CUDA_OK(cudaEventCreate(&p->ev_stop));
+  small_prepare();
+  // launch geometry of the row-streaming kernels: TMA-staged CSR tiles when a
+  // tile's segment fits shared memory (every stencil), else the direct kernels
+  int sms = NUM_SMS;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  int64_t maxt = 0;
+  for (int64_t r0 = 0; r0 < n_rows; r0 += MT_ROWS) {
+    const int64_t r1 = r0 + MT_ROWS < n_rows ? r0 + MT_ROWS : n_rows;
+    maxt = std::max<int64_t>(maxt, row_ptr[r1] - row_ptr[r0]);
+  }
+  const int64_t cap = (maxt + 4 + 3) / 4 * 4;
+  const int64_t ntiles = (n_rows + MT_ROWS - 1) / MT_ROWS;
+  if (staged_smem_bytes((int)cap) <= 200 * 1024) {
+    p->stage_cap = (int)cap;
+    staged_prepare(p->stage_cap);
+    int per_sm = staged_ctas_per_sm(p->stage_cap);
+    if (per_sm < 1) per_sm = 1;
+    p->red_n = (int)std::min<int64_t>({(int64_t)sms * per_sm, (int64_t)RED_BLOCKS, ntiles});
+  } else {
+    p->stage_cap = 0;
+    p->red_n = (int)std::min<int64_t>((int64_t)sms * 4, (n_rows + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
+  }
+  if (p->red_n < 1) p->red_n = 1;
+  return rc;
+}
+
+int create_wrapped(sscg_plan** out, const std::function<int(sscg_plan*)>& init) {
+  if (!out) return sscg_fail(SSCG_EINVAL, "out is NULL");
+  *out = nullptr;
+  sscg_plan* p = new sscg_plan();
+  const int rc = init(p);
   if (rc != SSCG_OK) {
     std::string keep = g_err;
     sscg_plan_destroy(p);
@@ -433,16 +454,111 @@ int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
   *out = p;
   return SSCG_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
+                     const int64_t* row_ptr, const int32_t* col_idx, const double* values) {
+  return create_wrapped(out, [&](sscg_plan* p) {
+    if (n < 1) return sscg_fail(SSCG_EINVAL, "n must be >= 1");
+    int64_t lvl[SMAX + 1];
+    for (int d = 0; d <= SMAX; ++d) lvl[d] = n;
+    return plan_init(p, device, n, n, n, nnz, row_ptr, col_idx, values, lvl, SMAX);
+  });
+}
+
+int sscg_nccl_unique_id(const char* nccl_lib, unsigned char* id128) {
+  if (!id128) return sscg_fail(SSCG_EINVAL, "NULL id buffer");
+  return nccl_unique_id(nccl_lib, id128);
+}
+
+int sscg_plan_create_part(sscg_plan** out, int32_t device, const sscg_part* part) {
+  return create_wrapped(out, [&](sscg_plan* p) {
+    if (!part) return sscg_fail(SSCG_EINVAL, "NULL partition");
+    const sscg_part& q = *part;
+    if (q.depth < 1 || q.depth > SMAX) return sscg_fail(SSCG_EINVAL, "ghost depth outside [1, %d]", SMAX);
+    if (!q.lvl_rows) return sscg_fail(SSCG_EINVAL, "NULL lvl_rows");
+    if (q.lvl_rows[0] != q.n_own || q.lvl_rows[q.depth] != q.n_local ||
+        q.lvl_rows[q.depth - 1] != q.n_rows)
+      return sscg_fail(SSCG_EINVAL, "lvl_rows inconsistent with n_own / n_rows / n_local");
+    int rc = plan_init(p, device, q.n_rows, q.n_own, q.n_local, q.nnz, q.row_ptr, q.col_idx,
+                       q.values, q.lvl_rows, q.depth);
+    if (rc) return rc;
+    p->partitioned = 1;
+    p->rank = q.rank;
+    p->world = q.world;
+    HaloPlan& h = p->halo;
+    h.n_peers = q.n_peers;
+    h.peer_rank = new int[q.n_peers > 0 ? q.n_peers : 1];
+    h.send_off = new int64_t[q.n_peers + 1];
+    h.recv_off = new int64_t[q.n_peers + 1];
+    h.send_off[0] = h.recv_off[0] = 0;
+    for (int i = 0; i < q.n_peers; ++i) {
+      h.peer_rank[i] = q.peer_rank[i];
+      h.send_off[i + 1] = q.send_off[i + 1];
+      h.recv_off[i + 1] = q.recv_off[i + 1];
+    }
+    h.n_send = (int)h.send_off[q.n_peers];
+    h.n_recv = (int)h.recv_off[q.n_peers];
+    std::vector<int> sdst(h.n_send), scnt(h.n_send), rsrc(h.n_recv), rcnt(h.n_recv);
+    for (int i = 0; i < q.n_peers; ++i) {
+      for (int64_t t = h.send_off[i]; t < h.send_off[i + 1]; ++t) {
+        sdst[t] = (int)(3 * h.send_off[i] + (t - h.send_off[i]));
+        scnt[t] = (int)(h.send_off[i + 1] - h.send_off[i]);
+      }
+      for (int64_t t = h.recv_off[i]; t < h.recv_off[i + 1]; ++t) {
+        rsrc[t] = (int)(3 * h.recv_off[i] + (t - h.recv_off[i]));
+        rcnt[t] = (int)(h.recv_off[i + 1] - h.recv_off[i]);
+      }
+    }
+    for (int64_t t = 0; t < h.n_send; ++t)
+      if (q.send_idx[t] < 0 || q.send_idx[t] >= q.n_own) return sscg_fail(SSCG_EINVAL, "send index not owned");
+    for (int64_t t = 0; t < h.n_recv; ++t)
+      if (q.recv_idx[t] < q.n_own || q.recv_idx[t] >= q.n_local) return sscg_fail(SSCG_EINVAL, "recv index not a ghost");
+    TRY(dalloc(p, &h.d_send_idx, h.n_send));
+    TRY(dalloc(p, &h.d_send_dst, h.n_send));
+    TRY(dalloc(p, &h.d_send_cnt, h.n_send));
+    TRY(dalloc(p, &h.d_recv_idx, h.n_recv));
+    TRY(dalloc(p, &h.d_recv_src, h.n_recv));
+    TRY(dalloc(p, &h.d_recv_cnt, h.n_recv));
+    TRY(dalloc(p, &h.d_sendbuf, 3 * (size_t)h.n_send));
+    TRY(dalloc(p, &h.d_recvbuf, 3 * (size_t)h.n_recv));
+    if (h.n_send) {
+      CUDA_OK(cudaMemcpy(h.d_send_idx, q.send_idx, sizeof(int) * h.n_send, cudaMemcpyHostToDevice));
+      CUDA_OK(cudaMemcpy(h.d_send_dst, sdst.data(), sizeof(int) * h.n_send, cudaMemcpyHostToDevice));
+      CUDA_OK(cudaMemcpy(h.d_send_cnt, scnt.data(), sizeof(int) * h.n_send, cudaMemcpyHostToDevice));
+    }
+    if (h.n_recv) {
+      CUDA_OK(cudaMemcpy(h.d_recv_idx, q.recv_idx, sizeof(int) * h.n_recv, cudaMemcpyHostToDevice));
+      CUDA_OK(cudaMemcpy(h.d_recv_src, rsrc.data(), sizeof(int) * h.n_recv, cudaMemcpyHostToDevice));
+      CUDA_OK(cudaMemcpy(h.d_recv_cnt, rcnt.data(), sizeof(int) * h.n_recv, cudaMemcpyHostToDevice));
+    }
+    if (q.nccl_id) {  // real multi-process run: one NCCL communicator per plan
+      TRY(nccl_load(q.nccl_lib));
+      TRY(nccl_comm_init(&p->comm, q.nccl_id, q.rank, q.world));
+    }
+    return SSCG_OK;
+  });
+}
 
 int sscg_plan_destroy(sscg_plan* p) {
   if (!p) return SSCG_OK;
   cudaSetDevice(p->device);
   if (p->stream) cudaStreamSynchronize(p->stream);
   if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  if (p->comm) nccl_comm_destroy(p->comm);
+  HaloPlan& h = p->halo;
+  for (void* b : {(void*)h.d_send_idx, (void*)h.d_send_dst, (void*)h.d_send_cnt, (void*)h.d_recv_idx,
+                  (void*)h.d_recv_src, (void*)h.d_recv_cnt, (void*)h.d_sendbuf, (void*)h.d_recvbuf})
+    if (b) cudaFree(b);
+  delete[] h.peer_rank;
+  delete[] h.send_off;
+  delete[] h.recv_off;
   void* bufs[] = {p->d_rp, p->d_col, p->d_val, p->d_Y, p->d_x, p->d_b, p->d_x0, p->d_xj,
                   p->d_rj, p->d_st, p->d_cfg, p->d_part_t, p->d_part_r, p->d_part_d,
                   p->d_part_g, p->d_leja, p->d_it, p->d_ri, p->d_rd, p->d_conds, p->d_th,
-                  p->d_ga, p->d_mu, p->d_otrue, p->d_fg};
+                  p->d_ga, p->d_mu, p->d_otrue, p->d_fg, p->d_red};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_done) cudaFreeHost(p->h_done);
@@ -465,11 +581,11 @@ int sscg_plan_device_bytes(const sscg_plan* p, int64_t* bytes) {
 int sscg_load(sscg_plan* p, const double* b, const double* x0) {
   if (!p || !b) return sscg_fail(SSCG_EINVAL, "NULL argument");
   CUDA_OK(cudaSetDevice(p->device));
-  CUDA_OK(cudaMemcpyAsync(p->d_b, b, sizeof(double) * p->n, cudaMemcpyHostToDevice, p->stream));
+  CUDA_OK(cudaMemcpyAsync(p->d_b, b, sizeof(double) * p->n_own, cudaMemcpyHostToDevice, p->stream));
   if (x0)
-    CUDA_OK(cudaMemcpyAsync(p->d_x0, x0, sizeof(double) * p->n, cudaMemcpyHostToDevice, p->stream));
+    CUDA_OK(cudaMemcpyAsync(p->d_x0, x0, sizeof(double) * p->n_local, cudaMemcpyHostToDevice, p->stream));
   else
-    CUDA_OK(cudaMemsetAsync(p->d_x0, 0, sizeof(double) * p->n, p->stream));
+    CUDA_OK(cudaMemsetAsync(p->d_x0, 0, sizeof(double) * p->n_local, p->stream));
   p->have_rhs = 1;
   return SSCG_OK;
 }
@@ -489,13 +605,22 @@ int sscg_get_profile(const sscg_plan* p, double* ms5, int64_t* counts5) {
   return SSCG_OK;
 }
 
-int sscg_run(sscg_plan* p, const sscg_config* cfg, sscg_logs* logs) {
+}  // extern "C"
+
+namespace {
+// validate, size the work buffers, upload the device config, scrub the logs
+int run_prepare(sscg_plan* p, const sscg_config* cfg) {
   if (!p) return sscg_fail(SSCG_EINVAL, "NULL plan");
   TRY(check_config(cfg));
   if (!p->have_rhs) return sscg_fail(SSCG_EINVAL, "sscg_load must precede sscg_run");
+  if (p->partitioned && cfg->sigma > p->depth)
+    return sscg_fail(SSCG_EINVAL, "sigma=%d exceeds the partition's ghost depth %d", cfg->sigma, p->depth);
+  if (p->partitioned && cfg->trace_full)
+    return sscg_fail(SSCG_EINVAL, "trace_full is not supported on a row-partitioned solve");
   CUDA_OK(cudaSetDevice(p->device));
   TRY(ensure_work(p, cfg->sigma, cfg->max_outer, cfg->leja_grid));
   p->cfg = *cfg;
+  p->halo.r_col = cfg->sigma + 1;
   DevConfig dc;
   memset(&dc, 0, sizeof(dc));
   dc.sigma = cfg->sigma;
@@ -522,14 +647,23 @@ int sscg_run(sscg_plan* p, const sscg_config* cfg, sscg_logs* logs) {
   dc.cap_iters = p->cap_iters;
   dc.cap_outer = p->cap_outer - 1;
   CUDA_OK(cudaMemcpyAsync(p->d_cfg, &dc, sizeof(dc), cudaMemcpyHostToDevice, p->stream));
-  // scrub logs so short runs leave NaN, not stale values
   CUDA_OK(cudaMemsetAsync(p->d_it, 0xff, sizeof(double) * p->cap_iters * SSCG_IT_N, p->stream));
+  return SSCG_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int sscg_run(sscg_plan* p, const sscg_config* cfg, sscg_logs* logs) {
+  TRY(run_prepare(p, cfg));
   const Ctx c = make_ctx(p);
   const int sigma = cfg->sigma, full = cfg->trace_full ? 1 : 0;
   if (!p->profiling) TRY(build_graph(p, c, sigma, full));
 
   CUDA_OK(cudaEventRecord(p->ev_start, p->stream));
   launch_init_residual(c, p->d_x0, p->stream);
+  launch_norm_pack(c, p->stream);
+  if (p->comm) TRY(nccl_allreduce(p->comm, c.red_buf, 1, p->stream));  // ||b||^2 once per solve
   launch_state_init(c, p->stream);
   CUDA_OK(cudaGetLastError());
 
@@ -596,7 +730,7 @@ int sscg_fetch(sscg_plan* p, double* x_out, sscg_logs* logs) {
   if (!p) return sscg_fail(SSCG_EINVAL, "NULL plan");
   CUDA_OK(cudaSetDevice(p->device));
   CUDA_OK(cudaStreamSynchronize(p->stream));
-  if (x_out) CUDA_OK(cudaMemcpy(x_out, p->d_x, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
+  if (x_out) CUDA_OK(cudaMemcpy(x_out, p->d_x, sizeof(double) * p->n_own, cudaMemcpyDeviceToHost));
   if (!logs) return SSCG_OK;
   SolverState st;
   CUDA_OK(cudaMemcpy(&st, p->d_st, sizeof(st), cudaMemcpyDeviceToHost));
@@ -647,6 +781,96 @@ int sscg_get_small_phases(const sscg_plan* p, int64_t* cycles8) {
   long long h[8];
   CUDA_OK(cudaMemcpy(h, p->d_st->phase_cycles, sizeof(h), cudaMemcpyDeviceToHost));
   for (int i = 0; i < 8; ++i) cycles8[i] = h[i];
+  return SSCG_OK;
+}
+
+// ---- virtual-rank group (single process, lock step, no NCCL) ------------------
+int sscg_vgroup_run(sscg_plan* const* plans, int32_t np, const sscg_config* cfg,
+                    const double* const* b, const double* const* x0, sscg_logs* logs0) {
+  if (!plans || np < 1 || !b) return sscg_fail(SSCG_EINVAL, "bad group arguments");
+  for (int i = 0; i < np; ++i) {
+    if (!plans[i] || !plans[i]->partitioned || plans[i]->comm || plans[i]->world != np ||
+        plans[i]->rank != i || plans[i]->device != plans[0]->device)
+      return sscg_fail(SSCG_EINVAL, "plan %d is not member %d of a %d-plan virtual group on one device",
+                       i, i, np);
+    TRY(sscg_load(plans[i], b[i], x0 ? x0[i] : nullptr));
+    CUDA_OK(cudaStreamSynchronize(plans[i]->stream));
+  }
+  for (int i = 0; i < np; ++i) TRY(run_prepare(plans[i], cfg));
+  for (int i = 0; i < np; ++i) CUDA_OK(cudaStreamSynchronize(plans[i]->stream));
+  cudaStream_t s = plans[0]->stream;
+  std::vector<Ctx> cs;
+  std::vector<double*> reds;
+  for (int i = 0; i < np; ++i) {
+    cs.push_back(make_ctx(plans[i]));
+    reds.push_back(plans[i]->d_red);
+  }
+  double** d_reds = nullptr;
+  CUDA_OK(cudaMalloc(&d_reds, sizeof(double*) * np));
+  CUDA_OK(cudaMemcpy(d_reds, reds.data(), sizeof(double*) * np, cudaMemcpyHostToDevice));
+  const int sigma = cfg->sigma, k = 2 * sigma + 1;
+  const int npack = k * (k + 1) / 2 + 2;
+  for (int i = 0; i < np; ++i) {
+    launch_init_residual(cs[i], plans[i]->d_x0, s);
+    launch_norm_pack(cs[i], s);
+  }
+  launch_vsum(d_reds, np, 1, s);
+  for (int i = 0; i < np; ++i) launch_state_init(cs[i], s);
+  int rc = SSCG_OK;
+  int launched = 0;
+  for (int outer = 0; outer <= cfg->max_outer && !rc; ++outer) {
+    // halo: pack on every member, device copies peer -> peer, unpack
+    for (int i = 0; i < np && !rc; ++i) rc = halo_exchange(plans[i]->halo, cs[i], nullptr, s);
+    for (int i = 0; i < np && !rc; ++i) {
+      const HaloPlan& h = plans[i]->halo;
+      for (int q = 0; q < h.n_peers && !rc; ++q) {
+        const int j = h.peer_rank[q];
+        const HaloPlan& hj = plans[j]->halo;
+        int qi = -1;
+        for (int t = 0; t < hj.n_peers; ++t)
+          if (hj.peer_rank[t] == i) qi = t;
+        const int64_t n = h.recv_off[q + 1] - h.recv_off[q];
+        if (qi < 0 || hj.send_off[qi + 1] - hj.send_off[qi] != n) {
+          rc = sscg_fail(SSCG_EINVAL, "halo lists of members %d and %d disagree", i, j);
+          break;
+        }
+        if (n) {
+          cudaError_t e = cudaMemcpyAsync(h.d_recvbuf + 3 * h.recv_off[q], hj.d_sendbuf + 3 * hj.send_off[qi],
+                                          sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s);
+          if (e != cudaSuccess) rc = sscg_fail_cuda(e, "halo copy");
+        }
+      }
+    }
+    if (rc) break;
+    for (int i = 0; i < np; ++i) halo_unpack(plans[i]->halo, cs[i], s);
+    for (int i = 0; i < np; ++i) {
+      launch_params_begin(cs[i], s);
+      for (int n = 2; n < sigma; ++n) launch_leja_point(cs[i], n, s);
+      for (int l = 0; l < sigma; ++l) launch_level(cs[i], l, s);
+      launch_gram(cs[i], k, s);
+    }
+    launch_vsum(d_reds, np, npack, s);
+    for (int i = 0; i < np; ++i) {
+      launch_small(cs[i], s);
+      launch_recover(cs[i], s);
+    }
+    ++launched;
+    int done = 0;
+    cudaError_t e = cudaMemcpyAsync(plans[0]->h_done, &plans[0]->d_st->done, sizeof(int),
+                                    cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      rc = sscg_fail_cuda(e, "virtual group step");
+      break;
+    }
+    done = plans[0]->h_done[0];
+    if (done) break;
+  }
+  cudaFree(d_reds);
+  if (rc) return rc;
+  CUDA_OK(cudaGetLastError());
+  for (int i = 0; i < np; ++i) plans[i]->last_launched = launched;
+  if (logs0) TRY(sscg_fetch(plans[0], nullptr, logs0));
   return SSCG_OK;
 }
 

@@ -13,6 +13,12 @@ namespace {
 
 constexpr int REC_THREADS = 256;
 
+// rows recovery updates: single GPU the whole padded column (padding stays 0);
+// row-partitioned: the owned rows (ghosts are refreshed by the next exchange)
+__device__ __forceinline__ int64_t rec_rows(const Ctx& c) {
+  return c.n_own == c.n ? c.ld : ((c.n_own + 1) & ~(int64_t)1);
+}
+
 struct ColSet {
   int n;
   int col[CMAX];
@@ -64,8 +70,9 @@ __global__ void __launch_bounds__(REC_THREADS) k_recover(Ctx c) {
   __syncthreads();
   double* P0 = c.Y;
   double* R0 = c.Y + (int64_t)(sigma + 1) * c.ld;
+  const int64_t lim = rec_rows(c);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2;
-  for (int64_t i2 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; i2 < c.ld; i2 += stride) {
+  for (int64_t i2 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; i2 < lim; i2 += stride) {
     double2 ax, ar, ap;
     combine<true>(c.Y, c.ld, i2, k, cols, sx_, sr_, sp_, ax, ar, ap);
     double2 xv = *reinterpret_cast<const double2*>(c.x + i2);
@@ -91,8 +98,9 @@ __global__ void __launch_bounds__(REC_THREADS) k_diag_form(Ctx c, int j) {
     sr_[threadIdx.x] = st->dr[j][threadIdx.x];
   }
   __syncthreads();
+  const int64_t lim = rec_rows(c);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2;
-  for (int64_t i2 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; i2 < c.ld; i2 += stride) {
+  for (int64_t i2 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; i2 < lim; i2 += stride) {
     double2 ax, ar, ap;
     combine<false>(c.Y, c.ld, i2, k, cols, sx_, sr_, nullptr, ax, ar, ap);
     double2 xv = *reinterpret_cast<const double2*>(c.x + i2);

@@ -1,0 +1,146 @@
+"""Row-partitioned adaptive s-step CG: host driver.
+
+Two ways to run the partitioned algorithm:
+
+* `solve_partitioned(rows, b, x0, cfg, rank, world, ...)` -- one process per GPU
+  (torchrun): this rank builds its slab + ghost zones (partition.py), the
+  ranks agree on an NCCL unique id over torch.distributed (plumbing only), and
+  the C library runs every outer loop as one CUDA graph containing one grouped
+  NCCL halo exchange and one NCCL allreduce.
+* `VirtualGroup` -- all ranks' plans in ONE process on one GPU, driven in lock
+  step with device copies for the halo and a fixed-order sum for the
+  allreduce: the multi-rank kernels and partition exercised on a single GPU.
+
+Every rank computes identical decisions (bitwise-identical reduced Gram), so
+the trace returned on each rank is the same.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+from .adaptive import LogBuffers, build_trace, make_config
+from .partition import partition_all, partition_rank
+
+
+def _part_struct(part, rank, world, nccl_id=None, nccl_lib=None):
+    keep = dict(
+        row_ptr=np.ascontiguousarray(part.row_ptr, dtype=np.int64),
+        col_idx=np.ascontiguousarray(part.col_idx, dtype=np.int32),
+        values=np.ascontiguousarray(part.values, dtype=np.float64),
+        lvl=np.ascontiguousarray(part.lvl_rows, dtype=np.int64),
+        peers=np.ascontiguousarray(part.peers, dtype=np.int32),
+        so=np.ascontiguousarray(part.send_off, dtype=np.int64),
+        ro=np.ascontiguousarray(part.recv_off, dtype=np.int64),
+        si=np.ascontiguousarray(part.send_idx, dtype=np.int32),
+        ri=np.ascontiguousarray(part.recv_idx, dtype=np.int32),
+    )
+    s = L.SscgPart()
+    s.n_own, s.n_rows, s.n_local = part.n_own, part.n_rows, part.n_local
+    s.nnz = len(keep["values"])
+    s.depth, s.rank, s.world, s.n_peers = part.depth, rank, world, len(part.peers)
+    i64 = C.POINTER(C.c_int64)
+    s.row_ptr = keep["row_ptr"].ctypes.data_as(i64)
+    s.col_idx = L.iptr(keep["col_idx"])
+    s.values = L.dptr(keep["values"])
+    s.lvl_rows = keep["lvl"].ctypes.data_as(i64)
+    s.peer_rank = L.iptr(keep["peers"])
+    s.send_off = keep["so"].ctypes.data_as(i64)
+    s.recv_off = keep["ro"].ctypes.data_as(i64)
+    s.send_idx = L.iptr(keep["si"])
+    s.recv_idx = L.iptr(keep["ri"])
+    if nccl_id is not None:
+        keep["id"] = C.create_string_buffer(bytes(nccl_id), 128)
+        s.nccl_id = C.cast(keep["id"], C.c_void_p)
+    s.nccl_lib = nccl_lib.encode() if nccl_lib else None
+    return s, keep
+
+
+class PartPlan:
+    """One rank's device plan (owns the sscg_plan handle)."""
+
+    def __init__(self, part, rank, world, device=0, nccl_id=None, nccl_lib=None):
+        lib = L.load()
+        L.require_device(device)
+        s, keep = _part_struct(part, rank, world, nccl_id, nccl_lib)
+        h = C.c_void_p()
+        L.check(lib.sscg_plan_create_part(C.byref(h), int(device), C.byref(s)))
+        self.handle, self.part, self._lib, self._keep = h, part, lib, keep
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self._lib.sscg_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _local_vectors(part, b_global, x0_global):
+    b = np.ascontiguousarray(b_global[part.row_lo:part.row_hi], dtype=np.float64)
+    x0 = np.ascontiguousarray(x0_global[part.global_rows], dtype=np.float64)
+    return b, x0
+
+
+class VirtualGroup:
+    """All `world` ranks of a partitioned solve as plans in this process."""
+
+    def __init__(self, rows, world, depth, device=0):
+        self.parts = partition_all(rows, world, depth)
+        self.plans = [PartPlan(p, r, world, device) for r, p in enumerate(self.parts)]
+        self.world = world
+
+    def solve(self, problem, cfg):
+        cfg, ccfg = make_config(cfg, problem, "fast")
+        bs, xs = zip(*[_local_vectors(p, problem.b, problem.x0) for p in self.parts])
+        vp = C.c_void_p * self.world
+        handles = vp(*[pl.handle.value for pl in self.plans])
+        bp = (L._DP * self.world)(*[L.dptr(v) for v in bs])
+        xp = (L._DP * self.world)(*[L.dptr(v) for v in xs])
+        logs = LogBuffers(cfg)
+        L.check(L.load().sscg_vgroup_run(C.cast(handles, C.POINTER(C.c_void_p)), self.world, ccfg,
+                                         bp, xp, logs.s))
+        x = np.empty(problem.a.n)
+        for pl, part in zip(self.plans, self.parts):
+            xo = np.empty(part.n_own)
+            L.check(L.load().sscg_fetch(pl.handle, L.dptr(xo), None))
+            x[part.row_lo:part.row_hi] = xo
+        tr, co = build_trace(cfg, logs, "fast")
+        return x, tr, co, logs
+
+
+def solve_partitioned(rows, problem_scalars, b_global, x0_global, cfg, rank, world, device,
+                      exchange, broadcast_bytes, nccl_lib=None, info=None):
+    """This rank's share of a multi-process partitioned solve (torchrun).
+
+    rows: row access to the global operator (partition.CsrRows / Stencil7Rows);
+    exchange(obj) -> list of every rank's obj; broadcast_bytes(b or None) -> the
+    128-byte NCCL id from rank 0.  Returns (x_owned, trace, coeffs, plan)."""
+    from .build import nccl_library
+
+    depth = cfg.sigma
+    part = partition_rank(rows, rank, world, depth, exchange)
+    lib = L.load()
+    nccl_lib = nccl_lib or nccl_library()
+    uid = None
+    if rank == 0:
+        buf = C.create_string_buffer(128)
+        L.check(lib.sscg_nccl_unique_id(nccl_lib.encode(), buf))
+        uid = bytes(buf.raw)
+    uid = broadcast_bytes(uid)
+    plan = PartPlan(part, rank, world, device, nccl_id=uid, nccl_lib=nccl_lib)
+    cfg, ccfg = make_config(cfg, problem_scalars, "fast")
+    b, x0 = _local_vectors(part, b_global, x0_global)
+    logs = LogBuffers(cfg)
+    xo = np.empty(part.n_own)
+    L.check(lib.sscg_solve(plan.handle, ccfg, L.dptr(b), L.dptr(x0), L.dptr(xo), logs.s))
+    tr, co = build_trace(cfg, logs, "fast")
+    if isinstance(info, dict):
+        info.update(plan=plan, part=part, logs=logs, ccfg=ccfg, b=b, x0=x0)
+    return xo, tr, co, plan
