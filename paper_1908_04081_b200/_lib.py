@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libsscg.so")
+LIB_PATH = os.environ.get("SSCG_LIB") or os.path.join(HERE, "_lib", "libsscg.so")
 
 # keep in sync with include/sscg.h
 ABI_VERSION = 1

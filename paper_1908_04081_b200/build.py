@@ -71,39 +71,42 @@ def _digest():
     return h.hexdigest()
 
 
-def build(force=False, verbose=False):
-    """Compile (if sources changed) and return the path of libsscg.so."""
+def build(force=False, verbose=False, out=None, defines=()):
+    """Compile (if sources changed) and return the path of libsscg.so
+    (`out` / `defines`: side builds of experimental variants)."""
     os.makedirs(OUT_DIR, exist_ok=True)
-    stamp = os.path.join(OUT_DIR, "libsscg.sha256")
-    dig = _digest()
-    if not force and os.path.exists(LIB) and os.path.exists(stamp):
+    lib_path = out or LIB
+    stamp = lib_path + ".sha256" if out else os.path.join(OUT_DIR, "libsscg.sha256")
+    dig = _digest() + "".join(defines)
+    if not force and os.path.exists(lib_path) and os.path.exists(stamp):
         with open(stamp) as f:
             if f.read().strip() == dig:
-                return LIB
+                return lib_path
     cc = nvcc()
     objs = []
     base = [cc, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE,
-            "-I", nccl_include(), "--expt-relaxed-constexpr"] + ARCH
+            "-I", nccl_include(), "--expt-relaxed-constexpr"] + ARCH + ["-D" + d for d in defines]
     for src in SOURCES:
-        obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
+        obj = os.path.join(OUT_DIR, (os.path.basename(lib_path) + "." if out else "") +
+                           src.replace(".cu", ".o"))
         cmd = base + (["-fmad=false"] if src in NO_FMAD else []) + [
             "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [cc, "-shared", "-o", tmp] + objs + ARCH + ["-cudart", "static", "-ldl",
                                                        "-Xlinker", "--no-undefined"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib_path)
     for o in objs:
         os.remove(o)
     with open(stamp, "w") as f:
         f.write(dig)
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
