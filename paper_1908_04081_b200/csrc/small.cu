@@ -401,9 +401,11 @@ __device__ double warp_cond_estimate(double* A, int n, double* scratch, bool dup
   // reported at LAPACK's noise level: 2^-60 ||T|| -> ~2^-61 ||T||, the median of
   // lambda_min / (lambda_max ulp) (2.5e-3) LAPACK returns for those directions on
   // the reference's golden fixtures (oracle/make_golden.py conds8).  Elsewhere
-  // the floor (2^-80 ||T||) only guarantees termination: noise-level eigenvalues
-  // keep their own magnitude, as LAPACK's do.
-  const double abs_tol = (dup_floor ? 8.673617379884035e-19 : 8.271806125530277e-25) * span;
+  // the floor (2^-160 ||T||) only guarantees termination: noise-level eigenvalues
+  // keep their own magnitude, as LAPACK's do -- including its long tail toward
+  // 0 (5% of its saturated estimates are below 1e-26 ulp); a higher cap would
+  // make numerically rank-deficient blocks look admissible (measured on c4p).
+  const double abs_tol = (dup_floor ? 8.673617379884035e-19 : 6.842277657836021e-49) * span;
   const double* e2 = v;
   // three searches at once, 10 lanes each: lambda_max and the eigenvalues
   // straddling 0 (lacore.py:111-117 needs lambda_max and the smallest |lambda|)
