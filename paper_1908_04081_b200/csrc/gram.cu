@@ -24,7 +24,8 @@ namespace {
 constexpr int GT_ROWS = 128;
 constexpr int GT_STAGES = 4;
 constexpr int GT_LD = GT_ROWS + 4;  // LD % 16 == 4: conflict-free fragment loads
-constexpr int GT_THREADS = 256;
+constexpr int GT_CONSUMERS = 8;                    // DMMA warps (16 rows of a tile each)
+constexpr int GT_THREADS = (GT_CONSUMERS + 1) * 32;  // + one TMA producer warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -44,6 +45,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           "r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0, spins = 0;
@@ -99,67 +103,70 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
     for (int cb = 0; cb <= NB; ++cb) accr[a][cb] = 0.0;
 
   const int kc = k < NC ? k : NC;
-  __shared__ __align__(8) uint64_t bars[GT_STAGES];
+  // warp-specialised pipeline: warp GT_CONSUMERS produces (TMA bulk copies into
+  // stage s after `empty[s]` completes), warps 0..7 consume (wait `full[s]`,
+  // DMMA, arrive on `empty[s]`) -- no CTA-wide barrier per tile
+  __shared__ __align__(8) uint64_t full[GT_STAGES], empty[GT_STAGES];
   if (tid == 0) {
-    for (int st = 0; st < GT_STAGES; ++st) mbar_init(&bars[st], 1);
+    for (int st = 0; st < GT_STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], GT_CONSUMERS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  // one elected thread moves a tile: kc bulk copies of GT_ROWS doubles (1 KB)
-  auto issue = [&](int64_t tile, int stage) {
-    double* dst = tiles + (size_t)stage * NC * GT_LD;
-    const double* src = Y + tile * GT_ROWS;
-    mbar_arrive_tx(&bars[stage], (uint32_t)(kc * GT_ROWS * sizeof(double)));
-    for (int cc = 0; cc < kc; ++cc)
-      bulk_g2s(dst + cc * GT_LD, src + (int64_t)cc * ld, GT_ROWS * sizeof(double), &bars[stage]);
-  };
-  if (tid == 0)
-    for (int st = 0; st < GT_STAGES; ++st) {
-      const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
-      if (t < ntiles) issue(t, st);
+  if (warp == GT_CONSUMERS) {
+    if (lane == 0) {
+      int64_t kk = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++kk) {
+        const int stage = (int)(kk % GT_STAGES);
+        if (kk >= GT_STAGES) mbar_wait(&empty[stage], (uint32_t)(((kk / GT_STAGES) - 1) & 1));
+        double* dst = tiles + (size_t)stage * NC * GT_LD;
+        const double* src = Y + tile * GT_ROWS;
+        mbar_arrive_tx(&full[stage], (uint32_t)(kc * GT_ROWS * sizeof(double)));
+        for (int cc = 0; cc < kc; ++cc)
+          bulk_g2s(dst + cc * GT_LD, src + (int64_t)cc * ld, GT_ROWS * sizeof(double), &full[stage]);
+      }
     }
-  int64_t kk = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++kk) {
-    const int stage = (int)(kk % GT_STAGES);
-    mbar_wait(&bars[stage], (uint32_t)((kk / GT_STAGES) & 1));
-    const double* ts = tiles + (size_t)stage * NC * GT_LD;
-    const int64_t valid = nrows - tile * GT_ROWS;  // rows of this tile below nrows
-    // 8 warps x 16 rows = 128 rows: four k-steps of 4 rows per warp
+  } else {
+    int64_t kk = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++kk) {
+      const int stage = (int)(kk % GT_STAGES);
+      mbar_wait(&full[stage], (uint32_t)((kk / GT_STAGES) & 1));
+      const double* ts = tiles + (size_t)stage * NC * GT_LD;
+      const int64_t valid = nrows - tile * GT_ROWS;  // rows of this tile below nrows
+      // 8 warps x 16 rows = 128 rows: four k-steps of 4 rows per warp
 #pragma unroll
-    for (int ks = 0; ks < GT_ROWS / 32; ++ks) {
-      const int row0 = warp * (GT_ROWS / 8) + ks * 4;
-      const bool live = row0 + t4 < valid;
-      double fr[NB > 0 ? NB : 1];
+      for (int ks = 0; ks < GT_ROWS / 32; ++ks) {
+        const int row0 = warp * (GT_ROWS / 8) + ks * 4;
+        const bool live = row0 + t4 < valid;
+        double fr[NB > 0 ? NB : 1];
 #pragma unroll
-      for (int cb = 0; cb < NB; ++cb) fr[cb] = live ? ts[(cb * 8 + g) * GT_LD + row0 + t4] : 0.0;
-      int q = 0;
+        for (int cb = 0; cb < NB; ++cb) fr[cb] = live ? ts[(cb * 8 + g) * GT_LD + row0 + t4] : 0.0;
+        int q = 0;
 #pragma unroll
-      for (int i = 0; i < NB; ++i)
+        for (int i = 0; i < NB; ++i)
 #pragma unroll
-        for (int j = 0; j <= i; ++j, ++q) dmma(acc[q][0], acc[q][1], fr[i], fr[j]);
-      if (REM > 0) {
+          for (int j = 0; j <= i; ++j, ++q) dmma(acc[q][0], acc[q][1], fr[i], fr[j]);
+        if (REM > 0) {
 #pragma unroll
-        for (int a = 0; a < REM; ++a) {
-          const double yr = live ? ts[(NB * 8 + a) * GT_LD + row0 + t4] : 0.0;
+          for (int a = 0; a < REM; ++a) {
+            const double yr = live ? ts[(NB * 8 + a) * GT_LD + row0 + t4] : 0.0;
 #pragma unroll
-          for (int cb = 0; cb < NB; ++cb) accr[a][cb] = fma(yr, fr[cb], accr[a][cb]);
-          // remainder x remainder (columns NB*8 .. NB*8+a), lanes g <= a
-          if (g <= a) {
-            const double yb = live ? ts[(NB * 8 + g) * GT_LD + row0 + t4] : 0.0;
-            accr[a][NB] = fma(yr, yb, accr[a][NB]);
+            for (int cb = 0; cb < NB; ++cb) accr[a][cb] = fma(yr, fr[cb], accr[a][cb]);
+            // remainder x remainder (columns NB*8 .. NB*8+a), lanes g <= a
+            if (g <= a) {
+              const double yb = live ? ts[(NB * 8 + g) * GT_LD + row0 + t4] : 0.0;
+              accr[a][NB] = fma(yr, yb, accr[a][NB]);
+            }
           }
         }
       }
-    }
-    __syncthreads();  // stage free again
-    if (tid == 0) {
-      const int64_t t = tile + (int64_t)GT_STAGES * gridDim.x;
-      if (t < ntiles) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        issue(t, stage);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
     }
   }
+  __syncthreads();
 
   // remainder partials: sum over the 4 row lanes (t4) of each g
   if (REM > 0) {
@@ -174,7 +181,7 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
       }
   }
   // combine warps in fixed order: red[q][g*8 + 2 t4 + e], redr[a][col]
-  for (int w = 0; w < GT_THREADS / 32; ++w) {
+  for (int w = 0; w < GT_CONSUMERS; ++w) {
     if (warp == w) {
 #pragma unroll
       for (int q = 0; q < T; ++q) {
