@@ -27,7 +27,9 @@
 #define ROWS_PER_CTA 256
 #define RED_BLOCKS (NUM_SMS * 8)   // capacity of the per-CTA partial-sum arrays
 #define MT_ROWS 256                 // rows per staged CSR tile (= threads per CTA)
+#ifndef MT_STAGES
 #define MT_STAGES 2                 // TMA double buffering of CSR tiles
+#endif
 #define GRAM_BLOCKS (2 * NUM_SMS)  // capacity of the Gram partials
 #define SMALL_THREADS 512
 
