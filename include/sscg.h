@@ -199,6 +199,14 @@ int sscg_get_profile(const sscg_plan* plan, double* ms5, int64_t* counts5);
  * [0] classify [1] Gram extract + c [2] nested conds [3] s~ + truncation
  * [4] inner loop + record [5] next-block parameters [6] unused [7] calls */
 int sscg_get_small_phases(const sscg_plan* plan, int64_t* cycles8);
+/* Matrix-powers schedule the plan uses for a given sigma:
+ * out[0] 0 = one CSR launch per level, 1 = wavefront passes (SSCG_WAVE=1),
+ *        2 = one pattern-compressed launch per level (the default when A's rows
+ *        reduce to a small pattern table; SSCG_PATTERN=0 disables);
+ * out[1] CTAs; out[2] wavefront dependency reach in row tiles, or the number
+ * of row patterns; out[3] passes P; then for q < P: out[4+2q] levels in pass
+ * q, out[5+2q] tile lag D of pass q.  out: 4+2*SSCG_MAX_SIGMA int32. */
+int sscg_plan_mpk_schedule(sscg_plan* plan, int32_t sigma, int32_t* out);
 
 /* ---- unit entry points (parity tests; one kernel family each) ------------- */
 /* lacore.py:25-34 spmv: y = A x (scipy csr_matvec rounding, bit for bit) */

@@ -35,6 +35,7 @@ EXPORTS = (
     "sscg_last_error", "sscg_abi_version", "sscg_device_count", "sscg_plan_create",
     "sscg_plan_destroy", "sscg_plan_device_bytes", "sscg_solve", "sscg_load", "sscg_run",
     "sscg_fetch", "sscg_set_profiling", "sscg_get_profile", "sscg_get_small_phases",
+    "sscg_plan_mpk_schedule",
     "sscg_spmv", "sscg_build_block",
     "sscg_gram", "sscg_recover", "sscg_nested_conds", "sscg_select_s_tilde",
     "sscg_leja_points", "sscg_params_for", "sscg_ritz_sequence", "sscg_sym_eig",
@@ -108,6 +109,7 @@ def _declare(lib):
         "sscg_set_profiling": (C.c_int, [vp, i32]),
         "sscg_get_profile": (C.c_int, [vp, _DP, C.POINTER(i64)]),
         "sscg_get_small_phases": (C.c_int, [vp, C.POINTER(i64)]),
+        "sscg_plan_mpk_schedule": (C.c_int, [vp, i32, _IP]),
         "sscg_spmv": (C.c_int, [vp, _DP, _DP]),
         "sscg_build_block": (C.c_int, [vp, _DP, _DP, i32, _DP, _DP, _DP, _DP, _DP]),
         "sscg_gram": (C.c_int, [i32, i64, i32, _DP, _DP]),
@@ -209,3 +211,16 @@ class Plan:
         v = C.c_int64(0)
         check(self._lib.sscg_plan_device_bytes(self.handle, C.byref(v)))
         return v.value
+
+    def mpk_schedule(self, sigma):
+        """Matrix-powers schedule for `sigma` (sscg_plan_mpk_schedule):
+        {"kind": "csr"|"wavefront"|"pattern", "wavefront": bool, "ctas": G,
+         "reach_tiles": L (wavefront), "patterns": P (pattern), "passes": [(levels, lag), ...]}."""
+        out = np.zeros(4 + 2 * 16, dtype=np.int32)
+        check(self._lib.sscg_plan_mpk_schedule(self.handle, int(sigma), iptr(out)))
+        npass = int(out[3])
+        kind = ("csr", "wavefront", "pattern")[int(out[0])]
+        return {"kind": kind, "wavefront": kind == "wavefront", "ctas": int(out[1]),
+                "reach_tiles": int(out[2]) if kind == "wavefront" else 0,
+                "patterns": int(out[2]) if kind == "pattern" else 0,
+                "passes": [(int(out[4 + 2 * q]), int(out[5 + 2 * q])) for q in range(npass)]}

@@ -30,6 +30,8 @@
 #ifndef MT_STAGES
 #define MT_STAGES 2                 // TMA double buffering of CSR tiles
 #endif
+#define WAVE_GROUP 4                // tiles per completion counter (wavefront MPK)
+#define WAVE_THREADS (MT_ROWS + 32) // 8 consumer warps + 1 producer warp
 #define GRAM_BLOCKS (2 * NUM_SMS)  // capacity of the Gram partials
 #define SMALL_THREADS 512
 
@@ -119,6 +121,17 @@ struct Ctx {
   int64_t n_own;                // owned rows: Gram, recovery, residual norms
   int64_t lvl_rows[SMAX + 1];   // lvl_rows[d] = local rows with ghost depth <= d
   double* red_buf;  // [GPACK + 2] packed Gram + ||b-Ax||^2 + ||r||^2 (allreduced)
+  // pattern-compressed operator (plan.cu pattern_setup; NULL pid: CSR kernels).
+  // Row i is pattern pid[i]: entries pat_ptr[p] .. pat_ptr[p+1] of
+  // (pat_off, pat_val), column = i + pat_off -- A's exact columns, values and
+  // stored order, at 1-2 bytes per row instead of 12 per nonzero.
+  const void* pid;
+  int pid_bytes;     // 1 (<= 256 patterns) or 2
+  int pat_np, pat_ne;
+  int pat_grid;      // CTAs of the pattern kernels of levels >= 1 (level 0: red_n)
+  const int* pat_ptr;
+  const int* pat_off;
+  const double* pat_val;
 };
 
 // rows level l must produce for P (ghost depth <= sigma-1-l) and R (<= sigma-2-l)
@@ -130,6 +143,17 @@ __host__ __device__ inline int64_t lvl_r_rows(const Ctx& c, int sigma, int l) {
   const int d = sigma - 2 - l;
   return c.lvl_rows[d < 0 ? 0 : d];
 }
+
+// one pass of the wavefront matrix-powers kernel (mpk.cu k_mpk_wave)
+struct WaveArgs {
+  int l0, nl;         // levels l0 .. l0+nl-1
+  int D;              // tile lag between consecutive levels
+  int ngroups;        // counters per level
+  int64_t nF;         // wavefront steps: tiles(l0) + (nl - 1) D
+  int* cnt;           // [SMAX][ngroups] finished tiles per WAVE_GROUP tiles
+  unsigned int* claim;  // position counter of this pass
+  const int2* dep;    // [tiles] monotone input-tile range of each row tile
+};
 
 // halo exchange lists of a row-partitioned plan (dist.cu)
 struct HaloPlan {
@@ -169,8 +193,13 @@ void launch_block_levels(const int* rp, const int* col, const double* val, int64
                          int* breakdown, cudaStream_t st);
 void launch_diag_resid(const Ctx& c, int j, cudaStream_t s);
 size_t staged_smem_bytes(int cap);
+size_t pattern_smem_bytes(int np, int ne);
+void pattern_prepare();
+int pattern_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 void staged_prepare(int cap);
 int staged_ctas_per_sm(int cap);
+int wave_ctas_per_sm(int cap);
+cudaError_t launch_wave(const Ctx& c, const WaveArgs& a, int grid, cudaStream_t s);
 // gram.cu (ld must be a multiple of gram_row_multiple(); padding rows zero)
 int gram_row_multiple();
 void launch_gram(const Ctx& c, int ncols, cudaStream_t s);

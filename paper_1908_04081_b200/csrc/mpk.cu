@@ -135,6 +135,15 @@ __host__ __device__ __forceinline__ size_t stage_bytes(int cap) {
   return ((size_t)(cap + 2) * 8 + (size_t)(cap + 4) * 4 + 15) / 16 * 16;
 }
 
+// wavefront stages also carry the tile's row_ptr[r0 .. r0 + MT_ROWS] (+ pad)
+#define WAVE_RP_BYTES ((MT_ROWS + 4) * 4)
+#ifndef WAVE_BATCH
+#define WAVE_BATCH 8  // a 7-point row's gathers in one round
+#endif
+__host__ __device__ __forceinline__ size_t wave_stage_bytes(int cap) {
+  return stage_bytes(cap) + WAVE_RP_BYTES;
+}
+
 // Runs fn(row, TileStage&) over rows [0, nrows) tile by tile.
 template <class Fn>
 __device__ __forceinline__ void staged_rows(const Ctx& c, int64_t nrows, Fn&& fn) {
@@ -192,28 +201,49 @@ __device__ __forceinline__ void staged_rows(const Ctx& c, int64_t nrows, Fn&& fn
   }
 }
 
-template <int NV>
+// gathers of vectors that are read-only for the whole launch
+struct LdNc {
+  static __device__ __forceinline__ double ld(const double* p) { return __ldg(p); }
+};
+// gathers of vectors other CTAs of the same launch produced (wavefront kernel):
+// coherent loads only, never the non-coherent read-only path
+struct LdCa {
+  static __device__ __forceinline__ double ld(const double* p) { return __ldca(p); }
+};
+
+#ifndef ROW_BATCH
+#define ROW_BATCH 4
+#endif
+// Row sums from a staged tile.  The gathers of a chunk of up to B nonzeros are
+// all issued before the chunk is accumulated -- B x NV loads in flight per
+// thread instead of a chain of dependent load rounds -- and the adds then run
+// strictly in stored order (a lane past the row end adds nothing, not +0.0,
+// so even the sign of a zero sum is csr_matvec's).
+template <int NV, class LD = LdNc, int B = (NV >= 3 ? (ROW_BATCH + 1) / 2 : ROW_BATCH)>
 __device__ __forceinline__ void row_dot_s(const TileStage& ts, int beg, int end,
                                           const double* const* __restrict__ xs, double* acc) {
 #pragma unroll
   for (int q = 0; q < NV; ++q) acc[q] = 0.0;
   const double* vv = ts.val - ts.beg_v;
   const int* cc = ts.col - ts.beg_c;
-  int jj = beg;
-  for (; jj + 2 <= end; jj += 2) {
-    const int c0 = cc[jj], c1 = cc[jj + 1];
-    const double v0 = vv[jj], v1 = vv[jj + 1];
+  for (int jj = beg; jj < end; jj += B) {
+    const int m = end - jj;
+    int cb[B];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      const double x0 = __ldg(xs[q] + c0), x1 = __ldg(xs[q] + c1);
-      acc[q] = __dadd_rn(__dadd_rn(acc[q], __dmul_rn(v0, x0)), __dmul_rn(v1, x1));
+    for (int k = 0; k < B; ++k) cb[k] = cc[jj + (k < m ? k : 0)];
+    double xb[NV][B];
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int k = 0; k < B; ++k) xb[q][k] = LD::ld(xs[q] + cb[k]);
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (k < m) {
+        const double v = vv[jj + k];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v, xb[q][k]));
+      }
     }
-  }
-  if (jj < end) {
-    const int c0 = cc[jj];
-    const double v0 = vv[jj];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v0, __ldg(xs[q] + c0)));
   }
 }
 
@@ -299,6 +329,503 @@ __global__ void __launch_bounds__(MT_ROWS) k_level_staged(Ctx c, int l) {
       bad |= !finite(wr);
     }
   });
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Wavefront matrix-powers pass: levels l0 .. l0+nl-1 of the block in ONE
+// persistent launch, so each CSR tile (and each freshly generated basis row) is
+// re-read from L2 instead of HBM by the later levels of the pass.
+//
+// Work item (l, t) = level l on row tile t.  It needs level l-1 on the tiles
+// dep[t] = [lo, hi] its rows' columns touch (host-computed from the CSR, made
+// monotone in t).  Items are ordered by F = t + (l - l0) * D, then l; with the
+// lag D > max(hi - t) every dependency comes strictly earlier in that order.
+// CTAs are co-resident (grid <= occupancy x SMs) and claim positions in order
+// from one atomic counter per pass, so any item a CTA waits on was claimed by
+// a running CTA that only waits on even earlier items: no deadlock.  Dynamic
+// claiming (not a static round robin) keeps CTAs from drifting apart: an item
+// claimed Delta positions earlier also STARTED about Delta / G item-times
+// earlier.  D carries slack (~6 G / nl tiles, twice the items in flight) so a
+// dependency is normally complete when it is checked.
+//
+// Completion: per level, one counter per WAVE_GROUP tiles (zeroed by a memset
+// node every outer loop).  Row arithmetic is the level kernels', so the basis
+// is bit-identical to the level-by-level path.
+//
+// Warp roles (WAVE_THREADS = 8 consumer warps + 1 producer warp):
+//  * the producer enumerates this CTA's items, checks their dependencies
+//    (acquire loads of the counters; it remembers per level how far it has
+//    verified -- dep ranges are monotone and a CTA's items of one level come in
+//    increasing t), stages the tile's CSR by TMA into a free buffer and arrives
+//    on full[s]; it publishes an item's completion (release add) once the
+//    consumers have arrived on empty[s].  It publishes finished items ALSO
+//    while spinning on a dependency: an item some other CTA waits for must
+//    never sit unpublished behind a wait of ours (that could close a cycle).
+//  * consumers wait on full[s], compute one row each, arrive on empty[s]; no
+//    CTA-wide barrier on the per-item path.
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+// named barrier over the consumer warps only
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"r"(MT_ROWS) : "memory");
+}
+
+#ifdef WAVE_DBG
+// side-build instrumentation (tools/wave_sweep.py --dbg): [0] consumer cycles
+// waiting on full, [1] consumer loop cycles, [2] consumer items (warp 0),
+// [3] producer dep-wait cycles, [4] producer stage-wait cycles, [5] producer
+// row_ptr cycles, [6] producer loop cycles, [7] dep-wait spin rounds
+__device__ unsigned long long g_wave_dbg[8];
+#define WDBG(...) __VA_ARGS__
+#else
+#define WDBG(...)
+#endif
+
+__global__ void __launch_bounds__(WAVE_THREADS, 4) k_mpk_wave(Ctx c, WaveArgs a) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  __shared__ __align__(8) uint64_t full[MT_STAGES], empty[MT_STAGES];
+  __shared__ int tb[MT_STAGES][2];
+  __shared__ int titem[MT_STAGES][2];  // (level, tile) staged in each buffer; level -1: stop
+  __shared__ int vhi[SMAX];            // producer: per input level, groups [.., vhi] verified
+  __shared__ double sm[MT_ROWS / 32];
+  __shared__ long long ntl[SMAX];      // tiles of each level of the pass (CA-MPK prefix rows)
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  const int sigma = c.cfg->sigma;
+  const int l0 = a.l0;
+  const int lend = (l0 + a.nl < sbar) ? l0 + a.nl : sbar;  // levels >= s_bar: nothing to build
+  if (l0 >= lend) return;
+  const int tid = threadIdx.x;
+  const int cap = c.stage_cap;
+  const size_t sb = wave_stage_bytes(cap);
+  if (tid < SMAX) {
+    ntl[tid] = (tid < a.nl) ? (lvl_p_rows(c, sigma, l0 + tid) + MT_ROWS - 1) / MT_ROWS : 0;
+    vhi[tid] = -1;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < MT_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MT_ROWS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (tid >= MT_ROWS) {  // ---------------- producer warp
+    const int lane = tid & 31;
+    const int64_t npos = a.nF * a.nl;
+    int64_t issued = 0, pub = 0;  // items staged / items whose completion is published
+    WDBG(unsigned long long d_dep = 0, d_stage = 0, d_rp = 0, d_spin = 0; const long long d_t0 = clock64();)
+    // publish item m (stage m % S) once its consumers are done; block or poll
+    auto publish = [&](bool block) {
+      while (pub < issued) {
+        const int s = (int)(pub % MT_STAGES);
+        const uint32_t par = (uint32_t)((pub / MT_STAGES) & 1);
+        if (block)
+          mbar_wait(&empty[s], par);
+        else if (!mbar_test(&empty[s], par))
+          return;
+        const int l = titem[s][0];
+        if (lane == 0 && l + 1 < lend)
+          red_release_add(a.cnt + (int64_t)l * a.ngroups + titem[s][1] / WAVE_GROUP, 1);
+        ++pub;
+      }
+    };
+    for (;;) {
+      int il = -1;
+      int64_t it = 0;
+      for (;;) {  // claim the next position of the pass; skip the empty ones
+        unsigned int w = 0;
+        if (lane == 0) w = atomicAdd(a.claim, 1u);
+        const int64_t wpos = (int64_t)__shfl_sync(0xffffffffu, w, 0);
+        if (wpos >= npos) break;
+        const int64_t F = wpos / a.nl;
+        const int li = (int)(wpos - F * a.nl);
+        const int64_t t = F - (int64_t)li * a.D;
+        if (l0 + li < lend && t >= 0 && t < ntl[li]) {
+          il = l0 + li;
+          it = t;
+          break;
+        }
+      }
+      if (il > l0) {  // wait for level il-1 on the dep tiles, publishing meanwhile
+        const int2 d = a.dep[it];
+        const int64_t nprev = ntl[il - 1 - l0];
+        const int64_t hi_t = d.y < nprev ? d.y : nprev - 1;
+        const int ghi = (int)(hi_t / WAVE_GROUP);
+        const int gs = max((int)(d.x / WAVE_GROUP), vhi[il - 1] + 1);
+        if (gs <= ghi) {
+          const int* cnt = a.cnt + (int64_t)(il - 1) * a.ngroups;
+          const uint64_t t0 = global_ns();
+          WDBG(const long long c0 = clock64();)
+          for (;;) {
+            WDBG(++d_spin;)
+            int ok = 1;
+            for (int g = gs + lane; g <= ghi; g += 32) {
+              const int64_t left = nprev - (int64_t)g * WAVE_GROUP;
+              const int need = left < WAVE_GROUP ? (int)left : WAVE_GROUP;
+              ok &= ld_acquire(cnt + g) >= need;
+            }
+            if (__all_sync(0xffffffffu, ok)) break;
+            publish(false);
+            if (global_ns() - t0 > 4000000000ull) __trap();  // lost item: fail, never hang
+            __nanosleep(32);
+          }
+          WDBG(d_dep += clock64() - c0;)
+          __syncwarp();
+          if (lane == 0) vhi[il - 1] = ghi;
+          __syncwarp();
+        }
+      }
+      WDBG(const long long c1 = clock64();)
+      // the tile's CSR segment (row_ptr loads) before blocking on a free stage
+      int bv = 0, bc = 0;
+      uint32_t nbv = 0, nbc = 0;
+      if (il >= 0 && lane == 0) {
+        const int64_t nrows = lvl_p_rows(c, sigma, il);
+        const int64_t r0 = it * MT_ROWS;
+        const int64_t r1 = r0 + MT_ROWS < nrows ? r0 + MT_ROWS : nrows;
+        const int beg = c.rp[r0], end = c.rp[r1];
+        bv = beg & ~1;
+        bc = beg & ~3;
+        nbv = (uint32_t)(((end - bv) * 8 + 15) / 16 * 16);
+        nbc = (uint32_t)(((end - bc) * 4 + 15) / 16 * 16);
+      }
+      const int s = (int)(issued % MT_STAGES);
+      WDBG(const long long c2 = clock64(); d_rp += (unsigned long long)(nbv + c2 - c1 - nbv);)
+      // stage s is free once item issued - S is consumed (and published)
+      while (pub + MT_STAGES <= issued) publish(true);
+      WDBG(d_stage += clock64() - c2;)
+      if (lane == 0) {
+        titem[s][0] = il;
+        titem[s][1] = (int)it;
+        if (il < 0) {
+          mbar_arrive1(&full[s]);  // stop marker
+        } else {
+          tb[s][0] = bv;
+          tb[s][1] = bc;
+          unsigned char* base = msm + (size_t)s * sb;
+          const int64_t r0 = it * MT_ROWS;
+          const int64_t rn = lvl_p_rows(c, sigma, il) - r0;
+          const uint32_t nbr = (uint32_t)((((rn < MT_ROWS ? rn : MT_ROWS) + 1) * 4 + 15) / 16 * 16);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          mbar_arrive_tx(&full[s], nbv + nbc + nbr);
+          if (nbv) bulk_g2s(base, c.val + bv, nbv, &full[s]);
+          if (nbc) bulk_g2s(base + (size_t)(cap + 2) * 8, c.col + bc, nbc, &full[s]);
+          bulk_g2s(base + stage_bytes(cap), c.rp + r0, nbr, &full[s]);
+        }
+      }
+      __syncwarp();
+      if (il < 0) break;
+      ++issued;
+    }
+    publish(true);
+    WDBG(if (lane == 0) {
+      atomicAdd(&g_wave_dbg[3], d_dep);
+      atomicAdd(&g_wave_dbg[4], d_stage);
+      atomicAdd(&g_wave_dbg[5], d_rp);
+      atomicAdd(&g_wave_dbg[6], (unsigned long long)(clock64() - d_t0));
+      atomicAdd(&g_wave_dbg[7], d_spin);
+    })
+    return;
+  }
+
+  // ---------------- consumer warps: one row per thread per item
+  double tt = 0.0, rr = 0.0;
+  int bad = 0;
+  const int64_t n_own = c.n_own;
+  WDBG(unsigned long long d_full = 0, d_items = 0; const long long d_t1 = clock64();)
+  for (int64_t k = 0;; ++k) {
+    const int s = (int)(k % MT_STAGES);
+    WDBG(const long long c0 = clock64();)
+    mbar_wait(&full[s], (uint32_t)((k / MT_STAGES) & 1));
+    WDBG(d_full += clock64() - c0; ++d_items;)
+    const int l = titem[s][0];
+    if (l < 0) break;
+    const int64_t t = titem[s][1];
+    TileStage ts;
+    unsigned char* base = msm + (size_t)s * sb;
+    ts.val = reinterpret_cast<const double*>(base);
+    ts.col = reinterpret_cast<const int*>(base + (size_t)(cap + 2) * 8);
+    ts.beg_v = tb[s][0];
+    ts.beg_c = tb[s][1];
+    const int* rps = reinterpret_cast<const int*>(base + stage_bytes(cap));
+    const int64_t i = t * MT_ROWS + tid;
+    const double th = st->prm.th[l], ga = st->prm.ga[l];
+    if (l == 0) {
+      const double* P0 = c.Y;
+      double* P1 = c.Y + c.ld;
+      const double* R0 = c.Y + (int64_t)(sigma + 1) * c.ld;
+      double* R1 = c.Y + (int64_t)(sigma + 2) * c.ld;
+      const bool do_r = sbar >= 2;
+      if (i < lvl_p_rows(c, sigma, 0)) {
+        const int beg = rps[tid], end = rps[tid + 1];
+        const double p = P0[i], r = R0[i];
+        double acc[3];
+        const double* xs[3] = {c.x, P0, R0};
+        if (do_r)
+          row_dot_s<3>(ts, beg, end, xs, acc);
+        else
+          row_dot_s<2>(ts, beg, end, xs, acc);
+        if (i < n_own) {
+          const double tv = __dsub_rn(c.b[i], acc[0]);
+          tt = fma(tv, tv, tt);
+          rr = fma(r, r, rr);
+        }
+        const double wp = recur(acc[1], p, 0.0, th, ga, 0.0, false);
+        P1[i] = wp;
+        bad |= !finite(wp);
+        if (do_r && i < lvl_r_rows(c, sigma, 0)) {
+          const double wr = recur(acc[2], r, 0.0, th, ga, 0.0, false);
+          R1[i] = wr;
+          bad |= !finite(wr);
+        }
+      }
+    } else {
+      const double mu = st->prm.mu[l - 1];
+      const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
+      const bool do_r = l < sbar - 1;
+      const double* Pl = c.Y + (int64_t)l * c.ld;
+      const double* Pm = Pl - c.ld;
+      double* Pn = c.Y + (int64_t)(l + 1) * c.ld;
+      const double* Rl = c.Y + (int64_t)(sigma + 1 + l) * c.ld;
+      const double* Rm = Rl - c.ld;
+      double* Rn = c.Y + (int64_t)(sigma + 2 + l) * c.ld;
+      if (i < lvl_p_rows(c, sigma, l)) {
+        const int beg = rps[tid], end = rps[tid + 1];
+        double acc[2];
+        const double* xs[2] = {Pl, Rl};
+        const bool rrow = do_r && i < lvl_r_rows(c, sigma, l);
+        // inputs produced earlier in this launch when l > l0: coherent loads
+        if (rrow)
+          row_dot_s<2, LdCa, WAVE_BATCH>(ts, beg, end, xs, acc);
+        else
+          row_dot_s<1, LdCa, WAVE_BATCH>(ts, beg, end, xs, acc);
+        const double wp =
+            recur(acc[0], __ldca(Pl + i), use_mu ? __ldca(Pm + i) : 0.0, th, ga, mu, use_mu);
+        Pn[i] = wp;
+        bad |= !finite(wp);
+        if (rrow) {
+          const double wr =
+              recur(acc[1], __ldca(Rl + i), use_mu ? __ldca(Rm + i) : 0.0, th, ga, mu, use_mu);
+          Rn[i] = wr;
+          bad |= !finite(wr);
+        }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive1(&empty[s]);  // this warp's rows are written
+  }
+  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicOr(&c.st->breakdown, 1);
+  WDBG(if (tid == 0) {
+    atomicAdd(&g_wave_dbg[0], d_full);
+    atomicAdd(&g_wave_dbg[1], (unsigned long long)(clock64() - d_t1));
+    atomicAdd(&g_wave_dbg[2], d_items);
+  })
+  if (l0 == 0) {  // level-0 norm partials over the consumer warps; slots beyond the grid zero
+    double v[2] = {tt, rr};
+    for (int q = 0; q < 2; ++q) {
+      double x = warp_sum(v[q]);
+      if ((tid & 31) == 0) sm[tid >> 5] = x;
+      consumers_sync();
+      if (tid == 0) {
+        double r = 0.0;
+#pragma unroll
+        for (int w = 0; w < MT_ROWS / 32; ++w) r += sm[w];
+        v[q] = r;
+      }
+      consumers_sync();
+    }
+    if (tid == 0) {
+      c.part_t[blockIdx.x] = v[0];
+      c.part_r[blockIdx.x] = v[1];
+      for (int j = blockIdx.x + gridDim.x; j < c.red_n; j += gridDim.x) c.part_t[j] = c.part_r[j] = 0.0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pattern-compressed level kernels.  A stencil-like operator has few distinct
+// rows up to translation: the pattern table (offsets relative to the row,
+// values, in stored order) sits in shared memory and each row streams only
+// its 1- or 2-byte pattern id, so a level moves ~33 bytes per row (ids, the
+// two input and two output basis entries) instead of ~120 with CSR.  The row
+// sum is the same sequence of rounded multiply-adds as csr_matvec -- same
+// columns, values and order -- hence bit-identical to the CSR kernels.
+struct PatSmem {
+  const double* val;
+  const int* off;
+  const int* ptr;
+};
+
+// table layout in dynamic shared memory: [val ne][ptr np+1][off ne]
+__device__ __forceinline__ PatSmem load_patterns(const Ctx& c) {
+  extern __shared__ __align__(16) double psm[];
+  double* sv = psm;
+  int* sp = reinterpret_cast<int*>(sv + c.pat_ne);
+  int* so = sp + c.pat_np + 1;
+  for (int j = threadIdx.x; j < c.pat_ne; j += blockDim.x) {
+    sv[j] = __ldg(c.pat_val + j);
+    so[j] = __ldg(c.pat_off + j);
+  }
+  for (int j = threadIdx.x; j <= c.pat_np; j += blockDim.x) sp[j] = __ldg(c.pat_ptr + j);
+  __syncthreads();
+  return PatSmem{sv, so, sp};
+}
+
+template <typename ID>
+__device__ __forceinline__ int row_pattern(const Ctx& c, int64_t i) {
+  return (int)__ldg(reinterpret_cast<const ID*>(c.pid) + i);
+}
+
+#ifndef PAT_BATCH
+#define PAT_BATCH 8
+#endif
+template <int NV, int B = (NV >= 3 ? PAT_BATCH / 2 : PAT_BATCH)>
+__device__ __forceinline__ void row_dot_p(const PatSmem& T, int b, int e, int i,
+                                          const double* const* __restrict__ xs, double* acc) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  for (int jj = b; jj < e; jj += B) {
+    const int m = e - jj;
+    int cb[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) cb[k] = i + T.off[jj + (k < m ? k : 0)];
+    double xb[NV][B];
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int k = 0; k < B; ++k) xb[q][k] = __ldg(xs[q] + cb[k]);
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (k < m) {
+        const double v = T.val[jj + k];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v, xb[q][k]));
+      }
+    }
+  }
+}
+
+template <typename ID>
+__global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_pat(Ctx c) {
+  __shared__ double sm[ROWS_PER_CTA / 32];
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const PatSmem T = load_patterns(c);
+  const int sbar = st->s_bar;
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[0], ga = st->prm.ga[0];
+  const bool do_r = sbar >= 2;
+  const double* P0 = c.Y;
+  double* P1 = c.Y + c.ld;
+  const double* R0 = c.Y + (int64_t)(sigma + 1) * c.ld;
+  double* R1 = c.Y + (int64_t)(sigma + 2) * c.ld;
+  double tt = 0.0, rr = 0.0;
+  int bad = 0;
+  const int64_t n_own = c.n_own, plim = lvl_p_rows(c, sigma, 0), rlim = lvl_r_rows(c, sigma, 0);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
+    const int pid = row_pattern<ID>(c, i);
+    const int b = T.ptr[pid], e = T.ptr[pid + 1];
+    const double p = P0[i], r = R0[i];
+    double acc[3];
+    const double* xs[3] = {c.x, P0, R0};
+    if (do_r)
+      row_dot_p<3>(T, b, e, (int)i, xs, acc);
+    else
+      row_dot_p<2>(T, b, e, (int)i, xs, acc);
+    if (i < n_own) {
+      const double t = __dsub_rn(c.b[i], acc[0]);
+      tt = fma(t, t, tt);
+      rr = fma(r, r, rr);
+    }
+    const double wp = recur(acc[1], p, 0.0, th, ga, 0.0, false);
+    P1[i] = wp;
+    bad |= !finite(wp);
+    if (do_r && i < rlim) {
+      const double wr = recur(acc[2], r, 0.0, th, ga, 0.0, false);
+      R1[i] = wr;
+      bad |= !finite(wr);
+    }
+  }
+  tt = block_sum<ROWS_PER_CTA>(tt, sm);
+  rr = block_sum<ROWS_PER_CTA>(rr, sm);
+  if (threadIdx.x == 0) {
+    c.part_t[blockIdx.x] = tt;
+    c.part_r[blockIdx.x] = rr;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+#ifndef PAT_MINB
+#define PAT_MINB 1
+#endif
+template <typename ID>
+__global__ void __launch_bounds__(ROWS_PER_CTA, PAT_MINB) k_level_pat(Ctx c, int l) {
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  if (l >= sbar) return;
+  const PatSmem T = load_patterns(c);
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[l], ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
+  const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
+  const bool do_r = l < sbar - 1;
+  const double* Pl = c.Y + (int64_t)l * c.ld;
+  const double* Pm = Pl - c.ld;
+  double* Pn = c.Y + (int64_t)(l + 1) * c.ld;
+  const double* Rl = c.Y + (int64_t)(sigma + 1 + l) * c.ld;
+  const double* Rm = Rl - c.ld;
+  double* Rn = c.Y + (int64_t)(sigma + 2 + l) * c.ld;
+  int bad = 0;
+  const int64_t plim = lvl_p_rows(c, sigma, l), rlim = lvl_r_rows(c, sigma, l);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
+    const int pid = row_pattern<ID>(c, i);
+    const int b = T.ptr[pid], e = T.ptr[pid + 1];
+    double acc[2];
+    const double* xs[2] = {Pl, Rl};
+    const bool rrow = do_r && i < rlim;
+    if (rrow)
+      row_dot_p<2>(T, b, e, (int)i, xs, acc);
+    else
+      row_dot_p<1>(T, b, e, (int)i, xs, acc);
+    const double wp = recur(acc[0], Pl[i], use_mu ? Pm[i] : 0.0, th, ga, mu, use_mu);
+    Pn[i] = wp;
+    bad |= !finite(wp);
+    if (rrow) {
+      const double wr = recur(acc[1], Rl[i], use_mu ? Rm[i] : 0.0, th, ga, mu, use_mu);
+      Rn[i] = wr;
+      bad |= !finite(wr);
+    }
+  }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
 }
 
@@ -526,6 +1053,38 @@ void staged_prepare(int cap) {
   const int bytes = 200 * 1024;
   cudaFuncSetAttribute(k_level0_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_level_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_mpk_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+int wave_ctas_per_sm(int cap) {
+  int a = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_mpk_wave, WAVE_THREADS, MT_STAGES * wave_stage_bytes(cap));
+  return a;
+}
+
+// co-residency of the whole grid is what makes the spin-waits safe: launch
+// cooperatively (the runtime refuses a grid that cannot be co-resident)
+#ifdef WAVE_DBG
+extern "C" int sscg_debug_wave_counters(unsigned long long* out8) {
+  cudaMemcpyFromSymbol(out8, g_wave_dbg, sizeof(unsigned long long) * 8);
+  static const unsigned long long zero[8] = {};
+  cudaMemcpyToSymbol(g_wave_dbg, zero, sizeof(zero));
+  return (int)cudaGetLastError();
+}
+#endif
+
+cudaError_t launch_wave(const Ctx& c, const WaveArgs& a, int grid, cudaStream_t s) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(WAVE_THREADS);
+  lc.dynamicSmemBytes = MT_STAGES * wave_stage_bytes(c.stage_cap);
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, k_mpk_wave, c, a);
 }
 
 int staged_ctas_per_sm(int cap) {
@@ -539,7 +1098,50 @@ int staged_ctas_per_sm(int cap) {
 void launch_init_residual(const Ctx& c, const double* x0, cudaStream_t s) {
   k_init_residual<<<c.red_n, ROWS_PER_CTA, 0, s>>>(c, x0);
 }
+size_t pattern_smem_bytes(int np, int ne) {
+  return (size_t)ne * 12 + (size_t)(np + 1) * 4;
+}
+
+void pattern_prepare() {
+  const int bytes = 48 * 1024;
+  cudaFuncSetAttribute(k_level0_pat<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_level0_pat<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_level_pat<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_level_pat<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+// level 0 (the partial-sum kernel) and levels >= 1: out[0], out[1]
+int pattern_ctas_per_sm(int np, int ne, int pid_bytes, int* out2) {
+  int a = 0, b = 0;
+  const size_t bytes = pattern_smem_bytes(np, ne);
+  if (pid_bytes == 1) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_level0_pat<uint8_t>, ROWS_PER_CTA, bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_level_pat<uint8_t>, ROWS_PER_CTA, bytes);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_level0_pat<uint16_t>, ROWS_PER_CTA, bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_level_pat<uint16_t>, ROWS_PER_CTA, bytes);
+  }
+  out2[0] = a;
+  out2[1] = b;
+  return a < b ? a : b;
+}
+
 void launch_level(const Ctx& c, int level, cudaStream_t s) {
+  if (c.pid) {
+    const size_t bytes = pattern_smem_bytes(c.pat_np, c.pat_ne);
+    if (c.pid_bytes == 1) {
+      if (level == 0)
+        k_level0_pat<uint8_t><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c);
+      else
+        k_level_pat<uint8_t><<<c.pat_grid, ROWS_PER_CTA, bytes, s>>>(c, level);
+    } else {
+      if (level == 0)
+        k_level0_pat<uint16_t><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c);
+      else
+        k_level_pat<uint16_t><<<c.pat_grid, ROWS_PER_CTA, bytes, s>>>(c, level);
+    }
+    return;
+  }
   if (c.stage_cap > 0) {
     const size_t bytes = staged_smem_bytes(c.stage_cap);
     if (level == 0)

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <functional>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "internal.cuh"
@@ -108,6 +109,24 @@ struct sscg_plan {
   HaloPlan halo;
   void* comm = nullptr;    // ncclComm_t, or NULL (single GPU / virtual group)
   int partitioned = 0;
+  // wavefront matrix-powers kernel (k_mpk_wave)
+  int wave_on = 0;
+  int wave_grid = 0;
+  int64_t wave_tiles = 0;
+  int wave_lhi = 0;        // max over tiles of (last input tile - tile)
+  double wave_row_bytes = 0.0;  // CSR bytes per row
+  int2* d_wdep = nullptr;
+  int* d_wcnt = nullptr;
+  int wave_ngroups = 0;
+  std::vector<WaveArgs> wave_passes;
+  int wave_sigma = -1;
+  // pattern-compressed operator (pattern_setup)
+  void* d_pid = nullptr;
+  int pid_bytes = 0;
+  int pat_np = 0, pat_ne = 0, pat_grid = 0;
+  int* d_pat_ptr = nullptr;
+  int* d_pat_off = nullptr;
+  double* d_pat_val = nullptr;
 };
 
 namespace {
@@ -205,6 +224,14 @@ Ctx make_ctx(sscg_plan* p) {
   c.n_own = p->n_own;
   for (int d = 0; d <= SMAX; ++d) c.lvl_rows[d] = p->lvl_rows[d];
   c.red_buf = p->d_red;
+  c.pid = p->d_pid;
+  c.pid_bytes = p->pid_bytes;
+  c.pat_np = p->pat_np;
+  c.pat_ne = p->pat_ne;
+  c.pat_grid = p->pat_grid;
+  c.pat_ptr = p->d_pat_ptr;
+  c.pat_off = p->d_pat_off;
+  c.pat_val = p->d_pat_val;
   return c;
 }
 
@@ -226,31 +253,36 @@ int check_config(const sscg_config* c) {
   return SSCG_OK;
 }
 
+int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s);
+void wave_plan_passes(sscg_plan* p, int sigma);
+
+// Next-block parameters (k_params_begin + Leja points 2..sigma-1) need only the
+// Ritz state K_small just updated, so they run on a side branch beside the
+// recovery and are joined at the end of the outer loop: the matrix-powers
+// kernel of the next outer loop finds every shift ready.  (Outer loop 0 uses
+// the initial parameters k_state_init set; params_begin is a no-op there.)
+void capture_params_branch(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s) {
+  cudaEventRecord(p->ev_fork, s);
+  cudaStreamWaitEvent(p->side, p->ev_fork, 0);
+  launch_params_begin(c, p->side);
+  for (int n = 2; n < sigma; ++n) launch_leja_point(c, n, p->side);
+  cudaEventRecord(p->ev_leja[0], p->side);
+}
+
 int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t s) {
   // halo of p, r, x for the communication-avoiding levels (partitioned plans)
   if (p->partitioned && p->comm) {
     TRY(halo_exchange(p->halo, c, p->comm, s));
     halo_unpack(p->halo, c, s);
   }
-  // next-block parameters: endpoints now, Leja points 2.. on the side branch,
-  // each joined right before the matrix-powers level that consumes it
-  launch_params_begin(c, s);
-  cudaEventRecord(p->ev_fork, s);
-  cudaStreamWaitEvent(p->side, p->ev_fork, 0);
-  for (int n = 2; n < sigma; ++n) {
-    launch_leja_point(c, n, p->side);
-    cudaEventRecord(p->ev_leja[n], p->side);
-  }
-  for (int l = 0; l < sigma; ++l) {
-    if (l >= 2) cudaStreamWaitEvent(s, p->ev_leja[l], 0);
-    launch_level(c, l, s);
-  }
+  TRY(launch_mpk(p, c, sigma, s));
   launch_gram(c, 2 * sigma + 1, s);
   if (p->comm) {  // the one synchronisation of the outer loop
     const int k = 2 * sigma + 1;
     TRY(nccl_allreduce(p->comm, c.red_buf, (int64_t)k * (k + 1) / 2 + 2, s));
   }
   launch_small(c, s);
+  capture_params_branch(p, c, sigma, s);
   if (full) {
     for (int j = 0; j < sigma; ++j) {
       launch_diag_form(c, j, s);
@@ -259,6 +291,7 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     }
   }
   launch_recover(c, s);
+  cudaStreamWaitEvent(s, p->ev_leja[0], 0);
   return SSCG_OK;
 }
 
@@ -309,9 +342,9 @@ int launch_outer_profiled(sscg_plan* p, const Ctx& c, int sigma, int full, int o
     TRY(rec(4, [&] { hrc = halo_exchange(p->halo, c, p->comm, p->stream); halo_unpack(p->halo, c, p->stream); }));
     TRY(hrc);
   }
-  TRY(rec(4, [&] { launch_params_begin(c, p->stream); }));
-  for (int n = 2; n < sigma; ++n) TRY(rec(4, [&] { launch_leja_point(c, n, p->stream); }));
-  for (int l = 0; l < sigma; ++l) TRY(rec(0, [&] { launch_level(c, l, p->stream); }));
+  int mrc = SSCG_OK;
+  TRY(rec(0, [&] { mrc = launch_mpk(p, c, sigma, p->stream); }));
+  TRY(mrc);
   TRY(rec(1, [&] { launch_gram(c, 2 * sigma + 1, p->stream); }));
   if (p->comm) {
     const int k = 2 * sigma + 1;
@@ -320,6 +353,8 @@ int launch_outer_profiled(sscg_plan* p, const Ctx& c, int sigma, int full, int o
     TRY(arc);
   }
   TRY(rec(2, [&] { launch_small(c, p->stream); }));
+  TRY(rec(4, [&] { launch_params_begin(c, p->stream); }));
+  for (int n = 2; n < sigma; ++n) TRY(rec(4, [&] { launch_leja_point(c, n, p->stream); }));
   if (full) {
     for (int j = 0; j < sigma; ++j) {
       TRY(rec(4, [&] { launch_diag_form(c, j, p->stream); }));
@@ -386,7 +421,8 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
     rp32[i] = (int)row_ptr[i];
   }
   // +4 / +2 elements: the staged kernels round bulk copies up to 16 bytes
-  TRY(dalloc(p, &p->d_rp, n_rows + 1));
+  TRY(dalloc(p, &p->d_rp, n_rows + 1 + 8));  // +8: 16-byte bulk copies of a tile's row_ptr
+  CUDA_OK(cudaMemset(p->d_rp, 0, sizeof(int) * (n_rows + 1 + 8)));
   TRY(dalloc(p, &p->d_col, nnz + 4));
   TRY(dalloc(p, &p->d_val, nnz + 2));
   CUDA_OK(cudaMemcpy(p->d_rp, rp32.data(), sizeof(int) * (n_rows + 1), cudaMemcpyHostToDevice));
@@ -440,6 +476,198 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   return rc;
 }
 
+const char* env_or(const char* name, const char* dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? v : dflt;
+}
+
+// Lossless pattern compression of the operator for the level kernels: rows
+// that are translates of each other -- same length, same column offsets
+// relative to the row, same values, same stored order -- share one table
+// entry.  Used when the table is small (shared memory, 1-2 byte ids);
+// otherwise the CSR kernels run.  SSCG_PATTERN=0 disables it (A/B tests).
+constexpr int PAT_MAX_BYTES = 16 * 1024;
+
+int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                  const double* values) {
+  p->d_pid = nullptr;
+  if (atoi(env_or("SSCG_PATTERN", "1")) == 0 || n_rows < 1) return SSCG_OK;
+  std::unordered_map<uint64_t, std::vector<int>> buckets;
+  std::vector<int> ptr{0}, off;
+  std::vector<double> val;
+  std::vector<uint16_t> ids((size_t)n_rows);
+  for (int64_t i = 0; i < n_rows; ++i) {
+    const int64_t b = row_ptr[i], e = row_ptr[i + 1];
+    uint64_t h = 1469598103934665603ull ^ (uint64_t)(e - b);
+    for (int64_t j = b; j < e; ++j) {
+      uint64_t vb;
+      std::memcpy(&vb, &values[j], 8);
+      h = (h ^ (uint64_t)(uint32_t)(col_idx[j] - (int32_t)i)) * 1099511628211ull;
+      h = (h ^ vb) * 1099511628211ull;
+    }
+    int id = -1;
+    auto& cand = buckets[h];
+    for (int q : cand) {
+      const int pb = ptr[q], pe = ptr[q + 1];
+      if (pe - pb != e - b) continue;
+      bool same = true;
+      for (int64_t j = b; j < e && same; ++j) {
+        const int k = pb + (int)(j - b);
+        same = off[k] == (int)(col_idx[j] - (int32_t)i) &&
+               std::memcmp(&val[k], &values[j], 8) == 0;
+      }
+      if (same) {
+        id = q;
+        break;
+      }
+    }
+    if (id < 0) {
+      id = (int)ptr.size() - 1;
+      const size_t ne = off.size() + (size_t)(e - b);
+      if (id >= 65535 || ne * 12 + (ptr.size() + 1) * 4 > (size_t)PAT_MAX_BYTES) return SSCG_OK;
+      for (int64_t j = b; j < e; ++j) {
+        off.push_back((int)(col_idx[j] - (int32_t)i));
+        val.push_back(values[j]);
+      }
+      ptr.push_back((int)off.size());
+      cand.push_back(id);
+    }
+    ids[(size_t)i] = (uint16_t)id;
+  }
+  const int np = (int)ptr.size() - 1, ne = (int)off.size();
+  int occ[2] = {0, 0};
+  pattern_prepare();
+  p->pid_bytes = np <= 256 ? 1 : 2;
+  pattern_ctas_per_sm(np, ne, p->pid_bytes, occ);
+  if (occ[0] < 1 || occ[1] < 1) return SSCG_OK;
+  if (p->pid_bytes == 1) {
+    std::vector<uint8_t> i8(ids.begin(), ids.end());
+    uint8_t* d = nullptr;
+    TRY(dalloc(p, &d, (size_t)n_rows));
+    CUDA_OK(cudaMemcpy(d, i8.data(), (size_t)n_rows, cudaMemcpyHostToDevice));
+    p->d_pid = d;
+  } else {
+    uint16_t* d = nullptr;
+    TRY(dalloc(p, &d, (size_t)n_rows));
+    CUDA_OK(cudaMemcpy(d, ids.data(), 2 * (size_t)n_rows, cudaMemcpyHostToDevice));
+    p->d_pid = d;
+  }
+  TRY(dalloc(p, &p->d_pat_ptr, ptr.size()));
+  TRY(dalloc(p, &p->d_pat_off, off.size()));
+  TRY(dalloc(p, &p->d_pat_val, val.size()));
+  CUDA_OK(cudaMemcpy(p->d_pat_ptr, ptr.data(), 4 * ptr.size(), cudaMemcpyHostToDevice));
+  if (ne) {
+    CUDA_OK(cudaMemcpy(p->d_pat_off, off.data(), 4 * off.size(), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(p->d_pat_val, val.data(), 8 * val.size(), cudaMemcpyHostToDevice));
+  }
+  p->pat_np = np;
+  p->pat_ne = ne;
+  int sms = NUM_SMS;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  const int64_t tiles = (n_rows + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
+  p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * occ[0], (int64_t)RED_BLOCKS, tiles}));
+  p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ[1], tiles));
+  return SSCG_OK;
+}
+
+// Wavefront MPK setup (single-GPU plans with staged tiles): per row tile the
+// range of input tiles its columns touch, made monotone (suffix min of lo,
+// prefix max of hi) so a CTA's dependency checks only move forward.
+int wave_setup(sscg_plan* p, const int64_t* row_ptr, const int32_t* col_idx) {
+  p->wave_on = 0;
+  // opt-in (SSCG_WAVE=1): correct and bit-identical, but on B200 today slower
+  // than one launch per level -- see DESIGN.md "wavefront experiment"
+  if (p->stage_cap <= 0 || p->partitioned || atoi(env_or("SSCG_WAVE", "0")) == 0) return SSCG_OK;
+  const int64_t n = p->n, nt = (n + MT_ROWS - 1) / MT_ROWS;
+  std::vector<int2> dep(nt);
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t r0 = t * MT_ROWS, r1 = std::min<int64_t>(n, r0 + MT_ROWS);
+    int64_t lo = t, hi = t;
+    for (int64_t j = row_ptr[r0]; j < row_ptr[r1]; ++j) {
+      const int64_t ct = col_idx[j] / MT_ROWS;
+      lo = std::min(lo, ct);
+      hi = std::max(hi, ct);
+    }
+    dep[t] = make_int2((int)lo, (int)hi);
+  }
+  for (int64_t t = nt - 2; t >= 0; --t) dep[t].x = std::min(dep[t].x, dep[t + 1].x);
+  int64_t lhi = 0;
+  for (int64_t t = 0; t < nt; ++t) {
+    if (t) dep[t].y = std::max(dep[t].y, dep[t - 1].y);
+    lhi = std::max<int64_t>(lhi, dep[t].y - t);
+  }
+  int sms = NUM_SMS;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  int per_sm = wave_ctas_per_sm(p->stage_cap);
+  const int want = atoi(env_or("SSCG_WAVE_CTAS", "0"));
+  if (want > 0 && want < per_sm) per_sm = want;
+  if (per_sm < 1) return SSCG_OK;
+  p->wave_grid = (int)std::min<int64_t>((int64_t)sms * per_sm, p->red_n);
+  p->wave_tiles = nt;
+  p->wave_lhi = (int)lhi;
+  p->wave_row_bytes = (12.0 * (double)p->nnz + 4.0 * (double)n) / (double)n;
+  p->wave_ngroups = (int)((nt + WAVE_GROUP - 1) / WAVE_GROUP);
+  TRY(dalloc(p, &p->d_wdep, nt));
+  TRY(dalloc(p, &p->d_wcnt, (size_t)SMAX * p->wave_ngroups + SMAX));  // + one claim counter per pass
+  CUDA_OK(cudaMemcpy(p->d_wdep, dep.data(), sizeof(int2) * nt, cudaMemcpyHostToDevice));
+  p->wave_on = 1;
+  p->wave_sigma = -1;
+  return SSCG_OK;
+}
+
+// Split sigma levels into passes whose wavefront window fits the L2 budget:
+// between the first and last level of a pass a tile's CSR and the basis rows
+// in flight must stay resident, ~ ((nl-1) D) tiles of A + nl (D + lhi) tiles
+// of vectors (P, R, the Chebyshev two-back term).
+void wave_plan_passes(sscg_plan* p, int sigma) {
+  if (p->wave_sigma == sigma) return;
+  p->wave_passes.clear();
+  p->wave_sigma = sigma;
+  const double budget = atof(env_or("SSCG_WAVE_L2_MB", "64")) * 1048576.0;
+  const int force = atoi(env_or("SSCG_WAVE_NL", "0"));
+  const double slack_f = atof(env_or("SSCG_WAVE_SLACK", "6"));
+  auto lag = [&](int nl) {
+    const int slack = (int)std::ceil(slack_f * p->wave_grid / nl);
+    return p->wave_lhi + 1 + slack;
+  };
+  int nl = 1;
+  for (int m = sigma; m >= 1; --m) {
+    const double D = lag(m);
+    const double win = ((m - 1) * D * p->wave_row_bytes + m * (D + p->wave_lhi) * 24.0) * MT_ROWS;
+    if (win <= budget || m == 1) {
+      nl = m;
+      break;
+    }
+  }
+  if (force > 0) nl = std::min(force, sigma);
+  const int npass = (sigma + nl - 1) / nl;
+  int l0 = 0;
+  for (int q = 0; q < npass; ++q) {
+    const int m = (sigma - l0 + (npass - q) - 1) / (npass - q);  // near-equal passes
+    WaveArgs a;
+    a.l0 = l0;
+    a.nl = m;
+    a.D = lag(m);
+    a.ngroups = p->wave_ngroups;
+    a.nF = p->wave_tiles + (int64_t)(m - 1) * a.D;
+    a.cnt = p->d_wcnt;
+    a.claim = reinterpret_cast<unsigned int*>(p->d_wcnt + (size_t)SMAX * p->wave_ngroups) + q;
+    a.dep = p->d_wdep;
+    p->wave_passes.push_back(a);
+    l0 += m;
+  }
+}
+
+int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s) {
+  if (!p->wave_on) {
+    for (int l = 0; l < sigma; ++l) launch_level(c, l, s);
+    return SSCG_OK;
+  }
+  CUDA_OK(cudaMemsetAsync(p->d_wcnt, 0, sizeof(int) * ((size_t)SMAX * p->wave_ngroups + SMAX), s));
+  for (const WaveArgs& a : p->wave_passes) CUDA_OK(launch_wave(c, a, p->wave_grid, s));
+  return SSCG_OK;
+}
+
 int create_wrapped(sscg_plan** out, const std::function<int(sscg_plan*)>& init) {
   if (!out) return sscg_fail(SSCG_EINVAL, "out is NULL");
   *out = nullptr;
@@ -464,7 +692,10 @@ int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
     if (n < 1) return sscg_fail(SSCG_EINVAL, "n must be >= 1");
     int64_t lvl[SMAX + 1];
     for (int d = 0; d <= SMAX; ++d) lvl[d] = n;
-    return plan_init(p, device, n, n, n, nnz, row_ptr, col_idx, values, lvl, SMAX);
+    TRY(plan_init(p, device, n, n, n, nnz, row_ptr, col_idx, values, lvl, SMAX));
+    TRY(pattern_setup(p, n, row_ptr, col_idx, values));
+    if (p->d_pid) return SSCG_OK;  // the pattern kernels replace the CSR staging
+    return wave_setup(p, row_ptr, col_idx);
   });
 }
 
@@ -485,6 +716,7 @@ int sscg_plan_create_part(sscg_plan** out, int32_t device, const sscg_part* part
     int rc = plan_init(p, device, q.n_rows, q.n_own, q.n_local, q.nnz, q.row_ptr, q.col_idx,
                        q.values, q.lvl_rows, q.depth);
     if (rc) return rc;
+    TRY(pattern_setup(p, q.n_rows, q.row_ptr, q.col_idx, q.values));
     p->partitioned = 1;
     p->rank = q.rank;
     p->world = q.world;
@@ -558,7 +790,8 @@ int sscg_plan_destroy(sscg_plan* p) {
   void* bufs[] = {p->d_rp, p->d_col, p->d_val, p->d_Y, p->d_x, p->d_b, p->d_x0, p->d_xj,
                   p->d_rj, p->d_st, p->d_cfg, p->d_part_t, p->d_part_r, p->d_part_d,
                   p->d_part_g, p->d_leja, p->d_it, p->d_ri, p->d_rd, p->d_conds, p->d_th,
-                  p->d_ga, p->d_mu, p->d_otrue, p->d_fg, p->d_red};
+                  p->d_ga, p->d_mu, p->d_otrue, p->d_fg, p->d_red, p->d_wdep, p->d_wcnt,
+                  p->d_pid, p->d_pat_ptr, p->d_pat_off, p->d_pat_val};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_done) cudaFreeHost(p->h_done);
@@ -619,6 +852,13 @@ int run_prepare(sscg_plan* p, const sscg_config* cfg) {
     return sscg_fail(SSCG_EINVAL, "trace_full is not supported on a row-partitioned solve");
   CUDA_OK(cudaSetDevice(p->device));
   TRY(ensure_work(p, cfg->sigma, cfg->max_outer, cfg->leja_grid));
+  if (p->wave_on && p->wave_sigma != cfg->sigma) {
+    wave_plan_passes(p, cfg->sigma);
+    if (p->gexec) {
+      cudaGraphExecDestroy(p->gexec);
+      p->gexec = nullptr;
+    }
+  }
   p->cfg = *cfg;
   p->halo.r_col = cfg->sigma + 1;
   DevConfig dc;
@@ -781,6 +1021,30 @@ int sscg_get_small_phases(const sscg_plan* p, int64_t* cycles8) {
   long long h[8];
   CUDA_OK(cudaMemcpy(h, p->d_st->phase_cycles, sizeof(h), cudaMemcpyDeviceToHost));
   for (int i = 0; i < 8; ++i) cycles8[i] = h[i];
+  return SSCG_OK;
+}
+
+int sscg_plan_mpk_schedule(sscg_plan* p, int32_t sigma, int32_t* out) {
+  if (!p || !out || sigma < 1 || sigma > SMAX) return sscg_fail(SSCG_EINVAL, "bad arguments");
+  for (int i = 0; i < 4 + 2 * SMAX; ++i) out[i] = 0;
+  out[0] = p->d_pid ? 2 : p->wave_on ? 1 : 0;
+  out[1] = p->wave_on ? p->wave_grid : p->red_n;
+  out[2] = p->d_pid ? p->pat_np : p->wave_lhi;
+  if (!p->wave_on) {
+    out[3] = sigma;
+    for (int q = 0; q < sigma; ++q) out[4 + 2 * q] = 1;
+    return SSCG_OK;
+  }
+  const int keep = p->wave_sigma;
+  std::vector<WaveArgs> saved = p->wave_passes;
+  wave_plan_passes(p, sigma);
+  out[3] = (int)p->wave_passes.size();
+  for (size_t q = 0; q < p->wave_passes.size(); ++q) {
+    out[4 + 2 * q] = p->wave_passes[q].nl;
+    out[5 + 2 * q] = p->wave_passes[q].D;
+  }
+  p->wave_passes = saved;  // a query must not invalidate the captured graph
+  p->wave_sigma = keep;
   return SSCG_OK;
 }
 

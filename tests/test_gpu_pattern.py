@@ -1,0 +1,112 @@
+"""GPU tier: pattern-compressed level kernels (mpk.cu k_level_pat).
+
+A plan whose rows reduce to a small table of (relative column, value)
+patterns streams 1- or 2-byte row ids instead of CSR.  Columns, values and
+stored order are A's, so every solve must be bit-identical to the CSR
+kernels (SSCG_PATTERN=0): basis, Gram, alphas and the iterate."""
+
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from paper_1908_04081_b200 import AdaptiveConfig, adaptive_solve, problems
+from paper_1908_04081_b200.kernels import _plan
+from paper_1908_04081_b200.types import ProblemInstance, SparseMatrix
+
+pytestmark = pytest.mark.gpu
+
+
+def _with_env(env, fn):
+    old = os.environ.get("SSCG_PATTERN")
+    try:
+        os.environ.pop("SSCG_PATTERN", None)
+        os.environ.update(env)
+        return fn()
+    finally:
+        if old is None:
+            os.environ.pop("SSCG_PATTERN", None)
+        else:
+            os.environ["SSCG_PATTERN"] = old
+
+
+def _instance(m, seed, label):
+    m = m.tocsr()
+    m.sort_indices()
+    n = m.shape[0]
+    a = SparseMatrix(n=n, row_ptr=m.indptr.astype(np.int64), col_idx=m.indices.astype(np.int32),
+                     values=m.data.astype(np.float64), n_a=int(np.diff(m.indptr).max()))
+    dense = m.toarray()
+    ev = np.linalg.eigvalsh(dense)
+    rng = np.random.default_rng(seed)
+    return ProblemInstance(a=a, b=rng.standard_normal(n), x0=np.zeros(n),
+                           norm_a=float(ev[-1]), norm_abs_a=float(np.linalg.norm(abs(dense), 2)),
+                           kappa_a=float(ev[-1] / ev[0]), label=label)
+
+
+def _tridiag_many_patterns(n=1200, distinct=300, seed=3):
+    """Tridiagonal SPD matrix with `distinct` diagonal values: > 256 patterns,
+    so the plan uses 2-byte row ids."""
+    rng = np.random.default_rng(seed)
+    diag = 2.5 + rng.integers(0, distinct, n) / distinct
+    return _instance(sp.diags([-np.ones(n - 1), diag, -np.ones(n - 1)], [-1, 0, 1]), seed, "tri")
+
+
+def _random_spd(n=800, seed=5):
+    m = sp.random(n, n, density=6.0 / n, random_state=seed, format="csr")
+    return _instance(m + m.T + sp.identity(n) * 14.0, seed, "rand")
+
+
+CASES = [
+    ("c1", lambda: problems.make_problem("c1"), dict(sigma=8, eps_star=1e-10, basis_kind="newton"),
+     "pattern"),
+    ("c3", lambda: problems.make_problem("c3", scale=24),
+     dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev"), "pattern"),
+    ("c5", lambda: problems.make_problem("c5", scale=28),
+     dict(sigma=12, eps_star=1e-10, basis_kind="newton"), "pattern"),
+    ("tri300", _tridiag_many_patterns, dict(sigma=6, eps_star=1e-9, basis_kind="newton"), "pattern"),
+    ("rand", _random_spd, dict(sigma=6, eps_star=1e-9, basis_kind="monomial"), "csr"),
+]
+
+
+@pytest.mark.parametrize("name,make,kw,kind", CASES, ids=[c[0] for c in CASES])
+def test_pattern_bit_identical_to_csr(gpu_ready, name, make, kw, kind):
+    cfg = AdaptiveConfig(**kw)
+
+    def run():
+        prob = make()
+        return _plan(prob.a).mpk_schedule(cfg.sigma), adaptive_solve(prob, cfg, trace="fast")
+
+    s0, ref = _with_env({"SSCG_PATTERN": "0"}, run)
+    s1, got = _with_env({}, run)
+    assert s0["kind"] == "csr" and s1["kind"] == kind, (s0, s1)
+    assert ref[1].converged
+    np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
+    np.testing.assert_array_equal(got[0], ref[0])
+    assert got[1].total_outer == ref[1].total_outer
+
+
+def test_pattern_counts(gpu_ready):
+    """Translation classes of the stencils: 2D 5-point 3x3 = 9, 3D 7-point 27;
+    the 300-value tridiagonal needs 2-byte ids."""
+    assert _plan(problems.make_problem("c1").a).mpk_schedule(8)["patterns"] == 9
+    assert _plan(problems.make_problem("c5", scale=16).a).mpk_schedule(8)["patterns"] == 27
+    s = _plan(_tridiag_many_patterns().a).mpk_schedule(6)
+    assert s["kind"] == "pattern" and 256 < s["patterns"] <= 900
+
+
+def test_pattern_full_trace_and_partitioned_agree(gpu_ready):
+    """Full diagnostics and the virtual-group (row-slab) path through the
+    pattern kernels reproduce the CSR single-GPU solve."""
+    from paper_1908_04081_b200.dist import VirtualGroup
+    from paper_1908_04081_b200.partition import CsrRows
+    kw = dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev")
+    ref = _with_env({"SSCG_PATTERN": "0"},
+                    lambda: adaptive_solve(problems.make_problem("c3", scale=24), AdaptiveConfig(**kw)))
+    x, tr, co = adaptive_solve(problems.make_problem("c3", scale=24), AdaptiveConfig(**kw))
+    np.testing.assert_array_equal(x, ref[0])
+    np.testing.assert_array_equal(tr.true_resid, ref[1].true_resid)
+    prob = problems.make_problem("c3", scale=24)
+    xg, tg, cg, _ = VirtualGroup(CsrRows.of(prob.a), 1, depth=10).solve(prob, AdaptiveConfig(**kw))
+    np.testing.assert_array_equal(xg, ref[0])

@@ -1,0 +1,83 @@
+"""A/B sweep of matrix-powers schedules on one problem (GPU box).
+
+    python tools/wave_sweep.py [--config c5w] [--outer 12] ENV1 ENV2 ...
+
+Each ENV is a comma list like "SSCG_WAVE=0" or "SSCG_WAVE_NL=4,SSCG_WAVE_CTAS=3"
+(empty string = defaults).  For every ENV a fresh plan is created with that
+environment, one solve capped at --outer outer loops runs unprofiled (device
+time) and once profiled (per-class kernel ms); prints one JSON line per ENV.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1908_04081_b200 import AdaptiveConfig, _lib as L, problems  # noqa: E402
+from paper_1908_04081_b200.adaptive import LogBuffers, make_config  # noqa: E402
+
+KEYS = ("SSCG_WAVE", "SSCG_WAVE_NL", "SSCG_WAVE_CTAS", "SSCG_WAVE_L2_MB")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c5w")
+    ap.add_argument("--outer", type=int, default=12)
+    ap.add_argument("envs", nargs="*")
+    args = ap.parse_args()
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    key, scale, sigma, basis, eps, desc = bench.CONFIGS[args.config]
+    prob = problems.make_problem(key, scale=scale)
+    lib = L.load()
+    cfg = AdaptiveConfig(sigma=sigma, eps_star=eps, basis_kind=basis, max_outer=args.outer)
+    cfg, ccfg = make_config(cfg, prob, "fast")
+    logs = LogBuffers(cfg)
+    b, x0 = L.f64(prob.b), L.f64(prob.x0)
+    for env in args.envs or [""]:
+        for k in KEYS:
+            os.environ.pop(k, None)
+        for kv in filter(None, env.split(",")):
+            k, v = kv.split("=")
+            os.environ[k] = v
+        plan = L.Plan(prob.a.n, prob.a.row_ptr, prob.a.col_idx, prob.a.values)
+        sched = plan.mpk_schedule(sigma)
+        L.check(lib.sscg_load(plan.handle, L.dptr(b), L.dptr(x0)))
+        ms = []
+        for _ in range(3):
+            L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
+            ms.append(logs.s.device_ms)
+        L.check(lib.sscg_fetch(plan.handle, None, logs.s))
+        outer = int(logs.s.total_outer)
+        dbg = None
+        if hasattr(lib, "sscg_debug_wave_counters"):  # WAVE_DBG side build
+            buf = (C.c_ulonglong * 8)()
+            lib.sscg_debug_wave_counters(buf)  # reset
+            L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
+            lib.sscg_debug_wave_counters(buf)
+            g = list(buf)
+            dbg = {"cons_full_wait_frac": g[0] / max(1, g[1]), "cons_items_w0": g[2],
+                   "prod_dep_wait_frac": g[3] / max(1, g[6]), "prod_stage_wait_frac": g[4] / max(1, g[6]),
+                   "prod_rp_frac": g[5] / max(1, g[6]), "spins": g[7],
+                   "cons_cycles_per_item": g[1] / max(1, g[2])}
+        L.check(lib.sscg_set_profiling(plan.handle, 1))
+        L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
+        L.check(lib.sscg_set_profiling(plan.handle, 0))
+        pms = np.zeros(5)
+        pcnt = np.zeros(5, dtype=np.int64)
+        L.check(lib.sscg_get_profile(plan.handle, L.dptr(pms), pcnt.ctypes.data_as(C.POINTER(C.c_int64))))
+        act = max(1, int(pcnt[1]))
+        print(json.dumps({"env": env, "sched": sched, "outer": outer, "iters": int(logs.s.total_iters),
+                          "dev_ms": min(ms), "ms_per_outer": min(ms) / act,
+                          "mpk_ms_per_outer": pms[0] / act, "gram": pms[1] / act,
+                          "small": pms[2] / act, "rec": pms[3] / act, "other": pms[4] / act, "dbg": dbg}),
+              flush=True)
+        plan.close()
+
+
+if __name__ == "__main__":
+    main()
