@@ -108,18 +108,27 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
 
 
-def mpk_bytes_per_outer(n, nnz, sigma, mu_nonzero):
+def a_bytes_per_level(n, nnz, sched):
+    """Bytes of the operator one matrix-powers level must stream: CSR
+    (12 nnz + 4 (n+1)) or, for a pattern-compressed plan, the
+    1- or 2-byte row ids (the pattern table lives in shared memory)."""
+    if sched and sched.get("kind") == "pattern":
+        return (1 if sched["patterns"] <= 256 else 2) * n
+    return 12 * nnz + 4 * (n + 1)
+
+
+def mpk_bytes_per_outer(n, nnz, sigma, mu_nonzero, sched=None):
     """Algorithmic bytes of the sigma matrix-powers levels of one outer loop
     (SURVEY.md 8(d)): A once per level, 16 n per generated column (+8 n for the
     Chebyshev two-back term), x and b on level 0 (true residual)."""
-    s_a = 12 * nnz + 4 * (n + 1)
+    s_a = a_bytes_per_level(n, nnz, sched)
     gen = 2 * sigma - 1
     two_back = (2 * sigma - 3) if mu_nonzero else 0  # columns with l >= 1
     return sigma * s_a + 16 * n * gen + 8 * n * two_back + 16 * n + 8 * n  # + r0 norm read
 
 
-def outer_bytes(n, nnz, sigma, s_t, mu_nonzero):
-    return (mpk_bytes_per_outer(n, nnz, sigma, mu_nonzero) + 8 * n * (2 * sigma + 1)
+def outer_bytes(n, nnz, sigma, s_t, mu_nonzero, sched=None):
+    return (mpk_bytes_per_outer(n, nnz, sigma, mu_nonzero, sched) + 8 * n * (2 * sigma + 1)
             + 8 * n * (2 * s_t + 1) + 8 * n + 24 * n)
 
 
@@ -341,18 +350,20 @@ def run_ours(args, rank, world):
     s_t = [int(v) for v in logs.rec_i[:total_outer, L.REC_STILDE]]
     mu_nz = basis == "chebyshev"
     active = total_outer + 1  # outer loops whose levels did real work
-    mpk_bytes = active * mpk_bytes_per_outer(n, nnz, sigma, mu_nz)
+    mpk_bytes = active * mpk_bytes_per_outer(n, nnz, sigma, mu_nz, sched)
     mpk_ms = float(pms[0])
     hbm_peak, peak_kind = peaks()
     mpk_gbs = mpk_bytes / (mpk_ms / 1e3) / 1e9
-    solve_bytes = sum(outer_bytes(n, nnz, sigma, st, mu_nz) for st in s_t) + \
-        mpk_bytes_per_outer(n, nnz, sigma, mu_nz) + 8 * (2 * sigma + 1) * n
+    solve_bytes = sum(outer_bytes(n, nnz, sigma, st, mu_nz, sched) for st in s_t) + \
+        mpk_bytes_per_outer(n, nnz, sigma, mu_nz, sched) + 8 * (2 * sigma + 1) * n
     solve_gbs = solve_bytes / (dev_ms / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get("mpk_level_bytes")
+            kname = {"pattern": "k_level_pat", "csr": "k_level_staged",
+                     "wavefront": "k_mpk_wave"}[sched["kind"]]
+            traffic = json.load(open(tpath)).get(args.config, {}).get(kname)
         except Exception:
             traffic = None
 
@@ -392,8 +403,11 @@ def run_ours(args, rank, world):
         "hbm": {"solve_gbs": solve_gbs, "frac_of_measured": solve_gbs / hbm_peak,
                 "frac_of_8tbs": solve_gbs / 8000.0, "algorithmic_bytes_per_solve": solve_bytes},
         "roofline": {"bound": "hbm",
-                     "kernel": ("k_mpk_wave (wavefront matrix powers + recurrence)"
-                                if sched["wavefront"] else "k_level (matrix powers + recurrence)"),
+                     "kernel": {"wavefront": "k_mpk_wave (wavefront matrix powers + recurrence)",
+                                "pattern": "k_level_pat (pattern-compressed matrix powers + recurrence)",
+                                "csr": "k_level_staged (CSR matrix powers + recurrence)"}[sched["kind"]],
+                     "a_bytes_per_level": a_bytes_per_level(n, nnz, sched),
+                     "a_bytes_per_level_csr": a_bytes_per_level(n, nnz, None),
                      "mpk_schedule": sched,
                      "achieved": mpk_gbs, "peak": hbm_peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": mpk_gbs / hbm_peak, "traffic": traffic,

@@ -75,12 +75,14 @@ __device__ __forceinline__ void row_dot(const int* __restrict__ col, const doubl
   }
 }
 
-// one recurrence step, reference order: ((Ay - th*y) - mu*y2) / ga
+// one recurrence step, reference order: ((Ay - th*y) - mu*y2) / ga.  The IEEE
+// quotient w / 1.0 is w exactly (NaN, +-0 and +-inf included), so the unit
+// scaling of the Newton and monomial bases skips the division sequence.
 __device__ __forceinline__ double recur(double ay, double y, double y2, double th, double ga,
                                         double mu, bool use_mu) {
   double w = __dsub_rn(ay, __dmul_rn(th, y));
   if (use_mu) w = __dsub_rn(w, __dmul_rn(mu, y2));
-  return __ddiv_rn(w, ga);
+  return ga == 1.0 ? w : __ddiv_rn(w, ga);
 }
 
 __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
@@ -751,8 +753,11 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_pat(Ctx c) {
   int bad = 0;
   const int64_t n_own = c.n_own, plim = lvl_p_rows(c, sigma, 0), rlim = lvl_r_rows(c, sigma, 0);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
-    const int pid = row_pattern<ID>(c, i);
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int pid_next = i < plim ? row_pattern<ID>(c, i) : 0;  // ids one row ahead
+  for (; i < plim; i += stride) {
+    const int pid = pid_next;
+    if (i + stride < plim) pid_next = row_pattern<ID>(c, i + stride);
     const int b = T.ptr[pid], e = T.ptr[pid + 1];
     const double p = P0[i], r = R0[i];
     double acc[3];
@@ -784,11 +789,18 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_pat(Ctx c) {
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
 }
 
+// (an explicit min-blocks of 1 lets ptxas take ~85 registers: 2 CTAs/SM;
+// 0 = no min-blocks hint)
 #ifndef PAT_MINB
-#define PAT_MINB 1
+#define PAT_MINB 0
+#endif
+#if PAT_MINB > 0
+#define PAT_LB __launch_bounds__(ROWS_PER_CTA, PAT_MINB)
+#else
+#define PAT_LB __launch_bounds__(ROWS_PER_CTA)
 #endif
 template <typename ID>
-__global__ void __launch_bounds__(ROWS_PER_CTA, PAT_MINB) k_level_pat(Ctx c, int l) {
+__global__ void PAT_LB k_level_pat(Ctx c, int l) {
   const SolverState* st = c.st;
   if (st->done) return;
   const int sbar = st->s_bar;
@@ -807,8 +819,11 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, PAT_MINB) k_level_pat(Ctx c, int
   int bad = 0;
   const int64_t plim = lvl_p_rows(c, sigma, l), rlim = lvl_r_rows(c, sigma, l);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
-    const int pid = row_pattern<ID>(c, i);
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int pid_next = i < plim ? row_pattern<ID>(c, i) : 0;  // ids one row ahead
+  for (; i < plim; i += stride) {
+    const int pid = pid_next;
+    if (i + stride < plim) pid_next = row_pattern<ID>(c, i + stride);
     const int b = T.ptr[pid], e = T.ptr[pid + 1];
     double acc[2];
     const double* xs[2] = {Pl, Rl};
