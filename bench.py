@@ -132,6 +132,23 @@ def outer_bytes(n, nnz, sigma, s_t, mu_nonzero, sched=None):
             + 8 * n * (2 * s_t + 1) + 8 * n + 24 * n)
 
 
+def cpu_threads():
+    """(threads the CPU path may use, description): OpenBLAS' pool (dgemm/dgemv
+    of the Gram and recovery) -- scipy csr_matvec and numpy element-wise work
+    run on one core."""
+    try:
+        import numpy
+        import threadpoolctl
+        numpy.ones(2) @ numpy.ones(2)
+        pools = [(d["internal_api"], int(d["num_threads"]), d.get("version"))
+                 for d in threadpoolctl.threadpool_info()]
+    except Exception:
+        pools = []
+    blas = max([t for _, t, _ in pools] or [1])
+    return blas, (f"os.cpu_count()={os.cpu_count()}; BLAS pools {pools}; scipy csr_matvec "
+                  "and numpy element-wise work (most of the time) are single-threaded")
+
+
 def cpu_sample(prob, cfg_kw, outer_count, total_iters):
     """Oracle port on this host: 1 outer loop of the same problem (bounded),
     per-outer time extrapolated to the solve's outer count."""
@@ -381,13 +398,13 @@ def run_ours(args, rank, world):
     cpu = None
     if not args.no_cpu:
         cpu_v, t1 = cpu_sample(prob, cfg_kw, total_outer, total_iters)
-        cpu = {"value": cpu_v, "unit": "iter/s", "cores": 1, "kind": "port",
+        cores, tnote = cpu_threads()
+        cpu = {"value": cpu_v, "unit": "iter/s", "cores": cores, "kind": "port",
                "sample": f"oracle/sscg_oracle.py (numpy/scipy, as the reference) on the same "
                          f"{n}-row problem, max_outer=1 took {t1:.2f}s; full solve extrapolated "
                          f"as (outer+1) x that = {t1 * (total_outer + 1):.1f}s for "
                          f"{total_iters} iterations",
-               "threads_note": f"os.cpu_count()={os.cpu_count()}; scipy csr_matvec and numpy "
-                               "element-wise work are single-threaded"}
+               "threads_note": tnote}
 
     line = {
         "metric": "cg_iterations_per_sec", "value": value, "unit": "iter/s", "n_gpus": world,
@@ -467,7 +484,8 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic, seeded", "impl": "reference",
         "config": {"workload": desc, "n": prob.a.n, "nnz": prob.a.nnz},
-        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cpu_threads()[0], "kind": "port",
+                         "threads_note": cpu_threads()[1],
                          "sample": f"each step = 1 outer loop of the oracle port on the full "
                                    f"problem ({t1:.2f}s); iters/s = {total} iters / "
                                    f"(({outer}+1) outer x step time), counts from "
