@@ -332,6 +332,79 @@ def gen_solves():
 
 
 # ---------------------------------------------------------------------------
+# Fixed s-step CG (sstep.py:79-174), SURVEY.md 8(f) row 1
+def sstep_cases():
+    """name -> (problem factory, sstep_solve kwargs); explicit `params` are
+    given as (kind, s, lo, hi) and built with the reference's params_for."""
+    c1 = lambda: to_ref(problems.make_problem("c1"))
+    c3p = lambda: to_ref(problems.make_problem("c3", scale=24))
+    p44 = dense_problem(spd_dense(50, 1e4, 44), "spd50")
+    p43 = dense_problem(spd_dense(40, 50.0, 43), "spd40")
+    from sstepcg.matio import load_problem
+    data = "/root/reference/pkg/data/matrices"
+    bus = load_problem(os.path.join(data, "494_bus.mtx"), label="494bus")
+    return {
+        "sstep_c1_mono4": (c1, dict(s=4, eps_star=1e-10)),
+        "sstep_c1_newton8": (c1, dict(s=8, eps_star=1e-10, basis_kind="newton",
+                                      spectral_bounds=(0.004, 8.0))),
+        "sstep_c1_mono10": (c1, dict(s=10, eps_star=1e-10, max_outer=60)),
+        "sstep_c3p_cheb8": (c3p, dict(s=8, eps_star=1e-10, basis_kind="chebyshev",
+                                      spectral_bounds=(0.04, 12.0))),
+        "sstep_spd50_newton6": (lambda: p44, dict(s=6, eps_star=1e-10, basis_kind="newton",
+                                                  spectral_bounds=(1.0, 1e4))),
+        "sstep_spd40_mono1": (lambda: p43, dict(s=1, eps_star=1e-10)),
+        "sstep_spd40_mono3": (lambda: p43, dict(s=3, eps_star=1e-10)),
+        "sstep_spd40_params5": (lambda: p43, dict(s=5, eps_star=1e-10,
+                                                  params=("chebyshev", 5, 1.0, 50.0))),
+        "sstep_494bus_mono5": (lambda: bus, dict(s=5, eps_star=1e-6)),
+        "sstep_494bus_cheb6": (lambda: bus, dict(s=6, eps_star=1e-8, basis_kind="chebyshev",
+                                                 spectral_bounds=(1e-3, 2.0))),
+    }
+
+
+def gen_sstep():
+    from sstepcg.sstep import sstep_solve
+    orig = ref_basis.gram
+    for name, (mk, kw) in sstep_cases().items():
+        prob = mk()
+        kw = dict(kw)
+        spec = kw.get("params")
+        if spec is not None:
+            kw["params"] = ref_basis.params_for(*spec)
+        first = {}
+
+        def spy(y):
+            g = orig(y)
+            first.setdefault("g", g.copy())
+            return g
+
+        ref_basis.gram = spy
+        try:
+            t0 = time.perf_counter()
+            x, tr, co = sstep_solve(prob, **kw)
+            dt = time.perf_counter() - t0
+        finally:
+            ref_basis.gram = orig
+        meta = {k: v for k, v in kw.items() if k != "params"}
+        if spec is not None:
+            meta["params"] = list(spec)
+        save(name, alphas=np.array(co.alphas), betas=np.array(co.betas),
+             s_schedule=np.array(tr.s_schedule), outer_marks=np.array(tr.outer_marks),
+             true_resid=np.array(tr.true_resid), upd_resid=np.array(tr.upd_resid),
+             resid_gap=np.array(tr.resid_gap), c_values=np.array(tr.c_values),
+             psi=np.array(tr.psi), lambda_min=np.array(tr.lambda_min),
+             lambda_max=np.array(tr.lambda_max),
+             flags=np.array([tr.converged, tr.stagnated, tr.diverged, tr.total_iters,
+                             tr.total_outer]),
+             x=x, first_g=first.get("g", np.zeros((0, 0))), wall=np.array(dt),
+             cfg=np.array(json.dumps(meta)),
+             **({"in_" + k: v for k, v in problem_arrays(prob).items()}
+                if name.startswith(("sstep_spd", "sstep_494")) else {}))
+        print(f"    {name}: outer={tr.total_outer} total={tr.total_iters} conv={tr.converged} "
+              f"stag={tr.stagnated} div={tr.diverged} final={tr.final_true_resid:.3e} ({dt:.2f}s)")
+
+
+# ---------------------------------------------------------------------------
 # Rounding-noise floor of the reference itself (SURVEY.md H1): the same solve
 # with only the Gram summation order changed.  Counts / s-sequences that move
 # under these perturbations cannot be demanded bit-exactly of any other

@@ -203,3 +203,58 @@ def test_sigma_one_reduces_to_hscg():
             sigma=1, eps_star=1e-10, variant=variant, basis_kind="monomial"))
         m = min(20, len(al2), len(al))
         np.testing.assert_allclose(al2[:m], al[:m], rtol=1e-8)
+
+
+# ---- fixed s-step CG (sstep.py:79-174), SURVEY.md 8(f) row 1 -----------------
+SSTEP_CASES = ["sstep_c1_mono4", "sstep_c1_newton8", "sstep_c1_mono10", "sstep_c3p_cheb8",
+               "sstep_spd50_newton6", "sstep_spd40_mono1", "sstep_spd40_mono3",
+               "sstep_spd40_params5", "sstep_494bus_mono5", "sstep_494bus_cheb6"]
+
+
+def sstep_problem(name, ref):
+    if name.startswith("sstep_c1"):
+        return problems.make_problem("c1")
+    if name.startswith("sstep_c3p"):
+        return problems.make_problem("c3", scale=24)
+    return problem_from_arrays(ref, "in_")
+
+
+def sstep_kwargs(ref):
+    kw = cfg_of(ref)
+    if "params" in kw:
+        kind, s, lo, hi = kw.pop("params")
+        kw["params"] = O.params_select(kind, int(s), lo, hi)
+    if "spectral_bounds" in kw:
+        kw["spectral_bounds"] = tuple(kw["spectral_bounds"])
+    return kw
+
+
+@pytest.mark.parametrize("name", SSTEP_CASES)
+def test_fixed_sstep_matches_reference(name):
+    ref = golden(name)
+    prob = sstep_problem(name, ref)
+    a = prob.a
+    x, tr, al, be = O.sstep(a.n, a.row_ptr, a.col_idx, a.values, prob.b, prob.x0,
+                            **sstep_kwargs(ref))
+    flags = ref["flags"]
+    assert [tr.converged, tr.stagnated, tr.diverged] == [bool(v) for v in flags[:3]]
+    assert tr.total_iters == int(flags[3]) and tr.total_outer == int(flags[4])
+    np.testing.assert_array_equal(tr.s_schedule, ref["s_schedule"])
+    np.testing.assert_array_equal(tr.outer_marks, ref["outer_marks"])
+    np.testing.assert_array_equal(al, ref["alphas"])
+    np.testing.assert_array_equal(be, ref["betas"])
+    for key in ("true_resid", "upd_resid", "resid_gap", "c_values", "psi", "lambda_min",
+                "lambda_max"):
+        np.testing.assert_array_equal(np.array(getattr(tr, key)), ref[key])
+    np.testing.assert_array_equal(x, ref["x"])
+    np.testing.assert_array_equal(tr.first_gram, ref["first_g"])
+
+
+def test_fixed_sstep_validation():
+    prob = problems.make_problem("c1", scale=8)
+    a = prob.a
+    with pytest.raises(ValueError):
+        O.sstep(a.n, a.row_ptr, a.col_idx, a.values, prob.b, prob.x0, 0, 1e-8)
+    with pytest.raises(O.OracleParamError):
+        O.sstep(a.n, a.row_ptr, a.col_idx, a.values, prob.b, prob.x0, 5, 1e-8,
+                params=O.params_monomial(3))
