@@ -40,6 +40,11 @@ extern "C" {
 #define SSCG_CONVERGED 1
 #define SSCG_STAGNATED 2
 #define SSCG_DIVERGED 3
+#define SSCG_EXHAUSTED 4  /* fixed s-step: max_outer ran out with no verdict (sstep.py:168-171) */
+
+/* sscg_config.solver */
+#define SSCG_SOLVER_ADAPTIVE 0  /* adaptive_solve (adaptive.py:111-268)             */
+#define SSCG_SOLVER_FIXED 1     /* sstep_solve, fixed s = sigma (sstep.py:79-174)  */
 
 /* basis kinds (basis.py:166-177) and c strategies (ritz.py:184-203) */
 #define SSCG_BASIS_MONOMIAL 0
@@ -95,7 +100,7 @@ typedef struct sscg_config {
   int32_t has_bounds;  /* spectral_bounds given (old variant / monomial path) */
   int32_t trace_full;  /* 1: per-inner-iteration true residual (adaptive.py:205-215) */
   int32_t n_a;         /* max row population (full-bound c) */
-  int32_t reserved;
+  int32_t solver;      /* SSCG_SOLVER_ADAPTIVE / SSCG_SOLVER_FIXED (s = sigma) */
   double eps_star;
   double bound_lo, bound_hi;
   double norm_a, norm_abs_a, kappa_a; /* ProblemInstance scalars (adaptive.py:119,153) */
@@ -115,7 +120,7 @@ typedef struct sscg_logs {
   double* outer_true;  /* [cap_outer+1] ||b-Ax||/||b|| at each outer boundary */
   double* first_gram;  /* [(2*sigma+1)^2] first block's G, or NULL */
   /* outputs */
-  int32_t status;      /* SSCG_CONVERGED / STAGNATED / DIVERGED   */
+  int32_t status;      /* SSCG_CONVERGED / STAGNATED / DIVERGED / EXHAUSTED */
   int32_t total_iters;
   int32_t total_outer;
   int32_t n_records;   /* len(trace.outer_records)                 */
@@ -194,6 +199,13 @@ int sscg_fetch(sscg_plan* plan, double* x_out, sscg_logs* logs);
  * counts[] launches of each class.  enable=1 makes the next runs record one
  * event pair per launch (no graph replay). */
 int sscg_set_profiling(sscg_plan* plan, int32_t enable);
+/* Caller-chosen basis parameters for the fixed s-step solver (sstep_solve's
+ * `params`, sstep.py:97-99): theta[s], gamma[s], mu[s-1] (mu may be NULL when
+ * s == 1).  They replace params_for(basis_kind, sigma, spectral_bounds) in the
+ * next runs with solver == SSCG_SOLVER_FIXED; s must be >= that sigma
+ * (ParameterError otherwise, status SSCG_EPARAM).  s == 0 clears them. */
+int sscg_set_basis_params(sscg_plan* plan, int32_t s, const double* theta, const double* gamma,
+                          const double* mu);
 int sscg_get_profile(const sscg_plan* plan, double* ms5, int64_t* counts5);
 /* K_small phase timers of the last run (SM clock cycles, thread 0):
  * [0] classify [1] Gram extract + c [2] nested conds [3] s~ + truncation

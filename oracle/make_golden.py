@@ -568,6 +568,40 @@ def gen_noise():
         print(f"    noise {name}: outer/total {[(int(r[0]), int(r[1])) for r in rows]}")
 
 
+def gen_sstep_noise():
+    """Noise floor of the reference's fixed s-step CG: the same runs with only
+    the Gram summation order changed.  alpha_horizon = the first iteration at
+    which any perturbed run's alpha moves by more than 1e-8 relative (parity of
+    alpha beyond it cannot be demanded of another implementation)."""
+    from sstepcg.sstep import sstep_solve
+    orig = ref_basis.gram
+    grams = {k: v[0] for k, v in PERTURBATIONS.items() if v[0] is not None}
+    for name, (mk, kw) in sstep_cases().items():
+        prob = mk()
+        kw = dict(kw)
+        if kw.get("params") is not None:
+            kw["params"] = ref_basis.params_for(*kw["params"])
+        _, tr0, co0 = sstep_solve(prob, **kw)
+        a0 = np.array(co0.alphas)
+        rows, horizon = [], len(a0)
+        for pname, gfn in grams.items():
+            ref_basis.gram = gfn
+            try:
+                _, tr, co = sstep_solve(prob, **kw)
+            finally:
+                ref_basis.gram = orig
+            a = np.array(co.alphas)
+            m = min(len(a), len(a0))
+            bad = np.nonzero(np.abs(a[:m] - a0[:m]) > 1e-8 * np.abs(a0[:m]))[0]
+            h = int(bad[0]) if len(bad) else (m if len(a) == len(a0) else m)
+            horizon = min(horizon, h)
+            rows.append([tr.total_outer, tr.total_iters, tr.converged, tr.stagnated, tr.diverged])
+        save("noise_" + name, counts=np.array(rows, dtype=float), alpha_horizon=np.array(horizon),
+             names=np.array(list(grams)))
+        print(f"    noise {name}: horizon={horizon} outer/total "
+              f"{sorted(set((int(r[0]), int(r[1])) for r in rows))}")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     print("reference:", sstepcg.__file__)

@@ -20,7 +20,8 @@ LIB_PATH = os.environ.get("SSCG_LIB") or os.path.join(HERE, "_lib", "libsscg.so"
 ABI_VERSION = 1
 MAX_SIGMA = 16
 OK, EINVAL, ECUDA, ENOMEM, EPARAM, ENODEV, EBREAKDOWN = range(7)
-RUNNING, CONVERGED, STAGNATED, DIVERGED = range(4)
+RUNNING, CONVERGED, STAGNATED, DIVERGED, EXHAUSTED = range(5)
+SOLVER_ADAPTIVE, SOLVER_FIXED = 0, 1
 BASIS = {"monomial": 0, "newton": 1, "chebyshev": 2}
 BASIS_NAMES = {v: k for k, v in BASIS.items()}
 CSTRAT = {"adaptive": 0, "unit": 1, "kappa-estimate": 2, "full-bound": 3}
@@ -35,7 +36,7 @@ EXPORTS = (
     "sscg_last_error", "sscg_abi_version", "sscg_device_count", "sscg_plan_create",
     "sscg_plan_destroy", "sscg_plan_device_bytes", "sscg_solve", "sscg_load", "sscg_run",
     "sscg_fetch", "sscg_set_profiling", "sscg_get_profile", "sscg_get_small_phases",
-    "sscg_plan_mpk_schedule",
+    "sscg_plan_mpk_schedule", "sscg_set_basis_params",
     "sscg_spmv", "sscg_build_block",
     "sscg_gram", "sscg_recover", "sscg_nested_conds", "sscg_select_s_tilde",
     "sscg_leja_points", "sscg_params_for", "sscg_ritz_sequence", "sscg_sym_eig",
@@ -48,7 +49,7 @@ class SscgConfig(C.Structure):
         ("sigma", C.c_int32), ("s_bar0", C.c_int32), ("f", C.c_int32),
         ("basis_kind", C.c_int32), ("c_strategy", C.c_int32), ("variant", C.c_int32),
         ("max_outer", C.c_int32), ("leja_grid", C.c_int32), ("has_bounds", C.c_int32),
-        ("trace_full", C.c_int32), ("n_a", C.c_int32), ("reserved", C.c_int32),
+        ("trace_full", C.c_int32), ("n_a", C.c_int32), ("solver", C.c_int32),
         ("eps_star", C.c_double), ("bound_lo", C.c_double), ("bound_hi", C.c_double),
         ("norm_a", C.c_double), ("norm_abs_a", C.c_double), ("kappa_a", C.c_double),
     ]
@@ -110,6 +111,7 @@ def _declare(lib):
         "sscg_get_profile": (C.c_int, [vp, _DP, C.POINTER(i64)]),
         "sscg_get_small_phases": (C.c_int, [vp, C.POINTER(i64)]),
         "sscg_plan_mpk_schedule": (C.c_int, [vp, i32, _IP]),
+        "sscg_set_basis_params": (C.c_int, [vp, i32, _DP, _DP, _DP]),
         "sscg_spmv": (C.c_int, [vp, _DP, _DP]),
         "sscg_build_block": (C.c_int, [vp, _DP, _DP, i32, _DP, _DP, _DP, _DP, _DP]),
         "sscg_gram": (C.c_int, [i32, i64, i32, _DP, _DP]),

@@ -101,8 +101,9 @@ class LogBuffers:
         self.s = s
 
 
-def build_trace(cfg, logs, trace_level):
-    """SolveTrace / CgCoefficients from the device logs (trace.py:25-81)."""
+def build_trace(cfg, logs, trace_level, records=True):
+    """SolveTrace / CgCoefficients from the device logs (trace.py:25-81).
+    records=False: no OuterLoopRecords (the fixed s-step solver keeps none)."""
     s = logs.s
     tr = SolveTrace(trace_level=trace_level)
     co = CgCoefficients()
@@ -115,6 +116,8 @@ def build_trace(cfg, logs, trace_level):
         tr.outer_marks.append(int(ri[L.REC_MARK]))
         tr.s_schedule.append(int(ri[L.REC_SACTUAL]))
         tr.total_outer += 1
+        if not records:
+            continue
         kind = L.BASIS_NAMES[int(ri[L.REC_PKIND])]
         gen = None
         if not math.isnan(rd[L.RECD_GEN_LO]):

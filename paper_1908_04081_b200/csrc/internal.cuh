@@ -52,6 +52,9 @@ struct ParamsDev {  // basis.py:39-55
 struct DevConfig {  // sscg_config + derived constants
   int sigma, s_bar0, f, basis_kind, c_strategy, variant, max_outer, leja_grid;
   int has_bounds, trace_full, n_a, ncols;  // ncols = 2 sigma + 1 (physical Y)
+  int solver;       // SSCG_SOLVER_ADAPTIVE / SSCG_SOLVER_FIXED
+  int has_fixed;    // fixed solver: caller's parameters below replace params_for
+  double fth[SMAX], fga[SMAX], fmu[SMAX];
   double eps_star, bound_lo, bound_hi, norm_a, norm_abs_a, kappa_a;
   double unit;      // 2^-53 (ritz.py:25)
   double c0;        // MACHINE_UNIT ** -0.5 (ritz.py:124)

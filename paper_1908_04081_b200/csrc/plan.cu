@@ -109,6 +109,9 @@ struct sscg_plan {
   HaloPlan halo;
   void* comm = nullptr;    // ncclComm_t, or NULL (single GPU / virtual group)
   int partitioned = 0;
+  // sscg_set_basis_params (fixed s-step solver)
+  int fixed_s = 0;
+  double fixed_th[SMAX] = {}, fixed_ga[SMAX] = {}, fixed_mu[SMAX] = {};
   // wavefront matrix-powers kernel (k_mpk_wave)
   int wave_on = 0;
   int wave_grid = 0;
@@ -250,6 +253,8 @@ int check_config(const sscg_config* c) {
     return sscg_fail(SSCG_EINVAL, "unknown c strategy %d", c->c_strategy);
   if (c->max_outer < 0) return sscg_fail(SSCG_EINVAL, "max_outer must be >= 0");
   if (c->leja_grid < 2) return sscg_fail(SSCG_EINVAL, "leja_grid must be >= 2");
+  if (c->solver != SSCG_SOLVER_ADAPTIVE && c->solver != SSCG_SOLVER_FIXED)
+    return sscg_fail(SSCG_EINVAL, "unknown solver %d", c->solver);
   return SSCG_OK;
 }
 
@@ -829,6 +834,24 @@ int sscg_set_profiling(sscg_plan* p, int32_t enable) {
   return SSCG_OK;
 }
 
+int sscg_set_basis_params(sscg_plan* p, int32_t s, const double* th, const double* ga,
+                          const double* mu) {
+  if (!p) return sscg_fail(SSCG_EINVAL, "NULL plan");
+  if (s == 0) {
+    p->fixed_s = 0;
+    return SSCG_OK;
+  }
+  if (s < 0 || !th || !ga || (s > 1 && !mu)) return sscg_fail(SSCG_EINVAL, "bad basis parameters");
+  const int keep = s < SMAX ? s : SMAX;  // degrees beyond SSCG_MAX_SIGMA are never used
+  for (int i = 0; i < SMAX; ++i) {
+    p->fixed_th[i] = i < keep ? th[i] : NAN;
+    p->fixed_ga[i] = i < keep ? ga[i] : NAN;
+    p->fixed_mu[i] = i < keep - 1 ? mu[i] : NAN;
+  }
+  p->fixed_s = s;
+  return SSCG_OK;
+}
+
 int sscg_get_profile(const sscg_plan* p, double* ms5, int64_t* counts5) {
   if (!p || !ms5 || !counts5) return sscg_fail(SSCG_EINVAL, "NULL argument");
   for (int i = 0; i < 5; ++i) {
@@ -875,6 +898,17 @@ int run_prepare(sscg_plan* p, const sscg_config* cfg) {
   dc.trace_full = cfg->trace_full;
   dc.n_a = cfg->n_a;
   dc.ncols = 2 * cfg->sigma + 1;
+  dc.solver = cfg->solver;
+  if (cfg->solver == SSCG_SOLVER_FIXED && p->fixed_s > 0) {
+    if (p->fixed_s < cfg->sigma)
+      return sscg_fail(SSCG_EPARAM, "params cover degree %d, need %d", p->fixed_s, cfg->sigma);
+    dc.has_fixed = 1;
+    for (int i = 0; i < SMAX; ++i) {
+      dc.fth[i] = i < cfg->sigma ? p->fixed_th[i] : NAN;
+      dc.fga[i] = i < cfg->sigma ? p->fixed_ga[i] : NAN;
+      dc.fmu[i] = i < cfg->sigma - 1 ? p->fixed_mu[i] : NAN;
+    }
+  }
   dc.eps_star = cfg->eps_star;
   dc.bound_lo = cfg->bound_lo;
   dc.bound_hi = cfg->bound_hi;

@@ -861,8 +861,9 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
       }
     }
     int outcome = SSCG_RUNNING;
-    if (k >= cf.max_outer) {  // loop exhausted: adaptive.py:262-266
-      outcome = (true_rel <= cf.eps_star) ? SSCG_CONVERGED : SSCG_STAGNATED;
+    if (k >= cf.max_outer) {  // loop exhausted: adaptive.py:262-266 / sstep.py:168-171
+      outcome = (true_rel <= cf.eps_star) ? SSCG_CONVERGED
+                : (cf.solver == SSCG_SOLVER_FIXED) ? SSCG_EXHAUSTED : SSCG_STAGNATED;
     } else if (true_rel <= cf.eps_star) {
       outcome = SSCG_CONVERGED;
     } else if (!isfinite(true_rel) || true_rel > 1e5) {
@@ -917,8 +918,11 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
   __syncthreads();
 
   PHASE(1);
-  // ---- nested condition estimates and s~ (adaptive.py:89-104)
-  cta_nested_conds(S.G, CMAX, sbar, S.conds, jac);
+  const bool fixed = cf.solver == SSCG_SOLVER_FIXED;
+  // ---- nested condition estimates and s~ (adaptive.py:89-104); the fixed
+  //      s-step solver always runs the whole block (sstep.py:124-125)
+  if (!fixed) cta_nested_conds(S.G, CMAX, sbar, S.conds, jac);
+  else if (tid <= SMAX) S.conds[tid] = NAN;
   __syncthreads();
   PHASE(2);
   if (tid == 0) {
@@ -927,7 +931,7 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
     int s_t = 1;
     for (int i = 1; i <= sbar; ++i)
       if (S.conds[i] <= bound) s_t = i;
-    S.si[SI_STILDE] = s_t;
+    S.si[SI_STILDE] = fixed ? sbar : s_t;
     S.sc[SC_RREL] = r_rel;
   }
   __syncthreads();
@@ -1034,6 +1038,7 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
       }
       ++it;
       if (rr >= 0.0 && est <= eps && j < s_t - 1) break;  // est_hit
+      if (fixed) continue;  // no basis-quality breaks in fixed s-step CG
       if (cf.variant == 1) {
         const double c_now =
             (cf.c_strategy == SSCG_C_FULLBOUND) ? c_blk : c_from_state(cf.c_strategy, rz, cf.c0);
@@ -1127,7 +1132,7 @@ __global__ void __launch_bounds__(NT) k_small(Ctx c) {
   __syncthreads();
   PHASE(5);
   if (tid == 0) {
-    const int nxt = S.si[SI_JDONE] + cf.f;
+    const int nxt = fixed ? sigma : S.si[SI_JDONE] + cf.f;
     st->s_bar = nxt < sigma ? nxt : sigma;
     st->k = st->k + 1;
     st->breakdown = 0;
@@ -1145,6 +1150,7 @@ __global__ void k_params_begin(Ctx c) {
   if (threadIdx.x != 0) return;
   st->leja_on = 0;
   if (st->done) return;
+  if (cf.solver == SSCG_SOLVER_FIXED) return;  // parameters fixed for the solve
   if (!(cf.variant == 1 && cf.basis_kind != SSCG_BASIS_MONOMIAL)) return;
   const RitzDev& rz = st->rz;
   if (!(st->total_iters > 1 && rz.count >= 2)) return;
@@ -1230,11 +1236,26 @@ __global__ void __launch_bounds__(NT) k_state_init(Ctx c) {
     ritz_init(st->rz, cf.c0);
   }
   __syncthreads();
-  if (cf.variant == 0 || cf.basis_kind == SSCG_BASIS_MONOMIAL)
+  if (cf.solver == SSCG_SOLVER_FIXED && cf.has_fixed) {  // sstep_solve(params=...)
+    if (threadIdx.x == 0) {
+      ParamsDev& p = st->prm;
+      p.kind = cf.basis_kind;
+      p.has_from = 0;
+      p.lo = p.hi = NAN;
+      for (int i = 0; i < SMAX; ++i) {
+        p.th[i] = cf.fth[i];
+        p.ga[i] = cf.fga[i];
+        p.mu[i] = cf.fmu[i];
+      }
+    }
+  } else if (cf.solver == SSCG_SOLVER_FIXED || cf.variant == 0 ||
+             cf.basis_kind == SSCG_BASIS_MONOMIAL) {
+    // fixed s-step: params_for(basis_kind, s, spectral_bounds) once (sstep.py:97-99)
     cta_params_for(cf.basis_kind, cf.sigma, cf.has_bounds != 0, cf.bound_lo, cf.bound_hi,
                    cf.leja_grid, &st->prm, c.leja_obj, S.L);
-  else if (threadIdx.x == 0)
+  } else if (threadIdx.x == 0) {
     set_monomial(st->prm, cf.sigma);
+  }
 }
 
 // ---- unit-entry kernels -----------------------------------------------------

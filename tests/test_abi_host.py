@@ -52,7 +52,8 @@ def test_abi_version_and_constants(lib):
     for name, val in [("SSCG_IT_N", L.IT_N), ("SSCG_REC_NI", L.REC_NI),
                       ("SSCG_RECD_ND", L.RECD_ND), ("SSCG_EBREAKDOWN", L.EBREAKDOWN),
                       ("SSCG_DIVERGED", L.DIVERGED), ("SSCG_BASIS_CHEBYSHEV", 2),
-                      ("SSCG_C_FULLBOUND", 3)]:
+                      ("SSCG_C_FULLBOUND", 3), ("SSCG_EXHAUSTED", L.EXHAUSTED),
+                      ("SSCG_SOLVER_FIXED", L.SOLVER_FIXED)]:
         assert re.search(rf"#define {name} {val}\b", txt), name
 
 
