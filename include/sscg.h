@@ -220,6 +220,15 @@ int sscg_get_small_phases(const sscg_plan* plan, int64_t* cycles8);
  * q, out[5+2q] tile lag D of pass q.  out: 4+2*SSCG_MAX_SIGMA int32. */
 int sscg_plan_mpk_schedule(sscg_plan* plan, int32_t sigma, int32_t* out);
 
+/* Hestenes-Stiefel CG on the plan's operator (classic.py:33-104 hscg_solve;
+ * single-GPU plans).  Every iteration recomputes the true residual b - A x
+ * like the reference; logs->iters rows carry alpha, beta, the Ritz values,
+ * xi, psi and the true / updated residuals and gap (SSCG_IT_*), at most
+ * logs->cap_iters of them; status CONVERGED / STAGNATED / DIVERGED, or
+ * EXHAUSTED when max_iters ran out.  max_iters < 0: 100 n. */
+int sscg_hscg(sscg_plan* plan, const double* b, const double* x0, double eps_star,
+              int64_t max_iters, double* x_out, sscg_logs* logs);
+
 /* ---- unit entry points (parity tests; one kernel family each) ------------- */
 /* lacore.py:25-34 spmv: y = A x (scipy csr_matvec rounding, bit for bit) */
 int sscg_spmv(sscg_plan* plan, const double* x, double* y);

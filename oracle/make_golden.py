@@ -602,6 +602,77 @@ def gen_sstep_noise():
               f"{sorted(set((int(r[0]), int(r[1])) for r in rows))}")
 
 
+# ---------------------------------------------------------------------------
+# Hestenes-Stiefel CG (classic.py:33-104), SURVEY.md 8(f) row 2
+def hscg_cases():
+    c1 = lambda: to_ref(problems.make_problem("c1"))
+    c3p = lambda: to_ref(problems.make_problem("c3", scale=24))
+    p44 = dense_problem(spd_dense(50, 1e4, 44), "spd50")
+    p43 = dense_problem(spd_dense(40, 50.0, 43), "spd40")
+    from sstepcg.matio import load_problem
+    data = "/root/reference/pkg/data/matrices"
+    bus = load_problem(os.path.join(data, "494_bus.mtx"), label="494bus")
+    return {
+        "hscg_c1": (c1, dict(eps_star=1e-10)),
+        "hscg_c1_cap50": (c1, dict(eps_star=1e-10, max_iters=50)),
+        "hscg_c3p": (c3p, dict(eps_star=1e-10)),
+        "hscg_spd40": (lambda: p43, dict(eps_star=1e-10)),
+        "hscg_spd50": (lambda: p44, dict(eps_star=1e-12)),
+        "hscg_494bus": (lambda: bus, dict(eps_star=1e-8)),
+    }
+
+
+class _DotShim:
+    """numpy stand-in for classic.py whose dot sums in chunks (another order)."""
+
+    def __init__(self, chunk):
+        self.chunk = chunk
+
+    def dot(self, a, b):
+        a, b = np.asarray(a), np.asarray(b)
+        return float(sum(np.dot(a[i:i + self.chunk], b[i:i + self.chunk])
+                         for i in range(0, len(a), self.chunk)))
+
+    def __getattr__(self, name):
+        return getattr(np, name)
+
+
+def gen_hscg():
+    from sstepcg import classic as ref_classic
+    for name, (mk, kw) in hscg_cases().items():
+        prob = mk()
+        t0 = time.perf_counter()
+        x, tr, co = ref_classic.hscg_solve(prob, **kw)
+        dt = time.perf_counter() - t0
+        rows = []
+        a0 = np.array(co.alphas)
+        horizon = len(a0)
+        for chunk in (7, 64, 1000):
+            ref_classic.np = _DotShim(chunk)
+            try:
+                _, tq, cq = ref_classic.hscg_solve(prob, **kw)
+            finally:
+                ref_classic.np = np
+            aq = np.array(cq.alphas)
+            m = min(len(aq), len(a0))
+            bad = np.nonzero(np.abs(aq[:m] - a0[:m]) > 1e-8 * np.abs(a0[:m]))[0]
+            horizon = min(horizon, int(bad[0]) if len(bad) else m)
+            rows.append([tq.total_iters, tq.converged, tq.stagnated, tq.diverged])
+        save(name, alphas=a0, betas=np.array(co.betas), true_resid=np.array(tr.true_resid),
+             upd_resid=np.array(tr.upd_resid), resid_gap=np.array(tr.resid_gap),
+             c_values=np.array(tr.c_values), psi=np.array(tr.psi),
+             lambda_min=np.array(tr.lambda_min), lambda_max=np.array(tr.lambda_max),
+             flags=np.array([tr.converged, tr.stagnated, tr.diverged, tr.total_iters,
+                             tr.total_outer]),
+             x=x, wall=np.array(dt), cfg=np.array(json.dumps(kw)),
+             noise_counts=np.array(rows, dtype=float), alpha_horizon=np.array(horizon),
+             **({"in_" + k: v for k, v in problem_arrays(prob).items()}
+                if name.startswith(("hscg_spd", "hscg_494")) else {}))
+        print(f"    {name}: iters={tr.total_iters} conv={tr.converged} stag={tr.stagnated} "
+              f"div={tr.diverged} final={tr.final_true_resid:.3e} horizon={horizon} "
+              f"noise iters {sorted(set(int(r[0]) for r in rows))} ({dt:.2f}s)")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     print("reference:", sstepcg.__file__)

@@ -25,6 +25,7 @@ from .types import (  # noqa: F401
 )
 from .adaptive import adaptive_solve, attained_accuracy_report, select_s_tilde  # noqa: F401
 from .sstep import sstep_solve  # noqa: F401
+from .classic import assemble_tridiag, hscg_attainable_accuracy, hscg_solve  # noqa: F401
 from .kernels import (  # noqa: F401
     RitzState,
     assemble_change_of_basis,

@@ -36,7 +36,7 @@ EXPORTS = (
     "sscg_last_error", "sscg_abi_version", "sscg_device_count", "sscg_plan_create",
     "sscg_plan_destroy", "sscg_plan_device_bytes", "sscg_solve", "sscg_load", "sscg_run",
     "sscg_fetch", "sscg_set_profiling", "sscg_get_profile", "sscg_get_small_phases",
-    "sscg_plan_mpk_schedule", "sscg_set_basis_params",
+    "sscg_plan_mpk_schedule", "sscg_set_basis_params", "sscg_hscg",
     "sscg_spmv", "sscg_build_block",
     "sscg_gram", "sscg_recover", "sscg_nested_conds", "sscg_select_s_tilde",
     "sscg_leja_points", "sscg_params_for", "sscg_ritz_sequence", "sscg_sym_eig",
@@ -112,6 +112,7 @@ def _declare(lib):
         "sscg_get_small_phases": (C.c_int, [vp, C.POINTER(i64)]),
         "sscg_plan_mpk_schedule": (C.c_int, [vp, i32, _IP]),
         "sscg_set_basis_params": (C.c_int, [vp, i32, _DP, _DP, _DP]),
+        "sscg_hscg": (C.c_int, [vp, _DP, _DP, dbl, i64, _DP, C.POINTER(SscgLogs)]),
         "sscg_spmv": (C.c_int, [vp, _DP, _DP]),
         "sscg_build_block": (C.c_int, [vp, _DP, _DP, i32, _DP, _DP, _DP, _DP, _DP]),
         "sscg_gram": (C.c_int, [i32, i64, i32, _DP, _DP]),

@@ -56,6 +56,7 @@ struct DevConfig {  // sscg_config + derived constants
   int has_fixed;    // fixed solver: caller's parameters below replace params_for
   double fth[SMAX], fga[SMAX], fmu[SMAX];
   double eps_star, bound_lo, bound_hi, norm_a, norm_abs_a, kappa_a;
+  int64_t max_iters;  // HSCG: classic.py:47 loop bound
   double unit;      // 2^-53 (ritz.py:25)
   double c0;        // MACHINE_UNIT ** -0.5 (ritz.py:124)
   double nu;        // norm_abs_a / norm_a (adaptive.py:119)
@@ -81,6 +82,7 @@ struct SolverState {
   int pad1;
   double best;
   double nb;      // ||b||
+  double hs_rr, hs_alpha, hs_beta;  // HSCG scalars (hscg.cu)
   ParamsDev prm;  // parameters of the block being built
   RitzDev rz;
   double cx[CMAX], cr[CMAX], cp[CMAX];      // recovery coefficients, physical columns
@@ -218,6 +220,10 @@ void launch_state_init(const Ctx& c, cudaStream_t s);
 void launch_small(const Ctx& c, cudaStream_t s);
 void launch_diag_fin(const Ctx& c, int j, cudaStream_t s);
 void launch_params_begin(const Ctx& c, cudaStream_t s);
+// hscg.cu
+void hscg_prepare();
+void launch_hscg_init(const Ctx& c, double* P, double* R, const double* x0, cudaStream_t s);
+void launch_hscg_iter(const Ctx& c, double* P, double* AP, double* R, cudaStream_t s);
 void launch_leja_point(const Ctx& c, int n, cudaStream_t s);
 size_t small_smem_bytes();
 // dist.cu

@@ -109,6 +109,10 @@ struct sscg_plan {
   HaloPlan halo;
   void* comm = nullptr;    // ncclComm_t, or NULL (single GPU / virtual group)
   int partitioned = 0;
+  // HSCG (sscg_hscg): graph of HS_CHUNK iterations, captured for this Y
+  cudaGraphExec_t hs_gexec = nullptr;
+  double* hs_y = nullptr;   // buffers the captured graph points at
+  double* hs_it = nullptr;
   // sscg_set_basis_params (fixed s-step solver)
   int fixed_s = 0;
   double fixed_th[SMAX] = {}, fixed_ga[SMAX] = {}, fixed_mu[SMAX] = {};
@@ -456,6 +460,7 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   CUDA_OK(cudaEventCreate(&p->ev_start));
   CUDA_OK(cudaEventCreate(&p->ev_stop));
   small_prepare();
+  hscg_prepare();
   // launch geometry of the row-streaming kernels: TMA-staged CSR tiles when a
   // tile's segment fits shared memory (every stencil), else the direct kernels
   int sms = NUM_SMS;
@@ -784,6 +789,7 @@ int sscg_plan_destroy(sscg_plan* p) {
   cudaSetDevice(p->device);
   if (p->stream) cudaStreamSynchronize(p->stream);
   if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  if (p->hs_gexec) cudaGraphExecDestroy(p->hs_gexec);
   if (p->comm) nccl_comm_destroy(p->comm);
   HaloPlan& h = p->halo;
   for (void* b : {(void*)h.d_send_idx, (void*)h.d_send_dst, (void*)h.d_send_cnt, (void*)h.d_recv_idx,
@@ -1079,6 +1085,90 @@ int sscg_plan_mpk_schedule(sscg_plan* p, int32_t sigma, int32_t* out) {
   }
   p->wave_passes = saved;  // a query must not invalidate the captured graph
   p->wave_sigma = keep;
+  return SSCG_OK;
+}
+
+// ---- Hestenes-Stiefel CG (classic.py:33-104) ----------------------------------
+namespace {
+constexpr int HS_CHUNK = 16;          // iterations per graph replay
+constexpr int64_t HS_LOG_CAP = 1 << 20;  // device log rows (iterations past it are not logged)
+}  // namespace
+
+int sscg_hscg(sscg_plan* p, const double* b, const double* x0, double eps_star, int64_t max_iters,
+              double* x_out, sscg_logs* logs) {
+  if (!p || !b) return sscg_fail(SSCG_EINVAL, "NULL argument");
+  if (p->partitioned) return sscg_fail(SSCG_EINVAL, "sscg_hscg runs on single-GPU plans");
+  if (!(eps_star >= 0.0)) return sscg_fail(SSCG_EINVAL, "eps_star must be >= 0");
+  if (max_iters < 0) max_iters = 100 * p->n;  // classic.py:46-47
+  CUDA_OK(cudaSetDevice(p->device));
+  TRY(sscg_load(p, b, x0));
+  TRY(ensure_work(p, 1, std::min<int64_t>(max_iters, HS_LOG_CAP), 2));  // Y: p, ap, r
+  DevConfig dc;
+  memset(&dc, 0, sizeof(dc));
+  dc.sigma = 1;
+  dc.eps_star = eps_star;
+  dc.unit = std::ldexp(1.0, -53);
+  dc.c0 = sscg_host_c0();
+  dc.cap_iters = p->cap_iters;
+  dc.cap_outer = p->cap_outer - 1;
+  dc.max_iters = max_iters;
+  CUDA_OK(cudaMemcpyAsync(p->d_cfg, &dc, sizeof(dc), cudaMemcpyHostToDevice, p->stream));
+  CUDA_OK(cudaMemsetAsync(p->d_it, 0xff, sizeof(double) * p->cap_iters * SSCG_IT_N, p->stream));
+  const Ctx c = make_ctx(p);
+  double* P = p->d_Y;
+  double* AP = p->d_Y + p->ld;
+  double* R = p->d_Y + 2 * p->ld;
+  if (!p->hs_gexec || p->hs_y != p->d_Y || p->hs_it != p->d_it) {
+    if (p->hs_gexec) cudaGraphExecDestroy(p->hs_gexec);
+    p->hs_gexec = nullptr;
+    cudaGraph_t g = nullptr;
+    CUDA_OK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < HS_CHUNK; ++i) launch_hscg_iter(c, P, AP, R, p->stream);
+    CUDA_OK(cudaStreamEndCapture(p->stream, &g));
+    const cudaError_t e = cudaGraphInstantiate(&p->hs_gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return sscg_fail_cuda(e, "cudaGraphInstantiate (hscg)");
+    p->hs_y = p->d_Y;
+    p->hs_it = p->d_it;
+  }
+  CUDA_OK(cudaEventRecord(p->ev_start, p->stream));
+  launch_hscg_init(c, P, R, p->d_x0, p->stream);
+  CUDA_OK(cudaGetLastError());
+  // replay chunks, polling `done` one chunk behind (the GPU never waits on the host)
+  const int64_t chunks = (max_iters + HS_CHUNK - 1) / HS_CHUNK;
+  int chunk_id = 0;
+  for (int64_t q = 0; q < chunks; ++q) {
+    CUDA_OK(cudaGraphLaunch(p->hs_gexec, p->stream));
+    const int slot = chunk_id & 1;
+    CUDA_OK(cudaMemcpyAsync(p->h_done + slot, &p->d_st->done, sizeof(int), cudaMemcpyDeviceToHost,
+                            p->stream));
+    CUDA_OK(cudaEventRecord(p->ev_chunk[slot], p->stream));
+    if (chunk_id >= 1) {
+      CUDA_OK(cudaEventSynchronize(p->ev_chunk[slot ^ 1]));
+      if (p->h_done[slot ^ 1]) break;
+    }
+    ++chunk_id;
+  }
+  CUDA_OK(cudaEventRecord(p->ev_stop, p->stream));
+  CUDA_OK(cudaStreamSynchronize(p->stream));
+  CUDA_OK(cudaGetLastError());
+  float ms = 0.f;
+  CUDA_OK(cudaEventElapsedTime(&ms, p->ev_start, p->ev_stop));
+  p->last_ms = ms;
+  if (x_out) CUDA_OK(cudaMemcpy(x_out, p->d_x, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
+  if (logs) {
+    SolverState st;
+    CUDA_OK(cudaMemcpy(&st, p->d_st, sizeof(st), cudaMemcpyDeviceToHost));
+    logs->status = st.done ? st.status : SSCG_EXHAUSTED;
+    logs->total_iters = st.total_iters;
+    logs->total_outer = st.total_iters;
+    logs->n_records = 0;
+    logs->outer_launched = chunk_id + 1;
+    logs->device_ms = ms;
+    const int64_t ni = std::min<int64_t>({(int64_t)st.total_iters, logs->cap_iters, p->cap_iters});
+    if (logs->iters && ni > 0)
+      CUDA_OK(cudaMemcpy(logs->iters, p->d_it, sizeof(double) * ni * SSCG_IT_N, cudaMemcpyDeviceToHost));
+  }
   return SSCG_OK;
 }
 

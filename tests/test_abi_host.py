@@ -194,3 +194,20 @@ def test_build_trace_from_synthetic_logs():
     assert r1.break_j == 0 and r1.s_tilde == 2 and r1.basis_params_used.kind == "newton"
     assert r1.basis_params_used.generated_from == (0.5, 2.0)
     assert tr.outer_records[0].break_j is None
+
+
+def test_assemble_tridiag_host():
+    """classic.py:12-30 on a hand-checked pair list (host helper, no GPU)."""
+    from paper_1908_04081_b200 import CgCoefficients, assemble_tridiag
+    co = CgCoefficients()
+    for a, b in [(0.5, 0.25), (0.25, 4.0), (1.0, 1.0)]:
+        co.append(a, b)
+    t = assemble_tridiag(co, 3)
+    want = np.array([[2.0, 1.0, 0.0],
+                     [1.0, 4.0 + 0.5, 8.0],
+                     [0.0, 8.0, 1.0 + 16.0]])
+    np.testing.assert_allclose(t, want)
+    with pytest.raises(ValueError):
+        assemble_tridiag(co, 0)
+    with pytest.raises(ValueError):
+        assemble_tridiag(co, 4)

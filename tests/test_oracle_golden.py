@@ -258,3 +258,33 @@ def test_fixed_sstep_validation():
     with pytest.raises(O.OracleParamError):
         O.sstep(a.n, a.row_ptr, a.col_idx, a.values, prob.b, prob.x0, 5, 1e-8,
                 params=O.params_monomial(3))
+
+
+# ---- Hestenes-Stiefel CG (classic.py:33-104), SURVEY.md 8(f) row 2 -----------
+HSCG_CASES = ["hscg_c1", "hscg_c1_cap50", "hscg_c3p", "hscg_spd40", "hscg_spd50", "hscg_494bus"]
+
+
+def hscg_problem(name, ref):
+    if name.startswith("hscg_c1"):
+        return problems.make_problem("c1")
+    if name.startswith("hscg_c3p"):
+        return problems.make_problem("c3", scale=24)
+    return problem_from_arrays(ref, "in_")
+
+
+@pytest.mark.parametrize("name", HSCG_CASES)
+def test_hscg_matches_reference(name):
+    ref = golden(name)
+    prob = hscg_problem(name, ref)
+    a = prob.a
+    x, tr, al, be = O.hscg_trace(a.n, a.row_ptr, a.col_idx, a.values, prob.b, prob.x0,
+                                 **cfg_of(ref))
+    flags = ref["flags"]
+    assert [tr.converged, tr.stagnated, tr.diverged] == [bool(v) for v in flags[:3]]
+    assert tr.total_iters == int(flags[3]) and tr.total_outer == int(flags[4])
+    np.testing.assert_array_equal(al, ref["alphas"])
+    np.testing.assert_array_equal(be, ref["betas"])
+    for key in ("true_resid", "upd_resid", "resid_gap", "c_values", "psi", "lambda_min",
+                "lambda_max"):
+        np.testing.assert_array_equal(np.array(getattr(tr, key)), ref[key])
+    np.testing.assert_array_equal(x, ref["x"])
