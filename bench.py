@@ -496,6 +496,59 @@ def run_reference(args, rank, world):
     print(json.dumps(line))
 
 
+def run_solver_compare(args):
+    """--solver sstep|hscg (one GPU, informational, not the driver's headline):
+    the same workload through fixed s-step CG (s = sigma, the config's basis
+    with Ritz-free spectral bounds of the stencil) or Hestenes-Stiefel CG
+    (classic.py: true residual every iteration), device time per solve.
+    `syncs_to_tol` counts the global reductions a multi-GPU run would need:
+    one per outer loop for s-step, two per iteration for HSCG (p.Ap, r.r)."""
+    from paper_1908_04081_b200 import _lib as L, problems
+    from paper_1908_04081_b200.kernels import _plan
+    from paper_1908_04081_b200.sstep import sstep_solve
+    key, scale, sigma, basis, eps, desc = CONFIGS[args.config]
+    prob = problems.make_problem(key, scale=args.scale or scale)
+    n = prob.a.n
+    plan = _plan(prob.a, 0)
+    lib = L.load()
+    b, x0 = L.f64(prob.b), L.f64(prob.x0)
+    ms, iters, syncs, status = [], 0, 0, None
+    with ClockSampler(0) as clk:
+        for k in range(args.warmup + args.steps):
+            if args.solver == "hscg":
+                logs = L.SscgLogs()
+                logs.cap_iters, logs.iters = 0, None
+                L.check(lib.sscg_hscg(plan.handle, L.dptr(b), L.dptr(x0), float(eps), -1, None,
+                                      logs))
+                dev, it, sy = logs.device_ms, int(logs.total_iters), 2 * int(logs.total_iters)
+                status = {L.CONVERGED: "converged", L.STAGNATED: "stagnated",
+                          L.DIVERGED: "diverged"}.get(int(logs.status), "max_iters")
+            else:
+                nx = round(n ** (1.0 / 3.0)) if key in ("c3", "c5") else None
+                lam = (6 - 6 * math.cos(math.pi / (nx + 1)), 6 + 6 * math.cos(math.pi / (nx + 1))) \
+                    if nx else None
+                info = {}
+                s_fixed = args.s or sigma
+                _, tr, _ = sstep_solve(prob, s_fixed, eps, basis_kind=basis, spectral_bounds=lam,
+                                       trace="fast", info=info)
+                dev, it, sy = info["device_ms"], tr.total_iters, tr.total_outer
+                status = ("converged" if tr.converged else "diverged" if tr.diverged
+                          else "stagnated" if tr.stagnated else "max_outer")
+            if k >= args.warmup:
+                ms.append(dev)
+                iters, syncs = it, sy
+    dev_ms = sum(ms) / len(ms)
+    print(json.dumps({
+        "metric": "cg_iterations_per_sec", "value": iters / (dev_ms / 1e3), "unit": "iter/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, seeded", "impl": "ours", "solver": args.solver,
+        "config": {"workload": desc, "n": n, "total_iters": iters, "syncs_to_tol": syncs,
+                   "status": status, "eps_star": eps,
+                   **({"s": args.s or sigma} if args.solver == "sstep" else {})},
+        "clocks": clk.summary()}))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -507,11 +560,16 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the row-partitioned NCCL path even at one GPU")
+    ap.add_argument("--solver", default="adaptive", choices=["adaptive", "sstep", "hscg"],
+                    help="adaptive (the headline); sstep / hscg: one-GPU comparison lines")
+    ap.add_argument("--s", type=int, default=None, help="fixed s for --solver sstep (default sigma)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.solver != "adaptive":
+        run_solver_compare(args)
     else:
         run_ours(args, rank, world)
 

@@ -42,6 +42,10 @@ extern "C" {
 #define SSCG_DIVERGED 3
 #define SSCG_EXHAUSTED 4  /* fixed s-step: max_outer ran out with no verdict (sstep.py:168-171) */
 
+/* device log capacity (rows past it are not logged; the solve itself is not cut) */
+#define SSCG_LOG_CAP_OUTER (1 << 18)
+#define SSCG_LOG_CAP_ITERS (1 << 21)
+
 /* sscg_config.solver */
 #define SSCG_SOLVER_ADAPTIVE 0  /* adaptive_solve (adaptive.py:111-268)             */
 #define SSCG_SOLVER_FIXED 1     /* sstep_solve, fixed s = sigma (sstep.py:79-174)  */

@@ -22,6 +22,7 @@ MAX_SIGMA = 16
 OK, EINVAL, ECUDA, ENOMEM, EPARAM, ENODEV, EBREAKDOWN = range(7)
 RUNNING, CONVERGED, STAGNATED, DIVERGED, EXHAUSTED = range(5)
 SOLVER_ADAPTIVE, SOLVER_FIXED = 0, 1
+LOG_CAP_OUTER, LOG_CAP_ITERS = 1 << 18, 1 << 21  # include/sscg.h SSCG_LOG_CAP_*
 BASIS = {"monomial": 0, "newton": 1, "chebyshev": 2}
 BASIS_NAMES = {v: k for k, v in BASIS.items()}
 CSTRAT = {"adaptive": 0, "unit": 1, "kappa-estimate": 2, "full-bound": 3}

@@ -80,8 +80,8 @@ class LogBuffers:
 
     def __init__(self, cfg):
         sig = cfg.sigma
-        co = int(cfg.max_outer) + 2
-        ci = (int(cfg.max_outer) + 1) * sig + 1
+        co = min(int(cfg.max_outer) + 2, L.LOG_CAP_OUTER)
+        ci = min((int(cfg.max_outer) + 1) * sig + 1, L.LOG_CAP_ITERS)
         self.iters = np.full((ci, L.IT_N), np.nan)
         self.rec_i = np.zeros((co, L.REC_NI), dtype=np.int32)
         self.rec_d = np.full((co, L.RECD_ND), np.nan)
@@ -107,8 +107,9 @@ def build_trace(cfg, logs, trace_level, records=True):
     s = logs.s
     tr = SolveTrace(trace_level=trace_level)
     co = CgCoefficients()
-    nrec = int(s.n_records)
-    nit = int(s.total_iters)
+    # runs longer than the log capacity keep their first rows (trace truncated)
+    nrec = min(int(s.n_records), len(logs.rec_i))
+    nit = min(int(s.total_iters), len(logs.iters))
     it = logs.iters[:nit]
     sig = cfg.sigma
     for r in range(nrec):

@@ -167,8 +167,10 @@ int ensure_work(sscg_plan* p, int sigma, int64_t max_outer, int leja_grid) {
       p->gexec = nullptr;
     }
   }
-  const int64_t co = max_outer + 2;
-  const int64_t ci = (max_outer + 1) * (int64_t)sigma + 1;
+  // log capacity is bounded independently of the loop bound (sstep_solve's
+  // default max_outer is 100 n / s): rows past it are not logged
+  const int64_t co = std::min<int64_t>(max_outer + 2, SSCG_LOG_CAP_OUTER);
+  const int64_t ci = std::min<int64_t>((max_outer + 1) * (int64_t)sigma + 1, SSCG_LOG_CAP_ITERS);
   if (co > p->cap_outer || ci > p->cap_iters) {
     const int64_t nco = co > p->cap_outer ? co : p->cap_outer;
     const int64_t nci = ci > p->cap_iters ? ci : p->cap_iters;

@@ -55,6 +55,10 @@ def test_abi_version_and_constants(lib):
                       ("SSCG_C_FULLBOUND", 3), ("SSCG_EXHAUSTED", L.EXHAUSTED),
                       ("SSCG_SOLVER_FIXED", L.SOLVER_FIXED)]:
         assert re.search(rf"#define {name} {val}\b", txt), name
+    for name, val in [("SSCG_LOG_CAP_OUTER", "(1 << 18)"), ("SSCG_LOG_CAP_ITERS", "(1 << 21)")]:
+        assert f"#define {name} {val}" in txt and eval(val) == getattr(L, name[5:])
+    for name, val in []:
+        assert re.search(rf"#define {name} {val}\b", txt), name
 
 
 def test_struct_layouts_match_c(tmp_path):
