@@ -217,14 +217,19 @@ class Plan:
         return v.value
 
     def mpk_schedule(self, sigma):
-        """Matrix-powers schedule for `sigma` (sscg_plan_mpk_schedule):
-        {"kind": "csr"|"wavefront"|"pattern", "wavefront": bool, "ctas": G,
-         "reach_tiles": L (wavefront), "patterns": P (pattern), "passes": [(levels, lag), ...]}."""
-        out = np.zeros(4 + 2 * 16, dtype=np.int32)
-        check(self._lib.sscg_plan_mpk_schedule(self.handle, int(sigma), iptr(out)))
-        npass = int(out[3])
-        kind = ("csr", "wavefront", "pattern")[int(out[0])]
-        return {"kind": kind, "wavefront": kind == "wavefront", "ctas": int(out[1]),
-                "reach_tiles": int(out[2]) if kind == "wavefront" else 0,
-                "patterns": int(out[2]) if kind == "pattern" else 0,
-                "passes": [(int(out[4 + 2 * q]), int(out[5 + 2 * q])) for q in range(npass)]}
+        """Matrix-powers schedule for `sigma` (see `plan_mpk_schedule`)."""
+        return plan_mpk_schedule(self._lib, self.handle, sigma)
+
+
+def plan_mpk_schedule(lib, handle, sigma):
+    """sscg_plan_mpk_schedule of a plan handle:
+    {"kind": "csr"|"wavefront"|"pattern", "wavefront": bool, "ctas": G,
+     "reach_tiles": L (wavefront), "patterns": P (pattern), "passes": [(levels, lag), ...]}."""
+    out = np.zeros(4 + 2 * 16, dtype=np.int32)
+    check(lib.sscg_plan_mpk_schedule(handle, int(sigma), iptr(out)))
+    npass = int(out[3])
+    kind = ("csr", "wavefront", "pattern")[int(out[0])]
+    return {"kind": kind, "wavefront": kind == "wavefront", "ctas": int(out[1]),
+            "reach_tiles": int(out[2]) if kind == "wavefront" else 0,
+            "patterns": int(out[2]) if kind == "pattern" else 0,
+            "passes": [(int(out[4 + 2 * q]), int(out[5 + 2 * q])) for q in range(npass)]}

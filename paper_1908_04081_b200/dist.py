@@ -70,6 +70,9 @@ class PartPlan:
         L.check(lib.sscg_plan_create_part(C.byref(h), int(device), C.byref(s)))
         self.handle, self.part, self._lib, self._keep = h, part, lib, keep
 
+    def mpk_schedule(self, sigma):
+        return L.plan_mpk_schedule(self._lib, self.handle, sigma)
+
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:
             self._lib.sscg_plan_destroy(self.handle)

@@ -1,0 +1,49 @@
+"""GPU tier: bench.py's own arms at a small scale (wiring, JSON contract),
+so a broken bench path fails the tests rather than the round-end run."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+REQUIRED = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+            "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config"}
+
+
+def _bench(*args, timeout=600):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args],
+                         capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
+    return json.loads(line)
+
+
+def test_bench_default_arm_small(gpu_ready):
+    d = _bench("--scale", "48", "--steps", "1", "--warmup", "1")
+    assert REQUIRED <= set(d) and d["value"] > 0 and d["config"]["converged"]
+    for key in ("roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert key in d
+    assert d["roofline"]["mpk_schedule"]["kind"] == "pattern"
+
+
+def test_bench_partitioned_arm_small(gpu_ready):
+    d = _bench("--partitioned", "--scale", "48", "--steps", "1", "--warmup", "1", "--no-cpu")
+    assert REQUIRED <= set(d) and d["value"] > 0
+
+
+@pytest.mark.parametrize("solver", ["hscg", "sstep"])
+def test_bench_solver_lines_small(gpu_ready, solver):
+    d = _bench("--solver", solver, "--scale", "48", "--steps", "1", "--warmup", "1",
+               *(["--s", "6"] if solver == "sstep" else []))
+    assert d["solver"] == solver and d["config"]["status"] == "converged"
+
+
+def test_bench_reference_arm_small(gpu_ready):
+    d = _bench("--impl", "reference", "--scale", "32", "--steps", "1", "--warmup", "1")
+    assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
