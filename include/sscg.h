@@ -34,6 +34,7 @@ extern "C" {
 #define SSCG_EPARAM 4  /* basis.py:31 ParameterError                      */
 #define SSCG_ENODEV 5  /* no CUDA device: there is no CPU fallback         */
 #define SSCG_EBREAKDOWN 6 /* basis.py:35 BasisBreakdownError (non-finite column) */
+#define SSCG_EFORMAT 7 /* matio.py:14 MatrixMarketError (line: sscg_mm_error_line) */
 
 /* solve outcome (trace.converged / stagnated / diverged, trace.py:43-45) */
 #define SSCG_RUNNING 0
@@ -232,6 +233,26 @@ int sscg_plan_mpk_schedule(sscg_plan* plan, int32_t sigma, int32_t* out);
  * EXHAUSTED when max_iters ran out.  max_iters < 0: 100 n. */
 int sscg_hscg(sscg_plan* plan, const double* b, const double* x0, double eps_star,
               int64_t max_iters, double* x_out, sscg_logs* logs);
+
+/* ---- problem setup (matio.py:104-275) ------------------------------------ */
+/* Matrix Market coordinate text -> full symmetric CSR (read_matrix_market,
+ * matio.py:104-184): parse `len` bytes (the caller reads / gunzips the file),
+ * then copy out row_ptr[n+1], col_idx[nnz], values[nnz] and free.  Errors are
+ * SSCG_EFORMAT with the reference's message; sscg_mm_error_line() gives the
+ * offending line (0: none). */
+typedef struct sscg_mm sscg_mm;
+int sscg_mm_parse(const char* text, int64_t len, sscg_mm** mm, int64_t* n, int64_t* nnz,
+                  int32_t* symmetric);
+int sscg_mm_take(sscg_mm* mm, int64_t* row_ptr, int32_t* col_idx, double* values);
+void sscg_mm_free(sscg_mm* mm);
+int sscg_mm_error_line(void);
+/* _power_iteration (matio.py:229-244) on the device for the plan's operator:
+ * mode 0: A v, 1: |A| v, 2: shift * v - A v.  v0 [n] is the normalised start
+ * vector (the caller's seeded draw).  Outputs the estimate, the iterations used
+ * and whether |lam_k - lam_{k-1}| <= tol |lam_k| was met. */
+int sscg_power_iteration(sscg_plan* plan, int32_t mode, double shift, const double* v0,
+                         int32_t iters, double tol, double* lam, int32_t* iters_used,
+                         int32_t* converged);
 
 /* ---- unit entry points (parity tests; one kernel family each) ------------- */
 /* lacore.py:25-34 spmv: y = A x (scipy csr_matvec rounding, bit for bit) */

@@ -673,6 +673,77 @@ def gen_hscg():
               f"noise iters {sorted(set(int(r[0]) for r in rows))} ({dt:.2f}s)")
 
 
+# ---------------------------------------------------------------------------
+# Problem setup (matio.py:104-307): synthetic Matrix
+# Market files written here, parsed / scaled / normed by the reference
+MM_DIR = os.path.join(OUT, "mm")
+
+
+def _write_mm(path, n, rows, cols, vals, sym="symmetric", field="real", comments=True,
+              fmt="{:.17g}"):
+    lines = [f"%%MatrixMarket matrix coordinate {field} {sym}"]
+    if comments:
+        lines += ["% synthetic test matrix (oracle/make_golden.py gen_matio)", "%", ""]
+    lines.append(f"{n} {n} {len(vals)}")
+    for r, c, v in zip(rows, cols, vals):
+        lines.append(f"{r + 1} {c + 1} " + (str(int(v)) if field == "integer" else fmt.format(v)))
+    text = "\n".join(lines) + "\n"
+    if path.endswith(".gz"):
+        import gzip
+        with gzip.open(path, "wt") as f:
+            f.write(text)
+    else:
+        with open(path, "w") as f:
+            f.write(text)
+
+
+def gen_matio():
+    from scipy import sparse as sp
+    from sstepcg import matio as ref_matio
+    os.makedirs(MM_DIR, exist_ok=True)
+    rng = np.random.default_rng(9001)
+    files = {}
+    # 2-D Poisson 48x48 (n > 2000: shifted power iteration), lower triangle, with comments
+    t = sp.diags([-np.ones(47), 2 * np.ones(48), -np.ones(47)], [-1, 0, 1])
+    lap = (sp.kron(sp.identity(48), t) + sp.kron(t, sp.identity(48))).tocoo()
+    low = lap.row >= lap.col
+    files["poisson48_sym.mtx"] = (2304, lap.row[low], lap.col[low], lap.data[low], "symmetric", "real")
+    # random SPD, general format (both triangles), shuffled entry order
+    m = sp.random(300, 300, density=0.02, random_state=5)
+    m = (m + m.T + sp.identity(300) * 8.0).tocoo()
+    perm = rng.permutation(m.nnz)
+    files["rand300_gen.mtx"] = (300, m.row[perm], m.col[perm], m.data[perm], "general", "real")
+    # integer field, with a duplicated diagonal entry (summed)
+    r = np.array([0, 1, 1, 2, 2, 0, 3, 3])
+    c = np.array([0, 0, 1, 1, 2, 0, 2, 3])
+    v = np.array([4.0, -1.0, 5.0, -2.0, 6.0, 3.0, -1.0, 7.0])
+    files["int4_dup.mtx"] = (4, r, c, v, "symmetric", "integer")
+    # gzipped, values with many digits
+    d = sp.random(120, 120, density=0.05, random_state=7)
+    d = (d + d.T + sp.identity(120) * 3.5).tocoo()
+    lo = d.row >= d.col
+    files["rand120_sym.mtx.gz"] = (120, d.row[lo], d.col[lo], d.data[lo] * np.pi, "symmetric", "real")
+    out = {}
+    for k, (name, (n, rr, cc, vv, sym, fld)) in enumerate(files.items()):
+        path = os.path.join(MM_DIR, name)
+        _write_mm(path, n, rr, cc, vv, sym, fld)
+        a = ref_matio.read_matrix_market(path)
+        ah, dinv = ref_matio.jacobi_precondition(a)
+        est = ref_matio.estimate_operator_norms(ah)
+        out[f"f{k}_name"] = np.array(name)
+        out[f"f{k}_row_ptr"] = a.row_ptr
+        out[f"f{k}_col_idx"] = a.col_idx
+        out[f"f{k}_values"] = a.values
+        out[f"f{k}_jvalues"] = ah.values
+        out[f"f{k}_dinv"] = dinv
+        out[f"f{k}_norms"] = np.array([est.norm_a, est.norm_abs_a, est.kappa_a, est.lambda_min,
+                                       est.iters_used, est.converged])
+        print(f"    {name}: n={a.n} nnz={a.nnz} norms {est.norm_a:.6g} {est.norm_abs_a:.6g} "
+              f"kappa {est.kappa_a:.6g} iters {est.iters_used}")
+    out["nfiles"] = np.array(len(files))
+    save("matio", **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     print("reference:", sstepcg.__file__)

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("SSCG_LIB") or os.path.join(HERE, "_lib", "libsscg.so"
 # keep in sync with include/sscg.h
 ABI_VERSION = 1
 MAX_SIGMA = 16
-OK, EINVAL, ECUDA, ENOMEM, EPARAM, ENODEV, EBREAKDOWN = range(7)
+OK, EINVAL, ECUDA, ENOMEM, EPARAM, ENODEV, EBREAKDOWN, EFORMAT = range(8)
 RUNNING, CONVERGED, STAGNATED, DIVERGED, EXHAUSTED = range(5)
 SOLVER_ADAPTIVE, SOLVER_FIXED = 0, 1
 LOG_CAP_OUTER, LOG_CAP_ITERS = 1 << 18, 1 << 21  # include/sscg.h SSCG_LOG_CAP_*
@@ -38,6 +38,7 @@ EXPORTS = (
     "sscg_plan_destroy", "sscg_plan_device_bytes", "sscg_solve", "sscg_load", "sscg_run",
     "sscg_fetch", "sscg_set_profiling", "sscg_get_profile", "sscg_get_small_phases",
     "sscg_plan_mpk_schedule", "sscg_set_basis_params", "sscg_hscg",
+    "sscg_mm_parse", "sscg_mm_take", "sscg_mm_free", "sscg_mm_error_line", "sscg_power_iteration",
     "sscg_spmv", "sscg_build_block",
     "sscg_gram", "sscg_recover", "sscg_nested_conds", "sscg_select_s_tilde",
     "sscg_leja_points", "sscg_params_for", "sscg_ritz_sequence", "sscg_sym_eig",
@@ -114,6 +115,12 @@ def _declare(lib):
         "sscg_plan_mpk_schedule": (C.c_int, [vp, i32, _IP]),
         "sscg_set_basis_params": (C.c_int, [vp, i32, _DP, _DP, _DP]),
         "sscg_hscg": (C.c_int, [vp, _DP, _DP, dbl, i64, _DP, C.POINTER(SscgLogs)]),
+        "sscg_mm_parse": (C.c_int, [C.c_char_p, i64, C.POINTER(vp), C.POINTER(i64),
+                                    C.POINTER(i64), _IP]),
+        "sscg_mm_take": (C.c_int, [vp, C.POINTER(i64), _IP, _DP]),
+        "sscg_mm_free": (None, [vp]),
+        "sscg_mm_error_line": (C.c_int, []),
+        "sscg_power_iteration": (C.c_int, [vp, i32, dbl, _DP, i32, dbl, _DP, _IP, _IP]),
         "sscg_spmv": (C.c_int, [vp, _DP, _DP]),
         "sscg_build_block": (C.c_int, [vp, _DP, _DP, i32, _DP, _DP, _DP, _DP, _DP]),
         "sscg_gram": (C.c_int, [i32, i64, i32, _DP, _DP]),

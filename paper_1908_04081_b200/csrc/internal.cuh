@@ -220,6 +220,10 @@ void launch_state_init(const Ctx& c, cudaStream_t s);
 void launch_small(const Ctx& c, cudaStream_t s);
 void launch_diag_fin(const Ctx& c, int j, cudaStream_t s);
 void launch_params_begin(const Ctx& c, cudaStream_t s);
+// setup.cu
+void launch_pw_apply(const Ctx& c, int mode, double shift, const double* v, double* out,
+                     const double* dotv, double* res, cudaStream_t s);
+void launch_pw_scale(int64_t n, const double* w, double nw, double* v, cudaStream_t s);
 // hscg.cu
 void hscg_prepare();
 void launch_hscg_init(const Ctx& c, double* P, double* R, const double* x0, cudaStream_t s);

@@ -1174,6 +1174,53 @@ int sscg_hscg(sscg_plan* p, const double* b, const double* x0, double eps_star, 
   return SSCG_OK;
 }
 
+// ---- power iteration (matio.py:229-244) --------------------------------------
+int sscg_power_iteration(sscg_plan* p, int32_t mode, double shift, const double* v0, int32_t iters,
+                         double tol, double* lam_out, int32_t* iters_used, int32_t* converged) {
+  if (!p || !v0 || !lam_out) return sscg_fail(SSCG_EINVAL, "NULL argument");
+  if (p->partitioned) return sscg_fail(SSCG_EINVAL, "power iteration runs on single-GPU plans");
+  if (mode < 0 || mode > 2) return sscg_fail(SSCG_EINVAL, "unknown power-iteration mode %d", mode);
+  CUDA_OK(cudaSetDevice(p->device));
+  TRY(ensure_work(p, 1, 1, 2));  // Y columns: v, w, u
+  const Ctx c = make_ctx(p);
+  double* V = p->d_Y;
+  double* W = p->d_Y + p->ld;
+  double* U = p->d_Y + 2 * p->ld;
+  double* res = p->d_red;  // two scalar slots
+  CUDA_OK(cudaMemcpyAsync(V, v0, sizeof(double) * p->n, cudaMemcpyHostToDevice, p->stream));
+  double lam = 0.0, h[2];
+  int32_t used = iters, conv = 0;
+  for (int32_t it = 1; it <= iters; ++it) {
+    launch_pw_apply(c, mode, shift, V, W, nullptr, res, p->stream);  // w = op(v), w.w
+    CUDA_OK(cudaMemcpyAsync(h, res, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_OK(cudaStreamSynchronize(p->stream));
+    const double nw = std::sqrt(h[0]);  // np.linalg.norm of a vector: sqrt(dot(w, w))
+    if (nw == 0.0) {
+      lam = 0.0;
+      used = it;
+      conv = 1;
+      break;
+    }
+    launch_pw_scale(p->n, W, nw, V, p->stream);                      // v = w / nw
+    launch_pw_apply(c, mode, shift, V, U, V, res + 1, p->stream);    // v . op(v)
+    CUDA_OK(cudaMemcpyAsync(h + 1, res + 1, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_OK(cudaStreamSynchronize(p->stream));
+    const double nl = h[1];
+    if (lam != 0.0 && std::fabs(nl - lam) <= tol * std::fabs(nl)) {
+      lam = nl;
+      used = it;
+      conv = 1;
+      break;
+    }
+    lam = nl;
+  }
+  CUDA_OK(cudaGetLastError());
+  *lam_out = lam;
+  if (iters_used) *iters_used = used;
+  if (converged) *converged = conv;
+  return SSCG_OK;
+}
+
 // ---- virtual-rank group (single process, lock step, no NCCL) ------------------
 int sscg_vgroup_run(sscg_plan* const* plans, int32_t np, const sscg_config* cfg,
                     const double* const* b, const double* const* x0, sscg_logs* logs0) {

@@ -46,6 +46,9 @@ class BreakdownSignal(ValueError):
 
 @dataclass
 class SparseMatrix:
+    """matio.py:28-84: symmetric CSR; the device plan is cached on it like the
+    reference caches its scipy view (`_csr`)."""
+
     n: int
     row_ptr: np.ndarray
     col_idx: np.ndarray
@@ -53,10 +56,49 @@ class SparseMatrix:
     n_a: int
     is_symmetric: bool = True
     _plan: object = field(default=None, repr=False, compare=False)
+    _csr: object = field(default=None, repr=False, compare=False)
 
     @property
     def nnz(self):
         return len(self.values)
+
+    def as_csr(self):
+        """scipy CSR view, built once and cached (host helper)."""
+        if self._csr is None:
+            import scipy.sparse as sp
+            self._csr = sp.csr_matrix((self.values, self.col_idx, self.row_ptr),
+                                      shape=(self.n, self.n))
+        return self._csr
+
+    def row_max(self):
+        """Largest stored entry of each row (signed; -inf for an empty row)."""
+        out = np.full(self.n, -np.inf)
+        lens = np.diff(self.row_ptr)
+        nz = lens > 0
+        if np.any(nz):
+            out[nz] = np.maximum.reduceat(np.asarray(self.values), np.asarray(self.row_ptr)[:-1][nz])
+        return out
+
+    def to_dense(self):
+        return self.as_csr().toarray()
+
+    def pattern_is_symmetric(self):
+        c = self.as_csr()
+        return ((c != 0) - (c.T != 0)).nnz == 0
+
+    def validate(self):
+        """matio.py:70-84 structural invariants; raises ValueError."""
+        if len(self.row_ptr) != self.n + 1:
+            raise ValueError("row_ptr length must be n+1")
+        if np.any(np.diff(self.row_ptr) < 0):
+            raise ValueError("row_ptr must be monotone nondecreasing")
+        if len(self.col_idx) and (self.col_idx.min() < 0 or self.col_idx.max() >= self.n):
+            raise ValueError("col_idx out of range")
+        true_na = int(np.diff(self.row_ptr).max()) if self.n else 0
+        if self.n_a != true_na:
+            raise ValueError(f"n_a={self.n_a} but true max row population is {true_na}")
+        if self.is_symmetric and not self.pattern_is_symmetric():
+            raise ValueError("flagged symmetric but stored pattern is not")
 
 
 @dataclass
