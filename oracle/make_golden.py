@@ -744,6 +744,29 @@ def gen_matio():
     save("matio", **out)
 
 
+def gen_grid():
+    """The reference's run_grid (harness.py:103-154) on a synthetic MM file:
+    rows and summary tables for tests/test_gpu_harness.py."""
+    import tempfile
+    from sstepcg import harness as ref_harness
+    spec = ref_harness.ExperimentSpec(
+        matrices=[(os.path.join(MM_DIR, "rand300_gen.mtx"), "rand300")], s_values=[4, 8],
+        eps_modes=["hscg-attainable", 1e-8], basis_kinds=["newton", "chebyshev"],
+        c_strategies=["adaptive"])
+    with tempfile.TemporaryDirectory() as tmp:
+        rows = ref_harness.run_grid(spec, tmp)
+        md = ref_harness.emit_summary_table(rows, "markdown", os.path.join(tmp, "t.md"))
+        table = open(md).read()
+    save("grid_rand300",
+         keys=np.array([f"{r.algorithm}|{r.basis}|{r.c_strategy}|{r.s}" for r in rows]),
+         eps=np.array([r.eps_star for r in rows]), outcome=np.array([r.outcome for r in rows]),
+         iters=np.array([r.total_iters for r in rows]), outer=np.array([r.total_outer for r in rows]),
+         cell=np.array([r.cell for r in rows]), table=np.array(table))
+    for r in rows:
+        print(f"    {r.algorithm:18s} {r.basis:9s} s={r.s:2d} eps={r.eps_star:.2e} {r.outcome:10s} "
+              f"{r.cell}")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     print("reference:", sstepcg.__file__)

@@ -215,3 +215,31 @@ def test_assemble_tridiag_host():
         assemble_tridiag(co, 0)
     with pytest.raises(ValueError):
         assemble_tridiag(co, 4)
+
+
+def test_harness_formats_host(tmp_path):
+    """emit_trace_csv / emit_summary_table / round_up_2sig (harness.py) on a
+    hand-built trace -- host formatting, no GPU."""
+    from paper_1908_04081_b200 import SolveTrace
+    from paper_1908_04081_b200.harness import (ExperimentSpec, ResultRow, emit_summary_table,
+                                               emit_trace_csv, round_up_2sig)
+    assert round_up_2sig(2.31e-16) == pytest.approx(2.4e-16)
+    assert round_up_2sig(0.0) == 0.0
+    tr = SolveTrace()
+    for s_k in (2, 1):
+        tr.mark_outer(s_k)
+        for _ in range(s_k):
+            tr.record_iteration(0.5, 0.25, 1e-3, 2.0, 0.1, 3.0, 0.9)
+    path = emit_trace_csv(tr, str(tmp_path / "t.csv"))
+    lines = open(path).read().splitlines()
+    assert lines[1] == "1,1,2,0.5,0.25,0.001,0.10000000000000001,3,2"
+    assert lines[3].startswith("3,2,1,")
+    rows = [ResultRow("m", "hscg", "", "", 0, 1e-8, "9 (9)", "converged", 9, 9, 1e-9),
+            ResultRow("m", "sstep", "monomial", "", 4, 1e-8, "3 (10)", "converged", 10, 3, 1e-9)]
+    md = open(emit_summary_table(rows, "markdown", str(tmp_path / "s.md"))).read()
+    assert md.splitlines()[0] == "| m eps*=1.00e-08 | s=4 |"
+    assert "| sstep monomial | 3 (10) |" in md and "| hscg | 9 (9) |" in md
+    with pytest.raises(ValueError):
+        ExperimentSpec(matrices=[])
+    with pytest.raises(ValueError):
+        ExperimentSpec(matrices=["x"], algorithms=["cg"])
