@@ -134,6 +134,8 @@ struct Ctx {
   int pid_bytes;     // 1 (<= 256 patterns) or 2
   int pat_np, pat_ne;
   int pat_grid;      // CTAs of the pattern kernels of levels >= 1 (level 0: red_n)
+  int win_r;         // windowed pattern kernels: near radius R (-1: not used)
+  int win_grid;      // CTAs of the windowed kernels of levels >= 1
   const int* pat_ptr;
   const int* pat_off;
   const double* pat_val;
@@ -199,6 +201,8 @@ void launch_block_levels(const int* rp, const int* col, const double* val, int64
 void launch_diag_resid(const Ctx& c, int j, cudaStream_t s);
 size_t staged_smem_bytes(int cap);
 size_t pattern_smem_bytes(int np, int ne);
+size_t window_smem_bytes(int np, int ne, int r, int nvw, int pid_bytes);
+int window_ctas_per_sm(int np, int ne, int r, int pid_bytes, int* out2);
 void pattern_prepare();
 int pattern_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 void staged_prepare(int cap);

@@ -554,6 +554,216 @@ __global__ void PAT_LB k_level_pat(Ctx c, int l) {
 }
 
 // ---------------------------------------------------------------------------
+// Windowed pattern kernels.  A CTA walks 256-row tiles; for each tile one TMA
+// bulk copy per input vector brings the contiguous window [base - R,
+// base + 256 + R) into shared memory (with the tile's row ids), double
+// buffered under an mbarrier, so every column within R of its row (the
+// diagonal, +-1, +-nx of a stencil) is a shared-memory read; only farther
+// columns are gathered from L2.  Same row arithmetic and order as the other
+// kernels: bit-identical.
+constexpr int WT = MT_ROWS;  // 256 rows per tile
+
+__host__ __device__ __forceinline__ int win_len(int r) { return WT + 2 * r; }
+__host__ __device__ __forceinline__ size_t win_stage_bytes(int r, int nvw, int pid_bytes) {
+  return ((size_t)nvw * win_len(r) * 8 + (size_t)WT * pid_bytes + 15) / 16 * 16;
+}
+__host__ __device__ __forceinline__ size_t win_table_bytes(int np, int ne) {
+  return (pattern_smem_bytes_dev(np, ne) + 15) / 16 * 16;
+}
+
+template <int NVW, typename ID>
+struct WinPipe {
+  unsigned char* base;  // stage 0
+  size_t sb;
+  uint64_t* bars;
+  int r, wl;
+  __device__ __forceinline__ double* win(int s, int q) const {
+    return reinterpret_cast<double*>(base + s * sb) + (size_t)q * wl;
+  }
+  __device__ __forceinline__ const ID* ids(int s) const {
+    return reinterpret_cast<const ID*>(base + s * sb + (size_t)NVW * wl * 8);
+  }
+  // thread 0: stage tile `tile` of the vectors into buffer s
+  __device__ __forceinline__ void issue(const Ctx& c, const double* const* vecs, int64_t tile, int s) const {
+    const int64_t t0 = tile * WT;
+    const int64_t lo = t0 - r > 0 ? t0 - r : 0;
+    const int64_t hi = t0 + WT + r < c.ld ? t0 + WT + r : c.ld;
+    const uint32_t vb = (uint32_t)((hi - lo) * 8);
+    const uint32_t ib = (uint32_t)(WT * sizeof(ID));
+    mbar_arrive_tx(&bars[s], NVW * vb + ib);
+#pragma unroll
+    for (int q = 0; q < NVW; ++q) bulk_g2s(win(s, q) + (lo - (t0 - r)), vecs[q] + lo, vb, &bars[s]);
+    bulk_g2s((void*)ids(s), reinterpret_cast<const ID*>(c.pid) + t0, ib, &bars[s]);
+  }
+};
+
+// row sum of NV staged vectors: near columns from the window, far ones gathered
+template <int NV, int NVW, typename ID>
+__device__ __forceinline__ void row_dot_win(const PatSmem& T, const WinPipe<NVW, ID>& W, int s,
+                                            int b, int e, int i, int tid,
+                                            const double* const* __restrict__ xs, double* acc) {
+  constexpr int B = NV >= 3 ? 4 : 8;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  const int r = W.r;
+  for (int jj = b; jj < e; jj += B) {
+    const int m = e - jj;
+    double xb[NV][B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int off = T.off[jj + (k < m ? k : 0)];
+      const bool near = off >= -r && off <= r;
+      if (near) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) xb[q][k] = W.win(s, q)[tid + r + off];
+      } else {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) xb[q][k] = __ldg(xs[q] + i + off);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (k < m) {
+        const double v = T.val[jj + k];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v, xb[q][k]));
+      }
+    }
+  }
+}
+
+template <int NVW, typename ID, class Body>
+__device__ __forceinline__ void win_tiles(const Ctx& c, int64_t nrows, const double* const* vecs,
+                                          Body&& body) {
+  extern __shared__ __align__(16) double psm[];
+  __shared__ __align__(8) uint64_t bars[2];
+  const PatSmem T = load_patterns(c);
+  WinPipe<NVW, ID> W;
+  W.base = reinterpret_cast<unsigned char*>(psm) + win_table_bytes(c.pat_np, c.pat_ne);
+  W.r = c.win_r;
+  W.wl = win_len(c.win_r);
+  W.sb = win_stage_bytes(c.win_r, NVW, sizeof(ID));
+  W.bars = bars;
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (nrows + WT - 1) / WT;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < 2; ++s) {
+      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+      if (t < ntiles) W.issue(c, vecs, t, s);
+    }
+  int64_t k = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int s = (int)(k & 1);
+    mbar_wait(&bars[s], (uint32_t)((k >> 1) & 1));
+    const int64_t i = tile * WT + tid;
+    if (i < nrows) body(T, W, s, i, tid, (int)W.ids(s)[tid]);
+    __syncthreads();  // stage s free
+    if (tid == 0) {
+      const int64_t t = tile + 2 * (int64_t)gridDim.x;
+      if (t < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        W.issue(c, vecs, t, s);
+      }
+    }
+  }
+}
+
+template <typename ID>
+__global__ void __launch_bounds__(WT) k_level0_win(Ctx c) {
+  __shared__ double sm[WT / 32];
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[0], ga = st->prm.ga[0];
+  const bool do_r = sbar >= 2;
+  const double* P0 = c.Y;
+  double* P1 = c.Y + c.ld;
+  const double* R0 = c.Y + (int64_t)(sigma + 1) * c.ld;
+  double* R1 = c.Y + (int64_t)(sigma + 2) * c.ld;
+  double tt = 0.0, rr = 0.0;
+  int bad = 0;
+  const int64_t n_own = c.n_own, plim = lvl_p_rows(c, sigma, 0), rlim = lvl_r_rows(c, sigma, 0);
+  const double* vecs[3] = {c.x, P0, R0};
+  win_tiles<3, ID>(c, plim, vecs, [&](const PatSmem& T, const WinPipe<3, ID>& W, int s, int64_t i,
+                                      int tid, int pid) {
+    const int b = T.ptr[pid], e = T.ptr[pid + 1];
+    const double p = W.win(s, 1)[tid + W.r], r = W.win(s, 2)[tid + W.r];
+    double acc[3];
+    if (do_r)
+      row_dot_win<3>(T, W, s, b, e, (int)i, tid, vecs, acc);
+    else
+      row_dot_win<2>(T, W, s, b, e, (int)i, tid, vecs, acc);
+    if (i < n_own) {
+      const double t = __dsub_rn(c.b[i], acc[0]);
+      tt = fma(t, t, tt);
+      rr = fma(r, r, rr);
+    }
+    const double wp = recur(acc[1], p, 0.0, th, ga, 0.0, false);
+    P1[i] = wp;
+    bad |= !finite(wp);
+    if (do_r && i < rlim) {
+      const double wr = recur(acc[2], r, 0.0, th, ga, 0.0, false);
+      R1[i] = wr;
+      bad |= !finite(wr);
+    }
+  });
+  tt = block_sum<WT>(tt, sm);
+  rr = block_sum<WT>(rr, sm);
+  if (threadIdx.x == 0) {
+    c.part_t[blockIdx.x] = tt;
+    c.part_r[blockIdx.x] = rr;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+template <typename ID>
+__global__ void __launch_bounds__(WT) k_level_win(Ctx c, int l) {
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  if (l >= sbar) return;
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[l], ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
+  const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
+  const bool do_r = l < sbar - 1;
+  const double* Pl = c.Y + (int64_t)l * c.ld;
+  const double* Pm = Pl - c.ld;
+  double* Pn = c.Y + (int64_t)(l + 1) * c.ld;
+  const double* Rl = c.Y + (int64_t)(sigma + 1 + l) * c.ld;
+  const double* Rm = Rl - c.ld;
+  double* Rn = c.Y + (int64_t)(sigma + 2 + l) * c.ld;
+  int bad = 0;
+  const int64_t plim = lvl_p_rows(c, sigma, l), rlim = lvl_r_rows(c, sigma, l);
+  const double* vecs[2] = {Pl, Rl};
+  win_tiles<2, ID>(c, plim, vecs, [&](const PatSmem& T, const WinPipe<2, ID>& W, int s, int64_t i,
+                                      int tid, int pid) {
+    const int b = T.ptr[pid], e = T.ptr[pid + 1];
+    const bool rrow = do_r && i < rlim;
+    double acc[2];
+    if (rrow)
+      row_dot_win<2>(T, W, s, b, e, (int)i, tid, vecs, acc);
+    else
+      row_dot_win<1>(T, W, s, b, e, (int)i, tid, vecs, acc);
+    const double wp = recur(acc[0], W.win(s, 0)[tid + W.r], use_mu ? Pm[i] : 0.0, th, ga, mu, use_mu);
+    Pn[i] = wp;
+    bad |= !finite(wp);
+    if (rrow) {
+      const double wr = recur(acc[1], W.win(s, 1)[tid + W.r], use_mu ? Rm[i] : 0.0, th, ga, mu, use_mu);
+      Rn[i] = wr;
+      bad |= !finite(wr);
+    }
+  });
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+// ---------------------------------------------------------------------------
 // Level 0 of an outer loop: t = b - A x (norm partial), ||r0||^2 partial,
 // P_1 and (if s_bar >= 2) R_1.
 __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0(Ctx c) {
@@ -850,7 +1060,44 @@ int pattern_ctas_per_sm(int np, int ne, int pid_bytes, int* out2) {
   return a < b ? a : b;
 }
 
+size_t window_smem_bytes(int np, int ne, int r, int nvw, int pid_bytes) {
+  return win_table_bytes(np, ne) + 2 * win_stage_bytes(r, nvw, pid_bytes);
+}
+
+int window_ctas_per_sm(int np, int ne, int r, int pid_bytes, int* out2) {
+  const size_t b0 = window_smem_bytes(np, ne, r, 3, pid_bytes), b1 = window_smem_bytes(np, ne, r, 2, pid_bytes);
+  const int lim = 200 * 1024;
+  if (pid_bytes == 1) {
+    cudaFuncSetAttribute(k_level0_win<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(k_level_win<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&out2[0], k_level0_win<uint8_t>, WT, b0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&out2[1], k_level_win<uint8_t>, WT, b1);
+  } else {
+    cudaFuncSetAttribute(k_level0_win<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(k_level_win<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&out2[0], k_level0_win<uint16_t>, WT, b0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&out2[1], k_level_win<uint16_t>, WT, b1);
+  }
+  return out2[0] < out2[1] ? out2[0] : out2[1];
+}
+
 void launch_level(const Ctx& c, int level, cudaStream_t s) {
+  if (c.pid && c.win_r >= 0) {
+    const int nvw = level == 0 ? 3 : 2;
+    const size_t bytes = window_smem_bytes(c.pat_np, c.pat_ne, c.win_r, nvw, c.pid_bytes);
+    if (c.pid_bytes == 1) {
+      if (level == 0)
+        k_level0_win<uint8_t><<<c.red_n, WT, bytes, s>>>(c);
+      else
+        k_level_win<uint8_t><<<c.win_grid, WT, bytes, s>>>(c, level);
+    } else {
+      if (level == 0)
+        k_level0_win<uint16_t><<<c.red_n, WT, bytes, s>>>(c);
+      else
+        k_level_win<uint16_t><<<c.win_grid, WT, bytes, s>>>(c, level);
+    }
+    return;
+  }
   if (c.pid) {
     const size_t bytes = pattern_smem_bytes(c.pat_np, c.pat_ne);
     if (c.pid_bytes == 1) {

@@ -131,6 +131,7 @@ struct sscg_plan {
   void* d_pid = nullptr;
   int pid_bytes = 0;
   int pat_np = 0, pat_ne = 0, pat_grid = 0;
+  int win_r = -1, win_grid = 0;
   int* d_pat_ptr = nullptr;
   int* d_pat_off = nullptr;
   double* d_pat_val = nullptr;
@@ -238,6 +239,8 @@ Ctx make_ctx(sscg_plan* p) {
   c.pat_np = p->pat_np;
   c.pat_ne = p->pat_ne;
   c.pat_grid = p->pat_grid;
+  c.win_r = p->win_r;
+  c.win_grid = p->win_grid;
   c.pat_ptr = p->d_pat_ptr;
   c.pat_off = p->d_pat_off;
   c.pat_val = p->d_pat_val;
@@ -499,6 +502,7 @@ const char* env_or(const char* name, const char* dflt) {
 // entry.  Used when the table is small (shared memory, 1-2 byte ids);
 // otherwise the CSR kernels run.  SSCG_PATTERN=0 disables it (A/B tests).
 constexpr int PAT_MAX_BYTES = 16 * 1024;
+constexpr int WIN_R_CAP = 512;  // near columns: within 512 rows (window <= 1280 rows per vector)
 
 int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
                   const double* values) {
@@ -555,12 +559,16 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
   if (p->pid_bytes == 1) {
     std::vector<uint8_t> i8(ids.begin(), ids.end());
     uint8_t* d = nullptr;
-    TRY(dalloc(p, &d, (size_t)n_rows));
+    const size_t padded = (size_t)round_up(n_rows, 256);  // whole tiles for the window kernels' bulk copies
+    TRY(dalloc(p, &d, padded));
+    CUDA_OK(cudaMemset(d, 0, padded));
     CUDA_OK(cudaMemcpy(d, i8.data(), (size_t)n_rows, cudaMemcpyHostToDevice));
     p->d_pid = d;
   } else {
     uint16_t* d = nullptr;
-    TRY(dalloc(p, &d, (size_t)n_rows));
+    const size_t padded = (size_t)round_up(n_rows, 256);
+    TRY(dalloc(p, &d, padded));
+    CUDA_OK(cudaMemset(d, 0, 2 * padded));
     CUDA_OK(cudaMemcpy(d, ids.data(), 2 * (size_t)n_rows, cudaMemcpyHostToDevice));
     p->d_pid = d;
   }
@@ -579,6 +587,21 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
   const int64_t tiles = (n_rows + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
   p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * occ[0], (int64_t)RED_BLOCKS, tiles}));
   p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ[1], tiles));
+  // windowed kernels: near radius = the largest |offset| up to WIN_R_CAP (even)
+  p->win_r = -1;
+  if (atoi(env_or("SSCG_PAT_WIN", "0")) != 0) {  // opt-in: measured slower, DESIGN.md 4b
+    int r = 0;
+    for (int v : off)
+      if (std::abs(v) <= WIN_R_CAP) r = std::max(r, std::abs(v));
+    r = (r + 1) & ~1;
+    int wocc[2] = {0, 0};
+    window_ctas_per_sm(np, ne, r, p->pid_bytes, wocc);
+    if (wocc[0] >= 1 && wocc[1] >= 1) {
+      p->win_r = r;
+      p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * wocc[0], (int64_t)RED_BLOCKS, tiles}));
+      p->win_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * wocc[1], tiles));
+    }
+  }
   return SSCG_OK;
 }
 

@@ -244,6 +244,10 @@ __device__ __forceinline__ void row_dot_s(const TileStage& ts, int beg, int end,
 // two input and two output basis entries) instead of ~120 with CSR.  The row
 // sum is the same sequence of rounded multiply-adds as csr_matvec -- same
 // columns, values and order -- hence bit-identical to the CSR kernels.
+__host__ __device__ __forceinline__ size_t pattern_smem_bytes_dev(int np, int ne) {
+  return (size_t)ne * 12 + (size_t)(np + 1) * 4;
+}
+
 struct PatSmem {
   const double* val;
   const int* off;

@@ -110,3 +110,27 @@ def test_pattern_full_trace_and_partitioned_agree(gpu_ready):
     prob = problems.make_problem("c3", scale=24)
     xg, tg, cg, _ = VirtualGroup(CsrRows.of(prob.a), 1, depth=10).solve(prob, AdaptiveConfig(**kw))
     np.testing.assert_array_equal(xg, ref[0])
+
+
+@pytest.mark.parametrize("name,make,kw,kind", CASES[:4], ids=[c[0] for c in CASES[:4]])
+def test_windowed_pattern_kernels_bit_identical(gpu_ready, name, make, kw, kind):
+    """The opt-in windowed kernels (SSCG_PAT_WIN=1: vector windows staged by
+    TMA, near columns from shared memory) reproduce the CSR solve bit for bit."""
+    cfg = AdaptiveConfig(**kw)
+
+    def run():
+        prob = make()
+        return adaptive_solve(prob, cfg, trace="fast")
+
+    ref = _with_env({"SSCG_PATTERN": "0"}, run)
+    old = os.environ.get("SSCG_PAT_WIN")
+    os.environ["SSCG_PAT_WIN"] = "1"
+    try:
+        got = run()
+    finally:
+        if old is None:
+            os.environ.pop("SSCG_PAT_WIN", None)
+        else:
+            os.environ["SSCG_PAT_WIN"] = old
+    np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
+    np.testing.assert_array_equal(got[0], ref[0])

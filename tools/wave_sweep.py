@@ -20,7 +20,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1908_04081_b200 import AdaptiveConfig, _lib as L, problems  # noqa: E402
 from paper_1908_04081_b200.adaptive import LogBuffers, make_config  # noqa: E402
 
-KEYS = ("SSCG_WAVE", "SSCG_WAVE_NL", "SSCG_WAVE_CTAS", "SSCG_WAVE_L2_MB")
+KEYS = ("SSCG_WAVE", "SSCG_WAVE_NL", "SSCG_WAVE_CTAS", "SSCG_WAVE_L2_MB", "SSCG_WAVE_SLACK",
+        "SSCG_PATTERN", "SSCG_PAT_WIN")
 
 
 def main():
