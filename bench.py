@@ -458,9 +458,15 @@ def run_reference(args, rank, world):
     from paper_1908_04081_b200 import problems
     from oracle import sscg_oracle as O
     key, scale, sigma, basis, eps, desc = CONFIGS[args.config]
-    prob = problems.make_problem(key, scale=args.scale or scale, world=world)
+    # One step = one outer loop of the CPU port on ONE slab-sized problem (for
+    # c5w the 256^3 slab every rank owns): the CPU cost of an outer loop of the
+    # global 256x256x(256N) problem is N times that (linear in rows), and the
+    # metric, like ours, counts per-slab iterations summed over the N slabs:
+    # value = N * total_N / ((outer_N + 1) * N * t_slab) = total_N / ((outer_N + 1) t_slab).
+    prob = problems.make_problem(key, scale=args.scale or scale, world=1)
     cfg_kw = dict(sigma=sigma, eps_star=eps, basis_kind=basis)
-    # outer / total counts of the full solve (measured on the GPU, parity-tested)
+    # outer / total counts of the full global solve (GPU-measured, parity-tested:
+    # tools/measure_counts.py)
     counts = {}
     cpath = os.path.join(ROOT, "profiles", "counts.json")
     if os.path.exists(cpath):
@@ -486,10 +492,11 @@ def run_reference(args, rank, world):
         "config": {"workload": desc, "n": prob.a.n, "nnz": prob.a.nnz},
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cpu_threads()[0], "kind": "port",
                          "threads_note": cpu_threads()[1],
-                         "sample": f"each step = 1 outer loop of the oracle port on the full "
-                                   f"problem ({t1:.2f}s); iters/s = {total} iters / "
-                                   f"(({outer}+1) outer x step time), counts from "
-                                   "profiles/counts.json"},
+                         "sample": f"each step = 1 outer loop of the oracle port on one "
+                                   f"{prob.a.n}-row slab ({t1:.2f}s); the global N={world} "
+                                   f"solve takes {outer}+1 outer loops of N x that; value = "
+                                   f"N x {total} iters / its time (per-slab iterations summed, "
+                                   "as the GPU arm); counts from profiles/counts.json"},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
