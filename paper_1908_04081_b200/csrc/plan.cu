@@ -404,6 +404,7 @@ namespace {
 // shared constructor: n_rows local rows carry matrix rows, n_own of them are
 // owned, n_local rows (>= n_rows) is the vector length; lvl[d] = rows with
 // ghost depth <= d (d = 0..depth)
+const char* env_or(const char* name, const char* dflt);
 int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64_t n_local,
               int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx, const double* values,
               const int64_t* lvl, int depth) {
@@ -477,11 +478,16 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   }
   const int64_t cap = (maxt + 4 + 3) / 4 * 4;
   const int64_t ntiles = (n_rows + MT_ROWS - 1) / MT_ROWS;
-  if (staged_smem_bytes((int)cap) <= 200 * 1024) {
+  // staged CSR tiles only while at least 3 CTAs fit an SM (long rows make the
+  // tiles large: 27-point rows give 1 CTA/SM, where the direct kernels win)
+  const int staged_max = atoi(env_or("SSCG_STAGE_MAX_KB", "200"));  // A/B: 0 = direct kernels
+  int per_sm = 0;
+  if (staged_smem_bytes((int)cap) <= (size_t)staged_max * 1024) {
+    staged_prepare((int)cap);
+    per_sm = staged_ctas_per_sm((int)cap);
+  }
+  if (per_sm >= std::max(1, atoi(env_or("SSCG_STAGE_MIN_CTAS", "3")))) {
     p->stage_cap = (int)cap;
-    staged_prepare(p->stage_cap);
-    int per_sm = staged_ctas_per_sm(p->stage_cap);
-    if (per_sm < 1) per_sm = 1;
     p->red_n = (int)std::min<int64_t>({(int64_t)sms * per_sm, (int64_t)RED_BLOCKS, ntiles});
   } else {
     p->stage_cap = 0;

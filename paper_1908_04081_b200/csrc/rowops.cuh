@@ -30,35 +30,52 @@ __device__ __forceinline__ double block_sum(double v, double* sm) {
 }
 
 // csr_matvec row sum for NV right-hand sides sharing one pass over the row
+#ifndef CSR_CHUNK
+#define CSR_CHUNK 4
+#endif
+// csr_matvec row sum from global CSR (direct kernels).  Chunks of CSR_CHUNK
+// entries: the next chunk's col/val loads are issued before this chunk's
+// gathers are consumed, so a long row costs about one load round per chunk
+// instead of two; adds in stored order (a lane past the end adds nothing).
 template <int NV>
 __device__ __forceinline__ void row_dot(const int* __restrict__ col, const double* __restrict__ val,
                                         int beg, int end, const double* const* __restrict__ xs,
                                         double* acc) {
+  constexpr int K = CSR_CHUNK;
 #pragma unroll
   for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-  int jj = beg;
-  for (; jj + 4 <= end; jj += 4) {
-    int c0 = __ldg(col + jj), c1 = __ldg(col + jj + 1), c2 = __ldg(col + jj + 2),
-        c3 = __ldg(col + jj + 3);
-    double v0 = __ldg(val + jj), v1 = __ldg(val + jj + 1), v2 = __ldg(val + jj + 2),
-           v3 = __ldg(val + jj + 3);
+  if (beg >= end) return;
+  int c[K];
+  double v[K];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      double x0 = __ldg(xs[q] + c0), x1 = __ldg(xs[q] + c1), x2 = __ldg(xs[q] + c2),
-             x3 = __ldg(xs[q] + c3);
-      double a = acc[q];
-      a = __dadd_rn(a, __dmul_rn(v0, x0));
-      a = __dadd_rn(a, __dmul_rn(v1, x1));
-      a = __dadd_rn(a, __dmul_rn(v2, x2));
-      a = __dadd_rn(a, __dmul_rn(v3, x3));
-      acc[q] = a;
-    }
+  for (int k = 0; k < K; ++k) {
+    const int j = beg + k < end ? beg + k : end - 1;
+    c[k] = __ldg(col + j);
+    v[k] = __ldg(val + j);
   }
-  for (; jj < end; ++jj) {
-    int c0 = __ldg(col + jj);
-    double v0 = __ldg(val + jj);
+  for (int jj = beg; jj < end; jj += K) {
+    double x[NV][K];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v0, __ldg(xs[q] + c0)));
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int k = 0; k < K; ++k) x[q][k] = __ldg(xs[q] + c[k]);
+    const int m = end - jj;
+    double vc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) vc[k] = v[k];
+    if (jj + K < end) {  // prefetch the next chunk
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int j = jj + K + k < end ? jj + K + k : end - 1;
+        c[k] = __ldg(col + j);
+        v[k] = __ldg(val + j);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (k < m)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(vc[k], x[q][k]));
   }
 }
 

@@ -21,7 +21,7 @@ from paper_1908_04081_b200.types import ProblemInstance, SparseMatrix
 pytestmark = pytest.mark.gpu
 
 ENV_KEYS = ("SSCG_WAVE", "SSCG_WAVE_NL", "SSCG_WAVE_CTAS", "SSCG_WAVE_L2_MB", "SSCG_WAVE_SLACK",
-            "SSCG_PATTERN")
+            "SSCG_PATTERN", "SSCG_STAGE_MIN_CTAS")
 
 
 def _with_env(env, fn):
@@ -61,7 +61,9 @@ CASES = [
      dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
     ("rand", lambda: _random_spd(1500, 5), dict(sigma=6, eps_star=1e-9, basis_kind="monomial")),
 ]
-ON = {"SSCG_WAVE": "1", "SSCG_PATTERN": "0"}  # the wavefront streams CSR tiles
+# the wavefront streams staged CSR tiles: force staging even where the direct
+# kernels would be chosen (long rows, few CTAs per SM)
+ON = {"SSCG_WAVE": "1", "SSCG_PATTERN": "0", "SSCG_STAGE_MIN_CTAS": "1"}
 SCHEDULES = [
     dict(ON),                                         # the L2-budgeted schedule
     dict(ON, SSCG_WAVE_NL="1"),                       # one level per pass

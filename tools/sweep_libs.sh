@@ -9,5 +9,5 @@ for l in sys.stdin:
 "; }
 for lib in ${LIBS:-libsscg.so}; do
   echo "== $lib"
-  SSCG_LIB=paper_1908_04081_b200/_lib/$lib timeout 300 python tools/wave_sweep.py --outer ${OUTER:-10} ${ENVS:-SSCG_WAVE=0} 2>&1 | fmt
+  SSCG_LIB=paper_1908_04081_b200/_lib/$lib timeout 600 python tools/wave_sweep.py --config ${CONFIG:-c5w} --outer ${OUTER:-10} ${ENVS:-SSCG_WAVE=0} 2>&1 | fmt
 done
