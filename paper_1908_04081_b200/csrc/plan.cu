@@ -113,6 +113,7 @@ struct sscg_plan {
   cudaGraphExec_t hs_gexec = nullptr;
   double* hs_y = nullptr;   // buffers the captured graph points at
   double* hs_it = nullptr;
+  int leja_head = 0;  // Leja chain at the start of the outer loop (small operators)
   // sscg_set_basis_params (fixed s-step solver)
   int fixed_s = 0;
   double fixed_th[SMAX] = {}, fixed_ga[SMAX] = {}, fixed_mu[SMAX] = {};
@@ -289,14 +290,32 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     TRY(halo_exchange(p->halo, c, p->comm, s));
     halo_unpack(p->halo, c, s);
   }
-  TRY(launch_mpk(p, c, sigma, s));
+  if (p->leja_head && !p->wave_on) {
+    // small operators: the recovery is too short to hide the Leja chain, so the
+    // chain starts the outer loop on a side branch and level l (l >= 2) joins
+    // point l only -- the levels run as the shifts arrive
+    launch_params_begin(c, s);
+    cudaEventRecord(p->ev_fork, s);
+    cudaStreamWaitEvent(p->side, p->ev_fork, 0);
+    for (int n = 2; n < sigma; ++n) {
+      launch_leja_point(c, n, p->side);
+      cudaEventRecord(p->ev_leja[n], p->side);
+    }
+    for (int l = 0; l < sigma; ++l) {
+      if (l >= 2) cudaStreamWaitEvent(s, p->ev_leja[l], 0);
+      launch_level(c, l, s);
+    }
+  } else {
+    TRY(launch_mpk(p, c, sigma, s));
+  }
   launch_gram(c, 2 * sigma + 1, s);
   if (p->comm) {  // the one synchronisation of the outer loop
     const int k = 2 * sigma + 1;
     TRY(nccl_allreduce(p->comm, c.red_buf, (int64_t)k * (k + 1) / 2 + 2, s));
   }
   launch_small(c, s);
-  capture_params_branch(p, c, sigma, s);
+  const bool tail = !(p->leja_head && !p->wave_on);
+  if (tail) capture_params_branch(p, c, sigma, s);
   if (full) {
     for (int j = 0; j < sigma; ++j) {
       launch_diag_form(c, j, s);
@@ -305,7 +324,7 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     }
   }
   launch_recover(c, s);
-  cudaStreamWaitEvent(s, p->ev_leja[0], 0);
+  if (tail) cudaStreamWaitEvent(s, p->ev_leja[0], 0);
   return SSCG_OK;
 }
 
@@ -494,6 +513,8 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
     p->red_n = (int)std::min<int64_t>((int64_t)sms * 4, (n_rows + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
   }
   if (p->red_n < 1) p->red_n = 1;
+  // where the next block's Leja chain runs (see capture_outer)
+  p->leja_head = atoi(env_or("SSCG_LEJA_HEAD", n_rows < ((int64_t)1 << 20) ? "1" : "0")) != 0;
   return rc;
 }
 
