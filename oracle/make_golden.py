@@ -767,6 +767,31 @@ def gen_grid():
               f"{r.cell}")
 
 
+def gen_nos1_counts():
+    """The paper's nos1 rows on the reference: HSCG and fixed
+    s = 10 at 1e-6, plus the fixed-s run under every Gram-order perturbation
+    (its count moves by 3x: a degree-10 monomial basis at nos1's conditioning)."""
+    from sstepcg.classic import hscg_solve
+    from sstepcg.matio import load_problem
+    from sstepcg.sstep import sstep_solve
+    prob = load_problem("/root/reference/pkg/data/matrices/nos1.mtx", label="nos1")
+    _, th, _ = hscg_solve(prob, 1e-6)
+    orig = ref_basis.gram
+    rows = []
+    for name, spec in [("reference", (None,))] + [(k, v) for k, v in PERTURBATIONS.items()
+                                                  if v[0] is not None]:
+        ref_basis.gram = spec[0] or orig
+        try:
+            _, tr, _ = sstep_solve(prob, 10, 1e-6)
+        finally:
+            ref_basis.gram = orig
+        rows.append([tr.total_outer, tr.total_iters, tr.converged])
+    save("nos1_counts", hscg=np.array([th.total_iters, th.converged]),
+         sstep10=np.array(rows, dtype=float),
+         names=np.array(["reference"] + [k for k, v in PERTURBATIONS.items() if v[0] is not None]))
+    print(f"    hscg {th.total_iters}; sstep s=10 outer/total {[(int(r[0]), int(r[1])) for r in rows]}")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     print("reference:", sstepcg.__file__)
