@@ -108,6 +108,13 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
 
 
+def kernel_name(sched):
+    """The level kernel (levels >= 1) a matrix-powers schedule runs."""
+    if sched["kind"] == "pattern":
+        return {"march": "k_level_zm", "superset": "k_level_ss"}.get(sched.get("form"), "k_level_pat")
+    return {"csr": "k_level_staged", "wavefront": "k_mpk_wave"}[sched["kind"]]
+
+
 def a_bytes_per_level(n, nnz, sched):
     """Bytes of the operator one matrix-powers level must stream: CSR
     (12 nnz + 4 (n+1)) or, for a pattern-compressed plan, the
@@ -378,8 +385,7 @@ def run_ours(args, rank, world):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            kname = {"pattern": "k_level_pat", "csr": "k_level_staged",
-                     "wavefront": "k_mpk_wave"}[sched["kind"]]
+            kname = kernel_name(sched)
             traffic = json.load(open(tpath)).get(args.config, {}).get(kname)
         except Exception:
             traffic = None
@@ -420,9 +426,11 @@ def run_ours(args, rank, world):
         "hbm": {"solve_gbs": solve_gbs, "frac_of_measured": solve_gbs / hbm_peak,
                 "frac_of_8tbs": solve_gbs / 8000.0, "algorithmic_bytes_per_solve": solve_bytes},
         "roofline": {"bound": "hbm",
-                     "kernel": {"wavefront": "k_mpk_wave (wavefront matrix powers + recurrence)",
-                                "pattern": "k_level_pat (pattern-compressed matrix powers + recurrence)",
-                                "csr": "k_level_staged (CSR matrix powers + recurrence)"}[sched["kind"]],
+                     "kernel": kernel_name(sched) + " " + {
+                         "wavefront": "(wavefront matrix powers + recurrence)",
+                         "pattern": "(pattern-compressed matrix powers + recurrence, "
+                                    f"{sched.get('form')} form)",
+                         "csr": "(CSR matrix powers + recurrence)"}[sched["kind"]],
                      "a_bytes_per_level": a_bytes_per_level(n, nnz, sched),
                      "a_bytes_per_level_csr": a_bytes_per_level(n, nnz, None),
                      "mpk_schedule": sched,

@@ -34,6 +34,7 @@
 #define WAVE_THREADS (MT_ROWS + 32) // 8 consumer warps + 1 producer warp
 #define GRAM_BLOCKS (2 * NUM_SMS)  // capacity of the Gram partials
 #define SMALL_THREADS 512
+#define SS_MAX_NE 8                // union size of the unrolled superset-mask pattern kernels
 
 struct RitzDev {  // ritz.py:28-158
   double hi_om, hi_h, hi_zeta;
@@ -139,6 +140,26 @@ struct Ctx {
   const int* pat_ptr;
   const int* pat_off;
   const double* pat_val;
+  // superset-mask form of the same table (plan.cu superset_setup; ss_ne == 0:
+  // not used): every pattern's offsets are a subsequence of the sorted union
+  // ss_off[0..ss_ne), so a row is (mask of present union entries, values per
+  // union slot).  The offsets travel as kernel parameters (constant bank) and
+  // the row loop unrolls fully at compile time.
+  int ss_ne;
+  int ss_off[SS_MAX_NE];
+  // plane-march form (mpk.cu k_level_zm): the union is symmetric, [-S .. 0 .. S]
+  // with S = zm_S >= 256.  Thread t of a CTA owns column c (row mod S) and walks
+  // rows c, c + S, c + 2S, ... of one chunk of zm_zc steps, so the -S / 0 / +S
+  // entries of a row are the previous step's values (registers) and only one
+  // coalesced load per vector per row brings the plane ahead.  zm_S == 0: off.
+  int64_t zm_S;
+  int zm_zc;       // steps per work item
+  int zm_ncb;      // column blocks of 256 columns
+  int64_t zm_items;  // work items = zm_ncb x ceil(steps / zm_zc)
+  int pf_off;    // pattern kernels: L2 prefetch at row + pf_ahead * stride + pf_off (0: off)
+  int pf_ahead;
+  const unsigned* ss_mask;  // [pat_np]
+  const double* ss_val;     // [pat_np][SS_MAX_NE], absent slots 0
 };
 
 // rows level l must produce for P (ghost depth <= sigma-1-l) and R (<= sigma-2-l)
@@ -192,7 +213,7 @@ int sscg_fail(int code, const char* fmt, ...);
 // ---- launchers (defined in the .cu files) ----
 // mpk.cu
 void launch_init_residual(const Ctx& c, const double* x0, cudaStream_t s);
-void launch_level(const Ctx& c, int level, cudaStream_t s);
+void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s);
 void launch_spmv(const int* rp, const int* col, const double* val, int64_t n, const double* x,
                  double* y, cudaStream_t s);
 void launch_block_levels(const int* rp, const int* col, const double* val, int64_t n, int64_t ld,
@@ -205,6 +226,9 @@ size_t window_smem_bytes(int np, int ne, int r, int nvw, int pid_bytes);
 int window_ctas_per_sm(int np, int ne, int r, int pid_bytes, int* out2);
 void pattern_prepare();
 int pattern_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
+size_t ss_smem_bytes(int np);
+int ss_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
+int zm_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 void staged_prepare(int cap);
 int staged_ctas_per_sm(int cap);
 int wave_ctas_per_sm(int cap);

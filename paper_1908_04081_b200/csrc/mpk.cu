@@ -466,6 +466,10 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_pat(Ctx c) {
   int pid_next = i < plim ? row_pattern<ID>(c, i) : 0;  // ids one row ahead
   for (; i < plim; i += stride) {
     const int pid = pid_next;
+    {
+      const double* pf[3] = {c.x, P0, R0};
+      prefetch_next<3>(c, i, stride, pf);
+    }
     if (i + stride < plim) pid_next = row_pattern<ID>(c, i + stride);
     const int b = T.ptr[pid], e = T.ptr[pid + 1];
     const double p = P0[i], r = R0[i];
@@ -532,6 +536,10 @@ __global__ void PAT_LB k_level_pat(Ctx c, int l) {
   int pid_next = i < plim ? row_pattern<ID>(c, i) : 0;  // ids one row ahead
   for (; i < plim; i += stride) {
     const int pid = pid_next;
+    {
+      const double* pf[2] = {Pl, Rl};
+      prefetch_next<2>(c, i, stride, pf);
+    }
     if (i + stride < plim) pid_next = row_pattern<ID>(c, i + stride);
     const int b = T.ptr[pid], e = T.ptr[pid + 1];
     double acc[2];
@@ -549,6 +557,359 @@ __global__ void PAT_LB k_level_pat(Ctx c, int l) {
       Rn[i] = wr;
       bad |= !finite(wr);
     }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+// Superset-mask pattern kernels: k_level0_pat / k_level_pat with the row sum
+// unrolled over the union of offsets (row_dot_m).  Same rows, same order of
+// rounded operations: bit-identical to the table-walking kernels above.
+#ifndef SS_MINB
+#define SS_MINB 0
+#endif
+#if SS_MINB > 0
+#define SS_LB __launch_bounds__(ROWS_PER_CTA, SS_MINB)
+#else
+#define SS_LB __launch_bounds__(ROWS_PER_CTA)
+#endif
+template <typename ID, int NE>
+__global__ void SS_LB k_level0_ss(Ctx c) {
+  __shared__ double sm[ROWS_PER_CTA / 32];
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const SsSmem S = load_ss(c);
+  const int sbar = st->s_bar;
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[0], ga = st->prm.ga[0];
+  const bool do_r = sbar >= 2;
+  const double* P0 = c.Y;
+  double* P1 = c.Y + c.ld;
+  const double* R0 = c.Y + (int64_t)(sigma + 1) * c.ld;
+  double* R1 = c.Y + (int64_t)(sigma + 2) * c.ld;
+  double tt = 0.0, rr = 0.0;
+  int bad = 0;
+  const int64_t n_own = c.n_own, plim = lvl_p_rows(c, sigma, 0), rlim = lvl_r_rows(c, sigma, 0);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int pid_next = i < plim ? row_pattern<ID>(c, i) : 0;
+  for (; i < plim; i += stride) {
+    const int pid = pid_next;
+    {
+      const double* pf[3] = {c.x, P0, R0};
+      prefetch_next<3>(c, i, stride, pf);
+    }
+    if (i + stride < plim) pid_next = row_pattern<ID>(c, i + stride);
+    double acc[3];
+    const double* xs[3] = {c.x, P0, R0};
+    const bool rrow = do_r && i < rlim;
+    if (rrow)
+      row_dot_m<3, NE>(c, S, pid, i, xs, acc);
+    else
+      row_dot_m<2, NE>(c, S, pid, i, xs, acc);
+    const double p = P0[i];
+    if (i < n_own) {
+      const double r = R0[i];
+      const double t = __dsub_rn(c.b[i], acc[0]);
+      tt = fma(t, t, tt);
+      rr = fma(r, r, rr);
+    }
+    const double wp = recur(acc[1], p, 0.0, th, ga, 0.0, false);
+    P1[i] = wp;
+    bad |= !finite(wp);
+    if (rrow) {
+      const double wr = recur(acc[2], R0[i], 0.0, th, ga, 0.0, false);
+      R1[i] = wr;
+      bad |= !finite(wr);
+    }
+  }
+  tt = block_sum<ROWS_PER_CTA>(tt, sm);
+  rr = block_sum<ROWS_PER_CTA>(rr, sm);
+  if (threadIdx.x == 0) {
+    c.part_t[blockIdx.x] = tt;
+    c.part_r[blockIdx.x] = rr;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+template <typename ID, int NE>
+__global__ void SS_LB k_level_ss(Ctx c, int l) {
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  if (l >= sbar) return;
+  const SsSmem S = load_ss(c);
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[l], ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
+  const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
+  const bool do_r = l < sbar - 1;
+  const double* Pl = c.Y + (int64_t)l * c.ld;
+  const double* Pm = Pl - c.ld;
+  double* Pn = c.Y + (int64_t)(l + 1) * c.ld;
+  const double* Rl = c.Y + (int64_t)(sigma + 1 + l) * c.ld;
+  const double* Rm = Rl - c.ld;
+  double* Rn = c.Y + (int64_t)(sigma + 2 + l) * c.ld;
+  int bad = 0;
+  const int64_t plim = lvl_p_rows(c, sigma, l), rlim = lvl_r_rows(c, sigma, l);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int pid_next = i < plim ? row_pattern<ID>(c, i) : 0;
+  for (; i < plim; i += stride) {
+    const int pid = pid_next;
+    {
+      const double* pf[2] = {Pl, Rl};
+      prefetch_next<2>(c, i, stride, pf);
+    }
+    if (i + stride < plim) pid_next = row_pattern<ID>(c, i + stride);
+    double acc[2];
+    const double* xs[2] = {Pl, Rl};
+    const bool rrow = do_r && i < rlim;
+    if (rrow)
+      row_dot_m<2, NE>(c, S, pid, i, xs, acc);
+    else
+      row_dot_m<1, NE>(c, S, pid, i, xs, acc);
+    const double wp = recur(acc[0], Pl[i], use_mu ? Pm[i] : 0.0, th, ga, mu, use_mu);
+    Pn[i] = wp;
+    bad |= !finite(wp);
+    if (rrow) {
+      const double wr = recur(acc[1], Rl[i], use_mu ? Rm[i] : 0.0, th, ga, mu, use_mu);
+      Rn[i] = wr;
+      bad |= !finite(wr);
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Plane-march pattern kernels (Ctx::zm_*).  The union of offsets is
+// [-S, ..., 0, ..., +S] (a stencil: S is the plane stride).  A work item is
+// 256 consecutive columns c (c = row mod S) x zm_zc consecutive steps; each
+// thread walks its column, keeping x[r - S], x[r], x[r + S] in registers, so
+// per row and vector one coalesced load (the plane ahead) replaces three
+// gathers; the other slots are gathered as in row_dot_m.  The adds run over
+// the slots in union order = stored order, absent slots adding +0.0 (exact,
+// see row_dot_m): bit-identical to the other level kernels.
+template <bool UNIT>
+__device__ __forceinline__ double recur_t(double ay, double y, double y2, double th, double ga,
+                                          double mu, bool use_mu) {
+  double w = __dsub_rn(ay, __dmul_rn(th, y));
+  if (use_mu) w = __dsub_rn(w, __dmul_rn(mu, y2));
+  return UNIT ? w : __ddiv_rn(w, ga);
+}
+
+// one column of one work item.  NV input vectors xs[0..NV) (level 0: x, P0, R0
+// with NV = 3; else P_l, R_l with NV = 2, or P_l alone with NV = 1).
+// L0: level 0 (no two-back term; outputs of vectors 1.. ; t = b - A x norms)
+template <typename ID, int NE, int NV, bool L0, bool UNIT>
+__device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, int col, int z0, int z1,
+                                          const double* const* __restrict__ xs,
+                                          const double* const* __restrict__ ym,
+                                          double* const* __restrict__ yo, double th, double ga,
+                                          double mu, bool use_mu, int plim, int rlim, int& bad,
+                                          double& tt, double& rr) {
+  constexpr int KC = NE / 2;
+  constexpr int NO = L0 ? NV - 1 : NV;  // output vectors
+  constexpr int Q0 = L0 ? 1 : 0;        // first input vector with an output
+  // 32-bit row indices (plan.cu enables the march only for n + S < 2^31)
+  // vectors hold ld >= local rows entries (ghost rows of a partitioned plan
+  // have vector entries beyond the rows the matrix stores)
+  const int S = (int)c.zm_S, n = (int)(c.ld < INT32_MAX ? c.ld : INT32_MAX), n_own = (int)c.n_own;
+  int r = z0 * S + col;
+  if (r >= plim) return;
+  // per-thread row pointers, advanced by one plane per step: each gather is
+  // then one wide multiply-add (slot offset x 8 + row pointer)
+  const double* px[NV];
+  double* po[NO];
+  const double* pm[NO];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) px[q] = xs[q] + r;
+#pragma unroll
+  for (int q = 0; q < NO; ++q) {
+    po[q] = yo[q] + r;
+    pm[q] = L0 ? nullptr : ym[q] + r;
+  }
+  int off[NE];
+#pragma unroll
+  for (int k = 0; k < NE; ++k) off[k] = c.ss_off[k];
+  double pv[NV], cu[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    pv[q] = r >= S ? __ldg(px[q] - S) : 0.0;
+    cu[q] = __ldg(px[q]);
+  }
+  const ID* pidp = reinterpret_cast<const ID*>(c.pid) + r;
+  for (int z = z0; z < z1 && r < plim; ++z) {
+    const int pid = (int)__ldg(pidp);
+    const unsigned m = T.mask[pid];
+    const bool rrow = r < rlim;  // the last vector (R) is produced on this row
+    double nx[NV];
+    const bool hasn = r + S < n;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) nx[q] = hasn ? __ldg(px[q] + S) : 0.0;
+    double xb[NV][NE];
+#pragma unroll
+    for (int k = 1; k < NE - 1; ++k) {
+      if (k == KC) continue;
+      const bool on = (m >> k) & 1u;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const bool ld = on && (q < NV - 1 || NV == 1 || rrow);
+        xb[q][k] = ld ? __ldg(px[q] + off[k]) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      xb[q][0] = (m & 1u) ? pv[q] : 0.0;
+      xb[q][KC] = (m & (1u << KC)) ? cu[q] : 0.0;
+      xb[q][NE - 1] = (m & (1u << (NE - 1))) ? nx[q] : 0.0;
+    }
+    const double2* v2 = reinterpret_cast<const double2*>(T.val + pid * SS_MAX_NE);
+    double acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+#pragma unroll
+    for (int k2 = 0; k2 < (NE + 1) / 2; ++k2) {
+      const double2 vv = v2[k2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = 2 * k2 + h;
+        if (k < NE) {
+          const double v = h ? vv.y : vv.x;
+#pragma unroll
+          for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v, xb[q][k]));
+        }
+      }
+    }
+    if (L0 && r < n_own) {
+      const double t = __dsub_rn(c.b[r], acc[0]);
+      tt = fma(t, t, tt);
+      rr = fma(cu[NV - 1], cu[NV - 1], rr);
+    }
+#pragma unroll
+    for (int q = 0; q < NO; ++q) {
+      if (q == NO - 1 && NO > 1 && !rrow) break;
+      const double y2 = (!L0 && use_mu) ? *pm[q] : 0.0;
+      const double w = recur_t<UNIT>(acc[Q0 + q], cu[Q0 + q], y2, th, ga, mu, !L0 && use_mu);
+      *po[q] = w;
+      bad |= !finite(w);
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      pv[q] = cu[q];
+      cu[q] = nx[q];
+      px[q] += S;
+    }
+#pragma unroll
+    for (int q = 0; q < NO; ++q) {
+      po[q] += S;
+      if (!L0) pm[q] += S;
+    }
+    pidp += S;
+    r += S;
+  }
+}
+
+template <typename ID, int NE, int NV, bool L0, bool UNIT>
+__device__ __forceinline__ void zm_items(const Ctx& c, const SsSmem& T, const double* const* xs,
+                                         const double* const* ym, double* const* yo, double th,
+                                         double ga, double mu, bool use_mu, int64_t plim,
+                                         int64_t rlim, int& bad, double& tt, double& rr) {
+  const int items = (int)c.zm_items, ncb = c.zm_ncb, zcs = c.zm_zc, S = (int)c.zm_S;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int cb = it % ncb, zc = it / ncb;
+    const int col = cb * ROWS_PER_CTA + threadIdx.x;
+    if (col >= S) continue;
+    const int z0 = zc * zcs;
+    zm_column<ID, NE, NV, L0, UNIT>(c, T, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu, use_mu,
+                                    (int)plim, (int)rlim, bad, tt, rr);
+  }
+}
+
+// the level's column pointers, formed on the host: kept opaque to the
+// compiler's index arithmetic, so each gather is one wide add off a base
+// register instead of a re-derived column * ld product
+struct ZmPtrs {
+  const double* xs[3];
+  const double* ym[2];
+  double* yo[2];
+};
+
+inline ZmPtrs zm_ptrs(const Ctx& c, int l, int sigma) {
+  ZmPtrs z;
+  const int64_t ld = c.ld;
+  if (l == 0) {
+    z.xs[0] = c.x;
+    z.xs[1] = c.Y;
+    z.xs[2] = c.Y + (int64_t)(sigma + 1) * ld;
+    z.ym[0] = z.ym[1] = nullptr;
+    z.yo[0] = c.Y + ld;
+    z.yo[1] = c.Y + (int64_t)(sigma + 2) * ld;
+  } else {
+    z.xs[0] = c.Y + (int64_t)l * ld;
+    z.xs[1] = c.Y + (int64_t)(sigma + 1 + l) * ld;
+    z.xs[2] = nullptr;
+    z.ym[0] = z.xs[0] - ld;
+    z.ym[1] = z.xs[1] - ld;
+    z.yo[0] = c.Y + (int64_t)(l + 1) * ld;
+    z.yo[1] = c.Y + (int64_t)(sigma + 2 + l) * ld;
+  }
+  return z;
+}
+
+template <typename ID, int NE>
+__global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_zm(Ctx c, ZmPtrs zp) {
+  __shared__ double sm[ROWS_PER_CTA / 32];
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const SsSmem T = load_ss(c);
+  const int sbar = st->s_bar;
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[0], ga = st->prm.ga[0];
+  const bool do_r = sbar >= 2;
+  double* yo[2] = {zp.yo[0], zp.yo[1]};
+  const double* xs[3] = {zp.xs[0], zp.xs[1], zp.xs[2]};
+  double tt = 0.0, rr = 0.0;
+  int bad = 0;
+  const int64_t plim = lvl_p_rows(c, sigma, 0), rlim = do_r ? lvl_r_rows(c, sigma, 0) : 0;
+  if (ga == 1.0)
+    zm_items<ID, NE, 3, true, true>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+  else
+    zm_items<ID, NE, 3, true, false>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+  tt = block_sum<ROWS_PER_CTA>(tt, sm);
+  rr = block_sum<ROWS_PER_CTA>(rr, sm);
+  if (threadIdx.x == 0) {
+    c.part_t[blockIdx.x] = tt;
+    c.part_r[blockIdx.x] = rr;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+template <typename ID, int NE>
+__global__ void __launch_bounds__(ROWS_PER_CTA) k_level_zm(Ctx c, int l, ZmPtrs zp) {
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  if (l >= sbar) return;
+  const SsSmem T = load_ss(c);
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[l], ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
+  const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
+  const bool do_r = l < sbar - 1;
+  const double* xs[2] = {zp.xs[0], zp.xs[1]};
+  const double* ym[2] = {zp.ym[0], zp.ym[1]};
+  double* yo[2] = {zp.yo[0], zp.yo[1]};
+  int bad = 0;
+  double tt = 0.0, rr = 0.0;
+  const int64_t plim = lvl_p_rows(c, sigma, l), rlim = lvl_r_rows(c, sigma, l);
+  if (do_r) {
+    if (ga == 1.0)
+      zm_items<ID, NE, 2, false, true>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, rlim, bad, tt, rr);
+    else
+      zm_items<ID, NE, 2, false, false>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, rlim, bad, tt, rr);
+  } else {
+    if (ga == 1.0)
+      zm_items<ID, NE, 1, false, true>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, plim, bad, tt, rr);
+    else
+      zm_items<ID, NE, 1, false, false>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, plim, bad, tt, rr);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
 }
@@ -1044,6 +1405,67 @@ void pattern_prepare() {
   cudaFuncSetAttribute(k_level_pat<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
+size_t ss_smem_bytes(int np) { return ss_smem_bytes_dev(np); }
+
+int ss_ne_bucket(int ne) { return ne <= 3 ? 3 : ne <= 5 ? 5 : ne <= 7 ? 7 : 8; }
+
+template <typename ID, int NE>
+void ss_occ(size_t bytes, int* a, int* b) {
+  const int lim = 48 * 1024;
+  cudaFuncSetAttribute(k_level0_ss<ID, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_level_ss<ID, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(a, k_level0_ss<ID, NE>, ROWS_PER_CTA, bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, k_level_ss<ID, NE>, ROWS_PER_CTA, bytes);
+}
+
+template <typename ID, int NE>
+void zm_occ(size_t bytes, int* a, int* b) {
+  const int lim = 48 * 1024;
+  cudaFuncSetAttribute(k_level0_zm<ID, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_level_zm<ID, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(a, k_level0_zm<ID, NE>, ROWS_PER_CTA, bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, k_level_zm<ID, NE>, ROWS_PER_CTA, bytes);
+}
+
+// plane-march kernels for a symmetric union of 3, 5 or 7 offsets
+int zm_ctas_per_sm(int np, int ne, int pid_bytes, int* out2) {
+  int a = 0, b = 0;
+  const size_t bytes = ss_smem_bytes_dev(np);
+  if (ne != 3 && ne != 5 && ne != 7) return 0;
+  if (pid_bytes == 1) {
+    if (ne == 3) zm_occ<uint8_t, 3>(bytes, &a, &b);
+    else if (ne == 5) zm_occ<uint8_t, 5>(bytes, &a, &b);
+    else zm_occ<uint8_t, 7>(bytes, &a, &b);
+  } else {
+    if (ne == 3) zm_occ<uint16_t, 3>(bytes, &a, &b);
+    else if (ne == 5) zm_occ<uint16_t, 5>(bytes, &a, &b);
+    else zm_occ<uint16_t, 7>(bytes, &a, &b);
+  }
+  out2[0] = a;
+  out2[1] = b;
+  return a < b ? a : b;
+}
+
+int ss_ctas_per_sm(int np, int ne, int pid_bytes, int* out2) {
+  int a = 0, b = 0;
+  const size_t bytes = ss_smem_bytes_dev(np);
+  const int nb = ss_ne_bucket(ne);
+  if (pid_bytes == 1) {
+    if (nb == 3) ss_occ<uint8_t, 3>(bytes, &a, &b);
+    else if (nb == 5) ss_occ<uint8_t, 5>(bytes, &a, &b);
+    else if (nb == 7) ss_occ<uint8_t, 7>(bytes, &a, &b);
+    else ss_occ<uint8_t, 8>(bytes, &a, &b);
+  } else {
+    if (nb == 3) ss_occ<uint16_t, 3>(bytes, &a, &b);
+    else if (nb == 5) ss_occ<uint16_t, 5>(bytes, &a, &b);
+    else if (nb == 7) ss_occ<uint16_t, 7>(bytes, &a, &b);
+    else ss_occ<uint16_t, 8>(bytes, &a, &b);
+  }
+  out2[0] = a;
+  out2[1] = b;
+  return a < b ? a : b;
+}
+
 // level 0 (the partial-sum kernel) and levels >= 1: out[0], out[1]
 int pattern_ctas_per_sm(int np, int ne, int pid_bytes, int* out2) {
   int a = 0, b = 0;
@@ -1081,7 +1503,7 @@ int window_ctas_per_sm(int np, int ne, int r, int pid_bytes, int* out2) {
   return out2[0] < out2[1] ? out2[0] : out2[1];
 }
 
-void launch_level(const Ctx& c, int level, cudaStream_t s) {
+void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s) {
   if (c.pid && c.win_r >= 0) {
     const int nvw = level == 0 ? 3 : 2;
     const size_t bytes = window_smem_bytes(c.pat_np, c.pat_ne, c.win_r, nvw, c.pid_bytes);
@@ -1095,6 +1517,49 @@ void launch_level(const Ctx& c, int level, cudaStream_t s) {
         k_level0_win<uint16_t><<<c.red_n, WT, bytes, s>>>(c);
       else
         k_level_win<uint16_t><<<c.win_grid, WT, bytes, s>>>(c, level);
+    }
+    return;
+  }
+  if (c.pid && c.ss_ne > 0 && c.zm_S > 0) {
+    const size_t bytes = ss_smem_bytes_dev(c.pat_np);
+    const ZmPtrs zp = zm_ptrs(c, level, sigma);
+#define ZM_LAUNCH(ID, NE)                                                      \
+  if (level == 0)                                                              \
+    k_level0_zm<ID, NE><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp);           \
+  else                                                                         \
+    k_level_zm<ID, NE><<<c.pat_grid, ROWS_PER_CTA, bytes, s>>>(c, level, zp);
+#define ZM_NE_SWITCH(ID)                   \
+  switch (c.ss_ne) {                       \
+    case 3: ZM_LAUNCH(ID, 3) break;        \
+    case 5: ZM_LAUNCH(ID, 5) break;        \
+    default: ZM_LAUNCH(ID, 7) break;       \
+  }
+    if (c.pid_bytes == 1) {
+      ZM_NE_SWITCH(uint8_t)
+    } else {
+      ZM_NE_SWITCH(uint16_t)
+    }
+    return;
+  }
+  if (c.pid && c.ss_ne > 0) {
+    const size_t bytes = ss_smem_bytes_dev(c.pat_np);
+    const int ne = ss_ne_bucket(c.ss_ne);
+#define SS_LAUNCH(ID, NE)                                                      \
+  if (level == 0)                                                              \
+    k_level0_ss<ID, NE><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c);               \
+  else                                                                         \
+    k_level_ss<ID, NE><<<c.pat_grid, ROWS_PER_CTA, bytes, s>>>(c, level);
+#define SS_NE_SWITCH(ID)                   \
+  switch (ne) {                            \
+    case 3: SS_LAUNCH(ID, 3) break;        \
+    case 5: SS_LAUNCH(ID, 5) break;        \
+    case 7: SS_LAUNCH(ID, 7) break;        \
+    default: SS_LAUNCH(ID, 8) break;       \
+  }
+    if (c.pid_bytes == 1) {
+      SS_NE_SWITCH(uint8_t)
+    } else {
+      SS_NE_SWITCH(uint16_t)
     }
     return;
   }

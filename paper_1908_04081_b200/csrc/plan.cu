@@ -136,6 +136,14 @@ struct sscg_plan {
   int* d_pat_ptr = nullptr;
   int* d_pat_off = nullptr;
   double* d_pat_val = nullptr;
+  int pf_off = 0, pf_ahead = 1;  // L2 prefetch of the pattern kernels (0: off)
+  int64_t zm_S = 0;  // plane-march form (0: off)
+  int zm_zc = 0, zm_ncb = 0;
+  int64_t zm_items = 0;
+  int ss_ne = 0;  // superset-mask form (superset_setup); 0: table-walking kernels
+  int ss_off[SS_MAX_NE] = {};
+  unsigned* d_ss_mask = nullptr;
+  double* d_ss_val = nullptr;
 };
 
 namespace {
@@ -245,6 +253,16 @@ Ctx make_ctx(sscg_plan* p) {
   c.pat_ptr = p->d_pat_ptr;
   c.pat_off = p->d_pat_off;
   c.pat_val = p->d_pat_val;
+  c.pf_off = p->pf_off;
+  c.pf_ahead = p->pf_ahead;
+  c.zm_S = p->zm_S;
+  c.zm_zc = p->zm_zc;
+  c.zm_ncb = p->zm_ncb;
+  c.zm_items = p->zm_items;
+  c.ss_ne = p->ss_ne;
+  for (int k = 0; k < SS_MAX_NE; ++k) c.ss_off[k] = p->ss_off[k];
+  c.ss_mask = p->d_ss_mask;
+  c.ss_val = p->d_ss_val;
   return c;
 }
 
@@ -303,7 +321,7 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     }
     for (int l = 0; l < sigma; ++l) {
       if (l >= 2) cudaStreamWaitEvent(s, p->ev_leja[l], 0);
-      launch_level(c, l, s);
+      launch_level(c, l, sigma, s);
     }
   } else {
     TRY(launch_mpk(p, c, sigma, s));
@@ -614,6 +632,68 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
   const int64_t tiles = (n_rows + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
   p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * occ[0], (int64_t)RED_BLOCKS, tiles}));
   p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ[1], tiles));
+  // L2 prefetch distance: the largest positive column offset (first touch)
+  p->pf_off = 0;
+  p->pf_ahead = std::max(1, atoi(env_or("SSCG_PF_AHEAD", "1")));
+  if (atoi(env_or("SSCG_PF", "1")) != 0)
+    for (int v : off) p->pf_off = std::max(p->pf_off, v);
+  // superset-mask form: every pattern sorted by column, union of offsets small
+  p->ss_ne = 0;
+  if (atoi(env_or("SSCG_PAT_SS", "1")) != 0) {
+    std::vector<int> uni(off.begin(), off.end());
+    std::sort(uni.begin(), uni.end());
+    uni.erase(std::unique(uni.begin(), uni.end()), uni.end());
+    bool ok = !uni.empty() && (int)uni.size() <= SS_MAX_NE;
+    for (int q = 0; q < np && ok; ++q)
+      for (int k = ptr[q] + 1; k < ptr[q + 1] && ok; ++k) ok = off[k - 1] < off[k];
+    int socc[2] = {0, 0};
+    if (ok) ss_ctas_per_sm(np, (int)uni.size(), p->pid_bytes, socc);
+    if (ok && socc[0] >= 1 && socc[1] >= 1) {
+      std::vector<unsigned> mask((size_t)np, 0u);
+      std::vector<double> sval((size_t)np * SS_MAX_NE, 0.0);
+      for (int q = 0; q < np; ++q)
+        for (int k = ptr[q]; k < ptr[q + 1]; ++k) {
+          const int slot = (int)(std::lower_bound(uni.begin(), uni.end(), off[k]) - uni.begin());
+          mask[(size_t)q] |= 1u << slot;
+          sval[(size_t)q * SS_MAX_NE + slot] = val[k];
+        }
+      TRY(dalloc(p, &p->d_ss_mask, mask.size()));
+      TRY(dalloc(p, &p->d_ss_val, sval.size()));
+      CUDA_OK(cudaMemcpy(p->d_ss_mask, mask.data(), 4 * mask.size(), cudaMemcpyHostToDevice));
+      CUDA_OK(cudaMemcpy(p->d_ss_val, sval.data(), 8 * sval.size(), cudaMemcpyHostToDevice));
+      p->ss_ne = (int)uni.size();
+      for (int k = 0; k < SS_MAX_NE; ++k) p->ss_off[k] = k < p->ss_ne ? uni[(size_t)k] : 0;
+      p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * socc[0], (int64_t)RED_BLOCKS, tiles}));
+      p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * socc[1], tiles));
+    }
+  }
+  // plane-march form: a symmetric union [-S .. 0 .. S] of 3, 5 or 7 offsets
+  // with S >= 256 (whole coalesced column blocks) and 32-bit row indices
+  p->zm_S = 0;
+  if (p->ss_ne > 0 && atoi(env_or("SSCG_ZM", "1")) != 0) {
+    const int ne = p->ss_ne;
+    const int64_t S = p->ss_off[ne - 1];
+    bool ok = (ne == 3 || ne == 5 || ne == 7) && S >= 256 && p->ss_off[ne / 2] == 0 &&
+              p->ld + S < ((int64_t)1 << 31);
+    for (int k = 0; k < ne && ok; ++k) ok = p->ss_off[k] == -p->ss_off[ne - 1 - k];
+    int zocc[2] = {0, 0};
+    if (ok) zm_ctas_per_sm(np, ne, p->pid_bytes, zocc);
+    if (ok && zocc[0] >= 1 && zocc[1] >= 1) {
+      const int64_t ncb = (S + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
+      const int64_t steps = (n_rows + S - 1) / S;
+      const int64_t grid = (int64_t)sms * zocc[1];
+      int64_t zc = atoi(env_or("SSCG_ZM_ZC", "0"));
+      // ~16 planes per item (measured best on 256^3: 8-32 within 1%), fewer
+      // when the operator is too small to give every CTA a few items
+      if (zc <= 0) zc = std::max<int64_t>(2, std::min<int64_t>(16, ncb * steps / (4 * grid)));
+      p->zm_S = S;
+      p->zm_zc = (int)zc;
+      p->zm_ncb = (int)ncb;
+      p->zm_items = ncb * ((steps + zc - 1) / zc);
+      p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * zocc[0], (int64_t)RED_BLOCKS, p->zm_items}));
+      p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, p->zm_items));
+    }
+  }
   // windowed kernels: near radius = the largest |offset| up to WIN_R_CAP (even)
   p->win_r = -1;
   if (atoi(env_or("SSCG_PAT_WIN", "0")) != 0) {  // opt-in: measured slower, DESIGN.md 4b
@@ -722,7 +802,7 @@ void wave_plan_passes(sscg_plan* p, int sigma) {
 
 int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s) {
   if (!p->wave_on) {
-    for (int l = 0; l < sigma; ++l) launch_level(c, l, s);
+    for (int l = 0; l < sigma; ++l) launch_level(c, l, sigma, s);
     return SSCG_OK;
   }
   CUDA_OK(cudaMemsetAsync(p->d_wcnt, 0, sizeof(int) * ((size_t)SMAX * p->wave_ngroups + SMAX), s));
@@ -854,7 +934,7 @@ int sscg_plan_destroy(sscg_plan* p) {
                   p->d_rj, p->d_st, p->d_cfg, p->d_part_t, p->d_part_r, p->d_part_d,
                   p->d_part_g, p->d_leja, p->d_it, p->d_ri, p->d_rd, p->d_conds, p->d_th,
                   p->d_ga, p->d_mu, p->d_otrue, p->d_fg, p->d_red, p->d_wdep, p->d_wcnt,
-                  p->d_pid, p->d_pat_ptr, p->d_pat_off, p->d_pat_val};
+                  p->d_pid, p->d_pat_ptr, p->d_pat_off, p->d_pat_val, p->d_ss_mask, p->d_ss_val};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_done) cudaFreeHost(p->h_done);
@@ -1122,6 +1202,8 @@ int sscg_plan_mpk_schedule(sscg_plan* p, int32_t sigma, int32_t* out) {
   out[0] = p->d_pid ? 2 : p->wave_on ? 1 : 0;
   out[1] = p->wave_on ? p->wave_grid : p->red_n;
   out[2] = p->d_pid ? p->pat_np : p->wave_lhi;
+  // last slot: pattern kernel form (0 table walk, 1 superset mask, 2 plane march)
+  if (p->d_pid) out[3 + 2 * SMAX] = p->zm_S > 0 ? 2 : p->ss_ne > 0 ? 1 : 0;
   if (!p->wave_on) {
     out[3] = sigma;
     for (int q = 0; q < sigma; ++q) out[4 + 2 * q] = 1;
@@ -1333,7 +1415,7 @@ int sscg_vgroup_run(sscg_plan* const* plans, int32_t np, const sscg_config* cfg,
     for (int i = 0; i < np; ++i) {
       launch_params_begin(cs[i], s);
       for (int n = 2; n < sigma; ++n) launch_leja_point(cs[i], n, s);
-      for (int l = 0; l < sigma; ++l) launch_level(cs[i], l, s);
+      for (int l = 0; l < sigma; ++l) launch_level(cs[i], l, sigma, s);
       launch_gram(cs[i], k, s);
     }
     launch_vsum(d_reds, np, npack, s);

@@ -100,6 +100,26 @@ __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
+// bulk L2 prefetch (TMA unit, no registers, no completion tracking)
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+// Row-streaming pattern kernels: the CTA's rows of the NEXT grid-stride
+// iteration first touch the input vectors around row + pf_off (the largest
+// positive column offset: a stencil's plane ahead).  One thread per CTA asks
+// the TMA unit to pull those 256-row windows into L2 now, so the gathers of
+// the next iteration hit L2 instead of waiting on HBM (more bytes in flight
+// per SM than the threads' own loads can keep).
+template <int NV>
+__device__ __forceinline__ void prefetch_next(const Ctx& c, int64_t i, int64_t stride,
+                                              const double* const* xs) {
+  if (c.pf_off == 0 || threadIdx.x != 0) return;
+  int64_t r0 = i + (int64_t)c.pf_ahead * stride + c.pf_off;
+  r0 &= ~(int64_t)1;
+  if (r0 < 0 || r0 + ROWS_PER_CTA > c.ld) return;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) l2_prefetch(xs[q] + r0, ROWS_PER_CTA * 8);
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -313,6 +333,73 @@ __device__ __forceinline__ void row_dot_p(const PatSmem& T, int b, int e, int i,
     for (int k = 0; k < B; ++k) {
       if (k < m) {
         const double v = T.val[jj + k];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v, xb[q][k]));
+      }
+    }
+  }
+}
+
+// Superset-mask form (Ctx::ss_*): the table as per-pattern masks over the
+// sorted union of offsets plus per-slot values.  The union offsets are kernel
+// parameters, so the row loop is fully unrolled: per present slot one address,
+// NV gathers, then the adds in slot order = the stored order of the row (a
+// pattern's offsets are a subsequence of the sorted union), i.e. the same
+// rounded multiply-adds as csr_matvec.  Table in shared memory:
+// [val np x SS_MAX_NE][mask np].
+__host__ __device__ __forceinline__ size_t ss_smem_bytes_dev(int np) {
+  return (size_t)np * SS_MAX_NE * 8 + (size_t)np * 4;
+}
+
+struct SsSmem {
+  const double* val;
+  const unsigned* mask;
+};
+
+__device__ __forceinline__ SsSmem load_ss(const Ctx& c) {
+  extern __shared__ __align__(16) double psm[];
+  double* sv = psm;
+  unsigned* sm = reinterpret_cast<unsigned*>(sv + (size_t)c.pat_np * SS_MAX_NE);
+  for (int j = threadIdx.x; j < c.pat_np * SS_MAX_NE; j += blockDim.x) sv[j] = __ldg(c.ss_val + j);
+  for (int j = threadIdx.x; j < c.pat_np; j += blockDim.x) sm[j] = __ldg(c.ss_mask + j);
+  __syncthreads();
+  return SsSmem{sv, sm};
+}
+
+// The adds run over every slot: an absent slot contributes 0.0 * 0.0 = +0.0,
+// and adding +0.0 is exact for every partial sum csr_matvec can hold (a sum
+// that starts at +0.0 is never -0.0 under round-to-nearest), so the result is
+// bit-identical to skipping the slot.  Only the gathers are predicated (an
+// absent slot's column may lie outside the vector).
+template <int NV, int NE>
+__device__ __forceinline__ void row_dot_m(const Ctx& c, const SsSmem& S, int pid, int64_t i,
+                                          const double* const* __restrict__ xs, double* acc) {
+  const unsigned m = S.mask[pid];
+  const double2* v2 = reinterpret_cast<const double2*>(S.val + pid * SS_MAX_NE);
+  const double* xi[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) xi[q] = xs[q] + i;  // row base; slot k reads xi[q][off_k]
+  double xb[NV][NE];
+#pragma unroll
+  for (int k = 0; k < NE; ++k) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) xb[q][k] = 0.0;
+    if (m & (1u << k)) {
+      const int o = c.ss_off[k];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) xb[q][k] = __ldg(xi[q] + o);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+#pragma unroll
+  for (int k2 = 0; k2 < (NE + 1) / 2; ++k2) {
+    const double2 vv = v2[k2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = 2 * k2 + h;
+      if (k < NE) {
+        const double v = h ? vv.y : vv.x;
 #pragma unroll
         for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v, xb[q][k]));
       }

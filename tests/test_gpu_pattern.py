@@ -1,4 +1,5 @@
-"""GPU tier: pattern-compressed level kernels (mpk.cu k_level_pat).
+"""GPU tier: pattern-compressed level kernels (mpk.cu k_level_pat, k_level_ss,
+k_level_zm).
 
 A plan whose rows reduce to a small table of (relative column, value)
 patterns streams 1- or 2-byte row ids instead of CSR.  Columns, values and
@@ -18,17 +19,22 @@ from paper_1908_04081_b200.types import ProblemInstance, SparseMatrix
 pytestmark = pytest.mark.gpu
 
 
+_KEYS = ("SSCG_PATTERN", "SSCG_PAT_SS", "SSCG_ZM", "SSCG_ZM_ZC")
+
+
 def _with_env(env, fn):
-    old = os.environ.get("SSCG_PATTERN")
+    old = {k: os.environ.get(k) for k in _KEYS}
     try:
-        os.environ.pop("SSCG_PATTERN", None)
+        for k in _KEYS:
+            os.environ.pop(k, None)
         os.environ.update(env)
         return fn()
     finally:
-        if old is None:
-            os.environ.pop("SSCG_PATTERN", None)
-        else:
-            os.environ["SSCG_PATTERN"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
 def _instance(m, seed, label):
@@ -96,6 +102,36 @@ def test_pattern_counts(gpu_ready):
     assert s["kind"] == "pattern" and 256 < s["patterns"] <= 900
 
 
+def test_pattern_kernel_forms(gpu_ready):
+    """Which pattern kernel a plan takes: the plane march for stencils whose
+    plane stride S >= 256 (c3, c5), the superset mask for small strides (c1:
+    S = 64; the tridiagonal), the table walk when disabled."""
+    def form(prob, env=None):
+        return _with_env(env or {}, lambda: _plan(prob().a).mpk_schedule(8)["form"])
+    assert form(lambda: problems.make_problem("c5", scale=28)) == "march"
+    assert form(lambda: problems.make_problem("c3", scale=24)) == "march"
+    assert form(lambda: problems.make_problem("c1")) == "superset"
+    assert form(_tridiag_many_patterns) == "superset"
+    assert form(lambda: problems.make_problem("c5", scale=28), {"SSCG_ZM": "0"}) == "superset"
+    assert form(lambda: problems.make_problem("c5", scale=28), {"SSCG_PAT_SS": "0"}) == "table"
+
+
+@pytest.mark.parametrize("env", [{"SSCG_ZM": "0"}, {"SSCG_PAT_SS": "0"}, {"SSCG_ZM_ZC": "3"}],
+                         ids=["superset", "table", "march_zc3"])
+def test_pattern_forms_bit_identical(gpu_ready, env):
+    """Plane march (default), superset mask and table walk run the same
+    rounded operations in the same order: identical solves (Newton and
+    Chebyshev bases, unit and non-unit gamma, mu != 0)."""
+    for key, scale, kw in (("c5", 28, dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
+                           ("c3", 24, dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev"))):
+        cfg = AdaptiveConfig(**kw)
+        ref = adaptive_solve(problems.make_problem(key, scale=scale), cfg, trace="fast")
+        got = _with_env(env, lambda: adaptive_solve(problems.make_problem(key, scale=scale), cfg,
+                                                    trace="fast"))
+        np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
+        np.testing.assert_array_equal(got[0], ref[0])
+
+
 def test_pattern_full_trace_and_partitioned_agree(gpu_ready):
     """Full diagnostics and the virtual-group (row-slab) path through the
     pattern kernels reproduce the CSR single-GPU solve."""
@@ -106,7 +142,10 @@ def test_pattern_full_trace_and_partitioned_agree(gpu_ready):
                     lambda: adaptive_solve(problems.make_problem("c3", scale=24), AdaptiveConfig(**kw)))
     x, tr, co = adaptive_solve(problems.make_problem("c3", scale=24), AdaptiveConfig(**kw))
     np.testing.assert_array_equal(x, ref[0])
-    np.testing.assert_array_equal(tr.true_resid, ref[1].true_resid)
+    # ||b - A x|| per outer loop: the same rows, summed in the kernel's own
+    # order (the plane-march level 0 groups rows by column), so only the
+    # rounding of the norm may differ
+    np.testing.assert_allclose(tr.true_resid, ref[1].true_resid, rtol=1e-14, atol=0)
     prob = problems.make_problem("c3", scale=24)
     xg, tg, cg, _ = VirtualGroup(CsrRows.of(prob.a), 1, depth=10).solve(prob, AdaptiveConfig(**kw))
     np.testing.assert_array_equal(xg, ref[0])
