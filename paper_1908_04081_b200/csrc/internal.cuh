@@ -156,6 +156,11 @@ struct Ctx {
   int zm_zc;       // steps per work item
   int zm_ncb;      // column blocks of 256 columns
   int64_t zm_items;  // work items = zm_ncb x ceil(steps / zm_zc)
+  int zm_pf;         // L2 prefetch of the plane zm_pf steps ahead (0: off)
+  int zm_o;          // 2-D column tiles with line stride zm_o (0: 256 consecutive columns)
+  int zm_pair;       // levels >= 1 by the row-pair march (k_level_zp; zm_items in pairs)
+  int zp_grid;       // CTAs of k_level_zp
+  int64_t zp_items;  // its work items (512 columns each)
   int pf_off;    // pattern kernels: L2 prefetch at row + pf_ahead * stride + pf_off (0: off)
   int pf_ahead;
   const unsigned* ss_mask;  // [pat_np]
@@ -229,6 +234,7 @@ int pattern_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 size_t ss_smem_bytes(int np);
 int ss_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 int zm_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
+int zp_ctas_per_sm(int np, int ne, int pid_bytes);
 void staged_prepare(int cap);
 int staged_ctas_per_sm(int cap);
 int wave_ctas_per_sm(int cap);

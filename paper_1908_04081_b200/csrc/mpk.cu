@@ -688,6 +688,9 @@ __global__ void SS_LB k_level_ss(Ctx c, int l) {
 // gathers; the other slots are gathered as in row_dot_m.  The adds run over
 // the slots in union order = stored order, absent slots adding +0.0 (exact,
 // see row_dot_m): bit-identical to the other level kernels.
+#ifndef ZM_PIPE  // plane-ahead loads one step early (measured slower: registers)
+#define ZM_PIPE 0
+#endif
 template <bool UNIT>
 __device__ __forceinline__ double recur_t(double ay, double y, double y2, double th, double ga,
                                           double mu, bool use_mu) {
@@ -699,7 +702,9 @@ __device__ __forceinline__ double recur_t(double ay, double y, double y2, double
 // one column of one work item.  NV input vectors xs[0..NV) (level 0: x, P0, R0
 // with NV = 3; else P_l, R_l with NV = 2, or P_l alone with NV = 1).
 // L0: level 0 (no two-back term; outputs of vectors 1.. ; t = b - A x norms)
-template <typename ID, int NE, int NV, bool L0, bool UNIT>
+// RK: recurrence kind, bit 0 = non-unit gamma (IEEE division), bit 1 = mu != 0
+// (two-back term) -- compile-time, so the Newton levels carry neither
+template <typename ID, int NE, int NV, bool L0, int RK>
 __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, int col, int z0, int z1,
                                           const double* const* __restrict__ xs,
                                           const double* const* __restrict__ ym,
@@ -707,6 +712,7 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, int col
                                           double mu, bool use_mu, int plim, int rlim, int& bad,
                                           double& tt, double& rr) {
   constexpr int KC = NE / 2;
+  constexpr bool UNIT = (RK & 1) == 0, MU = (RK & 2) != 0 && !L0;
   constexpr int NO = L0 ? NV - 1 : NV;  // output vectors
   constexpr int Q0 = L0 ? 1 : 0;        // first input vector with an output
   // 32-bit row indices (plan.cu enables the march only for n + S < 2^31)
@@ -736,15 +742,37 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, int col
     pv[q] = r >= S ? __ldg(px[q] - S) : 0.0;
     cu[q] = __ldg(px[q]);
   }
+#if ZM_PIPE
+  // the plane ahead (the only HBM stream) is loaded one step early, so its
+  // latency overlaps a whole step instead of sitting on each step's path
+  double nxa[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) nxa[q] = r + S < n ? __ldg(px[q] + S) : 0.0;
+#endif
+  // row ids two steps ahead and the pattern mask one step ahead: the gathers
+  // of a step (predicated on the mask) issue without waiting on an id load
   const ID* pidp = reinterpret_cast<const ID*>(c.pid) + r;
+  int pid_cur = (int)__ldg(pidp);
+  int pid_n1 = (z0 + 1 < z1 && r + S < plim) ? (int)__ldg(pidp + S) : 0;
+  unsigned m_cur = T.mask[pid_cur];
   for (int z = z0; z < z1 && r < plim; ++z) {
-    const int pid = (int)__ldg(pidp);
-    const unsigned m = T.mask[pid];
+    const int pid = pid_cur;
+    const unsigned m = m_cur;
+    const int pid_n2 = (z + 2 < z1 && r + 2 * S < plim) ? (int)__ldg(pidp + 2 * S) : 0;
     const bool rrow = r < rlim;  // the last vector (R) is produced on this row
     double nx[NV];
+#if ZM_PIPE
+    const bool hasn = z + 1 < z1 && r + 2 * S < n;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      nx[q] = nxa[q];
+      nxa[q] = hasn ? __ldg(px[q] + 2 * S) : 0.0;
+    }
+#else
     const bool hasn = r + S < n;
 #pragma unroll
     for (int q = 0; q < NV; ++q) nx[q] = hasn ? __ldg(px[q] + S) : 0.0;
+#endif
     double xb[NV][NE];
 #pragma unroll
     for (int k = 1; k < NE - 1; ++k) {
@@ -787,8 +815,8 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, int col
 #pragma unroll
     for (int q = 0; q < NO; ++q) {
       if (q == NO - 1 && NO > 1 && !rrow) break;
-      const double y2 = (!L0 && use_mu) ? *pm[q] : 0.0;
-      const double w = recur_t<UNIT>(acc[Q0 + q], cu[Q0 + q], y2, th, ga, mu, !L0 && use_mu);
+      const double y2 = MU ? *pm[q] : 0.0;
+      const double w = recur_t<UNIT>(acc[Q0 + q], cu[Q0 + q], y2, th, ga, mu, MU);
       *po[q] = w;
       bad |= !finite(w);
     }
@@ -801,14 +829,17 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, int col
 #pragma unroll
     for (int q = 0; q < NO; ++q) {
       po[q] += S;
-      if (!L0) pm[q] += S;
+      if (MU) pm[q] += S;
     }
+    pid_cur = pid_n1;
+    m_cur = T.mask[pid_n1];
+    pid_n1 = pid_n2;
     pidp += S;
     r += S;
   }
 }
 
-template <typename ID, int NE, int NV, bool L0, bool UNIT>
+template <typename ID, int NE, int NV, bool L0, int RK>
 __device__ __forceinline__ void zm_items(const Ctx& c, const SsSmem& T, const double* const* xs,
                                          const double* const* ym, double* const* yo, double th,
                                          double ga, double mu, bool use_mu, int64_t plim,
@@ -816,10 +847,21 @@ __device__ __forceinline__ void zm_items(const Ctx& c, const SsSmem& T, const do
   const int items = (int)c.zm_items, ncb = c.zm_ncb, zcs = c.zm_zc, S = (int)c.zm_S;
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
     const int cb = it % ncb, zc = it / ncb;
-    const int col = cb * ROWS_PER_CTA + threadIdx.x;
+    int col;
+    if (c.zm_o > 0) {
+      // 2-D tile of the plane: 32 consecutive columns per warp (x), the 8
+      // warps on consecutive lines of stride zm_o (y), so a row's +-zm_o
+      // neighbours are mostly rows another warp of this CTA just loaded (L1)
+      const int ntx = c.zm_o >> 5;
+      const int ty = (cb / ntx) * (ROWS_PER_CTA / 32) + (threadIdx.x >> 5);
+      col = ty * c.zm_o + (cb % ntx) * 32 + (threadIdx.x & 31);
+      if (ty >= S / c.zm_o) continue;
+    } else {
+      col = cb * ROWS_PER_CTA + threadIdx.x;
+    }
     if (col >= S) continue;
     const int z0 = zc * zcs;
-    zm_column<ID, NE, NV, L0, UNIT>(c, T, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu, use_mu,
+    zm_column<ID, NE, NV, L0, RK>(c, T, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu, use_mu,
                                     (int)plim, (int)rlim, bad, tt, rr);
   }
 }
@@ -855,8 +897,11 @@ inline ZmPtrs zm_ptrs(const Ctx& c, int l, int sigma) {
   return z;
 }
 
+#ifndef ZM0_MINB
+#define ZM0_MINB 3
+#endif
 template <typename ID, int NE>
-__global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_zm(Ctx c, ZmPtrs zp) {
+__global__ void __launch_bounds__(ROWS_PER_CTA, ZM0_MINB) k_level0_zm(Ctx c, ZmPtrs zp) {
   __shared__ double sm[ROWS_PER_CTA / 32];
   const SolverState* st = c.st;
   if (st->done) return;
@@ -871,9 +916,9 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_zm(Ctx c, ZmPtrs zp) {
   int bad = 0;
   const int64_t plim = lvl_p_rows(c, sigma, 0), rlim = do_r ? lvl_r_rows(c, sigma, 0) : 0;
   if (ga == 1.0)
-    zm_items<ID, NE, 3, true, true>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+    zm_items<ID, NE, 3, true, 0>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
   else
-    zm_items<ID, NE, 3, true, false>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+    zm_items<ID, NE, 3, true, 1>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
   tt = block_sum<ROWS_PER_CTA>(tt, sm);
   rr = block_sum<ROWS_PER_CTA>(rr, sm);
   if (threadIdx.x == 0) {
@@ -883,8 +928,11 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_zm(Ctx c, ZmPtrs zp) {
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
 }
 
+#ifndef ZM_MINB
+#define ZM_MINB 4
+#endif
 template <typename ID, int NE>
-__global__ void __launch_bounds__(ROWS_PER_CTA) k_level_zm(Ctx c, int l, ZmPtrs zp) {
+__global__ void __launch_bounds__(ROWS_PER_CTA, ZM_MINB) k_level_zm(Ctx c, int l, ZmPtrs zp) {
   const SolverState* st = c.st;
   if (st->done) return;
   const int sbar = st->s_bar;
@@ -900,17 +948,242 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level_zm(Ctx c, int l, ZmPtrs 
   int bad = 0;
   double tt = 0.0, rr = 0.0;
   const int64_t plim = lvl_p_rows(c, sigma, l), rlim = lvl_r_rows(c, sigma, l);
-  if (do_r) {
-    if (ga == 1.0)
-      zm_items<ID, NE, 2, false, true>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, rlim, bad, tt, rr);
-    else
-      zm_items<ID, NE, 2, false, false>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, rlim, bad, tt, rr);
-  } else {
-    if (ga == 1.0)
-      zm_items<ID, NE, 1, false, true>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, plim, bad, tt, rr);
-    else
-      zm_items<ID, NE, 1, false, false>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, plim, bad, tt, rr);
+  const int rk = (ga == 1.0 ? 0 : 1) | (use_mu ? 2 : 0);
+#define ZM_RK(NV, RL)                                                                          \
+  switch (rk) {                                                                                \
+    case 0: zm_items<ID, NE, NV, false, 0>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    case 1: zm_items<ID, NE, NV, false, 1>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    case 2: zm_items<ID, NE, NV, false, 2>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    default: zm_items<ID, NE, NV, false, 3>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
   }
+  if (do_r) {
+    ZM_RK(2, rlim)
+  } else {
+    ZM_RK(1, plim)
+  }
+#undef ZM_RK
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Row-pair plane march (levels >= 1; Ctx::zm_pair).  The union is the 2-D /
+// 3-D stencil form [-S, (-o,) -1, 0, 1, (o,) S] with S and o even: a thread
+// owns two adjacent columns (rows r, r + 1 with r even), so every even-offset
+// slot is ONE aligned 16-byte load serving both rows, the +-1 slots of one
+// row are the other row's centre, and only x[r - 1] and x[r + 2] are single
+// loads: per vector and row pair 4 (5 in 3-D) load instructions instead of
+// 10 (14).  Each row keeps its own pattern mask and values; products and adds
+// in union order as everywhere else: bit-identical.
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+
+template <typename ID, int NE, int NV, int RK>
+__device__ __forceinline__ void zp_column(const Ctx& c, const SsSmem& T, int col, int z0, int z1,
+                                          const double* const* __restrict__ xs,
+                                          const double* const* __restrict__ ym,
+                                          double* const* __restrict__ yo, double th, double ga,
+                                          double mu, bool use_mu, int plim, int rlim, int& bad) {
+  static_assert(NE == 5 || NE == 7, "pair march: 2-D or 3-D stencil unions");
+  constexpr bool UNIT = (RK & 1) == 0, MU = (RK & 2) != 0;
+  constexpr bool D3 = NE == 7;
+  constexpr int KM1 = D3 ? 2 : 1, KC = NE / 2, KP1 = KC + 1;  // slots of -1, 0, +1
+  const int S = (int)c.zm_S, n = (int)(c.ld < INT32_MAX ? c.ld : INT32_MAX);
+  const int o = D3 ? c.ss_off[NE - 2] : 0;
+  int r = z0 * S + col;  // even
+  if (r >= plim) return;
+  const double* px[NV];
+  double* po[NV];
+  const double* pm[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    px[q] = xs[q] + r;
+    po[q] = yo[q] + r;
+    pm[q] = ym[q] + r;
+  }
+  double2 pv[NV], cu[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    pv[q] = r >= S ? ld2(px[q] - S) : make_double2(0.0, 0.0);
+    cu[q] = ld2(px[q]);
+  }
+#if ZM_PIPE
+  double2 nxa[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) nxa[q] = r + S < n ? ld2(px[q] + S) : make_double2(0.0, 0.0);
+#endif
+  const ID* pidp = reinterpret_cast<const ID*>(c.pid) + r;
+  int p0 = (int)__ldg(pidp), p1 = (int)__ldg(pidp + 1);
+  int q0 = 0, q1 = 0;
+  if (z0 + 1 < z1 && r + S < plim) {
+    q0 = (int)__ldg(pidp + S);
+    q1 = (int)__ldg(pidp + S + 1);
+  }
+  unsigned mc0 = T.mask[p0], mc1 = T.mask[p1];
+  for (int z = z0; z < z1 && r < plim; ++z) {
+    const int pid0 = p0, pid1 = p1;
+    const unsigned m0 = mc0, m1 = mc1;
+    int t0 = 0, t1 = 0;
+    if (z + 2 < z1 && r + 2 * S < plim) {
+      t0 = (int)__ldg(pidp + 2 * S);
+      t1 = (int)__ldg(pidp + 2 * S + 1);
+    }
+    const unsigned mu01 = m0 | m1;
+    const bool row1 = r + 1 < plim;
+    const bool rr0 = r < rlim, rr1 = r + 1 < rlim;
+#if ZM_PIPE
+    const bool hasn = z + 1 < z1 && r + 2 * S < n;
+#else
+    const bool hasn = r + S < n;
+#endif
+    double2 nx[NV], lo[NV], hi[NV];
+    double lm1[NV], rp2[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const bool want = q < NV - 1 || NV == 1 || rr0;  // the R vector only on R rows
+#if ZM_PIPE
+      nx[q] = nxa[q];
+      nxa[q] = hasn ? ld2(px[q] + 2 * S) : make_double2(0.0, 0.0);
+#else
+      nx[q] = hasn ? ld2(px[q] + S) : make_double2(0.0, 0.0);
+#endif
+      lo[q] = hi[q] = make_double2(0.0, 0.0);
+      if (D3) {
+        if (want && (mu01 & 2u)) lo[q] = ld2(px[q] - o);
+        if (want && (mu01 & (1u << (NE - 2)))) hi[q] = ld2(px[q] + o);
+      }
+      lm1[q] = (want && (m0 >> KM1) & 1u) ? __ldg(px[q] - 1) : 0.0;
+      rp2[q] = (want && row1 && (m1 >> KP1) & 1u) ? __ldg(px[q] + 2) : 0.0;
+    }
+    // slot values of row r (.x) and row r + 1 (.y), absent slots 0.0
+    double a[2][NV][NE];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      a[0][q][0] = pv[q].x;
+      a[1][q][0] = pv[q].y;
+      if (D3) {
+        a[0][q][1] = lo[q].x;
+        a[1][q][1] = lo[q].y;
+        a[0][q][NE - 2] = hi[q].x;
+        a[1][q][NE - 2] = hi[q].y;
+      }
+      a[0][q][KM1] = lm1[q];
+      a[1][q][KM1] = cu[q].x;
+      a[0][q][KC] = cu[q].x;
+      a[1][q][KC] = cu[q].y;
+      a[0][q][KP1] = cu[q].y;
+      a[1][q][KP1] = rp2[q];
+      a[0][q][NE - 1] = nx[q].x;
+      a[1][q][NE - 1] = nx[q].y;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const unsigned m = h ? m1 : m0;
+      const int pid = h ? pid1 : pid0;
+      if (h == 1 && !row1) break;
+      const double2* v2 = reinterpret_cast<const double2*>(T.val + pid * SS_MAX_NE);
+      double acc[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+#pragma unroll
+      for (int k2 = 0; k2 < (NE + 1) / 2; ++k2) {
+        const double2 vv = v2[k2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int k = 2 * k2 + e;
+          if (k < NE) {
+            const double v = e ? vv.y : vv.x;
+            const bool on = (m >> k) & 1u;
+#pragma unroll
+            for (int q = 0; q < NV; ++q)
+              acc[q] = __dadd_rn(acc[q], __dmul_rn(v, on ? a[h][q][k] : 0.0));
+          }
+        }
+      }
+      const bool rrow = h ? rr1 : rr0;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        if (q == NV - 1 && NV > 1 && !rrow) break;
+        const double y2 = MU ? pm[q][h] : 0.0;
+        const double w = recur_t<UNIT>(acc[q], h ? cu[q].y : cu[q].x, y2, th, ga, mu, MU);
+        po[q][h] = w;
+        bad |= !finite(w);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      pv[q] = cu[q];
+      cu[q] = nx[q];
+      px[q] += S;
+      po[q] += S;
+      if (MU) pm[q] += S;
+    }
+    p0 = q0;
+    p1 = q1;
+    mc0 = T.mask[q0];
+    mc1 = T.mask[q1];
+    q0 = t0;
+    q1 = t1;
+    pidp += S;
+    r += S;
+  }
+}
+
+template <typename ID, int NE, int NV, int RK>
+__device__ __forceinline__ void zp_items(const Ctx& c, const SsSmem& T, const double* const* xs,
+                                         const double* const* ym, double* const* yo, double th,
+                                         double ga, double mu, bool use_mu, int64_t plim,
+                                         int64_t rlim, int& bad) {
+  const int S = (int)c.zm_S, zcs = c.zm_zc, items = (int)c.zp_items;
+  const int ncb = (S + 2 * ROWS_PER_CTA - 1) / (2 * ROWS_PER_CTA);  // 512 columns per item
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int cb = it % ncb, zc = it / ncb;
+    const int col = 2 * (cb * ROWS_PER_CTA + threadIdx.x);
+    if (col >= S) continue;
+    const int z0 = zc * zcs;
+    zp_column<ID, NE, NV, RK>(c, T, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu, use_mu, (int)plim,
+                                (int)rlim, bad);
+  }
+}
+
+#ifndef ZP_MINB
+#define ZP_MINB 0
+#endif
+#if ZP_MINB > 0
+#define ZP_LB __launch_bounds__(ROWS_PER_CTA, ZP_MINB)
+#else
+#define ZP_LB __launch_bounds__(ROWS_PER_CTA)
+#endif
+template <typename ID, int NE>
+__global__ void ZP_LB k_level_zp(Ctx c, int l, ZmPtrs zp) {
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  if (l >= sbar) return;
+  const SsSmem T = load_ss(c);
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[l], ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
+  const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
+  const bool do_r = l < sbar - 1;
+  const double* xs[2] = {zp.xs[0], zp.xs[1]};
+  const double* ym[2] = {zp.ym[0], zp.ym[1]};
+  double* yo[2] = {zp.yo[0], zp.yo[1]};
+  int bad = 0;
+  const int64_t plim = lvl_p_rows(c, sigma, l), rlim = lvl_r_rows(c, sigma, l);
+  const int rk = (ga == 1.0 ? 0 : 1) | (use_mu ? 2 : 0);
+#define ZP_RK(NV, RL)                                                                       \
+  switch (rk) {                                                                             \
+    case 0: zp_items<ID, NE, NV, 0>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad); break; \
+    case 1: zp_items<ID, NE, NV, 1>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad); break; \
+    case 2: zp_items<ID, NE, NV, 2>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad); break; \
+    default: zp_items<ID, NE, NV, 3>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad); break; \
+  }
+  if (do_r) {
+    ZP_RK(2, rlim)
+  } else {
+    ZP_RK(1, plim)
+  }
+#undef ZP_RK
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
 }
 
@@ -1446,6 +1719,23 @@ int zm_ctas_per_sm(int np, int ne, int pid_bytes, int* out2) {
   return a < b ? a : b;
 }
 
+// row-pair march (levels >= 1) for 5- and 7-slot unions
+int zp_ctas_per_sm(int np, int ne, int pid_bytes) {
+  int b = 0;
+  const size_t bytes = ss_smem_bytes_dev(np);
+  const int lim = 48 * 1024;
+#define ZP_OCC(ID, NE)                                                                       \
+  cudaFuncSetAttribute(k_level_zp<ID, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim); \
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_level_zp<ID, NE>, ROWS_PER_CTA, bytes);
+  if (pid_bytes == 1) {
+    if (ne == 5) { ZP_OCC(uint8_t, 5) } else if (ne == 7) { ZP_OCC(uint8_t, 7) }
+  } else {
+    if (ne == 5) { ZP_OCC(uint16_t, 5) } else if (ne == 7) { ZP_OCC(uint16_t, 7) }
+  }
+#undef ZP_OCC
+  return b;
+}
+
 int ss_ctas_per_sm(int np, int ne, int pid_bytes, int* out2) {
   int a = 0, b = 0;
   const size_t bytes = ss_smem_bytes_dev(np);
@@ -1526,6 +1816,8 @@ void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s) {
 #define ZM_LAUNCH(ID, NE)                                                      \
   if (level == 0)                                                              \
     k_level0_zm<ID, NE><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp);           \
+  else if (c.zm_pair && NE >= 5)                                               \
+    k_level_zp<ID, (NE >= 5 ? NE : 5)><<<c.zp_grid, ROWS_PER_CTA, bytes, s>>>(c, level, zp); \
   else                                                                         \
     k_level_zm<ID, NE><<<c.pat_grid, ROWS_PER_CTA, bytes, s>>>(c, level, zp);
 #define ZM_NE_SWITCH(ID)                   \

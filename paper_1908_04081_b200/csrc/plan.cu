@@ -138,7 +138,8 @@ struct sscg_plan {
   double* d_pat_val = nullptr;
   int pf_off = 0, pf_ahead = 1;  // L2 prefetch of the pattern kernels (0: off)
   int64_t zm_S = 0;  // plane-march form (0: off)
-  int zm_zc = 0, zm_ncb = 0;
+  int zm_zc = 0, zm_ncb = 0, zm_pf = 0, zm_o = 0, zm_pair = 0, zp_grid = 0;
+  int64_t zp_items = 0;
   int64_t zm_items = 0;
   int ss_ne = 0;  // superset-mask form (superset_setup); 0: table-walking kernels
   int ss_off[SS_MAX_NE] = {};
@@ -259,6 +260,11 @@ Ctx make_ctx(sscg_plan* p) {
   c.zm_zc = p->zm_zc;
   c.zm_ncb = p->zm_ncb;
   c.zm_items = p->zm_items;
+  c.zm_pf = p->zm_pf;
+  c.zm_o = p->zm_o;
+  c.zm_pair = p->zm_pair;
+  c.zp_grid = p->zp_grid;
+  c.zp_items = p->zp_items;
   c.ss_ne = p->ss_ne;
   for (int k = 0; k < SS_MAX_NE; ++k) c.ss_off[k] = p->ss_off[k];
   c.ss_mask = p->d_ss_mask;
@@ -679,7 +685,14 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
     int zocc[2] = {0, 0};
     if (ok) zm_ctas_per_sm(np, ne, p->pid_bytes, zocc);
     if (ok && zocc[0] >= 1 && zocc[1] >= 1) {
-      const int64_t ncb = (S + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
+      // 7-point-like union [-S, -o, -1, 0, 1, o, S] with o a multiple of 32
+      // dividing S: 2-D tiles (32 columns x 8 lines of stride o) per work item
+      int64_t o = ne == 7 ? p->ss_off[ne - 2] : 0;
+      if (!(o >= 32 && o % 32 == 0 && S % o == 0 && p->ss_off[ne - 3] == 1) ||
+          atoi(env_or("SSCG_ZM_2D", "1")) == 0)
+        o = 0;
+      const int64_t ncb = o ? (o / 32) * ((S / o + 7) / 8) : (S + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
+      p->zm_o = (int)o;
       const int64_t steps = (n_rows + S - 1) / S;
       const int64_t grid = (int64_t)sms * zocc[1];
       int64_t zc = atoi(env_or("SSCG_ZM_ZC", "0"));
@@ -690,6 +703,30 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       p->zm_zc = (int)zc;
       p->zm_ncb = (int)ncb;
       p->zm_items = ncb * ((steps + zc - 1) / zc);
+      p->zm_pf = std::max(0, atoi(env_or("SSCG_ZM_PF", "0")));
+      // row pairs (levels >= 1): unions [-S, -1, 0, 1, S] or [-S, -o, -1, 0, 1, o, S]
+      // with S and o even (every even-offset pair load 16-byte aligned)
+      p->zm_pair = 0;
+      const bool pair_shape =
+          (ne == 5 && p->ss_off[1] == -1 && p->ss_off[3] == 1) ||
+          (ne == 7 && p->ss_off[2] == -1 && p->ss_off[4] == 1 && p->ss_off[5] % 2 == 0);
+      // opt-in: 124 registers, 2 CTAs/SM -- measured slower than the single march
+      if (pair_shape && S % 2 == 0 && atoi(env_or("SSCG_ZM_PAIR", "0")) != 0) {
+        const int occ = zp_ctas_per_sm(np, ne, p->pid_bytes);
+        if (occ >= 1) {
+          const int64_t ncb2 = (S + 2 * ROWS_PER_CTA - 1) / (2 * ROWS_PER_CTA);
+          const int64_t g2 = (int64_t)sms * occ;
+          int64_t zc2 = atoi(env_or("SSCG_ZM_ZC", "0"));
+          if (zc2 <= 0) zc2 = std::max<int64_t>(2, std::min<int64_t>(16, ncb2 * steps / (4 * g2)));
+          if (zc2 != zc) {  // one step count for both kernels: keep the pair choice
+            p->zm_zc = (int)zc2;
+            p->zm_items = ncb * ((steps + zc2 - 1) / zc2);
+          }
+          p->zp_items = ncb2 * ((steps + zc2 - 1) / zc2);
+          p->zp_grid = (int)std::max<int64_t>(1, std::min<int64_t>(g2, p->zp_items));
+          p->zm_pair = 1;
+        }
+      }
       p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * zocc[0], (int64_t)RED_BLOCKS, p->zm_items}));
       p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, p->zm_items));
     }
@@ -1203,7 +1240,7 @@ int sscg_plan_mpk_schedule(sscg_plan* p, int32_t sigma, int32_t* out) {
   out[1] = p->wave_on ? p->wave_grid : p->red_n;
   out[2] = p->d_pid ? p->pat_np : p->wave_lhi;
   // last slot: pattern kernel form (0 table walk, 1 superset mask, 2 plane march)
-  if (p->d_pid) out[3 + 2 * SMAX] = p->zm_S > 0 ? 2 : p->ss_ne > 0 ? 1 : 0;
+  if (p->d_pid) out[3 + 2 * SMAX] = p->zm_S > 0 ? (p->zm_pair ? 3 : 2) : p->ss_ne > 0 ? 1 : 0;
   if (!p->wave_on) {
     out[3] = sigma;
     for (int q = 0; q < sigma; ++q) out[4 + 2 * q] = 1;
