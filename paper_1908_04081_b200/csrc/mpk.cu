@@ -773,22 +773,26 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, int col
 #pragma unroll
     for (int q = 0; q < NV; ++q) nx[q] = hasn ? __ldg(px[q] + S) : 0.0;
 #endif
+    // Absent slots carry the value 0.0 in the pattern table; they read the
+    // row's own entry (offset 0: always in range) or the register slot as is.
+    // Every input a live level reads is finite (a non-finite column ends the
+    // solve: basis.py:220, adaptive.py:146), so an absent slot adds 0.0 * x =
+    // +-0.0, which leaves any partial sum csr_matvec can hold unchanged (a sum
+    // that starts at +0.0 is never -0.0 under round-to-nearest): the result is
+    // bit-identical to skipping the slot, without predication or selects.
     double xb[NV][NE];
 #pragma unroll
     for (int k = 1; k < NE - 1; ++k) {
       if (k == KC) continue;
-      const bool on = (m >> k) & 1u;
+      const int o = ((m >> k) & 1u) ? off[k] : 0;
 #pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        const bool ld = on && (q < NV - 1 || NV == 1 || rrow);
-        xb[q][k] = ld ? __ldg(px[q] + off[k]) : 0.0;
-      }
+      for (int q = 0; q < NV; ++q) xb[q][k] = __ldg(px[q] + o);
     }
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
-      xb[q][0] = (m & 1u) ? pv[q] : 0.0;
-      xb[q][KC] = (m & (1u << KC)) ? cu[q] : 0.0;
-      xb[q][NE - 1] = (m & (1u << (NE - 1))) ? nx[q] : 0.0;
+      xb[q][0] = pv[q];
+      xb[q][KC] = cu[q];
+      xb[q][NE - 1] = nx[q];
     }
     const double2* v2 = reinterpret_cast<const double2*>(T.val + pid * SS_MAX_NE);
     double acc[NV];
