@@ -111,7 +111,7 @@ class ClockSampler:
 def kernel_name(sched):
     """The level kernel (levels >= 1) a matrix-powers schedule runs."""
     if sched["kind"] == "pattern":
-        return {"pair march": "k_level_zp", "march": "k_level_zm",
+        return {"tile march": "k_level_zt", "pair march": "k_level_zp", "march": "k_level_zm",
                 "superset": "k_level_ss"}.get(sched.get("form"), "k_level_pat")
     return {"csr": "k_level_staged", "wavefront": "k_mpk_wave"}[sched["kind"]]
 

@@ -158,6 +158,7 @@ struct Ctx {
   int64_t zm_items;  // work items = zm_ncb x ceil(steps / zm_zc)
   int zm_pf;         // L2 prefetch of the plane zm_pf steps ahead (0: off)
   int zm_o;          // 2-D column tiles with line stride zm_o (0: 256 consecutive columns)
+  int zt_on;         // levels >= 1 by the shared-memory tile march (k_level_zt; needs zm_o)
   int zm_pair;       // levels >= 1 by the row-pair march (k_level_zp; zm_items in pairs)
   int zp_grid;       // CTAs of k_level_zp
   int64_t zp_items;  // its work items (512 columns each)

@@ -970,6 +970,197 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, ZM_MINB) k_level_zm(Ctx c, int l
 }
 
 // ---------------------------------------------------------------------------
+// Tile march with the plane in shared memory (levels >= 1; Ctx::zt_on).  For
+// the 3-D stencil union [-S, -o, -1, 0, 1, o, S] a work item is a 32 x 8 tile
+// of one plane (32 consecutive columns per warp, the 8 warps on lines of
+// stride o) marched over zm_zc planes.  Each plane's tile values sit in
+// shared memory (double-buffered by plane parity): the centres come from the
+// threads' own registers (the previous step's plane-ahead load), the one-cell
+// halo (two lines of 32, two columns of 8) is fetched by 96 threads with
+// cp.async one step ahead, and one barrier per plane publishes both.  The
+// +-1 / +-o slots are then shared-memory reads; -S and +S stay in registers.
+// Same products and adds in union order: bit-identical.
+constexpr int ZT_W = 34, ZT_H = 10, ZT_CELLS = ZT_W * ZT_H;  // tile + halo
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool in_range) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(in_range ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <typename ID, int NV, int RK>
+__device__ __forceinline__ void zt_item(const Ctx& c, const SsSmem& T, double* __restrict__ sb,
+                                        int tile, int z0, int z1,
+                                        const double* const* __restrict__ xs,
+                                        const double* const* __restrict__ ym,
+                                        double* const* __restrict__ yo, double th, double ga,
+                                        double mu, int plim, int rlim, int& bad) {
+  constexpr bool UNIT = (RK & 1) == 0, MU = (RK & 2) != 0;
+  const int S = (int)c.zm_S, o = c.zm_o, n = (int)(c.ld < INT32_MAX ? c.ld : INT32_MAX);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ntx = o >> 5;
+  const int tx0 = (tile % ntx) * 32, ty0 = (tile / ntx) * 8;
+  const int col = (ty0 + w) * o + tx0 + lane;
+  // halo cell of this thread (threads 0..95): lines -1 / 8 (64), columns -1 / 32 (32)
+  int hcol = 0, hcell = -1;
+  if (threadIdx.x < 64) {
+    const int hy = threadIdx.x < 32 ? -1 : 8;
+    hcol = (ty0 + hy) * o + tx0 + lane;
+    hcell = (hy + 1) * ZT_W + lane + 1;
+  } else if (threadIdx.x < 96) {
+    const int t = threadIdx.x - 64, hy = t & 7, hx = t < 8 ? -1 : t < 16 ? 32 : -2;
+    if (hx != -2) {
+      hcol = (ty0 + hy) * o + tx0 + hx;
+      hcell = (hy + 1) * ZT_W + hx + 1;
+    }
+  }
+  const int ccell = (w + 1) * ZT_W + lane + 1;
+  int r = z0 * S + col;
+  const double* px[NV];
+  double* po[NV];
+  const double* pm[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    px[q] = xs[q] + r;
+    po[q] = yo[q] + r;
+    pm[q] = ym[q] + r;
+  }
+  double pv[NV], cu[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    pv[q] = r >= S && r - S < n ? __ldg(px[q] - S) : 0.0;
+    cu[q] = r < n ? __ldg(px[q]) : 0.0;
+  }
+  // plane z0: centres and halo into buffer z0 & 1
+  {
+    double* b = sb + (z0 & 1) * NV * ZT_CELLS;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) b[q * ZT_CELLS + ccell] = cu[q];
+    if (hcell >= 0) {
+      const int hr = z0 * S + hcol;
+      const bool ok = hr >= 0 && hr < n;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) cp_async8(b + q * ZT_CELLS + hcell, xs[q] + (ok ? hr : 0), ok);
+    }
+    cp_async_commit();
+  }
+  const ID* pidp = reinterpret_cast<const ID*>(c.pid);
+  // absent slots: value 0.0 times a finite in-range (or zero-filled) entry
+  int pid_cur = r < plim ? (int)__ldg(pidp + r) : 0;
+  int pid_n1 = (z0 + 1 < z1 && r + S < plim) ? (int)__ldg(pidp + r + S) : 0;
+  for (int z = z0; z < z1; ++z) {
+    cp_async_wait_all();
+    __syncthreads();  // plane z's centres and halo visible; plane z-1's buffer free
+    const double* b = sb + (z & 1) * NV * ZT_CELLS;
+    double* bn = sb + ((z + 1) & 1) * NV * ZT_CELLS;
+    if (z + 1 < z1) {
+      if (hcell >= 0) {
+        const int hr = (z + 1) * S + hcol;
+        const bool ok = hr >= 0 && hr < n;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) cp_async8(bn + q * ZT_CELLS + hcell, xs[q] + (ok ? hr : 0), ok);
+      }
+      cp_async_commit();
+    }
+    const int pid = pid_cur;
+    const int pid_n2 = (z + 2 < z1 && r + 2 * S < plim) ? (int)__ldg(pidp + r + 2 * S) : 0;
+    double nx[NV];
+    const bool hasn = r + S < n;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) nx[q] = hasn ? __ldg(px[q] + S) : 0.0;
+    if (r < plim) {
+      const bool rrow = r < rlim;
+      const double2* v2 = reinterpret_cast<const double2*>(T.val + pid * SS_MAX_NE);
+      const double2 v01 = v2[0], v23 = v2[1], v45 = v2[2], v6 = v2[3];
+      double acc[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const double* bq = b + q * ZT_CELLS + ccell;
+        const double xo_m = bq[-ZT_W], x1_m = bq[-1], x1_p = bq[1], xo_p = bq[ZT_W];
+        double a = __dadd_rn(0.0, __dmul_rn(v01.x, pv[q]));
+        a = __dadd_rn(a, __dmul_rn(v01.y, xo_m));
+        a = __dadd_rn(a, __dmul_rn(v23.x, x1_m));
+        a = __dadd_rn(a, __dmul_rn(v23.y, cu[q]));
+        a = __dadd_rn(a, __dmul_rn(v45.x, x1_p));
+        a = __dadd_rn(a, __dmul_rn(v45.y, xo_p));
+        acc[q] = __dadd_rn(a, __dmul_rn(v6.x, nx[q]));
+      }
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        if (q == NV - 1 && NV > 1 && !rrow) break;
+        const double y2 = MU ? *pm[q] : 0.0;
+        const double wv = recur_t<UNIT>(acc[q], cu[q], y2, th, ga, mu, MU);
+        *po[q] = wv;
+        bad |= !finite(wv);
+      }
+    }
+    if (z + 1 < z1) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) bn[q * ZT_CELLS + ccell] = nx[q];
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      pv[q] = cu[q];
+      cu[q] = nx[q];
+      px[q] += S;
+      po[q] += S;
+      if (MU) pm[q] += S;
+    }
+    pid_cur = pid_n1;
+    pid_n1 = pid_n2;
+    r += S;
+  }
+  __syncthreads();  // the next item reuses the buffers
+}
+
+template <typename ID>
+__global__ void __launch_bounds__(ROWS_PER_CTA, ZM_MINB) k_level_zt(Ctx c, int l, ZmPtrs zp) {
+  __shared__ __align__(16) double sb[2 * 2 * ZT_CELLS];
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  if (l >= sbar) return;
+  const SsSmem T = load_ss(c);
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[l], ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
+  const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
+  const bool do_r = l < sbar - 1;
+  const double* xs[2] = {zp.xs[0], zp.xs[1]};
+  const double* ym[2] = {zp.ym[0], zp.ym[1]};
+  double* yo[2] = {zp.yo[0], zp.yo[1]};
+  int bad = 0;
+  const int plim = (int)lvl_p_rows(c, sigma, l), rlim = (int)lvl_r_rows(c, sigma, l);
+  const int rk = (ga == 1.0 ? 0 : 1) | (use_mu ? 2 : 0);
+  const int items = (int)c.zm_items, ncb = c.zm_ncb, zcs = c.zm_zc;
+  const int steps = (int)((c.n + c.zm_S - 1) / c.zm_S);
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int tile = it % ncb, z0 = (it / ncb) * zcs;
+    const int z1 = min(z0 + zcs, steps);
+#define ZT_CALL(NV, RKV, RL) \
+  zt_item<ID, NV, RKV>(c, T, sb, tile, z0, z1, xs, ym, yo, th, ga, mu, plim, RL, bad)
+    if (do_r) {
+      switch (rk) {
+        case 0: ZT_CALL(2, 0, rlim); break;
+        case 1: ZT_CALL(2, 1, rlim); break;
+        case 2: ZT_CALL(2, 2, rlim); break;
+        default: ZT_CALL(2, 3, rlim); break;
+      }
+    } else {
+      switch (rk) {
+        case 0: ZT_CALL(1, 0, plim); break;
+        case 1: ZT_CALL(1, 1, plim); break;
+        case 2: ZT_CALL(1, 2, plim); break;
+        default: ZT_CALL(1, 3, plim); break;
+      }
+    }
+#undef ZT_CALL
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+// ---------------------------------------------------------------------------
 // Row-pair plane march (levels >= 1; Ctx::zm_pair).  The union is the 2-D /
 // 3-D stencil form [-S, (-o,) -1, 0, 1, (o,) S] with S and o even: a thread
 // owns two adjacent columns (rows r, r + 1 with r even), so every even-offset
@@ -1820,6 +2011,8 @@ void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s) {
 #define ZM_LAUNCH(ID, NE)                                                      \
   if (level == 0)                                                              \
     k_level0_zm<ID, NE><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp);           \
+  else if (c.zt_on && NE == 7)                                                 \
+    k_level_zt<ID><<<c.pat_grid, ROWS_PER_CTA, bytes, s>>>(c, level, zp);      \
   else if (c.zm_pair && NE >= 5)                                               \
     k_level_zp<ID, (NE >= 5 ? NE : 5)><<<c.zp_grid, ROWS_PER_CTA, bytes, s>>>(c, level, zp); \
   else                                                                         \

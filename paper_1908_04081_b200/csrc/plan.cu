@@ -138,7 +138,7 @@ struct sscg_plan {
   double* d_pat_val = nullptr;
   int pf_off = 0, pf_ahead = 1;  // L2 prefetch of the pattern kernels (0: off)
   int64_t zm_S = 0;  // plane-march form (0: off)
-  int zm_zc = 0, zm_ncb = 0, zm_pf = 0, zm_o = 0, zm_pair = 0, zp_grid = 0;
+  int zm_zc = 0, zm_ncb = 0, zm_pf = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0;
   int64_t zp_items = 0;
   int64_t zm_items = 0;
   int ss_ne = 0;  // superset-mask form (superset_setup); 0: table-walking kernels
@@ -263,6 +263,7 @@ Ctx make_ctx(sscg_plan* p) {
   c.zm_pf = p->zm_pf;
   c.zm_o = p->zm_o;
   c.zm_pair = p->zm_pair;
+  c.zt_on = p->zt_on;
   c.zp_grid = p->zp_grid;
   c.zp_items = p->zp_items;
   c.ss_ne = p->ss_ne;
@@ -704,6 +705,10 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       p->zm_ncb = (int)ncb;
       p->zm_items = ncb * ((steps + zc - 1) / zc);
       p->zm_pf = std::max(0, atoi(env_or("SSCG_ZM_PF", "0")));
+      // shared-memory tile march for the 2-D tiled 7-slot form: whole 32 x 8
+      // tiles (o a multiple of 32, lines per plane a multiple of 8)
+      // (opt-in: the per-plane barrier makes it slower than the register march)
+      p->zt_on = o > 0 && (S / o) % 8 == 0 && atoi(env_or("SSCG_ZT", "0")) != 0;
       // row pairs (levels >= 1): unions [-S, -1, 0, 1, S] or [-S, -o, -1, 0, 1, o, S]
       // with S and o even (every even-offset pair load 16-byte aligned)
       p->zm_pair = 0;
@@ -1240,7 +1245,8 @@ int sscg_plan_mpk_schedule(sscg_plan* p, int32_t sigma, int32_t* out) {
   out[1] = p->wave_on ? p->wave_grid : p->red_n;
   out[2] = p->d_pid ? p->pat_np : p->wave_lhi;
   // last slot: pattern kernel form (0 table walk, 1 superset mask, 2 plane march)
-  if (p->d_pid) out[3 + 2 * SMAX] = p->zm_S > 0 ? (p->zm_pair ? 3 : 2) : p->ss_ne > 0 ? 1 : 0;
+  if (p->d_pid)
+    out[3 + 2 * SMAX] = p->zm_S > 0 ? (p->zt_on ? 4 : p->zm_pair ? 3 : 2) : p->ss_ne > 0 ? 1 : 0;
   if (!p->wave_on) {
     out[3] = sigma;
     for (int q = 0; q < sigma; ++q) out[4 + 2 * q] = 1;

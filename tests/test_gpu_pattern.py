@@ -19,7 +19,8 @@ from paper_1908_04081_b200.types import ProblemInstance, SparseMatrix
 pytestmark = pytest.mark.gpu
 
 
-_KEYS = ("SSCG_PATTERN", "SSCG_PAT_SS", "SSCG_ZM", "SSCG_ZM_ZC")
+_KEYS = ("SSCG_PATTERN", "SSCG_PAT_SS", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_ZM_PAIR",
+         "SSCG_ZT")
 
 
 def _with_env(env, fn):
@@ -114,16 +115,22 @@ def test_pattern_kernel_forms(gpu_ready):
     assert form(_tridiag_many_patterns) == "superset"
     assert form(lambda: problems.make_problem("c5", scale=28), {"SSCG_ZM": "0"}) == "superset"
     assert form(lambda: problems.make_problem("c5", scale=28), {"SSCG_PAT_SS": "0"}) == "table"
+    assert form(lambda: problems.make_problem("c5", scale=32), {"SSCG_ZT": "1"}) == "tile march"
+    assert form(lambda: problems.make_problem("c5", scale=28), {"SSCG_ZM_PAIR": "1"}) == "pair march"
 
 
-@pytest.mark.parametrize("env", [{"SSCG_ZM": "0"}, {"SSCG_PAT_SS": "0"}, {"SSCG_ZM_ZC": "3"}],
-                         ids=["superset", "table", "march_zc3"])
+@pytest.mark.parametrize("env", [{"SSCG_ZM": "0"}, {"SSCG_PAT_SS": "0"}, {"SSCG_ZM_ZC": "3"},
+                                 {"SSCG_ZM_2D": "0"}, {"SSCG_ZM_PAIR": "1"}, {"SSCG_ZT": "1"}],
+                         ids=["superset", "table", "march_zc3", "march_1d", "pair", "tile"])
 def test_pattern_forms_bit_identical(gpu_ready, env):
-    """Plane march (default), superset mask and table walk run the same
-    rounded operations in the same order: identical solves (Newton and
-    Chebyshev bases, unit and non-unit gamma, mu != 0)."""
+    """Plane march (default), its opt-in variants, superset mask and table
+    walk run the same rounded operations in the same order: identical solves
+    (Newton and Chebyshev bases, unit and non-unit gamma, mu != 0).  The 32^3
+    grids give whole 32 x 8 column tiles (2-D tiled march, tile march)."""
     for key, scale, kw in (("c5", 28, dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
-                           ("c3", 24, dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev"))):
+                           ("c3", 24, dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev")),
+                           ("c5", 32, dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
+                           ("c3", 32, dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev"))):
         cfg = AdaptiveConfig(**kw)
         ref = adaptive_solve(problems.make_problem(key, scale=scale), cfg, trace="fast")
         got = _with_env(env, lambda: adaptive_solve(problems.make_problem(key, scale=scale), cfg,
