@@ -650,7 +650,9 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
     std::vector<int> uni(off.begin(), off.end());
     std::sort(uni.begin(), uni.end());
     uni.erase(std::unique(uni.begin(), uni.end()), uni.end());
-    bool ok = !uni.empty() && (int)uni.size() <= SS_MAX_NE;
+    // (a union of 1-2 offsets -- a diagonal or bidiagonal operator, L2-sized in
+    // the configs -- runs faster on the table walk: c2 46.6k vs 42.7k iter/s)
+    bool ok = (int)uni.size() >= 3 && (int)uni.size() <= SS_MAX_NE;
     for (int q = 0; q < np && ok; ++q)
       for (int k = ptr[q] + 1; k < ptr[q + 1] && ok; ++k) ok = off[k - 1] < off[k];
     int socc[2] = {0, 0};
