@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define SSCG_ABI_VERSION 1
+#define SSCG_ABI_VERSION 2
 #define SSCG_MAX_SIGMA 16 /* 2*sigma+1 <= 33 basis columns */
 
 /* status codes */
@@ -178,6 +178,9 @@ typedef struct sscg_part {
   const int32_t* recv_idx;  /* [recv_off[n_peers]] */
   const unsigned char* nccl_id; /* 128-byte ncclUniqueId shared by the world, or NULL */
   const char* nccl_lib;     /* path of libnccl.so.2 (NULL: default search) */
+  const int64_t* global_rows; /* [n_local] global index of each local row, or NULL: lets a
+                                 stencil slab keep the plane-march kernels (patterns in
+                                 global offsets, planes walked through a table) */
 } sscg_part;
 
 int sscg_nccl_unique_id(const char* nccl_lib, unsigned char* id128);

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SSCG_LIB") or os.path.join(HERE, "_lib", "libsscg.so")
 
 # keep in sync with include/sscg.h
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_SIGMA = 16
 OK, EINVAL, ECUDA, ENOMEM, EPARAM, ENODEV, EBREAKDOWN, EFORMAT = range(8)
 RUNNING, CONVERGED, STAGNATED, DIVERGED, EXHAUSTED = range(5)
@@ -82,6 +82,7 @@ class SscgPart(C.Structure):
         ("peer_rank", C.POINTER(C.c_int32)), ("send_off", C.POINTER(C.c_int64)),
         ("recv_off", C.POINTER(C.c_int64)), ("send_idx", C.POINTER(C.c_int32)),
         ("recv_idx", C.POINTER(C.c_int32)), ("nccl_id", C.c_void_p), ("nccl_lib", C.c_char_p),
+        ("global_rows", C.POINTER(C.c_int64)),
     ]
 
 

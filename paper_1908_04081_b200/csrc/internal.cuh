@@ -156,6 +156,8 @@ struct Ctx {
   int zm_zc;       // steps per work item
   int zm_ncb;      // column blocks of 256 columns
   int64_t zm_items;  // work items = zm_ncb x ceil(steps / zm_zc)
+  int zm_np;         // planes of the walk
+  const int* zm_base;  // [zm_np] first local row of each plane (partitioned), or NULL (z * S)
   int zm_pf;         // L2 prefetch of the plane zm_pf steps ahead (0: off)
   int zm_o;          // 2-D column tiles with line stride zm_o (0: 256 consecutive columns)
   int zt_on;         // levels >= 1 by the shared-memory tile march (k_level_zt; needs zm_o)

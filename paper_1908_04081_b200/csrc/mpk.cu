@@ -688,6 +688,23 @@ __global__ void SS_LB k_level_ss(Ctx c, int l) {
 // gathers; the other slots are gathered as in row_dot_m.  The adds run over
 // the slots in union order = stored order, absent slots adding +0.0 (exact,
 // see row_dot_m): bit-identical to the other level kernels.
+// plane table of a row-partitioned march (Ctx::zm_base) in dynamic shared
+// memory after the pattern table (load_ss); nullptr: plane z starts at z * S.
+// Callers run load_ss first (its barrier also covers this copy: the copy is
+// issued before it by the same threads -- see k_level0_zm / k_level_zm).
+__device__ __forceinline__ int* zm_plane_smem(const Ctx& c) {
+  extern __shared__ __align__(16) double psm[];
+  return reinterpret_cast<int*>(reinterpret_cast<char*>(psm) + ss_smem_bytes_dev(c.pat_np));
+}
+__device__ __forceinline__ void zm_plane_copy(const Ctx& c) {
+  if (!c.zm_base) return;
+  int* sb = zm_plane_smem(c);
+  for (int i = threadIdx.x; i < c.zm_np; i += blockDim.x) sb[i] = __ldg(c.zm_base + i);
+}
+__device__ __forceinline__ const int* zm_plane_table(const Ctx& c) {
+  return c.zm_base ? zm_plane_smem(c) : nullptr;
+}
+
 #ifndef ZM_PIPE  // plane-ahead loads one step early (measured slower: registers)
 #define ZM_PIPE 0
 #endif
@@ -705,7 +722,8 @@ __device__ __forceinline__ double recur_t(double ay, double y, double y2, double
 // RK: recurrence kind, bit 0 = non-unit gamma (IEEE division), bit 1 = mu != 0
 // (two-back term) -- compile-time, so the Newton levels carry neither
 template <typename ID, int NE, int NV, bool L0, int RK>
-__device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, int col, int z0, int z1,
+__device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const int* __restrict__ sbase,
+                                          int col, int z0, int z1,
                                           const double* const* __restrict__ xs,
                                           const double* const* __restrict__ ym,
                                           double* const* __restrict__ yo, double th, double ga,
@@ -715,131 +733,103 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, int col
   constexpr bool UNIT = (RK & 1) == 0, MU = (RK & 2) != 0 && !L0;
   constexpr int NO = L0 ? NV - 1 : NV;  // output vectors
   constexpr int Q0 = L0 ? 1 : 0;        // first input vector with an output
-  // 32-bit row indices (plan.cu enables the march only for n + S < 2^31)
-  // vectors hold ld >= local rows entries (ghost rows of a partitioned plan
-  // have vector entries beyond the rows the matrix stores)
+  // 32-bit row indices (plan.cu enables the march only for ld + S < 2^31).
+  // Plane z of the walk starts at local row sbase[z] (a row-partitioned plan:
+  // owned planes, then ghost planes by depth) or z * S (sbase == nullptr).
+  // Vectors hold ld >= local rows entries.
   const int S = (int)c.zm_S, n = (int)(c.ld < INT32_MAX ? c.ld : INT32_MAX), n_own = (int)c.n_own;
-  int r = z0 * S + col;
-  if (r >= plim) return;
-  // per-thread row pointers, advanced by one plane per step: each gather is
-  // then one wide multiply-add (slot offset x 8 + row pointer)
-  const double* px[NV];
-  double* po[NO];
-  const double* pm[NO];
-#pragma unroll
-  for (int q = 0; q < NV; ++q) px[q] = xs[q] + r;
-#pragma unroll
-  for (int q = 0; q < NO; ++q) {
-    po[q] = yo[q] + r;
-    pm[q] = L0 ? nullptr : ym[q] + r;
-  }
+  const int np = c.zm_np;
+  if (z1 > np) z1 = np;
+  auto row_of = [&](int z) { return (sbase ? sbase[z] : z * S) + col; };
+  int r = row_of(z0);
   int off[NE];
 #pragma unroll
   for (int k = 0; k < NE; ++k) off[k] = c.ss_off[k];
   double pv[NV], cu[NV];
+  {
+    const int rp = z0 > 0 ? row_of(z0 - 1) : -1;
 #pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    pv[q] = r >= S ? __ldg(px[q] - S) : 0.0;
-    cu[q] = __ldg(px[q]);
+    for (int q = 0; q < NV; ++q) {
+      pv[q] = rp >= 0 && rp < n ? __ldg(xs[q] + rp) : 0.0;
+      cu[q] = r < n ? __ldg(xs[q] + r) : 0.0;
+    }
   }
-#if ZM_PIPE
-  // the plane ahead (the only HBM stream) is loaded one step early, so its
-  // latency overlaps a whole step instead of sitting on each step's path
-  double nxa[NV];
-#pragma unroll
-  for (int q = 0; q < NV; ++q) nxa[q] = r + S < n ? __ldg(px[q] + S) : 0.0;
-#endif
-  // row ids two steps ahead and the pattern mask one step ahead: the gathers
-  // of a step (predicated on the mask) issue without waiting on an id load
-  const ID* pidp = reinterpret_cast<const ID*>(c.pid) + r;
-  int pid_cur = (int)__ldg(pidp);
-  int pid_n1 = (z0 + 1 < z1 && r + S < plim) ? (int)__ldg(pidp + S) : 0;
-  unsigned m_cur = T.mask[pid_cur];
-  for (int z = z0; z < z1 && r < plim; ++z) {
+  // row ids two steps ahead and the row of the next plane one step ahead
+  const ID* pidp = reinterpret_cast<const ID*>(c.pid);
+  int r1 = z0 + 1 < np ? row_of(z0 + 1) : n;  // row of plane z + 1
+  int pid_cur = r < plim ? (int)__ldg(pidp + r) : 0;
+  int pid_n1 = (z0 + 1 < z1 && r1 < plim) ? (int)__ldg(pidp + r1) : 0;
+  for (int z = z0; z < z1; ++z) {
     const int pid = pid_cur;
-    const unsigned m = m_cur;
-    const int pid_n2 = (z + 2 < z1 && r + 2 * S < plim) ? (int)__ldg(pidp + 2 * S) : 0;
-    const bool rrow = r < rlim;  // the last vector (R) is produced on this row
+    const int r2 = z + 2 < np ? row_of(z + 2) : n;
+    const int pid_n2 = (z + 2 < z1 && r2 < plim) ? (int)__ldg(pidp + r2) : 0;
     double nx[NV];
-#if ZM_PIPE
-    const bool hasn = z + 1 < z1 && r + 2 * S < n;
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      nx[q] = nxa[q];
-      nxa[q] = hasn ? __ldg(px[q] + 2 * S) : 0.0;
-    }
-#else
-    const bool hasn = r + S < n;
+    for (int q = 0; q < NV; ++q) nx[q] = r1 < n ? __ldg(xs[q] + r1) : 0.0;
+    if (r < plim) {
+      const bool rrow = r < rlim;  // the last vector (R) is produced on this row
+      const unsigned m = T.mask[pid];
+      // Absent slots carry the value 0.0 in the pattern table; they read the
+      // row's own entry (offset 0: always in range) or the register slot as
+      // is.  Every input a live level reads is finite (a non-finite column
+      // ends the solve: basis.py:220, adaptive.py:146), so an absent slot adds
+      // 0.0 * x = +-0.0, which leaves any partial sum csr_matvec can hold
+      // unchanged (a sum that starts at +0.0 is never -0.0 under
+      // round-to-nearest): bit-identical to skipping the slot.
+      double xb[NV][NE];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) nx[q] = hasn ? __ldg(px[q] + S) : 0.0;
-#endif
-    // Absent slots carry the value 0.0 in the pattern table; they read the
-    // row's own entry (offset 0: always in range) or the register slot as is.
-    // Every input a live level reads is finite (a non-finite column ends the
-    // solve: basis.py:220, adaptive.py:146), so an absent slot adds 0.0 * x =
-    // +-0.0, which leaves any partial sum csr_matvec can hold unchanged (a sum
-    // that starts at +0.0 is never -0.0 under round-to-nearest): the result is
-    // bit-identical to skipping the slot, without predication or selects.
-    double xb[NV][NE];
+      for (int k = 1; k < NE - 1; ++k) {
+        if (k == KC) continue;
+        const int o = ((m >> k) & 1u) ? off[k] : 0;
 #pragma unroll
-    for (int k = 1; k < NE - 1; ++k) {
-      if (k == KC) continue;
-      const int o = ((m >> k) & 1u) ? off[k] : 0;
+        for (int q = 0; q < NV; ++q) xb[q][k] = __ldg(xs[q] + (r + o));
+      }
 #pragma unroll
-      for (int q = 0; q < NV; ++q) xb[q][k] = __ldg(px[q] + o);
-    }
+      for (int q = 0; q < NV; ++q) {
+        xb[q][0] = pv[q];
+        xb[q][KC] = cu[q];
+        xb[q][NE - 1] = nx[q];
+      }
+      const double2* v2 = reinterpret_cast<const double2*>(T.val + pid * SS_MAX_NE);
+      double acc[NV];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      xb[q][0] = pv[q];
-      xb[q][KC] = cu[q];
-      xb[q][NE - 1] = nx[q];
-    }
-    const double2* v2 = reinterpret_cast<const double2*>(T.val + pid * SS_MAX_NE);
-    double acc[NV];
+      for (int q = 0; q < NV; ++q) acc[q] = 0.0;
 #pragma unroll
-    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+      for (int k2 = 0; k2 < (NE + 1) / 2; ++k2) {
+        const double2 vv = v2[k2];
 #pragma unroll
-    for (int k2 = 0; k2 < (NE + 1) / 2; ++k2) {
-      const double2 vv = v2[k2];
+        for (int h = 0; h < 2; ++h) {
+          const int k = 2 * k2 + h;
+          if (k < NE) {
+            const double v = h ? vv.y : vv.x;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int k = 2 * k2 + h;
-        if (k < NE) {
-          const double v = h ? vv.y : vv.x;
-#pragma unroll
-          for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v, xb[q][k]));
+            for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v, xb[q][k]));
+          }
         }
       }
-    }
-    if (L0 && r < n_own) {
-      const double t = __dsub_rn(c.b[r], acc[0]);
-      tt = fma(t, t, tt);
-      rr = fma(cu[NV - 1], cu[NV - 1], rr);
-    }
+      if (L0 && r < n_own) {
+        const double t = __dsub_rn(c.b[r], acc[0]);
+        tt = fma(t, t, tt);
+        rr = fma(cu[NV - 1], cu[NV - 1], rr);
+      }
 #pragma unroll
-    for (int q = 0; q < NO; ++q) {
-      if (q == NO - 1 && NO > 1 && !rrow) break;
-      const double y2 = MU ? *pm[q] : 0.0;
-      const double w = recur_t<UNIT>(acc[Q0 + q], cu[Q0 + q], y2, th, ga, mu, MU);
-      *po[q] = w;
-      bad |= !finite(w);
+      for (int q = 0; q < NO; ++q) {
+        if (q == NO - 1 && NO > 1 && !rrow) break;
+        const double y2 = MU ? ym[q][r] : 0.0;
+        const double w = recur_t<UNIT>(acc[Q0 + q], cu[Q0 + q], y2, th, ga, mu, MU);
+        yo[q][r] = w;
+        bad |= !finite(w);
+      }
     }
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
       pv[q] = cu[q];
       cu[q] = nx[q];
-      px[q] += S;
-    }
-#pragma unroll
-    for (int q = 0; q < NO; ++q) {
-      po[q] += S;
-      if (MU) pm[q] += S;
     }
     pid_cur = pid_n1;
-    m_cur = T.mask[pid_n1];
     pid_n1 = pid_n2;
-    pidp += S;
-    r += S;
+    r = r1;
+    r1 = r2;
   }
 }
 
@@ -849,6 +839,7 @@ __device__ __forceinline__ void zm_items(const Ctx& c, const SsSmem& T, const do
                                          double ga, double mu, bool use_mu, int64_t plim,
                                          int64_t rlim, int& bad, double& tt, double& rr) {
   const int items = (int)c.zm_items, ncb = c.zm_ncb, zcs = c.zm_zc, S = (int)c.zm_S;
+  const int* sbase = zm_plane_table(c);
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
     const int cb = it % ncb, zc = it / ncb;
     int col;
@@ -865,8 +856,8 @@ __device__ __forceinline__ void zm_items(const Ctx& c, const SsSmem& T, const do
     }
     if (col >= S) continue;
     const int z0 = zc * zcs;
-    zm_column<ID, NE, NV, L0, RK>(c, T, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu, use_mu,
-                                    (int)plim, (int)rlim, bad, tt, rr);
+    zm_column<ID, NE, NV, L0, RK>(c, T, sbase, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu, use_mu,
+                                  (int)plim, (int)rlim, bad, tt, rr);
   }
 }
 
@@ -909,6 +900,7 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, ZM0_MINB) k_level0_zm(Ctx c, ZmP
   __shared__ double sm[ROWS_PER_CTA / 32];
   const SolverState* st = c.st;
   if (st->done) return;
+  zm_plane_copy(c);
   const SsSmem T = load_ss(c);
   const int sbar = st->s_bar;
   const int sigma = c.cfg->sigma;
@@ -941,6 +933,7 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, ZM_MINB) k_level_zm(Ctx c, int l
   if (st->done) return;
   const int sbar = st->s_bar;
   if (l >= sbar) return;
+  zm_plane_copy(c);
   const SsSmem T = load_ss(c);
   const int sigma = c.cfg->sigma;
   const double th = st->prm.th[l], ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
@@ -2006,7 +1999,7 @@ void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s) {
     return;
   }
   if (c.pid && c.ss_ne > 0 && c.zm_S > 0) {
-    const size_t bytes = ss_smem_bytes_dev(c.pat_np);
+    const size_t bytes = ss_smem_bytes_dev(c.pat_np) + (c.zm_base ? 4 * (size_t)c.zm_np : 0);
     const ZmPtrs zp = zm_ptrs(c, level, sigma);
 #define ZM_LAUNCH(ID, NE)                                                      \
   if (level == 0)                                                              \

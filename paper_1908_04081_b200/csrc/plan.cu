@@ -138,6 +138,8 @@ struct sscg_plan {
   double* d_pat_val = nullptr;
   int pf_off = 0, pf_ahead = 1;  // L2 prefetch of the pattern kernels (0: off)
   int64_t zm_S = 0;  // plane-march form (0: off)
+  int zm_np = 0;
+  int* d_zm_base = nullptr;  // plane table of a partitioned march
   int zm_zc = 0, zm_ncb = 0, zm_pf = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0;
   int64_t zp_items = 0;
   int64_t zm_items = 0;
@@ -261,6 +263,8 @@ Ctx make_ctx(sscg_plan* p) {
   c.zm_ncb = p->zm_ncb;
   c.zm_items = p->zm_items;
   c.zm_pf = p->zm_pf;
+  c.zm_np = p->zm_np;
+  c.zm_base = p->d_zm_base;
   c.zm_o = p->zm_o;
   c.zm_pair = p->zm_pair;
   c.zt_on = p->zt_on;
@@ -556,21 +560,29 @@ const char* env_or(const char* name, const char* dflt) {
 constexpr int PAT_MAX_BYTES = 16 * 1024;
 constexpr int WIN_R_CAP = 512;  // near columns: within 512 rows (window <= 1280 rows per vector)
 
-int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
-                  const double* values) {
-  p->d_pid = nullptr;
-  if (atoi(env_or("SSCG_PATTERN", "1")) == 0 || n_rows < 1) return SSCG_OK;
+// Pattern table of the rows: offset(row, col) is col - row (local indices) or,
+// for a row-partitioned plan that passes its rows' global indices, grows[col] -
+// grows[row] (the slab's rows are translates in the GLOBAL grid even where the
+// local ordering -- owned rows, then ghost planes by depth -- is not).  false
+// when the table outgrows shared memory.
+bool build_patterns(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                    const double* values, const int64_t* grows, std::vector<int>& ptr,
+                    std::vector<int>& off, std::vector<double>& val, std::vector<uint16_t>& ids) {
   std::unordered_map<uint64_t, std::vector<int>> buckets;
-  std::vector<int> ptr{0}, off;
-  std::vector<double> val;
-  std::vector<uint16_t> ids((size_t)n_rows);
+  ptr.assign(1, 0);
+  off.clear();
+  val.clear();
+  ids.assign((size_t)n_rows, 0);
+  auto ofs = [&](int64_t i, int64_t j) -> int64_t {
+    return grows ? grows[col_idx[j]] - grows[i] : (int64_t)col_idx[j] - i;
+  };
   for (int64_t i = 0; i < n_rows; ++i) {
     const int64_t b = row_ptr[i], e = row_ptr[i + 1];
     uint64_t h = 1469598103934665603ull ^ (uint64_t)(e - b);
     for (int64_t j = b; j < e; ++j) {
       uint64_t vb;
       std::memcpy(&vb, &values[j], 8);
-      h = (h ^ (uint64_t)(uint32_t)(col_idx[j] - (int32_t)i)) * 1099511628211ull;
+      h = (h ^ (uint64_t)ofs(i, j)) * 1099511628211ull;
       h = (h ^ vb) * 1099511628211ull;
     }
     int id = -1;
@@ -581,8 +593,7 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       bool same = true;
       for (int64_t j = b; j < e && same; ++j) {
         const int k = pb + (int)(j - b);
-        same = off[k] == (int)(col_idx[j] - (int32_t)i) &&
-               std::memcmp(&val[k], &values[j], 8) == 0;
+        same = off[k] == ofs(i, j) && std::memcmp(&val[k], &values[j], 8) == 0;
       }
       if (same) {
         id = q;
@@ -592,15 +603,75 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
     if (id < 0) {
       id = (int)ptr.size() - 1;
       const size_t ne = off.size() + (size_t)(e - b);
-      if (id >= 65535 || ne * 12 + (ptr.size() + 1) * 4 > (size_t)PAT_MAX_BYTES) return SSCG_OK;
+      if (id >= 65535 || ne * 12 + (ptr.size() + 1) * 4 > (size_t)PAT_MAX_BYTES) return false;
       for (int64_t j = b; j < e; ++j) {
-        off.push_back((int)(col_idx[j] - (int32_t)i));
+        const int64_t o = ofs(i, j);
+        if (o != (int64_t)(int)o) return false;
+        off.push_back((int)o);
         val.push_back(values[j]);
       }
       ptr.push_back((int)off.size());
       cand.push_back(id);
     }
     ids[(size_t)i] = (uint16_t)id;
+  }
+  return true;
+}
+
+// The plane-march union: [-S .. 0 .. S], 3, 5 or 7 offsets, S >= 256.
+int64_t march_stride(const std::vector<int>& off) {
+  std::vector<int> uni(off.begin(), off.end());
+  std::sort(uni.begin(), uni.end());
+  uni.erase(std::unique(uni.begin(), uni.end()), uni.end());
+  const int ne = (int)uni.size();
+  if (ne != 3 && ne != 5 && ne != 7) return 0;
+  for (int k = 0; k < ne; ++k)
+    if (uni[(size_t)k] != -uni[(size_t)(ne - 1 - k)]) return 0;
+  return uni.back() >= 256 ? uni.back() : 0;
+}
+
+// Local planes of a partitioned plan: every block of S local rows holds one
+// whole global plane in global order, and the planes form one contiguous range.
+// Returns the local row of each plane's first row in geometric order, or empty.
+std::vector<int> plane_bases(int64_t n_local, const int64_t* grows, int64_t S) {
+  std::vector<int> none;
+  if (S <= 0 || n_local % S != 0) return none;
+  const int64_t np = n_local / S;
+  int64_t pmin = INT64_MAX;
+  for (int64_t b = 0; b < np; ++b) pmin = std::min(pmin, grows[b * S] / S);
+  std::vector<int> base((size_t)np, -1);
+  for (int64_t b = 0; b < np; ++b) {
+    const int64_t g0 = grows[b * S];
+    if (g0 % S != 0) return none;
+    for (int64_t k = 1; k < S; ++k)
+      if (grows[b * S + k] != g0 + k) return none;
+    const int64_t z = g0 / S - pmin;
+    if (z < 0 || z >= np || base[(size_t)z] >= 0) return none;
+    base[(size_t)z] = (int)(b * S);
+  }
+  return base;
+}
+
+int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                  const double* values, const int64_t* grows = nullptr, int64_t n_local = 0) {
+  p->d_pid = nullptr;
+  if (atoi(env_or("SSCG_PATTERN", "1")) == 0 || n_rows < 1) return SSCG_OK;
+  std::vector<int> ptr, off;
+  std::vector<double> val;
+  std::vector<uint16_t> ids;
+  // partitioned: the global-offset table, when its union marches and the local
+  // rows are whole global planes; otherwise the local-offset table
+  std::vector<int> bases;
+  bool ok = false;
+  if (grows && atoi(env_or("SSCG_ZM", "1")) != 0 &&
+      build_patterns(n_rows, row_ptr, col_idx, values, grows, ptr, off, val, ids)) {
+    const int64_t S = march_stride(off);
+    bases = plane_bases(n_local, grows, S);
+    ok = !bases.empty();
+  }
+  if (!ok) {
+    bases.clear();
+    if (!build_patterns(n_rows, row_ptr, col_idx, values, nullptr, ptr, off, val, ids)) return SSCG_OK;
   }
   const int np = (int)ptr.size() - 1, ne = (int)off.size();
   int occ[2] = {0, 0};
@@ -683,7 +754,7 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
     const int ne = p->ss_ne;
     const int64_t S = p->ss_off[ne - 1];
     bool ok = (ne == 3 || ne == 5 || ne == 7) && S >= 256 && p->ss_off[ne / 2] == 0 &&
-              p->ld + S < ((int64_t)1 << 31);
+              p->ld + S < ((int64_t)1 << 31) && bases.size() <= 4096;
     for (int k = 0; k < ne && ok; ++k) ok = p->ss_off[k] == -p->ss_off[ne - 1 - k];
     int zocc[2] = {0, 0};
     if (ok) zm_ctas_per_sm(np, ne, p->pid_bytes, zocc);
@@ -696,13 +767,19 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
         o = 0;
       const int64_t ncb = o ? (o / 32) * ((S / o + 7) / 8) : (S + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
       p->zm_o = (int)o;
-      const int64_t steps = (n_rows + S - 1) / S;
+      // planes of the walk: the partitioned plan's plane table, else ceil(n / S)
+      const int64_t steps = bases.empty() ? (n_rows + S - 1) / S : (int64_t)bases.size();
       const int64_t grid = (int64_t)sms * zocc[1];
       int64_t zc = atoi(env_or("SSCG_ZM_ZC", "0"));
       // ~16 planes per item (measured best on 256^3: 8-32 within 1%), fewer
       // when the operator is too small to give every CTA a few items
       if (zc <= 0) zc = std::max<int64_t>(2, std::min<int64_t>(16, ncb * steps / (4 * grid)));
       p->zm_S = S;
+      p->zm_np = (int)steps;
+      if (!bases.empty()) {
+        TRY(dalloc(p, &p->d_zm_base, bases.size()));
+        CUDA_OK(cudaMemcpy(p->d_zm_base, bases.data(), 4 * bases.size(), cudaMemcpyHostToDevice));
+      }
       p->zm_zc = (int)zc;
       p->zm_ncb = (int)ncb;
       p->zm_items = ncb * ((steps + zc - 1) / zc);
@@ -710,7 +787,7 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       // shared-memory tile march for the 2-D tiled 7-slot form: whole 32 x 8
       // tiles (o a multiple of 32, lines per plane a multiple of 8)
       // (opt-in: the per-plane barrier makes it slower than the register march)
-      p->zt_on = o > 0 && (S / o) % 8 == 0 && atoi(env_or("SSCG_ZT", "0")) != 0;
+      p->zt_on = o > 0 && (S / o) % 8 == 0 && bases.empty() && atoi(env_or("SSCG_ZT", "0")) != 0;
       // row pairs (levels >= 1): unions [-S, -1, 0, 1, S] or [-S, -o, -1, 0, 1, o, S]
       // with S and o even (every even-offset pair load 16-byte aligned)
       p->zm_pair = 0;
@@ -718,7 +795,7 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
           (ne == 5 && p->ss_off[1] == -1 && p->ss_off[3] == 1) ||
           (ne == 7 && p->ss_off[2] == -1 && p->ss_off[4] == 1 && p->ss_off[5] % 2 == 0);
       // opt-in: 124 registers, 2 CTAs/SM -- measured slower than the single march
-      if (pair_shape && S % 2 == 0 && atoi(env_or("SSCG_ZM_PAIR", "0")) != 0) {
+      if (pair_shape && S % 2 == 0 && bases.empty() && atoi(env_or("SSCG_ZM_PAIR", "0")) != 0) {
         const int occ = zp_ctas_per_sm(np, ne, p->pid_bytes);
         if (occ >= 1) {
           const int64_t ncb2 = (S + 2 * ROWS_PER_CTA - 1) / (2 * ROWS_PER_CTA);
@@ -737,6 +814,13 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * zocc[0], (int64_t)RED_BLOCKS, p->zm_items}));
       p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, p->zm_items));
     }
+  }
+  // a global-offset table is only valid for the march (the other kernels
+  // add offsets to local rows): without it, fall back to the CSR kernels
+  if (!bases.empty() && p->zm_S == 0) {
+    p->d_pid = nullptr;
+    p->ss_ne = 0;
+    return SSCG_OK;
   }
   // windowed kernels: near radius = the largest |offset| up to WIN_R_CAP (even)
   p->win_r = -1;
@@ -902,7 +986,7 @@ int sscg_plan_create_part(sscg_plan** out, int32_t device, const sscg_part* part
     int rc = plan_init(p, device, q.n_rows, q.n_own, q.n_local, q.nnz, q.row_ptr, q.col_idx,
                        q.values, q.lvl_rows, q.depth);
     if (rc) return rc;
-    TRY(pattern_setup(p, q.n_rows, q.row_ptr, q.col_idx, q.values));
+    TRY(pattern_setup(p, q.n_rows, q.row_ptr, q.col_idx, q.values, q.global_rows, q.n_local));
     p->partitioned = 1;
     p->rank = q.rank;
     p->world = q.world;
@@ -978,7 +1062,8 @@ int sscg_plan_destroy(sscg_plan* p) {
                   p->d_rj, p->d_st, p->d_cfg, p->d_part_t, p->d_part_r, p->d_part_d,
                   p->d_part_g, p->d_leja, p->d_it, p->d_ri, p->d_rd, p->d_conds, p->d_th,
                   p->d_ga, p->d_mu, p->d_otrue, p->d_fg, p->d_red, p->d_wdep, p->d_wcnt,
-                  p->d_pid, p->d_pat_ptr, p->d_pat_off, p->d_pat_val, p->d_ss_mask, p->d_ss_val};
+                  p->d_pid, p->d_pat_ptr, p->d_pat_off, p->d_pat_val, p->d_ss_mask, p->d_ss_val,
+                  p->d_zm_base};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_done) cudaFreeHost(p->h_done);

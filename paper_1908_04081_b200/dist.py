@@ -37,6 +37,7 @@ def _part_struct(part, rank, world, nccl_id=None, nccl_lib=None):
         ro=np.ascontiguousarray(part.recv_off, dtype=np.int64),
         si=np.ascontiguousarray(part.send_idx, dtype=np.int32),
         ri=np.ascontiguousarray(part.recv_idx, dtype=np.int32),
+        gr=np.ascontiguousarray(part.global_rows, dtype=np.int64),
     )
     s = L.SscgPart()
     s.n_own, s.n_rows, s.n_local = part.n_own, part.n_rows, part.n_local
@@ -52,6 +53,7 @@ def _part_struct(part, rank, world, nccl_id=None, nccl_lib=None):
     s.recv_off = keep["ro"].ctypes.data_as(i64)
     s.send_idx = L.iptr(keep["si"])
     s.recv_idx = L.iptr(keep["ri"])
+    s.global_rows = keep["gr"].ctypes.data_as(i64)
     if nccl_id is not None:
         keep["id"] = C.create_string_buffer(bytes(nccl_id), 128)
         s.nccl_id = C.cast(keep["id"], C.c_void_p)

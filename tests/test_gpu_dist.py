@@ -77,3 +77,15 @@ def test_partitioned_rejects_sigma_above_depth(gpu_ready):
     grp = VirtualGroup(CsrRows.of(prob.a), 2, depth=4)
     with pytest.raises(Exception):
         grp.solve(prob, AdaptiveConfig(sigma=6, eps_star=1e-8))
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_partitioned_slabs_keep_the_plane_march(gpu_ready, world):
+    """Every rank of a stencil slab partition runs the plane-march kernels:
+    patterns in global offsets, the owned and ghost planes walked through a
+    plane table (sscg_part.global_rows), not only the bottom slab whose local
+    rows happen to be in grid order."""
+    from paper_1908_04081_b200.dist import VirtualGroup
+    g = VirtualGroup(Stencil7Rows(32, 32, 32 * world), world, 12)
+    assert [pl.mpk_schedule(12)["form"] for pl in g.plans] == ["march"] * world
+
