@@ -47,6 +47,8 @@ CONFIGS = {
             "c5 weak-scaled: 3D Poisson 7-pt 256^3 per GPU, sigma=12 Newton, eps*=1e-10"),
     "c3": ("c3", None, 10, "chebyshev", 1e-10, "c3: 3D Poisson 7-pt 128^3, sigma=10 Chebyshev, 1e-10"),
     "c4": ("c4", None, 10, "newton", 1e-8, "c4: 27-pt var-coef 192^3, sigma=10 Newton, 1e-8"),
+    "c4j": ("c4j", None, 10, "newton", 1e-8,
+            "c4 Jacobi-scaled (secondary run, SURVEY.md H6): 27-pt var-coef 192^3, sigma=10 Newton, 1e-8"),
     "c1": ("c1", None, 8, "newton", 1e-10, "c1: 2D Poisson 64^2, sigma=8 Newton, 1e-10"),
     "c2": ("c2", None, 10, "chebyshev", 1e-8, "c2: Strakos 1e4, sigma=10 Chebyshev, 1e-8"),
 }

@@ -508,6 +508,8 @@ def solve_cases():
                       dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
         "solve_c4p": (lambda: to_ref(problems.make_problem("c4", scale=12)),
                       dict(sigma=10, eps_star=1e-8, basis_kind="newton", max_outer=400)),
+        "solve_c4jp": (lambda: to_ref(problems.make_problem("c4j", scale=12)),
+                       dict(sigma=10, eps_star=1e-8, basis_kind="newton")),
         "solve_494bus_old": (lambda: bus, dict(sigma=5, eps_star=1e-6, variant="old",
                                                basis_kind="monomial", c_strategy="unit")),
         "solve_494bus_cheb6": (lambda: bus, dict(sigma=6, eps_star=1e-8, basis_kind="chebyshev")),
@@ -531,6 +533,16 @@ def solve_cases():
                                                         basis_kind="newton",
                                                         c_strategy="full-bound"))
     return cases
+
+
+def gen_c4j():
+    """c4 Jacobi-scaled proxy (the secondary c4 run): the solve
+    with its inputs, and its Gram-order noise runs."""
+    c4jp = to_ref(problems.make_problem("c4j", scale=12))
+    save("solve_c4jp", **run_ref(c4jp, dict(sigma=10, eps_star=1e-8, basis_kind="newton")),
+         **{"in_" + k: v for k, v in problem_arrays(c4jp).items()})
+    os.environ["NOISE_ONLY"] = "solve_c4jp"
+    gen_noise()
 
 
 def gen_noise():

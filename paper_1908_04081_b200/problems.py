@@ -211,6 +211,20 @@ def varcoef27(n=192, sigma_ln=1.5, seed=0):
     return _problem(a, b, gersh, gersh, math.inf, f"varcoef27-{n}")
 
 
+def varcoef27_jacobi(n=192, seed=0):
+    """c4 with the paper's two-sided Jacobi scaling (matio.py
+    jacobi_precondition): A_hat = D^-1/2 A D^-1/2, the same b.  SURVEY.md H6:
+    BASELINE.json does not pin the scaling; the literal c4 is the primary run,
+    this the secondary one."""
+    from .matio import jacobi_precondition
+    base = varcoef27(n, seed=seed)
+    a_hat, _ = jacobi_precondition(base.a)
+    # |A_hat| <= Gershgorin of the scaled rows (unit diagonal)
+    rs = np.add.reduceat(np.abs(np.asarray(a_hat.values)), np.asarray(a_hat.row_ptr)[:-1])
+    g = float(rs.max())
+    return _problem(a_hat, base.b, g, g, math.inf, f"varcoef27-jacobi-{n}")
+
+
 CONFIGS = {
     "c1": dict(desc="2D Poisson 64^2, sigma=8 Newton, 1e-10", sigma=8, eps_star=1e-10,
                basis_kind="newton"),
@@ -222,6 +236,8 @@ CONFIGS = {
                eps_star=1e-10, basis_kind="chebyshev"),
     "c4": dict(desc="27-pt var-coef 192^3, sigma=10 Newton, 1e-8", sigma=10, eps_star=1e-8,
                basis_kind="newton"),
+    "c4j": dict(desc="27-pt var-coef 192^3, Jacobi-scaled, sigma=10 Newton, 1e-8", sigma=10,
+                eps_star=1e-8, basis_kind="newton"),
     "c5": dict(desc="3D Poisson 512^3, sigma=12 Newton, 1e-10", sigma=12, eps_star=1e-10,
                basis_kind="newton"),
     "c5w": dict(desc="3D Poisson 256^3 per GPU (weak), sigma=12 Newton, 1e-10", sigma=12,
@@ -239,6 +255,8 @@ def make_problem(name, seed=0, scale=None, world=1):
         return poisson3d(scale or 128, seed=seed)
     if name == "c4":
         return varcoef27(scale or 192, seed=seed)
+    if name == "c4j":
+        return varcoef27_jacobi(scale or 192, seed=seed)
     if name == "c5":
         return poisson3d(scale or 512, seed=seed)
     if name == "c5w":

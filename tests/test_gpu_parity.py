@@ -305,6 +305,14 @@ def test_c4_proxy_solve(gpu_ready):
     check_against_golden("solve_c4p", prob, ref, x, tr, co)
 
 
+def test_c4_jacobi_proxy_solve(gpu_ready):
+    """The secondary c4 run (two-sided Jacobi scaling)."""
+    ref = golden("solve_c4jp")
+    prob = problem_from_arrays(ref, "in_")
+    x, tr, co = solve(prob, AdaptiveConfig(**cfg_of(ref)))
+    check_against_golden("solve_c4jp", prob, ref, x, tr, co)
+
+
 @pytest.mark.parametrize("kind", ["newton", "chebyshev"])
 @pytest.mark.parametrize("strat", ["adaptive", "unit", "kappa-estimate"])
 def test_nos1_acceptance(gpu_ready, kind, strat):

@@ -149,6 +149,16 @@ def test_solve_c4_proxy_matches_reference():
     _check_solve(ref, x, tr, al, be)
 
 
+def test_solve_c4_jacobi_proxy_matches_reference():
+    ref = golden("solve_c4jp")
+    prob = problem_from_arrays(ref, "in_")
+    gen = problems.make_problem("c4j", scale=12)
+    np.testing.assert_array_equal(gen.a.values, prob.a.values)  # scaling pinned too
+    np.testing.assert_array_equal(gen.b, prob.b)
+    x, tr, al, be = O.solve_problem(prob, O.OracleConfig(**cfg_of(ref)))
+    _check_solve(ref, x, tr, al, be)
+
+
 @pytest.mark.parametrize("kind", ["newton", "chebyshev"])
 @pytest.mark.parametrize("strat", ["adaptive", "unit", "kappa-estimate"])
 def test_nos1_acceptance_runs_match_reference(kind, strat):
