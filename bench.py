@@ -115,7 +115,8 @@ def kernel_name(sched):
     if sched["kind"] == "pattern":
         return {"tile march": "k_level_zt", "pair march": "k_level_zp", "march": "k_level_zm",
                 "superset": "k_level_ss"}.get(sched.get("form"), "k_level_pat")
-    return {"csr": "k_level_staged", "wavefront": "k_mpk_wave"}[sched["kind"]]
+    return {"csr": "k_level_staged", "wavefront": "k_mpk_wave",
+            "stencil values": "k_level_vs"}[sched["kind"]]
 
 
 def a_bytes_per_level(n, nnz, sched):
@@ -124,6 +125,8 @@ def a_bytes_per_level(n, nnz, sched):
     1- or 2-byte row ids (the pattern table lives in shared memory)."""
     if sched and sched.get("kind") == "pattern":
         return (1 if sched["patterns"] <= 256 else 2) * n
+    if sched and sched.get("kind") == "stencil values":  # 8 bytes per union slot and row
+        return 8 * sched["slots"] * n
     return 12 * nnz + 4 * (n + 1)
 
 
@@ -433,7 +436,8 @@ def run_ours(args, rank, world):
                          "wavefront": "(wavefront matrix powers + recurrence)",
                          "pattern": "(pattern-compressed matrix powers + recurrence, "
                                     f"{sched.get('form')} form)",
-                         "csr": "(CSR matrix powers + recurrence)"}[sched["kind"]],
+                         "csr": "(CSR matrix powers + recurrence)",
+                         "stencil values": "(value-stream stencil matrix powers + recurrence)"}[sched["kind"]],
                      "a_bytes_per_level": a_bytes_per_level(n, nnz, sched),
                      "a_bytes_per_level_csr": a_bytes_per_level(n, nnz, None),
                      "mpk_schedule": sched,

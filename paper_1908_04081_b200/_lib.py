@@ -231,16 +231,17 @@ class Plan:
 
 def plan_mpk_schedule(lib, handle, sigma):
     """sscg_plan_mpk_schedule of a plan handle:
-    {"kind": "csr"|"wavefront"|"pattern", "form": pattern kernel form ("table" walk,
+    {"kind": "csr"|"wavefront"|"pattern"|"stencil values", "form": pattern kernel form ("table" walk,
     "superset" mask, plane "march", row-"pair march", shared-memory "tile march") or None, "wavefront": bool, "ctas": G,
      "reach_tiles": L (wavefront), "patterns": P (pattern), "passes": [(levels, lag), ...]}."""
     out = np.zeros(4 + 2 * 16, dtype=np.int32)
     check(lib.sscg_plan_mpk_schedule(handle, int(sigma), iptr(out)))
     npass = int(out[3])
-    kind = ("csr", "wavefront", "pattern")[int(out[0])]
+    kind = ("csr", "wavefront", "pattern", "stencil values")[int(out[0])]
     form = (("table", "superset", "march", "pair march", "tile march")[int(out[-1])]
             if kind == "pattern" else None)
     return {"kind": kind, "form": form, "wavefront": kind == "wavefront", "ctas": int(out[1]),
             "reach_tiles": int(out[2]) if kind == "wavefront" else 0,
             "patterns": int(out[2]) if kind == "pattern" else 0,
+            "slots": int(out[2]) if kind == "stencil values" else 0,
             "passes": [(int(out[4 + 2 * q]), int(out[5 + 2 * q])) for q in range(npass)]}

@@ -35,6 +35,7 @@
 #define GRAM_BLOCKS (2 * NUM_SMS)  // capacity of the Gram partials
 #define SMALL_THREADS 512
 #define SS_MAX_NE 8                // union size of the unrolled superset-mask pattern kernels
+#define VS_MAX_NE 32               // union size of the value-stream stencil kernels
 
 struct RitzDev {  // ritz.py:28-158
   double hi_om, hi_h, hi_zeta;
@@ -145,6 +146,14 @@ struct Ctx {
   // ss_off[0..ss_ne), so a row is (mask of present union entries, values per
   // union slot).  The offsets travel as kernel parameters (constant bank) and
   // the row loop unrolls fully at compile time.
+  // value-stream form (plan.cu vs_setup; vs_ne == 0: not used): a stencil
+  // operator whose values vary by row (c4) -- every row's offsets are a
+  // subsequence of the sorted union vs_off[0..vs_ne), values stored slot-major
+  // vs_val[k * ld + row] (absent slots 0.0): 8 bytes per slot and row, no
+  // column indices or row pointers.
+  int vs_ne;
+  int vs_off[VS_MAX_NE];
+  const double* vs_val;
   int ss_ne;
   int ss_off[SS_MAX_NE];
   // plane-march form (mpk.cu k_level_zm): the union is symmetric, [-S .. 0 .. S]
@@ -238,6 +247,7 @@ size_t ss_smem_bytes(int np);
 int ss_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 int zm_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 int zp_ctas_per_sm(int np, int ne, int pid_bytes);
+int vs_ctas_per_sm(int ne, int* out2);
 void staged_prepare(int cap);
 int staged_ctas_per_sm(int cap);
 int wave_ctas_per_sm(int cap);

@@ -1376,6 +1376,125 @@ __global__ void ZP_LB k_level_zp(Ctx c, int l, ZmPtrs zp) {
 }
 
 // ---------------------------------------------------------------------------
+// Value-stream stencil kernels (Ctx::vs_*): operators with a stencil's column
+// structure but row-varying values (c4: 27-point variable coefficients) do not
+// compress to patterns; here the column structure is the union of offsets
+// (kernel parameters) and the values stream slot-major, coalesced, 8 bytes per
+// slot and row -- no column indices, no row pointers (12 nnz + 4 n bytes of
+// CSR become 8 ne n).  One row per thread, slots in union order = stored order,
+// in chunks of VS_CHUNK (gathers of a chunk in flight together).  An absent
+// slot has value 0.0 and gathers from the clamped index (in range, finite:
+// see zm_column): adding 0.0 * x = +-0.0 is exact -- bit-identical to CSR.
+#ifndef VS_CHUNK
+#define VS_CHUNK 9
+#endif
+template <int NV, int NE>
+__device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
+                                       const double* const* __restrict__ xs, double* acc) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  const double* vp = c.vs_val + i;
+  const int64_t ldv = c.ld;
+#pragma unroll
+  for (int k0 = 0; k0 < NE; k0 += VS_CHUNK) {
+    double v[VS_CHUNK], xb[NV][VS_CHUNK];
+#pragma unroll
+    for (int kk = 0; kk < VS_CHUNK; ++kk) {
+      const int k = k0 + kk;
+      if (k < NE) {
+        v[kk] = __ldg(vp + (int64_t)k * ldv);
+        const int j = min(max(i + c.vs_off[k], 0), nm1);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) xb[q][kk] = __ldg(xs[q] + j);
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < VS_CHUNK; ++kk) {
+      if (k0 + kk < NE) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v[kk], xb[q][kk]));
+      }
+    }
+  }
+}
+
+template <int NE>
+__global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_vs(Ctx c, ZmPtrs zp) {
+  __shared__ double sm[ROWS_PER_CTA / 32];
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[0], ga = st->prm.ga[0];
+  const bool do_r = sbar >= 2;
+  const double* xs[3] = {zp.xs[0], zp.xs[1], zp.xs[2]};
+  double tt = 0.0, rr = 0.0;
+  int bad = 0;
+  const int n_own = (int)c.n_own, plim = (int)lvl_p_rows(c, sigma, 0);
+  const int rlim = do_r ? (int)lvl_r_rows(c, sigma, 0) : 0, nm1 = (int)c.n - 1;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
+    double acc[3];
+    vs_row<3, NE>(c, i, nm1, xs, acc);
+    const double p = xs[1][i], r = xs[2][i];
+    if (i < n_own) {
+      const double t = __dsub_rn(c.b[i], acc[0]);
+      tt = fma(t, t, tt);
+      rr = fma(r, r, rr);
+    }
+    const double wp = recur(acc[1], p, 0.0, th, ga, 0.0, false);
+    zp.yo[0][i] = wp;
+    bad |= !finite(wp);
+    if (i < rlim) {
+      const double wr = recur(acc[2], r, 0.0, th, ga, 0.0, false);
+      zp.yo[1][i] = wr;
+      bad |= !finite(wr);
+    }
+  }
+  tt = block_sum<ROWS_PER_CTA>(tt, sm);
+  rr = block_sum<ROWS_PER_CTA>(rr, sm);
+  if (threadIdx.x == 0) {
+    c.part_t[blockIdx.x] = tt;
+    c.part_r[blockIdx.x] = rr;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+template <int NE>
+__global__ void __launch_bounds__(ROWS_PER_CTA) k_level_vs(Ctx c, int l, ZmPtrs zp) {
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  if (l >= sbar) return;
+  const int sigma = c.cfg->sigma;
+  const double th = st->prm.th[l], ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
+  const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
+  const bool do_r = l < sbar - 1;
+  const int plim = (int)lvl_p_rows(c, sigma, l), rlim = (int)lvl_r_rows(c, sigma, l);
+  const int nm1 = (int)c.n - 1;
+  const int stride = gridDim.x * blockDim.x;
+  int bad = 0;
+  const double* xs[2] = {zp.xs[0], zp.xs[1]};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
+    double acc[2];
+    const bool rrow = do_r && i < rlim;
+    if (rrow)
+      vs_row<2, NE>(c, i, nm1, xs, acc);
+    else
+      vs_row<1, NE>(c, i, nm1, xs, acc);
+    const double wp = recur(acc[0], xs[0][i], use_mu ? zp.ym[0][i] : 0.0, th, ga, mu, use_mu);
+    zp.yo[0][i] = wp;
+    bad |= !finite(wp);
+    if (rrow) {
+      const double wr = recur(acc[1], xs[1][i], use_mu ? zp.ym[1][i] : 0.0, th, ga, mu, use_mu);
+      zp.yo[1][i] = wr;
+      bad |= !finite(wr);
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+// ---------------------------------------------------------------------------
 // Windowed pattern kernels.  A CTA walks 256-row tiles; for each tile one TMA
 // bulk copy per input vector brings the contiguous window [base - R,
 // base + 256 + R) into shared memory (with the tile's row ids), double
@@ -1924,6 +2043,20 @@ int zp_ctas_per_sm(int np, int ne, int pid_bytes) {
   return b;
 }
 
+// value-stream kernels: CTAs per SM of level 0 and levels >= 1
+int vs_ctas_per_sm(int ne, int* out2) {
+  const int nb = ne <= 9 ? 9 : ne <= 18 ? 18 : ne <= 27 ? 27 : 32;
+  int a = 0, b = 0;
+#define VS_OCC(NE)                                                                   \
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_level0_vs<NE>, ROWS_PER_CTA, 0); \
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_level_vs<NE>, ROWS_PER_CTA, 0);
+  if (nb == 9) { VS_OCC(9) } else if (nb == 18) { VS_OCC(18) } else if (nb == 27) { VS_OCC(27) } else { VS_OCC(32) }
+#undef VS_OCC
+  out2[0] = a;
+  out2[1] = b;
+  return a < b ? a : b;
+}
+
 int ss_ctas_per_sm(int np, int ne, int pid_bytes, int* out2) {
   int a = 0, b = 0;
   const size_t bytes = ss_smem_bytes_dev(np);
@@ -1996,6 +2129,23 @@ void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s) {
       else
         k_level_win<uint16_t><<<c.win_grid, WT, bytes, s>>>(c, level);
     }
+    return;
+  }
+  if (c.vs_ne > 0) {
+    const ZmPtrs zp = zm_ptrs(c, level, sigma);
+    const int ne = c.vs_ne <= 9 ? 9 : c.vs_ne <= 18 ? 18 : c.vs_ne <= 27 ? 27 : 32;
+#define VS_LAUNCH(NE)                                                        \
+  if (level == 0)                                                            \
+    k_level0_vs<NE><<<c.red_n, ROWS_PER_CTA, 0, s>>>(c, zp);                 \
+  else                                                                       \
+    k_level_vs<NE><<<c.pat_grid, ROWS_PER_CTA, 0, s>>>(c, level, zp);
+    switch (ne) {
+      case 9: VS_LAUNCH(9) break;
+      case 18: VS_LAUNCH(18) break;
+      case 27: VS_LAUNCH(27) break;
+      default: VS_LAUNCH(32) break;
+    }
+#undef VS_LAUNCH
     return;
   }
   if (c.pid && c.ss_ne > 0 && c.zm_S > 0) {

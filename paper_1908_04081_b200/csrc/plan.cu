@@ -143,6 +143,9 @@ struct sscg_plan {
   int zm_zc = 0, zm_ncb = 0, zm_pf = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0;
   int64_t zp_items = 0;
   int64_t zm_items = 0;
+  int vs_ne = 0;  // value-stream stencil form (vs_setup); 0: not used
+  int vs_off[VS_MAX_NE] = {};
+  double* d_vs_val = nullptr;
   int ss_ne = 0;  // superset-mask form (superset_setup); 0: table-walking kernels
   int ss_off[SS_MAX_NE] = {};
   unsigned* d_ss_mask = nullptr;
@@ -270,6 +273,9 @@ Ctx make_ctx(sscg_plan* p) {
   c.zt_on = p->zt_on;
   c.zp_grid = p->zp_grid;
   c.zp_items = p->zp_items;
+  c.vs_ne = p->vs_ne;
+  for (int k = 0; k < VS_MAX_NE; ++k) c.vs_off[k] = p->vs_off[k];
+  c.vs_val = p->d_vs_val;
   c.ss_ne = p->ss_ne;
   for (int k = 0; k < SS_MAX_NE; ++k) c.ss_off[k] = p->ss_off[k];
   c.ss_mask = p->d_ss_mask;
@@ -840,6 +846,54 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
   return SSCG_OK;
 }
 
+// Value-stream stencil form (single-GPU plans whose rows do not compress to
+// patterns): every row's column offsets, in stored order, are a strictly
+// increasing subsequence of a union of 3..32 offsets -- a stencil's structure
+// with row-varying values (c4).  Values go slot-major [k][ld] (absent 0.0).
+int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+             const double* values) {
+  p->vs_ne = 0;
+  // SSCG_PATTERN=0 forces the CSR kernels (A/B reference), SSCG_VS=0 this form only
+  if (atoi(env_or("SSCG_VS", "1")) == 0 || atoi(env_or("SSCG_PATTERN", "1")) == 0 || n < 1)
+    return SSCG_OK;
+  std::vector<int64_t> uni;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t prev = INT64_MIN;
+    for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; ++j) {
+      const int64_t o = (int64_t)col_idx[j] - i;
+      if (o <= prev) return SSCG_OK;  // unsorted row
+      prev = o;
+      auto it = std::lower_bound(uni.begin(), uni.end(), o);
+      if (it == uni.end() || *it != o) {
+        if ((int)uni.size() >= VS_MAX_NE) return SSCG_OK;
+        uni.insert(it, o);
+      }
+    }
+  }
+  const int ne = (int)uni.size();
+  int occ[2] = {0, 0};
+  if (ne < 3 || vs_ctas_per_sm(ne, occ) < 1) return SSCG_OK;
+  std::vector<double> sv((size_t)ne * (size_t)p->ld, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    int k = 0;
+    for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; ++j) {
+      const int64_t o = (int64_t)col_idx[j] - i;
+      while (uni[(size_t)k] != o) ++k;  // rows are sorted subsequences of uni
+      sv[(size_t)k * (size_t)p->ld + (size_t)i] = values[j];
+    }
+  }
+  TRY(dalloc(p, &p->d_vs_val, sv.size()));
+  CUDA_OK(cudaMemcpy(p->d_vs_val, sv.data(), 8 * sv.size(), cudaMemcpyHostToDevice));
+  p->vs_ne = ne;
+  for (int k = 0; k < VS_MAX_NE; ++k) p->vs_off[k] = k < ne ? (int)uni[(size_t)k] : 0;
+  int sms = NUM_SMS;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  const int64_t tiles = (n + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
+  p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * occ[0], (int64_t)RED_BLOCKS, tiles}));
+  p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ[1], tiles));
+  return SSCG_OK;
+}
+
 // Wavefront MPK setup (single-GPU plans with staged tiles): per row tile the
 // range of input tiles its columns touch, made monotone (suffix min of lo,
 // prefix max of hi) so a CTA's dependency checks only move forward.
@@ -965,6 +1019,8 @@ int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
     TRY(plan_init(p, device, n, n, n, nnz, row_ptr, col_idx, values, lvl, SMAX));
     TRY(pattern_setup(p, n, row_ptr, col_idx, values));
     if (p->d_pid) return SSCG_OK;  // the pattern kernels replace the CSR staging
+    TRY(vs_setup(p, n, row_ptr, col_idx, values));
+    if (p->vs_ne) return SSCG_OK;  // so do the value-stream stencil kernels
     return wave_setup(p, row_ptr, col_idx);
   });
 }
@@ -1063,7 +1119,7 @@ int sscg_plan_destroy(sscg_plan* p) {
                   p->d_part_g, p->d_leja, p->d_it, p->d_ri, p->d_rd, p->d_conds, p->d_th,
                   p->d_ga, p->d_mu, p->d_otrue, p->d_fg, p->d_red, p->d_wdep, p->d_wcnt,
                   p->d_pid, p->d_pat_ptr, p->d_pat_off, p->d_pat_val, p->d_ss_mask, p->d_ss_val,
-                  p->d_zm_base};
+                  p->d_zm_base, p->d_vs_val};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_done) cudaFreeHost(p->h_done);
@@ -1328,9 +1384,9 @@ int sscg_get_small_phases(const sscg_plan* p, int64_t* cycles8) {
 int sscg_plan_mpk_schedule(sscg_plan* p, int32_t sigma, int32_t* out) {
   if (!p || !out || sigma < 1 || sigma > SMAX) return sscg_fail(SSCG_EINVAL, "bad arguments");
   for (int i = 0; i < 4 + 2 * SMAX; ++i) out[i] = 0;
-  out[0] = p->d_pid ? 2 : p->wave_on ? 1 : 0;
+  out[0] = p->d_pid ? 2 : p->vs_ne ? 3 : p->wave_on ? 1 : 0;
   out[1] = p->wave_on ? p->wave_grid : p->red_n;
-  out[2] = p->d_pid ? p->pat_np : p->wave_lhi;
+  out[2] = p->d_pid ? p->pat_np : p->vs_ne ? p->vs_ne : p->wave_lhi;
   // last slot: pattern kernel form (0 table walk, 1 superset mask, 2 plane march)
   if (p->d_pid)
     out[3 + 2 * SMAX] = p->zm_S > 0 ? (p->zt_on ? 4 : p->zm_pair ? 3 : 2) : p->ss_ne > 0 ? 1 : 0;

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 
 _KEYS = ("SSCG_PATTERN", "SSCG_PAT_SS", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_ZM_PAIR",
-         "SSCG_ZT")
+         "SSCG_ZT", "SSCG_VS")
 
 
 def _with_env(env, fn):
@@ -180,3 +180,28 @@ def test_windowed_pattern_kernels_bit_identical(gpu_ready, name, make, kw, kind)
             os.environ["SSCG_PAT_WIN"] = old
     np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
     np.testing.assert_array_equal(got[0], ref[0])
+
+
+@pytest.mark.parametrize("key,kw", [
+    ("c4", dict(sigma=10, eps_star=1e-8, basis_kind="newton", max_outer=60)),
+    ("c4j", dict(sigma=10, eps_star=1e-8, basis_kind="newton")),
+    ("c4j", dict(sigma=8, eps_star=1e-8, basis_kind="chebyshev")),
+], ids=["c4", "c4j", "c4j_cheb"])
+def test_value_stream_bit_identical_to_csr(gpu_ready, key, kw):
+    """Row-varying 27-point operators (c4) run the value-stream stencil kernels
+    (k_level_vs: union offsets as parameters, values slot-major): the same
+    rounded operations in stored order as csr_matvec, so the solve is
+    identical to the CSR kernels' (SSCG_VS=0)."""
+    cfg = AdaptiveConfig(**kw)
+
+    def run():
+        prob = problems.make_problem(key, scale=16)
+        return _plan(prob.a).mpk_schedule(cfg.sigma), adaptive_solve(prob, cfg, trace="fast")
+
+    s0, ref = _with_env({"SSCG_VS": "0"}, run)
+    s1, got = _with_env({}, run)
+    assert s0["kind"] == "csr" and s1["kind"] == "stencil values" and s1["slots"] == 27, (s0, s1)
+    np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
+    np.testing.assert_array_equal(got[0], ref[0])
+    assert got[1].total_outer == ref[1].total_outer
+
