@@ -1386,7 +1386,7 @@ __global__ void ZP_LB k_level_zp(Ctx c, int l, ZmPtrs zp) {
 // slot has value 0.0 and gathers from the clamped index (in range, finite:
 // see zm_column): adding 0.0 * x = +-0.0 is exact -- bit-identical to CSR.
 #ifndef VS_CHUNK
-#define VS_CHUNK 9
+#define VS_CHUNK 5  // slots per batch of gathers (c4j: 3.80 ms/outer; 9: 4.1, 14: 4.6, 27: 4.3)
 #endif
 template <int NV, int NE>
 __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
