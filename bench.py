@@ -272,6 +272,18 @@ def run_partitioned(args, rank, world):
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     L.check(lib.sscg_fetch(plan.handle, None, logs.s))
     total_iters, total_outer = int(logs.s.total_iters), int(logs.s.total_outer)
+    # roofline of the matrix-powers kernel on this rank's owned rows (SURVEY.md
+    # 8(d): owned-row traffic only), from one profiled solve outside the timed
+    # region (every rank runs it: the collectives are inside), max over ranks
+    L.check(lib.sscg_set_profiling(plan.handle, 1))
+    dev_solve()
+    L.check(lib.sscg_set_profiling(plan.handle, 0))
+    pms = np.zeros(5)
+    pcnt = np.zeros(5, dtype=np.int64)
+    L.check(lib.sscg_get_profile(plan.handle, L.dptr(pms), pcnt.ctypes.data_as(C.POINTER(C.c_int64))))
+    mpk_ms_t = torch.tensor([float(pms[0])], dtype=torch.float64)
+    dist.all_reduce(mpk_ms_t, op=dist.ReduceOp.MAX)
+    L.check(lib.sscg_fetch(plan.handle, None, logs.s))
     # global true residual from the owned pieces (independent host SpMV)
     x_glob = torch.zeros(n, dtype=torch.float64)
     x_glob[lo:hi] = torch.from_numpy(xo)
@@ -307,6 +319,18 @@ def run_partitioned(args, rank, world):
                     "note": "sscg_solve per rank (host b, x0 -> x, logs), max over ranks"},
             "gpu_launches": launches, "clocks": clk.summary(),
         }
+        mu_nz = basis == "chebyshev"
+        mpk_bytes = (total_outer + 1) * mpk_bytes_per_outer(n_own, 7 * n_own, sigma, mu_nz, sched)
+        mpk_ms = mpk_ms_t.item()
+        hbm_peak, peak_kind = peaks()
+        ach = mpk_bytes / (mpk_ms / 1e3) / 1e9
+        line["roofline"] = {
+            "bound": "hbm", "kernel": kernel_name(sched) + " (owned rows; ghost-row levels are "
+                                                          "redundant work, not counted)",
+            "mpk_schedule": sched, "achieved": ach, "peak": hbm_peak, "peak_kind": peak_kind,
+            "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+            "kernel_ms": {"mpk": pms[0], "gram": pms[1], "small": pms[2], "recovery": pms[3],
+                          "other (halo, allreduce, Leja)": pms[4]}}
         print(json.dumps(line))
     dist.barrier()
 
