@@ -16,6 +16,7 @@
 #include <cstring>
 #include <functional>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -143,6 +144,13 @@ struct sscg_plan {
   int zm_zc = 0, zm_ncb = 0, zm_pf = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0;
   int64_t zp_items = 0;
   int64_t zm_items = 0;
+  // host <-> device staging of the solve's vectors (copy_h2d / copy_d2h):
+  // per copy thread two pinned chunks, a stream and two events
+  int st_threads = 0;
+  size_t st_chunk = 0;
+  std::vector<void*> st_pinned;
+  std::vector<cudaStream_t> st_streams;
+  std::vector<cudaEvent_t> st_events;
   int vs_ne = 0;  // value-stream stencil form (vs_setup); 0: not used
   int vs_off[VS_MAX_NE] = {};
   double* d_vs_val = nullptr;
@@ -171,6 +179,9 @@ int dalloc(sscg_plan* p, T** ptr, size_t count) {
     int rc__ = (expr);           \
     if (rc__ != SSCG_OK) return rc__; \
   } while (0)
+
+int copy_h2d(sscg_plan* p, void* d, const void* h, size_t bytes);  // staged copies (below)
+int copy_d2h(sscg_plan* p, void* h, const void* d, size_t bytes);
 
 int ensure_work(sscg_plan* p, int sigma, int64_t max_outer, int leja_grid) {
   if (sigma > p->sigma_alloc) {
@@ -1127,6 +1138,9 @@ int sscg_plan_destroy(sscg_plan* p) {
     if (ev) cudaEventDestroy(ev);
   for (auto ev : p->ev_leja)
     if (ev) cudaEventDestroy(ev);
+  for (void* h : p->st_pinned) cudaFreeHost(h);
+  for (auto st : p->st_streams) cudaStreamDestroy(st);
+  for (auto ev : p->st_events) cudaEventDestroy(ev);
   if (p->stream) cudaStreamDestroy(p->stream);
   if (p->side) cudaStreamDestroy(p->side);
   delete p;
@@ -1142,9 +1156,9 @@ int sscg_plan_device_bytes(const sscg_plan* p, int64_t* bytes) {
 int sscg_load(sscg_plan* p, const double* b, const double* x0) {
   if (!p || !b) return sscg_fail(SSCG_EINVAL, "NULL argument");
   CUDA_OK(cudaSetDevice(p->device));
-  CUDA_OK(cudaMemcpyAsync(p->d_b, b, sizeof(double) * p->n_own, cudaMemcpyHostToDevice, p->stream));
+  TRY(copy_h2d(p, p->d_b, b, sizeof(double) * p->n_own));
   if (x0)
-    CUDA_OK(cudaMemcpyAsync(p->d_x0, x0, sizeof(double) * p->n_local, cudaMemcpyHostToDevice, p->stream));
+    TRY(copy_h2d(p, p->d_x0, x0, sizeof(double) * p->n_local));
   else
     CUDA_OK(cudaMemsetAsync(p->d_x0, 0, sizeof(double) * p->n_local, p->stream));
   p->have_rhs = 1;
@@ -1187,6 +1201,97 @@ int sscg_get_profile(const sscg_plan* p, double* ms5, int64_t* counts5) {
 }  // extern "C"
 
 namespace {
+// ---- host <-> device copies of the solve's vectors --------------------------
+// A pageable cudaMemcpy of a 134 MB vector runs at ~10 GB/s (the driver stages
+// it through its own pinned buffer, one chunk at a time).  Here T threads each
+// own a slice of the vector and pipeline it through two pinned chunks of their
+// own: the host memcpy of one chunk overlaps the DMA of the other, and the T
+// slices overlap each other.  Small vectors take the plain path.
+constexpr size_t STAGE_MIN = (size_t)16 << 20;
+
+int stage_init(sscg_plan* p) {
+  if (p->st_threads) return SSCG_OK;
+  int t = atoi(env_or("SSCG_COPY_THREADS", "0"));
+  if (t <= 0) {
+    const unsigned hc = std::thread::hardware_concurrency();
+    t = (int)std::min<unsigned>(8u, std::max(1u, hc / 2));
+  }
+  p->st_chunk = (size_t)4 << 20;
+  for (int i = 0; i < t; ++i) {
+    cudaStream_t st;
+    CUDA_OK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    p->st_streams.push_back(st);
+    for (int k = 0; k < 2; ++k) {
+      void* h = nullptr;
+      CUDA_OK(cudaHostAlloc(&h, p->st_chunk, cudaHostAllocDefault));
+      p->st_pinned.push_back(h);
+      cudaEvent_t ev;
+      CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      p->st_events.push_back(ev);
+    }
+  }
+  p->st_threads = t;
+  return SSCG_OK;
+}
+
+int staged_copy(sscg_plan* p, char* dst, const char* src, size_t bytes, bool h2d) {
+  if (bytes < STAGE_MIN || atoi(env_or("SSCG_STAGE_COPY", "1")) == 0) {
+    CUDA_OK(cudaStreamSynchronize(p->stream));
+    CUDA_OK(cudaMemcpy(dst, src, bytes, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost));
+    return SSCG_OK;
+  }
+  TRY(stage_init(p));
+  CUDA_OK(cudaStreamSynchronize(p->stream));  // device buffers free / results complete
+  const int T = p->st_threads;
+  const size_t C = p->st_chunk, per = (bytes / T + 4095) & ~(size_t)4095;
+  std::vector<cudaError_t> err((size_t)T, cudaSuccess);
+  auto work = [&](int t) {
+    cudaError_t e = cudaSetDevice(p->device);
+    const size_t a = std::min(bytes, (size_t)t * per), b = std::min(bytes, a + per);
+    cudaStream_t st = p->st_streams[(size_t)t];
+    char* pin[2] = {(char*)p->st_pinned[(size_t)2 * t], (char*)p->st_pinned[(size_t)2 * t + 1]};
+    cudaEvent_t ev[2] = {p->st_events[(size_t)2 * t], p->st_events[(size_t)2 * t + 1]};
+    int k = 0;
+    size_t prev_off = 0, prev_len = 0;
+    for (size_t off = a; off < b && e == cudaSuccess; off += C, ++k) {
+      const size_t len = std::min(C, b - off);
+      const int sl = k & 1;
+      if (h2d) {
+        if (k >= 2) e = cudaEventSynchronize(ev[sl]);  // chunk k-2's DMA left this slot
+        if (e != cudaSuccess) break;
+        std::memcpy(pin[sl], src + off, len);
+        e = cudaMemcpyAsync(dst + off, pin[sl], len, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[sl], st);
+      } else {
+        e = cudaMemcpyAsync(pin[sl], src + off, len, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[sl], st);
+        if (e == cudaSuccess && k >= 1) {  // drain chunk k-1 while chunk k is in flight
+          e = cudaEventSynchronize(ev[sl ^ 1]);
+          if (e == cudaSuccess) std::memcpy(dst + prev_off, pin[sl ^ 1], prev_len);
+        }
+        prev_off = off;
+        prev_len = len;
+      }
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess && !h2d && k >= 1) std::memcpy(dst + prev_off, pin[(k - 1) & 1], prev_len);
+    err[(size_t)t] = e;
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  for (auto e : err) CUDA_OK(e);
+  return SSCG_OK;
+}
+
+int copy_h2d(sscg_plan* p, void* d, const void* h, size_t bytes) {
+  return staged_copy(p, (char*)d, (const char*)h, bytes, true);
+}
+int copy_d2h(sscg_plan* p, void* h, const void* d, size_t bytes) {
+  return staged_copy(p, (char*)h, (const char*)d, bytes, false);
+}
+
 // validate, size the work buffers, upload the device config, scrub the logs
 int run_prepare(sscg_plan* p, const sscg_config* cfg) {
   if (!p) return sscg_fail(SSCG_EINVAL, "NULL plan");
@@ -1327,7 +1432,7 @@ int sscg_fetch(sscg_plan* p, double* x_out, sscg_logs* logs) {
   if (!p) return sscg_fail(SSCG_EINVAL, "NULL plan");
   CUDA_OK(cudaSetDevice(p->device));
   CUDA_OK(cudaStreamSynchronize(p->stream));
-  if (x_out) CUDA_OK(cudaMemcpy(x_out, p->d_x, sizeof(double) * p->n_own, cudaMemcpyDeviceToHost));
+  if (x_out) TRY(copy_d2h(p, x_out, p->d_x, sizeof(double) * p->n_own));
   if (!logs) return SSCG_OK;
   SolverState st;
   CUDA_OK(cudaMemcpy(&st, p->d_st, sizeof(st), cudaMemcpyDeviceToHost));
