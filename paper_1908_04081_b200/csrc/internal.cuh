@@ -166,6 +166,7 @@ struct Ctx {
   int zm_ncb;      // column blocks of 256 columns
   int64_t zm_items;  // work items = zm_ncb x ceil(steps / zm_zc)
   int zm_np;         // planes of the walk
+  int zm_split;      // level 0 without the true residual; k_resid_zm computes it (side branch)
   const int* zm_base;  // [zm_np] first local row of each plane (partitioned), or NULL (z * S)
   int zm_pf;         // L2 prefetch of the plane zm_pf steps ahead (0: off)
   int zm_o;          // 2-D column tiles with line stride zm_o (0: 256 consecutive columns)
@@ -230,7 +231,8 @@ int sscg_fail(int code, const char* fmt, ...);
 // ---- launchers (defined in the .cu files) ----
 // mpk.cu
 void launch_init_residual(const Ctx& c, const double* x0, cudaStream_t s);
-void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s);
+void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s, bool with_resid = true);
+void launch_resid(const Ctx& c, int sigma, cudaStream_t s);
 void launch_spmv(const int* rp, const int* col, const double* val, int64_t n, const double* x,
                  double* y, cudaStream_t s);
 void launch_block_levels(const int* rp, const int* col, const double* val, int64_t n, int64_t ld,

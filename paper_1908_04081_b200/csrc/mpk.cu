@@ -718,10 +718,14 @@ __device__ __forceinline__ double recur_t(double ay, double y, double y2, double
 
 // one column of one work item.  NV input vectors xs[0..NV) (level 0: x, P0, R0
 // with NV = 3; else P_l, R_l with NV = 2, or P_l alone with NV = 1).
-// L0: level 0 (no two-back term; outputs of vectors 1.. ; t = b - A x norms)
+// MODE: ZM_LEVEL level l >= 1 (NV = 1 or 2 inputs, each with an output);
+// ZM_L0 fused level 0 (x, P0, R0 in; P1, R1 out; ||b - A x||^2 and ||r||^2
+// partials); ZM_L0PR level 0 without the residual (P0, R0 in, P1, R1 out,
+// ||r||^2); ZM_RESID the true residual alone (x in, ||b - A x||^2, no output)
 // RK: recurrence kind, bit 0 = non-unit gamma (IEEE division), bit 1 = mu != 0
 // (two-back term) -- compile-time, so the Newton levels carry neither
-template <typename ID, int NE, int NV, bool L0, int RK>
+enum { ZM_LEVEL = 0, ZM_L0 = 1, ZM_L0PR = 2, ZM_RESID = 3 };
+template <typename ID, int NE, int NV, int MODE, int RK>
 __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const int* __restrict__ sbase,
                                           int col, int z0, int z1,
                                           const double* const* __restrict__ xs,
@@ -730,9 +734,11 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
                                           double mu, bool use_mu, int plim, int rlim, int& bad,
                                           double& tt, double& rr) {
   constexpr int KC = NE / 2;
-  constexpr bool UNIT = (RK & 1) == 0, MU = (RK & 2) != 0 && !L0;
-  constexpr int NO = L0 ? NV - 1 : NV;  // output vectors
-  constexpr int Q0 = L0 ? 1 : 0;        // first input vector with an output
+  constexpr bool UNIT = (RK & 1) == 0, MU = (RK & 2) != 0 && MODE == ZM_LEVEL;
+  constexpr int NO = MODE == ZM_RESID ? 0 : MODE == ZM_L0 ? NV - 1 : NV;  // output vectors
+  constexpr int Q0 = MODE == ZM_L0 ? 1 : 0;  // first input vector with an output
+  constexpr bool TT = MODE == ZM_L0 || MODE == ZM_RESID;  // ||b - A x||^2 (acc[0])
+  constexpr bool RR = MODE == ZM_L0 || MODE == ZM_L0PR;   // ||r||^2 (the last input)
   // 32-bit row indices (plan.cu enables the march only for ld + S < 2^31).
   // Plane z of the walk starts at local row sbase[z] (a row-partitioned plan:
   // owned planes, then ghost planes by depth) or z * S (sbase == nullptr).
@@ -807,11 +813,11 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
           }
         }
       }
-      if (L0 && r < n_own) {
+      if (TT && r < n_own) {
         const double t = __dsub_rn(c.b[r], acc[0]);
         tt = fma(t, t, tt);
-        rr = fma(cu[NV - 1], cu[NV - 1], rr);
       }
+      if (RR && r < n_own) rr = fma(cu[NV - 1], cu[NV - 1], rr);
 #pragma unroll
       for (int q = 0; q < NO; ++q) {
         if (q == NO - 1 && NO > 1 && !rrow) break;
@@ -833,7 +839,7 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
   }
 }
 
-template <typename ID, int NE, int NV, bool L0, int RK>
+template <typename ID, int NE, int NV, int MODE, int RK>
 __device__ __forceinline__ void zm_items(const Ctx& c, const SsSmem& T, const double* const* xs,
                                          const double* const* ym, double* const* yo, double th,
                                          double ga, double mu, bool use_mu, int64_t plim,
@@ -856,7 +862,7 @@ __device__ __forceinline__ void zm_items(const Ctx& c, const SsSmem& T, const do
     }
     if (col >= S) continue;
     const int z0 = zc * zcs;
-    zm_column<ID, NE, NV, L0, RK>(c, T, sbase, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu, use_mu,
+    zm_column<ID, NE, NV, MODE, RK>(c, T, sbase, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu, use_mu,
                                   (int)plim, (int)rlim, bad, tt, rr);
   }
 }
@@ -895,7 +901,7 @@ inline ZmPtrs zm_ptrs(const Ctx& c, int l, int sigma) {
 #ifndef ZM0_MINB  // 64 registers, no spills: 4 CTAs/SM (1.52 vs 1.58 ms/outer at 3)
 #define ZM0_MINB 4
 #endif
-template <typename ID, int NE>
+template <typename ID, int NE, bool SPLIT>
 __global__ void __launch_bounds__(ROWS_PER_CTA, ZM0_MINB) k_level0_zm(Ctx c, ZmPtrs zp) {
   __shared__ double sm[ROWS_PER_CTA / 32];
   const SolverState* st = c.st;
@@ -911,17 +917,45 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, ZM0_MINB) k_level0_zm(Ctx c, ZmP
   double tt = 0.0, rr = 0.0;
   int bad = 0;
   const int64_t plim = lvl_p_rows(c, sigma, 0), rlim = do_r ? lvl_r_rows(c, sigma, 0) : 0;
-  if (ga == 1.0)
-    zm_items<ID, NE, 3, true, 0>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
-  else
-    zm_items<ID, NE, 3, true, 1>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
-  tt = block_sum<ROWS_PER_CTA>(tt, sm);
+  if (SPLIT) {  // the true residual runs beside the levels (k_resid_zm)
+    const double* xs2[2] = {xs[1], xs[2]};
+    if (ga == 1.0)
+      zm_items<ID, NE, 2, ZM_L0PR, 0>(c, T, xs2, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+    else
+      zm_items<ID, NE, 2, ZM_L0PR, 1>(c, T, xs2, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+  } else if (ga == 1.0) {
+    zm_items<ID, NE, 3, ZM_L0, 0>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+  } else {
+    zm_items<ID, NE, 3, ZM_L0, 1>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+  }
   rr = block_sum<ROWS_PER_CTA>(rr, sm);
+  if (!SPLIT) tt = block_sum<ROWS_PER_CTA>(tt, sm);
   if (threadIdx.x == 0) {
-    c.part_t[blockIdx.x] = tt;
+    if (!SPLIT) c.part_t[blockIdx.x] = tt;  // split: k_resid_zm writes these slots
     c.part_r[blockIdx.x] = rr;
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
+}
+
+// the true residual t = b - A x of the outer loop (adaptive.py:138) on its own:
+// ||t||^2 partials over the owned rows into part_t (same grid as level 0).
+// It needs only x and b, so the outer-loop graph runs it on a side branch
+// beside the matrix-powers levels (joined before the Gram kernel packs the
+// norms); the row sums are the same rounded operations as everywhere.
+template <typename ID, int NE>
+__global__ void __launch_bounds__(ROWS_PER_CTA, ZM0_MINB) k_resid_zm(Ctx c, ZmPtrs zp) {
+  __shared__ double sm[ROWS_PER_CTA / 32];
+  const SolverState* st = c.st;
+  if (st->done) return;
+  zm_plane_copy(c);
+  const SsSmem T = load_ss(c);
+  const double* xs[1] = {zp.xs[0]};
+  double tt = 0.0, rr = 0.0;
+  int bad = 0;
+  zm_items<ID, NE, 1, ZM_RESID, 0>(c, T, xs, nullptr, nullptr, 0.0, 1.0, 0.0, false, c.n_own, 0,
+                                   bad, tt, rr);
+  tt = block_sum<ROWS_PER_CTA>(tt, sm);
+  if (threadIdx.x == 0) c.part_t[blockIdx.x] = tt;
 }
 
 #ifndef ZM_MINB
@@ -948,10 +982,10 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, ZM_MINB) k_level_zm(Ctx c, int l
   const int rk = (ga == 1.0 ? 0 : 1) | (use_mu ? 2 : 0);
 #define ZM_RK(NV, RL)                                                                          \
   switch (rk) {                                                                                \
-    case 0: zm_items<ID, NE, NV, false, 0>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
-    case 1: zm_items<ID, NE, NV, false, 1>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
-    case 2: zm_items<ID, NE, NV, false, 2>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
-    default: zm_items<ID, NE, NV, false, 3>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    case 0: zm_items<ID, NE, NV, ZM_LEVEL, 0>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    case 1: zm_items<ID, NE, NV, ZM_LEVEL, 1>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    case 2: zm_items<ID, NE, NV, ZM_LEVEL, 2>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    default: zm_items<ID, NE, NV, ZM_LEVEL, 3>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
   }
   if (do_r) {
     ZM_RK(2, rlim)
@@ -1970,6 +2004,25 @@ int staged_ctas_per_sm(int cap) {
   return a < b ? a : b;
 }
 
+// the side-branch residual of a split level 0 (capture_outer)
+void launch_resid(const Ctx& c, int sigma, cudaStream_t s) {
+  const size_t bytes = ss_smem_bytes_dev(c.pat_np) + (c.zm_base ? 4 * (size_t)c.zm_np : 0);
+  const ZmPtrs zp = zm_ptrs(c, 0, sigma);
+  if (c.pid_bytes == 1) {
+    switch (c.ss_ne) {
+      case 3: k_resid_zm<uint8_t, 3><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp); break;
+      case 5: k_resid_zm<uint8_t, 5><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp); break;
+      default: k_resid_zm<uint8_t, 7><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp); break;
+    }
+  } else {
+    switch (c.ss_ne) {
+      case 3: k_resid_zm<uint16_t, 3><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp); break;
+      case 5: k_resid_zm<uint16_t, 5><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp); break;
+      default: k_resid_zm<uint16_t, 7><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp); break;
+    }
+  }
+}
+
 void launch_init_residual(const Ctx& c, const double* x0, cudaStream_t s) {
   k_init_residual<<<c.red_n, ROWS_PER_CTA, 0, s>>>(c, x0);
 }
@@ -2001,9 +2054,11 @@ void ss_occ(size_t bytes, int* a, int* b) {
 template <typename ID, int NE>
 void zm_occ(size_t bytes, int* a, int* b) {
   const int lim = 48 * 1024;
-  cudaFuncSetAttribute(k_level0_zm<ID, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_level0_zm<ID, NE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_level0_zm<ID, NE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_resid_zm<ID, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   cudaFuncSetAttribute(k_level_zm<ID, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(a, k_level0_zm<ID, NE>, ROWS_PER_CTA, bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(a, k_level0_zm<ID, NE, false>, ROWS_PER_CTA, bytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, k_level_zm<ID, NE>, ROWS_PER_CTA, bytes);
 }
 
@@ -2114,7 +2169,7 @@ int window_ctas_per_sm(int np, int ne, int r, int pid_bytes, int* out2) {
   return out2[0] < out2[1] ? out2[0] : out2[1];
 }
 
-void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s) {
+void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s, bool with_resid) {
   if (c.pid && c.win_r >= 0) {
     const int nvw = level == 0 ? 3 : 2;
     const size_t bytes = window_smem_bytes(c.pat_np, c.pat_ne, c.win_r, nvw, c.pid_bytes);
@@ -2152,8 +2207,11 @@ void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s) {
     const size_t bytes = ss_smem_bytes_dev(c.pat_np) + (c.zm_base ? 4 * (size_t)c.zm_np : 0);
     const ZmPtrs zp = zm_ptrs(c, level, sigma);
 #define ZM_LAUNCH(ID, NE)                                                      \
-  if (level == 0)                                                              \
-    k_level0_zm<ID, NE><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp);           \
+  if (level == 0 && c.zm_split) {                                             \
+    if (with_resid) k_resid_zm<ID, NE><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp); \
+    k_level0_zm<ID, NE, true><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp);     \
+  } else if (level == 0)                                                       \
+    k_level0_zm<ID, NE, false><<<c.red_n, ROWS_PER_CTA, bytes, s>>>(c, zp);    \
   else if (c.zt_on && NE == 7)                                                 \
     k_level_zt<ID><<<c.pat_grid, ROWS_PER_CTA, bytes, s>>>(c, level, zp);      \
   else if (c.zm_pair && NE >= 5)                                               \

@@ -84,6 +84,8 @@ struct sscg_plan {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // Leja branch of the outer-loop graph
   cudaEvent_t ev_fork = nullptr;
+  cudaStream_t side2 = nullptr;  // true-residual branch (split level 0)
+  cudaEvent_t ev_rfork = nullptr, ev_rjoin = nullptr;
   cudaEvent_t ev_leja[SMAX] = {};
   cudaGraphExec_t gexec = nullptr;
   int g_sigma = -1, g_full = -1;
@@ -142,6 +144,7 @@ struct sscg_plan {
   int zm_np = 0;
   int* d_zm_base = nullptr;  // plane table of a partitioned march
   int zm_zc = 0, zm_ncb = 0, zm_pf = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0;
+  int zm_split = 0;
   int64_t zp_items = 0;
   int64_t zm_items = 0;
   // host <-> device staging of the solve's vectors (copy_h2d / copy_d2h):
@@ -281,6 +284,7 @@ Ctx make_ctx(sscg_plan* p) {
   c.zm_base = p->d_zm_base;
   c.zm_o = p->zm_o;
   c.zm_pair = p->zm_pair;
+  c.zm_split = p->zm_split;
   c.zt_on = p->zt_on;
   c.zp_grid = p->zp_grid;
   c.zp_items = p->zp_items;
@@ -314,7 +318,7 @@ int check_config(const sscg_config* c) {
   return SSCG_OK;
 }
 
-int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s);
+int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s, bool with_resid = true);
 void wave_plan_passes(sscg_plan* p, int sigma);
 
 // Next-block parameters (k_params_begin + Leja points 2..sigma-1) need only the
@@ -336,6 +340,15 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     TRY(halo_exchange(p->halo, c, p->comm, s));
     halo_unpack(p->halo, c, s);
   }
+  // split level 0: the true residual (x, b only) on its own branch beside the
+  // levels, joined before the Gram kernel packs the norms
+  const bool side_resid = c.zm_split != 0;
+  if (side_resid) {
+    cudaEventRecord(p->ev_rfork, s);
+    cudaStreamWaitEvent(p->side2, p->ev_rfork, 0);
+    launch_resid(c, sigma, p->side2);
+    cudaEventRecord(p->ev_rjoin, p->side2);
+  }
   if (p->leja_head && !p->wave_on) {
     // small operators: the recovery is too short to hide the Leja chain, so the
     // chain starts the outer loop on a side branch and level l (l >= 2) joins
@@ -349,11 +362,12 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     }
     for (int l = 0; l < sigma; ++l) {
       if (l >= 2) cudaStreamWaitEvent(s, p->ev_leja[l], 0);
-      launch_level(c, l, sigma, s);
+      launch_level(c, l, sigma, s, !side_resid);
     }
   } else {
-    TRY(launch_mpk(p, c, sigma, s));
+    TRY(launch_mpk(p, c, sigma, s, !side_resid));
   }
+  if (side_resid) cudaStreamWaitEvent(s, p->ev_rjoin, 0);
   launch_gram(c, 2 * sigma + 1, s);
   if (p->comm) {  // the one synchronisation of the outer loop
     const int k = 2 * sigma + 1;
@@ -524,6 +538,9 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   CUDA_OK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   CUDA_OK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
   CUDA_OK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  CUDA_OK(cudaStreamCreateWithFlags(&p->side2, cudaStreamNonBlocking));
+  CUDA_OK(cudaEventCreateWithFlags(&p->ev_rfork, cudaEventDisableTiming));
+  CUDA_OK(cudaEventCreateWithFlags(&p->ev_rjoin, cudaEventDisableTiming));
   for (int i = 0; i < SMAX; ++i) CUDA_OK(cudaEventCreateWithFlags(&p->ev_leja[i], cudaEventDisableTiming));
   CUDA_OK(cudaHostAlloc((void**)&p->h_done, 2 * sizeof(int), cudaHostAllocDefault));
   for (auto* ev : {&p->ev_chunk[0], &p->ev_chunk[1]})
@@ -801,6 +818,10 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       p->zm_ncb = (int)ncb;
       p->zm_items = ncb * ((steps + zc - 1) / zc);
       p->zm_pf = std::max(0, atoi(env_or("SSCG_ZM_PF", "0")));
+      // level 0 split: P/R at the levels' cost, the true residual beside them
+      // (opt-in: measured 218.4 vs 215.9 ms per c5w solve -- the side branch
+      // takes SM slots from the latency-bound levels rather than idle HBM)
+      p->zm_split = atoi(env_or("SSCG_ZM_SPLIT", "0")) != 0;
       // shared-memory tile march for the 2-D tiled 7-slot form: whole 32 x 8
       // tiles (o a multiple of 32, lines per plane a multiple of 8)
       // (opt-in: the per-plane barrier makes it slower than the register march)
@@ -993,9 +1014,9 @@ void wave_plan_passes(sscg_plan* p, int sigma) {
   }
 }
 
-int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s) {
+int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s, bool with_resid) {
   if (!p->wave_on) {
-    for (int l = 0; l < sigma; ++l) launch_level(c, l, sigma, s);
+    for (int l = 0; l < sigma; ++l) launch_level(c, l, sigma, s, with_resid);
     return SSCG_OK;
   }
   CUDA_OK(cudaMemsetAsync(p->d_wcnt, 0, sizeof(int) * ((size_t)SMAX * p->wave_ngroups + SMAX), s));
@@ -1134,7 +1155,8 @@ int sscg_plan_destroy(sscg_plan* p) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_done) cudaFreeHost(p->h_done);
-  for (auto ev : {p->ev_chunk[0], p->ev_chunk[1], p->ev_start, p->ev_stop, p->ev_fork})
+  for (auto ev : {p->ev_chunk[0], p->ev_chunk[1], p->ev_start, p->ev_stop, p->ev_fork,
+                  p->ev_rfork, p->ev_rjoin})
     if (ev) cudaEventDestroy(ev);
   for (auto ev : p->ev_leja)
     if (ev) cudaEventDestroy(ev);
@@ -1143,6 +1165,7 @@ int sscg_plan_destroy(sscg_plan* p) {
   for (auto ev : p->st_events) cudaEventDestroy(ev);
   if (p->stream) cudaStreamDestroy(p->stream);
   if (p->side) cudaStreamDestroy(p->side);
+  if (p->side2) cudaStreamDestroy(p->side2);
   delete p;
   return SSCG_OK;
 }
