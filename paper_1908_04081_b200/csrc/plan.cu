@@ -577,7 +577,11 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   }
   if (p->red_n < 1) p->red_n = 1;
   // where the next block's Leja chain runs (see capture_outer)
-  p->leja_head = atoi(env_or("SSCG_LEJA_HEAD", n_rows < ((int64_t)1 << 20) ? "1" : "0")) != 0;
+  // the Leja chain at the head of the outer loop, level l joining point l:
+  // the full-wave recovery (rec.cu) leaves no SM slot for a chain beside it
+  // (c5w: 207.7 ms per solve here vs 224.8 beside the recovery, 215.9 with the
+  // former 1.33-wave recovery grid); SSCG_LEJA_HEAD=0 restores the side branch
+  p->leja_head = atoi(env_or("SSCG_LEJA_HEAD", "1")) != 0;
   return rc;
 }
 

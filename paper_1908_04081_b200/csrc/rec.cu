@@ -142,9 +142,23 @@ __global__ void __launch_bounds__(REC_THREADS)
   }
 }
 
+// one full wave of resident CTAs (grid-stride loops): a partial second wave
+// would leave most SMs idle at the tail of this HBM-bound pass
 int rec_grid(int64_t ld) {
+  static int per_sm = 0, sms = 0;
+  if (!per_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_recover, REC_THREADS, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
   int64_t g = (ld / 2 + REC_THREADS - 1) / REC_THREADS;
-  const int64_t cap = NUM_SMS * 8;
+#ifdef REC_PER_SM
+  const int64_t cap = (int64_t)sms * REC_PER_SM;
+#else
+  const int64_t cap = (int64_t)sms * per_sm;
+#endif
   if (g > cap) g = cap;
   return (int)(g < 1 ? 1 : g);
 }
