@@ -705,6 +705,9 @@ __device__ __forceinline__ const int* zm_plane_table(const Ctx& c) {
   return c.zm_base ? zm_plane_smem(c) : nullptr;
 }
 
+#ifndef ZM_L2PF  // per-thread L2 prefetch of the plane ZM_L2PF steps ahead (c5w: 1 -> +1.5 %, 2 -> -1.3 %, 3 -> -0.6 %, 4-8: 0)
+#define ZM_L2PF 2
+#endif
 #ifndef ZM_PIPE  // plane-ahead loads one step early (measured slower: registers)
 #define ZM_PIPE 0
 #endif
@@ -772,6 +775,15 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
     double nx[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) nx[q] = r1 < n ? __ldg(xs[q] + r1) : 0.0;
+#if ZM_L2PF > 0
+    if (z + ZM_L2PF < np) {
+      const int rf = row_of(z + ZM_L2PF);
+      if (rf < n) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(xs[q] + rf));
+      }
+    }
+#endif
     if (r < plim) {
       const bool rrow = r < rlim;  // the last vector (R) is produced on this row
       const unsigned m = T.mask[pid];
