@@ -781,6 +781,7 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
       if (rf < n) {
 #pragma unroll
         for (int q = 0; q < NV; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(xs[q] + rf));
+        if (TT && rf < n_own) asm volatile("prefetch.global.L2 [%0];" ::"l"(c.b + rf));
       }
     }
 #endif
