@@ -749,7 +749,7 @@ enum { SI_FLAG, SI_SBAR, SI_STILDE, SI_JDONE, SI_DIV, SI_BRKJ };
 
 // ---------------------------------------------------------------------------
 // K_small
-__global__ void __launch_bounds__(NT) k_small(Ctx c) {
+__global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
   extern __shared__ __align__(16) double dsm[];
   SmallShared& S = *reinterpret_cast<SmallShared*>(dsm);
   double* jac = dsm + (sizeof(SmallShared) + 7) / 8;
