@@ -166,6 +166,7 @@ struct Ctx {
   int zm_ncb;      // column blocks of 256 columns
   int64_t zm_items;  // work items = zm_ncb x ceil(steps / zm_zc)
   int zm_np;         // planes of the walk
+  unsigned* zm_ctr;  // [2 (SMAX + 1)] per-level claim / done counters (levels >= 1), or NULL
   int zm_split;      // level 0 without the true residual; k_resid_zm computes it (side branch)
   const int* zm_base;  // [zm_np] first local row of each plane (partitioned), or NULL (z * S)
   int zm_pf;         // L2 prefetch of the plane zm_pf steps ahead (0: off)

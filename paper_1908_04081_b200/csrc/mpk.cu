@@ -853,13 +853,27 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
 }
 
 template <typename ID, int NE, int NV, int MODE, int RK>
-__device__ __forceinline__ void zm_items(const Ctx& c, const SsSmem& T, const double* const* xs,
+__device__ __forceinline__ void zm_items(const Ctx& c, int lvl, const SsSmem& T,
+                                         const double* const* xs,
                                          const double* const* ym, double* const* yo, double th,
                                          double ga, double mu, bool use_mu, int64_t plim,
                                          int64_t rlim, int& bad, double& tt, double& rr) {
   const int items = (int)c.zm_items, ncb = c.zm_ncb, zcs = c.zm_zc, S = (int)c.zm_S;
   const int* sbase = zm_plane_table(c);
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+  // levels >= 1 with Ctx::zm_ctr: the CTA claims items from a per-level
+  // counter instead of a fixed stripe, so a CTA that started late (its SM
+  // slot held by a Leja-point kernel of the side branch) takes fewer items
+  // instead of delaying the whole level.  The row arithmetic is unchanged.
+  const bool dyn = MODE == ZM_LEVEL && c.zm_ctr != nullptr;
+  __shared__ int s_claim;
+  unsigned* ctr = dyn ? c.zm_ctr + 2 * lvl : nullptr;
+  int it = blockIdx.x;
+  if (dyn) {
+    if (threadIdx.x == 0) s_claim = (int)atomicAdd(ctr, 1u);
+    __syncthreads();
+    it = s_claim;
+  }
+  for (; it < items;) {
     const int cb = it % ncb, zc = it / ncb;
     int col;
     if (c.zm_o > 0) {
@@ -869,14 +883,29 @@ __device__ __forceinline__ void zm_items(const Ctx& c, const SsSmem& T, const do
       const int ntx = c.zm_o >> 5;
       const int ty = (cb / ntx) * (ROWS_PER_CTA / 32) + (threadIdx.x >> 5);
       col = ty * c.zm_o + (cb % ntx) * 32 + (threadIdx.x & 31);
-      if (ty >= S / c.zm_o) continue;
+      if (ty >= S / c.zm_o) goto next_item;
     } else {
       col = cb * ROWS_PER_CTA + threadIdx.x;
     }
-    if (col >= S) continue;
-    const int z0 = zc * zcs;
-    zm_column<ID, NE, NV, MODE, RK>(c, T, sbase, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu, use_mu,
-                                  (int)plim, (int)rlim, bad, tt, rr);
+    if (col >= S) goto next_item;
+    {
+      const int z0 = zc * zcs;
+      zm_column<ID, NE, NV, MODE, RK>(c, T, sbase, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu,
+                                      use_mu, (int)plim, (int)rlim, bad, tt, rr);
+    }
+  next_item:
+    if (dyn) {
+      __syncthreads();  // every thread has read s_claim
+      if (threadIdx.x == 0) s_claim = (int)atomicAdd(ctr, 1u);
+      __syncthreads();
+      it = s_claim;
+    } else {
+      it += gridDim.x;
+    }
+  }
+  if (dyn && threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+    atomicExch(ctr, 0u);  // the last CTA out resets the counters for the next launch
+    atomicExch(ctr + 1, 0u);
   }
 }
 
@@ -933,13 +962,13 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, ZM0_MINB) k_level0_zm(Ctx c, ZmP
   if (SPLIT) {  // the true residual runs beside the levels (k_resid_zm)
     const double* xs2[2] = {xs[1], xs[2]};
     if (ga == 1.0)
-      zm_items<ID, NE, 2, ZM_L0PR, 0>(c, T, xs2, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+      zm_items<ID, NE, 2, ZM_L0PR, 0>(c, 0, T, xs2, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
     else
-      zm_items<ID, NE, 2, ZM_L0PR, 1>(c, T, xs2, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+      zm_items<ID, NE, 2, ZM_L0PR, 1>(c, 0, T, xs2, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
   } else if (ga == 1.0) {
-    zm_items<ID, NE, 3, ZM_L0, 0>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+    zm_items<ID, NE, 3, ZM_L0, 0>(c, 0, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
   } else {
-    zm_items<ID, NE, 3, ZM_L0, 1>(c, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
+    zm_items<ID, NE, 3, ZM_L0, 1>(c, 0, T, xs, nullptr, yo, th, ga, 0.0, false, plim, rlim, bad, tt, rr);
   }
   rr = block_sum<ROWS_PER_CTA>(rr, sm);
   if (!SPLIT) tt = block_sum<ROWS_PER_CTA>(tt, sm);
@@ -965,7 +994,7 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, ZM0_MINB) k_resid_zm(Ctx c, ZmPt
   const double* xs[1] = {zp.xs[0]};
   double tt = 0.0, rr = 0.0;
   int bad = 0;
-  zm_items<ID, NE, 1, ZM_RESID, 0>(c, T, xs, nullptr, nullptr, 0.0, 1.0, 0.0, false, c.n_own, 0,
+  zm_items<ID, NE, 1, ZM_RESID, 0>(c, 0, T, xs, nullptr, nullptr, 0.0, 1.0, 0.0, false, c.n_own, 0,
                                    bad, tt, rr);
   tt = block_sum<ROWS_PER_CTA>(tt, sm);
   if (threadIdx.x == 0) c.part_t[blockIdx.x] = tt;
@@ -995,10 +1024,10 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, ZM_MINB) k_level_zm(Ctx c, int l
   const int rk = (ga == 1.0 ? 0 : 1) | (use_mu ? 2 : 0);
 #define ZM_RK(NV, RL)                                                                          \
   switch (rk) {                                                                                \
-    case 0: zm_items<ID, NE, NV, ZM_LEVEL, 0>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
-    case 1: zm_items<ID, NE, NV, ZM_LEVEL, 1>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
-    case 2: zm_items<ID, NE, NV, ZM_LEVEL, 2>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
-    default: zm_items<ID, NE, NV, ZM_LEVEL, 3>(c, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    case 0: zm_items<ID, NE, NV, ZM_LEVEL, 0>(c, l, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    case 1: zm_items<ID, NE, NV, ZM_LEVEL, 1>(c, l, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    case 2: zm_items<ID, NE, NV, ZM_LEVEL, 2>(c, l, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
+    default: zm_items<ID, NE, NV, ZM_LEVEL, 3>(c, l, T, xs, ym, yo, th, ga, mu, use_mu, plim, RL, bad, tt, rr); break; \
   }
   if (do_r) {
     ZM_RK(2, rlim)

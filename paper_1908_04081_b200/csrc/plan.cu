@@ -143,6 +143,7 @@ struct sscg_plan {
   int64_t zm_S = 0;  // plane-march form (0: off)
   int zm_np = 0;
   int* d_zm_base = nullptr;  // plane table of a partitioned march
+  unsigned* d_zm_ctr = nullptr;  // dynamic item counters of the level kernels
   int zm_zc = 0, zm_ncb = 0, zm_pf = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0;
   int zm_split = 0;
   int64_t zp_items = 0;
@@ -282,6 +283,7 @@ Ctx make_ctx(sscg_plan* p) {
   c.zm_pf = p->zm_pf;
   c.zm_np = p->zm_np;
   c.zm_base = p->d_zm_base;
+  c.zm_ctr = p->d_zm_ctr;
   c.zm_o = p->zm_o;
   c.zm_pair = p->zm_pair;
   c.zm_split = p->zm_split;
@@ -809,9 +811,12 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       const int64_t steps = bases.empty() ? (n_rows + S - 1) / S : (int64_t)bases.size();
       const int64_t grid = (int64_t)sms * zocc[1];
       int64_t zc = atoi(env_or("SSCG_ZM_ZC", "0"));
-      // ~16 planes per item (measured best on 256^3: 8-32 within 1%), fewer
+      // up to 24 planes per item with dynamic claiming (c5w: 20-28 best,
+      // 198.4-199.7 ms per solve; 16: 201.8), 16 with fixed stripes; fewer
       // when the operator is too small to give every CTA a few items
-      if (zc <= 0) zc = std::max<int64_t>(2, std::min<int64_t>(16, ncb * steps / (4 * grid)));
+      const bool dyn = atoi(env_or("SSCG_ZM_DYN", "1")) != 0;
+      if (zc <= 0)
+        zc = std::max<int64_t>(2, std::min<int64_t>(dyn ? 24 : 16, ncb * steps / (4 * grid)));
       p->zm_S = S;
       p->zm_np = (int)steps;
       if (!bases.empty()) {
@@ -819,6 +824,10 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
         CUDA_OK(cudaMemcpy(p->d_zm_base, bases.data(), 4 * bases.size(), cudaMemcpyHostToDevice));
       }
       p->zm_zc = (int)zc;
+      if (dyn) {
+        TRY(dalloc(p, &p->d_zm_ctr, 2 * (SMAX + 1)));
+        CUDA_OK(cudaMemset(p->d_zm_ctr, 0, sizeof(unsigned) * 2 * (SMAX + 1)));
+      }
       p->zm_ncb = (int)ncb;
       p->zm_items = ncb * ((steps + zc - 1) / zc);
       p->zm_pf = std::max(0, atoi(env_or("SSCG_ZM_PF", "0")));
@@ -1155,7 +1164,7 @@ int sscg_plan_destroy(sscg_plan* p) {
                   p->d_part_g, p->d_leja, p->d_it, p->d_ri, p->d_rd, p->d_conds, p->d_th,
                   p->d_ga, p->d_mu, p->d_otrue, p->d_fg, p->d_red, p->d_wdep, p->d_wcnt,
                   p->d_pid, p->d_pat_ptr, p->d_pat_off, p->d_pat_val, p->d_ss_mask, p->d_ss_val,
-                  p->d_zm_base, p->d_vs_val};
+                  p->d_zm_base, p->d_vs_val, p->d_zm_ctr};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_done) cudaFreeHost(p->h_done);

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 
 _KEYS = ("SSCG_PATTERN", "SSCG_PAT_SS", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_ZM_PAIR",
-         "SSCG_ZT", "SSCG_VS", "SSCG_ZM_SPLIT")
+         "SSCG_ZT", "SSCG_VS", "SSCG_ZM_SPLIT", "SSCG_ZM_DYN")
 
 
 def _with_env(env, fn):
@@ -121,9 +121,9 @@ def test_pattern_kernel_forms(gpu_ready):
 
 @pytest.mark.parametrize("env", [{"SSCG_ZM": "0"}, {"SSCG_PAT_SS": "0"}, {"SSCG_ZM_ZC": "3"},
                                  {"SSCG_ZM_2D": "0"}, {"SSCG_ZM_PAIR": "1"}, {"SSCG_ZT": "1"},
-                                 {"SSCG_ZM_SPLIT": "1"}],
+                                 {"SSCG_ZM_SPLIT": "1"}, {"SSCG_ZM_DYN": "0"}],
                          ids=["superset", "table", "march_zc3", "march_1d", "pair", "tile",
-                              "split_resid"])
+                              "split_resid", "static_items"])
 def test_pattern_forms_bit_identical(gpu_ready, env):
     """Plane march (default), its opt-in variants, superset mask and table
     walk run the same rounded operations in the same order: identical solves
