@@ -864,7 +864,9 @@ __device__ __forceinline__ void zm_items(const Ctx& c, int lvl, const SsSmem& T,
   // counter instead of a fixed stripe, so a CTA that started late (its SM
   // slot held by a Leja-point kernel of the side branch) takes fewer items
   // instead of delaying the whole level.  The row arithmetic is unchanged.
-  const bool dyn = MODE == ZM_LEVEL && c.zm_ctr != nullptr;
+  // (only while the Leja chain of this block runs: st->leja_on; a Chebyshev
+  // or monomial basis has no side branch and keeps the fixed stripes)
+  const bool dyn = MODE == ZM_LEVEL && c.zm_ctr != nullptr && c.st->leja_on;
   __shared__ int s_claim;
   unsigned* ctr = dyn ? c.zm_ctr + 2 * lvl : nullptr;
   int it = blockIdx.x;

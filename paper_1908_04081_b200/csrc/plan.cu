@@ -811,12 +811,11 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       const int64_t steps = bases.empty() ? (n_rows + S - 1) / S : (int64_t)bases.size();
       const int64_t grid = (int64_t)sms * zocc[1];
       int64_t zc = atoi(env_or("SSCG_ZM_ZC", "0"));
-      // up to 24 planes per item with dynamic claiming (c5w: 20-28 best,
-      // 198.4-199.7 ms per solve; 16: 201.8), 16 with fixed stripes; fewer
-      // when the operator is too small to give every CTA a few items
+      // planes per item: about 1.7 items per resident CTA, at most 24 (c5w:
+      // 24 -- 197.9 ms per solve with per-CTA claiming, 202.7 fixed stripes,
+      // 204.5 at 16; c3 128^3: 8 -- 27.6 ms, 28.6 at 6, 31.2 at 12)
       const bool dyn = atoi(env_or("SSCG_ZM_DYN", "1")) != 0;
-      if (zc <= 0)
-        zc = std::max<int64_t>(2, std::min<int64_t>(dyn ? 24 : 16, ncb * steps / (4 * grid)));
+      if (zc <= 0) zc = std::max<int64_t>(2, std::min<int64_t>(24, ncb * steps * 10 / (grid * 17)));
       p->zm_S = S;
       p->zm_np = (int)steps;
       if (!bases.empty()) {
