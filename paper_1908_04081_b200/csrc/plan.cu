@@ -84,6 +84,7 @@ struct sscg_plan {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // Leja branch of the outer-loop graph
   cudaEvent_t ev_fork = nullptr;
+  int leja_after0 = 1;  // the head chain forks after level 0
   cudaStream_t side2 = nullptr;  // true-residual branch (split level 0)
   cudaEvent_t ev_rfork = nullptr, ev_rjoin = nullptr;
   cudaEvent_t ev_leja[SMAX] = {};
@@ -356,13 +357,19 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     // chain starts the outer loop on a side branch and level l (l >= 2) joins
     // point l only -- the levels run as the shifts arrive
     launch_params_begin(c, s);
+    // the chain forks after level 0 (SSCG_LEJA_AFTER0, default) or before it:
+    // level 0 keeps fixed stripes (deterministic norm sums), so a Leja kernel
+    // holding one of its SM slots would delay it; level 1 (lambda_min) needs
+    // no Leja point, and point 2 (42 us) is ready long before level 2
+    const bool after0 = p->leja_after0 && sigma > 1;
+    if (after0) launch_level(c, 0, sigma, s, !side_resid);
     cudaEventRecord(p->ev_fork, s);
     cudaStreamWaitEvent(p->side, p->ev_fork, 0);
     for (int n = 2; n < sigma; ++n) {
       launch_leja_point(c, n, p->side);
       cudaEventRecord(p->ev_leja[n], p->side);
     }
-    for (int l = 0; l < sigma; ++l) {
+    for (int l = after0 ? 1 : 0; l < sigma; ++l) {
       if (l >= 2) cudaStreamWaitEvent(s, p->ev_leja[l], 0);
       launch_level(c, l, sigma, s, !side_resid);
     }
@@ -584,6 +591,9 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   // (c5w: 207.7 ms per solve here vs 224.8 beside the recovery, 215.9 with the
   // former 1.33-wave recovery grid); SSCG_LEJA_HEAD=0 restores the side branch
   p->leja_head = atoi(env_or("SSCG_LEJA_HEAD", "1")) != 0;
+  // (c5w: 197.1 vs 198.6 ms; c1, whose levels are shorter than a Leja point,
+  // is faster with the fork before level 0: 9.43 vs 9.58 ms)
+  p->leja_after0 = atoi(env_or("SSCG_LEJA_AFTER0", n_rows >= ((int64_t)1 << 20) ? "1" : "0")) != 0;
   return rc;
 }
 
