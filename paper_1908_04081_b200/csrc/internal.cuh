@@ -169,7 +169,6 @@ struct Ctx {
   unsigned* zm_ctr;  // [2 (SMAX + 1)] per-level claim / done counters (levels >= 1), or NULL
   int zm_split;      // level 0 without the true residual; k_resid_zm computes it (side branch)
   const int* zm_base;  // [zm_np] first local row of each plane (partitioned), or NULL (z * S)
-  int zm_pf;         // L2 prefetch of the plane zm_pf steps ahead (0: off)
   int zm_o;          // 2-D column tiles with line stride zm_o (0: 256 consecutive columns)
   int zt_on;         // levels >= 1 by the shared-memory tile march (k_level_zt; needs zm_o)
   int zm_pair;       // levels >= 1 by the row-pair march (k_level_zp; zm_items in pairs)

@@ -145,7 +145,7 @@ struct sscg_plan {
   int zm_np = 0;
   int* d_zm_base = nullptr;  // plane table of a partitioned march
   unsigned* d_zm_ctr = nullptr;  // dynamic item counters of the level kernels
-  int zm_zc = 0, zm_ncb = 0, zm_pf = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0;
+  int zm_zc = 0, zm_ncb = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0;
   int zm_split = 0;
   int64_t zp_items = 0;
   int64_t zm_items = 0;
@@ -281,7 +281,6 @@ Ctx make_ctx(sscg_plan* p) {
   c.zm_zc = p->zm_zc;
   c.zm_ncb = p->zm_ncb;
   c.zm_items = p->zm_items;
-  c.zm_pf = p->zm_pf;
   c.zm_np = p->zm_np;
   c.zm_base = p->d_zm_base;
   c.zm_ctr = p->d_zm_ctr;
@@ -839,7 +838,6 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       }
       p->zm_ncb = (int)ncb;
       p->zm_items = ncb * ((steps + zc - 1) / zc);
-      p->zm_pf = std::max(0, atoi(env_or("SSCG_ZM_PF", "0")));
       // level 0 split: P/R at the levels' cost, the true residual beside them
       // (opt-in: measured 218.4 vs 215.9 ms per c5w solve -- the side branch
       // takes SM slots from the latency-bound levels rather than idle HBM)
