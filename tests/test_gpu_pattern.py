@@ -207,3 +207,29 @@ def test_value_stream_bit_identical_to_csr(gpu_ready, key, kw):
     np.testing.assert_array_equal(got[0], ref[0])
     assert got[1].total_outer == ref[1].total_outer
 
+
+
+def test_staged_host_copies_round_trip(gpu_ready):
+    """Vectors of >= 16 MB move through the per-thread pinned chunk pipelines
+    (plan.cu staged_copy); the solve must be bit-identical to plain
+    cudaMemcpy transfers (SSCG_STAGE_COPY=0)."""
+    kw = dict(sigma=12, eps_star=1e-10, basis_kind="newton", max_outer=3)
+
+    def run(env):
+        old = os.environ.get("SSCG_STAGE_COPY")
+        os.environ["SSCG_STAGE_COPY"] = env
+        try:
+            prob = problems.make_problem("c5", scale=136)  # 2.5 M rows: 20 MB vectors
+            prob.x0[:] = np.linspace(-1e-3, 1e-3, prob.a.n)  # a non-trivial x0 upload
+            return adaptive_solve(prob, AdaptiveConfig(**kw), trace="fast")
+        finally:
+            if old is None:
+                os.environ.pop("SSCG_STAGE_COPY", None)
+            else:
+                os.environ["SSCG_STAGE_COPY"] = old
+
+    ref = run("0")
+    got = run("1")
+    assert ref[0].nbytes >= 16 << 20
+    np.testing.assert_array_equal(got[0], ref[0])
+    np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
