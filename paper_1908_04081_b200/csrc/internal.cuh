@@ -162,7 +162,9 @@ struct Ctx {
   // entries of a row are the previous step's values (registers) and only one
   // coalesced load per vector per row brings the plane ahead.  zm_S == 0: off.
   int64_t zm_S;
-  int zm_zc;       // steps per work item
+  int zm_zc;       // steps per work item (levels >= 1)
+  int zm_zc0;      // steps per work item of level 0 (fixed stripes)
+  int64_t zm_items0;
   int zm_ncb;      // column blocks of 256 columns
   int64_t zm_items;  // work items = zm_ncb x ceil(steps / zm_zc)
   int zm_np;         // planes of the walk

@@ -858,7 +858,11 @@ __device__ __forceinline__ void zm_items(const Ctx& c, int lvl, const SsSmem& T,
                                          const double* const* ym, double* const* yo, double th,
                                          double ga, double mu, bool use_mu, int64_t plim,
                                          int64_t rlim, int& bad, double& tt, double& rr) {
-  const int items = (int)c.zm_items, ncb = c.zm_ncb, zcs = c.zm_zc, S = (int)c.zm_S;
+  // level 0 and the residual use fixed stripes with their own item size
+  // (zm_zc0: whole rounds of items over the grid), levels >= 1 zm_zc
+  const bool l0 = MODE != ZM_LEVEL;
+  const int items = (int)(l0 ? c.zm_items0 : c.zm_items), ncb = c.zm_ncb;
+  const int zcs = l0 ? c.zm_zc0 : c.zm_zc, S = (int)c.zm_S;
   const int* sbase = zm_plane_table(c);
   // levels >= 1 with Ctx::zm_ctr: the CTA claims items from a per-level
   // counter instead of a fixed stripe, so a CTA that started late (its SM

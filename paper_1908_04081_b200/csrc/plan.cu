@@ -145,7 +145,8 @@ struct sscg_plan {
   int zm_np = 0;
   int* d_zm_base = nullptr;  // plane table of a partitioned march
   unsigned* d_zm_ctr = nullptr;  // dynamic item counters of the level kernels
-  int zm_zc = 0, zm_ncb = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0;
+  int zm_zc = 0, zm_ncb = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0, zm_zc0 = 0;
+  int64_t zm_items0 = 0;
   int zm_split = 0;
   int64_t zp_items = 0;
   int64_t zm_items = 0;
@@ -281,6 +282,8 @@ Ctx make_ctx(sscg_plan* p) {
   c.zm_zc = p->zm_zc;
   c.zm_ncb = p->zm_ncb;
   c.zm_items = p->zm_items;
+  c.zm_zc0 = p->zm_zc0;
+  c.zm_items0 = p->zm_items0;
   c.zm_np = p->zm_np;
   c.zm_base = p->d_zm_base;
   c.zm_ctr = p->d_zm_ctr;
@@ -838,6 +841,25 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       }
       p->zm_ncb = (int)ncb;
       p->zm_items = ncb * ((steps + zc - 1) / zc);
+      // level 0 keeps fixed stripes: pick the item size whose whole rounds over
+      // its grid cost the fewest planes (+1.5 per item for the two prologue
+      // loads) -- c5w: 16 (7 rounds) where 24 would leave a partial 5th round
+      {
+        const int64_t g0 = std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * zocc[0], (int64_t)RED_BLOCKS}));
+        double best = 1e300;
+        int64_t zb = zc;
+        for (int64_t z = 2; z <= 32; ++z) {
+          const int64_t it = ncb * ((steps + z - 1) / z);
+          const double cost = (double)((it + g0 - 1) / g0) * ((double)std::min(z, steps) + 1.5);
+          if (cost < best - 1e-9) {
+            best = cost;
+            zb = z;
+          }
+        }
+        const int64_t z0env = atoi(env_or("SSCG_ZM_ZC0", "0"));
+        p->zm_zc0 = (int)(z0env > 0 ? z0env : zb);
+        p->zm_items0 = ncb * ((steps + p->zm_zc0 - 1) / p->zm_zc0);
+      }
       // level 0 split: P/R at the levels' cost, the true residual beside them
       // (opt-in: measured 218.4 vs 215.9 ms per c5w solve -- the side branch
       // takes SM slots from the latency-bound levels rather than idle HBM)
@@ -869,7 +891,7 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
           p->zm_pair = 1;
         }
       }
-      p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * zocc[0], (int64_t)RED_BLOCKS, p->zm_items}));
+      p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * zocc[0], (int64_t)RED_BLOCKS, p->zm_items0}));
       p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, p->zm_items));
     }
   }
