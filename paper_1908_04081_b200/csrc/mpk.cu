@@ -728,7 +728,7 @@ __device__ __forceinline__ double recur_t(double ay, double y, double y2, double
 // RK: recurrence kind, bit 0 = non-unit gamma (IEEE division), bit 1 = mu != 0
 // (two-back term) -- compile-time, so the Newton levels carry neither
 enum { ZM_LEVEL = 0, ZM_L0 = 1, ZM_L0PR = 2, ZM_RESID = 3 };
-template <typename ID, int NE, int NV, int MODE, int RK>
+template <typename ID, int NE, int NV, int MODE, int RK, bool TAB>
 __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const int* __restrict__ sbase,
                                           int col, int z0, int z1,
                                           const double* const* __restrict__ xs,
@@ -749,7 +749,7 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
   const int S = (int)c.zm_S, n = (int)(c.ld < INT32_MAX ? c.ld : INT32_MAX), n_own = (int)c.n_own;
   const int np = c.zm_np;
   if (z1 > np) z1 = np;
-  auto row_of = [&](int z) { return (sbase ? sbase[z] : z * S) + col; };
+  auto row_of = [&](int z) { return (TAB ? sbase[z] : z * S) + col; };
   int r = row_of(z0);
   int off[NE];
 #pragma unroll
@@ -896,8 +896,12 @@ __device__ __forceinline__ void zm_items(const Ctx& c, int lvl, const SsSmem& T,
     if (col >= S) goto next_item;
     {
       const int z0 = zc * zcs;
-      zm_column<ID, NE, NV, MODE, RK>(c, T, sbase, col, z0, z0 + zcs, xs, ym, yo, th, ga, mu,
-                                      use_mu, (int)plim, (int)rlim, bad, tt, rr);
+      if (sbase)  // plane table (partitioned) or arithmetic planes, a compile-time choice
+        zm_column<ID, NE, NV, MODE, RK, true>(c, T, sbase, col, z0, z0 + zcs, xs, ym, yo, th, ga,
+                                              mu, use_mu, (int)plim, (int)rlim, bad, tt, rr);
+      else
+        zm_column<ID, NE, NV, MODE, RK, false>(c, T, sbase, col, z0, z0 + zcs, xs, ym, yo, th, ga,
+                                               mu, use_mu, (int)plim, (int)rlim, bad, tt, rr);
     }
   next_item:
     if (dyn) {
