@@ -751,9 +751,6 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
   if (z1 > np) z1 = np;
   auto row_of = [&](int z) { return (TAB ? sbase[z] : z * S) + col; };
   int r = row_of(z0);
-  int off[NE];
-#pragma unroll
-  for (int k = 0; k < NE; ++k) off[k] = c.ss_off[k];
   double pv[NV], cu[NV];
   {
     const int rp = z0 > 0 ? row_of(z0 - 1) : -1;
@@ -787,7 +784,6 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
 #endif
     if (r < plim) {
       const bool rrow = r < rlim;  // the last vector (R) is produced on this row
-      const unsigned m = T.mask[pid];
       // Absent slots carry the value 0.0 in the pattern table; they read the
       // row's own entry (offset 0: always in range) or the register slot as
       // is.  Every input a live level reads is finite (a non-finite column
@@ -796,10 +792,12 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
       // unchanged (a sum that starts at +0.0 is never -0.0 under
       // round-to-nearest): bit-identical to skipping the slot.
       double xb[NV][NE];
+      const int4 eo = T.eoff[pid];  // middle-slot offsets of this row (0: absent)
 #pragma unroll
       for (int k = 1; k < NE - 1; ++k) {
         if (k == KC) continue;
-        const int o = ((m >> k) & 1u) ? off[k] : 0;
+        const int o = NE == 7 ? (k == 1 ? eo.x : k == 2 ? eo.y : k == 4 ? eo.z : eo.w)
+                              : (k == 1 ? eo.x : eo.y);
 #pragma unroll
         for (int q = 0; q < NV; ++q) xb[q][k] = __ldg(xs[q] + (r + o));
       }

@@ -347,23 +347,47 @@ __device__ __forceinline__ void row_dot_p(const PatSmem& T, int b, int e, int i,
 // pattern's offsets are a subsequence of the sorted union), i.e. the same
 // rounded multiply-adds as csr_matvec.  Table in shared memory:
 // [val np x SS_MAX_NE][mask np].
+// [val np x SS_MAX_NE][mask np][pad to 16][eoff np x int4]
+__host__ __device__ __forceinline__ size_t ss_eoff_offset(int np) {
+  return ((size_t)np * SS_MAX_NE * 8 + (size_t)np * 4 + 15) / 16 * 16;
+}
 __host__ __device__ __forceinline__ size_t ss_smem_bytes_dev(int np) {
-  return (size_t)np * SS_MAX_NE * 8 + (size_t)np * 4;
+  return ss_eoff_offset(np) + (size_t)np * 16;
 }
 
 struct SsSmem {
   const double* val;
   const unsigned* mask;
+  const int4* eoff;  // per pattern: the offsets of the union's middle slots (plane
+                     // march: slots 1, 2, NE-3, NE-2 of 7; 1, 3 of 5), 0 where absent
 };
 
 __device__ __forceinline__ SsSmem load_ss(const Ctx& c) {
   extern __shared__ __align__(16) double psm[];
   double* sv = psm;
   unsigned* sm = reinterpret_cast<unsigned*>(sv + (size_t)c.pat_np * SS_MAX_NE);
+  int4* se = reinterpret_cast<int4*>(reinterpret_cast<char*>(psm) + ss_eoff_offset(c.pat_np));
   for (int j = threadIdx.x; j < c.pat_np * SS_MAX_NE; j += blockDim.x) sv[j] = __ldg(c.ss_val + j);
-  for (int j = threadIdx.x; j < c.pat_np; j += blockDim.x) sm[j] = __ldg(c.ss_mask + j);
+  const int ne = c.ss_ne;
+  for (int j = threadIdx.x; j < c.pat_np; j += blockDim.x) {
+    const unsigned m = __ldg(c.ss_mask + j);
+    sm[j] = m;
+    // middle slots of a symmetric 7- or 5-slot union (the -S / 0 / +S slots
+    // of the march come from registers); an absent slot reads offset 0
+    int4 e = make_int4(0, 0, 0, 0);
+    if (ne == 7) {
+      e.x = (m >> 1) & 1u ? c.ss_off[1] : 0;
+      e.y = (m >> 2) & 1u ? c.ss_off[2] : 0;
+      e.z = (m >> 4) & 1u ? c.ss_off[4] : 0;
+      e.w = (m >> 5) & 1u ? c.ss_off[5] : 0;
+    } else if (ne == 5) {
+      e.x = (m >> 1) & 1u ? c.ss_off[1] : 0;
+      e.y = (m >> 3) & 1u ? c.ss_off[3] : 0;
+    }
+    se[j] = e;
+  }
   __syncthreads();
-  return SsSmem{sv, sm};
+  return SsSmem{sv, sm, se};
 }
 
 // The adds run over every slot: an absent slot contributes 0.0 * 0.0 = +0.0,
