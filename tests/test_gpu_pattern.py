@@ -233,3 +233,28 @@ def test_staged_host_copies_round_trip(gpu_ready):
     assert ref[0].nbytes >= 16 << 20
     np.testing.assert_array_equal(got[0], ref[0])
     np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
+
+
+@pytest.mark.parametrize("shape", [(17, 16, 5), (40, 9, 13), (33, 33, 3), (256, 1, 6),
+                                   (64, 8, 2), (32, 16, 40), (96, 24, 7)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_march_edge_shapes_bit_identical(gpu_ready, shape):
+    """Plane-march edge cases against the CSR kernels: x-lines that are not a
+    multiple of 32 (no 2-D tiles), planes of a single line (the 5-slot union),
+    two or three planes, more planes per item than the grid has, partial last
+    items -- Newton (Leja chain: per-CTA claiming) and Chebyshev (fixed
+    stripes, two-back term)."""
+    from paper_1908_04081_b200.problems import poisson3d
+    for kw in (dict(sigma=6, eps_star=1e-10, basis_kind="newton", max_outer=8),
+               dict(sigma=5, eps_star=1e-10, basis_kind="chebyshev", max_outer=8)):
+        cfg = AdaptiveConfig(**kw)
+
+        def run():
+            prob = poisson3d(*shape)
+            return _plan(prob.a).mpk_schedule(cfg.sigma), adaptive_solve(prob, cfg, trace="fast")
+
+        s0, ref = _with_env({"SSCG_PATTERN": "0"}, run)
+        s1, got = _with_env({}, run)
+        assert s0["kind"] == "csr" and s1["kind"] == "pattern", (s0, s1)
+        np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
+        np.testing.assert_array_equal(got[0], ref[0])
