@@ -464,3 +464,24 @@ def test_full_size_c3_first_outer_loops(gpu_ready):
     assert tr.converged and true_rel(prob, x) <= 1e-10
     # survey probe of the reference on the same config: 46 outer / 425 total
     assert abs(tr.total_outer - 46) <= 0.05 * 46 and abs(tr.total_iters - 425) <= 0.05 * 425
+
+
+@pytest.mark.slow
+def test_full_size_c5w_first_outer_loops(gpu_ready):
+    """The headline workload at its bench size (256^3, sigma = 12 Newton, the
+    plane-march kernels): first-2 s sequence, first Gram, Ritz and alphas
+    against the oracle bounded to 2 outer loops on the CPU (~25 s); the full
+    GPU solve converges to eps* checked with an independent host SpMV."""
+    prob = problems.make_problem("c5w")
+    cfg = dict(sigma=12, eps_star=1e-10, basis_kind="newton")
+    ox, otr, oal, _ = O.solve_problem(prob, O.OracleConfig(max_outer=2, **cfg),
+                                      diagnostics=False)
+    x, tr, co = solve(prob, AdaptiveConfig(**cfg), trace="fast")
+    got = [(r.s_tilde, r.s_actual) for r in tr.outer_records[:2]]
+    assert got == [(r.s_tilde, r.s_actual) for r in otr.outer_records[:2]]
+    gram_close(tr._first_gram, otr.first_gram)
+    m = otr.total_iters
+    np.testing.assert_allclose(co.alphas[:m], oal, rtol=1e-8)
+    np.testing.assert_allclose(tr.lambda_max[:m], otr.lambda_max, rtol=1e-8)
+    np.testing.assert_allclose(tr.lambda_min[:m], otr.lambda_min, rtol=1e-8)
+    assert tr.converged and true_rel(prob, x) <= 1e-10
