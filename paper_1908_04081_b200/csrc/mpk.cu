@@ -1,4 +1,16 @@
-// mpk.cu -- K_mpk: fp64 CSR matrix-powers kernel fused with the basis recurrence.
+// mpk.cu -- K_mpk: fp64 matrix-powers kernels fused with the basis recurrence.
+//
+// Kernel families (plan.cu picks one per operator; all bit-identical):
+//   k_level0_zm / k_level_zm      plane march over a pattern-compressed stencil
+//                                 (the default for c1 c3 c5: 1-byte row ids)
+//   k_level0_ss / k_level_ss      superset-mask pattern rows (small strides)
+//   k_level0_pat / k_level_pat    table-walk pattern rows (any pattern operator)
+//   k_level0_vs / k_level_vs      value stream: stencil structure, row-varying
+//                                 values (c4), no column indices
+//   k_level0_staged / k_level_staged, k_level0 / k_level   general CSR
+//   opt-in experiments: k_mpk_wave (wavefront), *_win (TMA windows),
+//   k_level_zp (row pairs), k_level_zt (shared-memory tile march),
+//   k_resid_zm (split level 0) -- measured, see DESIGN.md 4a / 4b
 //
 // Reference: basis.py:210-225 `_recurrence_columns` over lacore.py:25-34 `spmv`
 // (scipy csr_matvec).  One launch per level l builds BOTH P_{l+1} and R_{l+1}
@@ -14,8 +26,9 @@
 // Level 0 also forms the true residual t = b - A x (adaptive.py:138) and the
 // partial sums of ||t||^2 and ||r||^2 (adaptive.py:139,158) on the same pass.
 //
-// Roofline (HBM-bound): per level 12 nnz + 4 (n+1) bytes of A plus
-// 16 n per generated column (+8 n with the Chebyshev two-back term).
+// Roofline (HBM-bound): per level 12 nnz + 4 (n+1) bytes of A for
+// CSR (1-2 n for a pattern operator, 8 ne n for a value stream) plus 16 n per
+// generated column (+8 n with the Chebyshev two-back term).
 #include "internal.cuh"
 #include "rowops.cuh"
 
