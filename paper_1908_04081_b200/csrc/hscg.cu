@@ -24,18 +24,26 @@ namespace {
 
 constexpr int HS_T = ROWS_PER_CTA;  // 256
 
-// row sums: 0 = CSR (unstaged), 1 = pattern ids uint8, 2 = pattern ids uint16
+// row sums: 0 = CSR (unstaged), 1 = pattern ids uint8, 2 = pattern ids uint16,
+// 3 = superset-mask rows with uint8 ids (the union of offsets unrolled: about
+// half the instructions of the table walk; same rounded operations)
 template <int MODE>
 struct RowSum {
   PatSmem T;
+  SsSmem S;
   __device__ __forceinline__ void init(const Ctx& c) {
-    if (MODE != 0) T = load_patterns(c);
+    if (MODE == 3)
+      S = load_ss(c);
+    else if (MODE != 0)
+      T = load_patterns(c);
   }
   __device__ __forceinline__ double dot(const Ctx& c, int64_t i, const double* x) const {
     double acc[1];
     const double* xs[1] = {x};
     if (MODE == 0) {
       row_dot<1>(c.col, c.val, c.rp[i], c.rp[i + 1], xs, acc);
+    } else if (MODE == 3) {
+      row_dot_m<1, SS_MAX_NE>(c, S, row_pattern<uint8_t>(c, i), i, xs, acc);
     } else {
       const int pid = MODE == 1 ? row_pattern<uint8_t>(c, i) : row_pattern<uint16_t>(c, i);
       row_dot_p<1>(T, T.ptr[pid], T.ptr[pid + 1], (int)i, xs, acc);
@@ -258,7 +266,15 @@ void hs_launch_iter(const Ctx& c, double* P, double* AP, double* R, size_t smem,
   k_hs_pt<MODE><<<c.red_n, HS_T, smem, s>>>(c, P, R);
 }
 
-int hs_mode(const Ctx& c) { return c.pid ? (c.pid_bytes == 1 ? 1 : 2) : 0; }
+int hs_mode(const Ctx& c) {
+  if (!c.pid) return 0;
+  if (c.pid_bytes == 1 && c.ss_ne > 0 && c.hs_ss) return 3;
+  return c.pid_bytes == 1 ? 1 : 2;
+}
+size_t hs_smem(const Ctx& c) {
+  if (!c.pid) return 0;
+  return hs_mode(c) == 3 ? ss_smem_bytes(c.pat_np) : pattern_smem_bytes(c.pat_np, c.pat_ne);
+}
 
 }  // namespace
 
@@ -270,11 +286,15 @@ void hscg_prepare() {
   cudaFuncSetAttribute(k_hs_ap<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_hs_pt<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_hs_pt<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_hs_init<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_hs_ap<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_hs_pt<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 void launch_hscg_init(const Ctx& c, double* P, double* R, const double* x0, cudaStream_t s) {
-  const size_t smem = c.pid ? pattern_smem_bytes(c.pat_np, c.pat_ne) : 0;
+  const size_t smem = hs_smem(c);
   switch (hs_mode(c)) {
+    case 3: hs_launch_init<3>(c, P, R, x0, smem, s); break;
     case 1: hs_launch_init<1>(c, P, R, x0, smem, s); break;
     case 2: hs_launch_init<2>(c, P, R, x0, smem, s); break;
     default: hs_launch_init<0>(c, P, R, x0, 0, s); break;
@@ -282,8 +302,9 @@ void launch_hscg_init(const Ctx& c, double* P, double* R, const double* x0, cuda
 }
 
 void launch_hscg_iter(const Ctx& c, double* P, double* AP, double* R, cudaStream_t s) {
-  const size_t smem = c.pid ? pattern_smem_bytes(c.pat_np, c.pat_ne) : 0;
+  const size_t smem = hs_smem(c);
   switch (hs_mode(c)) {
+    case 3: hs_launch_iter<3>(c, P, AP, R, smem, s); break;
     case 1: hs_launch_iter<1>(c, P, AP, R, smem, s); break;
     case 2: hs_launch_iter<2>(c, P, AP, R, smem, s); break;
     default: hs_launch_iter<0>(c, P, AP, R, 0, s); break;

@@ -156,6 +156,7 @@ struct Ctx {
   const double* vs_val;
   int ss_ne;
   int ss_off[SS_MAX_NE];
+  int hs_ss;         // HSCG row sums through the superset mask (SSCG_HS_SS)
   // plane-march form (mpk.cu k_level_zm): the union is symmetric, [-S .. 0 .. S]
   // with S = zm_S >= 256.  Thread t of a CTA owns column c (row mod S) and walks
   // rows c, c + S, c + 2S, ... of one chunk of zm_zc steps, so the -S / 0 / +S

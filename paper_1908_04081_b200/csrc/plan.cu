@@ -85,6 +85,7 @@ struct sscg_plan {
   cudaStream_t side = nullptr;  // Leja branch of the outer-loop graph
   cudaEvent_t ev_fork = nullptr;
   int leja_after0 = 1;  // the head chain forks after level 0
+  int hs_ss = 1;        // HSCG row sums through the superset mask
   cudaStream_t side2 = nullptr;  // true-residual branch (split level 0)
   cudaEvent_t ev_rfork = nullptr, ev_rjoin = nullptr;
   cudaEvent_t ev_leja[SMAX] = {};
@@ -297,6 +298,7 @@ Ctx make_ctx(sscg_plan* p) {
   for (int k = 0; k < VS_MAX_NE; ++k) c.vs_off[k] = p->vs_off[k];
   c.vs_val = p->d_vs_val;
   c.ss_ne = p->ss_ne;
+  c.hs_ss = p->hs_ss;
   for (int k = 0; k < SS_MAX_NE; ++k) c.ss_off[k] = p->ss_off[k];
   c.ss_mask = p->d_ss_mask;
   c.ss_val = p->d_ss_val;
@@ -593,6 +595,7 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   // (c5w: 207.7 ms per solve here vs 224.8 beside the recovery, 215.9 with the
   // former 1.33-wave recovery grid); SSCG_LEJA_HEAD=0 restores the side branch
   p->leja_head = atoi(env_or("SSCG_LEJA_HEAD", "1")) != 0;
+  p->hs_ss = atoi(env_or("SSCG_HS_SS", "1")) != 0;
   // (c5w: 197.1 vs 198.6 ms; c1, whose levels are shorter than a Leja point,
   // is faster with the fork before level 0: 9.43 vs 9.58 ms)
   p->leja_after0 = atoi(env_or("SSCG_LEJA_AFTER0", n_rows >= ((int64_t)1 << 20) ? "1" : "0")) != 0;

@@ -56,21 +56,29 @@ def test_hscg_parity(gpu_ready, name):
         np.testing.assert_allclose(tr.true_resid[-1], _true_rel(prob, x), rtol=1e-6)
 
 
-def test_hscg_kernel_modes_agree(gpu_ready):
-    """Pattern and CSR row sums give the same solve bit for bit (c1)."""
+@pytest.mark.parametrize("env,cases", [
+    ({"SSCG_PATTERN": "0"}, (("c1", None),)),
+    ({"SSCG_HS_SS": "0"}, (("c1", None), ("c5", 28))),
+], ids=["csr", "table_walk"])
+def test_hscg_kernel_modes_agree(gpu_ready, env, cases):
+    """Superset-mask pattern rows (default), table-walk pattern rows and CSR
+    rows give the same solve bit for bit: the row sums are identical, and the
+    dots too where both plans use the same grid (c1 for CSR; the pattern forms
+    of one plan always do, c5 proxy for the 7-slot union)."""
     import os
-    prob = problems.make_problem("c1")
-    assert _plan(prob.a).mpk_schedule(8)["kind"] == "pattern"
-    x1, t1, c1 = hscg_solve(prob, 1e-10)
-    os.environ["SSCG_PATTERN"] = "0"
-    try:
-        prob2 = problems.make_problem("c1")
-        assert _plan(prob2.a).mpk_schedule(8)["kind"] == "csr"
-        x2, t2, c2 = hscg_solve(prob2, 1e-10)
-    finally:
-        os.environ.pop("SSCG_PATTERN", None)
-    np.testing.assert_array_equal(c1.alphas, c2.alphas)
-    np.testing.assert_array_equal(x1, x2)
+    for key, scale in cases:
+        prob = problems.make_problem(key, scale=scale)
+        assert _plan(prob.a).mpk_schedule(8)["kind"] == "pattern"
+        x1, t1, c1 = hscg_solve(prob, 1e-10)
+        os.environ.update(env)
+        try:
+            prob2 = problems.make_problem(key, scale=scale)
+            x2, t2, c2 = hscg_solve(prob2, 1e-10)
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+        np.testing.assert_array_equal(c1.alphas, c2.alphas)
+        np.testing.assert_array_equal(x1, x2)
 
 
 def test_hscg_max_iters_zero_and_tridiag(gpu_ready):
