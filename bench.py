@@ -6,22 +6,27 @@
 One step = one full solve to eps* (the hot path: every outer loop's matrix-powers
 levels, Gram, O(s^2) control kernel and recovery, on the device).  Workload at
 N=1: config c5 weak-scaled, a 256^3 7-point Poisson slab per GPU, sigma=12,
-dynamic Newton basis, eps*=1e-10 (BASELINE.json configs[4]); the other configs
-are parity-test cases (tests/), selectable with --config for reference.
+dynamic Newton basis, eps*=1e-10 (BASELINE.json configs[4]); --config picks the
+other partitioned configs (c4 / c4j 192^3 and c5 512^3 strong-scaled, c3 128^3).
 
-value   CG iterations/s of the solve with b, x0 and A resident in HBM, device
-        time (CUDA events on the solver stream) summed over the K timed solves.
-e2e     the same metric through the public drop-in `adaptive_solve(problem, cfg,
-        trace="fast")` with host buffers: H2D of b and x0 and D2H of x and the
-        logs inside the timed region (wall clock, synchronised).
-roofline  dominant kernel = K_mpk (matrix-powers levels): algorithmic bytes
-        (12 nnz + 4 (n+1) per level of A, 16 n per generated
-        column, + x, b on level 0) / its CUDA-event time, from one profiled solve
-        after the timed region, against MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline  the CPU oracle port (oracle/sscg_oracle.py: the reference's
-        numpy/scipy arithmetic, diagnostics off) timed on this host for a
-        bounded sample (1 outer loop of the same problem), extrapolated to the
-        solve's outer-loop count.
+--gpus N > 1 runs the row-partitioned solve, one process per GPU: under
+torchrun (WORLD_SIZE set, it must equal N) or, without it, bench.py re-launches
+itself under torch.distributed.run with N ranks.  --partitioned takes the
+partitioned (NCCL) path at N = 1 too.
+
+value   CG iterations/s, device time (CUDA events on the solver stream) with b,
+        x0 and A resident in HBM; max over ranks.  Weak scaling (c5w): N x
+        total_iters / time (one unit = one CG iteration on one 256^3 slab);
+        strong scaling (c3 / c4 / c4j / c5): total_iters / time.
+e2e     the same metric through the public API with host buffers (H2D of b, x0
+        and D2H of x and the logs inside the timed region).
+roofline  dominant kernel = the matrix-powers levels: algorithmic bytes
+         / their CUDA-event time from one profiled
+        solve after the timed region, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the reference's CPU arithmetic (oracle/sscg_oracle.py, a port of
+        its numpy/scipy calls) as shipped -- per-iteration diagnostics on --
+        timed on this host for one outer loop of the same problem and
+        extrapolated to the solve's counts.
 """
 
 from __future__ import annotations
@@ -30,6 +35,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -41,26 +47,32 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# name: (problem key, sigma, basis, eps*, scaling, description)
 CONFIGS = {
-    # name: (problem key, scale override, sigma, basis, eps*, description)
-    "c5w": ("c5w", None, 12, "newton", 1e-10,
+    "c5w": ("c5w", 12, "newton", 1e-10, "weak",
             "c5 weak-scaled: 3D Poisson 7-pt 256^3 per GPU, sigma=12 Newton, eps*=1e-10"),
-    "c3": ("c3", None, 10, "chebyshev", 1e-10, "c3: 3D Poisson 7-pt 128^3, sigma=10 Chebyshev, 1e-10"),
-    "c4": ("c4", None, 10, "newton", 1e-8, "c4: 27-pt var-coef 192^3, sigma=10 Newton, 1e-8"),
-    "c4j": ("c4j", None, 10, "newton", 1e-8,
-            "c4 Jacobi-scaled (secondary run, SURVEY.md H6): 27-pt var-coef 192^3, sigma=10 Newton, 1e-8"),
-    "c1": ("c1", None, 8, "newton", 1e-10, "c1: 2D Poisson 64^2, sigma=8 Newton, 1e-10"),
-    "c2": ("c2", None, 10, "chebyshev", 1e-8, "c2: Strakos 1e4, sigma=10 Chebyshev, 1e-8"),
+    "c5": ("c5", 12, "newton", 1e-10, "strong",
+           "c5: 3D Poisson 7-pt 512^3 row-slab partitioned, sigma=12 Newton, eps*=1e-10"),
+    "c3": ("c3", 10, "chebyshev", 1e-10, "strong",
+           "c3: 3D Poisson 7-pt 128^3, sigma=10 Chebyshev, eps*=1e-10"),
+    "c4": ("c4", 10, "newton", 1e-8, "strong",
+           "c4: 27-pt var-coef 192^3 (lognormal 1.5), sigma=10 Newton, eps*=1e-8"),
+    "c4j": ("c4j", 10, "newton", 1e-8, "strong",
+            "c4 Jacobi-scaled (secondary run, SURVEY.md H6): 27-pt var-coef 192^3, "
+            "sigma=10 Newton, eps*=1e-8"),
+    "c1": ("c1", 8, "newton", 1e-10, "strong", "c1: 2D Poisson 64^2, sigma=8 Newton, eps*=1e-10"),
+    "c2": ("c2", 10, "chebyshev", 1e-8, "strong", "c2: Strakos 1e4, sigma=10 Chebyshev, eps*=1e-8"),
 }
+GOLDEN_COUNTS = {"c5w": "full_c5w", "c3": "full_c3"}  # reference runs at the full size
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -110,37 +122,39 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
 
 
+# ---------------------------------------------------------------------------
+# algorithmic bytes
 def kernel_name(sched):
     """The level kernel (levels >= 1) a matrix-powers schedule runs."""
     if sched["kind"] == "pattern":
-        return {"tile march": "k_level_zt", "pair march": "k_level_zp", "march": "k_level_zm",
-                "superset": "k_level_ss"}.get(sched.get("form"), "k_level_pat")
-    return {"csr": "k_level_staged", "wavefront": "k_mpk_wave",
-            "stencil values": "k_level_vs"}[sched["kind"]]
+        return {"march": "k_level_zm", "superset": "k_level_ss"}.get(sched.get("form"), "k_level_pat")
+    return {"csr": "k_level_staged", "stencil values": "k_level_vs"}[sched["kind"]]
 
 
 def a_bytes_per_level(n, nnz, sched):
     """Bytes of the operator one matrix-powers level must stream: CSR
     (12 nnz + 4 (n+1)) or, for a pattern-compressed plan, the
-    1- or 2-byte row ids (the pattern table lives in shared memory)."""
+    1- or 2-byte row ids (the pattern table lives in shared memory), or the
+    value stream's 8 bytes per union slot and row."""
     if sched and sched.get("kind") == "pattern":
         return (1 if sched["patterns"] <= 256 else 2) * n
-    if sched and sched.get("kind") == "stencil values":  # 8 bytes per union slot and row
+    if sched and sched.get("kind") == "stencil values":
         return 8 * sched["slots"] * n
     return 12 * nnz + 4 * (n + 1)
 
 
 def mpk_bytes_per_outer(n, nnz, sigma, mu_nonzero, sched=None):
-    """Algorithmic bytes of the sigma matrix-powers levels of one outer loop
-    (SURVEY.md 8(d)): A once per level, 16 n per generated column (+8 n for the
-    Chebyshev two-back term), x and b on level 0 (true residual)."""
+    """Algorithmic bytes of the sigma matrix-powers levels of one outer loop:
+    A once per level, 16 n per generated column (in + out), +8 n for the
+    Chebyshev two-back term (levels >= 1), x and b on level 0 (true residual)."""
     s_a = a_bytes_per_level(n, nnz, sched)
     gen = 2 * sigma - 1
-    two_back = (2 * sigma - 3) if mu_nonzero else 0  # columns with l >= 1
-    return sigma * s_a + 16 * n * gen + 8 * n * two_back + 16 * n + 8 * n  # + r0 norm read
+    two_back = (2 * sigma - 3) if mu_nonzero else 0
+    return sigma * s_a + 16 * n * gen + 8 * n * two_back + 16 * n
 
 
 def outer_bytes(n, nnz, sigma, s_t, mu_nonzero, sched=None):
+    """One outer loop: the levels, the Gram (one read of Y), the recovery."""
     return (mpk_bytes_per_outer(n, nnz, sigma, mu_nonzero, sched) + 8 * n * (2 * sigma + 1)
             + 8 * n * (2 * s_t + 1) + 8 * n + 24 * n)
 
@@ -150,9 +164,8 @@ def cpu_threads():
     of the Gram and recovery) -- scipy csr_matvec and numpy element-wise work
     run on one core."""
     try:
-        import numpy
         import threadpoolctl
-        numpy.ones(2) @ numpy.ones(2)
+        np.ones(2) @ np.ones(2)
         pools = [(d["internal_api"], int(d["num_threads"]), d.get("version"))
                  for d in threadpoolctl.threadpool_info()]
     except Exception:
@@ -162,62 +175,320 @@ def cpu_threads():
                   "and numpy element-wise work (most of the time) are single-threaded")
 
 
-def cpu_sample(prob, cfg_kw, outer_count, total_iters):
-    """Oracle port on this host: 1 outer loop of the same problem (bounded),
-    per-outer time extrapolated to the solve's outer count."""
-    from oracle import sscg_oracle as O
+def workload_config(args, world):
+    """The `config` dict -- identical in both arms (same workload)."""
+    key, sigma, basis, eps, scaling, desc = CONFIGS[args.config]
+    c = {"workload": desc, "config": args.config, "sigma": sigma, "basis": basis,
+         "eps_star": eps, "scaling": scaling, "x0": "0",
+         "l2": "inputs larger than L2 (each vector >= 16 MB; Y >= 0.35 GB)"
+               if key not in ("c1", "c2") else "L2-resident (latency-bound)"}
+    if args.scale:
+        c["scale"] = args.scale
+    c["parallelism"] = (f"dp{world} row slabs (ghost depth sigma; one halo exchange + one "
+                        "allreduce per outer loop)") if (world > 1 or args.partitioned) else "dp1"
+    return c
+
+
+def global_shape(args, world):
+    """(problem key, nx, ny, nz) of the global problem of a partitioned run."""
+    key = CONFIGS[args.config][0]
+    if key == "c5w":
+        e = args.scale or 256
+        return key, e, e, e * world
+    e = args.scale or {"c5": 512, "c3": 128, "c4": 192, "c4j": 192}.get(key, 0)
+    if not e:
+        raise SystemExit(f"--config {args.config} is not a partitioned 3-D workload")
+    return key, e, e, e
+
+
+# ---------------------------------------------------------------------------
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(n):
+    """--gpus N > 1 without torchrun: run this same command as N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    return subprocess.call(cmd)
+
+
+def init_gloo(rank, world):
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29533))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return dist
+
+
+# ---------------------------------------------------------------------------
+def profile_solve(lib, L, handle, run):
+    """One profiled solve (per-kernel-class event times) outside the timed region."""
+    import ctypes as C
+    L.check(lib.sscg_set_profiling(handle, 1))
+    run()
+    L.check(lib.sscg_set_profiling(handle, 0))
+    pms = np.zeros(5)
+    pcnt = np.zeros(5, dtype=np.int64)
+    L.check(lib.sscg_get_profile(handle, L.dptr(pms), pcnt.ctypes.data_as(C.POINTER(C.c_int64))))
+    return pms, pcnt
+
+
+def roofline(n, nnz, sigma, basis, sched, pms, pcnt, outer_active, traffic=None):
+    """roofline object of the matrix-powers levels: algorithmic bytes of the
+    profiled solve's active outer loops / their CUDA-event time."""
+    mu_nz = basis == "chebyshev"
+    mpk_bytes = outer_active * mpk_bytes_per_outer(n, nnz, sigma, mu_nz, sched)
+    peak, peak_kind = peaks()
+    launches = max(1, outer_active * sigma)
+    ach = mpk_bytes / (float(pms[0]) / 1e3) / 1e9
+    tot = max(float(pms.sum()), 1e-9)
+    return {
+        "bound": "hbm", "kernel": kernel_name(sched), "schedule": sched,
+        "a_bytes_per_level": a_bytes_per_level(n, nnz, sched),
+        "a_bytes_per_level_csr": a_bytes_per_level(n, nnz, None),
+        "achieved": ach, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+        "frac": ach / peak, "traffic": traffic,
+        "algorithmic_bytes_per_launch": mpk_bytes / launches,
+        "avg_launch_ms": float(pms[0]) / launches,
+        "kernel_ms": {"mpk": pms[0], "gram": pms[1], "small": pms[2], "recovery": pms[3],
+                      "other": pms[4]},
+        "kernel_launches": {"mpk_outer_loops": int(pcnt[0]), "gram": int(pcnt[1]),
+                            "small": int(pcnt[2]), "recovery": int(pcnt[3])},
+        "share_of_step": {k: float(v) / tot for k, v in
+                          zip(("mpk", "gram", "small", "recovery", "other"), pms)},
+    }
+
+
+def traffic_for(config, kname):
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(tpath)).get(config, {}).get(kname)
+    except Exception:
+        return None
+
+
+def single_plan_line(prob, cfg_kw, steps, warmup, env=None, label=None):
+    """Device-time solves of one problem on a single-GPU plan (optionally under
+    an environment override, e.g. SSCG_PATTERN=0 for the CSR kernels)."""
+    from paper_1908_04081_b200 import AdaptiveConfig, _lib as L
+    from paper_1908_04081_b200.adaptive import LogBuffers, make_config
+    old = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        t0 = time.perf_counter()
+        plan = L.Plan(prob.a.n, prob.a.row_ptr, prob.a.col_idx, prob.a.values, device=0)
+        t_plan = time.perf_counter() - t0
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    lib = L.load()
+    cfg, ccfg = make_config(AdaptiveConfig(**cfg_kw), prob, "fast")
+    logs = LogBuffers(cfg)
+    b, x0 = L.f64(prob.b), L.f64(prob.x0)
+    L.check(lib.sscg_load(plan.handle, L.dptr(b), L.dptr(x0)))
+    ms = []
+    for k in range(warmup + steps):
+        L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
+        if k >= warmup:
+            ms.append(logs.s.device_ms)
+    L.check(lib.sscg_fetch(plan.handle, None, logs.s))
+    tot, outer = int(logs.s.total_iters), int(logs.s.total_outer)
+    pms, pcnt = profile_solve(lib, L, plan.handle,
+                              lambda: L.check(lib.sscg_run(plan.handle, ccfg, logs.s)))
+    sched = plan.mpk_schedule(cfg.sigma)
+    dev = sum(ms) / len(ms)
+    n, nnz = prob.a.n, prob.a.nnz
+    line = {"workload": label, "value": tot / (dev / 1e3), "unit": "iter/s", "ms_per_step": dev,
+            "steps": steps, "syncs_to_tol": outer, "total_iters": tot,
+            "converged": int(logs.s.status) == L.CONVERGED, "plan_create_s": round(t_plan, 2),
+            "roofline": roofline(n, nnz, cfg.sigma, cfg.basis_kind, sched, pms, pcnt, outer + 1)}
+    plan.close()
+    return line
+
+
+# ---------------------------------------------------------------------------
+def run_single(args):
+    """N = 1 on the single-GPU plan (the default headline line)."""
+    import ctypes as C
+
+    import scipy.sparse as sp
+
+    from paper_1908_04081_b200 import AdaptiveConfig, _lib as L, adaptive_solve, problems
+    from paper_1908_04081_b200.adaptive import LogBuffers, make_config
+    from paper_1908_04081_b200.kernels import _plan
+
+    key, sigma, basis, eps, scaling, desc = CONFIGS[args.config]
     t0 = time.perf_counter()
-    O.solve_problem(prob, O.OracleConfig(max_outer=1, **cfg_kw), diagnostics=False)
-    t1 = time.perf_counter() - t0
-    est = t1 * (outer_count + 1)
-    return total_iters / est, t1
+    prob = problems.make_problem(key, scale=args.scale)
+    t_gen = time.perf_counter() - t0
+    cfg_kw = dict(sigma=sigma, eps_star=eps, basis_kind=basis)
+    n, nnz = prob.a.n, prob.a.nnz
+    # first call through the public API on a matrix with no cached plan: plan
+    # creation (upload, pattern compression) + the solve, host buffers in / out
+    t0 = time.perf_counter()
+    adaptive_solve(prob, AdaptiveConfig(**cfg_kw), trace="fast")
+    t_first = time.perf_counter() - t0
+    plan = _plan(prob.a, 0)
+    lib = L.load()
+    cfg, ccfg = make_config(AdaptiveConfig(**cfg_kw), prob, "fast")
+    logs = LogBuffers(cfg)
+    b, x0 = L.f64(prob.b), L.f64(prob.x0)
+    L.check(lib.sscg_load(plan.handle, L.dptr(b), L.dptr(x0)))
+    sched = plan.mpk_schedule(sigma)
+
+    def dev_solve():
+        L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
+        return logs.s.device_ms, int(logs.s.outer_launched)
+
+    for _ in range(args.warmup):
+        dev_solve()
+    ms_list, launches = [], 0
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            ms, ol = dev_solve()
+            ms_list.append(ms)
+            # per outer loop: sigma levels, gram, small, params + (sigma-2) Leja, recovery
+            launches += 2 + ol * (sigma + sigma + 2)
+    L.check(lib.sscg_fetch(plan.handle, None, logs.s))
+    total_iters, total_outer = int(logs.s.total_iters), int(logs.s.total_outer)
+    converged = int(logs.s.status) == L.CONVERGED
+    x = np.empty(n)
+    L.check(lib.sscg_fetch(plan.handle, L.dptr(x), logs.s))
+    a = prob.a
+    rel = float(np.linalg.norm(prob.b - sp.csr_matrix((a.values, a.col_idx, a.row_ptr),
+                                                      shape=(n, n)) @ x) / np.linalg.norm(prob.b))
+    dev_ms = sum(ms_list) / len(ms_list)
+    value = total_iters / (dev_ms / 1e3)
+
+    pms, pcnt = profile_solve(lib, L, plan.handle, dev_solve)
+    ph = np.zeros(8, dtype=np.int64)
+    L.check(lib.sscg_get_small_phases(plan.handle, ph.ctypes.data_as(C.POINTER(C.c_int64))))
+    calls = max(1, int(ph[7]))
+    names = ["classify", "gram_extract_c", "nested_conds", "select_truncate", "inner_loop",
+             "next_params"]
+    small_phases = {nm: round(float(ph[i]) / calls / 1965.0, 2) for i, nm in enumerate(names)}
+    s_t = [int(v) for v in logs.rec_i[:total_outer, L.REC_STILDE]]
+    mu_nz = basis == "chebyshev"
+    solve_bytes = sum(outer_bytes(n, nnz, sigma, st, mu_nz, sched) for st in s_t) + \
+        mpk_bytes_per_outer(n, nnz, sigma, mu_nz, sched) + 8 * (2 * sigma + 1) * n
+    hbm_peak, _ = peaks()
+    solve_gbs = solve_bytes / (dev_ms / 1e3) / 1e9
+    rl = roofline(n, nnz, sigma, basis, sched, pms, pcnt, total_outer + 1,
+                  traffic_for(args.config, kernel_name(sched)))
+    rl["small_phases_us_per_call"] = small_phases
+
+    # end to end through the public API (host buffers), plan cached on the matrix
+    e2e_times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        xe, tr, co = adaptive_solve(prob, AdaptiveConfig(**cfg_kw), trace="fast")
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_value = tr.total_iters / (sum(e2e_times) / len(e2e_times))
+    log_bytes = int(logs.iters.nbytes + logs.rec_i.nbytes + logs.rec_d.nbytes +
+                    logs.conds.nbytes + 3 * logs.thetas.nbytes + logs.outer_true.nbytes)
+
+    cpu = None
+    if not args.no_cpu:
+        cpu = cpu_baseline_sample(prob, cfg_kw, total_outer, total_iters)
+
+    secondary = []
+    if args.config == "c5w" and not args.no_secondary:
+        # the general CSR kernels on the same operator (no pattern compression)
+        secondary.append(single_plan_line(
+            prob, cfg_kw, min(args.steps, 3), 1, env={"SSCG_PATTERN": "0"},
+            label="c5w through the general CSR kernels (SSCG_PATTERN=0): " + desc))
+        # the value-stream kernels on c4j (27-point, row-varying values)
+        _, s4, b4, e4, _, d4 = CONFIGS["c4j"]
+        p4 = problems.make_problem("c4j", scale=args.scale and max(16, args.scale * 3 // 4))
+        secondary.append(single_plan_line(p4, dict(sigma=s4, eps_star=e4, basis_kind=b4),
+                                          min(args.steps, 3), 1, label=d4))
+        del p4
+
+    line = {
+        "metric": "cg_iterations_per_sec", "value": value, "unit": "iter/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, seeded (np.random.default_rng(0)): x*~U[-1,1], b=A x*, x0=0",
+        "config": workload_config(args, 1),
+        "solve": {"n": n, "nnz": nnz, "syncs_to_tol": total_outer, "total_iters": total_iters,
+                  "converged": converged, "final_true_rel_resid": rel, "trace": "fast",
+                  "problem_gen_s": round(t_gen, 2), "collectives": plan.collectives(),
+                  "syncs_note": "one global reduction point (the Gram) per outer loop; a "
+                                "single-GPU plan needs no NCCL call for it"},
+        "hbm": {"solve_gbs": solve_gbs, "frac_of_measured": solve_gbs / hbm_peak,
+                "frac_of_8tbs": solve_gbs / 8000.0, "algorithmic_bytes_per_solve": solve_bytes},
+        "roofline": rl,
+        "e2e": {"value": e2e_value, "unit": "iter/s", "h2d_bytes_per_step": 16 * n,
+                "d2h_bytes_per_step": 8 * n + log_bytes,
+                "first_call_s": round(t_first, 3),
+                "first_call_iter_per_s": total_iters / t_first,
+                "note": "adaptive_solve(problem, cfg, trace='fast') with the plan cached on the "
+                        "matrix like SparseMatrix._csr; first_call_s = the first call on a fresh "
+                        "matrix: plan creation (upload + pattern compression) + the solve"},
+        "cpu_baseline": cpu,
+        "secondary": secondary,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
+def partition_rows(key, nx, ny, nz):
+    from paper_1908_04081_b200.partition import Stencil7Rows, Varcoef27Rows
+    if key in ("c4", "c4j"):
+        return Varcoef27Rows(nx, jacobi=key == "c4j")
+    return Stencil7Rows(nx, ny, nz)
 
 
 def run_partitioned(args, rank, world):
-    """One rank of the row-partitioned solve (torchrun, one process per GPU):
-    gloo carries the setup plumbing (ghost requests, the NCCL id, the final
-    max-over-ranks time), NCCL carries the per-outer-loop halo exchange and the
-    one Gram allreduce inside the CUDA graph."""
-    import ctypes as C
+    """One rank of the row-partitioned solve (one process per GPU): gloo
+    carries the setup plumbing (ghost requests, the NCCL id, the final
+    max-over-ranks time), NCCL the per-outer-loop halo exchange and the one
+    Gram allreduce inside the CUDA graph."""
     import types
 
     import scipy.sparse as sp
     import torch
-    import torch.distributed as dist
 
     from paper_1908_04081_b200 import AdaptiveConfig, _lib as L
-    from paper_1908_04081_b200.adaptive import LogBuffers
-    from paper_1908_04081_b200.dist import solve_partitioned
-    from paper_1908_04081_b200.partition import Stencil7Rows
+    from paper_1908_04081_b200.dist import check_ranks_agree, logs_digest, solve_partitioned
+    from paper_1908_04081_b200.partition import slab_bounds
 
-    key, scale, sigma, basis, eps, desc = CONFIGS[args.config]
-    if key != "c5w":
-        raise SystemExit("the partitioned bench runs the weak-scaled c5 slabs (--config c5w)")
-    if not dist.is_initialized():
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29533")
-        dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist = init_gloo(rank, world)
+    key, sigma, basis, eps, scaling, desc = CONFIGS[args.config]
     local = int(os.environ.get("LOCAL_RANK", rank))
-    edge = args.scale or 256
-    nx = ny = edge
-    nz = edge * world
-    rows = Stencil7Rows(nx, ny, nz)
+    key, nx, ny, nz = global_shape(args, world)
+    rows = partition_rows(key, nx, ny, nz)
     n = rows.n
     t0 = time.perf_counter()
-    xs = np.random.default_rng(0).uniform(-1.0, 1.0, n)  # same x* as problems.poisson3d
-    from paper_1908_04081_b200.partition import slab_bounds
     bnd = slab_bounds(n, world)
     lo, hi = int(bnd[rank]), int(bnd[rank + 1])
     ip, cols, vals = rows.rows(np.arange(lo, hi))
-    b_own = sp.csr_matrix((vals, cols, ip), shape=(hi - lo, n)) @ xs
-    b_glob = np.zeros(n)
-    b_glob[lo:hi] = b_own
+    a_own = sp.csr_matrix((vals, cols, ip), shape=(hi - lo, n))
+    if key in ("c4", "c4j"):
+        b_glob = rows.rhs()
+        b_own = b_glob[lo:hi]
+    else:  # b = A x*, x* ~ U[-1, 1] from seed 0 (problems.poisson3d)
+        xs = np.random.default_rng(0).uniform(-1.0, 1.0, n)
+        b_own = a_own @ xs
+        del xs
+        b_glob = np.zeros(n)
+        b_glob[lo:hi] = b_own
     nb2 = torch.tensor([float(b_own @ b_own)], dtype=torch.float64)
     dist.all_reduce(nb2)
     lam = [2.0 - 2.0 * math.cos(math.pi / (m + 1)) for m in (nx, ny, nz)]
-    lmax = sum(2.0 + 2.0 * math.cos(math.pi / (m + 1)) for m in (nx, ny, nz)) - 0.0
-    scal = types.SimpleNamespace(a=types.SimpleNamespace(n_a=7), norm_a=lmax, norm_abs_a=lmax,
-                                 kappa_a=lmax / sum(lam))
+    lmax = sum(2.0 + 2.0 * math.cos(math.pi / (m + 1)) for m in (nx, ny, nz))
+    scal = types.SimpleNamespace(a=types.SimpleNamespace(n_a=27 if key.startswith("c4") else 7),
+                                 norm_a=lmax, norm_abs_a=lmax, kappa_a=lmax / sum(lam))
     cfg = AdaptiveConfig(sigma=sigma, eps_star=eps, basis_kind=basis)
 
     def exchange(obj):
@@ -234,11 +505,10 @@ def run_partitioned(args, rank, world):
     xo, tr, co, plan = solve_partitioned(rows, scal, b_glob, np.zeros(n), cfg, rank, world, local,
                                          exchange, bcast, info=info)
     t_setup = time.perf_counter() - t0
+    del b_glob
     lib = L.load()
     logs, ccfg = info["logs"], info["ccfg"]
-
     sched = plan.mpk_schedule(sigma)
-    mpk_launches = len(sched["passes"])  # wavefront passes (or sigma level launches)
 
     def dev_solve():
         L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
@@ -253,12 +523,13 @@ def run_partitioned(args, rank, world):
             dist.barrier()
             ms, ol = dev_solve()
             ms_list.append(ms)
-            launches += 3 + ol * (2 * sigma + 4)  # init 3; halo pack/unpack, params, Leja, levels, ...
+            # per outer loop: halo pack/unpack, sigma levels, gram, small,
+            # params + (sigma-2) Leja points, recovery (+ NCCL's own kernels)
+            launches += 3 + ol * (2 * sigma + 4)
     dev_ms = sum(ms_list) / len(ms_list)
     tmax = torch.tensor([dev_ms], dtype=torch.float64)
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    # end to end through the C ABI with host buffers: H2D of b and x0, D2H of x
-    # and the logs inside the timed region, max over ranks
+    # end to end through the C ABI with host buffers, max over ranks
     b_loc, x0_loc = info["b"], info["x0"]
     x_host = np.empty(hi - lo)
     e2e = []
@@ -272,288 +543,183 @@ def run_partitioned(args, rank, world):
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     L.check(lib.sscg_fetch(plan.handle, None, logs.s))
     total_iters, total_outer = int(logs.s.total_iters), int(logs.s.total_outer)
-    # roofline of the matrix-powers kernel on this rank's owned rows (SURVEY.md
-    # 8(d): owned-row traffic only), from one profiled solve outside the timed
-    # region (every rank runs it: the collectives are inside), max over ranks
-    L.check(lib.sscg_set_profiling(plan.handle, 1))
-    dev_solve()
-    L.check(lib.sscg_set_profiling(plan.handle, 0))
-    pms = np.zeros(5)
-    pcnt = np.zeros(5, dtype=np.int64)
-    L.check(lib.sscg_get_profile(plan.handle, L.dptr(pms), pcnt.ctypes.data_as(C.POINTER(C.c_int64))))
+    # every rank decided the same: compare the decision hash across ranks
+    check_ranks_agree(exchange(logs_digest(logs)))
+    coll = plan.collectives()
+    pms, pcnt = profile_solve(lib, L, plan.handle, dev_solve)
     mpk_ms_t = torch.tensor([float(pms[0])], dtype=torch.float64)
     dist.all_reduce(mpk_ms_t, op=dist.ReduceOp.MAX)
     L.check(lib.sscg_fetch(plan.handle, None, logs.s))
     # global true residual from the owned pieces (independent host SpMV)
     x_glob = torch.zeros(n, dtype=torch.float64)
-    x_glob[lo:hi] = torch.from_numpy(xo)
+    x_glob[lo:hi] = torch.from_numpy(x_host)
     dist.all_reduce(x_glob)
-    resid = sp.csr_matrix((vals, cols, ip), shape=(hi - lo, n)) @ x_glob.numpy() - b_own
+    resid = a_own @ x_glob.numpy() - b_own
     rr = torch.tensor([float(resid @ resid)], dtype=torch.float64)
     dist.all_reduce(rr)
     rel = math.sqrt(rr.item() / nb2.item())
     ms = tmax.item()
-    value = world * total_iters / (ms / 1e3)
+    units = world if scaling == "weak" else 1
+    value = units * total_iters / (ms / 1e3)
     if rank == 0:
         n_own = hi - lo
+        pms[0] = mpk_ms_t.item()
+        rl = roofline(n_own, int(ip[-1]), sigma, basis, sched, pms, pcnt, total_outer + 1)
+        rl["kernel"] += " (owned rows; ghost-row levels are redundant work, not counted)"
+        cpu = None
+        if not args.no_cpu and world == 1:
+            from paper_1908_04081_b200 import problems
+            prob = problems.make_problem(key, scale=args.scale, world=1)
+            cpu = cpu_baseline_sample(prob, dict(sigma=sigma, eps_star=eps, basis_kind=basis),
+                                      total_outer, total_iters)
         line = {
             "metric": "cg_iterations_per_sec", "value": value, "unit": "iter/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic, seeded (np.random.default_rng(0)): x*~U[-1,1], b=A x*, x0=0",
-            "config": {"workload": desc + f" (global {nx}x{ny}x{nz})", "n": n, "n_per_gpu": n_own,
-                       "sigma": sigma, "basis": basis, "eps_star": eps,
-                       "syncs_to_tol": total_outer, "total_iters": total_iters,
-                       "converged": int(logs.s.status) == L.CONVERGED,
-                       "final_true_rel_resid": rel, "trace": "fast",
-                       "parallelism": f"dp{world} (row slabs, ghost depth {sigma}, one NCCL "
-                                      "halo exchange + one NCCL allreduce per outer loop)",
-                       "value_definition": "per-slab CG iterations/s summed over ranks = "
-                                           "world x total_iters / max-over-ranks device time",
-                       "global_iters_per_sec": total_iters / (ms / 1e3),
-                       "setup_s": round(t_setup, 2),
-                       "allreduce_per_outer": 1, "halo_exchanges_per_outer": 1},
-            "e2e": {"value": world * total_iters / te.item(), "unit": "iter/s",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic, seeded (np.random.default_rng(0))",
+            "config": workload_config(args, world),
+            "solve": {"global_shape": [nx, ny, nz], "n": n, "n_per_gpu": n_own,
+                      "syncs_to_tol": total_outer, "total_iters": total_iters,
+                      "converged": int(logs.s.status) == L.CONVERGED,
+                      "final_true_rel_resid": rel, "trace": "fast",
+                      "value_definition": ("world x total_iters / max-over-ranks device time "
+                                           "(one unit = a CG iteration on one slab)"
+                                           if scaling == "weak" else
+                                           "total_iters / max-over-ranks device time"),
+                      "global_iters_per_sec": total_iters / (ms / 1e3),
+                      "setup_s": round(t_setup, 2), "collectives": coll,
+                      "ranks_agree": True},
+            "roofline": rl,
+            "e2e": {"value": units * total_iters / te.item(), "unit": "iter/s",
                     "h2d_bytes_per_step": int(8 * (len(b_loc) + len(x0_loc))),
                     "d2h_bytes_per_step": int(8 * (hi - lo) + logs.iters.nbytes),
                     "note": "sscg_solve per rank (host b, x0 -> x, logs), max over ranks"},
+            "cpu_baseline": cpu,
             "gpu_launches": launches, "clocks": clk.summary(),
         }
-        mu_nz = basis == "chebyshev"
-        mpk_bytes = (total_outer + 1) * mpk_bytes_per_outer(n_own, 7 * n_own, sigma, mu_nz, sched)
-        mpk_ms = mpk_ms_t.item()
-        hbm_peak, peak_kind = peaks()
-        ach = mpk_bytes / (mpk_ms / 1e3) / 1e9
-        line["roofline"] = {
-            "bound": "hbm", "kernel": kernel_name(sched) + " (owned rows; ghost-row levels are "
-                                                          "redundant work, not counted)",
-            "mpk_schedule": sched, "achieved": ach, "peak": hbm_peak, "peak_kind": peak_kind,
-            "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
-            "kernel_ms": {"mpk": pms[0], "gram": pms[1], "small": pms[2], "recovery": pms[3],
-                          "other (halo, allreduce, Leja)": pms[4]}}
         print(json.dumps(line))
     dist.barrier()
 
 
-def run_ours(args, rank, world):
-    from paper_1908_04081_b200 import AdaptiveConfig, _lib as L, adaptive_solve, problems
-    from paper_1908_04081_b200.adaptive import LogBuffers, make_config
-    from paper_1908_04081_b200.kernels import _plan
+# ---------------------------------------------------------------------------
+# CPU: the reference's arithmetic (oracle port) on this host
+def reference_counts(config, world):
+    """(outer, total, source) of the global solve the CPU figure extrapolates to:
+    the reference's own full-size run when one is committed (tests/golden/
+    full_*.npz, made by running the reference here), else the GPU counts."""
+    name = GOLDEN_COUNTS.get(config) if world == 1 else None
+    if name:
+        path = os.path.join(ROOT, "tests", "golden", name + ".npz")
+        if os.path.exists(path):
+            f = np.load(path)["flags"]
+            return int(f[4]), int(f[3]), f"the reference's own full run ({name}.npz)"
+    cpath = os.path.join(ROOT, "profiles", "counts.json")
+    if os.path.exists(cpath):
+        c = json.load(open(cpath)).get(f"{config}_w{world}")
+        if c:
+            return int(c["outer"]), int(c["total"]), "GPU solve of the global problem (counts.json)"
+    return None
 
-    key, scale, sigma, basis, eps, desc = CONFIGS[args.config]
-    if world > 1 or args.partitioned:
-        return run_partitioned(args, rank, world)
+
+def time_outer(prob, cfg_kw, diagnostics):
+    """Seconds of one outer loop (max_outer=1) of the oracle port, and the
+    inner iterations it ran."""
+    from oracle import sscg_oracle as O
     t0 = time.perf_counter()
-    prob = problems.make_problem(key, scale=args.scale or scale, world=world)
-    t_gen = time.perf_counter() - t0
-    cfg_kw = dict(sigma=sigma, eps_star=eps, basis_kind=basis)
-    cfg = AdaptiveConfig(**cfg_kw)
-    n, nnz = prob.a.n, prob.a.nnz
-    plan = _plan(prob.a, 0)
-    lib = L.load()
-    cfg, ccfg = make_config(cfg, prob, "fast")
-    logs = LogBuffers(cfg)
-    b = L.f64(prob.b)
-    x0 = L.f64(prob.x0)
-    L.check(lib.sscg_load(plan.handle, L.dptr(b), L.dptr(x0)))
+    _, tr, _, _ = O.solve_problem(prob, O.OracleConfig(max_outer=1, **cfg_kw),
+                                  diagnostics=diagnostics)
+    return time.perf_counter() - t0, max(1, tr.total_iters)
 
-    sched = plan.mpk_schedule(sigma)
-    mpk_launches = len(sched["passes"])  # wavefront passes (or sigma level launches)
 
-    def dev_solve():
-        L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
-        return logs.s.device_ms, int(logs.s.outer_launched)
-
-    for _ in range(args.warmup):
-        dev_solve()
-    # ---- timed region (device time, inputs resident in HBM)
-    ms_list, launches = [], 0
-    with ClockSampler(0) as clk:
-        for _ in range(args.steps):
-            ms, ol = dev_solve()
-            ms_list.append(ms)
-            # per outer: mpk passes, gram, small, params + (sigma-2) Leja, recovery
-            launches += 2 + ol * (mpk_launches + sigma + 2)
-    L.check(lib.sscg_fetch(plan.handle, None, logs.s))
-    total_iters, total_outer = int(logs.s.total_iters), int(logs.s.total_outer)
-    converged = int(logs.s.status) == L.CONVERGED
-    x = np.empty(n)
-    L.check(lib.sscg_fetch(plan.handle, L.dptr(x), logs.s))
-    import scipy.sparse as sp
-    a = prob.a
-    rel = float(np.linalg.norm(prob.b - sp.csr_matrix((a.values, a.col_idx, a.row_ptr),
-                                                      shape=(n, n)) @ x) / np.linalg.norm(prob.b))
-    dev_ms = sum(ms_list) / len(ms_list)
-    value = total_iters / (dev_ms / 1e3)
-
-    # ---- profiled solve (per-kernel-class event times), outside the timed region
-    L.check(lib.sscg_set_profiling(plan.handle, 1))
-    dev_solve()
-    L.check(lib.sscg_set_profiling(plan.handle, 0))
-    import ctypes as C
-    pms = np.zeros(5)
-    pcnt = np.zeros(5, dtype=np.int64)
-    L.check(lib.sscg_get_profile(plan.handle, L.dptr(pms),
-                                 pcnt.ctypes.data_as(C.POINTER(C.c_int64))))
-    ph = np.zeros(8, dtype=np.int64)
-    L.check(lib.sscg_get_small_phases(plan.handle, ph.ctypes.data_as(C.POINTER(C.c_int64))))
-    calls = max(1, int(ph[7]))
-    names = ["classify", "gram_extract_c", "nested_conds", "select_truncate", "inner_loop",
-             "next_params"]
-    small_phases = {nm: round(float(ph[i]) / calls / 1965.0, 2) for i, nm in enumerate(names)}
-    s_t = [int(v) for v in logs.rec_i[:total_outer, L.REC_STILDE]]
-    mu_nz = basis == "chebyshev"
-    active = total_outer + 1  # outer loops whose levels did real work
-    mpk_bytes = active * mpk_bytes_per_outer(n, nnz, sigma, mu_nz, sched)
-    mpk_ms = float(pms[0])
-    hbm_peak, peak_kind = peaks()
-    mpk_gbs = mpk_bytes / (mpk_ms / 1e3) / 1e9
-    solve_bytes = sum(outer_bytes(n, nnz, sigma, st, mu_nz, sched) for st in s_t) + \
-        mpk_bytes_per_outer(n, nnz, sigma, mu_nz, sched) + 8 * (2 * sigma + 1) * n
-    solve_gbs = solve_bytes / (dev_ms / 1e3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            kname = kernel_name(sched)
-            traffic = json.load(open(tpath)).get(args.config, {}).get(kname)
-        except Exception:
-            traffic = None
-
-    # ---- end to end through the public API (host buffers)
-    e2e_times = []
-    for i in range(max(1, min(args.steps, 3))):
-        t0 = time.perf_counter()
-        xe, tr, co = adaptive_solve(prob, AdaptiveConfig(**cfg_kw), trace="fast")
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_value = tr.total_iters / (sum(e2e_times) / len(e2e_times))
-    log_bytes = int(logs.iters.nbytes + logs.rec_i.nbytes + logs.rec_d.nbytes +
-                    logs.conds.nbytes + 3 * logs.thetas.nbytes + logs.outer_true.nbytes)
-
-    # ---- CPU baseline (oracle port, bounded sample)
-    cpu = None
-    if not args.no_cpu:
-        cpu_v, t1 = cpu_sample(prob, cfg_kw, total_outer, total_iters)
-        cores, tnote = cpu_threads()
-        cpu = {"value": cpu_v, "unit": "iter/s", "cores": cores, "kind": "port",
-               "sample": f"oracle/sscg_oracle.py (numpy/scipy, as the reference) on the same "
-                         f"{n}-row problem, max_outer=1 took {t1:.2f}s; full solve extrapolated "
-                         f"as (outer+1) x that = {t1 * (total_outer + 1):.1f}s for "
-                         f"{total_iters} iterations",
-               "threads_note": tnote}
-
-    line = {
-        "metric": "cg_iterations_per_sec", "value": value, "unit": "iter/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic, seeded (np.random.default_rng(0)): x*~U[-1,1], b=A x*, x0=0",
-        "config": {"workload": desc, "n": n, "nnz": nnz, "sigma": sigma, "basis": basis,
-                   "eps_star": eps, "syncs_to_tol": total_outer, "total_iters": total_iters,
-                   "converged": converged, "final_true_rel_resid": rel,
-                   "trace": "fast", "l2": "inputs larger than L2 (each vector "
-                   f"{8 * n / 1e6:.0f} MB, Y {8 * n * (2 * sigma + 1) / 1e9:.2f} GB)",
-                   "problem_gen_s": round(t_gen, 2), "parallelism": f"dp{world} (row slabs)"},
-        "hbm": {"solve_gbs": solve_gbs, "frac_of_measured": solve_gbs / hbm_peak,
-                "frac_of_8tbs": solve_gbs / 8000.0, "algorithmic_bytes_per_solve": solve_bytes},
-        "roofline": {"bound": "hbm",
-                     "kernel": kernel_name(sched) + " " + {
-                         "wavefront": "(wavefront matrix powers + recurrence)",
-                         "pattern": "(pattern-compressed matrix powers + recurrence, "
-                                    f"{sched.get('form')} form)",
-                         "csr": "(CSR matrix powers + recurrence)",
-                         "stencil values": "(value-stream stencil matrix powers + recurrence)"}[sched["kind"]],
-                     "a_bytes_per_level": a_bytes_per_level(n, nnz, sched),
-                     "a_bytes_per_level_csr": a_bytes_per_level(n, nnz, None),
-                     "mpk_schedule": sched,
-                     "achieved": mpk_gbs, "peak": hbm_peak, "peak_kind": peak_kind,
-                     "unit": "GB/s", "frac": mpk_gbs / hbm_peak, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": mpk_bytes / max(1, active * mpk_launches),
-                     "avg_launch_ms": mpk_ms / max(1, active * mpk_launches),
-                     "kernel_ms": {"mpk": pms[0], "gram": pms[1], "small": pms[2],
-                                   "recovery": pms[3], "other": pms[4]},
-                     "small_phases_us_per_call": small_phases,
-                     "kernel_launches": {"mpk": int(pcnt[0]), "gram": int(pcnt[1]),
-                                         "small": int(pcnt[2]), "recovery": int(pcnt[3])},
-                     "share_of_step": {"mpk": pms[0] / max(pms.sum(), 1e-9),
-                                       "gram": pms[1] / max(pms.sum(), 1e-9),
-                                       "small": pms[2] / max(pms.sum(), 1e-9),
-                                       "recovery": pms[3] / max(pms.sum(), 1e-9)}},
-        "e2e": {"value": e2e_value, "unit": "iter/s", "h2d_bytes_per_step": 16 * n,
-                "d2h_bytes_per_step": 8 * n + log_bytes,
-                "note": "adaptive_solve(problem, cfg, trace='fast'); CSR plan cached on the "
-                        "matrix like SparseMatrix._csr"},
-        "cpu_baseline": cpu,
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
-    }
-    print(json.dumps(line))
+def cpu_baseline_sample(prob, cfg_kw, outer, total):
+    """The as-shipped reference (per-iteration diagnostics on, adaptive.py:205-215)
+    on this host: one outer loop with the diagnostics and one without split its
+    time into a per-outer part and a per-iteration diagnostic part; the solve is
+    (outer + 1) x per-outer + total x per-iteration."""
+    t_off, _ = time_outer(prob, cfg_kw, False)
+    t_on, it_on = time_outer(prob, cfg_kw, True)
+    per_it = max(0.0, (t_on - t_off) / it_on)
+    est = t_off * (outer + 1) + per_it * total
+    cores, tnote = cpu_threads()
+    return {"value": total / est, "unit": "iter/s", "cores": cores, "kind": "port",
+            "value_diagnostics_off": total / (t_off * (outer + 1)),
+            "sample": f"oracle/sscg_oracle.py (the reference's numpy/scipy arithmetic) on the "
+                      f"same {prob.a.n}-row problem: one outer loop {t_off:.2f}s without and "
+                      f"{t_on:.2f}s with the per-iteration diagnostics ({it_on} iterations); "
+                      f"solve = {outer}+1 outer loops + {total} iterations = {est:.1f}s",
+            "threads_note": tnote}
 
 
 def run_reference(args, rank, world):
-    """The reference's CPU path (oracle port of its numpy/scipy arithmetic) on
-    this host, same config / metric; rank 0 only."""
+    """The reference's CPU path (oracle port of its numpy/scipy arithmetic, as
+    shipped: per-iteration diagnostics on) on this host, same config / metric;
+    rank 0 only.  A step = one outer loop of it on one slab-sized problem (for
+    c5w the 256^3 slab every rank owns; an outer loop of the global
+    256x256x(256N) problem costs N x that, linear in rows); the value
+    extrapolates to the global solve's counts."""
     if rank != 0:
         return
     from paper_1908_04081_b200 import problems
-    from oracle import sscg_oracle as O
-    key, scale, sigma, basis, eps, desc = CONFIGS[args.config]
-    # One step = one outer loop of the CPU port on ONE slab-sized problem (for
-    # c5w the 256^3 slab every rank owns): the CPU cost of an outer loop of the
-    # global 256x256x(256N) problem is N times that (linear in rows), and the
-    # metric, like ours, counts per-slab iterations summed over the N slabs:
-    # value = N * total_N / ((outer_N + 1) * N * t_slab) = total_N / ((outer_N + 1) t_slab).
-    prob = problems.make_problem(key, scale=args.scale or scale, world=1)
+    key, sigma, basis, eps, scaling, desc = CONFIGS[args.config]
+    prob = problems.make_problem(key, scale=args.scale, world=1)
     cfg_kw = dict(sigma=sigma, eps_star=eps, basis_kind=basis)
-    # outer / total counts of the full global solve (GPU-measured, parity-tested:
-    # tools/measure_counts.py)
-    counts = {}
-    cpath = os.path.join(ROOT, "profiles", "counts.json")
-    if os.path.exists(cpath):
-        counts = json.load(open(cpath)).get(f"{args.config}_w{world}", {})
-    outer = counts.get("outer", 90)
-    total = counts.get("total", 1000)
-    small = problems.make_problem(key, scale=32 if key.startswith("c5") else None, world=1) \
-        if key in ("c5w", "c5", "c3", "c4") else prob
+    counts = reference_counts(args.config, world)
+    if counts is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"no outer/total counts for {args.config} at N={world}"}))
+        return
+    outer, total, src = counts
+    small = problems.make_problem(key, scale=24 if key in ("c5w", "c5", "c3") else 12,
+                                  world=1) if key in ("c5w", "c5", "c3", "c4", "c4j") else prob
     for _ in range(args.warmup):  # warm imports / allocator on a small instance
-        O.solve_problem(small, O.OracleConfig(max_outer=1, **cfg_kw), diagnostics=False)
-    times = []
+        time_outer(small, cfg_kw, True)
+    t_off, _ = time_outer(prob, cfg_kw, False)  # splits a step into per-outer / per-iteration
+    on, its = [], 1
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.solve_problem(prob, O.OracleConfig(max_outer=1, **cfg_kw), diagnostics=False)
-        times.append(time.perf_counter() - t0)
-    t1 = sum(times) / len(times)
-    value = total / (t1 * (outer + 1))
+        t, its = time_outer(prob, cfg_kw, True)
+        on.append(t)
+    t_on = sum(on) / len(on)
+    per_it = max(0.0, (t_on - t_off) / its)
+    # the global problem is N slabs (weak scaling) or the problem itself (strong)
+    slabs = world if scaling == "weak" else 1
+    est = slabs * (t_off * (outer + 1) + per_it * total)
+    units = world if scaling == "weak" else 1
+    value = units * total / est
+    cores, tnote = cpu_threads()
     line = {
         "metric": "cg_iterations_per_sec", "value": value, "unit": "iter/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t1 * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic, seeded", "impl": "reference",
-        "config": {"workload": desc, "n": prob.a.n, "nnz": prob.a.nnz},
-        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cpu_threads()[0], "kind": "port",
-                         "threads_note": cpu_threads()[1],
-                         "sample": f"each step = 1 outer loop of the oracle port on one "
-                                   f"{prob.a.n}-row slab ({t1:.2f}s); the global N={world} "
-                                   f"solve takes {outer}+1 outer loops of N x that; value = "
-                                   f"N x {total} iters / its time (per-slab iterations summed, "
-                                   "as the GPU arm); counts from profiles/counts.json"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_on * 1e3,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, seeded (np.random.default_rng(0))", "impl": "reference",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cores, "kind": "port",
+                         "threads_note": tnote,
+                         "value_diagnostics_off": units * total / (slabs * t_off * (outer + 1)),
+                         "sample": f"each step = one outer loop of the oracle port as shipped "
+                                   f"(diagnostics on) on one {prob.a.n}-row problem "
+                                   f"({t_on:.2f}s, {its} iterations; {t_off:.2f}s without the "
+                                   f"diagnostics); the global N={world} solve = {slabs} x "
+                                   f"({outer}+1 outer loops + {total} iterations) = {est:.1f}s; "
+                                   f"counts: {src}"},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
+# ---------------------------------------------------------------------------
 def run_solver_compare(args):
     """--solver sstep|hscg (one GPU, informational, not the driver's headline):
     the same workload through fixed s-step CG (s = sigma, the config's basis
-    with Ritz-free spectral bounds of the stencil) or Hestenes-Stiefel CG
-    (classic.py: true residual every iteration), device time per solve.
-    `syncs_to_tol` counts the global reductions a multi-GPU run would need:
-    one per outer loop for s-step, two per iteration for HSCG (p.Ap, r.r)."""
+    with the stencil's exact spectral bounds) or Hestenes-Stiefel CG,
+    device time per solve.  `syncs_to_tol` counts the global reductions a
+    multi-GPU run would need: one per outer loop for s-step, two per iteration
+    for HSCG (p.Ap, r.r)."""
     from paper_1908_04081_b200 import _lib as L, problems
     from paper_1908_04081_b200.kernels import _plan
     from paper_1908_04081_b200.sstep import sstep_solve
-    key, scale, sigma, basis, eps, desc = CONFIGS[args.config]
-    prob = problems.make_problem(key, scale=args.scale or scale)
+    key, sigma, basis, eps, scaling, desc = CONFIGS[args.config]
+    prob = problems.make_problem(key, scale=args.scale)
     n = prob.a.n
     plan = _plan(prob.a, 0)
     lib = L.load()
@@ -570,7 +736,7 @@ def run_solver_compare(args):
                 status = {L.CONVERGED: "converged", L.STAGNATED: "stagnated",
                           L.DIVERGED: "diverged"}.get(int(logs.status), "max_iters")
             else:
-                nx = round(n ** (1.0 / 3.0)) if key in ("c3", "c5") else None
+                nx = round(n ** (1.0 / 3.0)) if key in ("c3", "c5", "c5w") else None
                 lam = (6 - 6 * math.cos(math.pi / (nx + 1)), 6 + 6 * math.cos(math.pi / (nx + 1))) \
                     if nx else None
                 info = {}
@@ -587,11 +753,11 @@ def run_solver_compare(args):
     print(json.dumps({
         "metric": "cg_iterations_per_sec", "value": iters / (dev_ms / 1e3), "unit": "iter/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic, seeded", "impl": "ours", "solver": args.solver,
-        "config": {"workload": desc, "n": n, "total_iters": iters, "syncs_to_tol": syncs,
-                   "status": status, "eps_star": eps,
-                   **({"s": args.s or sigma} if args.solver == "sstep" else {})},
+        "config": workload_config(args, 1),
+        "solve": {"n": n, "total_iters": iters, "syncs_to_tol": syncs, "status": status,
+                  **({"s": args.s or sigma} if args.solver == "sstep" else {})},
         "clocks": clk.summary()}))
 
 
@@ -604,20 +770,34 @@ def main():
     ap.add_argument("--scale", type=int, default=None, help="override grid edge (testing)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the secondary (CSR path, value-stream c4j) lines at N=1")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the row-partitioned NCCL path even at one GPU")
     ap.add_argument("--solver", default="adaptive", choices=["adaptive", "sstep", "hscg"],
                     help="adaptive (the headline); sstep / hscg: one-GPU comparison lines")
     ap.add_argument("--s", type=int, default=None, help="fixed s for --solver sstep (default sigma)")
+    ap.add_argument("--check-launch", action="store_true",
+                    help="print this rank's (rank, world) and exit (launcher test)")
     args = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1 and args.impl == "ours":
+        sys.exit(relaunch_under_torchrun(args.gpus))
+    world = int(env_world) if env_world is not None else args.gpus
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.check_launch:
+        print(json.dumps({"rank": rank, "world": world}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
     elif args.solver != "adaptive":
         run_solver_compare(args)
+    elif world > 1 or args.partitioned:
+        run_partitioned(args, rank, world)
     else:
-        run_ours(args, rank, world)
+        run_single(args)
 
 
 if __name__ == "__main__":

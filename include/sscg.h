@@ -228,6 +228,29 @@ int sscg_get_small_phases(const sscg_plan* plan, int64_t* cycles8);
  * q, out[5+2q] tile lag D of pass q.  out: 4+2*SSCG_MAX_SIGMA int32. */
 int sscg_plan_mpk_schedule(sscg_plan* plan, int32_t sigma, int32_t* out);
 
+/* What one outer loop of the plan's captured CUDA graph contains (available
+ * after a solve built it, else -1): out[0] ncclAllReduce calls captured into
+ * it, out[1] grouped NCCL halo exchanges, out[2] NCCL kernel nodes (by device
+ * function name), out[3] kernel nodes, out[4] graph nodes.  A row-partitioned
+ * plan must show exactly one allreduce: the algorithm's one synchronisation
+ * per outer loop (trace.py:60-64, counted at adaptive.py:178). */
+int sscg_plan_collectives(const sscg_plan* plan, int32_t* out5);
+
+/* ---- single-process multi-GPU ------------------------------
+ * The drop-in `adaptive_solve(problem, cfg, devices=[...])`: nplans
+ * row-partitioned plans in ONE process, plan i (rank i) on devices[i] (distinct
+ * GPUs), their NCCL communicators made together by ncclCommInitAll (no
+ * unique-id plumbing; parts[i].nccl_id is ignored).  sscg_group_solve runs
+ * sscg_solve on every plan concurrently, one host thread and one stream per
+ * GPU; b[i] / x_out[i] are rank i's owned rows, x0[i] its local rows, logs[i]
+ * its logs (any may be NULL except b).  Destroy each plan with
+ * sscg_plan_destroy. */
+int sscg_group_create(sscg_plan** plans_out, int32_t nplans, const int32_t* devices,
+                      const sscg_part* parts);
+int sscg_group_solve(sscg_plan* const* plans, int32_t nplans, const sscg_config* cfg,
+                     const double* const* b, const double* const* x0, double* const* x_out,
+                     sscg_logs* const* logs);
+
 /* Hestenes-Stiefel CG on the plan's operator (classic.py:33-104 hscg_solve;
  * single-GPU plans).  Every iteration recomputes the true residual b - A x
  * like the reference; logs->iters rows carry alpha, beta, the Ritz values,

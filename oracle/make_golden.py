@@ -256,6 +256,10 @@ def run_ref(prob, cfg_kwargs, store_x=True):
     )
     if store_x:
         d["x"] = x
+    else:
+        d["x_digest"] = np.array([float(np.sum(x)), float(np.linalg.norm(x))])
+        d["x_head"] = np.asarray(x[:256]).copy()
+    d["final_true"] = np.array(trace.final_true_resid)
     # conds of the first 8 outer loops (ragged -> padded)
     k8 = min(8, len(recs))
     if k8:
@@ -802,6 +806,48 @@ def gen_nos1_counts():
          sstep10=np.array(rows, dtype=float),
          names=np.array(["reference"] + [k for k, v in PERTURBATIONS.items() if v[0] is not None]))
     print(f"    hscg {th.total_iters}; sstep s=10 outer/total {[(int(r[0]), int(r[1])) for r in rows]}")
+
+
+def _full_record(prob, cfg_kwargs, name, keep_outer=5):
+    """Run the reference's adaptive_solve (as shipped, diagnostics on) on a
+    BASELINE config at its full size and keep what the -m gpu tests compare:
+    counts, flags, the per-outer (s_bar, s_tilde, s_actual) records, the first
+    Gram, alphas / betas / Ritz values of every iteration (small: ~1k iters),
+    the final true residual and a checksum of x (x itself is 134 MB at 256^3).
+    The wall time of the reference run is kept too (the as-shipped CPU figure
+    on this 8-core container; bench.py re-times the port on the GPU host)."""
+    d = run_ref(prob, cfg_kwargs, store_x=False)
+    d["keep_outer"] = np.array(keep_outer)
+    d["n"] = np.array(prob.a.n)
+    d["nnz"] = np.array(int(np.asarray(prob.a.row_ptr)[-1]))
+    d["threads"] = np.array(os.cpu_count())
+    save(name, **d)
+
+
+def gen_full():
+    """Full-size reference goldens (pin parity at the headline size).
+
+    c3 128^3 Chebyshev, full run; c4 192^3 Newton and c4j (Jacobi-scaled),
+    max_outer = 5; c5w 256^3 sigma = 12 Newton, full run (~20-30 min here).
+    Selected with FULL=c3,c4,c4j,c5w (default all)."""
+    which = os.environ.get("FULL", "c3,c4,c4j,c5w").split(",")
+    jobs = {
+        "c3": ("c3", dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev")),
+        "c4": ("c4", dict(sigma=10, eps_star=1e-8, basis_kind="newton", max_outer=5)),
+        "c4j": ("c4j", dict(sigma=10, eps_star=1e-8, basis_kind="newton", max_outer=5)),
+        "c5w": ("c5w", dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
+        "c5w2": ("c5w2", dict(sigma=12, eps_star=1e-10, basis_kind="newton", max_outer=5)),
+    }
+    for key in which:
+        cname, kw = jobs[key]
+        t0 = time.perf_counter()
+        if cname == "c5w2":
+            prob = problems.make_problem("c5w", world=2)
+        else:
+            prob = problems.make_problem(cname)
+        print(f"  built {cname} n={prob.a.n} in {time.perf_counter() - t0:.1f}s", flush=True)
+        _full_record(to_ref(prob), kw, f"full_{key}")
+        del prob
 
 
 def main():

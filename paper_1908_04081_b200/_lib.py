@@ -43,6 +43,7 @@ EXPORTS = (
     "sscg_gram", "sscg_recover", "sscg_nested_conds", "sscg_select_s_tilde",
     "sscg_leja_points", "sscg_params_for", "sscg_ritz_sequence", "sscg_sym_eig",
     "sscg_nccl_unique_id", "sscg_plan_create_part", "sscg_vgroup_run",
+    "sscg_plan_collectives", "sscg_group_create", "sscg_group_solve",
 )
 
 
@@ -136,6 +137,11 @@ def _declare(lib):
         "sscg_plan_create_part": (C.c_int, [C.POINTER(vp), i32, C.POINTER(SscgPart)]),
         "sscg_vgroup_run": (C.c_int, [C.POINTER(vp), i32, C.POINTER(SscgConfig),
                                       C.POINTER(_DP), C.POINTER(_DP), C.POINTER(SscgLogs)]),
+        "sscg_plan_collectives": (C.c_int, [vp, _IP]),
+        "sscg_group_create": (C.c_int, [C.POINTER(vp), i32, _IP, C.POINTER(SscgPart)]),
+        "sscg_group_solve": (C.c_int, [C.POINTER(vp), i32, C.POINTER(SscgConfig), C.POINTER(_DP),
+                                       C.POINTER(_DP), C.POINTER(_DP),
+                                       C.POINTER(C.POINTER(SscgLogs))]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -190,6 +196,17 @@ def require_device(device=0):
         raise SscgError(ENODEV, f"no CUDA device {device} ({n} visible); this build has no CPU path")
 
 
+def plan_collectives(lib, handle):
+    """What one outer loop of a plan's captured graph contains
+    (sscg_plan_collectives): allreduce calls, halo exchange groups, NCCL
+    kernel nodes, kernel nodes, graph nodes (-1 before the first solve)."""
+    out = np.zeros(5, dtype=np.int32)
+    check(lib.sscg_plan_collectives(handle, iptr(out)))
+    keys = ("allreduce_per_outer", "halo_exchanges_per_outer", "nccl_kernel_nodes",
+            "kernel_nodes", "graph_nodes")
+    return {k: int(v) for k, v in zip(keys, out)}
+
+
 class Plan:
     """Device copy of one CSR operator (owns the sscg_plan handle)."""
 
@@ -228,20 +245,21 @@ class Plan:
         """Matrix-powers schedule for `sigma` (see `plan_mpk_schedule`)."""
         return plan_mpk_schedule(self._lib, self.handle, sigma)
 
+    def collectives(self):
+        return plan_collectives(self._lib, self.handle)
+
 
 def plan_mpk_schedule(lib, handle, sigma):
     """sscg_plan_mpk_schedule of a plan handle:
-    {"kind": "csr"|"wavefront"|"pattern"|"stencil values", "form": pattern kernel form ("table" walk,
-    "superset" mask, plane "march", row-"pair march", shared-memory "tile march") or None, "wavefront": bool, "ctas": G,
-     "reach_tiles": L (wavefront), "patterns": P (pattern), "passes": [(levels, lag), ...]}."""
+    {"kind": "csr"|"pattern"|"stencil values", "form": pattern kernel form ("table" walk,
+    "superset" mask, plane "march") or None, "ctas": G, "patterns": P (pattern),
+    "slots": union size (stencil values), "passes": [(1, 0)] * sigma (one launch per level)}."""
     out = np.zeros(4 + 2 * 16, dtype=np.int32)
     check(lib.sscg_plan_mpk_schedule(handle, int(sigma), iptr(out)))
     npass = int(out[3])
-    kind = ("csr", "wavefront", "pattern", "stencil values")[int(out[0])]
-    form = (("table", "superset", "march", "pair march", "tile march")[int(out[-1])]
-            if kind == "pattern" else None)
-    return {"kind": kind, "form": form, "wavefront": kind == "wavefront", "ctas": int(out[1]),
-            "reach_tiles": int(out[2]) if kind == "wavefront" else 0,
+    kind = ("csr", "csr", "pattern", "stencil values")[int(out[0])]
+    form = ("table", "superset", "march")[int(out[-1])] if kind == "pattern" else None
+    return {"kind": kind, "form": form, "ctas": int(out[1]),
             "patterns": int(out[2]) if kind == "pattern" else 0,
             "slots": int(out[2]) if kind == "stencil values" else 0,
             "passes": [(int(out[4 + 2 * q]), int(out[5 + 2 * q])) for q in range(npass)]}

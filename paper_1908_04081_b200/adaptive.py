@@ -17,6 +17,7 @@ columns differ as documented on `SolveTrace`.
 from __future__ import annotations
 
 import math
+import warnings
 
 import numpy as np
 
@@ -58,7 +59,7 @@ def make_config(cfg, problem, trace="full"):
     c.basis_kind = L.BASIS[cfg.basis_kind]
     c.c_strategy = L.CSTRAT[cfg.c_strategy]
     c.variant = 1 if cfg.variant == "improved" else 0
-    c.max_outer = int(cfg.max_outer)
+    c.max_outer = clamp_i32(cfg.max_outer)
     c.leja_grid = int(cfg.leja_grid)
     if cfg.spectral_bounds:
         c.has_bounds = 1
@@ -75,13 +76,24 @@ def make_config(cfg, problem, trace="full"):
     return cfg, c
 
 
+INT32_LOOP_MAX = 2**31 - 2
+
+
+def clamp_i32(v):
+    """A loop bound for the ABI's int32 fields: the reference's defaults (e.g.
+    sstep's 100 n / s) can exceed int32 on huge operators; the solve ends on
+    its verdict long before such a bound, so clamping changes nothing."""
+    return int(min(max(int(v), 0), INT32_LOOP_MAX))
+
+
 class LogBuffers:
     """Host arrays the device logs are copied into (caller-owned per the ABI)."""
 
     def __init__(self, cfg):
         sig = cfg.sigma
-        co = min(int(cfg.max_outer) + 2, L.LOG_CAP_OUTER)
-        ci = min((int(cfg.max_outer) + 1) * sig + 1, L.LOG_CAP_ITERS)
+        mo = clamp_i32(cfg.max_outer)
+        co = min(mo + 2, L.LOG_CAP_OUTER)
+        ci = min((mo + 1) * sig + 1, L.LOG_CAP_ITERS)
         self.iters = np.full((ci, L.IT_N), np.nan)
         self.rec_i = np.zeros((co, L.REC_NI), dtype=np.int32)
         self.rec_d = np.full((co, L.RECD_ND), np.nan)
@@ -144,15 +156,61 @@ def build_trace(cfg, logs, trace_level, records=True):
     tr.diverged = s.status == L.DIVERGED
     nt = min(len(logs.outer_true), nrec + 1)
     tr.outer_true_resid = [float(v) for v in logs.outer_true[:nt] if not math.isnan(v)]
+    # the device logs keep at most SSCG_LOG_CAP_ITERS iterations and
+    # SSCG_LOG_CAP_OUTER outer loops; a longer solve is complete but its trace
+    # holds only the first rows -- say so instead of returning it silently
+    tr.truncated = nit < int(s.total_iters) or nrec < int(s.n_records)
+    if tr.truncated:
+        warnings.warn(f"trace truncated: {nit} of {int(s.total_iters)} iterations and {nrec} of "
+                      f"{int(s.n_records)} outer loops logged (device log capacity)",
+                      RuntimeWarning, stacklevel=3)
     return tr, co
 
 
-def adaptive_solve(problem, cfg, *, trace="full", device=0, info=None):
+def _group(a, devices, depth):
+    """Multi-GPU plans cached on the matrix object (like the single plan)."""
+    from .dist import DeviceGroup
+    from .partition import CsrRows
+    key = (tuple(int(d) for d in devices), int(depth))
+    cache = getattr(a, "_sscg_groups", None)
+    if cache is None:
+        cache = {}
+        try:
+            object.__setattr__(a, "_sscg_groups", cache)
+        except Exception:
+            pass
+    grp = cache.get(key)
+    if grp is None:
+        grp = cache[key] = DeviceGroup(CsrRows.of(a), list(devices), depth)
+    return grp
+
+
+def adaptive_solve(problem, cfg, *, trace=None, device=0, devices=None, info=None):
     """Run improved / old adaptive s-step CG on the GPU (adaptive.py:111-268).
 
     Returns (x, SolveTrace, CgCoefficients) like the reference.  `info`, if a
     dict, receives device_ms / outer_launched / first_gram / device logs.
+    `devices=[d0, d1, ...]` (two or more GPUs) row-partitions the operator over
+    them from this one process (one halo exchange and one
+    NCCL allreduce per outer loop); trace defaults to "full" on one GPU
+    (reference semantics) and must be "fast" on several.
     """
+    if devices is not None and len(devices) > 1:
+        trace = "fast" if trace is None else trace
+        if trace != "fast":
+            raise ValueError("a multi-GPU solve records trace='fast' (per-iteration true "
+                             "residuals are a single-GPU diagnostic)")
+        cfg, ccfg = make_config(cfg, problem, trace)
+        a = problem.a
+        if np.asarray(problem.b).shape != (a.n,) or np.asarray(problem.x0).shape != (a.n,):
+            raise ValueError("b / x0 do not match the matrix dimension")
+        grp = _group(a, devices, cfg.sigma)
+        x, tr, co = grp.solve(problem, cfg, info=info)
+        tr.check_consistency()
+        return x, tr, co
+    if devices is not None and len(devices) == 1:
+        device = int(devices[0])
+    trace = "full" if trace is None else trace
     cfg, ccfg = make_config(cfg, problem, trace)
     a = problem.a
     plan = _plan(a, device)

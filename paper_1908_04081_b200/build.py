@@ -86,15 +86,25 @@ def build(force=False, verbose=False, out=None, defines=()):
     objs = []
     base = [cc, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE,
             "-I", nccl_include(), "--expt-relaxed-constexpr"] + ARCH + ["-D" + d for d in defines]
+    cmds = []
     for src in SOURCES:
         obj = os.path.join(OUT_DIR, (os.path.basename(lib_path) + "." if out else "") +
                            src.replace(".cu", ".o"))
-        cmd = base + (["-fmad=false"] if src in NO_FMAD else []) + [
-            "-c", os.path.join(CSRC, src), "-o", obj]
-        if verbose:
-            print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
+        cmds.append(base + (["-fmad=false"] if src in NO_FMAD else []) + [
+            "-c", os.path.join(CSRC, src), "-o", obj])
         objs.append(obj)
+    # translation units compile independently: one nvcc per source, in parallel
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = max(1, min(len(cmds), int(os.environ.get("SSCG_BUILD_JOBS", os.cpu_count() or 1))))
+    with ThreadPoolExecutor(jobs) as ex:
+        for cmd, proc in zip(cmds, ex.map(lambda c: subprocess.run(c, capture_output=True,
+                                                                     text=True), cmds)):
+            if verbose:
+                print(" ".join(cmd))
+                sys.stdout.write(proc.stdout + proc.stderr)
+            if proc.returncode != 0:
+                sys.stderr.write(proc.stdout + proc.stderr)
+                raise subprocess.CalledProcessError(proc.returncode, cmd)
     tmp = lib_path + ".tmp"
     cmd = [cc, "-shared", "-o", tmp] + objs + ARCH + ["-cudart", "static", "-ldl",
                                                        "-Xlinker", "--no-undefined"]

@@ -20,22 +20,20 @@ from .types import CgCoefficients, SolveTrace
 
 
 def assemble_tridiag(coeffs, i):
-    """Lanczos tridiagonal T_i from the first i CG coefficient pairs
-    (classic.py:12-30): T[0,0] = 1/alpha_0, T[l,l] = 1/alpha_l +
-    beta_{l-1}/alpha_{l-1}, T[l-1,l] = T[l,l-1] = sqrt(beta_{l-1})/alpha_{l-1}."""
+    """The Lanczos tridiagonal T_i that the first i CG coefficient pairs define
+    (classic.py:12-30): diagonal 1/alpha_l (+ beta_{l-1}/alpha_{l-1} for
+    l >= 1), off-diagonal sqrt(beta_{l-1})/alpha_{l-1}; built from whole
+    coefficient vectors (the same per-entry operations)."""
     if i < 1:
         raise ValueError("need at least one coefficient pair")
     if i > len(coeffs.alphas):
         raise ValueError(f"only {len(coeffs.alphas)} coefficient pairs stored")
-    al, be = coeffs.alphas, coeffs.betas
-    t = np.zeros((i, i))
-    t[0, 0] = 1.0 / al[0]
-    for l in range(1, i):
-        t[l, l] = 1.0 / al[l] + be[l - 1] / al[l - 1]
-        off = np.sqrt(be[l - 1]) / al[l - 1]
-        t[l - 1, l] = off
-        t[l, l - 1] = off
-    return t
+    al = np.asarray(coeffs.alphas[:i], dtype=float)
+    be = np.asarray(coeffs.betas[:i - 1], dtype=float)
+    diag = 1.0 / al
+    diag[1:] += be / al[:-1]
+    off = np.sqrt(be) / al[:-1]
+    return np.diag(diag) + np.diag(off, 1) + np.diag(off, -1)
 
 
 def hscg_solve(problem, eps_star, max_iters=None, *, device=0, info=None):

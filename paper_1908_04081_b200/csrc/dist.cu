@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <mutex>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -22,6 +23,7 @@ struct NcclApi {
   void* h = nullptr;
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commInitAll)(ncclComm_t*, int, const int*) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
@@ -33,6 +35,9 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 std::mutex g_nccl_mu;
+// collective calls issued (per thread): capture_outer reads the difference
+// across one capture = the collectives in one outer-loop graph
+thread_local long long g_allreduce_calls = 0, g_halo_groups = 0;
 
 template <class F>
 bool sym(void* h, const char* name, F& f) {
@@ -104,7 +109,7 @@ int nccl_load(const char* path) {
             sym(h, "ncclCommDestroy", a.commDestroy) && sym(h, "ncclAllReduce", a.allReduce) &&
             sym(h, "ncclSend", a.send) && sym(h, "ncclRecv", a.recv) &&
             sym(h, "ncclGroupStart", a.groupStart) && sym(h, "ncclGroupEnd", a.groupEnd) &&
-            sym(h, "ncclGetErrorString", a.errorString);
+            sym(h, "ncclGetErrorString", a.errorString) && sym(h, "ncclCommInitAll", a.commInitAll);
   if (!ok) return sscg_fail(SSCG_EINVAL, "NCCL library %s lacks a required symbol", p);
   g_nccl = a;
   return SSCG_OK;
@@ -133,6 +138,21 @@ int nccl_comm_init(void** comm, const unsigned char* id128, int rank, int world)
   if (rc) return rc;
   *comm = c;
   return SSCG_OK;
+}
+
+// one communicator per device of a single-process group (ncclCommInitAll:
+// rank i on devs[i]; the devices must be distinct)
+int nccl_comm_init_all(void** comms, int n, const int* devs) {
+  std::vector<ncclComm_t> c((size_t)n, nullptr);
+  int rc = nccl_check(g_nccl.commInitAll(c.data(), n, devs), "ncclCommInitAll");
+  if (rc) return rc;
+  for (int i = 0; i < n; ++i) comms[i] = c[(size_t)i];
+  return SSCG_OK;
+}
+
+void collective_counts(long long* allreduce, long long* halo) {
+  *allreduce = g_allreduce_calls;
+  *halo = g_halo_groups;
 }
 
 void nccl_comm_destroy(void* comm) {
@@ -169,6 +189,7 @@ int halo_exchange(const HaloPlan& h, const Ctx& c, void* comm, cudaStream_t s) {
     }
     rc = nccl_check(g_nccl.groupEnd(), "ncclGroupEnd");
     if (rc) return rc;
+    ++g_halo_groups;
   }
   return SSCG_OK;
 }
@@ -184,6 +205,7 @@ void halo_unpack(const HaloPlan& h, const Ctx& c, cudaStream_t s) {
 
 int nccl_allreduce(void* comm, double* buf, int64_t count, cudaStream_t s) {
   if (!comm) return SSCG_OK;
+  ++g_allreduce_calls;
   return nccl_check(g_nccl.allReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum,
                                      static_cast<ncclComm_t>(comm), s),
                     "ncclAllReduce");

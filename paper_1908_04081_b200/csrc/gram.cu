@@ -301,13 +301,13 @@ constexpr size_t gram_smem() {
 
 template <int NB, int REM>
 void set_attr() {
-  static bool done = false;
-  if (!done) {
+  static std::atomic<unsigned long long> done{0};  // per device
+  if (first_use_on_device(done)) {
     cudaFuncSetAttribute(k_gram_state<NB, REM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)gram_smem<NB, REM>());
     cudaFuncSetAttribute(k_gram_raw<NB, REM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)gram_smem<NB, REM>());
-    done = true;
+    mark_device_done(done);
   }
 }
 

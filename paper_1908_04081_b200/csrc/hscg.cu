@@ -80,7 +80,9 @@ __device__ __forceinline__ double* hs_log(const Ctx& c, int64_t it) {
 __device__ void hs_classify(SolverState* st, const DevConfig& cf, double true_rel, double r_norm) {
   const int i = st->total_iters;
   int out = SSCG_RUNNING;
-  if (true_rel <= cf.eps_star) {
+  if ((int64_t)i >= cf.max_iters) {
+    out = SSCG_EXHAUSTED;  // `while i < max_iters` exits before any verdict
+  } else if (true_rel <= cf.eps_star) {
     out = SSCG_CONVERGED;
   } else if (!isfinite(true_rel) || true_rel > 1e5) {
     out = SSCG_DIVERGED;
@@ -90,7 +92,6 @@ __device__ void hs_classify(SolverState* st, const DevConfig& cf, double true_re
   } else if (i - st->best_iter >= 200 && r_norm <= 0.01 * true_rel * st->nb) {
     out = SSCG_STAGNATED;
   }
-  if (out == SSCG_RUNNING && (int64_t)i >= cf.max_iters) out = SSCG_EXHAUSTED;  // while i < max_iters
   if (out != SSCG_RUNNING) {
     st->status = out;
     st->done = 1;

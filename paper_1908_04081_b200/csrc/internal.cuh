@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/sscg.h"
 
 #define SMAX SSCG_MAX_SIGMA   // 16
@@ -30,8 +32,6 @@
 #ifndef MT_STAGES
 #define MT_STAGES 2                 // TMA double buffering of CSR tiles
 #endif
-#define WAVE_GROUP 4                // tiles per completion counter (wavefront MPK)
-#define WAVE_THREADS (MT_ROWS + 32) // 8 consumer warps + 1 producer warp
 #define GRAM_BLOCKS (2 * NUM_SMS)  // capacity of the Gram partials
 #define SMALL_THREADS 512
 #define SS_MAX_NE 8                // union size of the unrolled superset-mask pattern kernels
@@ -136,8 +136,6 @@ struct Ctx {
   int pid_bytes;     // 1 (<= 256 patterns) or 2
   int pat_np, pat_ne;
   int pat_grid;      // CTAs of the pattern kernels of levels >= 1 (level 0: red_n)
-  int win_r;         // windowed pattern kernels: near radius R (-1: not used)
-  int win_grid;      // CTAs of the windowed kernels of levels >= 1
   const int* pat_ptr;
   const int* pat_off;
   const double* pat_val;
@@ -154,6 +152,18 @@ struct Ctx {
   int vs_ne;
   int vs_off[VS_MAX_NE];
   const double* vs_val;
+  // a row-partitioned value stream (vs_S > 0): local rows are whole global
+  // planes of vs_S rows in a permuted order, so a slot's neighbour is found
+  // through plane tables, not by adding the offset: union offset k = vs_dz[k]
+  // planes + vs_r[k] rows within the plane; local block b of vs_S rows is
+  // geometric plane vs_geo[b]; geometric plane z starts at local row
+  // vs_base[z] (-1: not held; only absent slots can point there)
+  int64_t vs_S;
+  int vs_np;
+  signed char vs_dz[VS_MAX_NE];
+  int vs_r[VS_MAX_NE];
+  const int* vs_geo;
+  const int* vs_base;
   int ss_ne;
   int ss_off[SS_MAX_NE];
   int hs_ss;         // HSCG row sums through the superset mask (SSCG_HS_SS)
@@ -170,13 +180,8 @@ struct Ctx {
   int64_t zm_items;  // work items = zm_ncb x ceil(steps / zm_zc)
   int zm_np;         // planes of the walk
   unsigned* zm_ctr;  // [2 (SMAX + 1)] per-level claim / done counters (levels >= 1), or NULL
-  int zm_split;      // level 0 without the true residual; k_resid_zm computes it (side branch)
   const int* zm_base;  // [zm_np] first local row of each plane (partitioned), or NULL (z * S)
   int zm_o;          // 2-D column tiles with line stride zm_o (0: 256 consecutive columns)
-  int zt_on;         // levels >= 1 by the shared-memory tile march (k_level_zt; needs zm_o)
-  int zm_pair;       // levels >= 1 by the row-pair march (k_level_zp; zm_items in pairs)
-  int zp_grid;       // CTAs of k_level_zp
-  int64_t zp_items;  // its work items (512 columns each)
   int pf_off;    // pattern kernels: L2 prefetch at row + pf_ahead * stride + pf_off (0: off)
   int pf_ahead;
   const unsigned* ss_mask;  // [pat_np]
@@ -192,17 +197,6 @@ __host__ __device__ inline int64_t lvl_r_rows(const Ctx& c, int sigma, int l) {
   const int d = sigma - 2 - l;
   return c.lvl_rows[d < 0 ? 0 : d];
 }
-
-// one pass of the wavefront matrix-powers kernel (mpk.cu k_mpk_wave)
-struct WaveArgs {
-  int l0, nl;         // levels l0 .. l0+nl-1
-  int D;              // tile lag between consecutive levels
-  int ngroups;        // counters per level
-  int64_t nF;         // wavefront steps: tiles(l0) + (nl - 1) D
-  int* cnt;           // [SMAX][ngroups] finished tiles per WAVE_GROUP tiles
-  unsigned int* claim;  // position counter of this pass
-  const int2* dep;    // [tiles] monotone input-tile range of each row tile
-};
 
 // halo exchange lists of a row-partitioned plan (dist.cu)
 struct HaloPlan {
@@ -222,6 +216,24 @@ struct HaloPlan {
   int r_col = 0;                // physical column of R_0 (sigma + 1) of the current run
 };
 
+// Kernel attributes (dynamic shared-memory ceilings) are per device: a
+// process that drives several GPUs (adaptive_solve(device=k), the
+// single-process multi-GPU group) must set them on each.  Returns true the
+// first time it is called for the current device with this mask (the caller
+// then sets its attributes); concurrent callers may both see true (setting an
+// attribute twice is harmless).
+inline bool first_use_on_device(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  return (mask.load(std::memory_order_acquire) & bit) == 0;
+}
+inline void mark_device_done(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  mask.fetch_or(1ull << (dev & 63), std::memory_order_release);
+}
+
 #define CUDA_OK(expr)                                             \
   do {                                                            \
     cudaError_t e__ = (expr);                                     \
@@ -234,8 +246,7 @@ int sscg_fail(int code, const char* fmt, ...);
 // ---- launchers (defined in the .cu files) ----
 // mpk.cu
 void launch_init_residual(const Ctx& c, const double* x0, cudaStream_t s);
-void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s, bool with_resid = true);
-void launch_resid(const Ctx& c, int sigma, cudaStream_t s);
+void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s);
 void launch_spmv(const int* rp, const int* col, const double* val, int64_t n, const double* x,
                  double* y, cudaStream_t s);
 void launch_block_levels(const int* rp, const int* col, const double* val, int64_t n, int64_t ld,
@@ -244,19 +255,14 @@ void launch_block_levels(const int* rp, const int* col, const double* val, int64
 void launch_diag_resid(const Ctx& c, int j, cudaStream_t s);
 size_t staged_smem_bytes(int cap);
 size_t pattern_smem_bytes(int np, int ne);
-size_t window_smem_bytes(int np, int ne, int r, int nvw, int pid_bytes);
-int window_ctas_per_sm(int np, int ne, int r, int pid_bytes, int* out2);
 void pattern_prepare();
 int pattern_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 size_t ss_smem_bytes(int np);
 int ss_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 int zm_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
-int zp_ctas_per_sm(int np, int ne, int pid_bytes);
 int vs_ctas_per_sm(int ne, int* out2);
 void staged_prepare(int cap);
 int staged_ctas_per_sm(int cap);
-int wave_ctas_per_sm(int cap);
-cudaError_t launch_wave(const Ctx& c, const WaveArgs& a, int grid, cudaStream_t s);
 // gram.cu (ld must be a multiple of gram_row_multiple(); padding rows zero)
 int gram_row_multiple();
 void launch_gram(const Ctx& c, int ncols, cudaStream_t s);
@@ -287,6 +293,8 @@ int nccl_load(const char* path);
 int nccl_unique_id(const char* path, unsigned char* id128);
 int nccl_comm_init(void** comm, const unsigned char* id128, int rank, int world);
 void nccl_comm_destroy(void* comm);
+int nccl_comm_init_all(void** comms, int n, const int* devs);
+void collective_counts(long long* allreduce, long long* halo);
 int halo_exchange(const HaloPlan& h, const Ctx& c, void* comm, cudaStream_t s);
 void halo_unpack(const HaloPlan& h, const Ctx& c, cudaStream_t s);
 int nccl_allreduce(void* comm, double* buf, int64_t count, cudaStream_t s);

@@ -86,11 +86,12 @@ struct sscg_plan {
   cudaEvent_t ev_fork = nullptr;
   int leja_after0 = 1;  // the head chain forks after level 0
   int hs_ss = 1;        // HSCG row sums through the superset mask
-  cudaStream_t side2 = nullptr;  // true-residual branch (split level 0)
-  cudaEvent_t ev_rfork = nullptr, ev_rjoin = nullptr;
   cudaEvent_t ev_leja[SMAX] = {};
   cudaGraphExec_t gexec = nullptr;
   int g_sigma = -1, g_full = -1;
+  // census of the outer-loop graph last built: [0] ncclAllReduce calls, [1]
+  // grouped halo exchanges, [2] NCCL kernel nodes, [3] kernel nodes, [4] nodes
+  int census[5] = {-1, -1, -1, -1, -1};
   int* h_done = nullptr;  // pinned [2]
   cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
@@ -122,22 +123,10 @@ struct sscg_plan {
   // sscg_set_basis_params (fixed s-step solver)
   int fixed_s = 0;
   double fixed_th[SMAX] = {}, fixed_ga[SMAX] = {}, fixed_mu[SMAX] = {};
-  // wavefront matrix-powers kernel (k_mpk_wave)
-  int wave_on = 0;
-  int wave_grid = 0;
-  int64_t wave_tiles = 0;
-  int wave_lhi = 0;        // max over tiles of (last input tile - tile)
-  double wave_row_bytes = 0.0;  // CSR bytes per row
-  int2* d_wdep = nullptr;
-  int* d_wcnt = nullptr;
-  int wave_ngroups = 0;
-  std::vector<WaveArgs> wave_passes;
-  int wave_sigma = -1;
   // pattern-compressed operator (pattern_setup)
   void* d_pid = nullptr;
   int pid_bytes = 0;
   int pat_np = 0, pat_ne = 0, pat_grid = 0;
-  int win_r = -1, win_grid = 0;
   int* d_pat_ptr = nullptr;
   int* d_pat_off = nullptr;
   double* d_pat_val = nullptr;
@@ -146,10 +135,8 @@ struct sscg_plan {
   int zm_np = 0;
   int* d_zm_base = nullptr;  // plane table of a partitioned march
   unsigned* d_zm_ctr = nullptr;  // dynamic item counters of the level kernels
-  int zm_zc = 0, zm_ncb = 0, zm_o = 0, zm_pair = 0, zp_grid = 0, zt_on = 0, zm_zc0 = 0;
+  int zm_zc = 0, zm_ncb = 0, zm_o = 0, zm_zc0 = 0;
   int64_t zm_items0 = 0;
-  int zm_split = 0;
-  int64_t zp_items = 0;
   int64_t zm_items = 0;
   // host <-> device staging of the solve's vectors (copy_h2d / copy_d2h):
   // per copy thread two pinned chunks, a stream and two events
@@ -161,6 +148,12 @@ struct sscg_plan {
   int vs_ne = 0;  // value-stream stencil form (vs_setup); 0: not used
   int vs_off[VS_MAX_NE] = {};
   double* d_vs_val = nullptr;
+  int64_t vs_S = 0;  // partitioned value stream: plane size (0: plain offsets)
+  int vs_np = 0;
+  signed char vs_dz[VS_MAX_NE] = {};
+  int vs_r[VS_MAX_NE] = {};
+  int* d_vs_geo = nullptr;
+  int* d_vs_base = nullptr;
   int ss_ne = 0;  // superset-mask form (superset_setup); 0: table-walking kernels
   int ss_off[SS_MAX_NE] = {};
   unsigned* d_ss_mask = nullptr;
@@ -272,8 +265,6 @@ Ctx make_ctx(sscg_plan* p) {
   c.pat_np = p->pat_np;
   c.pat_ne = p->pat_ne;
   c.pat_grid = p->pat_grid;
-  c.win_r = p->win_r;
-  c.win_grid = p->win_grid;
   c.pat_ptr = p->d_pat_ptr;
   c.pat_off = p->d_pat_off;
   c.pat_val = p->d_pat_val;
@@ -289,14 +280,17 @@ Ctx make_ctx(sscg_plan* p) {
   c.zm_base = p->d_zm_base;
   c.zm_ctr = p->d_zm_ctr;
   c.zm_o = p->zm_o;
-  c.zm_pair = p->zm_pair;
-  c.zm_split = p->zm_split;
-  c.zt_on = p->zt_on;
-  c.zp_grid = p->zp_grid;
-  c.zp_items = p->zp_items;
   c.vs_ne = p->vs_ne;
   for (int k = 0; k < VS_MAX_NE; ++k) c.vs_off[k] = p->vs_off[k];
   c.vs_val = p->d_vs_val;
+  c.vs_S = p->vs_S;
+  c.vs_np = p->vs_np;
+  for (int k = 0; k < VS_MAX_NE; ++k) {
+    c.vs_dz[k] = p->vs_dz[k];
+    c.vs_r[k] = p->vs_r[k];
+  }
+  c.vs_geo = p->d_vs_geo;
+  c.vs_base = p->d_vs_base;
   c.ss_ne = p->ss_ne;
   c.hs_ss = p->hs_ss;
   for (int k = 0; k < SS_MAX_NE; ++k) c.ss_off[k] = p->ss_off[k];
@@ -325,8 +319,7 @@ int check_config(const sscg_config* c) {
   return SSCG_OK;
 }
 
-int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s, bool with_resid = true);
-void wave_plan_passes(sscg_plan* p, int sigma);
+int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s);
 
 // Next-block parameters (k_params_begin + Leja points 2..sigma-1) need only the
 // Ritz state K_small just updated, so they run on a side branch beside the
@@ -347,16 +340,7 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     TRY(halo_exchange(p->halo, c, p->comm, s));
     halo_unpack(p->halo, c, s);
   }
-  // split level 0: the true residual (x, b only) on its own branch beside the
-  // levels, joined before the Gram kernel packs the norms
-  const bool side_resid = c.zm_split != 0;
-  if (side_resid) {
-    cudaEventRecord(p->ev_rfork, s);
-    cudaStreamWaitEvent(p->side2, p->ev_rfork, 0);
-    launch_resid(c, sigma, p->side2);
-    cudaEventRecord(p->ev_rjoin, p->side2);
-  }
-  if (p->leja_head && !p->wave_on) {
+  if (p->leja_head) {
     // small operators: the recovery is too short to hide the Leja chain, so the
     // chain starts the outer loop on a side branch and level l (l >= 2) joins
     // point l only -- the levels run as the shifts arrive
@@ -366,7 +350,7 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     // holding one of its SM slots would delay it; level 1 (lambda_min) needs
     // no Leja point, and point 2 (42 us) is ready long before level 2
     const bool after0 = p->leja_after0 && sigma > 1;
-    if (after0) launch_level(c, 0, sigma, s, !side_resid);
+    if (after0) launch_level(c, 0, sigma, s);
     cudaEventRecord(p->ev_fork, s);
     cudaStreamWaitEvent(p->side, p->ev_fork, 0);
     for (int n = 2; n < sigma; ++n) {
@@ -375,19 +359,18 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     }
     for (int l = after0 ? 1 : 0; l < sigma; ++l) {
       if (l >= 2) cudaStreamWaitEvent(s, p->ev_leja[l], 0);
-      launch_level(c, l, sigma, s, !side_resid);
+      launch_level(c, l, sigma, s);
     }
   } else {
-    TRY(launch_mpk(p, c, sigma, s, !side_resid));
+    TRY(launch_mpk(p, c, sigma, s));
   }
-  if (side_resid) cudaStreamWaitEvent(s, p->ev_rjoin, 0);
   launch_gram(c, 2 * sigma + 1, s);
   if (p->comm) {  // the one synchronisation of the outer loop
     const int k = 2 * sigma + 1;
     TRY(nccl_allreduce(p->comm, c.red_buf, (int64_t)k * (k + 1) / 2 + 2, s));
   }
   launch_small(c, s);
-  const bool tail = !(p->leja_head && !p->wave_on);
+  const bool tail = !p->leja_head;
   if (tail) capture_params_branch(p, c, sigma, s);
   if (full) {
     for (int j = 0; j < sigma; ++j) {
@@ -401,6 +384,30 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
   return SSCG_OK;
 }
 
+// what the captured outer-loop graph contains: kernel nodes, and among them
+// NCCL's (by device-function name) -- the collectives one outer loop issues,
+// read back from the graph itself
+void graph_census(cudaGraph_t g, int* census) {
+  size_t nn = 0;
+  census[2] = census[3] = census[4] = 0;
+  if (cudaGraphGetNodes(g, nullptr, &nn) != cudaSuccess) return;
+  std::vector<cudaGraphNode_t> nodes(nn);
+  if (nn && cudaGraphGetNodes(g, nodes.data(), &nn) != cudaSuccess) return;
+  census[4] = (int)nn;
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+    ++census[3];
+    cudaKernelNodeParams kp;
+    const char* name = nullptr;
+    if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func &&
+        cudaFuncGetName(&name, kp.func) == cudaSuccess && name &&
+        (strstr(name, "nccl") || strstr(name, "NCCL")))
+      ++census[2];
+  }
+  cudaGetLastError();  // a kernel of another library may not resolve by name
+}
+
 int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
   if (p->gexec && p->g_sigma == sigma && p->g_full == full) return SSCG_OK;
   if (p->gexec) {
@@ -408,6 +415,8 @@ int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
     p->gexec = nullptr;
   }
   cudaGraph_t g = nullptr;
+  long long ar0, halo0, ar1, halo1;
+  collective_counts(&ar0, &halo0);
   CUDA_OK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
   const int crc = capture_outer(p, c, sigma, full, p->stream);
   cudaError_t e = cudaStreamEndCapture(p->stream, &g);
@@ -416,6 +425,10 @@ int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
     return crc;
   }
   if (e != cudaSuccess) return sscg_fail_cuda(e, "cudaStreamEndCapture");
+  collective_counts(&ar1, &halo1);
+  p->census[0] = (int)(ar1 - ar0);
+  p->census[1] = (int)(halo1 - halo0);
+  graph_census(g, p->census);
   e = cudaGraphInstantiate(&p->gexec, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return sscg_fail_cuda(e, "cudaGraphInstantiate");
@@ -551,9 +564,6 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   CUDA_OK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   CUDA_OK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
   CUDA_OK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
-  CUDA_OK(cudaStreamCreateWithFlags(&p->side2, cudaStreamNonBlocking));
-  CUDA_OK(cudaEventCreateWithFlags(&p->ev_rfork, cudaEventDisableTiming));
-  CUDA_OK(cudaEventCreateWithFlags(&p->ev_rjoin, cudaEventDisableTiming));
   for (int i = 0; i < SMAX; ++i) CUDA_OK(cudaEventCreateWithFlags(&p->ev_leja[i], cudaEventDisableTiming));
   CUDA_OK(cudaHostAlloc((void**)&p->h_done, 2 * sizeof(int), cudaHostAllocDefault));
   for (auto* ev : {&p->ev_chunk[0], &p->ev_chunk[1]})
@@ -613,7 +623,6 @@ const char* env_or(const char* name, const char* dflt) {
 // entry.  Used when the table is small (shared memory, 1-2 byte ids);
 // otherwise the CSR kernels run.  SSCG_PATTERN=0 disables it (A/B tests).
 constexpr int PAT_MAX_BYTES = 16 * 1024;
-constexpr int WIN_R_CAP = 512;  // near columns: within 512 rows (window <= 1280 rows per vector)
 
 // Pattern table of the rows: offset(row, col) is col - row (local indices) or,
 // for a row-partitioned plan that passes its rows' global indices, grows[col] -
@@ -863,37 +872,6 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
         p->zm_zc0 = (int)(z0env > 0 ? z0env : zb);
         p->zm_items0 = ncb * ((steps + p->zm_zc0 - 1) / p->zm_zc0);
       }
-      // level 0 split: P/R at the levels' cost, the true residual beside them
-      // (opt-in: measured 218.4 vs 215.9 ms per c5w solve -- the side branch
-      // takes SM slots from the latency-bound levels rather than idle HBM)
-      p->zm_split = atoi(env_or("SSCG_ZM_SPLIT", "0")) != 0;
-      // shared-memory tile march for the 2-D tiled 7-slot form: whole 32 x 8
-      // tiles (o a multiple of 32, lines per plane a multiple of 8)
-      // (opt-in: the per-plane barrier makes it slower than the register march)
-      p->zt_on = o > 0 && (S / o) % 8 == 0 && bases.empty() && atoi(env_or("SSCG_ZT", "0")) != 0;
-      // row pairs (levels >= 1): unions [-S, -1, 0, 1, S] or [-S, -o, -1, 0, 1, o, S]
-      // with S and o even (every even-offset pair load 16-byte aligned)
-      p->zm_pair = 0;
-      const bool pair_shape =
-          (ne == 5 && p->ss_off[1] == -1 && p->ss_off[3] == 1) ||
-          (ne == 7 && p->ss_off[2] == -1 && p->ss_off[4] == 1 && p->ss_off[5] % 2 == 0);
-      // opt-in: 124 registers, 2 CTAs/SM -- measured slower than the single march
-      if (pair_shape && S % 2 == 0 && bases.empty() && atoi(env_or("SSCG_ZM_PAIR", "0")) != 0) {
-        const int occ = zp_ctas_per_sm(np, ne, p->pid_bytes);
-        if (occ >= 1) {
-          const int64_t ncb2 = (S + 2 * ROWS_PER_CTA - 1) / (2 * ROWS_PER_CTA);
-          const int64_t g2 = (int64_t)sms * occ;
-          int64_t zc2 = atoi(env_or("SSCG_ZM_ZC", "0"));
-          if (zc2 <= 0) zc2 = std::max<int64_t>(2, std::min<int64_t>(16, ncb2 * steps / (4 * g2)));
-          if (zc2 != zc) {  // one step count for both kernels: keep the pair choice
-            p->zm_zc = (int)zc2;
-            p->zm_items = ncb * ((steps + zc2 - 1) / zc2);
-          }
-          p->zp_items = ncb2 * ((steps + zc2 - 1) / zc2);
-          p->zp_grid = (int)std::max<int64_t>(1, std::min<int64_t>(g2, p->zp_items));
-          p->zm_pair = 1;
-        }
-      }
       p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * zocc[0], (int64_t)RED_BLOCKS, p->zm_items0}));
       p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, p->zm_items));
     }
@@ -905,39 +883,32 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
     p->ss_ne = 0;
     return SSCG_OK;
   }
-  // windowed kernels: near radius = the largest |offset| up to WIN_R_CAP (even)
-  p->win_r = -1;
-  if (atoi(env_or("SSCG_PAT_WIN", "0")) != 0) {  // opt-in: measured slower, DESIGN.md 4b
-    int r = 0;
-    for (int v : off)
-      if (std::abs(v) <= WIN_R_CAP) r = std::max(r, std::abs(v));
-    r = (r + 1) & ~1;
-    int wocc[2] = {0, 0};
-    window_ctas_per_sm(np, ne, r, p->pid_bytes, wocc);
-    if (wocc[0] >= 1 && wocc[1] >= 1) {
-      p->win_r = r;
-      p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * wocc[0], (int64_t)RED_BLOCKS, tiles}));
-      p->win_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * wocc[1], tiles));
-    }
-  }
   return SSCG_OK;
 }
 
-// Value-stream stencil form (single-GPU plans whose rows do not compress to
-// patterns): every row's column offsets, in stored order, are a strictly
+// Value-stream stencil form for operators whose rows do not compress to
+// patterns: every row's column offsets, in stored order, are a strictly
 // increasing subsequence of a union of 3..32 offsets -- a stencil's structure
 // with row-varying values (c4).  Values go slot-major [k][ld] (absent 0.0).
+// A row-partitioned plan passes its rows' global indices: offsets are then
+// global, and the local rows must be whole global planes (plane tables; the
+// plane size S is the union offset for which they are, with every offset
+// decomposing into dz planes + |r| < S / 2 rows).
 int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
-             const double* values) {
+             const double* values, const int64_t* grows = nullptr, int64_t n_local = 0) {
   p->vs_ne = 0;
+  p->vs_S = 0;
   // SSCG_PATTERN=0 forces the CSR kernels (A/B reference), SSCG_VS=0 this form only
   if (atoi(env_or("SSCG_VS", "1")) == 0 || atoi(env_or("SSCG_PATTERN", "1")) == 0 || n < 1)
     return SSCG_OK;
+  auto ofs = [&](int64_t i, int64_t j) -> int64_t {
+    return grows ? grows[col_idx[j]] - grows[i] : (int64_t)col_idx[j] - i;
+  };
   std::vector<int64_t> uni;
   for (int64_t i = 0; i < n; ++i) {
     int64_t prev = INT64_MIN;
     for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; ++j) {
-      const int64_t o = (int64_t)col_idx[j] - i;
+      const int64_t o = ofs(i, j);
       if (o <= prev) return SSCG_OK;  // unsorted row
       prev = o;
       auto it = std::lower_bound(uni.begin(), uni.end(), o);
@@ -950,19 +921,56 @@ int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col
   const int ne = (int)uni.size();
   int occ[2] = {0, 0};
   if (ne < 3 || vs_ctas_per_sm(ne, occ) < 1) return SSCG_OK;
+  std::vector<int> geo, base;
+  if (grows) {  // plane tables of the partitioned form
+    int64_t S = 0;
+    std::vector<int> bases;
+    for (int64_t cand : uni) {
+      if (cand <= 0 || cand < S) continue;
+      bool dec = true;
+      for (int64_t o : uni) {
+        const int64_t dz = (o >= 0 ? o + cand / 2 : o - cand / 2) / cand, r = o - dz * cand;
+        dec = dec && 2 * std::llabs(r) < cand && std::llabs(dz) <= 127;
+      }
+      if (!dec) continue;
+      std::vector<int> b = plane_bases(n_local, grows, cand);
+      if (!b.empty()) {
+        S = cand;
+        bases.swap(b);
+      }
+    }
+    if (S == 0 || (int64_t)bases.size() * S != n_local) return SSCG_OK;
+    p->vs_S = S;
+    p->vs_np = (int)bases.size();
+    base = bases;
+    geo.assign(bases.size(), -1);
+    for (size_t z = 0; z < bases.size(); ++z) geo[(size_t)(bases[z] / S)] = (int)z;
+    for (int k = 0; k < ne; ++k) {
+      const int64_t o = uni[(size_t)k];
+      const int64_t dz = (o >= 0 ? o + S / 2 : o - S / 2) / S;
+      p->vs_dz[k] = (signed char)dz;
+      p->vs_r[k] = (int)(o - dz * S);
+    }
+  }
   std::vector<double> sv((size_t)ne * (size_t)p->ld, 0.0);
   for (int64_t i = 0; i < n; ++i) {
     int k = 0;
     for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; ++j) {
-      const int64_t o = (int64_t)col_idx[j] - i;
+      const int64_t o = ofs(i, j);
       while (uni[(size_t)k] != o) ++k;  // rows are sorted subsequences of uni
       sv[(size_t)k * (size_t)p->ld + (size_t)i] = values[j];
     }
   }
+  if (grows) {
+    TRY(dalloc(p, &p->d_vs_geo, geo.size()));
+    TRY(dalloc(p, &p->d_vs_base, base.size()));
+    CUDA_OK(cudaMemcpy(p->d_vs_geo, geo.data(), 4 * geo.size(), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(p->d_vs_base, base.data(), 4 * base.size(), cudaMemcpyHostToDevice));
+  }
   TRY(dalloc(p, &p->d_vs_val, sv.size()));
   CUDA_OK(cudaMemcpy(p->d_vs_val, sv.data(), 8 * sv.size(), cudaMemcpyHostToDevice));
   p->vs_ne = ne;
-  for (int k = 0; k < VS_MAX_NE; ++k) p->vs_off[k] = k < ne ? (int)uni[(size_t)k] : 0;
+  for (int k = 0; k < VS_MAX_NE; ++k) p->vs_off[k] = k < ne ? (int)uni[(size_t)k] : 0;  // (plain form)
   int sms = NUM_SMS;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
   const int64_t tiles = (n + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
@@ -971,101 +979,9 @@ int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col
   return SSCG_OK;
 }
 
-// Wavefront MPK setup (single-GPU plans with staged tiles): per row tile the
-// range of input tiles its columns touch, made monotone (suffix min of lo,
-// prefix max of hi) so a CTA's dependency checks only move forward.
-int wave_setup(sscg_plan* p, const int64_t* row_ptr, const int32_t* col_idx) {
-  p->wave_on = 0;
-  // opt-in (SSCG_WAVE=1): correct and bit-identical, but on B200 today slower
-  // than one launch per level -- see DESIGN.md "wavefront experiment"
-  if (p->stage_cap <= 0 || p->partitioned || atoi(env_or("SSCG_WAVE", "0")) == 0) return SSCG_OK;
-  const int64_t n = p->n, nt = (n + MT_ROWS - 1) / MT_ROWS;
-  std::vector<int2> dep(nt);
-  for (int64_t t = 0; t < nt; ++t) {
-    const int64_t r0 = t * MT_ROWS, r1 = std::min<int64_t>(n, r0 + MT_ROWS);
-    int64_t lo = t, hi = t;
-    for (int64_t j = row_ptr[r0]; j < row_ptr[r1]; ++j) {
-      const int64_t ct = col_idx[j] / MT_ROWS;
-      lo = std::min(lo, ct);
-      hi = std::max(hi, ct);
-    }
-    dep[t] = make_int2((int)lo, (int)hi);
-  }
-  for (int64_t t = nt - 2; t >= 0; --t) dep[t].x = std::min(dep[t].x, dep[t + 1].x);
-  int64_t lhi = 0;
-  for (int64_t t = 0; t < nt; ++t) {
-    if (t) dep[t].y = std::max(dep[t].y, dep[t - 1].y);
-    lhi = std::max<int64_t>(lhi, dep[t].y - t);
-  }
-  int sms = NUM_SMS;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-  int per_sm = wave_ctas_per_sm(p->stage_cap);
-  const int want = atoi(env_or("SSCG_WAVE_CTAS", "0"));
-  if (want > 0 && want < per_sm) per_sm = want;
-  if (per_sm < 1) return SSCG_OK;
-  p->wave_grid = (int)std::min<int64_t>((int64_t)sms * per_sm, p->red_n);
-  p->wave_tiles = nt;
-  p->wave_lhi = (int)lhi;
-  p->wave_row_bytes = (12.0 * (double)p->nnz + 4.0 * (double)n) / (double)n;
-  p->wave_ngroups = (int)((nt + WAVE_GROUP - 1) / WAVE_GROUP);
-  TRY(dalloc(p, &p->d_wdep, nt));
-  TRY(dalloc(p, &p->d_wcnt, (size_t)SMAX * p->wave_ngroups + SMAX));  // + one claim counter per pass
-  CUDA_OK(cudaMemcpy(p->d_wdep, dep.data(), sizeof(int2) * nt, cudaMemcpyHostToDevice));
-  p->wave_on = 1;
-  p->wave_sigma = -1;
-  return SSCG_OK;
-}
-
-// Split sigma levels into passes whose wavefront window fits the L2 budget:
-// between the first and last level of a pass a tile's CSR and the basis rows
-// in flight must stay resident, ~ ((nl-1) D) tiles of A + nl (D + lhi) tiles
-// of vectors (P, R, the Chebyshev two-back term).
-void wave_plan_passes(sscg_plan* p, int sigma) {
-  if (p->wave_sigma == sigma) return;
-  p->wave_passes.clear();
-  p->wave_sigma = sigma;
-  const double budget = atof(env_or("SSCG_WAVE_L2_MB", "64")) * 1048576.0;
-  const int force = atoi(env_or("SSCG_WAVE_NL", "0"));
-  const double slack_f = atof(env_or("SSCG_WAVE_SLACK", "6"));
-  auto lag = [&](int nl) {
-    const int slack = (int)std::ceil(slack_f * p->wave_grid / nl);
-    return p->wave_lhi + 1 + slack;
-  };
-  int nl = 1;
-  for (int m = sigma; m >= 1; --m) {
-    const double D = lag(m);
-    const double win = ((m - 1) * D * p->wave_row_bytes + m * (D + p->wave_lhi) * 24.0) * MT_ROWS;
-    if (win <= budget || m == 1) {
-      nl = m;
-      break;
-    }
-  }
-  if (force > 0) nl = std::min(force, sigma);
-  const int npass = (sigma + nl - 1) / nl;
-  int l0 = 0;
-  for (int q = 0; q < npass; ++q) {
-    const int m = (sigma - l0 + (npass - q) - 1) / (npass - q);  // near-equal passes
-    WaveArgs a;
-    a.l0 = l0;
-    a.nl = m;
-    a.D = lag(m);
-    a.ngroups = p->wave_ngroups;
-    a.nF = p->wave_tiles + (int64_t)(m - 1) * a.D;
-    a.cnt = p->d_wcnt;
-    a.claim = reinterpret_cast<unsigned int*>(p->d_wcnt + (size_t)SMAX * p->wave_ngroups) + q;
-    a.dep = p->d_wdep;
-    p->wave_passes.push_back(a);
-    l0 += m;
-  }
-}
-
-int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s, bool with_resid) {
-  if (!p->wave_on) {
-    for (int l = 0; l < sigma; ++l) launch_level(c, l, sigma, s, with_resid);
-    return SSCG_OK;
-  }
-  CUDA_OK(cudaMemsetAsync(p->d_wcnt, 0, sizeof(int) * ((size_t)SMAX * p->wave_ngroups + SMAX), s));
-  for (const WaveArgs& a : p->wave_passes) CUDA_OK(launch_wave(c, a, p->wave_grid, s));
+int launch_mpk(sscg_plan* p, const Ctx& c, int sigma, cudaStream_t s) {
+  (void)p;
+  for (int l = 0; l < sigma; ++l) launch_level(c, l, sigma, s);
   return SSCG_OK;
 }
 
@@ -1096,9 +1012,7 @@ int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
     TRY(plan_init(p, device, n, n, n, nnz, row_ptr, col_idx, values, lvl, SMAX));
     TRY(pattern_setup(p, n, row_ptr, col_idx, values));
     if (p->d_pid) return SSCG_OK;  // the pattern kernels replace the CSR staging
-    TRY(vs_setup(p, n, row_ptr, col_idx, values));
-    if (p->vs_ne) return SSCG_OK;  // so do the value-stream stencil kernels
-    return wave_setup(p, row_ptr, col_idx);
+    return vs_setup(p, n, row_ptr, col_idx, values);
   });
 }
 
@@ -1120,6 +1034,9 @@ int sscg_plan_create_part(sscg_plan** out, int32_t device, const sscg_part* part
                        q.values, q.lvl_rows, q.depth);
     if (rc) return rc;
     TRY(pattern_setup(p, q.n_rows, q.row_ptr, q.col_idx, q.values, q.global_rows, q.n_local));
+    // no pattern table (row-varying values): the value stream in global offsets
+    if (!p->d_pid && q.global_rows)
+      TRY(vs_setup(p, q.n_rows, q.row_ptr, q.col_idx, q.values, q.global_rows, q.n_local));
     p->partitioned = 1;
     p->rank = q.rank;
     p->world = q.world;
@@ -1194,14 +1111,13 @@ int sscg_plan_destroy(sscg_plan* p) {
   void* bufs[] = {p->d_rp, p->d_col, p->d_val, p->d_Y, p->d_x, p->d_b, p->d_x0, p->d_xj,
                   p->d_rj, p->d_st, p->d_cfg, p->d_part_t, p->d_part_r, p->d_part_d,
                   p->d_part_g, p->d_leja, p->d_it, p->d_ri, p->d_rd, p->d_conds, p->d_th,
-                  p->d_ga, p->d_mu, p->d_otrue, p->d_fg, p->d_red, p->d_wdep, p->d_wcnt,
+                  p->d_ga, p->d_mu, p->d_otrue, p->d_fg, p->d_red,
                   p->d_pid, p->d_pat_ptr, p->d_pat_off, p->d_pat_val, p->d_ss_mask, p->d_ss_val,
-                  p->d_zm_base, p->d_vs_val, p->d_zm_ctr};
+                  p->d_zm_base, p->d_vs_val, p->d_zm_ctr, p->d_vs_geo, p->d_vs_base};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_done) cudaFreeHost(p->h_done);
-  for (auto ev : {p->ev_chunk[0], p->ev_chunk[1], p->ev_start, p->ev_stop, p->ev_fork,
-                  p->ev_rfork, p->ev_rjoin})
+  for (auto ev : {p->ev_chunk[0], p->ev_chunk[1], p->ev_start, p->ev_stop, p->ev_fork})
     if (ev) cudaEventDestroy(ev);
   for (auto ev : p->ev_leja)
     if (ev) cudaEventDestroy(ev);
@@ -1210,7 +1126,6 @@ int sscg_plan_destroy(sscg_plan* p) {
   for (auto ev : p->st_events) cudaEventDestroy(ev);
   if (p->stream) cudaStreamDestroy(p->stream);
   if (p->side) cudaStreamDestroy(p->side);
-  if (p->side2) cudaStreamDestroy(p->side2);
   delete p;
   return SSCG_OK;
 }
@@ -1371,13 +1286,6 @@ int run_prepare(sscg_plan* p, const sscg_config* cfg) {
     return sscg_fail(SSCG_EINVAL, "trace_full is not supported on a row-partitioned solve");
   CUDA_OK(cudaSetDevice(p->device));
   TRY(ensure_work(p, cfg->sigma, cfg->max_outer, cfg->leja_grid));
-  if (p->wave_on && p->wave_sigma != cfg->sigma) {
-    wave_plan_passes(p, cfg->sigma);
-    if (p->gexec) {
-      cudaGraphExecDestroy(p->gexec);
-      p->gexec = nullptr;
-    }
-  }
   p->cfg = *cfg;
   p->halo.r_col = cfg->sigma + 1;
   DevConfig dc;
@@ -1557,27 +1465,79 @@ int sscg_get_small_phases(const sscg_plan* p, int64_t* cycles8) {
 int sscg_plan_mpk_schedule(sscg_plan* p, int32_t sigma, int32_t* out) {
   if (!p || !out || sigma < 1 || sigma > SMAX) return sscg_fail(SSCG_EINVAL, "bad arguments");
   for (int i = 0; i < 4 + 2 * SMAX; ++i) out[i] = 0;
-  out[0] = p->d_pid ? 2 : p->vs_ne ? 3 : p->wave_on ? 1 : 0;
-  out[1] = p->wave_on ? p->wave_grid : p->red_n;
-  out[2] = p->d_pid ? p->pat_np : p->vs_ne ? p->vs_ne : p->wave_lhi;
+  out[0] = p->d_pid ? 2 : p->vs_ne ? 3 : 0;
+  out[1] = p->red_n;
+  out[2] = p->d_pid ? p->pat_np : p->vs_ne;
   // last slot: pattern kernel form (0 table walk, 1 superset mask, 2 plane march)
-  if (p->d_pid)
-    out[3 + 2 * SMAX] = p->zm_S > 0 ? (p->zt_on ? 4 : p->zm_pair ? 3 : 2) : p->ss_ne > 0 ? 1 : 0;
-  if (!p->wave_on) {
-    out[3] = sigma;
-    for (int q = 0; q < sigma; ++q) out[4 + 2 * q] = 1;
-    return SSCG_OK;
+  if (p->d_pid) out[3 + 2 * SMAX] = p->zm_S > 0 ? 2 : p->ss_ne > 0 ? 1 : 0;
+  out[3] = sigma;
+  for (int q = 0; q < sigma; ++q) out[4 + 2 * q] = 1;
+  return SSCG_OK;
+}
+
+int sscg_plan_collectives(const sscg_plan* p, int32_t* out5) {
+  if (!p || !out5) return sscg_fail(SSCG_EINVAL, "NULL argument");
+  for (int i = 0; i < 5; ++i) out5[i] = p->census[i];
+  return SSCG_OK;
+}
+
+// ---- single-process multi-GPU group (one host thread and one
+// stream per GPU, communicators from ncclCommInitAll) -------------------------
+int sscg_group_create(sscg_plan** out, int32_t nplans, const int32_t* devices,
+                      const sscg_part* parts) {
+  if (!out || nplans < 1 || !devices || !parts) return sscg_fail(SSCG_EINVAL, "bad group arguments");
+  for (int i = 0; i < nplans; ++i) out[i] = nullptr;
+  for (int i = 0; i < nplans; ++i)
+    for (int j = 0; j < i; ++j)
+      if (devices[i] == devices[j])
+        return sscg_fail(SSCG_EINVAL, "group devices must be distinct (device %d twice)", devices[i]);
+  auto undo = [&](int rc) {
+    std::string keep = g_err;
+    for (int i = 0; i < nplans; ++i)
+      if (out[i]) sscg_plan_destroy(out[i]), out[i] = nullptr;
+    g_err = keep;
+    return rc;
+  };
+  for (int i = 0; i < nplans; ++i) {
+    if (parts[i].rank != i || parts[i].world != nplans)
+      return undo(sscg_fail(SSCG_EINVAL, "part %d is not rank %d of %d", i, i, nplans));
+    sscg_part q = parts[i];
+    q.nccl_id = nullptr;  // no per-rank init: the group's communicators come below
+    const int rc = sscg_plan_create_part(&out[i], devices[i], &q);
+    if (rc) return undo(rc);
   }
-  const int keep = p->wave_sigma;
-  std::vector<WaveArgs> saved = p->wave_passes;
-  wave_plan_passes(p, sigma);
-  out[3] = (int)p->wave_passes.size();
-  for (size_t q = 0; q < p->wave_passes.size(); ++q) {
-    out[4 + 2 * q] = p->wave_passes[q].nl;
-    out[5 + 2 * q] = p->wave_passes[q].D;
-  }
-  p->wave_passes = saved;  // a query must not invalidate the captured graph
-  p->wave_sigma = keep;
+  int rc = nccl_load(parts[0].nccl_lib);
+  if (rc) return undo(rc);
+  std::vector<void*> comms((size_t)nplans, nullptr);
+  std::vector<int> devs(devices, devices + nplans);
+  rc = nccl_comm_init_all(comms.data(), nplans, devs.data());
+  if (rc) return undo(rc);
+  for (int i = 0; i < nplans; ++i) out[i]->comm = comms[(size_t)i];
+  return SSCG_OK;
+}
+
+int sscg_group_solve(sscg_plan* const* plans, int32_t nplans, const sscg_config* cfg,
+                     const double* const* b, const double* const* x0, double* const* x_out,
+                     sscg_logs* const* logs) {
+  if (!plans || nplans < 1 || !b) return sscg_fail(SSCG_EINVAL, "bad group arguments");
+  for (int i = 0; i < nplans; ++i)
+    if (!plans[i] || !plans[i]->comm || plans[i]->rank != i || plans[i]->world != nplans)
+      return sscg_fail(SSCG_EINVAL, "plan %d is not rank %d of a %d-GPU group", i, i, nplans);
+  // every rank must run concurrently (each outer loop allreduces across all of
+  // them): one host thread per GPU, each driving its own plan's stream
+  std::vector<int> rcs((size_t)nplans, SSCG_OK);
+  std::vector<std::string> errs((size_t)nplans);
+  auto run = [&](int i) {
+    rcs[(size_t)i] = sscg_solve(plans[i], cfg, b[i], x0 ? x0[i] : nullptr,
+                                x_out ? x_out[i] : nullptr, logs ? logs[i] : nullptr);
+    if (rcs[(size_t)i]) errs[(size_t)i] = g_err;
+  };
+  std::vector<std::thread> th;
+  for (int i = 1; i < nplans; ++i) th.emplace_back(run, i);
+  run(0);
+  for (auto& t : th) t.join();
+  for (int i = 0; i < nplans; ++i)
+    if (rcs[(size_t)i]) return sscg_fail(rcs[(size_t)i], "group rank %d: %s", i, errs[(size_t)i].c_str());
   return SSCG_OK;
 }
 

@@ -145,13 +145,19 @@ __global__ void __launch_bounds__(REC_THREADS)
 // one full wave of resident CTAs (grid-stride loops): a partial second wave
 // would leave most SMs idle at the tail of this HBM-bound pass
 int rec_grid(int64_t ld) {
-  static int per_sm = 0, sms = 0;
+  // occupancy and SM count per device (a process may drive several GPUs)
+  static std::atomic<int> cache_sms[64], cache_per_sm[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  int sms = cache_sms[dev].load(std::memory_order_relaxed);
+  int per_sm = cache_per_sm[dev].load(std::memory_order_relaxed);
   if (!per_sm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_recover, REC_THREADS, 0);
     if (per_sm < 1) per_sm = 1;
+    cache_sms[dev].store(sms, std::memory_order_relaxed);
+    cache_per_sm[dev].store(per_sm, std::memory_order_relaxed);
   }
   int64_t g = (ld / 2 + REC_THREADS - 1) / REC_THREADS;
 #ifdef REC_PER_SM

@@ -161,15 +161,6 @@ __host__ __device__ __forceinline__ size_t stage_bytes(int cap) {
   return ((size_t)(cap + 2) * 8 + (size_t)(cap + 4) * 4 + 15) / 16 * 16;
 }
 
-// wavefront stages also carry the tile's row_ptr[r0 .. r0 + MT_ROWS] (+ pad)
-#define WAVE_RP_BYTES ((MT_ROWS + 4) * 4)
-#ifndef WAVE_BATCH
-#define WAVE_BATCH 8  // a 7-point row's gathers in one round
-#endif
-__host__ __device__ __forceinline__ size_t wave_stage_bytes(int cap) {
-  return stage_bytes(cap) + WAVE_RP_BYTES;
-}
-
 // Runs fn(row, TileStage&) over rows [0, nrows) tile by tile.
 template <class Fn>
 __device__ __forceinline__ void staged_rows(const Ctx& c, int64_t nrows, Fn&& fn) {
@@ -231,12 +222,6 @@ __device__ __forceinline__ void staged_rows(const Ctx& c, int64_t nrows, Fn&& fn
 struct LdNc {
   static __device__ __forceinline__ double ld(const double* p) { return __ldg(p); }
 };
-// gathers of vectors other CTAs of the same launch produced (wavefront kernel):
-// coherent loads only, never the non-coherent read-only path
-struct LdCa {
-  static __device__ __forceinline__ double ld(const double* p) { return __ldca(p); }
-};
-
 #ifndef ROW_BATCH
 #define ROW_BATCH 4
 #endif

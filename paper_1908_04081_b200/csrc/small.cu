@@ -1261,16 +1261,16 @@ __global__ void k_unit_symeig(int n, const double* M, double* w) {
   }
 }
 
-bool g_attr_set = false;
+std::atomic<unsigned long long> g_attr_set{0};  // per device
 void ensure_attr() {
-  if (g_attr_set) return;
+  if (!first_use_on_device(g_attr_set)) return;
   const int bytes = (int)small_smem_bytes();
   cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_state_init, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_unit_conds, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_unit_params, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_unit_leja, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  g_attr_set = true;
+  mark_device_done(g_attr_set);
 }
 
 double host_c0() { return pow(ldexp(1.0, -53), -0.5); }

@@ -1,12 +1,15 @@
 """Row-partitioned adaptive s-step CG: host driver.
 
-Two ways to run the partitioned algorithm:
+Three ways to run the partitioned algorithm:
 
 * `solve_partitioned(rows, b, x0, cfg, rank, world, ...)` -- one process per GPU
   (torchrun): this rank builds its slab + ghost zones (partition.py), the
   ranks agree on an NCCL unique id over torch.distributed (plumbing only), and
   the C library runs every outer loop as one CUDA graph containing one grouped
   NCCL halo exchange and one NCCL allreduce.
+* `DeviceGroup` -- one process, one rank per listed GPU: the
+  communicators come from ncclCommInitAll and one host thread + stream per GPU
+  runs that rank's solve; `adaptive_solve(problem, cfg, devices=[...])`.
 * `VirtualGroup` -- all ranks' plans in ONE process on one GPU, driven in lock
   step with device copies for the halo and a fixed-order sum for the
   allreduce: the multi-rank kernels and partition exercised on a single GPU.
@@ -18,6 +21,7 @@ the trace returned on each rank is the same.
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 
 import numpy as np
 
@@ -87,6 +91,32 @@ class PartPlan:
             pass
 
 
+def logs_digest(logs):
+    """Hash of everything a rank decided: status, counts, the per-outer
+    records (s_bar, s~, s_actual, breaks) and every alpha / beta bit.  Every
+    rank of a partitioned solve reduces the same Gram bits and so must take the
+    same decisions; a mismatch means the ranks desynchronised."""
+    s = logs.s
+    h = hashlib.sha256()
+    h.update(np.array([s.status, s.total_iters, s.total_outer, s.n_records], np.int64).tobytes())
+    nrec = min(int(s.n_records), len(logs.rec_i))
+    nit = min(int(s.total_iters), len(logs.iters))
+    h.update(np.ascontiguousarray(logs.rec_i[:nrec, :5]).tobytes())
+    h.update(np.ascontiguousarray(logs.iters[:nit, :2]).tobytes())
+    return h.hexdigest()
+
+
+class RankMismatch(RuntimeError):
+    """The ranks of a partitioned solve did not take identical decisions."""
+
+
+def check_ranks_agree(digests):
+    if len(set(digests)) != 1:
+        bad = [r for r, d in enumerate(digests) if d != digests[0]]
+        raise RankMismatch(f"ranks {bad} disagree with rank 0 on the solve's decisions "
+                           "(s sequence / alphas / counts)")
+
+
 def _local_vectors(part, b_global, x0_global):
     b = np.ascontiguousarray(b_global[part.row_lo:part.row_hi], dtype=np.float64)
     x0 = np.ascontiguousarray(x0_global[part.global_rows], dtype=np.float64)
@@ -120,6 +150,82 @@ class VirtualGroup:
         return x, tr, co, logs
 
 
+class DeviceGroup:
+    """A row-partitioned solve over several GPUs from ONE process (SURVEY.md
+    5): rank i on devices[i], communicators by ncclCommInitAll, one host
+    thread and stream per GPU (sscg_group_create / sscg_group_solve).  The
+    plans are built once (cached on the matrix by `adaptive_solve`) and reused
+    for every solve with sigma <= depth."""
+
+    def __init__(self, rows, devices, depth, nccl_lib=None):
+        from .build import nccl_library
+        lib = L.load()
+        self.devices = [int(d) for d in devices]
+        self.world = len(self.devices)
+        if len(set(self.devices)) != self.world:
+            raise ValueError("devices must be distinct GPUs")
+        for d in self.devices:
+            L.require_device(d)
+        self.depth = int(depth)
+        self.parts = partition_all(rows, self.world, self.depth)
+        nccl_lib = nccl_lib or nccl_library()
+        structs, self._keep = [], []
+        for r, p in enumerate(self.parts):
+            st, keep = _part_struct(p, r, self.world, None, nccl_lib)
+            structs.append(st)
+            self._keep.append(keep)
+        arr = (L.SscgPart * self.world)(*structs)
+        hs = (C.c_void_p * self.world)()
+        devs = np.array(self.devices, dtype=np.int32)
+        L.check(lib.sscg_group_create(C.cast(hs, C.POINTER(C.c_void_p)), self.world,
+                                      L.iptr(devs), arr))
+        self.handles = [C.c_void_p(h) for h in hs]
+        self._lib = lib
+
+    def mpk_schedule(self, sigma):
+        return [L.plan_mpk_schedule(self._lib, h, sigma) for h in self.handles]
+
+    def collectives(self):
+        return [L.plan_collectives(self._lib, h) for h in self.handles]
+
+    def solve(self, problem, cfg, info=None):
+        cfg, ccfg = make_config(cfg, problem, "fast")
+        if cfg.sigma > self.depth:
+            raise ValueError(f"sigma={cfg.sigma} exceeds the group's ghost depth {self.depth}")
+        vecs = [_local_vectors(p, problem.b, problem.x0) for p in self.parts]
+        xs = [np.empty(p.n_own) for p in self.parts]
+        logs = [LogBuffers(cfg) for _ in self.parts]
+        w = self.world
+        hp = (C.c_void_p * w)(*[h.value for h in self.handles])
+        bp = (L._DP * w)(*[L.dptr(v[0]) for v in vecs])
+        xp = (L._DP * w)(*[L.dptr(v[1]) for v in vecs])
+        op = (L._DP * w)(*[L.dptr(x) for x in xs])
+        lp = (C.POINTER(L.SscgLogs) * w)(*[C.pointer(lg.s) for lg in logs])
+        L.check(self._lib.sscg_group_solve(C.cast(hp, C.POINTER(C.c_void_p)), w, ccfg, bp, xp,
+                                           op, lp))
+        check_ranks_agree([logs_digest(lg) for lg in logs])
+        x = np.empty(problem.a.n)
+        for p, xo in zip(self.parts, xs):
+            x[p.row_lo:p.row_hi] = xo
+        tr, co = build_trace(cfg, logs[0], "fast")
+        if isinstance(info, dict):
+            info.update(device_ms=max(lg.s.device_ms for lg in logs), logs=logs[0],
+                        outer_launched=logs[0].s.outer_launched, first_gram=logs[0].first_gram)
+        return x, tr, co
+
+    def close(self):
+        for h in getattr(self, "handles", []):
+            if h is not None and h.value:
+                self._lib.sscg_plan_destroy(h)
+        self.handles = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def solve_partitioned(rows, problem_scalars, b_global, x0_global, cfg, rank, world, device,
                       exchange, broadcast_bytes, nccl_lib=None, info=None):
     """This rank's share of a multi-process partitioned solve (torchrun).
@@ -145,6 +251,9 @@ def solve_partitioned(rows, problem_scalars, b_global, x0_global, cfg, rank, wor
     logs = LogBuffers(cfg)
     xo = np.empty(part.n_own)
     L.check(lib.sscg_solve(plan.handle, ccfg, L.dptr(b), L.dptr(x0), L.dptr(xo), logs.s))
+    # every rank must have taken the same decisions (bitwise-identical reduced
+    # Gram); a divergence would desynchronise the halo -- fail loudly
+    check_ranks_agree(exchange(logs_digest(logs)))
     tr, co = build_trace(cfg, logs, "fast")
     if isinstance(info, dict):
         info.update(plan=plan, part=part, logs=logs, ccfg=ccfg, b=b, x0=x0)

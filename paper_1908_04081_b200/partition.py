@@ -88,6 +88,88 @@ class Stencil7Rows:
         return indptr, cols, vals
 
 
+class Varcoef27Rows:
+    """Rows of the c4 operator (problems.varcoef27: 27-point variable-coefficient
+    diffusion on n^3, lognormal cells, harmonic-mean face weights / |o|^2,
+    Dirichlet) generated on demand with the same values, column order and
+    rounding, so a rank builds only its slab + ghost planes.  The cell field k
+    and the diagonal are global (n^3 doubles each: 57 MB at 192^3); the
+    right-hand side is the generator's (`rhs()`).  jacobi=True gives the
+    two-sided Jacobi-scaled operator of problems.varcoef27_jacobi."""
+
+    OFFS = [(dz, dy, dx) for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1)]
+
+    def __init__(self, n, sigma_ln=1.5, seed=0, jacobi=False):
+        self.m, self.n = n, n ** 3
+        rng = np.random.default_rng(seed)
+        k = np.exp(rng.normal(0.0, sigma_ln, (n, n, n)))
+        b = rng.standard_normal(self.n)
+        self._b = b / np.linalg.norm(b)
+        self.k = k.ravel()
+        self.jacobi = jacobi
+        # the diagonal in the generator's accumulation order (offsets in
+        # lexicographic order, in-domain w h, out-of-domain w k_i)
+        idx = np.arange(n)
+        diag = np.zeros((n, n, n))
+        for (dz, dy, dx) in self.OFFS:
+            if (dz, dy, dx) == (0, 0, 0):
+                continue
+            m = self._mask3(idx, dz, dy, dx)
+            w0 = 1.0 / (dz * dz + dy * dy + dx * dx)
+            shifted = np.zeros_like(k)
+            sz, sy, sx = (slice(max(0, -d), n - max(0, d)) for d in (dz, dy, dx))
+            tz, ty, tx = (slice(max(0, d), n - max(0, -d)) for d in (dz, dy, dx))
+            shifted[sz, sy, sx] = k[tz, ty, tx]
+            h = np.where(m, 2.0 * k * shifted / np.where(m, k + shifted, 1.0), 0.0)
+            diag += np.where(m, w0 * h, w0 * k)
+        self.diag = diag.ravel()
+        self.root = np.sqrt(self.diag) if jacobi else None
+
+    @staticmethod
+    def _mask3(idx, dz, dy, dx):
+        n = len(idx)
+        mz = (idx + dz >= 0) & (idx + dz < n)
+        my = (idx + dy >= 0) & (idx + dy < n)
+        mx = (idx + dx >= 0) & (idx + dx < n)
+        return mz[:, None, None] & my[None, :, None] & mx[None, None, :]
+
+    def rhs(self):
+        return self._b
+
+    def rows(self, idx):
+        idx = np.asarray(idx, dtype=np.int64)
+        n = self.m
+        ix, iy, iz = idx % n, (idx // n) % n, idx // (n * n)
+        masks = []
+        counts = np.zeros(len(idx), dtype=np.int64)
+        for (dz, dy, dx) in self.OFFS:
+            m = ((iz + dz >= 0) & (iz + dz < n) & (iy + dy >= 0) & (iy + dy < n) &
+                 (ix + dx >= 0) & (ix + dx < n))
+            masks.append(m)
+            counts += m
+        indptr = np.zeros(len(idx) + 1, dtype=np.int64)
+        np.cumsum(counts, out=indptr[1:])
+        cols = np.empty(indptr[-1], dtype=np.int64)
+        vals = np.empty(indptr[-1], dtype=np.float64)
+        pos = indptr[:-1].copy()
+        for (dz, dy, dx), m in zip(self.OFFS, masks):
+            sel = np.nonzero(m)[0]
+            rows = idx[sel]
+            if (dz, dy, dx) == (0, 0, 0):
+                c, v = rows, self.diag[rows]
+            else:
+                c = rows + (dz * n * n + dy * n + dx)
+                w0 = 1.0 / (dz * dz + dy * dy + dx * dx)
+                ki, kc = self.k[rows], self.k[c]
+                v = -(w0 * (2.0 * ki * kc / (ki + kc)))
+            if self.jacobi:  # matio.jacobi_precondition: / (root[min] * root[max])
+                v = v / (self.root[np.minimum(rows, c)] * self.root[np.maximum(rows, c)])
+            cols[pos[sel]] = c
+            vals[pos[sel]] = v
+            pos[sel] += 1
+        return indptr, cols, vals
+
+
 def slab_bounds(n, world, align=1):
     """Contiguous row ranges, as equal as possible (multiples of `align`)."""
     units = n // align

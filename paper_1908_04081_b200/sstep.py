@@ -17,7 +17,7 @@ from types import SimpleNamespace
 import numpy as np
 
 from . import _lib as L
-from .adaptive import LogBuffers, build_trace
+from .adaptive import LogBuffers, build_trace, clamp_i32
 from .kernels import _plan
 from .types import DEFAULT_LEJA_GRID, ParameterError
 
@@ -48,7 +48,7 @@ def sstep_solve(problem, s, eps_star, max_outer=None, params=None, basis_kind="m
                            else basis_kind]
     c.c_strategy = L.CSTRAT["adaptive"]  # only the trace's xi estimate, as sstep.py:151
     c.variant = 1
-    c.max_outer = int(max_outer)
+    c.max_outer = clamp_i32(max_outer)
     c.leja_grid = DEFAULT_LEJA_GRID
     if spectral_bounds and spectral_bounds[0] is not None and spectral_bounds[1] is not None:
         c.has_bounds = 1
@@ -64,7 +64,7 @@ def sstep_solve(problem, s, eps_star, max_outer=None, params=None, basis_kind="m
     bv, x0 = L.f64(b), L.f64(problem.x0)
     if bv.shape != (a.n,) or x0.shape != (a.n,):
         raise ValueError("b / x0 do not match the matrix dimension")
-    shape = SimpleNamespace(sigma=s, s_bar0=s, max_outer=int(max_outer))
+    shape = SimpleNamespace(sigma=s, s_bar0=s, max_outer=clamp_i32(max_outer))
     logs = LogBuffers(shape)
     x = np.empty(a.n)
     if params is not None:

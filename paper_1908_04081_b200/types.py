@@ -239,6 +239,7 @@ class SolveTrace:
     outer_records: list = field(default_factory=list)
     trace_level: str = "full"
     outer_true_resid: list = field(default_factory=list)
+    truncated: bool = False  # device log capacity ran out (the solve itself is complete)
 
     def record_iteration(self, true_rel, upd_rel, gap, c_val, lmin, lmax, psi=float("nan")):
         self.true_resid.append(float(true_rel))

@@ -70,6 +70,11 @@ def test_nccl_world1_matches_single_gpu(gpu_ready):
     np.testing.assert_array_equal(xo, x1)
     np.testing.assert_array_equal(co.alphas, c1.alphas)
     assert tr.converged and tr.total_outer == t1.total_outer
+    # the captured outer-loop graph holds exactly one allreduce (the algorithm's
+    # one synchronisation per outer loop) and one grouped halo exchange
+    coll = plan.collectives()
+    assert coll["allreduce_per_outer"] == 1 and coll["halo_exchanges_per_outer"] == 1, coll
+    assert coll["kernel_nodes"] >= 2 * kw["sigma"], coll
 
 
 def test_partitioned_rejects_sigma_above_depth(gpu_ready):
@@ -106,3 +111,72 @@ def test_partitioned_march_edge_shapes(gpu_ready, shape, world):
     xg, tg, cg, _ = grp.solve(prob, AdaptiveConfig(**kw))
     assert tg.converged and true_rel(prob, xg) <= kw["eps_star"]
     np.testing.assert_allclose(cg.alphas[:5], c1.alphas[:5], rtol=1e-8)
+
+
+@pytest.mark.parametrize("key,jacobi", [("c4", False), ("c4j", True)])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_partitioned_value_stream(gpu_ready, key, jacobi, world):
+    """Row-varying 27-point slabs (c4 / c4j) keep the value-stream kernels on
+    every rank: values slot-major in GLOBAL offsets, neighbours through the
+    plane tables.  P = 1 is bit-identical to the single-GPU value stream (and
+    so to CSR); P > 1 agrees up to the Gram summation order."""
+    from paper_1908_04081_b200.partition import Varcoef27Rows
+    n = 12
+    prob = problems.make_problem(key, scale=n)
+    kw = dict(sigma=10, eps_star=1e-8, basis_kind="newton", max_outer=30)
+    x1, t1, c1 = adaptive_solve(prob, AdaptiveConfig(**kw), trace="fast")
+    grp = VirtualGroup(Varcoef27Rows(n, jacobi=jacobi), world, depth=kw["sigma"])
+    assert [pl.mpk_schedule(10)["kind"] for pl in grp.plans] == ["stencil values"] * world
+    xg, tg, cg, _ = grp.solve(prob, AdaptiveConfig(**kw))
+    if world == 1:
+        np.testing.assert_array_equal(xg, x1)
+        np.testing.assert_array_equal(cg.alphas, c1.alphas)
+        return
+    got = [(r.s_tilde, r.s_actual) for r in tg.outer_records[:3]]
+    assert got == [(r.s_tilde, r.s_actual) for r in t1.outer_records[:3]]
+    np.testing.assert_allclose(cg.alphas[:5], c1.alphas[:5], rtol=1e-8)
+
+
+def test_device_group_single_process(gpu_ready):
+    """The single-process multi-GPU drop-in (DeviceGroup: ncclCommInitAll, one
+    host thread + stream per GPU) at the one GPU this box has: bit-identical to
+    the single-GPU solve, one allreduce per outer loop in its graph, and
+    adaptive_solve(devices=[...]) reaches it."""
+    from paper_1908_04081_b200.dist import DeviceGroup
+    prob = problems.make_problem("c3", scale=24)
+    kw = dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev")
+    x1, t1, c1 = adaptive_solve(prob, AdaptiveConfig(**kw), trace="fast")
+    g = DeviceGroup(CsrRows.of(prob.a), [0], depth=10)
+    info = {}
+    x, tr, co = g.solve(prob, AdaptiveConfig(**kw), info=info)
+    np.testing.assert_array_equal(x, x1)
+    np.testing.assert_array_equal(co.alphas, c1.alphas)
+    assert tr.converged and tr.total_outer == t1.total_outer and info["device_ms"] > 0
+    coll = g.collectives()[0]
+    assert coll["allreduce_per_outer"] == 1 and coll["halo_exchanges_per_outer"] == 1, coll
+    g.close()
+    # devices=[0] is the single-GPU path; duplicate devices are refused
+    x2, _, _ = adaptive_solve(prob, AdaptiveConfig(**kw), trace="fast", devices=[0])
+    np.testing.assert_array_equal(x2, x1)
+    with pytest.raises(ValueError):
+        adaptive_solve(prob, AdaptiveConfig(**kw), devices=[0, 0])
+    with pytest.raises(ValueError):
+        adaptive_solve(prob, AdaptiveConfig(**kw), trace="full", devices=[0, 1])
+
+
+def test_group_create_refuses_duplicate_devices_in_c(gpu_ready):
+    """sscg_group_create itself rejects a device listed twice (NCCL cannot put
+    two ranks of one communicator on one GPU)."""
+    import ctypes as C
+
+    from paper_1908_04081_b200 import _lib as L
+    from paper_1908_04081_b200.dist import _part_struct
+    from paper_1908_04081_b200.partition import partition_all
+    prob = problems.make_problem("c1", scale=16)
+    parts = partition_all(CsrRows.of(prob.a), 2, 4)
+    st = [_part_struct(p, r, 2, None, None) for r, p in enumerate(parts)]
+    arr = (L.SscgPart * 2)(*[s for s, _ in st])
+    hs = (C.c_void_p * 2)()
+    devs = np.array([0, 0], dtype=np.int32)
+    rc = L.load().sscg_group_create(C.cast(hs, C.POINTER(C.c_void_p)), 2, L.iptr(devs), arr)
+    assert rc == L.EINVAL and b"distinct" in L.load().sscg_last_error()

@@ -19,8 +19,8 @@ from paper_1908_04081_b200.types import ProblemInstance, SparseMatrix
 pytestmark = pytest.mark.gpu
 
 
-_KEYS = ("SSCG_PATTERN", "SSCG_PAT_SS", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_ZM_PAIR",
-         "SSCG_ZT", "SSCG_VS", "SSCG_ZM_SPLIT", "SSCG_ZM_DYN")
+_KEYS = ("SSCG_PATTERN", "SSCG_PAT_SS", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_VS",
+         "SSCG_ZM_DYN")
 
 
 def _with_env(env, fn):
@@ -115,20 +115,16 @@ def test_pattern_kernel_forms(gpu_ready):
     assert form(_tridiag_many_patterns) == "superset"
     assert form(lambda: problems.make_problem("c5", scale=28), {"SSCG_ZM": "0"}) == "superset"
     assert form(lambda: problems.make_problem("c5", scale=28), {"SSCG_PAT_SS": "0"}) == "table"
-    assert form(lambda: problems.make_problem("c5", scale=32), {"SSCG_ZT": "1"}) == "tile march"
-    assert form(lambda: problems.make_problem("c5", scale=28), {"SSCG_ZM_PAIR": "1"}) == "pair march"
 
 
 @pytest.mark.parametrize("env", [{"SSCG_ZM": "0"}, {"SSCG_PAT_SS": "0"}, {"SSCG_ZM_ZC": "3"},
-                                 {"SSCG_ZM_2D": "0"}, {"SSCG_ZM_PAIR": "1"}, {"SSCG_ZT": "1"},
-                                 {"SSCG_ZM_SPLIT": "1"}, {"SSCG_ZM_DYN": "0"}],
-                         ids=["superset", "table", "march_zc3", "march_1d", "pair", "tile",
-                              "split_resid", "static_items"])
+                                 {"SSCG_ZM_2D": "0"}, {"SSCG_ZM_DYN": "0"}],
+                         ids=["superset", "table", "march_zc3", "march_1d", "static_items"])
 def test_pattern_forms_bit_identical(gpu_ready, env):
     """Plane march (default), its opt-in variants, superset mask and table
     walk run the same rounded operations in the same order: identical solves
     (Newton and Chebyshev bases, unit and non-unit gamma, mu != 0).  The 32^3
-    grids give whole 32 x 8 column tiles (2-D tiled march, tile march)."""
+    grids give whole 32 x 8 column tiles (2-D tiled march)."""
     for key, scale, kw in (("c5", 28, dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
                            ("c3", 24, dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev")),
                            ("c5", 32, dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
@@ -158,30 +154,6 @@ def test_pattern_full_trace_and_partitioned_agree(gpu_ready):
     prob = problems.make_problem("c3", scale=24)
     xg, tg, cg, _ = VirtualGroup(CsrRows.of(prob.a), 1, depth=10).solve(prob, AdaptiveConfig(**kw))
     np.testing.assert_array_equal(xg, ref[0])
-
-
-@pytest.mark.parametrize("name,make,kw,kind", CASES[:4], ids=[c[0] for c in CASES[:4]])
-def test_windowed_pattern_kernels_bit_identical(gpu_ready, name, make, kw, kind):
-    """The opt-in windowed kernels (SSCG_PAT_WIN=1: vector windows staged by
-    TMA, near columns from shared memory) reproduce the CSR solve bit for bit."""
-    cfg = AdaptiveConfig(**kw)
-
-    def run():
-        prob = make()
-        return adaptive_solve(prob, cfg, trace="fast")
-
-    ref = _with_env({"SSCG_PATTERN": "0"}, run)
-    old = os.environ.get("SSCG_PAT_WIN")
-    os.environ["SSCG_PAT_WIN"] = "1"
-    try:
-        got = run()
-    finally:
-        if old is None:
-            os.environ.pop("SSCG_PAT_WIN", None)
-        else:
-            os.environ["SSCG_PAT_WIN"] = old
-    np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
-    np.testing.assert_array_equal(got[0], ref[0])
 
 
 @pytest.mark.parametrize("key,kw", [

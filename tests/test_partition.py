@@ -183,3 +183,41 @@ def test_gloo_world2_partitioned_protocol(tmp_path):
         np.testing.assert_array_equal(np.load(tmp_path / f"g{rank}.npy"), g0)  # identical on ranks
     scale = np.sqrt(np.outer(np.diag(g_ref), np.diag(g_ref)))
     assert np.max(np.abs(g0 - g_ref) / scale) < 1e-13
+
+
+@pytest.mark.parametrize("jacobi", [False, True])
+def test_varcoef27_rows_match_the_generator(jacobi):
+    """The on-demand c4 / c4j rows (what a partitioned rank builds its slab
+    from) are the global generator's rows bit for bit, in any order."""
+    from paper_1908_04081_b200.partition import Varcoef27Rows
+    n = 9
+    prob = problems.make_problem("c4j" if jacobi else "c4", scale=n)
+    g = Varcoef27Rows(n, jacobi=jacobi)
+    ip, cols, vals = g.rows(np.arange(n ** 3))
+    np.testing.assert_array_equal(ip, np.asarray(prob.a.row_ptr))
+    np.testing.assert_array_equal(cols, np.asarray(prob.a.col_idx))
+    np.testing.assert_array_equal(vals, np.asarray(prob.a.values))
+    np.testing.assert_array_equal(g.rhs(), prob.b)
+    sel = np.array([700, 5, 364, 0, 728])
+    for x, y in zip(g.rows(sel), CsrRows.of(prob.a).rows(sel)):
+        np.testing.assert_array_equal(x, y)
+    parts = partition_all(g, 3, 4)
+    for p in parts:  # slabs of whole planes: what the plane-table value stream needs
+        assert p.n_local % (n * n) == 0
+
+
+def test_rank_decision_digests():
+    """The cross-rank check of a partitioned solve: identical digests pass, any
+    divergence raises (a desynchronised rank would corrupt the halo)."""
+    from types import SimpleNamespace
+
+    from paper_1908_04081_b200.dist import RankMismatch, check_ranks_agree, logs_digest
+    def fake(alpha):
+        s = SimpleNamespace(status=1, total_iters=2, total_outer=1, n_records=1)
+        it = np.zeros((4, 10))
+        it[:2, 0] = alpha
+        return SimpleNamespace(s=s, rec_i=np.zeros((3, 8), np.int32), iters=it)
+    a, b = logs_digest(fake(0.5)), logs_digest(fake(0.5))
+    check_ranks_agree([a, b])
+    with pytest.raises(RankMismatch):
+        check_ranks_agree([a, logs_digest(fake(np.nextafter(0.5, 1.0)))])

@@ -1,8 +1,8 @@
 """A/B sweep of matrix-powers schedules on one problem (GPU box).
 
-    python tools/wave_sweep.py [--config c5w] [--outer 12] ENV1 ENV2 ...
+    python tools/ab_sweep.py [--config c5w] [--outer 12] ENV1 ENV2 ...
 
-Each ENV is a comma list like "SSCG_WAVE=0" or "SSCG_WAVE_NL=4,SSCG_WAVE_CTAS=3"
+Each ENV is a comma list like "SSCG_ZM=0" or "SSCG_ZM_ZC=16,SSCG_ZM_DYN=0"
 (empty string = defaults).  For every ENV a fresh plan is created with that
 environment, one solve capped at --outer outer loops runs unprofiled (device
 time) and once profiled (per-class kernel ms); prints one JSON line per ENV.
@@ -20,9 +20,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1908_04081_b200 import AdaptiveConfig, _lib as L, problems  # noqa: E402
 from paper_1908_04081_b200.adaptive import LogBuffers, make_config  # noqa: E402
 
-KEYS = ("SSCG_WAVE", "SSCG_WAVE_NL", "SSCG_WAVE_CTAS", "SSCG_WAVE_L2_MB", "SSCG_WAVE_SLACK",
-        "SSCG_PATTERN", "SSCG_PAT_WIN", "SSCG_STAGE_MAX_KB", "SSCG_LEJA_HEAD", "SSCG_PAT_SS",
-        "SSCG_PF", "SSCG_PF_AHEAD", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_ZM_PAIR", "SSCG_ZT", "SSCG_ZM_SPLIT", "SSCG_ZM_DYN", "SSCG_LEJA_AFTER0", "SSCG_ZM_ZC0")
+KEYS = ("SSCG_PATTERN", "SSCG_STAGE_MAX_KB", "SSCG_LEJA_HEAD", "SSCG_PAT_SS", "SSCG_PF",
+        "SSCG_PF_AHEAD", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_ZM_DYN", "SSCG_LEJA_AFTER0",
+        "SSCG_ZM_ZC0", "SSCG_VS")
 
 
 def main():

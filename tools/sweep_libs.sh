@@ -1,5 +1,5 @@
 # A/B of matrix-powers schedules over side-built libraries (GPU box):
-#   LIBS="libsscg.so libsscg_x.so" ENVS="SSCG_WAVE=0 SSCG_WAVE=1,SSCG_WAVE_NL=2" bash tools/sweep_libs.sh
+#   LIBS="libsscg.so libsscg_x.so" ENVS="SSCG_ZM=1 SSCG_ZM=0" bash tools/sweep_libs.sh
 fmt() { python -c "
 import sys,json
 for l in sys.stdin:
@@ -9,5 +9,5 @@ for l in sys.stdin:
 "; }
 for lib in ${LIBS:-libsscg.so}; do
   echo "== $lib"
-  SSCG_LIB=paper_1908_04081_b200/_lib/$lib timeout 600 python tools/wave_sweep.py --config ${CONFIG:-c5w} --outer ${OUTER:-10} ${ENVS:-SSCG_WAVE=0} 2>&1 | fmt
+  SSCG_LIB=paper_1908_04081_b200/_lib/$lib timeout 600 python tools/ab_sweep.py --config ${CONFIG:-c5w} --outer ${OUTER:-10} ${ENVS:-SSCG_ZM=1} 2>&1 | fmt
 done
