@@ -663,7 +663,12 @@ def run_reference(args, rank, world):
     key, sigma, basis, eps, scaling, desc = CONFIGS[args.config]
     prob = problems.make_problem(key, scale=args.scale, world=1)
     cfg_kw = dict(sigma=sigma, eps_star=eps, basis_kind=basis)
-    counts = reference_counts(args.config, world)
+    if args.scale:  # a test-sized problem: the oracle's own full solve gives the counts
+        from oracle import sscg_oracle as O
+        _, otr, _, _ = O.solve_problem(prob, O.OracleConfig(**cfg_kw), diagnostics=False)
+        counts = (otr.total_outer, otr.total_iters, "the oracle's full solve of this scaled problem")
+    else:
+        counts = reference_counts(args.config, world)
     if counts is None:
         print(json.dumps({"impl": "reference", "unavailable":
                           f"no outer/total counts for {args.config} at N={world}"}))

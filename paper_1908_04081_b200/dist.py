@@ -79,6 +79,9 @@ class PartPlan:
     def mpk_schedule(self, sigma):
         return L.plan_mpk_schedule(self._lib, self.handle, sigma)
 
+    def collectives(self):
+        return L.plan_collectives(self._lib, self.handle)
+
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:
             self._lib.sscg_plan_destroy(self.handle)

@@ -26,24 +26,36 @@ def _bench(*args, timeout=600):
 
 def test_bench_default_arm_small(gpu_ready):
     d = _bench("--scale", "48", "--steps", "1", "--warmup", "1")
-    assert REQUIRED <= set(d) and d["value"] > 0 and d["config"]["converged"]
+    assert REQUIRED <= set(d) and d["value"] > 0 and d["solve"]["converged"]
     for key in ("roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
         assert key in d
-    assert d["roofline"]["mpk_schedule"]["kind"] == "pattern"
+    assert d["roofline"]["schedule"]["kind"] == "pattern"
+    assert d["e2e"]["first_call_s"] > 0 and len(d["secondary"]) == 2
+    assert d["secondary"][0]["roofline"]["schedule"]["kind"] == "csr"
+    assert d["secondary"][1]["roofline"]["schedule"]["kind"] == "stencil values"
 
 
-def test_bench_partitioned_arm_small(gpu_ready):
-    d = _bench("--partitioned", "--scale", "48", "--steps", "1", "--warmup", "1", "--no-cpu")
+@pytest.mark.parametrize("config,scale", [("c5w", 48), ("c4", 24), ("c4j", 24), ("c5", 40)])
+def test_bench_partitioned_arm_small(gpu_ready, config, scale):
+    d = _bench("--partitioned", "--config", config, "--scale", str(scale), "--steps", "1",
+               "--warmup", "1", "--no-cpu")
     assert REQUIRED <= set(d) and d["value"] > 0
+    assert d["solve"]["collectives"]["allreduce_per_outer"] == 1
+    assert d["solve"]["ranks_agree"] and d["solve"]["converged"] or config == "c4"
+    kind = "stencil values" if config.startswith("c4") else "pattern"
+    assert d["roofline"]["schedule"]["kind"] == kind
 
 
 @pytest.mark.parametrize("solver", ["hscg", "sstep"])
 def test_bench_solver_lines_small(gpu_ready, solver):
     d = _bench("--solver", solver, "--scale", "48", "--steps", "1", "--warmup", "1",
                *(["--s", "6"] if solver == "sstep" else []))
-    assert d["solver"] == solver and d["config"]["status"] == "converged"
+    assert d["solver"] == solver and d["solve"]["status"] == "converged"
 
 
 def test_bench_reference_arm_small(gpu_ready):
-    d = _bench("--impl", "reference", "--scale", "32", "--steps", "1", "--warmup", "1")
+    d = _bench("--impl", "reference", "--config", "c3", "--scale", "32", "--steps", "1",
+               "--warmup", "1")
     assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
+    ours = _bench("--config", "c3", "--scale", "32", "--steps", "1", "--warmup", "1", "--no-cpu")
+    assert ours["config"] == d["config"]  # the driver's same_config check

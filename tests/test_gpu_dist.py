@@ -124,17 +124,25 @@ def test_partitioned_value_stream(gpu_ready, key, jacobi, world):
     n = 12
     prob = problems.make_problem(key, scale=n)
     kw = dict(sigma=10, eps_star=1e-8, basis_kind="newton", max_outer=30)
-    x1, t1, c1 = adaptive_solve(prob, AdaptiveConfig(**kw), trace="fast")
+    info = {}
+    x1, t1, c1 = adaptive_solve(prob, AdaptiveConfig(**kw), trace="fast", info=info)
     grp = VirtualGroup(Varcoef27Rows(n, jacobi=jacobi), world, depth=kw["sigma"])
     assert [pl.mpk_schedule(10)["kind"] for pl in grp.plans] == ["stencil values"] * world
-    xg, tg, cg, _ = grp.solve(prob, AdaptiveConfig(**kw))
+    xg, tg, cg, logs = grp.solve(prob, AdaptiveConfig(**kw))
     if world == 1:
         np.testing.assert_array_equal(xg, x1)
         np.testing.assert_array_equal(cg.alphas, c1.alphas)
         return
-    got = [(r.s_tilde, r.s_actual) for r in tg.outer_records[:3]]
-    assert got == [(r.s_tilde, r.s_actual) for r in t1.outer_records[:3]]
-    np.testing.assert_allclose(cg.alphas[:5], c1.alphas[:5], rtol=1e-8)
+    # the first block's Gram differs only in summation order (per-rank partials)
+    g1, gg = info["first_gram"], logs.first_gram
+    scale = np.sqrt(np.outer(np.diag(g1), np.diag(g1)))
+    assert np.all(np.abs(gg - g1) <= 1e-12 * scale)
+    # decisions agree until the noise horizon of this ill-conditioned operator
+    # (c4j 12^3 moves s~ at outer loop 3 under a reordered Gram sum)
+    got = [(r.s_tilde, r.s_actual) for r in tg.outer_records[:2]]
+    assert got == [(r.s_tilde, r.s_actual) for r in t1.outer_records[:2]]
+    m = sum(r.s_actual for r in t1.outer_records[:2])
+    np.testing.assert_allclose(cg.alphas[:m], c1.alphas[:m], rtol=1e-8)
 
 
 def test_device_group_single_process(gpu_ready):
