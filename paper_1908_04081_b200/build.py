@@ -23,7 +23,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libsscg.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["mpk.cu", "gram.cu", "rec.cu", "small.cu", "hscg.cu", "setup.cu", "dist.cu", "plan.cu"]
+SOURCES = ["mpk.cu", "tmarch.cu", "gram.cu", "rec.cu", "small.cu", "hscg.cu", "setup.cu", "dist.cu", "plan.cu"]
 NO_FMAD = {"small.cu", "hscg.cu"}
 
 

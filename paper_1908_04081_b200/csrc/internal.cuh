@@ -12,6 +12,7 @@
 //   SolverState  all control state of adaptive_solve (adaptive.py:111-268): the
 //             outer loop runs without host round trips; the host only polls `done`.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -36,6 +37,15 @@
 #define SMALL_THREADS 512
 #define SS_MAX_NE 8                // union size of the unrolled superset-mask pattern kernels
 #define VS_MAX_NE 32               // union size of the value-stream stencil kernels
+#ifndef TM_R
+#define TM_R 6                     // TMA plane-march ring depth (stages per CTA)
+#endif
+
+// TMA tensor maps of the plane march (tmarch.cu): Y as [col][plane][line][x],
+// x and b as [plane][line][x], the 1-byte row ids as [plane][line][x]
+struct TmMaps {
+  CUtensorMap y, x, b, id;
+};
 
 struct RitzDev {  // ritz.py:28-158
   double hi_om, hi_h, hi_zeta;
@@ -182,6 +192,10 @@ struct Ctx {
   unsigned* zm_ctr;  // [2 (SMAX + 1)] per-level claim / done counters (levels >= 1), or NULL
   const int* zm_base;  // [zm_np] first local row of each plane (partitioned), or NULL (z * S)
   int zm_o;          // 2-D column tiles with line stride zm_o (0: 256 consecutive columns)
+  // TMA plane march (tmarch.cu; tm == nullptr: the register march): host
+  // pointer to the plan's tensor maps (passed to the kernel by value)
+  const TmMaps* tm;
+  int tm_grid;       // CTAs of its levels >= 1 (level 0: red_n)
   int pf_off;    // pattern kernels: L2 prefetch at row + pf_ahead * stride + pf_off (0: off)
   int pf_ahead;
   const unsigned* ss_mask;  // [pat_np]
@@ -196,6 +210,37 @@ __host__ __device__ inline int64_t lvl_p_rows(const Ctx& c, int sigma, int l) {
 __host__ __device__ inline int64_t lvl_r_rows(const Ctx& c, int sigma, int l) {
   const int d = sigma - 2 - l;
   return c.lvl_rows[d < 0 ? 0 : d];
+}
+
+// the level's column pointers, formed on the host: kept opaque to the
+// compiler's index arithmetic, so each gather is one wide add off a base
+// register instead of a re-derived column * ld product
+struct ZmPtrs {
+  const double* xs[3];
+  const double* ym[2];
+  double* yo[2];
+};
+
+inline ZmPtrs zm_ptrs(const Ctx& c, int l, int sigma) {
+  ZmPtrs z;
+  const int64_t ld = c.ld;
+  if (l == 0) {
+    z.xs[0] = c.x;
+    z.xs[1] = c.Y;
+    z.xs[2] = c.Y + (int64_t)(sigma + 1) * ld;
+    z.ym[0] = z.ym[1] = nullptr;
+    z.yo[0] = c.Y + ld;
+    z.yo[1] = c.Y + (int64_t)(sigma + 2) * ld;
+  } else {
+    z.xs[0] = c.Y + (int64_t)l * ld;
+    z.xs[1] = c.Y + (int64_t)(sigma + 1 + l) * ld;
+    z.xs[2] = nullptr;
+    z.ym[0] = z.xs[0] - ld;
+    z.ym[1] = z.xs[1] - ld;
+    z.yo[0] = c.Y + (int64_t)(l + 1) * ld;
+    z.yo[1] = c.Y + (int64_t)(sigma + 2 + l) * ld;
+  }
+  return z;
 }
 
 // halo exchange lists of a row-partitioned plan (dist.cu)
@@ -261,6 +306,11 @@ size_t ss_smem_bytes(int np);
 int ss_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 int zm_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 int vs_ctas_per_sm(int ne, int* out2);
+// tmarch.cu
+int tm_make_maps(TmMaps* m, const double* Y, int64_t ld, int ncols, const double* x, const double* b,
+                 const void* pid, int64_t o, int64_t S, int64_t planes, int64_t id_planes);
+void tm_occupancy(int pat_np, int zm_np, bool table, int* occ0, int* occ1);
+void launch_level_tm(const Ctx& c, int level, int sigma, cudaStream_t s);
 void staged_prepare(int cap);
 int staged_ctas_per_sm(int cap);
 // gram.cu (ld must be a multiple of gram_row_multiple(); padding rows zero)

@@ -591,37 +591,6 @@ __device__ __forceinline__ void zm_items(const Ctx& c, int lvl, const SsSmem& T,
   }
 }
 
-// the level's column pointers, formed on the host: kept opaque to the
-// compiler's index arithmetic, so each gather is one wide add off a base
-// register instead of a re-derived column * ld product
-struct ZmPtrs {
-  const double* xs[3];
-  const double* ym[2];
-  double* yo[2];
-};
-
-inline ZmPtrs zm_ptrs(const Ctx& c, int l, int sigma) {
-  ZmPtrs z;
-  const int64_t ld = c.ld;
-  if (l == 0) {
-    z.xs[0] = c.x;
-    z.xs[1] = c.Y;
-    z.xs[2] = c.Y + (int64_t)(sigma + 1) * ld;
-    z.ym[0] = z.ym[1] = nullptr;
-    z.yo[0] = c.Y + ld;
-    z.yo[1] = c.Y + (int64_t)(sigma + 2) * ld;
-  } else {
-    z.xs[0] = c.Y + (int64_t)l * ld;
-    z.xs[1] = c.Y + (int64_t)(sigma + 1 + l) * ld;
-    z.xs[2] = nullptr;
-    z.ym[0] = z.xs[0] - ld;
-    z.ym[1] = z.xs[1] - ld;
-    z.yo[0] = c.Y + (int64_t)(l + 1) * ld;
-    z.yo[1] = c.Y + (int64_t)(sigma + 2 + l) * ld;
-  }
-  return z;
-}
-
 #ifndef ZM0_MINB  // 64 registers, no spills: 4 CTAs/SM (1.52 vs 1.58 ms/outer at 3)
 #define ZM0_MINB 4
 #endif
@@ -1189,6 +1158,10 @@ void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s) {
       default: VS_LAUNCH(32) break;
     }
 #undef VS_LAUNCH
+    return;
+  }
+  if (c.tm) {  // the TMA plane march (tmarch.cu)
+    launch_level_tm(c, level, sigma, s);
     return;
   }
   if (c.pid && c.ss_ne > 0 && c.zm_S > 0) {

@@ -136,6 +136,10 @@ struct sscg_plan {
   int* d_zm_base = nullptr;  // plane table of a partitioned march
   unsigned* d_zm_ctr = nullptr;  // dynamic item counters of the level kernels
   int zm_zc = 0, zm_ncb = 0, zm_o = 0, zm_zc0 = 0;
+  // TMA plane march (tmarch.cu): on for 2-D-tiled 7-slot marches
+  int tm_on = 0, tm_grid = 0;
+  int64_t tm_planes = 0, tm_id_planes = 0;
+  TmMaps tm{};
   int64_t zm_items0 = 0;
   int64_t zm_items = 0;
   // host <-> device staging of the solve's vectors (copy_h2d / copy_d2h):
@@ -189,6 +193,9 @@ int ensure_work(sscg_plan* p, int sigma, int64_t max_outer, int leja_grid) {
     TRY(dalloc(p, &p->d_Y, (size_t)p->ld * ncols));
     CUDA_OK(cudaMemset(p->d_Y, 0, sizeof(double) * (size_t)p->ld * ncols));
     p->sigma_alloc = sigma;
+    if (p->tm_on)  // the maps point at Y: rebuild them for the new block
+      TRY(tm_make_maps(&p->tm, p->d_Y, p->ld, ncols, p->d_x, p->d_b, p->d_pid, p->zm_o, p->zm_S,
+                       p->tm_planes, p->tm_id_planes));
     if (p->gexec) {
       cudaGraphExecDestroy(p->gexec);
       p->gexec = nullptr;
@@ -268,6 +275,8 @@ Ctx make_ctx(sscg_plan* p) {
   c.pat_ptr = p->d_pat_ptr;
   c.pat_off = p->d_pat_off;
   c.pat_val = p->d_pat_val;
+  c.tm = p->tm_on ? &p->tm : nullptr;
+  c.tm_grid = p->tm_grid;
   c.pf_off = p->pf_off;
   c.pf_ahead = p->pf_ahead;
   c.zm_S = p->zm_S;
@@ -874,6 +883,21 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       }
       p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * zocc[0], (int64_t)RED_BLOCKS, p->zm_items0}));
       p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, p->zm_items));
+      // TMA plane march: the 2-D tiled 7-slot form, 1-byte ids, whole planes
+      // (SSCG_TM=0: the register march)
+      const int64_t nl = bases.empty() ? n_rows : n_local;
+      if (o > 0 && ne == 7 && p->pid_bytes == 1 && nl % S == 0 && n_rows % S == 0 &&
+          atoi(env_or("SSCG_TM", "1")) != 0) {
+        int t0 = 0, t1 = 0;
+        tm_occupancy(np, p->zm_np, !bases.empty(), &t0, &t1);
+        if (t0 >= 1 && t1 >= 1) {
+          p->tm_on = 1;
+          p->tm_planes = nl / S;
+          p->tm_id_planes = n_rows / S;
+          p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * t0, (int64_t)RED_BLOCKS, p->zm_items0}));
+          p->tm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * t1, p->zm_items));
+        }
+      }
     }
   }
   // a global-offset table is only valid for the march (the other kernels

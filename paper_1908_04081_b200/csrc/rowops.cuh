@@ -3,6 +3,8 @@
 // TMA-staged CSR tiles or the pattern-compressed operator, the basis
 // recurrence step.  Header-only, internal linkage (one copy per .cu).
 #pragma once
+#include <cstdio>
+
 #include "internal.cuh"
 
 namespace {
@@ -136,11 +138,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+#ifdef MBAR_DEBUG
+// debug side builds: a timed-out wait records (count, block, thread, barrier,
+// parity) here and gives up instead of trapping, so the host can read it
+__device__ unsigned g_mbar_dbg[8];
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   uint32_t spins = 0;
   while (!done) {
+#ifdef MBAR_DEBUG
+    if (++spins > (1u << 20)) {
+      if (atomicAdd(&g_mbar_dbg[0], 1u) == 0) {
+        g_mbar_dbg[1] = blockIdx.x;
+        g_mbar_dbg[2] = threadIdx.x;
+        g_mbar_dbg[3] = smem_u32(bar);
+        g_mbar_dbg[4] = parity;
+      }
+      return;
+    }
+#else
     if (++spins > (1u << 26)) __trap();  // a lost transaction must fail, not hang
+#endif
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"

@@ -1,0 +1,448 @@
+// tmarch.cu -- K_mpk for 7-point stencil operators: the plane march fed by TMA.
+//
+// Reference: basis.py:210-225 `_recurrence_columns` over lacore.py:25-34 `spmv`
+// (scipy csr_matvec), the same per-row arithmetic as every other level kernel
+// (mpk.cu): row sum over the union [-S, -o, -1, 0, +1, +o, +S] in stored order
+// with separately rounded products and adds, then the recurrence op by op --
+// bit-identical to csr_matvec / the CSR kernels.
+//
+// Layout: a work item is a 32 x 8 tile of a plane (32 columns of a line, 8
+// lines of stride o) marched over zc planes.  Warp 8 of the CTA (one elected
+// thread) is the producer: for every plane of its items it issues one 4-D TMA
+// box per input vector -- the tile plus its halo, 36 x 10 doubles, out
+// of bounds filled with zeros -- plus the tile's 1-byte row ids (and b on level
+// 0) into a ring of TM_R shared-memory stages, each completed on an mbarrier
+// (expect_tx).  Warps 0-7 are consumers: warp w owns line w of the tile and
+// walks the planes keeping x[r - S], x[r], x[r + S] in registers (one
+// shared-memory read per vector and plane brings the plane ahead), reading the
+// +-1 / +-o neighbours from the staged plane.  A consumer warp releases a stage
+// by one arrive on its `empty` barrier (8 arrivals per phase); there is no
+// CTA-wide barrier on the per-plane path, so warps drift by up to the ring
+// depth and the producer keeps TM_R - 2 planes of every input vector in flight
+// per CTA (the HBM stream the register march could not keep deep enough).
+//
+// Roofline (HBM): per level 1 byte of row id + 16 bytes per row and generated
+// column (in + out; + 8 for a Chebyshev two-back read; + x and b on level 0).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "internal.cuh"
+#include "rowops.cuh"
+
+namespace {
+
+// staged tile + halo (doubles): 8 lines + 1 above and below; 32 columns + 2
+// each side -- a box's first x coordinate must be 16-byte aligned, so the
+// one-cell halo in x is loaded as two (x0 - 2 .. x0 + 33)
+constexpr int TM_W = 36, TM_H = 10, TM_XH = 2;
+constexpr int TM_BOX = TM_W * TM_H;                // 360
+constexpr int TM_BOXB = (TM_BOX * 8 + 127) / 128 * 128;  // 2944: 128-byte aligned boxes
+constexpr int TM_THREADS = 288;                    // 8 consumer warps + 1 producer warp
+#ifndef TM_MINB
+#define TM_MINB 3  // CTAs per SM the register budget must allow (72 registers)
+#endif
+
+__host__ __device__ constexpr int tm_stage_bytes(int nv, bool l0) {
+  return nv * TM_BOXB + (l0 ? 2048 : 0) + 256;
+}
+__host__ __device__ constexpr uint32_t tm_tx_bytes(int nv, bool l0) {
+  return (uint32_t)(nv * TM_BOX * 8 + (l0 ? 2048 : 0) + 256);
+}
+__host__ __device__ inline size_t tm_head_bytes(int pat_np, int zm_np, bool table) {
+  const size_t a = (size_t)pat_np * SS_MAX_NE * 8 + (table ? 4 * (size_t)zm_np : 0);
+  return (a + 127) / 128 * 128;
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_plain(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumers_bar() {
+  asm volatile("bar.sync 1, 256;\n" ::: "memory");
+}
+
+template <bool UNIT>
+__device__ __forceinline__ double tm_recur(double ay, double y, double y2, double th, double ga,
+                                           double mu, bool use_mu) {
+  double w = __dsub_rn(ay, __dmul_rn(th, y));
+  if (use_mu) w = __dsub_rn(w, __dmul_rn(mu, y2));
+  return UNIT ? w : __ddiv_rn(w, ga);
+}
+
+// One launch of a level.  NV input vectors: level 0 (L0) x, P_0, R_0 -> P_1,
+// R_1 (+ ||b - A x||^2 and ||r||^2 partials); levels >= 1 P_l, R_l ->
+// P_{l+1}, R_{l+1} (NV = 2) or P alone (NV = 1, the block's last level).  RK:
+// bit 0 non-unit gamma, bit 1 two-back term (mu != 0) -- read from the device
+// state, so the kernel picks the instantiation (the graph is captured once).
+// dyn: levels >= 1 claim items from a counter while a Leja chain runs beside
+// them (a CTA whose SM slot a Leja kernel holds starts late and takes fewer
+// items); level 0 keeps a fixed assignment (deterministic norm partials).
+struct TmShared {
+  uint64_t* full;
+  uint64_t* empty;
+  int* sitem;
+  double (*red)[8];
+  const double* pval;
+  const int* ptab;
+  unsigned char* stg;
+};
+
+template <int NV, bool L0, int RK>
+__device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, const TmMaps& maps,
+                                        const TmShared& sh, bool dyn, bool do_r) {
+  constexpr bool UNIT = (RK & 1) == 0, MU = (RK & 2) != 0 && !L0;
+  constexpr int NO = L0 ? NV - 1 : NV;  // output vectors
+  constexpr int Q0 = L0 ? 1 : 0;        // first input with an output
+  constexpr int SB = tm_stage_bytes(L0 ? 3 : 2, L0);  // stage stride (the kernel's largest NV)
+  constexpr int IDO = (L0 ? 3 : 2) * TM_BOXB + (L0 ? 2048 : 0);  // row ids within a stage
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool table = c.zm_base != nullptr;
+  const int S = (int)c.zm_S, o = c.zm_o, lines = S / o, ntx = o >> 5;
+  const int ncb = ntx * ((lines + 7) >> 3);
+  const int np = c.zm_np;
+  const int zcs = L0 ? c.zm_zc0 : c.zm_zc;
+  const int items = (int)(L0 ? c.zm_items0 : c.zm_items);
+  const int sigma = c.cfg->sigma;
+  uint64_t* full = sh.full;
+  uint64_t* empty = sh.empty;
+  unsigned char* stg = sh.stg;
+
+  if (warp == 8) {  // ---------------------------------------------- producer
+    if (lane != 0) return;
+    // Y columns of the inputs (4-D map [col][plane][line][x]); level 0's x has
+    // its own 3-D map
+    int colq[3];
+    if (L0) {
+      colq[0] = -1;
+      colq[1] = 0;
+      colq[2] = sigma + 1;
+    } else {
+      colq[0] = l;
+      colq[1] = sigma + 1 + l;
+      colq[2] = -1;
+    }
+    unsigned* ctr = dyn ? c.zm_ctr + 2 * l : nullptr;
+    uint32_t k = 0;
+    int it = dyn ? (int)atomicAdd(ctr, 1u) : blockIdx.x;
+    for (;;) {
+      if (it >= items) {  // end marker: one stage carrying item -1, no data
+        const int s0 = k % TM_R;
+        if (k >= TM_R) mbar_wait(&empty[s0], ((k / TM_R) - 1) & 1);
+        sh.sitem[s0] = -1;
+        mbar_arrive_plain(&full[s0]);
+        break;
+      }
+      const int cb = it % ncb, zc = it / ncb;
+      const int x0 = (cb % ntx) * 32, y0 = (cb / ntx) * 8;
+      const int z0 = zc * zcs, z1 = min(z0 + zcs, np);
+      for (int zz = z0 - 1; zz <= z1; ++zz, ++k) {
+        const int s = k % TM_R;
+        if (k >= TM_R) mbar_wait(&empty[s], ((k / TM_R) - 1) & 1);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        if (zz == z0 - 1) sh.sitem[s] = it;
+        // plane coordinate: geometric plane -> local block (plane table) or
+        // itself; outside the walk -1 (zero fill)
+        const int pz = (zz >= 0 && zz < np) ? (table ? sh.ptab[zz] / S : zz) : -1;
+        unsigned char* dst = stg + (size_t)s * SB;
+        mbar_arrive_tx(&full[s], tm_tx_bytes(NV, L0));
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          if (L0 && q == 0)
+            tma_load_3d(dst, &maps.x, x0 - TM_XH, y0 - 1, pz, &full[s]);
+          else
+            tma_load_4d(dst + q * TM_BOXB, &maps.y, x0 - TM_XH, y0 - 1, pz, colq[q], &full[s]);
+        }
+        if (L0) tma_load_3d(dst + 3 * TM_BOXB, &maps.b, x0, y0, pz, &full[s]);
+        tma_load_3d(dst + IDO, &maps.id, x0, y0, pz, &full[s]);
+      }
+      it = dyn ? (int)atomicAdd(ctr, 1u) : it + (int)gridDim.x;
+    }
+    if (dyn && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+      atomicExch(ctr, 0u);  // the last producer out resets the counters for the next launch
+      atomicExch(ctr + 1, 0u);
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------- consumers
+  const SolverState* st = c.st;
+  const double th = st->prm.th[L0 ? 0 : l], ga = st->prm.ga[L0 ? 0 : l];
+  const double mu = L0 ? 0.0 : st->prm.mu[l - 1];
+  const int plim = (int)lvl_p_rows(c, sigma, L0 ? 0 : l);
+  const int rlim = do_r ? (int)lvl_r_rows(c, sigma, L0 ? 0 : l) : 0;
+  const int n_own = (int)c.n_own;
+  const int cpos = (warp + 1) * TM_W + (lane + TM_XH);
+  double tt = 0.0, rr = 0.0;
+  int bad = 0;
+  uint32_t k = 0;
+  for (;;) {
+    // the item's first stage: plane z0 - 1 (and the item id)
+    const int s = k % TM_R;
+    mbar_wait(&full[s], (k / TM_R) & 1);
+    const int it = sh.sitem[s];
+    if (it < 0) break;
+    const int cb = it % ncb, zc = it / ncb;
+    const int x0 = (cb % ntx) * 32, y0 = (cb / ntx) * 8;
+    const int z0 = zc * zcs, z1 = min(z0 + zcs, np);
+    const int line = y0 + warp, colx = x0 + lane;
+    const bool live = line < lines;
+    double pv[NV], cu[NV], nx[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+      pv[q] = reinterpret_cast<const double*>(stg + (size_t)s * SB + q * TM_BOXB)[cpos];
+    __syncwarp();
+    if (lane == 0) mbar_arrive_plain(&empty[s]);
+    ++k;
+    int sc = k % TM_R;
+    mbar_wait(&full[sc], (k / TM_R) & 1);
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+      cu[q] = reinterpret_cast<const double*>(stg + (size_t)sc * SB + q * TM_BOXB)[cpos];
+    ++k;
+    for (int z = z0; z < z1; ++z, ++k) {
+      const int s1 = k % TM_R;
+      mbar_wait(&full[s1], (k / TM_R) & 1);
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+        nx[q] = reinterpret_cast<const double*>(stg + (size_t)s1 * SB + q * TM_BOXB)[cpos];
+      const unsigned char* cur = stg + (size_t)sc * SB;
+      const int r = (table ? sh.ptab[z] : z * S) + line * o + colx;
+      if (live && r < plim) {
+        const int pid = cur[IDO + warp * 32 + lane];
+        const double2* v2 = reinterpret_cast<const double2*>(sh.pval + pid * SS_MAX_NE);
+        const double2 va = v2[0], vb = v2[1], vc = v2[2], vd = v2[3];
+        const double v[7] = {va.x, va.y, vb.x, vb.y, vc.x, vc.y, vd.x};
+        double acc[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          const double* bx = reinterpret_cast<const double*>(cur + q * TM_BOXB);
+          const double xb[7] = {pv[q], bx[cpos - TM_W], bx[cpos - 1], cu[q], bx[cpos + 1],
+                                bx[cpos + TM_W], nx[q]};
+          double a = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 7; ++kk) a = __dadd_rn(a, __dmul_rn(v[kk], xb[kk]));
+          acc[q] = a;
+        }
+        if (L0 && r < n_own) {
+          const double bi = reinterpret_cast<const double*>(cur + 3 * TM_BOXB)[warp * 32 + lane];
+          const double t = __dsub_rn(bi, acc[0]);
+          tt = fma(t, t, tt);
+          rr = fma(cu[NV - 1], cu[NV - 1], rr);
+        }
+#pragma unroll
+        for (int q = 0; q < NO; ++q) {
+          if (q == NO - 1 && NO > 1 && r >= rlim) break;
+          const double y2 = MU ? __ldg(zp.ym[q] + r) : 0.0;
+          const double w = tm_recur<UNIT>(acc[Q0 + q], cu[Q0 + q], y2, th, ga, mu, MU);
+          zp.yo[q][r] = w;
+          bad |= !finite(w);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_plain(&empty[sc]);
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        pv[q] = cu[q];
+        cu[q] = nx[q];
+      }
+      sc = s1;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_plain(&empty[sc]);  // plane z1 (k already points past it)
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&c.st->breakdown, 1);
+  if (L0) {  // fixed-order partials of this CTA (static item assignment)
+    tt = warp_sum(tt);
+    rr = warp_sum(rr);
+    if (lane == 0) {
+      sh.red[0][warp] = tt;
+      sh.red[1][warp] = rr;
+    }
+    consumers_bar();
+    if (tid == 0) {
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        a += sh.red[0][w];
+        b += sh.red[1][w];
+      }
+      c.part_t[blockIdx.x] = a;
+      c.part_r[blockIdx.x] = b;
+    }
+  }
+}
+
+template <bool L0>
+__global__ void __launch_bounds__(TM_THREADS, TM_MINB)
+    k_level_tm(Ctx c, int l, ZmPtrs zp, const __grid_constant__ TmMaps maps) {
+  const SolverState* st = c.st;
+  if (st->done) return;
+  const int sbar = st->s_bar;
+  if (!L0 && l >= sbar) return;
+  extern __shared__ __align__(128) unsigned char tsm[];
+  __shared__ __align__(8) uint64_t full[TM_R], empty[TM_R];
+  __shared__ int sitem[TM_R];
+  __shared__ double red[2][8];
+  const int tid = threadIdx.x;
+  const bool table = c.zm_base != nullptr;
+  double* pval = reinterpret_cast<double*>(tsm);
+  int* ptab = reinterpret_cast<int*>(tsm + (size_t)c.pat_np * SS_MAX_NE * 8);
+  for (int j = tid; j < c.pat_np * SS_MAX_NE; j += blockDim.x) pval[j] = __ldg(c.ss_val + j);
+  if (table)
+    for (int j = tid; j < c.zm_np; j += blockDim.x) ptab[j] = __ldg(c.zm_base + j);
+  if (tid == 0) {
+    for (int s = 0; s < TM_R; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  TmShared sh{full, empty, sitem, red, pval, ptab,
+              tsm + tm_head_bytes(c.pat_np, c.zm_np, table)};
+  if (L0) {
+    const bool do_r = sbar >= 2;
+    if (st->prm.ga[0] == 1.0)
+      tm_body<3, true, 0>(c, 0, zp, maps, sh, false, do_r);
+    else
+      tm_body<3, true, 1>(c, 0, zp, maps, sh, false, do_r);
+    return;
+  }
+  const double ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
+  const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
+  const int rk = (ga == 1.0 ? 0 : 1) | (use_mu ? 2 : 0);
+  const bool do_r = l < sbar - 1;
+  const bool dyn = c.zm_ctr != nullptr && st->leja_on;
+#define TM_RK(NV)                                                      \
+  switch (rk) {                                                        \
+    case 0: tm_body<NV, false, 0>(c, l, zp, maps, sh, dyn, do_r); break; \
+    case 1: tm_body<NV, false, 1>(c, l, zp, maps, sh, dyn, do_r); break; \
+    case 2: tm_body<NV, false, 2>(c, l, zp, maps, sh, dyn, do_r); break; \
+    default: tm_body<NV, false, 3>(c, l, zp, maps, sh, dyn, do_r); break; \
+  }
+  if (do_r) {
+    TM_RK(2)
+  } else {
+    TM_RK(1)
+  }
+#undef TM_RK
+}
+
+template <bool L0>
+size_t tm_smem(const Ctx& c) {
+  return tm_head_bytes(c.pat_np, c.zm_np, c.zm_base != nullptr) +
+         (size_t)TM_R * tm_stage_bytes(L0 ? 3 : 2, L0);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int encode(CUtensorMap* m, CUtensorMapDataType t, int rank, const void* base, const uint64_t* dims,
+           const uint64_t* strides, const uint32_t* box) {
+  auto fn = encode_fn();
+  if (!fn) return sscg_fail(SSCG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    if (i < rank - 1) st[i] = strides[i];
+  }
+  const CUresult r = fn(m, t, (cuuint32_t)rank, const_cast<void*>(base), d, st, b, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return sscg_fail(SSCG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SSCG_OK;
+}
+
+}  // namespace
+
+#ifdef MBAR_DEBUG
+extern "C" int sscg_debug_mbar(unsigned* out8) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, g_mbar_dbg, sizeof(unsigned) * 8);
+  const unsigned zero[8] = {};
+  cudaMemcpyToSymbol(g_mbar_dbg, zero, sizeof(zero));
+  return (int)cudaGetLastError();
+}
+#endif
+
+// tensor maps of one plan: Y (4-D [col][plane][line][x] over every allocated
+// column), x and b (3-D, level 0) and the 1-byte row ids (3-D)
+int tm_make_maps(TmMaps* m, const double* Y, int64_t ld, int ncols, const double* x, const double* b,
+                 const void* pid, int64_t o, int64_t S, int64_t planes, int64_t id_planes) {
+  const uint64_t lines = (uint64_t)(S / o);
+  {
+    const uint64_t dims[4] = {(uint64_t)o, lines, (uint64_t)planes, (uint64_t)ncols};
+    const uint64_t str[3] = {8ull * o, 8ull * S, 8ull * ld};
+    const uint32_t box[4] = {TM_W, TM_H, 1, 1};
+    int rc = encode(&m->y, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, Y, dims, str, box);
+    if (rc) return rc;
+  }
+  const uint64_t dims3[3] = {(uint64_t)o, lines, (uint64_t)planes};
+  const uint64_t str3[2] = {8ull * o, 8ull * S};
+  {
+    const uint32_t box[3] = {TM_W, TM_H, 1};
+    int rc = encode(&m->x, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, x, dims3, str3, box);
+    if (rc) return rc;
+  }
+  {
+    const uint32_t box[3] = {32, 8, 1};
+    int rc = encode(&m->b, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, b, dims3, str3, box);
+    if (rc) return rc;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)o, lines, (uint64_t)id_planes};
+    const uint64_t str[2] = {(uint64_t)o, (uint64_t)S};
+    const uint32_t box[3] = {32, 8, 1};
+    int rc = encode(&m->id, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, pid, dims, str, box);
+    if (rc) return rc;
+  }
+  return SSCG_OK;
+}
+
+// CTAs per SM of level 0 / levels >= 1 (with the dynamic shared memory the
+// plan's pattern table and plane table need)
+void tm_occupancy(int pat_np, int zm_np, bool table, int* occ0, int* occ1) {
+  const int lim = 200 * 1024;
+  cudaFuncSetAttribute(k_level_tm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_level_tm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  const size_t head = tm_head_bytes(pat_np, zm_np, table);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ0, k_level_tm<true>, TM_THREADS,
+                                                head + (size_t)TM_R * tm_stage_bytes(3, true));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ1, k_level_tm<false>, TM_THREADS,
+                                                head + (size_t)TM_R * tm_stage_bytes(2, false));
+}
+
+void launch_level_tm(const Ctx& c, int level, int sigma, cudaStream_t s) {
+  const ZmPtrs zp = zm_ptrs(c, level, sigma);
+  if (level == 0)
+    k_level_tm<true><<<c.red_n, TM_THREADS, tm_smem<true>(c), s>>>(c, 0, zp, *c.tm);
+  else
+    k_level_tm<false><<<c.tm_grid, TM_THREADS, tm_smem<false>(c), s>>>(c, level, zp, *c.tm);
+}

@@ -22,7 +22,7 @@ from paper_1908_04081_b200.adaptive import LogBuffers, make_config  # noqa: E402
 
 KEYS = ("SSCG_PATTERN", "SSCG_STAGE_MAX_KB", "SSCG_LEJA_HEAD", "SSCG_PAT_SS", "SSCG_PF",
         "SSCG_PF_AHEAD", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_ZM_DYN", "SSCG_LEJA_AFTER0",
-        "SSCG_ZM_ZC0", "SSCG_VS")
+        "SSCG_ZM_ZC0", "SSCG_VS", "SSCG_TM")
 
 
 def main():
@@ -33,8 +33,8 @@ def main():
     args = ap.parse_args()
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import bench
-    key, scale, sigma, basis, eps, desc = bench.CONFIGS[args.config]
-    prob = problems.make_problem(key, scale=scale)
+    key, sigma, basis, eps, _, desc = bench.CONFIGS[args.config]
+    prob = problems.make_problem(key)
     lib = L.load()
     cfg = AdaptiveConfig(sigma=sigma, eps_star=eps, basis_kind=basis, max_outer=args.outer)
     cfg, ccfg = make_config(cfg, prob, "fast")
@@ -56,16 +56,6 @@ def main():
         L.check(lib.sscg_fetch(plan.handle, None, logs.s))
         outer = int(logs.s.total_outer)
         dbg = None
-        if hasattr(lib, "sscg_debug_wave_counters"):  # WAVE_DBG side build
-            buf = (C.c_ulonglong * 8)()
-            lib.sscg_debug_wave_counters(buf)  # reset
-            L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
-            lib.sscg_debug_wave_counters(buf)
-            g = list(buf)
-            dbg = {"cons_full_wait_frac": g[0] / max(1, g[1]), "cons_items_w0": g[2],
-                   "prod_dep_wait_frac": g[3] / max(1, g[6]), "prod_stage_wait_frac": g[4] / max(1, g[6]),
-                   "prod_rp_frac": g[5] / max(1, g[6]), "spins": g[7],
-                   "cons_cycles_per_item": g[1] / max(1, g[2])}
         L.check(lib.sscg_set_profiling(plan.handle, 1))
         L.check(lib.sscg_run(plan.handle, ccfg, logs.s))
         L.check(lib.sscg_set_profiling(plan.handle, 0))
