@@ -894,6 +894,15 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
           p->tm_on = 1;
           p->tm_planes = nl / S;
           p->tm_id_planes = n_rows / S;
+          // planes per item of levels >= 1: the producer streams across item
+          // boundaries, so items may be longer (each costs two extra planes
+          // of staging) -- about 1.7 per CTA, at most 32 (c5w: 32, 1.255 vs
+          // 1.288 ms per outer at 24)
+          if (atoi(env_or("SSCG_ZM_ZC", "0")) <= 0) {
+            const int64_t g1 = (int64_t)sms * t1;
+            p->zm_zc = (int)std::max<int64_t>(2, std::min<int64_t>(32, ncb * steps * 10 / (g1 * 17)));
+            p->zm_items = ncb * ((steps + p->zm_zc - 1) / p->zm_zc);
+          }
           p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * t0, (int64_t)RED_BLOCKS, p->zm_items0}));
           p->tm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * t1, p->zm_items));
         }

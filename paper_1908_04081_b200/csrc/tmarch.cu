@@ -41,6 +41,13 @@ constexpr int TM_THREADS = 288;                    // 8 consumer warps + 1 produ
 #ifndef TM_MINB
 #define TM_MINB 3  // CTAs per SM the register budget must allow (72 registers)
 #endif
+#ifndef TM_R0
+#define TM_R0 TM_R  // ring depth of level 0 (larger stages: x, P_0, R_0, b)
+#endif
+template <bool L0>
+struct Ring {
+  static constexpr int R = L0 ? TM_R0 : TM_R;
+};
 
 __host__ __device__ constexpr int tm_stage_bytes(int nv, bool l0) {
   return nv * TM_BOXB + (l0 ? 2048 : 0) + 256;
@@ -68,6 +75,38 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, int
       " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];\n" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+// consumer wait on a full barrier (phase parity ph): a lost transaction traps
+__device__ __forceinline__ void tm_wait(uint32_t bar, uint32_t ph) {
+  uint32_t done = 0, spins = 0;
+  for (;;) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(ph)
+        : "memory");
+    if (done) break;
+    if (++spins > (1u << 26)) __trap();
+  }
 }
 __device__ __forceinline__ void mbar_arrive_plain(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
@@ -106,6 +145,7 @@ template <int NV, bool L0, int RK>
 __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, const TmMaps& maps,
                                         const TmShared& sh, bool dyn, bool do_r) {
   constexpr bool UNIT = (RK & 1) == 0, MU = (RK & 2) != 0 && !L0;
+  constexpr int RING = Ring<L0>::R;
   constexpr int NO = L0 ? NV - 1 : NV;  // output vectors
   constexpr int Q0 = L0 ? 1 : 0;        // first input with an output
   constexpr int SB = tm_stage_bytes(L0 ? 3 : 2, L0);  // stage stride (the kernel's largest NV)
@@ -141,8 +181,8 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
     int it = dyn ? (int)atomicAdd(ctr, 1u) : blockIdx.x;
     for (;;) {
       if (it >= items) {  // end marker: one stage carrying item -1, no data
-        const int s0 = k % TM_R;
-        if (k >= TM_R) mbar_wait(&empty[s0], ((k / TM_R) - 1) & 1);
+        const int s0 = k % RING;
+        if (k >= RING) mbar_wait(&empty[s0], ((k / RING) - 1) & 1);
         sh.sitem[s0] = -1;
         mbar_arrive_plain(&full[s0]);
         break;
@@ -151,8 +191,8 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
       const int x0 = (cb % ntx) * 32, y0 = (cb / ntx) * 8;
       const int z0 = zc * zcs, z1 = min(z0 + zcs, np);
       for (int zz = z0 - 1; zz <= z1; ++zz, ++k) {
-        const int s = k % TM_R;
-        if (k >= TM_R) mbar_wait(&empty[s], ((k / TM_R) - 1) & 1);
+        const int s = k % RING;
+        if (k >= RING) mbar_wait(&empty[s], ((k / RING) - 1) & 1);
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         if (zz == z0 - 1) sh.sitem[s] = it;
         // plane coordinate: geometric plane -> local block (plane table) or
@@ -180,66 +220,76 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
   }
 
   // ------------------------------------------------------------- consumers
+  // shared-memory addresses as 32-bit shared-window offsets, formed once
+  // (every per-plane access below is an explicit ld.shared / mbarrier op)
   const SolverState* st = c.st;
   const double th = st->prm.th[L0 ? 0 : l], ga = st->prm.ga[L0 ? 0 : l];
   const double mu = L0 ? 0.0 : st->prm.mu[l - 1];
   const int plim = (int)lvl_p_rows(c, sigma, L0 ? 0 : l);
   const int rlim = do_r ? (int)lvl_r_rows(c, sigma, L0 ? 0 : l) : 0;
   const int n_own = (int)c.n_own;
-  const int cpos = (warp + 1) * TM_W + (lane + TM_XH);
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+  const uint32_t cpos8 = 8u * (uint32_t)((warp + 1) * TM_W + (lane + TM_XH));
+  const uint32_t my0 = smem_u32(stg) + cpos8;                       // centre, stage 0, vector 0
+  const uint32_t id0 = smem_u32(stg) + IDO + (uint32_t)(warp * 32 + lane);  // row id, stage 0
+  const uint32_t pv0 = smem_u32(sh.pval);
   double tt = 0.0, rr = 0.0;
-  int bad = 0;
-  uint32_t k = 0;
+  unsigned badm = 0;
+  int s = 0;        // stage of the next plane to consume
+  uint32_t ph = 0;  // its phase parity
+  auto advance = [&]() {
+    if (++s == RING) {
+      s = 0;
+      ph ^= 1u;
+    }
+  };
   for (;;) {
     // the item's first stage: plane z0 - 1 (and the item id)
-    const int s = k % TM_R;
-    mbar_wait(&full[s], (k / TM_R) & 1);
+    tm_wait(full0 + 8u * s, ph);
     const int it = sh.sitem[s];
     if (it < 0) break;
     const int cb = it % ncb, zc = it / ncb;
     const int x0 = (cb % ntx) * 32, y0 = (cb / ntx) * 8;
     const int z0 = zc * zcs, z1 = min(z0 + zcs, np);
-    const int line = y0 + warp, colx = x0 + lane;
+    const int line = y0 + warp;
+    const int rel = line * o + x0 + lane;  // row within its plane
     const bool live = line < lines;
     double pv[NV], cu[NV], nx[NV];
 #pragma unroll
-    for (int q = 0; q < NV; ++q)
-      pv[q] = reinterpret_cast<const double*>(stg + (size_t)s * SB + q * TM_BOXB)[cpos];
+    for (int q = 0; q < NV; ++q) pv[q] = lds_f64(my0 + s * SB + q * TM_BOXB);
     __syncwarp();
-    if (lane == 0) mbar_arrive_plain(&empty[s]);
-    ++k;
-    int sc = k % TM_R;
-    mbar_wait(&full[sc], (k / TM_R) & 1);
+    if (lane == 0) mbar_arrive_u32(empty0 + 8u * s);
+    advance();
+    tm_wait(full0 + 8u * s, ph);
 #pragma unroll
-    for (int q = 0; q < NV; ++q)
-      cu[q] = reinterpret_cast<const double*>(stg + (size_t)sc * SB + q * TM_BOXB)[cpos];
-    ++k;
-    for (int z = z0; z < z1; ++z, ++k) {
-      const int s1 = k % TM_R;
-      mbar_wait(&full[s1], (k / TM_R) & 1);
+    for (int q = 0; q < NV; ++q) cu[q] = lds_f64(my0 + s * SB + q * TM_BOXB);
+    int sc = s;
+    advance();
+    for (int z = z0; z < z1; ++z) {
+      tm_wait(full0 + 8u * s, ph);
 #pragma unroll
-      for (int q = 0; q < NV; ++q)
-        nx[q] = reinterpret_cast<const double*>(stg + (size_t)s1 * SB + q * TM_BOXB)[cpos];
-      const unsigned char* cur = stg + (size_t)sc * SB;
-      const int r = (table ? sh.ptab[z] : z * S) + line * o + colx;
+      for (int q = 0; q < NV; ++q) nx[q] = lds_f64(my0 + s * SB + q * TM_BOXB);
+      const int r = (table ? sh.ptab[z] : z * S) + rel;
       if (live && r < plim) {
-        const int pid = cur[IDO + warp * 32 + lane];
-        const double2* v2 = reinterpret_cast<const double2*>(sh.pval + pid * SS_MAX_NE);
-        const double2 va = v2[0], vb = v2[1], vc = v2[2], vd = v2[3];
-        const double v[7] = {va.x, va.y, vb.x, vb.y, vc.x, vc.y, vd.x};
+        const uint32_t cur = my0 + sc * SB;  // this plane's centre
+        const uint32_t pid = lds_u8(id0 + sc * SB);
+        const uint32_t va = pv0 + pid * (SS_MAX_NE * 8);
+        const double2 v01 = lds_f64x2(va), v23 = lds_f64x2(va + 16), v45 = lds_f64x2(va + 32);
+        const double v6 = lds_f64(va + 48);
+        const double v[7] = {v01.x, v01.y, v23.x, v23.y, v45.x, v45.y, v6};
         double acc[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-          const double* bx = reinterpret_cast<const double*>(cur + q * TM_BOXB);
-          const double xb[7] = {pv[q], bx[cpos - TM_W], bx[cpos - 1], cu[q], bx[cpos + 1],
-                                bx[cpos + TM_W], nx[q]};
+          const uint32_t bx = cur + q * TM_BOXB;
+          const double xb[7] = {pv[q], lds_f64(bx - 8 * TM_W), lds_f64(bx - 8), cu[q],
+                                lds_f64(bx + 8), lds_f64(bx + 8 * TM_W), nx[q]};
           double a = 0.0;
 #pragma unroll
           for (int kk = 0; kk < 7; ++kk) a = __dadd_rn(a, __dmul_rn(v[kk], xb[kk]));
           acc[q] = a;
         }
         if (L0 && r < n_own) {
-          const double bi = reinterpret_cast<const double*>(cur + 3 * TM_BOXB)[warp * 32 + lane];
+          const double bi = lds_f64(smem_u32(stg) + sc * SB + 3 * TM_BOXB + 8u * (warp * 32 + lane));
           const double t = __dsub_rn(bi, acc[0]);
           tt = fma(t, t, tt);
           rr = fma(cu[NV - 1], cu[NV - 1], rr);
@@ -250,21 +300,24 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
           const double y2 = MU ? __ldg(zp.ym[q] + r) : 0.0;
           const double w = tm_recur<UNIT>(acc[Q0 + q], cu[Q0 + q], y2, th, ga, mu, MU);
           zp.yo[q][r] = w;
-          bad |= !finite(w);
+          // exponent all ones (inf / NaN) carries into bit 31: checked once at the end
+          badm |= (((unsigned)__double2hiint(w)) & 0x7ff00000u) + 0x00100000u;
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_plain(&empty[sc]);
+      if (lane == 0) mbar_arrive_u32(empty0 + 8u * sc);
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
         pv[q] = cu[q];
         cu[q] = nx[q];
       }
-      sc = s1;
+      sc = s;
+      advance();
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive_plain(&empty[sc]);  // plane z1 (k already points past it)
+    if (lane == 0) mbar_arrive_u32(empty0 + 8u * sc);  // plane z1
   }
+  const int bad = (badm & 0x80000000u) != 0;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&c.st->breakdown, 1);
   if (L0) {  // fixed-order partials of this CTA (static item assignment)
     tt = warp_sum(tt);
@@ -295,8 +348,9 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB)
   const int sbar = st->s_bar;
   if (!L0 && l >= sbar) return;
   extern __shared__ __align__(128) unsigned char tsm[];
-  __shared__ __align__(8) uint64_t full[TM_R], empty[TM_R];
-  __shared__ int sitem[TM_R];
+  constexpr int RING = Ring<L0>::R;
+  __shared__ __align__(8) uint64_t full[RING], empty[RING];
+  __shared__ int sitem[RING];
   __shared__ double red[2][8];
   const int tid = threadIdx.x;
   const bool table = c.zm_base != nullptr;
@@ -306,7 +360,7 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB)
   if (table)
     for (int j = tid; j < c.zm_np; j += blockDim.x) ptab[j] = __ldg(c.zm_base + j);
   if (tid == 0) {
-    for (int s = 0; s < TM_R; ++s) {
+    for (int s = 0; s < RING; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 8);
     }
@@ -346,7 +400,7 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB)
 template <bool L0>
 size_t tm_smem(const Ctx& c) {
   return tm_head_bytes(c.pat_np, c.zm_np, c.zm_base != nullptr) +
-         (size_t)TM_R * tm_stage_bytes(L0 ? 3 : 2, L0);
+         (size_t)Ring<L0>::R * tm_stage_bytes(L0 ? 3 : 2, L0);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -434,7 +488,7 @@ void tm_occupancy(int pat_np, int zm_np, bool table, int* occ0, int* occ1) {
   cudaFuncSetAttribute(k_level_tm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   const size_t head = tm_head_bytes(pat_np, zm_np, table);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ0, k_level_tm<true>, TM_THREADS,
-                                                head + (size_t)TM_R * tm_stage_bytes(3, true));
+                                                head + (size_t)TM_R0 * tm_stage_bytes(3, true));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ1, k_level_tm<false>, TM_THREADS,
                                                 head + (size_t)TM_R * tm_stage_bytes(2, false));
 }
