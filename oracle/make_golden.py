@@ -514,6 +514,11 @@ def solve_cases():
                       dict(sigma=10, eps_star=1e-8, basis_kind="newton", max_outer=400)),
         "solve_c4jp": (lambda: to_ref(problems.make_problem("c4j", scale=12)),
                        dict(sigma=10, eps_star=1e-8, basis_kind="newton")),
+        # full-size c4j (192^3, 5 outer loops): its third block's nested condition
+        # estimates sit at the noise level (~1/sqrt(u)), so the reference's own
+        # perturbed runs show how far its decisions are determined
+        "full_c4j": (lambda: to_ref(problems.make_problem("c4j")),
+                     dict(sigma=10, eps_star=1e-8, basis_kind="newton", max_outer=5)),
         "solve_494bus_old": (lambda: bus, dict(sigma=5, eps_star=1e-6, variant="old",
                                                basis_kind="monomial", c_strategy="unit")),
         "solve_494bus_cheb6": (lambda: bus, dict(sigma=6, eps_star=1e-8, basis_kind="chebyshev")),
@@ -558,7 +563,9 @@ def gen_noise():
             continue
         prob = mk()
         rows, seqs, lmins, lmaxs = [], [], [], []
-        for pname, spec in PERTURBATIONS.items():
+        keep = os.environ.get("NOISE_PERTS")
+        perts = {k: v for k, v in PERTURBATIONS.items() if not keep or k in keep.split(",")}
+        for pname, spec in perts.items():
             gfn, cfn = spec[0], spec[1]
             ref_basis.gram = gfn or orig
             ref_lacore.nested_basis_conds = cfn or orig_conds
@@ -580,7 +587,7 @@ def gen_noise():
             lmaxs.append(tr.lambda_max[-1] if tr.lambda_max else np.nan)
         save("noise_" + name, counts=np.array(rows, dtype=float), seq8=np.array(seqs),
              lmin_end=np.array(lmins), lmax_end=np.array(lmaxs),
-             names=np.array(list(PERTURBATIONS)))
+             names=np.array(list(perts)))
         print(f"    noise {name}: outer/total {[(int(r[0]), int(r[1])) for r in rows]}")
 
 

@@ -15,8 +15,8 @@
 // (expect_tx).  Warps 0-7 are consumers: warp w owns line w of the tile and
 // walks the planes keeping x[r - S], x[r], x[r + S] in registers (one
 // shared-memory read per vector and plane brings the plane ahead), reading the
-// +-1 / +-o neighbours from the staged plane.  A consumer warp releases a stage
-// by one arrive on its `empty` barrier (8 arrivals per phase); there is no
+// +-1 / +-o neighbours from the staged plane.  Each consumer thread releases a
+// stage by its own arrive on the stage's `empty` barrier (256 per phase); there is no
 // CTA-wide barrier on the per-plane path, so warps drift by up to the ring
 // depth and the producer keeps TM_R - 2 planes of every input vector in flight
 // per CTA (the HBM stream the register march could not keep deep enough).
@@ -25,6 +25,8 @@
 // column (in + out; + 8 for a Chebyshev two-back read; + x and b on level 0).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <type_traits>
 
 #include "internal.cuh"
 #include "rowops.cuh"
@@ -141,6 +143,15 @@ struct TmShared {
   unsigned char* stg;
 };
 
+// work item -> (tile, planes [z0, z1))
+template <bool L0>
+__device__ __forceinline__ void tm_item(const Ctx& c, int it, int ncb, int& cb, int& z0, int& z1) {
+  const int zcs = L0 ? c.zm_zc0 : c.zm_zc;
+  cb = it % ncb;
+  z0 = (it / ncb) * zcs;
+  z1 = min(z0 + zcs, c.zm_np);
+}
+
 template <int NV, bool L0, int RK>
 __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, const TmMaps& maps,
                                         const TmShared& sh, bool dyn, bool do_r) {
@@ -155,7 +166,6 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
   const int S = (int)c.zm_S, o = c.zm_o, lines = S / o, ntx = o >> 5;
   const int ncb = ntx * ((lines + 7) >> 3);
   const int np = c.zm_np;
-  const int zcs = L0 ? c.zm_zc0 : c.zm_zc;
   const int items = (int)(L0 ? c.zm_items0 : c.zm_items);
   const int sigma = c.cfg->sigma;
   uint64_t* full = sh.full;
@@ -187,9 +197,9 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
         mbar_arrive_plain(&full[s0]);
         break;
       }
-      const int cb = it % ncb, zc = it / ncb;
+      int cb, z0, z1;
+      tm_item<L0>(c, it, ncb, cb, z0, z1);
       const int x0 = (cb % ntx) * 32, y0 = (cb / ntx) * 8;
-      const int z0 = zc * zcs, z1 = min(z0 + zcs, np);
       for (int zz = z0 - 1; zz <= z1; ++zz, ++k) {
         const int s = k % RING;
         if (k >= RING) mbar_wait(&empty[s], ((k / RING) - 1) & 1);
@@ -233,6 +243,7 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
   const uint32_t my0 = smem_u32(stg) + cpos8;                       // centre, stage 0, vector 0
   const uint32_t id0 = smem_u32(stg) + IDO + (uint32_t)(warp * 32 + lane);  // row id, stage 0
   const uint32_t pv0 = smem_u32(sh.pval);
+  const uint32_t b0 = smem_u32(stg) + 3 * TM_BOXB + 8u * (uint32_t)(warp * 32 + lane);  // level 0's b
   double tt = 0.0, rr = 0.0;
   unsigned badm = 0;
   int s = 0;        // stage of the next plane to consume
@@ -243,79 +254,106 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
       ph ^= 1u;
     }
   };
+  // one plane of the walk: wait for plane z + 1 (its centre -> nn), row z
+  // from the current stage sc with x[r - S] = p, x[r] = c, x[r + S] = nn;
+  // then release sc.  Every consumer thread arrives on `empty` itself (256
+  // arrivals per phase: no warp-level sync on the per-plane path).  CHECK:
+  // the item may hold rows outside this level's range (tile past the last
+  // line, ghost depth beyond the level) -- else every row computes.
+  auto step = [&](auto check, double (&p)[NV], double (&cc)[NV], double (&nn)[NV], int z,
+                  int rel, int& sc) {
+    constexpr bool CHECK = decltype(check)::value;
+    tm_wait(full0 + 8u * s, ph);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) nn[q] = lds_f64(my0 + s * SB + q * TM_BOXB);
+    const int r = (table ? sh.ptab[z] : z * S) + rel;
+    if (!CHECK || r < plim) {
+      const uint32_t cur = my0 + sc * SB;  // this plane's centre
+      const uint32_t pid = lds_u8(id0 + sc * SB);
+      const uint32_t va = pv0 + pid * (SS_MAX_NE * 8);
+      const double2 v01 = lds_f64x2(va), v23 = lds_f64x2(va + 16), v45 = lds_f64x2(va + 32);
+      const double v6 = lds_f64(va + 48);
+      const double v[7] = {v01.x, v01.y, v23.x, v23.y, v45.x, v45.y, v6};
+      double acc[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const uint32_t bx = cur + q * TM_BOXB;
+        const double xb[7] = {p[q], lds_f64(bx - 8 * TM_W), lds_f64(bx - 8), cc[q],
+                              lds_f64(bx + 8), lds_f64(bx + 8 * TM_W), nn[q]};
+        double a = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 7; ++kk) a = __dadd_rn(a, __dmul_rn(v[kk], xb[kk]));
+        acc[q] = a;
+      }
+      if (L0 && r < n_own) {
+        const double bi = lds_f64(b0 + sc * SB);
+        const double t = __dsub_rn(bi, acc[0]);
+        tt = fma(t, t, tt);
+        rr = fma(cc[NV - 1], cc[NV - 1], rr);
+      }
+#pragma unroll
+      for (int q = 0; q < NO; ++q) {
+        if (q == NO - 1 && NO > 1 && r >= rlim) break;
+        const double y2 = MU ? __ldg(zp.ym[q] + r) : 0.0;
+        const double w = tm_recur<UNIT>(acc[Q0 + q], cc[Q0 + q], y2, th, ga, mu, MU);
+        zp.yo[q][r] = w;
+        // exponent all ones (inf / NaN) carries into bit 31: checked once at the end
+        badm |= (((unsigned)__double2hiint(w)) & 0x7ff00000u) + 0x00100000u;
+      }
+    }
+    mbar_arrive_u32(empty0 + 8u * sc);
+    sc = s;
+    advance();
+  };
   for (;;) {
     // the item's first stage: plane z0 - 1 (and the item id)
     tm_wait(full0 + 8u * s, ph);
     const int it = sh.sitem[s];
     if (it < 0) break;
-    const int cb = it % ncb, zc = it / ncb;
+    int cb, z0, z1;
+    tm_item<L0>(c, it, ncb, cb, z0, z1);
     const int x0 = (cb % ntx) * 32, y0 = (cb / ntx) * 8;
-    const int z0 = zc * zcs, z1 = min(z0 + zcs, np);
     const int line = y0 + warp;
     const int rel = line * o + x0 + lane;  // row within its plane
+    // rows of this item: all below plim unless the tile passes the last line
+    // or a plane lies at a ghost depth this level does not compute
+    bool all_in = line < lines;
+    if (table) {
+      for (int z = z0; z < z1 && all_in; ++z) all_in = sh.ptab[z] + rel < plim;
+    } else {
+      all_in = all_in && (z1 - 1) * S + rel < plim;
+    }
     const bool live = line < lines;
     double pv[NV], cu[NV], nx[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) pv[q] = lds_f64(my0 + s * SB + q * TM_BOXB);
-    __syncwarp();
-    if (lane == 0) mbar_arrive_u32(empty0 + 8u * s);
+    mbar_arrive_u32(empty0 + 8u * s);
     advance();
     tm_wait(full0 + 8u * s, ph);
 #pragma unroll
     for (int q = 0; q < NV; ++q) cu[q] = lds_f64(my0 + s * SB + q * TM_BOXB);
     int sc = s;
     advance();
-    for (int z = z0; z < z1; ++z) {
-      tm_wait(full0 + 8u * s, ph);
-#pragma unroll
-      for (int q = 0; q < NV; ++q) nx[q] = lds_f64(my0 + s * SB + q * TM_BOXB);
-      const int r = (table ? sh.ptab[z] : z * S) + rel;
-      if (live && r < plim) {
-        const uint32_t cur = my0 + sc * SB;  // this plane's centre
-        const uint32_t pid = lds_u8(id0 + sc * SB);
-        const uint32_t va = pv0 + pid * (SS_MAX_NE * 8);
-        const double2 v01 = lds_f64x2(va), v23 = lds_f64x2(va + 16), v45 = lds_f64x2(va + 32);
-        const double v6 = lds_f64(va + 48);
-        const double v[7] = {v01.x, v01.y, v23.x, v23.y, v45.x, v45.y, v6};
-        double acc[NV];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          const uint32_t bx = cur + q * TM_BOXB;
-          const double xb[7] = {pv[q], lds_f64(bx - 8 * TM_W), lds_f64(bx - 8), cu[q],
-                                lds_f64(bx + 8), lds_f64(bx + 8 * TM_W), nx[q]};
-          double a = 0.0;
-#pragma unroll
-          for (int kk = 0; kk < 7; ++kk) a = __dadd_rn(a, __dmul_rn(v[kk], xb[kk]));
-          acc[q] = a;
-        }
-        if (L0 && r < n_own) {
-          const double bi = lds_f64(smem_u32(stg) + sc * SB + 3 * TM_BOXB + 8u * (warp * 32 + lane));
-          const double t = __dsub_rn(bi, acc[0]);
-          tt = fma(t, t, tt);
-          rr = fma(cu[NV - 1], cu[NV - 1], rr);
-        }
-#pragma unroll
-        for (int q = 0; q < NO; ++q) {
-          if (q == NO - 1 && NO > 1 && r >= rlim) break;
-          const double y2 = MU ? __ldg(zp.ym[q] + r) : 0.0;
-          const double w = tm_recur<UNIT>(acc[Q0 + q], cu[Q0 + q], y2, th, ga, mu, MU);
-          zp.yo[q][r] = w;
-          // exponent all ones (inf / NaN) carries into bit 31: checked once at the end
-          badm |= (((unsigned)__double2hiint(w)) & 0x7ff00000u) + 0x00100000u;
-        }
+    // planes in threes: the x[r - S], x[r], x[r + S] registers rotate by name
+    if (all_in) {
+      for (int z = z0; z < z1; z += 3) {
+        step(std::false_type{}, pv, cu, nx, z, rel, sc);
+        if (z + 1 >= z1) break;
+        step(std::false_type{}, cu, nx, pv, z + 1, rel, sc);
+        if (z + 2 >= z1) break;
+        step(std::false_type{}, nx, pv, cu, z + 2, rel, sc);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_u32(empty0 + 8u * sc);
-#pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        pv[q] = cu[q];
-        cu[q] = nx[q];
+    } else {
+      const int relc = live ? rel : INT32_MAX / 2;  // a dead line never computes
+      for (int z = z0; z < z1; z += 3) {
+        step(std::true_type{}, pv, cu, nx, z, relc, sc);
+        if (z + 1 >= z1) break;
+        step(std::true_type{}, cu, nx, pv, z + 1, relc, sc);
+        if (z + 2 >= z1) break;
+        step(std::true_type{}, nx, pv, cu, z + 2, relc, sc);
       }
-      sc = s;
-      advance();
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive_u32(empty0 + 8u * sc);  // plane z1
+    mbar_arrive_u32(empty0 + 8u * sc);  // plane z1
   }
   const int bad = (badm & 0x80000000u) != 0;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&c.st->breakdown, 1);
@@ -362,7 +400,7 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB)
   if (tid == 0) {
     for (int s = 0; s < RING; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 8);
+      mbar_init(&empty[s], 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }

@@ -10,11 +10,13 @@ vectors and the CPU oracle, at the north-star tolerances:
   * final true residual ||b - A x|| / ||b|| <= eps*.
 """
 
+import os
+
 import numpy as np
 import pytest
 import scipy.sparse as sp
 
-from conftest import cfg_of, golden, golden_problem, problem_from_arrays
+from conftest import GOLDEN, cfg_of, golden, golden_problem, problem_from_arrays
 from oracle import sscg_oracle as O
 from paper_1908_04081_b200 import (
     AdaptiveConfig,
@@ -445,43 +447,57 @@ def test_edge_cases(gpu_ready):
     assert tr.s_schedule[:5] == ref_tr.s_schedule[:5] and tr.converged
 
 
-def test_full_size_c3_first_outer_loops(gpu_ready):
-    """c3 at its BASELINE size (128^3): first-5 s sequence, first Gram, Ritz
-    and alphas against the oracle (bounded to 5 outer loops on the CPU); the
-    full GPU solve converges to eps* checked with an independent host SpMV."""
-    prob = problems.make_problem("c3")
-    cfg = dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev")
-    ox, otr, oal, _ = O.solve_problem(prob, O.OracleConfig(max_outer=5, **cfg),
-                                      diagnostics=False)
-    x, tr, co = solve(prob, AdaptiveConfig(**cfg), trace="fast")
-    got = [(r.s_tilde, r.s_actual) for r in tr.outer_records[:5]]
-    assert got == [(r.s_tilde, r.s_actual) for r in otr.outer_records[:5]]
-    gram_close(tr._first_gram, otr.first_gram)
-    m = otr.total_iters
-    np.testing.assert_allclose(co.alphas[:m], oal, rtol=1e-8)
-    np.testing.assert_allclose(tr.lambda_max[:m], otr.lambda_max, rtol=1e-8)
-    np.testing.assert_allclose(tr.lambda_min[:m], otr.lambda_min, rtol=1e-8)
-    assert tr.converged and true_rel(prob, x) <= 1e-10
-    # survey probe of the reference on the same config: 46 outer / 425 total
-    assert abs(tr.total_outer - 46) <= 0.05 * 46 and abs(tr.total_iters - 425) <= 0.05 * 425
+FULL_CASES = [("full_c3", "c3"), ("full_c5w", "c5w"), ("full_c4", "c4"), ("full_c4j", "c4j")]
 
 
-@pytest.mark.slow
-def test_full_size_c5w_first_outer_loops(gpu_ready):
-    """The headline workload at its bench size (256^3, sigma = 12 Newton, the
-    plane-march kernels): first-2 s sequence, first Gram, Ritz and alphas
-    against the oracle bounded to 2 outer loops on the CPU (~25 s); the full
-    GPU solve converges to eps* checked with an independent host SpMV."""
-    prob = problems.make_problem("c5w")
-    cfg = dict(sigma=12, eps_star=1e-10, basis_kind="newton")
-    ox, otr, oal, _ = O.solve_problem(prob, O.OracleConfig(max_outer=2, **cfg),
-                                      diagnostics=False)
+@pytest.mark.parametrize("name,key", FULL_CASES, ids=[k for _, k in FULL_CASES])
+def test_full_size_against_reference_run(gpu_ready, name, key):
+    """BASELINE configs at their full size against the REFERENCE's own runs
+    (oracle/make_golden.py gen_full: adaptive_solve of /root/reference on this
+    exact problem, as shipped): c3 128^3 and c5w 256^3 (the headline) to
+    convergence, c4 / c4j 192^3 (the value-stream kernels) for 5 outer loops.
+    North-star bar: first Gram 1e-12, the (s~, s_actual) sequence identical
+    for the first 5 outer loops, Ritz estimates and alphas 1e-8 through them,
+    outer / total counts within 2%, the final true residual <= eps*."""
+    ref = golden(name)
+    cfg = cfg_of(ref)
+    prob = problems.make_problem(key)
     x, tr, co = solve(prob, AdaptiveConfig(**cfg), trace="fast")
-    got = [(r.s_tilde, r.s_actual) for r in tr.outer_records[:2]]
-    assert got == [(r.s_tilde, r.s_actual) for r in otr.outer_records[:2]]
-    gram_close(tr._first_gram, otr.first_gram)
-    m = otr.total_iters
-    np.testing.assert_allclose(co.alphas[:m], oal, rtol=1e-8)
-    np.testing.assert_allclose(tr.lambda_max[:m], otr.lambda_max, rtol=1e-8)
-    np.testing.assert_allclose(tr.lambda_min[:m], otr.lambda_min, rtol=1e-8)
-    assert tr.converged and true_rel(prob, x) <= 1e-10
+    gram_close(tr._first_gram, ref["first_g"])
+    recs = ref["rec_int"]
+    # where the reference's own perturbed runs (Gram summation order,
+    # eigensolver, libm) move its decisions, the comparison stops there (c4j:
+    # its third block's nested condition estimates are at the noise level)
+    noisy = os.path.exists(os.path.join(GOLDEN, "noise_" + name + ".npz"))
+    horizon = noise_floor(name, ref)[0] if noisy else 5
+    k5 = min(5, horizon, len(recs))
+    got = np.array([[r.s_tilde, r.s_actual] for r in tr.outer_records[:k5]]).reshape(-1, 2)
+    np.testing.assert_array_equal(got, recs[:k5, 2:4])
+    m = int(ref["outer_marks"][k5 - 1] + recs[k5 - 1, 3])
+    np.testing.assert_allclose(co.alphas[:m], ref["alphas"][:m], rtol=1e-8)
+    np.testing.assert_allclose(co.betas[:m], ref["betas"][:m], rtol=1e-8)
+    for k in ("lambda_min", "lambda_max"):
+        np.testing.assert_allclose(np.array(getattr(tr, k))[:m], ref[k][:m], rtol=1e-8)
+    flags = ref["flags"]
+    n_tot, n_out = int(flags[3]), int(flags[4])
+    if noisy:  # inside the envelope of the reference's perturbed runs, widened 2%
+        env = count_envelope(name, ref)
+        for got_c, (lo, hi), refc in ((tr.total_outer, env[0], n_out),
+                                      (tr.total_iters, env[1], n_tot)):
+            tol = max(0.02 * refc, 1)
+            assert lo - tol <= got_c <= hi + tol, (got_c, refc, (lo, hi))
+    else:
+        assert abs(tr.total_outer - n_out) <= max(1, 0.02 * n_out), (tr.total_outer, n_out)
+        assert abs(tr.total_iters - n_tot) <= max(1, 0.02 * n_tot), (tr.total_iters, n_tot)
+    assert [tr.converged, tr.stagnated, tr.diverged] == [bool(v) for v in flags[:3]]
+    rel = true_rel(prob, x)
+    if tr.converged:
+        assert rel <= cfg["eps_star"] and tr.final_true_resid <= cfg["eps_star"]
+    elif k5 == 5:  # a bounded run on the same trajectory: the same residual
+        assert rel == pytest.approx(float(ref["final_true"]), rel=1e-6)
+    if k5 < 5:
+        return
+    # the iterate itself: its first entries against the reference's
+    head = np.asarray(ref["x_head"])
+    err = np.max(np.abs(x[:len(head)] - head)) / max(np.max(np.abs(head)), 1e-300)
+    assert err <= (1e-6 if tr.converged else 1e-9), err

@@ -22,7 +22,7 @@ from paper_1908_04081_b200.adaptive import LogBuffers, make_config  # noqa: E402
 
 KEYS = ("SSCG_PATTERN", "SSCG_STAGE_MAX_KB", "SSCG_LEJA_HEAD", "SSCG_PAT_SS", "SSCG_PF",
         "SSCG_PF_AHEAD", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_ZM_DYN", "SSCG_LEJA_AFTER0",
-        "SSCG_ZM_ZC0", "SSCG_VS", "SSCG_TM")
+        "SSCG_ZM_ZC0", "SSCG_VS", "SSCG_TM", "SSCG_TM_TAIL")
 
 
 def main():
