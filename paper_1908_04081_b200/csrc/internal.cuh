@@ -121,6 +121,7 @@ struct Ctx {
   double* part_d;   // [3][RED_BLOCKS] full-trace partials
   double* part_g;   // [GRAM_BLOCKS][GPACK] Gram partials
   double* leja_obj; // [leja_grid] scratch
+  int leja_grid_host;  // cfg->leja_grid as the host knew it at launch / capture
   // logs (device)
   double* it_log;   // [cap_iters][SSCG_IT_N]
   int* rec_i;       // [cap_outer][SSCG_REC_NI]

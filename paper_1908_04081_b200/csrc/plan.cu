@@ -88,7 +88,7 @@ struct sscg_plan {
   int hs_ss = 1;        // HSCG row sums through the superset mask
   cudaEvent_t ev_leja[SMAX] = {};
   cudaGraphExec_t gexec = nullptr;
-  int g_sigma = -1, g_full = -1;
+  int g_sigma = -1, g_full = -1, g_grid = -1;
   // census of the outer-loop graph last built: [0] ncclAllReduce calls, [1]
   // grouped halo exchanges, [2] NCCL kernel nodes, [3] kernel nodes, [4] nodes
   int census[5] = {-1, -1, -1, -1, -1};
@@ -253,6 +253,7 @@ Ctx make_ctx(sscg_plan* p) {
   c.part_d = p->d_part_d;
   c.part_g = p->d_part_g;
   c.leja_obj = p->d_leja;
+  c.leja_grid_host = p->cfg.leja_grid;
   c.it_log = p->d_it;
   c.rec_i = p->d_ri;
   c.rec_d = p->d_rd;
@@ -418,7 +419,8 @@ void graph_census(cudaGraph_t g, int* census) {
 }
 
 int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
-  if (p->gexec && p->g_sigma == sigma && p->g_full == full) return SSCG_OK;
+  if (p->gexec && p->g_sigma == sigma && p->g_full == full && p->g_grid == c.leja_grid_host)
+    return SSCG_OK;
   if (p->gexec) {
     cudaGraphExecDestroy(p->gexec);
     p->gexec = nullptr;
@@ -443,6 +445,7 @@ int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
   if (e != cudaSuccess) return sscg_fail_cuda(e, "cudaGraphInstantiate");
   p->g_sigma = sigma;
   p->g_full = full;
+  p->g_grid = c.leja_grid_host;
   return SSCG_OK;
 }
 

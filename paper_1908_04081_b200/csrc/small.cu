@@ -27,6 +27,7 @@ constexpr int NT = SMALL_THREADS;  // 512
 constexpr int NW = NT / 32;        // 16 warps
 constexpr int JLD = CMAX;          // work matrix leading dimension (odd: conflict-free row access)
 constexpr int LEJA_CAND_CAP = 256;
+constexpr int LEJA_SMEM_GRID = 16384;  // grid objective in shared memory up to this many points
 
 
 // ritz.py:164-171
@@ -429,14 +430,16 @@ __device__ __forceinline__ double np_sum_warp(double term, int n) {
   }
   return res;
 }
-__device__ __forceinline__ double leja_f(double x, const double* pts, int n) {
+// sum_j log|x - pts[j]| + 1e-300 in numpy's order; lane j holds pts[j] in pl
+__device__ __forceinline__ double leja_f(double x, double pl, int n) {
   const int lane = threadIdx.x & 31;
-  const double term = (lane < n) ? log(fabs(x - pts[lane]) + 1e-300) : 0.0;
+  const double term = (lane < n) ? log(fabs(x - pl) + 1e-300) : 0.0;
   return np_sum_warp(term, n);
 }
 // basis.py:70-88 golden-section maximisation (warp-uniform)
-__device__ void golden_refine(const double* pts, int n, double lo, double hi, double* xo,
+__device__ void golden_refine(const double* pts_, int n, double lo, double hi, double* xo,
                               double* vo) {
+  const double pts = (threadIdx.x & 31) < n ? pts_[threadIdx.x & 31] : 0.0;  // this lane's point
   const double ratio = (sqrt(5.0) - 1.0) / 2.0;
   double a = lo, b = hi;
   double c = b - ratio * (b - a);
@@ -466,6 +469,7 @@ __device__ void golden_refine(const double* pts, int n, double lo, double hi, do
 struct LejaShared {
   double pts[SMAX];
   double rx[4], rv[4];
+  double cval[LEJA_CAND_CAP];  // objective at each candidate (the sort reads no global memory)
   int cand[LEJA_CAND_CAP];
   int ncand;
   int top[4];
@@ -483,79 +487,133 @@ __device__ __forceinline__ double lin_x(int i, int grid, double lo, double hi, d
 // One greedy Leja step (basis.py:105-126, one pass of the `while` loop): given
 // pts[0..n-1] (in L.pts) and the grid objective of pts[0..n-2] in `obj` (global
 // scratch, carried between calls), append pts[n].  CTA-wide.
+#ifdef LEJA_DBG
+__device__ unsigned long long g_leja_dbg[8];
+#define LDBG(i)                                                             \
+  do {                                                                      \
+    __syncthreads();                                                        \
+    if (threadIdx.x == 0) {                                                 \
+      const long long t__ = clock64();                                      \
+      atomicAdd(&g_leja_dbg[i], (unsigned long long)(t__ - t_prev__));       \
+      t_prev__ = t__;                                                       \
+    }                                                                       \
+  } while (0)
+#else
+#define LDBG(i)
+#endif
+// One grid point's objective after adding pts[n-1] (pts[0..n-1] for n = 2, 8:
+// numpy's pairwise blocks restart there), from its value for pts[0..n-2]
+__device__ __forceinline__ double leja_obj_point(double x, double prev, int n, const double* pts) {
+  if (n == 2) {
+    double o = 0.0;
+    o += log(fabs(x - pts[0]) + 1e-300);
+    o += log(fabs(x - pts[1]) + 1e-300);
+    return o;
+  }
+  if (n == 8) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = log(fabs(x - pts[j]) + 1e-300);
+    return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  }
+  return prev + log(fabs(x - pts[n - 1]) + 1e-300);
+}
+
+// sobj: the objective in shared memory as well (k_leja_point, grid <=
+// LEJA_SMEM_GRID) -- the scans then read no global memory; nullptr: global only
 __device__ void cta_leja_point(double lo, double hi, int n, int grid, double* obj,
-                               LejaShared& L) {
+                               LejaShared& L, double* sobj = nullptr) {
+#ifdef LEJA_DBG
+  long long t_prev__ = clock64();
+#endif
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nt = blockDim.x;
   const double step = (hi - lo) / (double)(grid - 1);
   const bool zero_step = (step == 0.0);
-  // grid objective, incrementally in numpy's pairwise order (see np_sum_warp)
-  for (int i = tid; i < grid; i += nt) {
-    const double x = lin_x(i, grid, lo, hi, step, zero_step);
-    double o;
-    if (n == 2) {
-      o = 0.0;
-      o += log(fabs(x - L.pts[0]) + 1e-300);
-      o += log(fabs(x - L.pts[1]) + 1e-300);
-    } else if (n == 8) {
-      double r[8];
+  // grid objective, incrementally in numpy's pairwise order (see np_sum_warp);
+  // points in batches of 8 per thread: the loads of a batch are in flight
+  // together and its logs are independent
+  constexpr int LB = 8;
+  for (int i0 = tid; i0 < grid; i0 += LB * nt) {
+    double prev[LB];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = log(fabs(x - L.pts[j]) + 1e-300);
-      o = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    } else {
-      o = obj[i] + log(fabs(x - L.pts[n - 1]) + 1e-300);
+    for (int k = 0; k < LB; ++k) {
+      const int i = i0 + k * nt;
+      prev[k] = (n != 2 && n != 8 && i < grid) ? obj[i] : 0.0;
     }
-    obj[i] = o;
+#pragma unroll
+    for (int k = 0; k < LB; ++k) {
+      const int i = i0 + k * nt;
+      if (i < grid) {
+        const double o = leja_obj_point(lin_x(i, grid, lo, hi, step, zero_step), prev[k], n, L.pts);
+        obj[i] = o;
+        if (sobj) sobj[i] = o;
+      }
+    }
   }
+  const double* ob = sobj ? sobj : obj;
   if (tid == 0) L.ncand = 0;
   __syncthreads();
+  LDBG(0);
   // interior local maxima (>= both neighbours)
   for (int i = tid + 1; i < grid - 1; i += nt) {
-    const double v = obj[i];
-    if (v >= obj[i - 1] && v >= obj[i + 1]) {
+    const double v = ob[i];
+    if (v >= ob[i - 1] && v >= ob[i + 1]) {
       const int slot = atomicAdd(&L.ncand, 1);
-      if (slot < LEJA_CAND_CAP) L.cand[slot] = i;
+      if (slot < LEJA_CAND_CAP) {
+        L.cand[slot] = i;
+        L.cval[slot] = v;
+      }
     }
   }
   __syncthreads();
+  LDBG(1);
   if (tid == 0) {
     int nc = L.ncand < LEJA_CAND_CAP ? L.ncand : LEJA_CAND_CAP;
     if (nc == 0) {  // np.argmax: first maximal index
       int best = 0;
-      double bv = obj[0];
+      double bv = ob[0];
       for (int i = 1; i < grid; ++i)
-        if (obj[i] > bv) {
-          bv = obj[i];
+        if (ob[i] > bv) {
+          bv = ob[i];
           best = i;
         }
       L.cand[0] = best;
+      L.cval[0] = bv;
       nc = 1;
     }
-    // np.nonzero order (ascending index), then a stable ascending sort by value
+    // np.nonzero order (ascending index), then a stable ascending sort by
+    // value -- (index, value) pairs in shared memory
     for (int a = 1; a < nc; ++a) {
       const int v = L.cand[a];
+      const double ov = L.cval[a];
       int b = a - 1;
       while (b >= 0 && L.cand[b] > v) {
         L.cand[b + 1] = L.cand[b];
+        L.cval[b + 1] = L.cval[b];
         --b;
       }
       L.cand[b + 1] = v;
+      L.cval[b + 1] = ov;
     }
     for (int a = 1; a < nc; ++a) {
       const int v = L.cand[a];
-      const double ov = obj[v];
+      const double ov = L.cval[a];
       int b = a - 1;
-      while (b >= 0 && obj[L.cand[b]] > ov) {
+      while (b >= 0 && L.cval[b] > ov) {
         L.cand[b + 1] = L.cand[b];
+        L.cval[b + 1] = L.cval[b];
         --b;
       }
       L.cand[b + 1] = v;
+      L.cval[b + 1] = ov;
     }
     const int ntop = nc < 4 ? nc : 4;
     for (int a = 0; a < ntop; ++a) L.top[a] = L.cand[nc - ntop + a];
     L.ntop = ntop;
   }
   __syncthreads();
+  LDBG(2);
   if (warp < L.ntop) {
     const int i = L.top[warp];
     const int il = i - 1 > 0 ? i - 1 : 0;
@@ -569,6 +627,7 @@ __device__ void cta_leja_point(double lo, double hi, int n, int grid, double* ob
     }
   }
   __syncthreads();
+  LDBG(3);
   if (tid == 0) {
     double vmax = L.rv[0];
     for (int a = 1; a < L.ntop; ++a) vmax = py_max(vmax, L.rv[a]);
@@ -584,6 +643,10 @@ __device__ void cta_leja_point(double lo, double hi, int n, int grid, double* ob
     L.pts[n] = best;
   }
   __syncthreads();
+  LDBG(4);
+#ifdef LEJA_DBG
+  if (threadIdx.x == 0) atomicAdd(&g_leja_dbg[7], 1ull);
+#endif
 }
 
 // basis.py:91-127 leja_points, CTA-wide; obj is a global scratch of `grid` doubles
@@ -1108,11 +1171,14 @@ __global__ void k_params_begin(Ctx c) {
 // Leja point n (2 <= n < sigma) of the next block (basis.py:105-126)
 __global__ void __launch_bounds__(NT) k_leja_point(Ctx c, int n) {
   __shared__ LejaShared L;
+  extern __shared__ double lsm[];  // the grid objective (LEJA_SMEM_GRID points at most)
   SolverState* st = c.st;
   if (!st->leja_on || n >= c.cfg->sigma) return;
   if (threadIdx.x < n) L.pts[threadIdx.x] = st->prm.th[threadIdx.x];
   __syncthreads();
-  cta_leja_point(st->prm.lo, st->prm.hi, n, c.cfg->leja_grid, c.leja_obj, L);
+  const int grid = c.cfg->leja_grid;
+  cta_leja_point(st->prm.lo, st->prm.hi, n, grid, c.leja_obj, L,
+                 grid <= LEJA_SMEM_GRID ? lsm : nullptr);
   if (threadIdx.x == 0) st->prm.th[n] = L.pts[n];
 }
 
@@ -1270,6 +1336,8 @@ void ensure_attr() {
   cudaFuncSetAttribute(k_unit_conds, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_unit_params, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_unit_leja, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_leja_point, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       8 * LEJA_SMEM_GRID);
   mark_device_done(g_attr_set);
 }
 
@@ -1287,7 +1355,13 @@ void launch_state_init(const Ctx& c, cudaStream_t s) {
 void launch_small(const Ctx& c, cudaStream_t s) { k_small<<<1, NT, small_smem_bytes(), s>>>(c); }
 void launch_diag_fin(const Ctx& c, int j, cudaStream_t s) { k_diag_fin<<<1, NT, 0, s>>>(c, j); }
 void launch_params_begin(const Ctx& c, cudaStream_t s) { k_params_begin<<<1, 32, 0, s>>>(c); }
-void launch_leja_point(const Ctx& c, int n, cudaStream_t s) { k_leja_point<<<1, NT, 0, s>>>(c, n); }
+void launch_leja_point(const Ctx& c, int n, cudaStream_t s) {
+  // the grid objective in shared memory when it fits (sized from the host's
+  // leja_grid, known at capture: the plan rebuilds its graph when it changes)
+  const int grid = c.leja_grid_host;
+  const size_t bytes = grid <= LEJA_SMEM_GRID ? 8 * (size_t)grid : 0;
+  k_leja_point<<<1, NT, bytes, s>>>(c, n);
+}
 
 // ---- unit entry helpers (synchronous, own allocations) ----------------------
 #define U_OK(expr)                                   \
@@ -1396,3 +1470,13 @@ done:
 }
 
 double sscg_host_c0() { return host_c0(); }
+
+#ifdef LEJA_DBG
+extern "C" int sscg_debug_leja(unsigned long long* out8) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, g_leja_dbg, sizeof(unsigned long long) * 8);
+  const unsigned long long z[8] = {};
+  cudaMemcpyToSymbol(g_leja_dbg, z, sizeof(z));
+  return (int)cudaGetLastError();
+}
+#endif
