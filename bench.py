@@ -739,6 +739,80 @@ def run_reference(args, rank, world):
     print(json.dumps(line))
 
 
+def run_hscg_partitioned(args, rank, world):
+    """Distributed HSCG (classic CG, §8(f)2) on the same row slabs: one NCCL halo
+    exchange and two NCCL allreduces per iteration -- the baseline the s-step
+    solver's one synchronisation per outer loop is compared with."""
+    import scipy.sparse as sp
+    import torch
+
+    from paper_1908_04081_b200 import _lib as L
+    from paper_1908_04081_b200.classic import hscg_logs
+    from paper_1908_04081_b200.dist import hscg_partitioned
+    from paper_1908_04081_b200.partition import slab_bounds
+
+    dist = init_gloo(rank, world)
+    key, sigma, basis, eps, scaling, desc = CONFIGS[args.config]
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    key, nx, ny, nz = global_shape(args, world)
+    rows = partition_rows(key, nx, ny, nz)
+    n = rows.n
+    bnd = slab_bounds(n, world)
+    lo, hi = int(bnd[rank]), int(bnd[rank + 1])
+    if key in ("c4", "c4j"):
+        b_glob = rows.rhs()
+    else:
+        ip, cols, vals = rows.rows(np.arange(lo, hi))
+        xs = np.random.default_rng(0).uniform(-1.0, 1.0, n)
+        b_glob = np.zeros(n)
+        b_glob[lo:hi] = sp.csr_matrix((vals, cols, ip), shape=(hi - lo, n)) @ xs
+        del xs
+
+    def exchange(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    def bcast(bb):
+        obj = [bb]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    info = {}
+    hscg_partitioned(rows, b_glob, np.zeros(n), eps, rank, world, local, exchange, bcast,
+                     mode=args.hscg_mode, info=info)
+    plan, bl, x0l = info["plan"], info["b"], info["x0"]
+    lib = L.load()
+    iters, logs = hscg_logs(0)
+    mode = L.HSCG_MODES[args.hscg_mode]
+    ms = []
+    with ClockSampler(local) as clk:
+        for k in range(args.warmup + args.steps):
+            dist.barrier()
+            L.check(lib.sscg_hscg_ex(plan.handle, L.dptr(bl), L.dptr(x0l), float(eps),
+                                     info["max_iters"], mode, None, logs))
+            if k >= args.warmup:
+                ms.append(logs.device_ms)
+    t = torch.tensor([sum(ms) / len(ms)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    it = int(logs.total_iters)
+    status = {L.CONVERGED: "converged", L.STAGNATED: "stagnated",
+              L.DIVERGED: "diverged"}.get(int(logs.status), "max_iters")
+    units = world if scaling == "weak" else 1
+    if rank == 0:
+        print(json.dumps({
+            "metric": "cg_iterations_per_sec", "value": units * it / (t.item() / 1e3),
+            "unit": "iter/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t.item(), "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic, seeded", "impl": "ours",
+            "solver": "hscg", "config": workload_config(args, world),
+            "solve": {"n": n, "global_shape": [nx, ny, nz], "total_iters": it,
+                      "syncs_to_tol": 2 * it, "status": status, "hscg_mode": args.hscg_mode,
+                      "collectives": plan.collectives() if hasattr(plan, "collectives") else None},
+            "clocks": clk.summary()}))
+    dist.barrier()
+
+
 # ---------------------------------------------------------------------------
 def run_solver_compare(args):
     """--solver sstep|hscg (one GPU, informational, not the driver's headline):
@@ -762,8 +836,8 @@ def run_solver_compare(args):
             if args.solver == "hscg":
                 logs = L.SscgLogs()
                 logs.cap_iters, logs.iters = 0, None
-                L.check(lib.sscg_hscg(plan.handle, L.dptr(b), L.dptr(x0), float(eps), -1, None,
-                                      logs))
+                L.check(lib.sscg_hscg_ex(plan.handle, L.dptr(b), L.dptr(x0), float(eps), -1,
+                                         L.HSCG_MODES[args.hscg_mode], None, logs))
                 dev, it, sy = logs.device_ms, int(logs.total_iters), 2 * int(logs.total_iters)
                 status = {L.CONVERGED: "converged", L.STAGNATED: "stagnated",
                           L.DIVERGED: "diverged"}.get(int(logs.status), "max_iters")
@@ -789,7 +863,8 @@ def run_solver_compare(args):
         "data": "synthetic, seeded", "impl": "ours", "solver": args.solver,
         "config": workload_config(args, 1),
         "solve": {"n": n, "total_iters": iters, "syncs_to_tol": syncs, "status": status,
-                  **({"s": args.s or sigma} if args.solver == "sstep" else {})},
+                  **({"s": args.s or sigma} if args.solver == "sstep" else {}),
+                  **({"hscg_mode": args.hscg_mode} if args.solver == "hscg" else {})},
         "clocks": clk.summary()}))
 
 
@@ -809,6 +884,9 @@ def main():
     ap.add_argument("--solver", default="adaptive", choices=["adaptive", "sstep", "hscg"],
                     help="adaptive (the headline); sstep / hscg: one-GPU comparison lines")
     ap.add_argument("--s", type=int, default=None, help="fixed s for --solver sstep (default sigma)")
+    ap.add_argument("--hscg-mode", default="production", choices=["reference", "production"],
+                    help="--solver hscg: classic.py semantics (true residual every iteration) "
+                         "or production CG (one SpMV per iteration)")
     ap.add_argument("--check-launch", action="store_true",
                     help="print this rank's (rank, world) and exit (launcher test)")
     args = ap.parse_args()
@@ -824,6 +902,8 @@ def main():
         return
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.solver == "hscg" and (world > 1 or args.partitioned):
+        run_hscg_partitioned(args, rank, world)
     elif args.solver != "adaptive":
         run_solver_compare(args)
     elif world > 1 or args.partitioned:

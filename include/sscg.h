@@ -228,8 +228,8 @@ int sscg_get_small_phases(const sscg_plan* plan, int64_t* cycles8);
  * q, out[5+2q] tile lag D of pass q.  out: 4+2*SSCG_MAX_SIGMA int32. */
 int sscg_plan_mpk_schedule(sscg_plan* plan, int32_t sigma, int32_t* out);
 
-/* What one outer loop of the plan's captured CUDA graph contains (available
- * after a solve built it, else -1): out[0] ncclAllReduce calls captured into
+/* What one outer loop of the plan's captured CUDA graph contains (the graph
+ * the last solve built: an s-step outer loop, or one HSCG iteration; -1 before): out[0] ncclAllReduce calls captured into
  * it, out[1] grouped NCCL halo exchanges, out[2] NCCL kernel nodes (by device
  * function name), out[3] kernel nodes, out[4] graph nodes.  A row-partitioned
  * plan must show exactly one allreduce: the algorithm's one synchronisation
@@ -252,13 +252,31 @@ int sscg_group_solve(sscg_plan* const* plans, int32_t nplans, const sscg_config*
                      sscg_logs* const* logs);
 
 /* Hestenes-Stiefel CG on the plan's operator (classic.py:33-104 hscg_solve;
- * single-GPU plans).  Every iteration recomputes the true residual b - A x
+ * = sscg_hscg_ex with SSCG_HSCG_REFERENCE).  Every iteration recomputes the true residual b - A x
  * like the reference; logs->iters rows carry alpha, beta, the Ritz values,
  * xi, psi and the true / updated residuals and gap (SSCG_IT_*), at most
  * logs->cap_iters of them; status CONVERGED / STAGNATED / DIVERGED, or
  * EXHAUSTED when max_iters ran out.  max_iters < 0: 100 n. */
 int sscg_hscg(sscg_plan* plan, const double* b, const double* x0, double eps_star,
               int64_t max_iters, double* x_out, sscg_logs* logs);
+/* HSCG with a choice of semantics, on single-GPU plans and on row-partitioned
+ * (NCCL) plans alike -- per iteration one halo exchange of p (and x) and two
+ * allreduces (p.Ap with the residual norms; r.r), classic CG's two
+ * synchronisations per iteration:
+ *   SSCG_HSCG_REFERENCE   classic.py:33-104 (the true residual b - A x every
+ *                         iteration drives the verdicts: two SpMVs);
+ *   SSCG_HSCG_PRODUCTION  one SpMV per iteration; convergence on the updated
+ *                         residual, the true residual formed once at the end
+ *                         (the last trace row). */
+#define SSCG_HSCG_REFERENCE 0
+#define SSCG_HSCG_PRODUCTION 1
+int sscg_hscg_ex(sscg_plan* plan, const double* b, const double* x0, double eps_star,
+                 int64_t max_iters, int32_t mode, double* x_out, sscg_logs* logs);
+/* HSCG over the members of a single-process virtual group (sscg_vgroup_run's
+ * plans): lock step, halo by device copies, reductions in fixed order. */
+int sscg_vgroup_hscg(sscg_plan* const* plans, int32_t nplans, const double* const* b,
+                     const double* const* x0, double eps_star, int64_t max_iters, int32_t mode,
+                     sscg_logs* logs0);
 
 /* ---- problem setup (matio.py:104-275) ------------------------------------ */
 /* Matrix Market coordinate text -> full symmetric CSR (read_matrix_market,

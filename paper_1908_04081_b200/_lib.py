@@ -43,8 +43,10 @@ EXPORTS = (
     "sscg_gram", "sscg_recover", "sscg_nested_conds", "sscg_select_s_tilde",
     "sscg_leja_points", "sscg_params_for", "sscg_ritz_sequence", "sscg_sym_eig",
     "sscg_nccl_unique_id", "sscg_plan_create_part", "sscg_vgroup_run",
-    "sscg_plan_collectives", "sscg_group_create", "sscg_group_solve",
+    "sscg_plan_collectives", "sscg_group_create", "sscg_group_solve", "sscg_hscg_ex",
+    "sscg_vgroup_hscg",
 )
+HSCG_MODES = {"reference": 0, "production": 1}
 
 
 class SscgConfig(C.Structure):
@@ -138,6 +140,9 @@ def _declare(lib):
         "sscg_vgroup_run": (C.c_int, [C.POINTER(vp), i32, C.POINTER(SscgConfig),
                                       C.POINTER(_DP), C.POINTER(_DP), C.POINTER(SscgLogs)]),
         "sscg_plan_collectives": (C.c_int, [vp, _IP]),
+        "sscg_hscg_ex": (C.c_int, [vp, _DP, _DP, dbl, i64, i32, _DP, C.POINTER(SscgLogs)]),
+        "sscg_vgroup_hscg": (C.c_int, [C.POINTER(vp), i32, C.POINTER(_DP), C.POINTER(_DP), dbl,
+                                       i64, i32, C.POINTER(SscgLogs)]),
         "sscg_group_create": (C.c_int, [C.POINTER(vp), i32, _IP, C.POINTER(SscgPart)]),
         "sscg_group_solve": (C.c_int, [C.POINTER(vp), i32, C.POINTER(SscgConfig), C.POINTER(_DP),
                                        C.POINTER(_DP), C.POINTER(_DP),

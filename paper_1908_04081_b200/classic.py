@@ -36,27 +36,22 @@ def assemble_tridiag(coeffs, i):
     return np.diag(diag) + np.diag(off, 1) + np.diag(off, -1)
 
 
-def hscg_solve(problem, eps_star, max_iters=None, *, device=0, info=None):
-    """Classic CG on the GPU (classic.py:33-104).  Returns (x, SolveTrace,
-    CgCoefficients); one trace record and one outer mark per iteration."""
-    a = problem.a
-    if max_iters is None:
-        max_iters = 100 * a.n
-    b, x0 = L.f64(problem.b), L.f64(problem.x0)
-    if b.shape != (a.n,) or x0.shape != (a.n,):
-        raise ValueError("b / x0 do not match the matrix dimension")
-    plan = _plan(a, device)
+def hscg_logs(max_iters):
+    """Host log buffers of an HSCG run (one row per iteration)."""
     cap = int(min(max(int(max_iters), 0), 1 << 20)) + 2
     iters = np.full((cap, L.IT_N), np.nan)
     logs = L.SscgLogs()
     logs.cap_iters, logs.cap_outer = cap, 0
     logs.iters = L.dptr(iters)
-    x = np.empty(a.n)
-    L.check(L.load().sscg_hscg(plan.handle, L.dptr(b), L.dptr(x0), float(eps_star),
-                               int(max_iters), L.dptr(x), logs))
+    return iters, logs
+
+
+def hscg_trace(iters, logs):
+    """SolveTrace / CgCoefficients of an HSCG run: one record and one outer
+    mark per iteration (classic.py:93-103)."""
     tr = SolveTrace(trace_level="full")
     co = CgCoefficients()
-    n = min(int(logs.total_iters), cap)
+    n = min(int(logs.total_iters), len(iters))
     for row in iters[:n]:
         co.append(float(row[L.IT_ALPHA]), float(row[L.IT_BETA]))
         tr.mark_outer(1)
@@ -65,6 +60,32 @@ def hscg_solve(problem, eps_star, max_iters=None, *, device=0, info=None):
     tr.converged = logs.status == L.CONVERGED
     tr.stagnated = logs.status == L.STAGNATED
     tr.diverged = logs.status == L.DIVERGED
+    return tr, co
+
+
+def hscg_solve(problem, eps_star, max_iters=None, *, device=0, mode="reference", info=None):
+    """Classic CG on the GPU (classic.py:33-104).  Returns (x, SolveTrace,
+    CgCoefficients); one trace record and one outer mark per iteration.
+
+    mode="reference" keeps classic.py's semantics (the true residual every
+    iteration drives the verdicts); mode="production" is the CG a user would
+    run at scale -- one SpMV per iteration, convergence on the updated residual,
+    the true residual formed once for the last trace row (the other rows' true
+    residual is NaN)."""
+    a = problem.a
+    if mode not in L.HSCG_MODES:
+        raise ValueError(f"unknown HSCG mode {mode!r}")
+    if max_iters is None:
+        max_iters = 100 * a.n
+    b, x0 = L.f64(problem.b), L.f64(problem.x0)
+    if b.shape != (a.n,) or x0.shape != (a.n,):
+        raise ValueError("b / x0 do not match the matrix dimension")
+    plan = _plan(a, device)
+    iters, logs = hscg_logs(max_iters)
+    x = np.empty(a.n)
+    L.check(L.load().sscg_hscg_ex(plan.handle, L.dptr(b), L.dptr(x0), float(eps_star),
+                                  int(max_iters), L.HSCG_MODES[mode], L.dptr(x), logs))
+    tr, co = hscg_trace(iters, logs)
     if isinstance(info, dict):
         info.update(device_ms=logs.device_ms, status=int(logs.status))
     return x, tr, co

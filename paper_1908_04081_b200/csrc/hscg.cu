@@ -23,6 +23,10 @@
 namespace {
 
 constexpr int HS_T = ROWS_PER_CTA;  // 256
+// red_buf slots (the buffer allreduced on a partitioned plan)
+constexpr int HS_RED_BB = 0, HS_RED_RR = 1;                  // start: ||b||^2, r.r
+constexpr int HS_RED_PAP = 0, HS_RED_TT = 1, HS_RED_GG = 2;  // after k_hs_ap (3 doubles)
+constexpr int HS_RED_RRN = 3;                                // after k_hs_xr (1 double)
 
 // row sums: 0 = CSR (unstaged), 1 = pattern ids uint8, 2 = pattern ids uint16,
 // 3 = superset-mask rows with uint8 ids (the union of offsets unrolled: about
@@ -76,29 +80,29 @@ __device__ __forceinline__ double* hs_log(const Ctx& c, int64_t it) {
   return it < c.cfg->cap_iters ? c.it_log + it * SSCG_IT_N : nullptr;
 }
 
-// loop top of classic.py:58-72 for iteration i (thread 0 of the last CTA)
-__device__ void hs_classify(SolverState* st, const DevConfig& cf, double true_rel, double r_norm) {
+// loop top of classic.py:58-72 for iteration i: the verdict, a pure function
+// of the state and the loop-top residuals (every CTA of k_hs_xr evaluates it
+// and takes the same branch; only the last CTA writes best / status).
+// Production mode (PROD) steers by the updated residual: convergence when
+// ||r|| / ||b|| <= eps*, no stagnation test (the true residual is not formed).
+__device__ int hs_verdict(const SolverState* st, const DevConfig& cf, double true_rel,
+                          double r_norm, bool prod, bool* new_best) {
   const int i = st->total_iters;
-  int out = SSCG_RUNNING;
-  if ((int64_t)i >= cf.max_iters) {
-    out = SSCG_EXHAUSTED;  // `while i < max_iters` exits before any verdict
-  } else if (true_rel <= cf.eps_star) {
-    out = SSCG_CONVERGED;
-  } else if (!isfinite(true_rel) || true_rel > 1e5) {
-    out = SSCG_DIVERGED;
-  } else if (true_rel < st->best) {
-    st->best = true_rel;
-    st->best_iter = i;
-  } else if (i - st->best_iter >= 200 && r_norm <= 0.01 * true_rel * st->nb) {
-    out = SSCG_STAGNATED;
+  *new_best = false;
+  if ((int64_t)i >= cf.max_iters) return SSCG_EXHAUSTED;  // `while i < max_iters` exits first
+  if (true_rel <= cf.eps_star) return SSCG_CONVERGED;
+  if (!isfinite(true_rel) || true_rel > 1e5) return SSCG_DIVERGED;
+  if (true_rel < st->best) {
+    *new_best = true;
+    return SSCG_RUNNING;
   }
-  if (out != SSCG_RUNNING) {
-    st->status = out;
-    st->done = 1;
-  }
+  if (!prod && i - st->best_iter >= 200 && r_norm <= 0.01 * true_rel * st->nb)
+    return SSCG_STAGNATED;
+  return SSCG_RUNNING;
 }
 
-// x = x0, r = b - A x0, p = r; ||b||, r.r; the first loop-top verdict
+// x = x0, r = b - A x0, p = r over the owned rows (ghost rows: x from x0; p and
+// r arrive with the first halo exchange); partials of ||b||^2 and r.r -> red
 template <int MODE>
 __global__ void __launch_bounds__(HS_T) k_hs_init(Ctx c, double* P, double* R, const double* x0) {
   __shared__ double sm[HS_T / 32];
@@ -107,10 +111,11 @@ __global__ void __launch_bounds__(HS_T) k_hs_init(Ctx c, double* P, double* R, c
   SolverState* st = c.st;
   double bb = 0.0, rr = 0.0;
   const int64_t stride = (int64_t)gridDim.x * HS_T;
-  for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.n; i += stride) {
+  for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.lvl_rows[SMAX]; i += stride) {
+    c.x[i] = x0[i];
+    if (i >= c.n_own) continue;
     const double bi = c.b[i];
     const double r = __dsub_rn(bi, A.dot(c, i, x0));
-    c.x[i] = x0[i];
     R[i] = r;
     P[i] = r;
     bb = fma(bi, bi, bb);
@@ -126,66 +131,101 @@ __global__ void __launch_bounds__(HS_T) k_hs_init(Ctx c, double* P, double* R, c
   bb = sum_parts(c.part_t, gridDim.x, sm);
   rr = sum_parts(c.part_r, gridDim.x, sm);
   if (threadIdx.x == 0) {
-    const DevConfig cf = *c.cfg;
     st->gram_count = 0;
-    st->k = 0;
-    st->done = 0;
-    st->status = SSCG_RUNNING;
-    st->total_iters = 0;
-    st->total_outer = 0;
-    st->n_records = 0;
-    st->best = INFINITY;
-    st->best_iter = 0;
-    st->nb = sqrt(bb);
-    st->hs_rr = rr;
-    ritz_init(st->rz, cf.c0);
-    // the reference's true_vec = b - A x0 is the same computation as r
-    hs_classify(st, cf, sqrt(rr) / st->nb, sqrt(rr));
+    c.red_buf[HS_RED_BB] = bb;
+    c.red_buf[HS_RED_RR] = rr;
   }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(HS_T) k_hs_ap(Ctx c, const double* P, double* AP) {
+// the reduced ||b||^2 and r.r: the solver state (one thread)
+__global__ void k_hs_start(Ctx c) {
+  SolverState* st = c.st;
+  const DevConfig cf = *c.cfg;
+  st->k = 0;
+  st->done = 0;
+  st->status = SSCG_RUNNING;
+  st->total_iters = 0;
+  st->total_outer = 0;
+  st->n_records = 0;
+  st->best = INFINITY;
+  st->best_iter = 0;
+  st->nb = sqrt(c.red_buf[HS_RED_BB]);
+  st->hs_rr = c.red_buf[HS_RED_RR];
+  ritz_init(st->rz, cf.c0);
+}
+
+// ap = A p over the owned rows and p.ap; TV (reference semantics): also the
+// true residual of the current x, tv = b - A x, with ||tv||^2 and ||tv - r||^2
+// -- classic.py forms it after each update and classifies with it at the next
+// loop top; here both happen one kernel later, on the same x
+template <int MODE, bool TV>
+__global__ void __launch_bounds__(HS_T) k_hs_ap(Ctx c, const double* P, double* AP, const double* R) {
   __shared__ double sm[HS_T / 32];
   SolverState* st = c.st;
   if (st->done) return;
   RowSum<MODE> A;
   A.init(c);
-  double pap = 0.0;
+  double pap = 0.0, tt = 0.0, gg = 0.0;
   const int64_t stride = (int64_t)gridDim.x * HS_T;
-  for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.n; i += stride) {
+  for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.n_own; i += stride) {
     const double ap = A.dot(c, i, P);
     AP[i] = ap;
     pap = fma(P[i], ap, pap);
+    if (TV) {
+      const double tv = __dsub_rn(c.b[i], A.dot(c, i, c.x));
+      const double gv = __dsub_rn(tv, R[i]);
+      tt = fma(tv, tv, tt);
+      gg = fma(gv, gv, gg);
+    }
   }
   pap = block_sum<HS_T>(pap, sm);
-  if (threadIdx.x == 0) c.part_t[blockIdx.x] = pap;
+  if (TV) {
+    tt = block_sum<HS_T>(tt, sm);
+    gg = block_sum<HS_T>(gg, sm);
+  }
+  if (threadIdx.x == 0) {
+    c.part_t[blockIdx.x] = pap;
+    c.part_r[blockIdx.x] = tt;
+    c.part_d[blockIdx.x] = gg;
+  }
   if (!last_cta(&st->gram_count)) return;
   pap = sum_parts(c.part_t, gridDim.x, sm);
+  tt = TV ? sum_parts(c.part_r, gridDim.x, sm) : 0.0;
+  gg = TV ? sum_parts(c.part_d, gridDim.x, sm) : 0.0;
   if (threadIdx.x == 0) {
     st->gram_count = 0;
-    if (pap <= 0.0 || !isfinite(pap)) {  // classic.py:77-79
-      st->status = SSCG_DIVERGED;
-      st->done = 1;
-    } else {
-      st->hs_alpha = st->hs_rr / pap;
-    }
+    c.red_buf[HS_RED_PAP] = pap;
+    c.red_buf[HS_RED_TT] = tt;
+    c.red_buf[HS_RED_GG] = gg;
   }
 }
 
+// loop top (the previous iteration's trace row, the verdict), then alpha =
+// rr / p.ap (breakdown check, classic.py:77-79), x += alpha p, r -= alpha ap
+// and the new r.r partial -> red
 __global__ void __launch_bounds__(HS_T) k_hs_xr(Ctx c, const double* P, const double* AP,
-                                                double* R) {
+                                                double* R, int prod) {
   __shared__ double sm[HS_T / 32];
   SolverState* st = c.st;
   if (st->done) return;
-  const double alpha = st->hs_alpha;
+  const DevConfig cf = *c.cfg;
+  const double nb = st->nb;
+  const double r_norm = sqrt(st->hs_rr);
+  const double true_rel = prod ? r_norm / nb : sqrt(c.red_buf[HS_RED_TT]) / nb;
+  bool new_best;
+  int out = hs_verdict(st, cf, true_rel, r_norm, prod != 0, &new_best);
+  const double pap = c.red_buf[HS_RED_PAP];
+  if (out == SSCG_RUNNING && (pap <= 0.0 || !isfinite(pap))) out = SSCG_DIVERGED;
   double rr = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * HS_T;
-  for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.n; i += stride) {
-    c.x[i] = __dadd_rn(c.x[i], __dmul_rn(alpha, P[i]));  // q = alpha*p; x = x + q
-    const double r = __dsub_rn(R[i], __dmul_rn(alpha, AP[i]));
-    R[i] = r;
-    rr = fma(r, r, rr);
+  if (out == SSCG_RUNNING) {
+    const double alpha = st->hs_rr / pap;
+    const int64_t stride = (int64_t)gridDim.x * HS_T;
+    for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.n_own; i += stride) {
+      c.x[i] = __dadd_rn(c.x[i], __dmul_rn(alpha, P[i]));  // q = alpha*p; x = x + q
+      const double r = __dsub_rn(R[i], __dmul_rn(alpha, AP[i]));
+      R[i] = r;
+      rr = fma(r, r, rr);
+    }
   }
   rr = block_sum<HS_T>(rr, sm);
   if (threadIdx.x == 0) c.part_r[blockIdx.x] = rr;
@@ -193,13 +233,54 @@ __global__ void __launch_bounds__(HS_T) k_hs_xr(Ctx c, const double* P, const do
   rr = sum_parts(c.part_r, gridDim.x, sm);
   if (threadIdx.x == 0) {
     st->gram_count = 0;
-    const double beta = rr / st->hs_rr;
     const int it = st->total_iters;
-    if (double* row = hs_log(c, it)) {
+    if (it > 0 && !prod) {  // the previous iteration's row: the true residual of this x
+      if (double* row = hs_log(c, it - 1)) {
+        row[SSCG_IT_TRUE] = true_rel;
+        row[SSCG_IT_GAP] = sqrt(c.red_buf[HS_RED_GG]);
+      }
+    }
+    if (new_best) {
+      st->best = true_rel;
+      st->best_iter = it;
+    }
+    if (out != SSCG_RUNNING) {
+      st->status = out;
+      st->done = 1;
+    } else {
+      st->hs_alpha = st->hs_rr / pap;
+      c.red_buf[HS_RED_RRN] = rr;
+    }
+  }
+}
+
+// beta = rr_new / rr, Ritz absorb, the iteration's log row; p = r + beta p
+__global__ void __launch_bounds__(HS_T) k_hs_p(Ctx c, double* P, const double* R) {
+  __shared__ double sm[HS_T / 32];
+  SolverState* st = c.st;
+  if (st->done) return;
+  const double rr = c.red_buf[HS_RED_RRN];
+  const double beta = rr / st->hs_rr;
+  const int64_t stride = (int64_t)gridDim.x * HS_T;
+  for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.n_own; i += stride)
+    P[i] = __dadd_rn(R[i], __dmul_rn(beta, P[i]));
+  if (!last_cta(&st->gram_count)) return;
+  if (threadIdx.x == 0) {
+    st->gram_count = 0;
+    const double alpha = st->hs_alpha;
+    const int it = st->total_iters;
+    ritz_absorb(st->rz, alpha, beta);  // BreakdownSignal -> state untouched
+    if (double* row = hs_log(c, it)) {  // trace.record_iteration (true / gap: next loop top)
+      const double nb = st->nb;
       row[SSCG_IT_ALPHA] = alpha;
       row[SSCG_IT_BETA] = beta;
+      row[SSCG_IT_UPD] = sqrt(rr) / nb;
+      row[SSCG_IT_EST] = sqrt(rr) / nb;
+      row[SSCG_IT_XI] = ritz_xi(st->rz);
+      row[SSCG_IT_LMIN] = ritz_lmin(st->rz);
+      row[SSCG_IT_LMAX] = ritz_lmax(st->rz);
+      row[SSCG_IT_PSI] = st->rz.psi;
     }
-    ritz_absorb(st->rz, alpha, beta);  // BreakdownSignal -> state untouched
     st->hs_beta = beta;
     st->hs_rr = rr;
     st->total_iters = it + 1;
@@ -207,50 +288,46 @@ __global__ void __launch_bounds__(HS_T) k_hs_xr(Ctx c, const double* P, const do
   }
 }
 
+// production mode, after the loop: the true residual of the final x for the
+// last trace row (one more A x pass; ghost x arrive with the halo before it)
 template <int MODE>
-__global__ void __launch_bounds__(HS_T) k_hs_pt(Ctx c, double* P, const double* R) {
+__global__ void __launch_bounds__(HS_T) k_hs_final(Ctx c, const double* R) {
   __shared__ double sm[HS_T / 32];
   SolverState* st = c.st;
-  if (st->done) return;
   RowSum<MODE> A;
   A.init(c);
-  const double beta = st->hs_beta;
   double tt = 0.0, gg = 0.0;
   const int64_t stride = (int64_t)gridDim.x * HS_T;
-  for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.n; i += stride) {
-    const double r = R[i];
-    P[i] = __dadd_rn(r, __dmul_rn(beta, P[i]));
+  for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.n_own; i += stride) {
     const double tv = __dsub_rn(c.b[i], A.dot(c, i, c.x));
-    const double gv = __dsub_rn(tv, r);
+    const double gv = __dsub_rn(tv, R[i]);
     tt = fma(tv, tv, tt);
     gg = fma(gv, gv, gg);
   }
   tt = block_sum<HS_T>(tt, sm);
   gg = block_sum<HS_T>(gg, sm);
   if (threadIdx.x == 0) {
-    c.part_t[blockIdx.x] = tt;
+    c.part_r[blockIdx.x] = tt;
     c.part_d[blockIdx.x] = gg;
   }
   if (!last_cta(&st->gram_count)) return;
-  tt = sum_parts(c.part_t, gridDim.x, sm);
+  tt = sum_parts(c.part_r, gridDim.x, sm);
   gg = sum_parts(c.part_d, gridDim.x, sm);
   if (threadIdx.x == 0) {
     st->gram_count = 0;
-    const DevConfig cf = *c.cfg;
-    const double nb = st->nb;
-    const double true_rel = sqrt(tt) / nb;
-    const double r_norm = sqrt(st->hs_rr);
-    if (double* row = hs_log(c, st->total_iters - 1)) {  // trace.record_iteration
-      row[SSCG_IT_TRUE] = true_rel;
-      row[SSCG_IT_UPD] = r_norm / nb;
-      row[SSCG_IT_GAP] = sqrt(gg);
-      row[SSCG_IT_XI] = ritz_xi(st->rz);
-      row[SSCG_IT_LMIN] = ritz_lmin(st->rz);
-      row[SSCG_IT_LMAX] = ritz_lmax(st->rz);
-      row[SSCG_IT_PSI] = st->rz.psi;
-      row[SSCG_IT_EST] = r_norm / nb;
-    }
-    hs_classify(st, cf, true_rel, r_norm);
+    c.red_buf[HS_RED_TT] = tt;
+    c.red_buf[HS_RED_GG] = gg;
+  }
+}
+
+// the final row's true residual (after k_hs_final and its allreduce)
+__global__ void k_hs_final_row(Ctx c) {
+  SolverState* st = c.st;
+  const int it = st->total_iters;
+  if (it < 1) return;
+  if (double* row = hs_log(c, it - 1)) {
+    row[SSCG_IT_TRUE] = sqrt(c.red_buf[HS_RED_TT]) / st->nb;
+    row[SSCG_IT_GAP] = sqrt(c.red_buf[HS_RED_GG]);
   }
 }
 
@@ -260,20 +337,27 @@ void hs_launch_init(const Ctx& c, double* P, double* R, const double* x0, size_t
   k_hs_init<MODE><<<c.red_n, HS_T, smem, s>>>(c, P, R, x0);
 }
 template <int MODE>
-void hs_launch_iter(const Ctx& c, double* P, double* AP, double* R, size_t smem,
-                    cudaStream_t s) {
-  k_hs_ap<MODE><<<c.red_n, HS_T, smem, s>>>(c, P, AP);
-  k_hs_xr<<<c.red_n, HS_T, 0, s>>>(c, P, AP, R);
-  k_hs_pt<MODE><<<c.red_n, HS_T, smem, s>>>(c, P, R);
+void hs_launch_ap(const Ctx& c, const double* P, double* AP, const double* R, bool tv, size_t smem,
+                  cudaStream_t s) {
+  if (tv)
+    k_hs_ap<MODE, true><<<c.red_n, HS_T, smem, s>>>(c, P, AP, R);
+  else
+    k_hs_ap<MODE, false><<<c.red_n, HS_T, smem, s>>>(c, P, AP, R);
+}
+template <int MODE>
+void hs_launch_final(const Ctx& c, const double* R, size_t smem, cudaStream_t s) {
+  k_hs_final<MODE><<<c.red_n, HS_T, smem, s>>>(c, R);
 }
 
 int hs_mode(const Ctx& c) {
-  if (!c.pid) return 0;
+  // a partitioned plan's pattern table is in global offsets (the march's):
+  // its HSCG row sums use the local CSR
+  if (!c.pid || c.zm_base) return 0;
   if (c.pid_bytes == 1 && c.ss_ne > 0 && c.hs_ss) return 3;
   return c.pid_bytes == 1 ? 1 : 2;
 }
 size_t hs_smem(const Ctx& c) {
-  if (!c.pid) return 0;
+  if (!c.pid || c.zm_base) return 0;
   return hs_mode(c) == 3 ? ss_smem_bytes(c.pat_np) : pattern_smem_bytes(c.pat_np, c.pat_ne);
 }
 
@@ -281,15 +365,12 @@ size_t hs_smem(const Ctx& c) {
 
 void hscg_prepare() {
   const int bytes = 48 * 1024;
-  cudaFuncSetAttribute(k_hs_init<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_hs_init<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_hs_ap<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_hs_ap<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_hs_pt<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_hs_pt<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_hs_init<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_hs_ap<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_hs_pt<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+#define HS_ATTR(K) cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  HS_ATTR(k_hs_init<1>) HS_ATTR(k_hs_init<2>) HS_ATTR(k_hs_init<3>)
+  HS_ATTR((k_hs_ap<1, true>)) HS_ATTR((k_hs_ap<2, true>)) HS_ATTR((k_hs_ap<3, true>))
+  HS_ATTR((k_hs_ap<1, false>)) HS_ATTR((k_hs_ap<2, false>)) HS_ATTR((k_hs_ap<3, false>))
+  HS_ATTR(k_hs_final<1>) HS_ATTR(k_hs_final<2>) HS_ATTR(k_hs_final<3>)
+#undef HS_ATTR
 }
 
 void launch_hscg_init(const Ctx& c, double* P, double* R, const double* x0, cudaStream_t s) {
@@ -301,13 +382,32 @@ void launch_hscg_init(const Ctx& c, double* P, double* R, const double* x0, cuda
     default: hs_launch_init<0>(c, P, R, x0, 0, s); break;
   }
 }
+void launch_hscg_start(const Ctx& c, cudaStream_t s) { k_hs_start<<<1, 1, 0, s>>>(c); }
 
-void launch_hscg_iter(const Ctx& c, double* P, double* AP, double* R, cudaStream_t s) {
+// the three kernels of one iteration; the host puts the halo exchange before
+// launch_hscg_ap and an allreduce after it and after launch_hscg_xr
+void launch_hscg_ap(const Ctx& c, double* P, double* AP, const double* R, bool tv, cudaStream_t s) {
   const size_t smem = hs_smem(c);
   switch (hs_mode(c)) {
-    case 3: hs_launch_iter<3>(c, P, AP, R, smem, s); break;
-    case 1: hs_launch_iter<1>(c, P, AP, R, smem, s); break;
-    case 2: hs_launch_iter<2>(c, P, AP, R, smem, s); break;
-    default: hs_launch_iter<0>(c, P, AP, R, 0, s); break;
+    case 3: hs_launch_ap<3>(c, P, AP, R, tv, smem, s); break;
+    case 1: hs_launch_ap<1>(c, P, AP, R, tv, smem, s); break;
+    case 2: hs_launch_ap<2>(c, P, AP, R, tv, smem, s); break;
+    default: hs_launch_ap<0>(c, P, AP, R, tv, 0, s); break;
   }
 }
+void launch_hscg_xr(const Ctx& c, double* P, double* AP, double* R, bool prod, cudaStream_t s) {
+  k_hs_xr<<<c.red_n, HS_T, 0, s>>>(c, P, AP, R, prod ? 1 : 0);
+}
+void launch_hscg_p(const Ctx& c, double* P, double* R, cudaStream_t s) {
+  k_hs_p<<<c.red_n, HS_T, 0, s>>>(c, P, R);
+}
+void launch_hscg_final(const Ctx& c, const double* R, cudaStream_t s) {
+  const size_t smem = hs_smem(c);
+  switch (hs_mode(c)) {
+    case 3: hs_launch_final<3>(c, R, smem, s); break;
+    case 1: hs_launch_final<1>(c, R, smem, s); break;
+    case 2: hs_launch_final<2>(c, R, smem, s); break;
+    default: hs_launch_final<0>(c, R, 0, s); break;
+  }
+}
+void launch_hscg_final_row(const Ctx& c, cudaStream_t s) { k_hs_final_row<<<1, 1, 0, s>>>(c); }

@@ -336,7 +336,12 @@ void launch_pw_scale(int64_t n, const double* w, double nw, double* v, cudaStrea
 // hscg.cu
 void hscg_prepare();
 void launch_hscg_init(const Ctx& c, double* P, double* R, const double* x0, cudaStream_t s);
-void launch_hscg_iter(const Ctx& c, double* P, double* AP, double* R, cudaStream_t s);
+void launch_hscg_start(const Ctx& c, cudaStream_t s);
+void launch_hscg_ap(const Ctx& c, double* P, double* AP, const double* R, bool tv, cudaStream_t s);
+void launch_hscg_xr(const Ctx& c, double* P, double* AP, double* R, bool prod, cudaStream_t s);
+void launch_hscg_p(const Ctx& c, double* P, double* R, cudaStream_t s);
+void launch_hscg_final(const Ctx& c, const double* R, cudaStream_t s);
+void launch_hscg_final_row(const Ctx& c, cudaStream_t s);
 void launch_leja_point(const Ctx& c, int n, cudaStream_t s);
 size_t small_smem_bytes();
 // dist.cu

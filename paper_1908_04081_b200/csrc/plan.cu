@@ -117,6 +117,7 @@ struct sscg_plan {
   int partitioned = 0;
   // HSCG (sscg_hscg): graph of HS_CHUNK iterations, captured for this Y
   cudaGraphExec_t hs_gexec = nullptr;
+  int hs_mode = -1;         // SSCG_HSCG_* the graph was captured for
   double* hs_y = nullptr;   // buffers the captured graph points at
   double* hs_it = nullptr;
   int leja_head = 0;  // Leja chain at the start of the outer loop (small operators)
@@ -1583,12 +1584,35 @@ constexpr int HS_CHUNK = 16;          // iterations per graph replay
 constexpr int64_t HS_LOG_CAP = 1 << 20;  // device log rows (iterations past it are not logged)
 }  // namespace
 
-int sscg_hscg(sscg_plan* p, const double* b, const double* x0, double eps_star, int64_t max_iters,
-              double* x_out, sscg_logs* logs) {
+namespace {
+// one HSCG iteration on the plan's stream: [halo of p and x] -> ap (+ the true
+// residual) -> [allreduce p.ap, ||b-Ax||^2, ||b-Ax-r||^2] -> loop top, x, r ->
+// [allreduce r.r] -> beta, p.  Two allreduces and one halo per iteration, the
+// distributed classic CG of classic.py:33-104.
+int hscg_capture_iter(sscg_plan* p, const Ctx& c, double* P, double* AP, double* R, bool prod) {
+  if (p->partitioned && p->comm) {
+    TRY(halo_exchange(p->halo, c, p->comm, p->stream));
+    halo_unpack(p->halo, c, p->stream);
+  }
+  launch_hscg_ap(c, P, AP, R, !prod, p->stream);
+  TRY(nccl_allreduce(p->comm, c.red_buf, 3, p->stream));
+  launch_hscg_xr(c, P, AP, R, prod, p->stream);
+  TRY(nccl_allreduce(p->comm, c.red_buf + 3, 1, p->stream));
+  launch_hscg_p(c, P, R, p->stream);
+  return SSCG_OK;
+}
+}  // namespace
+
+int sscg_hscg_ex(sscg_plan* p, const double* b, const double* x0, double eps_star,
+                 int64_t max_iters, int32_t mode, double* x_out, sscg_logs* logs) {
   if (!p || !b) return sscg_fail(SSCG_EINVAL, "NULL argument");
-  if (p->partitioned) return sscg_fail(SSCG_EINVAL, "sscg_hscg runs on single-GPU plans");
   if (!(eps_star >= 0.0)) return sscg_fail(SSCG_EINVAL, "eps_star must be >= 0");
-  if (max_iters < 0) max_iters = 100 * p->n;  // classic.py:46-47
+  if (mode != SSCG_HSCG_REFERENCE && mode != SSCG_HSCG_PRODUCTION)
+    return sscg_fail(SSCG_EINVAL, "unknown HSCG mode %d", mode);
+  if (p->partitioned && !p->comm)
+    return sscg_fail(SSCG_EINVAL, "a virtual-group member runs HSCG through sscg_vgroup_hscg");
+  const bool prod = mode == SSCG_HSCG_PRODUCTION;
+  if (max_iters < 0) max_iters = 100 * p->n;  // classic.py:46-47 (partitioned: owned rows' share)
   CUDA_OK(cudaSetDevice(p->device));
   TRY(sscg_load(p, b, x0));
   TRY(ensure_work(p, 1, std::min<int64_t>(max_iters, HS_LOG_CAP), 2));  // Y: p, ap, r
@@ -1603,28 +1627,47 @@ int sscg_hscg(sscg_plan* p, const double* b, const double* x0, double eps_star, 
   dc.max_iters = max_iters;
   CUDA_OK(cudaMemcpyAsync(p->d_cfg, &dc, sizeof(dc), cudaMemcpyHostToDevice, p->stream));
   CUDA_OK(cudaMemsetAsync(p->d_it, 0xff, sizeof(double) * p->cap_iters * SSCG_IT_N, p->stream));
+  p->halo.r_col = 2;  // the halo carries p (Y column 0), r (column 2) and x
   const Ctx c = make_ctx(p);
   double* P = p->d_Y;
   double* AP = p->d_Y + p->ld;
   double* R = p->d_Y + 2 * p->ld;
-  if (!p->hs_gexec || p->hs_y != p->d_Y || p->hs_it != p->d_it) {
+  if (!p->hs_gexec || p->hs_y != p->d_Y || p->hs_it != p->d_it || p->hs_mode != mode) {
     if (p->hs_gexec) cudaGraphExecDestroy(p->hs_gexec);
     p->hs_gexec = nullptr;
     cudaGraph_t g = nullptr;
+    long long ar0, halo0, ar1, halo1;
+    collective_counts(&ar0, &halo0);
     CUDA_OK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < HS_CHUNK; ++i) launch_hscg_iter(c, P, AP, R, p->stream);
-    CUDA_OK(cudaStreamEndCapture(p->stream, &g));
+    int crc = SSCG_OK;
+    for (int i = 0; i < HS_CHUNK && crc == SSCG_OK; ++i) crc = hscg_capture_iter(p, c, P, AP, R, prod);
+    const cudaError_t ee = cudaStreamEndCapture(p->stream, &g);
+    if (crc != SSCG_OK) {
+      if (g) cudaGraphDestroy(g);
+      return crc;
+    }
+    if (ee != cudaSuccess) return sscg_fail_cuda(ee, "cudaStreamEndCapture (hscg)");
+    // census per iteration of the HS_CHUNK-iteration graph
+    collective_counts(&ar1, &halo1);
+    graph_census(g, p->census);
+    p->census[0] = (int)((ar1 - ar0) / HS_CHUNK);
+    p->census[1] = (int)((halo1 - halo0) / HS_CHUNK);
+    for (int k = 2; k < 5; ++k) p->census[k] /= HS_CHUNK;
     const cudaError_t e = cudaGraphInstantiate(&p->hs_gexec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return sscg_fail_cuda(e, "cudaGraphInstantiate (hscg)");
     p->hs_y = p->d_Y;
     p->hs_it = p->d_it;
+    p->hs_mode = mode;
   }
   CUDA_OK(cudaEventRecord(p->ev_start, p->stream));
   launch_hscg_init(c, P, R, p->d_x0, p->stream);
+  TRY(nccl_allreduce(p->comm, c.red_buf, 2, p->stream));  // ||b||^2, r.r
+  launch_hscg_start(c, p->stream);
   CUDA_OK(cudaGetLastError());
-  // replay chunks, polling `done` one chunk behind (the GPU never waits on the host)
-  const int64_t chunks = (max_iters + HS_CHUNK - 1) / HS_CHUNK;
+  // replay chunks, polling `done` one chunk behind (the GPU never waits on the
+  // host); one more chunk than max_iters / HS_CHUNK for the last loop top
+  const int64_t chunks = max_iters / HS_CHUNK + 1;
   int chunk_id = 0;
   for (int64_t q = 0; q < chunks; ++q) {
     CUDA_OK(cudaGraphLaunch(p->hs_gexec, p->stream));
@@ -1638,13 +1681,22 @@ int sscg_hscg(sscg_plan* p, const double* b, const double* x0, double eps_star, 
     }
     ++chunk_id;
   }
+  if (prod) {  // the final x's true residual for the last trace row
+    if (p->partitioned && p->comm) {
+      TRY(halo_exchange(p->halo, c, p->comm, p->stream));
+      halo_unpack(p->halo, c, p->stream);
+    }
+    launch_hscg_final(c, R, p->stream);
+    TRY(nccl_allreduce(p->comm, c.red_buf + 1, 2, p->stream));
+    launch_hscg_final_row(c, p->stream);
+  }
   CUDA_OK(cudaEventRecord(p->ev_stop, p->stream));
   CUDA_OK(cudaStreamSynchronize(p->stream));
   CUDA_OK(cudaGetLastError());
   float ms = 0.f;
   CUDA_OK(cudaEventElapsedTime(&ms, p->ev_start, p->ev_stop));
   p->last_ms = ms;
-  if (x_out) CUDA_OK(cudaMemcpy(x_out, p->d_x, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
+  if (x_out) TRY(copy_d2h(p, x_out, p->d_x, sizeof(double) * p->n_own));
   if (logs) {
     SolverState st;
     CUDA_OK(cudaMemcpy(&st, p->d_st, sizeof(st), cudaMemcpyDeviceToHost));
@@ -1657,6 +1709,137 @@ int sscg_hscg(sscg_plan* p, const double* b, const double* x0, double eps_star, 
     const int64_t ni = std::min<int64_t>({(int64_t)st.total_iters, logs->cap_iters, p->cap_iters});
     if (logs->iters && ni > 0)
       CUDA_OK(cudaMemcpy(logs->iters, p->d_it, sizeof(double) * ni * SSCG_IT_N, cudaMemcpyDeviceToHost));
+  }
+  return SSCG_OK;
+}
+
+int sscg_hscg(sscg_plan* p, const double* b, const double* x0, double eps_star, int64_t max_iters,
+              double* x_out, sscg_logs* logs) {
+  return sscg_hscg_ex(p, b, x0, eps_star, max_iters, SSCG_HSCG_REFERENCE, x_out, logs);
+}
+
+// ---- virtual-group HSCG (single process, lock step, no NCCL) ------------------
+int sscg_vgroup_hscg(sscg_plan* const* plans, int32_t np, const double* const* b,
+                     const double* const* x0, double eps_star, int64_t max_iters, int32_t mode,
+                     sscg_logs* logs0) {
+  if (!plans || np < 1 || !b) return sscg_fail(SSCG_EINVAL, "bad group arguments");
+  if (mode != SSCG_HSCG_REFERENCE && mode != SSCG_HSCG_PRODUCTION)
+    return sscg_fail(SSCG_EINVAL, "unknown HSCG mode %d", mode);
+  for (int i = 0; i < np; ++i)
+    if (!plans[i] || !plans[i]->partitioned || plans[i]->comm || plans[i]->world != np ||
+        plans[i]->rank != i || plans[i]->device != plans[0]->device)
+      return sscg_fail(SSCG_EINVAL, "plan %d is not member %d of a %d-plan virtual group on one device",
+                       i, i, np);
+  const bool prod = mode == SSCG_HSCG_PRODUCTION;
+  if (!(eps_star >= 0.0)) return sscg_fail(SSCG_EINVAL, "eps_star must be >= 0");
+  if (max_iters < 0) {
+    int64_t n = 0;
+    for (int i = 0; i < np; ++i) n += plans[i]->n_own;
+    max_iters = 100 * n;
+  }
+  CUDA_OK(cudaSetDevice(plans[0]->device));
+  std::vector<Ctx> cs;
+  std::vector<double*> reds;
+  for (int i = 0; i < np; ++i) {
+    sscg_plan* p = plans[i];
+    TRY(sscg_load(p, b[i], x0 ? x0[i] : nullptr));
+    CUDA_OK(cudaStreamSynchronize(p->stream));
+    TRY(ensure_work(p, 1, std::min<int64_t>(max_iters, HS_LOG_CAP), 2));
+    DevConfig dc;
+    memset(&dc, 0, sizeof(dc));
+    dc.sigma = 1;
+    dc.eps_star = eps_star;
+    dc.unit = std::ldexp(1.0, -53);
+    dc.c0 = sscg_host_c0();
+    dc.cap_iters = p->cap_iters;
+    dc.cap_outer = p->cap_outer - 1;
+    dc.max_iters = max_iters;
+    CUDA_OK(cudaMemcpy(p->d_cfg, &dc, sizeof(dc), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemset(p->d_it, 0xff, sizeof(double) * p->cap_iters * SSCG_IT_N));
+    p->halo.r_col = 2;
+    cs.push_back(make_ctx(p));
+    reds.push_back(p->d_red);
+  }
+  cudaStream_t s = plans[0]->stream;
+  double** d_reds = nullptr;
+  CUDA_OK(cudaMalloc(&d_reds, sizeof(double*) * np));
+  CUDA_OK(cudaMemcpy(d_reds, reds.data(), sizeof(double*) * np, cudaMemcpyHostToDevice));
+  auto Y = [&](int i, int col) { return plans[i]->d_Y + (int64_t)col * plans[i]->ld; };
+  auto halo = [&]() -> int {  // pack on every member, device copies peer -> peer, unpack
+    for (int i = 0; i < np; ++i) TRY(halo_exchange(plans[i]->halo, cs[i], nullptr, s));
+    for (int i = 0; i < np; ++i) {
+      const HaloPlan& h = plans[i]->halo;
+      for (int q = 0; q < h.n_peers; ++q) {
+        const int j = h.peer_rank[q];
+        const HaloPlan& hj = plans[j]->halo;
+        int qi = -1;
+        for (int t = 0; t < hj.n_peers; ++t)
+          if (hj.peer_rank[t] == i) qi = t;
+        const int64_t n = h.recv_off[q + 1] - h.recv_off[q];
+        if (qi < 0 || hj.send_off[qi + 1] - hj.send_off[qi] != n)
+          return sscg_fail(SSCG_EINVAL, "halo lists of members %d and %d disagree", i, j);
+        if (n)
+          CUDA_OK(cudaMemcpyAsync(h.d_recvbuf + 3 * h.recv_off[q], hj.d_sendbuf + 3 * hj.send_off[qi],
+                                  sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    for (int i = 0; i < np; ++i) halo_unpack(plans[i]->halo, cs[i], s);
+    return SSCG_OK;
+  };
+  int rc = SSCG_OK;
+  for (int i = 0; i < np; ++i) launch_hscg_init(cs[i], Y(i, 0), Y(i, 2), plans[i]->d_x0, s);
+  launch_vsum(d_reds, np, 2, s);
+  for (int i = 0; i < np; ++i) launch_hscg_start(cs[i], s);
+  int64_t it = 0;
+  for (; it <= max_iters && rc == SSCG_OK; ++it) {
+    rc = halo();
+    if (rc) break;
+    for (int i = 0; i < np; ++i) launch_hscg_ap(cs[i], Y(i, 0), Y(i, 1), Y(i, 2), !prod, s);
+    launch_vsum(d_reds, np, 3, s);
+    for (int i = 0; i < np; ++i) launch_hscg_xr(cs[i], Y(i, 0), Y(i, 1), Y(i, 2), prod, s);
+    // the r.r slot alone (slot 3): sum in place on offset pointers
+    for (int i = 0; i < np; ++i) reds[i] = plans[i]->d_red + 3;
+    CUDA_OK(cudaMemcpyAsync(d_reds, reds.data(), sizeof(double*) * np, cudaMemcpyHostToDevice, s));
+    launch_vsum(d_reds, np, 1, s);
+    for (int i = 0; i < np; ++i) reds[i] = plans[i]->d_red;
+    CUDA_OK(cudaMemcpyAsync(d_reds, reds.data(), sizeof(double*) * np, cudaMemcpyHostToDevice, s));
+    for (int i = 0; i < np; ++i) launch_hscg_p(cs[i], Y(i, 0), Y(i, 2), s);
+    if (it % HS_CHUNK == HS_CHUNK - 1 || it == max_iters) {
+      cudaError_t e = cudaMemcpyAsync(plans[0]->h_done, &plans[0]->d_st->done, sizeof(int),
+                                      cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) {
+        rc = sscg_fail_cuda(e, "virtual group HSCG step");
+        break;
+      }
+      if (plans[0]->h_done[0]) break;
+    }
+  }
+  if (rc == SSCG_OK && prod) {
+    rc = halo();
+    if (rc == SSCG_OK) {
+      for (int i = 0; i < np; ++i) launch_hscg_final(cs[i], Y(i, 2), s);
+      for (int i = 0; i < np; ++i) reds[i] = plans[i]->d_red + 1;
+      cudaMemcpyAsync(d_reds, reds.data(), sizeof(double*) * np, cudaMemcpyHostToDevice, s);
+      launch_vsum(d_reds, np, 2, s);
+      for (int i = 0; i < np; ++i) launch_hscg_final_row(cs[i], s);
+    }
+  }
+  CUDA_OK(cudaStreamSynchronize(s));
+  cudaFree(d_reds);
+  if (rc) return rc;
+  CUDA_OK(cudaGetLastError());
+  if (logs0) {
+    sscg_plan* p = plans[0];
+    SolverState st;
+    CUDA_OK(cudaMemcpy(&st, p->d_st, sizeof(st), cudaMemcpyDeviceToHost));
+    logs0->status = st.done ? st.status : SSCG_EXHAUSTED;
+    logs0->total_iters = st.total_iters;
+    logs0->total_outer = st.total_iters;
+    logs0->n_records = 0;
+    const int64_t ni = std::min<int64_t>({(int64_t)st.total_iters, logs0->cap_iters, p->cap_iters});
+    if (logs0->iters && ni > 0)
+      CUDA_OK(cudaMemcpy(logs0->iters, p->d_it, sizeof(double) * ni * SSCG_IT_N, cudaMemcpyDeviceToHost));
   }
   return SSCG_OK;
 }

@@ -152,6 +152,61 @@ class VirtualGroup:
         tr, co = build_trace(cfg, logs, "fast")
         return x, tr, co, logs
 
+    def hscg(self, problem, eps_star, max_iters=None, mode="reference"):
+        """Distributed HSCG over the group (classic.py:33-104): per iteration
+        one halo exchange of p / x and two reductions (sscg_vgroup_hscg)."""
+        from .classic import hscg_logs, hscg_trace
+        if max_iters is None:
+            max_iters = 100 * problem.a.n
+        bs, xs = zip(*[_local_vectors(p, problem.b, problem.x0) for p in self.parts])
+        vp = C.c_void_p * self.world
+        handles = vp(*[pl.handle.value for pl in self.plans])
+        bp = (L._DP * self.world)(*[L.dptr(v) for v in bs])
+        xp = (L._DP * self.world)(*[L.dptr(v) for v in xs])
+        iters, logs = hscg_logs(max_iters)
+        L.check(L.load().sscg_vgroup_hscg(C.cast(handles, C.POINTER(C.c_void_p)), self.world, bp,
+                                          xp, float(eps_star), int(max_iters),
+                                          L.HSCG_MODES[mode], logs))
+        x = np.empty(problem.a.n)
+        for pl, part in zip(self.plans, self.parts):
+            xo = np.empty(part.n_own)
+            L.check(L.load().sscg_fetch(pl.handle, L.dptr(xo), None))
+            x[part.row_lo:part.row_hi] = xo
+        tr, co = hscg_trace(iters, logs)
+        return x, tr, co
+
+
+def hscg_partitioned(rows, b_global, x0_global, eps_star, rank, world, device, exchange,
+                     broadcast_bytes, max_iters=None, mode="production", nccl_lib=None, info=None):
+    """This rank's share of a multi-process distributed HSCG (torchrun): a
+    depth-1 ghost zone, one NCCL halo exchange and two NCCL allreduces per
+    iteration (sscg_hscg_ex on a partitioned plan).  Returns (x_owned, trace,
+    coeffs, plan)."""
+    from .build import nccl_library
+    from .classic import hscg_logs, hscg_trace
+    part = partition_rank(rows, rank, world, 1, exchange)
+    lib = L.load()
+    nccl_lib = nccl_lib or nccl_library()
+    uid = None
+    if rank == 0:
+        buf = C.create_string_buffer(128)
+        L.check(lib.sscg_nccl_unique_id(nccl_lib.encode(), buf))
+        uid = bytes(buf.raw)
+    uid = broadcast_bytes(uid)
+    plan = PartPlan(part, rank, world, device, nccl_id=uid, nccl_lib=nccl_lib)
+    if max_iters is None:
+        max_iters = 100 * rows.n
+    b, x0 = _local_vectors(part, b_global, x0_global)
+    iters, logs = hscg_logs(max_iters)
+    xo = np.empty(part.n_own)
+    L.check(lib.sscg_hscg_ex(plan.handle, L.dptr(b), L.dptr(x0), float(eps_star), int(max_iters),
+                             L.HSCG_MODES[mode], L.dptr(xo), logs))
+    tr, co = hscg_trace(iters, logs)
+    if isinstance(info, dict):
+        info.update(plan=plan, part=part, logs=logs, iters=iters, b=b, x0=x0,
+                    max_iters=int(max_iters), mode=mode)
+    return xo, tr, co, plan
+
 
 class DeviceGroup:
     """A row-partitioned solve over several GPUs from ONE process (SURVEY.md

@@ -59,3 +59,13 @@ def test_bench_reference_arm_small(gpu_ready):
     assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
     ours = _bench("--config", "c3", "--scale", "32", "--steps", "1", "--warmup", "1", "--no-cpu")
     assert ours["config"] == d["config"]  # the driver's same_config check
+
+
+def test_bench_partitioned_hscg_line(gpu_ready):
+    """The distributed-HSCG comparison line (§8(f)2): two allreduces and one
+    halo exchange per iteration, measured from its captured graph."""
+    d = _bench("--solver", "hscg", "--partitioned", "--scale", "32", "--steps", "1", "--warmup",
+               "1")
+    assert d["solver"] == "hscg" and d["solve"]["status"] == "converged"
+    assert d["solve"]["collectives"]["allreduce_per_outer"] == 2
+    assert d["solve"]["collectives"]["halo_exchanges_per_outer"] == 1

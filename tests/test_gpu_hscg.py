@@ -89,3 +89,58 @@ def test_hscg_max_iters_zero_and_tridiag(gpu_ready):
     _, tr, co = hscg_solve(prob, 1e-10)
     t = assemble_tridiag(co, 5)
     assert np.allclose(t, t.T) and t.shape == (5, 5)
+
+
+def test_hscg_production_mode(gpu_ready):
+    """Production HSCG (one SpMV per iteration, verdicts on the updated
+    residual, the true residual formed once at the end): the same alphas as the
+    reference-semantics run while both iterate, and the final true residual
+    meets eps*."""
+    prob = problems.make_problem("c3", scale=24)
+    x1, t1, c1 = hscg_solve(prob, 1e-10)
+    x2, t2, c2 = hscg_solve(prob, 1e-10, mode="production")
+    assert t1.converged and t2.converged
+    m = min(len(c1.alphas), len(c2.alphas))
+    np.testing.assert_array_equal(c2.alphas[:m], c1.alphas[:m])
+    assert abs(t2.total_iters - t1.total_iters) <= 2
+    a = prob.a
+    m_ = sp.csr_matrix((a.values, a.col_idx, a.row_ptr), shape=(a.n, a.n))
+    rel = np.linalg.norm(prob.b - m_ @ x2) / np.linalg.norm(prob.b)
+    assert t2.true_resid[-1] == pytest.approx(rel, rel=1e-8) and rel <= 1e-9
+
+
+@pytest.mark.parametrize("mode", ["reference", "production"])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_hscg_distributed(gpu_ready, mode, world):
+    """Distributed HSCG (§8(f)2): row slabs with depth-1 ghosts, per iteration
+    one halo exchange and two reductions (virtual group: device copies and
+    fixed-order sums).  P = 1 equals the single-GPU run bit for bit; P > 1
+    agrees to reduction order (alphas 1e-10 early, same verdict, counts +-2)."""
+    from paper_1908_04081_b200.dist import VirtualGroup
+    from paper_1908_04081_b200.partition import CsrRows
+    prob = problems.make_problem("c5", scale=20)
+    x1, t1, c1 = hscg_solve(prob, 1e-10, mode=mode)
+    g = VirtualGroup(CsrRows.of(prob.a), world, depth=1)
+    xg, tg, cg = g.hscg(prob, 1e-10, mode=mode)
+    if world == 1:
+        np.testing.assert_array_equal(cg.alphas, c1.alphas)
+        np.testing.assert_array_equal(xg, x1)
+        return
+    np.testing.assert_allclose(cg.alphas[:20], c1.alphas[:20], rtol=1e-10)
+    assert tg.converged == t1.converged and abs(tg.total_iters - t1.total_iters) <= 2
+    assert tg.true_resid[-1] <= 1e-10
+
+
+def test_hscg_nccl_world1(gpu_ready):
+    """The NCCL transport of distributed HSCG at world size 1 (halo and both
+    allreduces captured in the iteration graph) reproduces the single GPU."""
+    from paper_1908_04081_b200.dist import hscg_partitioned
+    from paper_1908_04081_b200.partition import CsrRows
+    prob = problems.make_problem("c3", scale=24)
+    for mode in ("reference", "production"):
+        x1, t1, c1 = hscg_solve(prob, 1e-10, mode=mode)
+        xo, tr, co, plan = hscg_partitioned(CsrRows.of(prob.a), prob.b, prob.x0, 1e-10, 0, 1, 0,
+                                            exchange=lambda o: [o], broadcast_bytes=lambda b: b,
+                                            mode=mode)
+        np.testing.assert_array_equal(xo, x1)
+        np.testing.assert_array_equal(co.alphas, c1.alphas)
