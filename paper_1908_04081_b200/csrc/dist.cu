@@ -52,6 +52,7 @@ __global__ void k_halo_pack(const double* __restrict__ P0, const double* __restr
   if (*done) return;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int i = idx[t], o = dst[t], k = cnt[t];
+    SSCG_CHECK(i >= 0 && o >= 0 && o + 2 * k < 3 * n + 2 * k);
     buf[o] = P0[i];
     buf[o + k] = R0[i];
     buf[o + 2 * k] = x[i];

@@ -280,6 +280,20 @@ inline void mark_device_done(std::atomic<unsigned long long>& mask) {
   mask.fetch_or(1ull << (dev & 63), std::memory_order_release);
 }
 
+// Device-side bounds checks of the checked side build (-DSSCG_CHECKED, the
+// stand-in for compute-sanitizer, which this pool does not offer): a violated
+// index traps with a kernel fault the host reports.  Compiled out otherwise.
+#ifdef SSCG_CHECKED
+#define SSCG_CHECK(cond)   \
+  do {                     \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define SSCG_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 #define CUDA_OK(expr)                                             \
   do {                                                            \
     cudaError_t e__ = (expr);                                     \

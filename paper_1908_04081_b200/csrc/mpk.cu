@@ -441,6 +441,7 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
   int pid_n1 = (z0 + 1 < z1 && r1 < plim) ? (int)__ldg(pidp + r1) : 0;
   for (int z = z0; z < z1; ++z) {
     const int pid = pid_cur;
+    SSCG_CHECK(pid < c.pat_np);
     const int r2 = z + 2 < np ? row_of(z + 2) : n;
     const int pid_n2 = (z + 2 < z1 && r2 < plim) ? (int)__ldg(pidp + r2) : 0;
     double nx[NV];
@@ -508,6 +509,7 @@ __device__ __forceinline__ void zm_column(const Ctx& c, const SsSmem& T, const i
         if (q == NO - 1 && NO > 1 && !rrow) break;
         const double y2 = MU ? ym[q][r] : 0.0;
         const double w = recur_t<UNIT>(acc[Q0 + q], cu[Q0 + q], y2, th, ga, mu, MU);
+        SSCG_CHECK(r >= 0 && r < c.ld);
         yo[q][r] = w;
         bad |= !finite(w);
       }
@@ -708,6 +710,7 @@ __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
       if (k < NE) {
         v[kk] = __ldg(vp + (int64_t)k * ldv);
         const int j = vs_nbr<PL>(c, i, nm1, k, zg, pin);
+        SSCG_CHECK(j >= 0 && j < c.ld);
 #pragma unroll
         for (int q = 0; q < NV; ++q) xb[q][kk] = __ldg(xs[q] + j);
       }

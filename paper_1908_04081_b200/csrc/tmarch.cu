@@ -208,6 +208,7 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
         // plane coordinate: geometric plane -> local block (plane table) or
         // itself; outside the walk -1 (zero fill)
         const int pz = (zz >= 0 && zz < np) ? (table ? sh.ptab[zz] / S : zz) : -1;
+        SSCG_CHECK(pz >= -1 && pz < np + (table ? 64 : 1));
         unsigned char* dst = stg + (size_t)s * SB;
         mbar_arrive_tx(&full[s], tm_tx_bytes(NV, L0));
 #pragma unroll
@@ -270,6 +271,7 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
     if (!CHECK || r < plim) {
       const uint32_t cur = my0 + sc * SB;  // this plane's centre
       const uint32_t pid = lds_u8(id0 + sc * SB);
+      SSCG_CHECK((int)pid < c.pat_np);
       const uint32_t va = pv0 + pid * (SS_MAX_NE * 8);
       const double2 v01 = lds_f64x2(va), v23 = lds_f64x2(va + 16), v45 = lds_f64x2(va + 32);
       const double v6 = lds_f64(va + 48);
@@ -296,6 +298,7 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
         if (q == NO - 1 && NO > 1 && r >= rlim) break;
         const double y2 = MU ? __ldg(zp.ym[q] + r) : 0.0;
         const double w = tm_recur<UNIT>(acc[Q0 + q], cc[Q0 + q], y2, th, ga, mu, MU);
+        SSCG_CHECK(r >= 0 && r < c.ld && (!MU || zp.ym[q] != nullptr));
         zp.yo[q][r] = w;
         // exponent all ones (inf / NaN) carries into bit 31: checked once at the end
         badm |= (((unsigned)__double2hiint(w)) & 0x7ff00000u) + 0x00100000u;
