@@ -857,7 +857,76 @@ def gen_full():
         del prob
 
 
+def first_block_cases():
+    """x0 = 0 problems (the first block's P and R columns are bitwise
+    duplicates: p = r): 2-D / 3-D Poisson with random x*, random dense SPD
+    spectra, Strakos diagonals -- with Newton, Chebyshev and monomial bases."""
+    cases = []
+    for seed in range(6):
+        cases.append((f"p2d_{seed}", lambda s=seed: to_ref(problems.poisson2d(24 + 4 * s, seed=s)),
+                      dict(sigma=8, eps_star=1e-10, basis_kind="newton")))
+        cases.append((f"p3d_{seed}", lambda s=seed: to_ref(problems.poisson3d(10 + s, seed=s)),
+                      dict(sigma=10, eps_star=1e-10, basis_kind=("chebyshev" if seed % 2 else "newton"))))
+        kap = [1e2, 1e4, 1e6, 1e3, 1e5, 3e4][seed]
+        cases.append((f"spd_{seed}", lambda s=seed, k=kap: dense_problem(spd_dense(60, k, 100 + s),
+                                                                          f"spd{s}"),
+                      dict(sigma=6 + seed % 3, eps_star=1e-9,
+                           basis_kind=("newton", "chebyshev", "monomial")[seed % 3])))
+        cases.append((f"strakos_{seed}", lambda s=seed: to_ref(problems.strakos(400 + 100 * s, seed=s)),
+                      dict(sigma=10, eps_star=1e-8, basis_kind=("chebyshev" if seed % 2 else "newton"))))
+    return cases
+
+
+def _first_blocks_run():
+    """(in a subprocess with OPENBLAS_CORETYPE set) the reference's first three
+    outer loops of every first-block case: (s~, s_actual) and the first conds."""
+    out = {}
+    for name, mk, kw in first_block_cases():
+        prob = mk()
+        cfg = ref_adaptive.AdaptiveConfig(max_outer=3, **kw)
+        _, tr, co = ref_adaptive.adaptive_solve(prob, cfg)
+        out[name] = dict(seq=[[r.s_tilde, r.s_actual] for r in tr.outer_records],
+                         conds=[float(v) for v in tr.outer_records[0].cond_used],
+                         alphas=[float(a) for a in co.alphas[:6]])
+    print("JSON" + json.dumps(out))
+
+
+def gen_first_blocks():
+    """The first-block decisions (p = r, duplicated Gram columns: the noise-level
+    condition estimates DESIGN.md 5 discusses) of the reference under two
+    OpenBLAS kernel choices (OPENBLAS_CORETYPE Haswell / SkylakeX): the
+    decisions the GPU's calibrated noise floor must reproduce."""
+    import subprocess
+    res = {}
+    for core in ("Haswell", "SkylakeX"):
+        env = dict(os.environ, OPENBLAS_CORETYPE=core, PYTHONPATH=REF_SRC)
+        p = subprocess.run([sys.executable, os.path.abspath(__file__), "_first_blocks_run"],
+                           env=env, capture_output=True, text=True, check=True)
+        line = [l for l in p.stdout.splitlines() if l.startswith("JSON")][-1]
+        res[core] = json.loads(line[4:])
+    cases = first_block_cases()
+    names = [n for n, _, _ in cases]
+    out = {"names": np.array(names), "cores": np.array(list(res))}
+    for name, mk, kw in cases:  # dense SPD inputs are stored (their QR is BLAS-dependent)
+        if name.startswith("spd_"):
+            out.update({f"{name}_in_" + k: v for k, v in problem_arrays(mk()).items()})
+    for ci, core in enumerate(res):
+        for name in names:
+            d = res[core][name]
+            seq = np.full((3, 2), -1, dtype=np.int64)
+            seq[:len(d["seq"])] = d["seq"]
+            out[f"{name}_{core}_seq"] = seq
+            out[f"{name}_{core}_conds"] = np.array(d["conds"])
+            out[f"{name}_{core}_alphas"] = np.array(d["alphas"])
+    save("first_blocks", **out)
+    same = sum(np.array_equal(out[f"{n}_Haswell_seq"], out[f"{n}_SkylakeX_seq"]) for n in names)
+    print(f"    {len(names)} cases; the two kernel choices agree on {same}")
+
+
 def main():
+    if sys.argv[1:] == ["_first_blocks_run"]:
+        _first_blocks_run()
+        return
     os.makedirs(OUT, exist_ok=True)
     print("reference:", sstepcg.__file__)
     which = sys.argv[1:] or ["leja", "params", "ritz", "gram_conds", "blocks", "solves"]
