@@ -320,7 +320,7 @@ int pattern_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 size_t ss_smem_bytes(int np);
 int ss_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
 int zm_ctas_per_sm(int np, int ne, int pid_bytes, int* out2);
-int vs_ctas_per_sm(int ne, int* out2);
+int vs_ctas_per_sm(int ne, bool pl, int* out2);
 // tmarch.cu
 int tm_make_maps(TmMaps* m, const double* Y, int64_t ld, int ncols, const double* x, const double* b,
                  const void* pid, int64_t o, int64_t S, int64_t planes, int64_t id_planes);

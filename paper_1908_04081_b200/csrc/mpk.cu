@@ -677,15 +677,15 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, ZM_MINB) k_level_zm(Ctx c, int l
 #ifndef VS_CHUNK
 #define VS_CHUNK 5  // slots per batch of gathers (c4j: 3.80 ms/outer; 9: 4.1, 14: 4.6, 27: 4.3)
 #endif
-// neighbour row of union slot k (PL: a row-partitioned plan's plane tables;
-// the row's own index for a slot whose plane is not held -- absent slots only)
+// neighbour row of union slot k.  PL (a row-partitioned plan): slot k lies
+// vs_dz[k] in {-1, 0, 1} planes away at vs_r[k] rows within the plane; pb[]
+// holds the local first rows of the planes below / of / above the row (the
+// row's own plane where one is not held -- absent slots only, value 0.0).
+// Either way an absent slot reads some in-range row (clamped).
 template <bool PL>
-__device__ __forceinline__ int vs_nbr(const Ctx& c, int i, int nm1, int k, int zg, int pin) {
+__device__ __forceinline__ int vs_nbr(const Ctx& c, int i, int nm1, int k, const int* pb, int pin) {
   if (!PL) return min(max(i + c.vs_off[k], 0), nm1);
-  const int S = (int)c.vs_S;
-  const int zz = zg + c.vs_dz[k];
-  const int b = (zz >= 0 && zz < c.vs_np) ? __ldg(c.vs_base + zz) : -1;
-  return b >= 0 ? b + min(max(pin + c.vs_r[k], 0), S - 1) : i;
+  return min(max(pb[c.vs_dz[k] + 1] + pin + c.vs_r[k], 0), nm1);
 }
 
 template <int NV, int NE, bool PL = false>
@@ -695,11 +695,17 @@ __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
   for (int q = 0; q < NV; ++q) acc[q] = 0.0;
   const double* vp = c.vs_val + i;
   const int64_t ldv = c.ld;
-  int zg = 0, pin = 0;
+  int pb[3] = {0, 0, 0}, pin = 0;
   if (PL) {
     const int S = (int)c.vs_S, blk = i / S;
-    zg = __ldg(c.vs_geo + blk);
+    const int zg = __ldg(c.vs_geo + blk);
     pin = i - blk * S;
+    const int own = i - pin;
+    const int bm = zg > 0 ? __ldg(c.vs_base + zg - 1) : -1;
+    const int bp = zg + 1 < c.vs_np ? __ldg(c.vs_base + zg + 1) : -1;
+    pb[0] = bm >= 0 ? bm : own;
+    pb[1] = own;
+    pb[2] = bp >= 0 ? bp : own;
   }
 #pragma unroll
   for (int k0 = 0; k0 < NE; k0 += VS_CHUNK) {
@@ -709,7 +715,7 @@ __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
       const int k = k0 + kk;
       if (k < NE) {
         v[kk] = __ldg(vp + (int64_t)k * ldv);
-        const int j = vs_nbr<PL>(c, i, nm1, k, zg, pin);
+        const int j = vs_nbr<PL>(c, i, nm1, k, pb, pin);
         SSCG_CHECK(j >= 0 && j < c.ld);
 #pragma unroll
         for (int q = 0; q < NV; ++q) xb[q][kk] = __ldg(xs[q] + j);
@@ -738,7 +744,8 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_vs(Ctx c, ZmPtrs zp) {
   double tt = 0.0, rr = 0.0;
   int bad = 0;
   const int n_own = (int)c.n_own, plim = (int)lvl_p_rows(c, sigma, 0);
-  const int rlim = do_r ? (int)lvl_r_rows(c, sigma, 0) : 0, nm1 = (int)c.n - 1;
+  const int rlim = do_r ? (int)lvl_r_rows(c, sigma, 0) : 0;
+  const int nm1 = (int)(PL ? c.lvl_rows[SMAX] : c.n) - 1;
   const int stride = gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
     double acc[3];
@@ -778,7 +785,7 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level_vs(Ctx c, int l, ZmPtrs 
   const bool use_mu = !(mu == 0.0);  // basis.py:217 `if mu != 0.0` (NaN counts)
   const bool do_r = l < sbar - 1;
   const int plim = (int)lvl_p_rows(c, sigma, l), rlim = (int)lvl_r_rows(c, sigma, l);
-  const int nm1 = (int)c.n - 1;
+  const int nm1 = (int)(PL ? c.lvl_rows[SMAX] : c.n) - 1;
   const int stride = gridDim.x * blockDim.x;
   int bad = 0;
   const double* xs[2] = {zp.xs[0], zp.xs[1]};
@@ -1091,13 +1098,19 @@ int zm_ctas_per_sm(int np, int ne, int pid_bytes, int* out2) {
   return a < b ? a : b;
 }
 
-// value-stream kernels: CTAs per SM of level 0 and levels >= 1
-int vs_ctas_per_sm(int ne, int* out2) {
+// value-stream kernels (plain or plane-table form): CTAs per SM of level 0
+// and levels >= 1
+int vs_ctas_per_sm(int ne, bool pl, int* out2) {
   const int nb = ne <= 9 ? 9 : ne <= 18 ? 18 : ne <= 27 ? 27 : 32;
   int a = 0, b = 0;
-#define VS_OCC(NE)                                                                          \
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_level0_vs<NE, true>, ROWS_PER_CTA, 0);  \
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_level_vs<NE, true>, ROWS_PER_CTA, 0);
+#define VS_OCC(NE)                                                                              \
+  if (pl) {                                                                                     \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_level0_vs<NE, true>, ROWS_PER_CTA, 0);  \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_level_vs<NE, true>, ROWS_PER_CTA, 0);   \
+  } else {                                                                                      \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_level0_vs<NE, false>, ROWS_PER_CTA, 0); \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_level_vs<NE, false>, ROWS_PER_CTA, 0);  \
+  }
   if (nb == 9) { VS_OCC(9) } else if (nb == 18) { VS_OCC(18) } else if (nb == 27) { VS_OCC(27) } else { VS_OCC(32) }
 #undef VS_OCC
   out2[0] = a;

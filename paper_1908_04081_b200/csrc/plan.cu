@@ -957,7 +957,7 @@ int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col
   }
   const int ne = (int)uni.size();
   int occ[2] = {0, 0};
-  if (ne < 3 || vs_ctas_per_sm(ne, occ) < 1) return SSCG_OK;
+  if (ne < 3 || vs_ctas_per_sm(ne, grows != nullptr, occ) < 1) return SSCG_OK;
   std::vector<int> geo, base;
   if (grows) {  // plane tables of the partitioned form
     int64_t S = 0;
@@ -967,7 +967,7 @@ int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col
       bool dec = true;
       for (int64_t o : uni) {
         const int64_t dz = (o >= 0 ? o + cand / 2 : o - cand / 2) / cand, r = o - dz * cand;
-        dec = dec && 2 * std::llabs(r) < cand && std::llabs(dz) <= 127;
+        dec = dec && 2 * std::llabs(r) < cand && std::llabs(dz) <= 1;  // neighbour planes only
       }
       if (!dec) continue;
       std::vector<int> b = plane_bases(n_local, grows, cand);
