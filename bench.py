@@ -127,7 +127,8 @@ class ClockSampler:
 def kernel_name(sched):
     """The level kernel (levels >= 1) a matrix-powers schedule runs."""
     if sched["kind"] == "pattern":
-        return {"march": "k_level_zm", "superset": "k_level_ss"}.get(sched.get("form"), "k_level_pat")
+        return {"tma march": "k_level_tm", "march": "k_level_zm",
+                "superset": "k_level_ss"}.get(sched.get("form"), "k_level_pat")
     return {"csr": "k_level_staged", "stencil values": "k_level_vs"}[sched["kind"]]
 
 

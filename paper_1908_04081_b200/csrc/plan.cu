@@ -1505,8 +1505,10 @@ int sscg_plan_mpk_schedule(sscg_plan* p, int32_t sigma, int32_t* out) {
   out[0] = p->d_pid ? 2 : p->vs_ne ? 3 : 0;
   out[1] = p->red_n;
   out[2] = p->d_pid ? p->pat_np : p->vs_ne;
-  // last slot: pattern kernel form (0 table walk, 1 superset mask, 2 plane march)
-  if (p->d_pid) out[3 + 2 * SMAX] = p->zm_S > 0 ? 2 : p->ss_ne > 0 ? 1 : 0;
+  // last slot: pattern kernel form (0 table walk, 1 superset mask, 2 plane
+  // march, 3 the TMA plane march)
+  if (p->d_pid) out[3 + 2 * SMAX] = p->zm_S > 0 ? (p->tm_on ? 3 : 2) : p->ss_ne > 0 ? 1 : 0;
+  if (p->tm_on) out[1] = p->tm_grid;
   out[3] = sigma;
   for (int q = 0; q < sigma; ++q) out[4 + 2 * q] = 1;
   return SSCG_OK;

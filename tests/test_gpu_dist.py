@@ -92,6 +92,9 @@ def test_partitioned_slabs_keep_the_plane_march(gpu_ready, world):
     rows happen to be in grid order."""
     from paper_1908_04081_b200.dist import VirtualGroup
     g = VirtualGroup(Stencil7Rows(32, 32, 32 * world), world, 12)
+    assert [pl.mpk_schedule(12)["form"] for pl in g.plans] == ["tma march"] * world
+    # x lines of 28: the register march (the TMA boxes need 32-column tiles)
+    g = VirtualGroup(Stencil7Rows(28, 28, 28 * world), world, 12)
     assert [pl.mpk_schedule(12)["form"] for pl in g.plans] == ["march"] * world
 
 

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 
 _KEYS = ("SSCG_PATTERN", "SSCG_PAT_SS", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_VS",
-         "SSCG_ZM_DYN")
+         "SSCG_ZM_DYN", "SSCG_TM")
 
 
 def _with_env(env, fn):
@@ -110,6 +110,8 @@ def test_pattern_kernel_forms(gpu_ready):
     def form(prob, env=None):
         return _with_env(env or {}, lambda: _plan(prob().a).mpk_schedule(8)["form"])
     assert form(lambda: problems.make_problem("c5", scale=28)) == "march"
+    assert form(lambda: problems.make_problem("c5", scale=32)) == "tma march"
+    assert form(lambda: problems.make_problem("c5", scale=32), {"SSCG_TM": "0"}) == "march"
     assert form(lambda: problems.make_problem("c3", scale=24)) == "march"
     assert form(lambda: problems.make_problem("c1")) == "superset"
     assert form(_tridiag_many_patterns) == "superset"
@@ -118,13 +120,17 @@ def test_pattern_kernel_forms(gpu_ready):
 
 
 @pytest.mark.parametrize("env", [{"SSCG_ZM": "0"}, {"SSCG_PAT_SS": "0"}, {"SSCG_ZM_ZC": "3"},
-                                 {"SSCG_ZM_2D": "0"}, {"SSCG_ZM_DYN": "0"}],
-                         ids=["superset", "table", "march_zc3", "march_1d", "static_items"])
+                                 {"SSCG_ZM_2D": "0"}, {"SSCG_ZM_DYN": "0"}, {"SSCG_TM": "0"},
+                                 {"SSCG_TM": "0", "SSCG_ZM_DYN": "0"}],
+                         ids=["superset", "table", "march_zc3", "march_1d", "static_items",
+                              "register_march", "register_march_static"])
 def test_pattern_forms_bit_identical(gpu_ready, env):
     """Plane march (default), its opt-in variants, superset mask and table
     walk run the same rounded operations in the same order: identical solves
     (Newton and Chebyshev bases, unit and non-unit gamma, mu != 0).  The 32^3
-    grids give whole 32 x 8 column tiles (2-D tiled march)."""
+    grids give whole 32 x 8 column tiles: the default there is the TMA march,
+    so the reference run and every variant compare the TMA-fed and register
+    marches too."""
     for key, scale, kw in (("c5", 28, dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
                            ("c3", 24, dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev")),
                            ("c5", 32, dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
