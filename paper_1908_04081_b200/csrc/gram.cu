@@ -21,8 +21,14 @@
 
 namespace {
 
-constexpr int GT_ROWS = 128;
-constexpr int GT_STAGES = 4;
+#ifndef GT_ROWS_DEF
+#define GT_ROWS_DEF 128
+#endif
+#ifndef GT_STAGES_DEF
+#define GT_STAGES_DEF 4
+#endif
+constexpr int GT_ROWS = GT_ROWS_DEF;
+constexpr int GT_STAGES = GT_STAGES_DEF;
 constexpr int GT_LD = GT_ROWS + 4;  // LD % 16 == 4: conflict-free fragment loads
 constexpr int GT_CONSUMERS = 8;                    // DMMA warps (16 rows of a tile each)
 constexpr int GT_THREADS = (GT_CONSUMERS + 1) * 32;  // + one TMA producer warp

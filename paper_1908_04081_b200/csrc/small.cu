@@ -366,6 +366,30 @@ __device__ __forceinline__ int nested_col(int s_bar, int i, int q) {
   return q <= i ? q : s_bar + 1 + (q - i - 1);
 }
 
+// nested_basis_conds over warps w0 .. NW-1 (k_small: warp 0 runs the
+// coefficient-space loop meanwhile): warp w handles i = w - w0 + 1, + (NW - w0), ...
+__device__ void cta_nested_conds_from(const double* G, int ldg, int s_bar, double* conds,
+                                      double* jac, int w0) {
+  const int rr = s_bar + 1;
+  const bool dup = G[0] == G[rr * ldg + rr] && G[0] == G[rr];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* A = jac + (size_t)warp * (CMAX * JLD + 4 * CMAX);
+  double* rot = A + CMAX * JLD;
+  if (warp == w0 && lane == 0) conds[0] = NAN;
+  // largest blocks first: they set the critical path
+  for (int i = s_bar - (warp - w0); i >= 1; i -= NW - w0) {
+    const int n = 2 * i + 1;
+    for (int e = lane; e < n * n; e += 32) {
+      const int a = e / n, b = e % n;
+      A[a * JLD + b] = G[nested_col(s_bar, i, a) * ldg + nested_col(s_bar, i, b)];
+    }
+    __syncwarp();
+    const double cnd = warp_cond_estimate(A, n, rot, dup);
+    if (lane == 0) conds[i] = cnd;
+    __syncwarp();
+  }
+}
+
 // nested_basis_conds: warp w handles i = w+1, w+1+NW, ...  G has leading dim ldg.
 __device__ void cta_nested_conds(const double* G, int ldg, int s_bar, double* conds,
                                  double* jac /* NW * (CMAX*JLD + 68) */) {
@@ -768,6 +792,44 @@ __device__ __forceinline__ void warp_bapply(const double* B, int ldb, const doub
   __syncwarp();
 }
 
+// the speculative coefficient-space loop's per-iteration record (k_small)
+struct SpecRecord {
+  double xp[SMAX + 1][CMAX], rp[SMAX + 1][CMAX], pp[SMAX + 1][CMAX];  // after iteration j-1
+  RitzDev rz[SMAX + 1];
+  double alpha[SMAX], beta[SMAX], rr[SMAX], est[SMAX], phi[SMAX], cnow[SMAX];
+  double phi0;
+  int n, div_at;
+};
+
+// adaptive.py:89-104: the largest i with conds[i] <= bound (default 1)
+__device__ __forceinline__ int select_stilde(const double* conds, int sbar, double bound) {
+  int s_t = 1;
+  for (int i = 1; i <= sbar; ++i)
+    if (conds[i] <= bound) s_t = i;
+  return s_t;
+}
+
+// would the reference's loop have stopped at or before recorded iteration
+// j_next - 1 (given s~)?  The loop bound, est_hit, or a basis-quality break.
+// Full-bound c depends on s~'s B_t: those runs decide only in the final scan.
+__device__ __forceinline__ bool spec_stops(const SpecRecord& R, int j_next, int s_t,
+                                           const double* conds, const DevConfig& cf, bool fixed,
+                                           double u, double c_sel) {
+  for (int j = 0; j < j_next; ++j) {
+    if (j >= s_t) return true;
+    if (R.rr[j] >= 0.0 && R.est[j] <= cf.eps_star && j < s_t - 1) return true;
+    if (fixed || cf.c_strategy == SSCG_C_FULLBOUND) continue;
+    if (cf.variant == 1) {
+      const double thr = cf.eps_star / (R.cnow[j] * u * R.phi[j]);
+      if (j < s_t - 1 && conds[j + 2] >= thr) return true;
+    } else if (R.est[j] > 0.0) {
+      const double thr = cf.eps_star / (c_sel * u * R.est[j]);  // c_blk: the block-start c
+      if (conds[s_t] >= thr) return true;
+    }
+  }
+  return false;
+}
+
 __device__ double cta_sum(const double* part, int n, double* red) {
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += NT) s += part[i];
@@ -786,12 +848,14 @@ struct SmallShared {
   double G[CMAX * CMAX];   // s_bar-block Gram, ld CMAX
   double B[CMAX * CMAX];   // B(s_bar) then B_t, ld CMAX
   double Gt[CMAX * CMAX];  // truncated Gram, ld CMAX
+  double Bt[CMAX * CMAX];  // truncated B, ld CMAX
   double conds[SMAX + 1];
   double xp[CMAX], rp[CMAX], pp[CMAX], t1[CMAX], t2[CMAX];
   double red[NT];
   double sc[16];
   int si[16];
   LejaShared L;
+  SpecRecord R;
 };
 
 constexpr size_t JAC_BYTES = sizeof(double) * (size_t)NW * (CMAX * JLD + 4 * CMAX);
@@ -808,7 +872,7 @@ enum { SC_TRUE, SC_UPD, SC_CSEL, SC_RREL, SC_CBLK, SC_PHI };
       t_prev__ = now__;                                                 \
     }                                                                   \
   } while (0)
-enum { SI_FLAG, SI_SBAR, SI_STILDE, SI_JDONE, SI_DIV, SI_BRKJ };
+enum { SI_FLAG, SI_SBAR, SI_STILDE, SI_JDONE, SI_DIV, SI_BRKJ, SI_CDONE, SI_CWARPS };
 
 // ---------------------------------------------------------------------------
 // K_small
@@ -913,38 +977,169 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
 
   PHASE(1);
   const bool fixed = cf.solver == SSCG_SOLVER_FIXED;
-  // ---- nested condition estimates and s~ (adaptive.py:89-104); the fixed
-  //      s-step solver always runs the whole block (sstep.py:124-125)
-  if (!fixed) cta_nested_conds(S.G, CMAX, sbar, S.conds, jac);
-  else if (tid <= SMAX) S.conds[tid] = NAN;
+  // ---- the coefficient-space loop (adaptive.py:173-246) runs on warp 0 WHILE
+  //      warps 1.. compute the nested condition estimates (adaptive.py:89-104):
+  //      it iterates speculatively on the whole s_bar block.  When s~ = s_bar
+  //      (most blocks of the BASELINE solves) that IS the block's iteration;
+  //      each iteration's stop data are recorded, and once s~ is known the
+  //      reference's stop rules pick the iteration the block ends at -- its
+  //      recorded state is the result, the same whenever s~ became known.
+  //      When s~ < s_bar the loop reruns on the truncated block (below).
+  build_bmat(S.B, CMAX, sbar, st->prm);  // B(s_bar) (syncs)
+  if (tid == 0) {
+    S.si[SI_CDONE] = fixed ? 1 : 0;
+    S.si[SI_CWARPS] = 0;
+  }
+  __syncthreads();
+  SpecRecord& R = S.R;
+  // the loop on warp 0 over a block in layout sb (P_0..P_sb, R_0..R_{sb-1} with
+  // Gram Gm and change of basis Bm, ld CMAX); s_fix >= 0: s~ is known, else
+  // it is learnt when the estimates finish (SI_CDONE)
+  auto run_loop = [&](const double* Gm, const double* Bm, int sb, int s_fix) {
+    const int Dl = 2 * sb + 1;
+    for (int i = lane; i < CMAX; i += 32) {
+      S.xp[i] = 0.0;
+      S.rp[i] = (i == sb + 1) ? 1.0 : 0.0;
+      S.pp[i] = (i == 0) ? 1.0 : 0.0;
+      R.xp[0][i] = S.xp[i];
+      R.rp[0][i] = S.rp[i];
+      R.pp[0][i] = S.pp[i];
+    }
+    __syncwarp();
+    warp_matvec(Gm, CMAX, S.rp, S.t1, Dl);
+    const double q0 = warp_dot0(S.rp, S.t1, Dl);
+    double phi = sqrt(py_max(0.0, q0)) / nb;
+    if (lane == 0) {
+      R.phi0 = phi;
+      R.rz[0] = st->rz;
+    }
+    RitzDev rz = st->rz;
+    double num = q0;  // r'^T G r' of iteration j = rr of iteration j-1 (same operands)
+    int nj = 0, div_at = -1;
+    int s_known = s_fix;
+    for (int j = 0; j < sb; ++j) {
+      if (s_known < 0) {  // the estimates just finished: s~ bounds the loop from here on
+        int cd = lane == 0 ? *(volatile int*)&S.si[SI_CDONE] : 0;
+        cd = __shfl_sync(0xffffffffu, cd, 0);  // one view for the whole warp
+        if (cd) {
+          __threadfence_block();
+          s_known = select_stilde(S.conds, sbar, eps / (S.sc[SC_CSEL] * u * S.sc[SC_UPD]));
+        }
+      }
+      if (s_known >= 0 &&
+          (j >= s_known || spec_stops(R, j, s_known, S.conds, cf, fixed, u, S.sc[SC_CSEL])))
+        break;
+      warp_bapply(Bm, CMAX, S.pp, S.t1, Dl);
+      warp_matvec(Gm, CMAX, S.t1, S.t2, Dl);
+      const double den = warp_dot0(S.pp, S.t2, Dl);
+      if (den <= 0.0 || num < 0.0 || !isfinite(den) || !isfinite(num)) {
+        div_at = j;
+        break;
+      }
+      const double alpha = num / den;
+      for (int i = lane; i < Dl; i += 32) {
+        const double q = alpha * S.pp[i];
+        S.t1[i] = q;
+        S.xp[i] = S.xp[i] + q;
+      }
+      __syncwarp();
+      warp_bapply(Bm, CMAX, S.t1, S.t2, Dl);
+      for (int i = lane; i < Dl; i += 32) S.rp[i] = S.rp[i] - S.t2[i];
+      __syncwarp();
+      warp_matvec(Gm, CMAX, S.rp, S.t1, Dl);
+      const double rr = warp_dot0(S.rp, S.t1, Dl);
+      const double beta = rr / num;
+      for (int i = lane; i < Dl; i += 32) S.pp[i] = S.rp[i] + beta * S.pp[i];
+      __syncwarp();
+      num = rr;
+      if (alpha > 0.0 && beta > 0.0 && isfinite(alpha) && isfinite(beta))
+        ritz_absorb(rz, alpha, beta);  // identical in every lane
+      const double est = sqrt(py_max(0.0, rr)) / nb;
+      phi = py_max(phi, est);
+      for (int i = lane; i < CMAX; i += 32) {
+        R.xp[j + 1][i] = S.xp[i];
+        R.rp[j + 1][i] = S.rp[i];
+        R.pp[j + 1][i] = S.pp[i];
+      }
+      if (lane == 0) {
+        R.alpha[j] = alpha;
+        R.beta[j] = beta;
+        R.rr[j] = rr;
+        R.est[j] = est;
+        R.phi[j] = phi;
+        R.cnow[j] = c_from_state(cf.c_strategy, rz, cf.c0);
+        R.rz[j + 1] = rz;
+      }
+      if (cf.trace_full) {
+        // physical-column coordinates of (x_j - x, r_j)
+        for (int i = lane; i < CMAX; i += 32) {
+          st->dx[j][i] = 0.0;
+          st->dr[j][i] = 0.0;
+        }
+        __syncwarp();
+        for (int i = lane; i < Dl; i += 32) {
+          const int ph = (i <= sb) ? i : sigma + 1 + (i - sb - 1);
+          st->dx[j][ph] = S.xp[i];
+          st->dr[j][ph] = S.rp[i];
+        }
+      }
+      __syncwarp();
+      nj = j + 1;
+    }
+    if (lane == 0) {
+      R.n = nj;
+      R.div_at = div_at;
+    }
+  };
+  if (warp == 0) {
+    run_loop(S.G, S.B, sbar, fixed ? sbar : -1);
+  } else if (!fixed) {
+    cta_nested_conds_from(S.G, CMAX, sbar, S.conds, jac, 1);  // warps 1 .. NW-1
+    __syncwarp();
+    __threadfence_block();  // this warp's estimates before its count
+    if (lane == 0 && atomicAdd(&S.si[SI_CWARPS], 1) == NW - 2) {
+      __threadfence_block();
+      *(volatile int*)&S.si[SI_CDONE] = 1;
+    }
+  }
   __syncthreads();
   PHASE(2);
   if (tid == 0) {
     const double r_rel = S.sc[SC_UPD];
     const double bound = eps / (S.sc[SC_CSEL] * u * r_rel);
-    int s_t = 1;
-    for (int i = 1; i <= sbar; ++i)
-      if (S.conds[i] <= bound) s_t = i;
-    S.si[SI_STILDE] = fixed ? sbar : s_t;
+    if (fixed)
+      for (int i = 0; i <= SMAX; ++i) S.conds[i] = NAN;
+    S.si[SI_STILDE] = fixed ? sbar : select_stilde(S.conds, sbar, bound);
     S.sc[SC_RREL] = r_rel;
   }
   __syncthreads();
   const int s_t = S.si[SI_STILDE];
   const int dim = 2 * s_t + 1;
-
-  // ---- truncated block: G_t and B_t (adaptive.py:162-171)
-  for (int e = tid; e < dim * dim; e += NT) {
-    const int i = e / dim, j = e % dim;
-    const int gi = i <= s_t ? i : sbar + 1 + (i - s_t - 1);
-    const int gj = j <= s_t ? j : sbar + 1 + (j - s_t - 1);
-    S.Gt[i * CMAX + j] = S.G[gi * CMAX + gj];
+  // ---- s~ < s_bar: the block is truncated (adaptive.py:162-171).  The
+  //      speculative iterates are mathematically the truncated block's, but
+  //      its dot products would add the dropped columns' zeros at other lane
+  //      positions; to keep the truncated layout's rounding the loop runs
+  //      again on G_t, B_t (the common s~ = s_bar block keeps the speculation).
+  const bool rerun = !fixed && s_t < sbar;
+  const int lsb = rerun ? s_t : sbar;  // layout of the recorded iterates
+  if (rerun || cf.c_strategy == SSCG_C_FULLBOUND) {
+    for (int e = tid; e < dim * dim; e += NT) {
+      const int i = e / dim, j = e % dim;
+      const int gi = i <= s_t ? i : sbar + 1 + (i - s_t - 1);
+      const int gj = j <= s_t ? j : sbar + 1 + (j - s_t - 1);
+      S.Gt[i * CMAX + j] = S.G[gi * CMAX + gj];
+    }
+    build_bmat(S.Bt, CMAX, s_t, st->prm);  // B_t (syncs)
   }
-  build_bmat(S.B, CMAX, s_t, st->prm);  // (syncs)
+  if (rerun) {
+    if (warp == 0) run_loop(S.Gt, S.Bt, s_t, s_t);
+    __syncthreads();
+  }
 
-  // ---- c_block (adaptive.py:175)
+  // ---- c_block (adaptive.py:175); full-bound needs |B_t| of the truncated block
   if (cf.c_strategy == SSCG_C_FULLBOUND) {
     if (warp == 0) {
-      const double an = warp_abs_norm(S.B, CMAX, dim, jac);
+      const double an = warp_abs_norm(S.Bt, CMAX, dim, jac);
       if (lane == 0)
         S.sc[SC_CBLK] = full_bound_c(s_t, cf.n_a, cf.nu, an / cf.norm_a, cf.kappa_a);
     }
@@ -954,97 +1149,32 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
   __syncthreads();
 
   PHASE(3);
-  // ---- coefficient-space inner loop (adaptive.py:173-246), warp 0
+  // ---- the block's end by the reference's stop rules over the recorded
+  //      iterations, then the record and the log rows
   if (warp == 0) {
-    for (int i = lane; i < CMAX; i += 32) {
-      S.xp[i] = 0.0;
-      S.rp[i] = (i == s_t + 1) ? 1.0 : 0.0;
-      S.pp[i] = (i == 0) ? 1.0 : 0.0;
-    }
-    __syncwarp();
-    warp_matvec(S.Gt, CMAX, S.rp, S.t1, dim);
-    const double q0 = warp_dot0(S.rp, S.t1, dim);
-    double phi = sqrt(py_max(0.0, q0)) / nb;
     const double c_blk = S.sc[SC_CBLK];
     const int mark = st->total_iters;
-    int it = st->total_iters;
     int j_done = 0, diverged = 0, brk_j = -1;
     double brk_l = NAN, brk_r = NAN;
-    RitzDev rz = st->rz;
-    // num = r'^T G r' of iteration j equals rr of iteration j-1 (same operands)
-    double num = q0;
     for (int j = 0; j < s_t; ++j) {
-      warp_bapply(S.B, CMAX, S.pp, S.t1, dim);
-      warp_matvec(S.Gt, CMAX, S.t1, S.t2, dim);
-      const double den = warp_dot0(S.pp, S.t2, dim);
-      if (den <= 0.0 || num < 0.0 || !isfinite(den) || !isfinite(num)) {
-        diverged = 1;
+      if (j == R.div_at || j >= R.n) {  // den <= 0 or non-finite (adaptive.py:184-186)
+        diverged = (j == R.div_at);
         break;
       }
-      const double alpha = num / den;
-      for (int i = lane; i < dim; i += 32) {
-        const double q = alpha * S.pp[i];
-        S.t1[i] = q;
-        S.xp[i] = S.xp[i] + q;
-      }
-      __syncwarp();
-      warp_bapply(S.B, CMAX, S.t1, S.t2, dim);
-      for (int i = lane; i < dim; i += 32) S.rp[i] = S.rp[i] - S.t2[i];
-      __syncwarp();
-      warp_matvec(S.Gt, CMAX, S.rp, S.t1, dim);
-      const double rr = warp_dot0(S.rp, S.t1, dim);
-      const double beta = rr / num;
-      for (int i = lane; i < dim; i += 32) S.pp[i] = S.rp[i] + beta * S.pp[i];
-      __syncwarp();
-      num = rr;
       j_done = j + 1;
-      if (alpha > 0.0 && beta > 0.0 && isfinite(alpha) && isfinite(beta))
-        ritz_absorb(rz, alpha, beta);  // identical in every lane
-      const double est = sqrt(py_max(0.0, rr)) / nb;
-      phi = py_max(phi, est);
-      if (lane == 0 && it < cf.cap_iters) {
-        double* row = c.it_log + (int64_t)it * SSCG_IT_N;
-        row[SSCG_IT_ALPHA] = alpha;
-        row[SSCG_IT_BETA] = beta;
-        row[SSCG_IT_XI] = ritz_xi(rz);
-        row[SSCG_IT_LMIN] = ritz_lmin(rz);
-        row[SSCG_IT_LMAX] = ritz_lmax(rz);
-        row[SSCG_IT_PSI] = rz.psi;
-        row[SSCG_IT_EST] = est;
-        if (!cf.trace_full) {
-          row[SSCG_IT_TRUE] = est;
-          row[SSCG_IT_UPD] = est;
-          row[SSCG_IT_GAP] = NAN;
-        }
-      }
-      if (cf.trace_full) {
-        // physical-column coordinates of (x_j - x, r_j)
-        for (int i = lane; i < CMAX; i += 32) {
-          st->dx[j][i] = 0.0;
-          st->dr[j][i] = 0.0;
-        }
-        __syncwarp();
-        for (int i = lane; i < dim; i += 32) {
-          const int ph = (i <= s_t) ? i : sigma + 1 + (i - s_t - 1);
-          st->dx[j][ph] = S.xp[i];
-          st->dr[j][ph] = S.rp[i];
-        }
-      }
-      ++it;
-      if (rr >= 0.0 && est <= eps && j < s_t - 1) break;  // est_hit
+      if (R.rr[j] >= 0.0 && R.est[j] <= eps && j < s_t - 1) break;  // est_hit
       if (fixed) continue;  // no basis-quality breaks in fixed s-step CG
       if (cf.variant == 1) {
-        const double c_now =
-            (cf.c_strategy == SSCG_C_FULLBOUND) ? c_blk : c_from_state(cf.c_strategy, rz, cf.c0);
-        const double thr = eps / (c_now * u * phi);
+        const double c_now = (cf.c_strategy == SSCG_C_FULLBOUND) ? c_blk : R.cnow[j];
+        const double thr = eps / (c_now * u * R.phi[j]);
         if (j < s_t - 1 && S.conds[j + 2] >= thr) {
           brk_j = j;
           brk_l = S.conds[j + 2];
           brk_r = thr;
           break;
         }
-      } else if (est > 0.0) {
-        const double thr = eps / (c_blk * u * est);
+      } else if (R.est[j] > 0.0) {
+        const double thr = eps / (c_blk * u * R.est[j]);
         if (S.conds[s_t] >= thr) {
           brk_j = j;
           brk_l = S.conds[s_t];
@@ -1053,12 +1183,33 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
         }
       }
     }
+    const double phi = j_done > 0 ? R.phi[j_done - 1] : R.phi0;
+    // log rows of the iterations the block keeps (trace.record_iteration)
+    for (int j = lane; j < j_done; j += 32) {
+      const int it = mark + j;
+      if (it < cf.cap_iters) {
+        const RitzDev& rj = R.rz[j + 1];
+        double* row = c.it_log + (int64_t)it * SSCG_IT_N;
+        row[SSCG_IT_ALPHA] = R.alpha[j];
+        row[SSCG_IT_BETA] = R.beta[j];
+        row[SSCG_IT_XI] = ritz_xi(rj);
+        row[SSCG_IT_LMIN] = ritz_lmin(rj);
+        row[SSCG_IT_LMAX] = ritz_lmax(rj);
+        row[SSCG_IT_PSI] = rj.psi;
+        row[SSCG_IT_EST] = R.est[j];
+        if (!cf.trace_full) {
+          row[SSCG_IT_TRUE] = R.est[j];
+          row[SSCG_IT_UPD] = R.est[j];
+          row[SSCG_IT_GAP] = NAN;
+        }
+      }
+    }
     if (lane == 0) {
-      st->rz = rz;
+      st->rz = R.rz[j_done];
       // trace.mark_outer + record (adaptive.py:178, 232-246)
       const int k = st->k;
       st->total_outer += 1;
-      st->total_iters = it;
+      st->total_iters = mark + j_done;
       st->diag_base = mark;
       st->diag_n = cf.trace_full ? j_done : 0;
       st->s_tilde = s_t;
@@ -1100,20 +1251,24 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
       S.si[SI_DIV] = diverged;
       S.si[SI_JDONE] = j_done;
     }
-    // recovery coefficients in physical columns (zero elsewhere)
+    // recovery coefficients in physical columns (zero elsewhere): the iterate
+    // recorded after the block's last kept iteration (layout lsb)
     __syncwarp();
     if (!S.si[SI_DIV]) {
+      const double* xj = R.xp[j_done];
+      const double* rj = R.rp[j_done];
+      const double* pj = R.pp[j_done];
       for (int i = lane; i < CMAX; i += 32) {
         st->cx[i] = 0.0;
         st->cr[i] = 0.0;
         st->cp[i] = 0.0;
       }
       __syncwarp();
-      for (int i = lane; i < dim; i += 32) {
-        const int ph = (i <= s_t) ? i : sigma + 1 + (i - s_t - 1);
-        st->cx[ph] = S.xp[i];
-        st->cr[ph] = S.rp[i];
-        st->cp[ph] = S.pp[i];
+      for (int i = lane; i < 2 * lsb + 1; i += 32) {
+        const int ph = (i <= lsb) ? i : sigma + 1 + (i - lsb - 1);
+        st->cx[ph] = xj[i];
+        st->cr[ph] = rj[i];
+        st->cp[ph] = pj[i];
       }
     }
   }
