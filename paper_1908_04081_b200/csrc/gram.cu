@@ -288,8 +288,11 @@ __device__ __forceinline__ void gram_body(const double* __restrict__ Y, int64_t 
 template <int NB, int REM>
 __global__ void __launch_bounds__(GT_THREADS) k_gram_state(Ctx c) {
   if (c.st->done) return;
+  TL_K(c, 0);
+  TL_BEGIN(c, 16);
   gram_body<NB, REM, true>(c.Y, c.ld, c.n_own, c.cfg->ncols, c.part_g, c.red_buf,
                            &c.st->gram_count, c.part_t, c.part_r, c.red_n);
+  TL_END(c, 16);
 }
 
 template <int NB, int REM>

@@ -120,7 +120,7 @@ struct Ctx {
   double* part_r;   // [RED_BLOCKS] ||r||^2 partials
   double* part_d;   // [3][RED_BLOCKS] full-trace partials
   double* part_g;   // [GRAM_BLOCKS][GPACK] Gram partials
-  double* leja_obj; // [leja_grid] scratch
+  double* leja_obj; // [4 leja_grid] grid objective + pairwise-sum state (small.cu leja_obj_point)
   int leja_grid_host;  // cfg->leja_grid as the host knew it at launch / capture
   // logs (device)
   double* it_log;   // [cap_iters][SSCG_IT_N]
@@ -201,7 +201,37 @@ struct Ctx {
   int pf_ahead;
   const unsigned* ss_mask;  // [pat_np]
   const double* ss_val;     // [pat_np][SS_MAX_NE], absent slots 0
+#ifdef SSCG_TIMELINE
+  unsigned long long* tl;   // [TL_REPS][TL_NODES][2] first start / last end (globaltimer ns)
+#endif
 };
+
+// Timeline side build (-DSSCG_TIMELINE, tools/timeline.py): every kernel of the
+// outer-loop graph records its first CTA's start and its last warp's end per
+// outer loop -- where the time between the kernels goes (there is no nsys here).
+#ifdef SSCG_TIMELINE
+constexpr int TL_NODES = 40, TL_REPS = 128;
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_K(c, adj) const int tlk__ = (c).st->k + (adj)
+#define TL_BEGIN(c, node)                                                         \
+  do {                                                                            \
+    if (threadIdx.x == 0 && tlk__ >= 0 && tlk__ < TL_REPS)                        \
+      atomicMin(&(c).tl[(tlk__ * TL_NODES + (node)) * 2], tl_now());              \
+  } while (0)
+#define TL_END(c, node)                                                           \
+  do {                                                                            \
+    if ((threadIdx.x & 31) == 0 && tlk__ >= 0 && tlk__ < TL_REPS)                 \
+      atomicMax(&(c).tl[(tlk__ * TL_NODES + (node)) * 2 + 1], tl_now());          \
+  } while (0)
+#else
+#define TL_K(c, adj)
+#define TL_BEGIN(c, node)
+#define TL_END(c, node)
+#endif
 
 // rows level l must produce for P (ghost depth <= sigma-1-l) and R (<= sigma-2-l)
 __host__ __device__ inline int64_t lvl_p_rows(const Ctx& c, int sigma, int l) {

@@ -225,7 +225,7 @@ int ensure_work(sscg_plan* p, int sigma, int64_t max_outer, int leja_grid) {
     }
   }
   if (leja_grid > p->leja_cap) {
-    TRY(dalloc(p, &p->d_leja, (size_t)leja_grid));
+    TRY(dalloc(p, &p->d_leja, 4 * (size_t)leja_grid));  // objective + pairwise-sum state
     p->leja_cap = leja_grid;
     if (p->gexec) {
       cudaGraphExecDestroy(p->gexec);
@@ -235,8 +235,26 @@ int ensure_work(sscg_plan* p, int sigma, int64_t max_outer, int leja_grid) {
   return SSCG_OK;
 }
 
+#ifdef SSCG_TIMELINE
+unsigned long long* g_tl_buf = nullptr;
+void tl_reset() {
+  const size_t n = (size_t)TL_REPS * TL_NODES;
+  std::vector<unsigned long long> h(2 * n);
+  for (size_t i = 0; i < n; ++i) {
+    h[2 * i] = ~0ull;
+    h[2 * i + 1] = 0;
+  }
+  if (!g_tl_buf) cudaMalloc(&g_tl_buf, sizeof(unsigned long long) * 2 * n);
+  cudaMemcpy(g_tl_buf, h.data(), sizeof(unsigned long long) * 2 * n, cudaMemcpyHostToDevice);
+}
+#endif
+
 Ctx make_ctx(sscg_plan* p) {
   Ctx c;
+#ifdef SSCG_TIMELINE
+  if (!g_tl_buf) tl_reset();
+  c.tl = g_tl_buf;
+#endif
   c.rp = p->d_rp;
   c.col = p->d_col;
   c.val = p->d_val;
@@ -501,6 +519,55 @@ int launch_outer_profiled(sscg_plan* p, const Ctx& c, int sigma, int full, int o
 }  // namespace
 
 extern "C" {
+
+#ifdef SSCG_TIMELINE
+// copy out [TL_REPS][TL_NODES][2] and reset (single device, debugging only)
+int sscg_debug_timeline(unsigned long long* out, int* reps, int* nodes) {
+  cudaDeviceSynchronize();
+  *reps = TL_REPS;
+  *nodes = TL_NODES;
+  if (!g_tl_buf) tl_reset();
+  if (out) {
+    cudaMemcpy(out, g_tl_buf, sizeof(unsigned long long) * 2 * TL_REPS * TL_NODES,
+               cudaMemcpyDeviceToHost);
+    tl_reset();
+  }
+  return (int)cudaGetLastError();
+}
+#endif
+
+#ifdef SSCG_TIMELINE
+// `reps` back-to-back launches of one HBM-bound kernel on the plan's buffers
+// (0: Gram of k columns, 1: recovery from k columns): the kernel's time at
+// its own steady-state clocks, to compare with its time inside the graph
+int sscg_debug_steady(sscg_plan* p, int which, int k, int reps, float* ms_per_launch) {
+  cudaSetDevice(p->device);
+  double* coef = nullptr;
+  cudaMalloc(&coef, sizeof(double) * 3 * CMAX);
+  cudaMemset(coef, 0, sizeof(double) * 3 * CMAX);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaMemsetAsync(&p->d_st->gram_count, 0, sizeof(int), p->stream);
+  cudaEventRecord(a, p->stream);
+  for (int i = 0; i < reps; ++i) {
+    if (which == 0)
+      launch_gram_raw(p->d_Y, p->n_own, p->ld, k, p->d_part_g, p->d_red, &p->d_st->gram_count, p->stream);
+    else
+      launch_recover_raw(p->d_Y, p->n_own, p->ld, k, coef, p->d_x, p->d_x, p->d_Y + (int64_t)(p->cfg.sigma + 1) * p->ld,
+                         p->d_Y, p->stream);
+  }
+  cudaEventRecord(b, p->stream);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  *ms_per_launch = ms / reps;
+  cudaFree(coef);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return (int)cudaGetLastError();
+}
+#endif
 
 const char* sscg_last_error(void) { return g_err.c_str(); }
 int sscg_abi_version(void) { return SSCG_ABI_VERSION; }

@@ -64,6 +64,8 @@ __global__ void __launch_bounds__(REC_THREADS) k_recover(Ctx c) {
   __shared__ int cols[CMAX];
   const SolverState* st = c.st;
   if (!st->rec_valid) return;
+  TL_K(c, -1);
+  TL_BEGIN(c, 18);
   const int sigma = c.cfg->sigma, s_t = st->s_tilde;
   const int k = 2 * s_t + 1;
   if (threadIdx.x == 0) active_cols(s_t, sigma, cols);
@@ -87,6 +89,7 @@ __global__ void __launch_bounds__(REC_THREADS) k_recover(Ctx c) {
     *reinterpret_cast<double2*>(R0 + i2) = ar;
     *reinterpret_cast<double2*>(P0 + i2) = ap;
   }
+  TL_END(c, 18);
 }
 
 // full trace: x_j = x + Y x'_j, r_j = Y r'_j into scratch (adaptive.py:205)

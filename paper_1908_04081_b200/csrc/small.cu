@@ -510,7 +510,8 @@ __device__ __forceinline__ double lin_x(int i, int grid, double lo, double hi, d
 
 // One greedy Leja step (basis.py:105-126, one pass of the `while` loop): given
 // pts[0..n-1] (in L.pts) and the grid objective of pts[0..n-2] in `obj` (global
-// scratch, carried between calls), append pts[n].  CTA-wide.
+// scratch of 4 * grid doubles -- the objective and the pairwise-sum state of
+// leja_obj_point -- carried between calls), append pts[n].  CTA-wide.
 #ifdef LEJA_DBG
 __device__ unsigned long long g_leja_dbg[8];
 #define LDBG(i)                                                             \
@@ -525,22 +526,35 @@ __device__ unsigned long long g_leja_dbg[8];
 #else
 #define LDBG(i)
 #endif
-// One grid point's objective after adding pts[n-1] (pts[0..n-1] for n = 2, 8:
-// numpy's pairwise blocks restart there), from its value for pts[0..n-2]
-__device__ __forceinline__ double leja_obj_point(double x, double prev, int n, const double* pts) {
+// One grid point's objective after adding pts[n-1], from the state carried for
+// that grid point.  numpy sums the n < 16 log terms r_0..r_{n-1} pairwise:
+// n < 8 a running sum from 0.0; n >= 8 ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+// then the tail in order.  So that the step to n = 8 needs one new log like
+// every other step (not all eight again), the tree's partial sums are carried
+// beside the running sum: A = r0+r1 (n = 2), then (r0+r1)+(r2+r3) (n = 4);
+// B = r4+r5 (n = 6); T = the odd term waiting for its pair (n = 3, 5, 7).
+// st = the grid point's slot in the state arrays [A | B | T], each `grid` long.
+__device__ __forceinline__ double leja_obj_point(double x, double prev, int n, const double* pts,
+                                                 double* st, int grid) {
   if (n == 2) {
+    const double r0 = log(fabs(x - pts[0]) + 1e-300), r1 = log(fabs(x - pts[1]) + 1e-300);
     double o = 0.0;
-    o += log(fabs(x - pts[0]) + 1e-300);
-    o += log(fabs(x - pts[1]) + 1e-300);
+    o += r0;
+    o += r1;
+    st[0] = r0 + r1;
     return o;
   }
-  if (n == 8) {
-    double r[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = log(fabs(x - pts[j]) + 1e-300);
-    return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  const double r = log(fabs(x - pts[n - 1]) + 1e-300);
+  switch (n) {
+    case 3:
+    case 5:
+    case 7: st[2 * grid] = r; break;
+    case 4: st[0] = st[0] + (st[2 * grid] + r); break;
+    case 6: st[grid] = st[2 * grid] + r; break;
+    case 8: return st[0] + (st[grid] + (st[2 * grid] + r));
+    default: break;
   }
-  return prev + log(fabs(x - pts[n - 1]) + 1e-300);
+  return prev + r;
 }
 
 // sobj: the objective in shared memory as well (k_leja_point, grid <=
@@ -563,13 +577,14 @@ __device__ void cta_leja_point(double lo, double hi, int n, int grid, double* ob
 #pragma unroll
     for (int k = 0; k < LB; ++k) {
       const int i = i0 + k * nt;
-      prev[k] = (n != 2 && n != 8 && i < grid) ? obj[i] : 0.0;
+      prev[k] = (n != 2 && n != 8 && i < grid) ? obj[i] : 0.0;  // n = 8 restarts from the tree
     }
 #pragma unroll
     for (int k = 0; k < LB; ++k) {
       const int i = i0 + k * nt;
       if (i < grid) {
-        const double o = leja_obj_point(lin_x(i, grid, lo, hi, step, zero_step), prev[k], n, L.pts);
+        const double o = leja_obj_point(lin_x(i, grid, lo, hi, step, zero_step), prev[k], n, L.pts,
+                                        obj + grid + i, grid);
         obj[i] = o;
         if (sobj) sobj[i] = o;
       }
@@ -673,7 +688,7 @@ __device__ void cta_leja_point(double lo, double hi, int n, int grid, double* ob
 #endif
 }
 
-// basis.py:91-127 leja_points, CTA-wide; obj is a global scratch of `grid` doubles
+// basis.py:91-127 leja_points, CTA-wide; obj is a global scratch of 4 * grid doubles
 __device__ void cta_leja(double lo, double hi, int count, int grid, double* out, double* obj,
                          LejaShared& L) {
   if (threadIdx.x == 0) {
@@ -892,6 +907,8 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
     return;
   }
   long long t_prev__ = clock64();
+  TL_K(c, 0);
+  TL_BEGIN(c, 17);
   if (tid == 0) st->phase_cycles[7] += 1;
   // the Gram kernel packed [G lower | ||b-Ax||^2 | ||r||^2] into red_buf (and on
   // a row-partitioned solve NCCL has allreduced it): one synchronisation
@@ -1286,6 +1303,7 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
     st->k = st->k + 1;
     st->breakdown = 0;
   }
+  TL_END(c, 17);
 }
 
 // Next-block basis parameters (adaptive.py:254-258 -> basis.py:166-177), run at
@@ -1297,6 +1315,8 @@ __global__ void k_params_begin(Ctx c) {
   SolverState* st = c.st;
   const DevConfig cf = *c.cfg;  // by value: global log stores would force reloads
   if (threadIdx.x != 0) return;
+  TL_K(c, 0);
+  TL_BEGIN(c, 19);
   st->leja_on = 0;
   if (st->done) return;
   if (cf.solver == SSCG_SOLVER_FIXED) return;  // parameters fixed for the solve
@@ -1329,12 +1349,15 @@ __global__ void __launch_bounds__(NT) k_leja_point(Ctx c, int n) {
   extern __shared__ double lsm[];  // the grid objective (LEJA_SMEM_GRID points at most)
   SolverState* st = c.st;
   if (!st->leja_on || n >= c.cfg->sigma) return;
+  TL_K(c, 0);
+  TL_BEGIN(c, 20 + n);
   if (threadIdx.x < n) L.pts[threadIdx.x] = st->prm.th[threadIdx.x];
   __syncthreads();
   const int grid = c.cfg->leja_grid;
   cta_leja_point(st->prm.lo, st->prm.hi, n, grid, c.leja_obj, L,
                  grid <= LEJA_SMEM_GRID ? lsm : nullptr);
   if (threadIdx.x == 0) st->prm.th[n] = L.pts[n];
+  TL_END(c, 20 + n);
 }
 
 // full trace: reduce the diag partials of inner iteration j into the log
@@ -1556,7 +1579,7 @@ int unit_leja(double lo, double hi, int count, int grid, double* out) {
   int rc = SSCG_OK;
   double *dout = nullptr, *obj = nullptr;
   U_OK(cudaMalloc(&dout, sizeof(double) * SMAX));
-  U_OK(cudaMalloc(&obj, sizeof(double) * (grid > 0 ? grid : 1)));
+  U_OK(cudaMalloc(&obj, sizeof(double) * 4 * (grid > 0 ? grid : 1)));
   k_unit_leja<<<1, NT, small_smem_bytes()>>>(lo, hi, count, grid, dout, obj);
   U_OK(cudaGetLastError());
   U_OK(cudaMemcpy(out, dout, sizeof(double) * count, cudaMemcpyDeviceToHost));
@@ -1574,7 +1597,7 @@ int unit_params_for(int kind, int s, int has, double lo, double hi, int grid, do
   double* obj = nullptr;
   ParamsDev hp;
   U_OK(cudaMalloc(&dp, sizeof(ParamsDev)));
-  U_OK(cudaMalloc(&obj, sizeof(double) * (grid > 0 ? grid : 1)));
+  U_OK(cudaMalloc(&obj, sizeof(double) * 4 * (grid > 0 ? grid : 1)));
   k_unit_params<<<1, NT, small_smem_bytes()>>>(kind, s, has, lo, hi, grid, dp, obj);
   U_OK(cudaGetLastError());
   U_OK(cudaMemcpy(&hp, dp, sizeof(ParamsDev), cudaMemcpyDeviceToHost));

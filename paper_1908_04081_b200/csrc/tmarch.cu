@@ -410,12 +410,15 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB)
   __syncthreads();
   TmShared sh{full, empty, sitem, red, pval, ptab,
               tsm + tm_head_bytes(c.pat_np, c.zm_np, table)};
+  TL_K(c, 0);
+  TL_BEGIN(c, l);
   if (L0) {
     const bool do_r = sbar >= 2;
     if (st->prm.ga[0] == 1.0)
       tm_body<3, true, 0>(c, 0, zp, maps, sh, false, do_r);
     else
       tm_body<3, true, 1>(c, 0, zp, maps, sh, false, do_r);
+    TL_END(c, 0);
     return;
   }
   const double ga = st->prm.ga[l], mu = st->prm.mu[l - 1];
@@ -436,6 +439,7 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB)
     TM_RK(1)
   }
 #undef TM_RK
+  TL_END(c, l);
 }
 
 template <bool L0>
