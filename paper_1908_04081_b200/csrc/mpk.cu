@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, ZM_MINB) k_level_zm(Ctx c, int l
 // slot has value 0.0 and gathers from the clamped index (in range, finite:
 // see zm_column): adding 0.0 * x = +-0.0 is exact -- bit-identical to CSR.
 #ifndef VS_CHUNK
-#define VS_CHUNK 5  // slots per batch of gathers (c4j: 3.80 ms/outer; 9: 4.1, 14: 4.6, 27: 4.3)
+#define VS_CHUNK 7  // slots per batch of gathers
 #endif
 // neighbour row of union slot k.  PL (a row-partitioned plan): slot k lies
 // vs_dz[k] in {-1, 0, 1} planes away at vs_r[k] rows within the plane; pb[]
@@ -688,13 +688,40 @@ __device__ __forceinline__ int vs_nbr(const Ctx& c, int i, int nm1, int k, const
   return min(max(pb[c.vs_dz[k] + 1] + pin + c.vs_r[k], 0), nm1);
 }
 
+// The value stream is the DRAM stream of these kernels, so each chunk's values
+// are requested VS_DEPTH chunks before their use -- across rows too: vq holds
+// the next VS_DEPTH chunks (of this row, then of the row this thread handles
+// next, inext; < 0: none), a register queue the unrolled loop renames for free.
+#ifndef VS_DEPTH
+#define VS_DEPTH 1
+#endif
+#ifndef VS_MINB
+#define VS_MINB 4  // CTAs per SM the register allocation must allow (64 registers)
+#endif
+template <int NE>
+__device__ __forceinline__ void vs_request(const Ctx& c, int i, int chunk, double (&v)[VS_CHUNK]) {
+  const double* vp = c.vs_val + i + (int64_t)(chunk * VS_CHUNK) * c.ld;
+#pragma unroll
+  for (int kk = 0; kk < VS_CHUNK; ++kk)
+    if (chunk * VS_CHUNK + kk < NE) v[kk] = __ldg(vp + (int64_t)kk * c.ld);
+}
+// the first row's first VS_DEPTH chunks
+template <int NE>
+__device__ __forceinline__ void vs_first(const Ctx& c, int i, double (&vq)[VS_DEPTH][VS_CHUNK]) {
+#pragma unroll
+  constexpr int NCH = (NE + VS_CHUNK - 1) / VS_CHUNK;
+#pragma unroll
+  for (int d = 0; d < (VS_DEPTH < NCH ? VS_DEPTH : NCH); ++d) vs_request<NE>(c, i, d, vq[d]);
+}
+
 template <int NV, int NE, bool PL = false>
 __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
-                                       const double* const* __restrict__ xs, double* acc) {
+                                       const double* const* __restrict__ xs, double* acc,
+                                       double (&vq)[VS_DEPTH][VS_CHUNK], int inext) {
+  constexpr int NCH = (NE + VS_CHUNK - 1) / VS_CHUNK;
+  constexpr int D = VS_DEPTH < NCH ? VS_DEPTH : NCH;  // the queue reaches at most one row ahead
 #pragma unroll
   for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-  const double* vp = c.vs_val + i;
-  const int64_t ldv = c.ld;
   int pb[3] = {0, 0, 0}, pin = 0;
   if (PL) {
     const int S = (int)c.vs_S, blk = i / S;
@@ -708,13 +735,23 @@ __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
     pb[2] = bp >= 0 ? bp : own;
   }
 #pragma unroll
-  for (int k0 = 0; k0 < NE; k0 += VS_CHUNK) {
+  for (int ch = 0; ch < NCH; ++ch) {
+    const int k0 = ch * VS_CHUNK;
     double v[VS_CHUNK], xb[NV][VS_CHUNK];
+#pragma unroll
+    for (int kk = 0; kk < VS_CHUNK; ++kk) v[kk] = vq[0][kk];
+#pragma unroll
+    for (int d = 0; d + 1 < D; ++d)
+#pragma unroll
+      for (int kk = 0; kk < VS_CHUNK; ++kk) vq[d][kk] = vq[d + 1][kk];
+    if (ch + D < NCH)
+      vs_request<NE>(c, i, ch + D, vq[D - 1]);
+    else if (inext >= 0)
+      vs_request<NE>(c, inext, ch + D - NCH, vq[D - 1]);
 #pragma unroll
     for (int kk = 0; kk < VS_CHUNK; ++kk) {
       const int k = k0 + kk;
       if (k < NE) {
-        v[kk] = __ldg(vp + (int64_t)k * ldv);
         const int j = vs_nbr<PL>(c, i, nm1, k, pb, pin);
         SSCG_CHECK(j >= 0 && j < c.ld);
 #pragma unroll
@@ -732,7 +769,7 @@ __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
 }
 
 template <int NE, bool PL>
-__global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_vs(Ctx c, ZmPtrs zp) {
+__global__ void __launch_bounds__(ROWS_PER_CTA, VS_MINB) k_level0_vs(Ctx c, ZmPtrs zp) {
   __shared__ double sm[ROWS_PER_CTA / 32];
   const SolverState* st = c.st;
   if (st->done) return;
@@ -747,9 +784,12 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_vs(Ctx c, ZmPtrs zp) {
   const int rlim = do_r ? (int)lvl_r_rows(c, sigma, 0) : 0;
   const int nm1 = (int)(PL ? c.lvl_rows[SMAX] : c.n) - 1;
   const int stride = gridDim.x * blockDim.x;
+  double vn[VS_DEPTH][VS_CHUNK];
+  if ((int)(blockIdx.x * blockDim.x + threadIdx.x) < plim)
+    vs_first<NE>(c, blockIdx.x * blockDim.x + threadIdx.x, vn);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
     double acc[3];
-    vs_row<3, NE, PL>(c, i, nm1, xs, acc);
+    vs_row<3, NE, PL>(c, i, nm1, xs, acc, vn, i + stride < plim ? i + stride : -1);
     const double p = xs[1][i], r = xs[2][i];
     if (i < n_own) {
       const double t = __dsub_rn(c.b[i], acc[0]);
@@ -775,7 +815,7 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level0_vs(Ctx c, ZmPtrs zp) {
 }
 
 template <int NE, bool PL>
-__global__ void __launch_bounds__(ROWS_PER_CTA) k_level_vs(Ctx c, int l, ZmPtrs zp) {
+__global__ void __launch_bounds__(ROWS_PER_CTA, VS_MINB) k_level_vs(Ctx c, int l, ZmPtrs zp) {
   const SolverState* st = c.st;
   if (st->done) return;
   const int sbar = st->s_bar;
@@ -789,13 +829,17 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_level_vs(Ctx c, int l, ZmPtrs 
   const int stride = gridDim.x * blockDim.x;
   int bad = 0;
   const double* xs[2] = {zp.xs[0], zp.xs[1]};
+  double vn[VS_DEPTH][VS_CHUNK];
+  if ((int)(blockIdx.x * blockDim.x + threadIdx.x) < plim)
+    vs_first<NE>(c, blockIdx.x * blockDim.x + threadIdx.x, vn);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
     double acc[2];
     const bool rrow = do_r && i < rlim;
+    const int inext = i + stride < plim ? i + stride : -1;
     if (rrow)
-      vs_row<2, NE, PL>(c, i, nm1, xs, acc);
+      vs_row<2, NE, PL>(c, i, nm1, xs, acc, vn, inext);
     else
-      vs_row<1, NE, PL>(c, i, nm1, xs, acc);
+      vs_row<1, NE, PL>(c, i, nm1, xs, acc, vn, inext);
     const double wp = recur(acc[0], xs[0][i], use_mu ? zp.ym[0][i] : 0.0, th, ga, mu, use_mu);
     zp.yo[0][i] = wp;
     bad |= !finite(wp);

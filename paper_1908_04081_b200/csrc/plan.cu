@@ -1056,7 +1056,10 @@ int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col
       p->vs_r[k] = (int)(o - dz * S);
     }
   }
-  std::vector<double> sv((size_t)ne * (size_t)p->ld, 0.0);
+  // the kernels unroll over a bucket of slots (9 / 18 / 27 / 32): slots past the
+  // union exist and hold 0.0
+  const int nb = ne <= 9 ? 9 : ne <= 18 ? 18 : ne <= 27 ? 27 : 32;
+  std::vector<double> sv((size_t)nb * (size_t)p->ld, 0.0);
   for (int64_t i = 0; i < n; ++i) {
     int k = 0;
     for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; ++j) {
