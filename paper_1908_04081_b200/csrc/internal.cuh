@@ -45,6 +45,7 @@
 // x and b as [plane][line][x], the 1-byte row ids as [plane][line][x]
 struct TmMaps {
   CUtensorMap y, x, b, id;
+  CUtensorMap y8;  // Y again with a 32 x 8 box (no halo): the two-back vectors of a Chebyshev level
 };
 
 struct RitzDev {  // ritz.py:28-158

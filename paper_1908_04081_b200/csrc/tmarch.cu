@@ -51,11 +51,13 @@ struct Ring {
   static constexpr int R = L0 ? TM_R0 : TM_R;
 };
 
+// a stage: the input boxes, then 2 KB tiles without halo -- level 0: b; levels
+// >= 1: the two two-back vectors (loaded only when mu != 0) -- then the row ids
 __host__ __device__ constexpr int tm_stage_bytes(int nv, bool l0) {
-  return nv * TM_BOXB + (l0 ? 2048 : 0) + 256;
+  return nv * TM_BOXB + (l0 ? 2048 : 4096) + 256;
 }
-__host__ __device__ constexpr uint32_t tm_tx_bytes(int nv, bool l0) {
-  return (uint32_t)(nv * TM_BOX * 8 + (l0 ? 2048 : 0) + 256);
+__host__ __device__ constexpr uint32_t tm_tx_bytes(int nv, bool l0, bool mu) {
+  return (uint32_t)(nv * TM_BOX * 8 + (l0 ? 2048 : mu ? nv * 2048 : 0) + 256);
 }
 __host__ __device__ inline size_t tm_head_bytes(int pat_np, int zm_np, bool table) {
   const size_t a = (size_t)pat_np * SS_MAX_NE * 8 + (table ? 4 * (size_t)zm_np : 0);
@@ -160,7 +162,8 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
   constexpr int NO = L0 ? NV - 1 : NV;  // output vectors
   constexpr int Q0 = L0 ? 1 : 0;        // first input with an output
   constexpr int SB = tm_stage_bytes(L0 ? 3 : 2, L0);  // stage stride (the kernel's largest NV)
-  constexpr int IDO = (L0 ? 3 : 2) * TM_BOXB + (L0 ? 2048 : 0);  // row ids within a stage
+  constexpr int IDO = (L0 ? 3 : 2) * TM_BOXB + (L0 ? 2048 : 4096);  // row ids within a stage
+  constexpr int YMO = 2 * TM_BOXB;  // two-back tiles within a stage (levels >= 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool table = c.zm_base != nullptr;
   const int S = (int)c.zm_S, o = c.zm_o, lines = S / o, ntx = o >> 5;
@@ -210,7 +213,7 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
         const int pz = (zz >= 0 && zz < np) ? (table ? sh.ptab[zz] / S : zz) : -1;
         SSCG_CHECK(pz >= -1 && pz < np + (table ? 64 : 1));
         unsigned char* dst = stg + (size_t)s * SB;
-        mbar_arrive_tx(&full[s], tm_tx_bytes(NV, L0));
+        mbar_arrive_tx(&full[s], tm_tx_bytes(NV, L0, MU));
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
           if (L0 && q == 0)
@@ -219,6 +222,11 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
             tma_load_4d(dst + q * TM_BOXB, &maps.y, x0 - TM_XH, y0 - 1, pz, colq[q], &full[s]);
         }
         if (L0) tma_load_3d(dst + 3 * TM_BOXB, &maps.b, x0, y0, pz, &full[s]);
+        if (MU) {  // y_{l-1} of the tile (basis.py:217-218), no halo
+#pragma unroll
+          for (int q = 0; q < NV; ++q)
+            tma_load_4d(dst + YMO + q * 2048, &maps.y8, x0, y0, pz, colq[q] - 1, &full[s]);
+        }
         tma_load_3d(dst + IDO, &maps.id, x0, y0, pz, &full[s]);
       }
       it = dyn ? (int)atomicAdd(ctr, 1u) : it + (int)gridDim.x;
@@ -245,6 +253,7 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
   const uint32_t id0 = smem_u32(stg) + IDO + (uint32_t)(warp * 32 + lane);  // row id, stage 0
   const uint32_t pv0 = smem_u32(sh.pval);
   const uint32_t b0 = smem_u32(stg) + 3 * TM_BOXB + 8u * (uint32_t)(warp * 32 + lane);  // level 0's b
+  const uint32_t ym0 = smem_u32(stg) + YMO + 8u * (uint32_t)(warp * 32 + lane);  // two-back, vector 0
   double tt = 0.0, rr = 0.0;
   unsigned badm = 0;
   int s = 0;        // stage of the next plane to consume
@@ -296,9 +305,9 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
 #pragma unroll
       for (int q = 0; q < NO; ++q) {
         if (q == NO - 1 && NO > 1 && r >= rlim) break;
-        const double y2 = MU ? __ldg(zp.ym[q] + r) : 0.0;
+        const double y2 = MU ? lds_f64(ym0 + sc * SB + q * 2048) : 0.0;
         const double w = tm_recur<UNIT>(acc[Q0 + q], cc[Q0 + q], y2, th, ga, mu, MU);
-        SSCG_CHECK(r >= 0 && r < c.ld && (!MU || zp.ym[q] != nullptr));
+        SSCG_CHECK(r >= 0 && r < c.ld);
         zp.yo[q][r] = w;
         // exponent all ones (inf / NaN) carries into bit 31: checked once at the end
         badm |= (((unsigned)__double2hiint(w)) & 0x7ff00000u) + 0x00100000u;
@@ -513,6 +522,13 @@ int tm_make_maps(TmMaps* m, const double* Y, int64_t ld, int ncols, const double
   {
     const uint32_t box[3] = {32, 8, 1};
     int rc = encode(&m->b, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, b, dims3, str3, box);
+    if (rc) return rc;
+  }
+  {
+    const uint64_t dims[4] = {(uint64_t)o, lines, (uint64_t)planes, (uint64_t)ncols};
+    const uint64_t str[3] = {8ull * o, 8ull * S, 8ull * ld};
+    const uint32_t box[4] = {32, 8, 1, 1};
+    int rc = encode(&m->y8, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, Y, dims, str, box);
     if (rc) return rc;
   }
   {
