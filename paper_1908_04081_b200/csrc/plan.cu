@@ -88,7 +88,7 @@ struct sscg_plan {
   int hs_ss = 1;        // HSCG row sums through the superset mask
   cudaEvent_t ev_leja[SMAX] = {};
   cudaGraphExec_t gexec = nullptr;
-  int g_sigma = -1, g_full = -1, g_grid = -1;
+  int g_sigma = -1, g_full = -1, g_grid = -1, g_basis = -1;
   // census of the outer-loop graph last built: [0] ncclAllReduce calls, [1]
   // grouped halo exchanges, [2] NCCL kernel nodes, [3] kernel nodes, [4] nodes
   int census[5] = {-1, -1, -1, -1, -1};
@@ -380,14 +380,19 @@ int capture_outer(sscg_plan* p, const Ctx& c, int sigma, int full, cudaStream_t 
     // no Leja point, and point 2 (42 us) is ready long before level 2
     const bool after0 = p->leja_after0 && sigma > 1;
     if (after0) launch_level(c, 0, sigma, s);
-    cudaEventRecord(p->ev_fork, s);
-    cudaStreamWaitEvent(p->side, p->ev_fork, 0);
-    for (int n = 2; n < sigma; ++n) {
-      launch_leja_point(c, n, p->side);
-      cudaEventRecord(p->ev_leja[n], p->side);
+    // only a Newton basis has a chain (the graph is rebuilt when the basis
+    // kind changes); without one the levels follow each other directly
+    const bool chain = p->cfg.basis_kind == SSCG_BASIS_NEWTON && sigma > 2;
+    if (chain) {
+      cudaEventRecord(p->ev_fork, s);
+      cudaStreamWaitEvent(p->side, p->ev_fork, 0);
+      for (int n = 2; n < sigma; ++n) {
+        launch_leja_point(c, n, p->side);
+        cudaEventRecord(p->ev_leja[n], p->side);
+      }
     }
     for (int l = after0 ? 1 : 0; l < sigma; ++l) {
-      if (l >= 2) cudaStreamWaitEvent(s, p->ev_leja[l], 0);
+      if (chain && l >= 2) cudaStreamWaitEvent(s, p->ev_leja[l], 0);
       launch_level(c, l, sigma, s);
     }
   } else {
@@ -438,7 +443,8 @@ void graph_census(cudaGraph_t g, int* census) {
 }
 
 int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
-  if (p->gexec && p->g_sigma == sigma && p->g_full == full && p->g_grid == c.leja_grid_host)
+  if (p->gexec && p->g_sigma == sigma && p->g_full == full && p->g_grid == c.leja_grid_host &&
+      p->g_basis == p->cfg.basis_kind)
     return SSCG_OK;
   if (p->gexec) {
     cudaGraphExecDestroy(p->gexec);
@@ -447,8 +453,12 @@ int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
   cudaGraph_t g = nullptr;
   long long ar0, halo0, ar1, halo1;
   collective_counts(&ar0, &halo0);
+  // one graph = CHUNK outer loops (the host looks at `done` once per chunk, and
+  // an outer loop past the end is a no-op: K_small stops the solve on the
+  // device) -- one graph-launch boundary per CHUNK outer loops
   CUDA_OK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-  const int crc = capture_outer(p, c, sigma, full, p->stream);
+  int crc = SSCG_OK;
+  for (int u = 0; u < CHUNK && crc == SSCG_OK; ++u) crc = capture_outer(p, c, sigma, full, p->stream);
   cudaError_t e = cudaStreamEndCapture(p->stream, &g);
   if (crc != SSCG_OK) {
     if (g) cudaGraphDestroy(g);
@@ -456,15 +466,17 @@ int build_graph(sscg_plan* p, const Ctx& c, int sigma, int full) {
   }
   if (e != cudaSuccess) return sscg_fail_cuda(e, "cudaStreamEndCapture");
   collective_counts(&ar1, &halo1);
-  p->census[0] = (int)(ar1 - ar0);
-  p->census[1] = (int)(halo1 - halo0);
+  p->census[0] = (int)((ar1 - ar0) / CHUNK);  // per outer loop
+  p->census[1] = (int)((halo1 - halo0) / CHUNK);
   graph_census(g, p->census);
+  for (int k = 2; k < 5; ++k) p->census[k] /= CHUNK;
   e = cudaGraphInstantiate(&p->gexec, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return sscg_fail_cuda(e, "cudaGraphInstantiate");
   p->g_sigma = sigma;
   p->g_full = full;
   p->g_grid = c.leja_grid_host;
+  p->g_basis = p->cfg.basis_kind;
   return SSCG_OK;
 }
 
@@ -1458,13 +1470,12 @@ int sscg_run(sscg_plan* p, const sscg_config* cfg, sscg_logs* logs) {
   std::vector<ProfEv> evs;
   bool finished = false;
   while (launched < total && !finished) {
-    const int64_t m = (total - launched) < CHUNK ? (total - launched) : CHUNK;
-    for (int64_t i = 0; i < m; ++i) {
-      if (p->profiling) {
+    const int64_t m = p->profiling ? std::min<int64_t>(total - launched, CHUNK) : CHUNK;
+    if (p->profiling) {
+      for (int64_t i = 0; i < m; ++i)
         TRY(launch_outer_profiled(p, c, sigma, full, (int)(launched + i), evs));
-      } else {
-        CUDA_OK(cudaGraphLaunch(p->gexec, p->stream));
-      }
+    } else {
+      CUDA_OK(cudaGraphLaunch(p->gexec, p->stream));  // CHUNK outer loops
     }
     launched += m;
     const int slot = chunk_id & 1;
