@@ -434,7 +434,10 @@ def run_single(args):
                 "first_call_iter_per_s": total_iters / t_first,
                 "note": "adaptive_solve(problem, cfg, trace='fast') with the plan cached on the "
                         "matrix like SparseMatrix._csr; first_call_s = the first call on a fresh "
-                        "matrix: plan creation (upload + pattern compression) + the solve"},
+                        "matrix: plan creation (upload + pattern compression) + the solve",
+                "h2d_note": "h2d_bytes_per_step = the host buffers handed over (b and x0); the "
+                            "staging threads read both, and chunks that are all zero (x0 = 0: "
+                            "8 n bytes) are set on the device instead of crossing PCIe"},
         "cpu_baseline": cpu,
         "secondary": secondary,
         "gpu_launches": launches,

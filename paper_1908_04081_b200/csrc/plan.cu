@@ -1336,6 +1336,28 @@ int stage_init(sscg_plan* p) {
   return SSCG_OK;
 }
 
+// every byte of [p, p + len) zero?  (x0 = 0 is the usual start: a chunk of
+// zeros is set on the device instead of crossing the host's memory twice and
+// PCIe once; any other chunk leaves at its first nonzero word)
+bool all_zero(const char* p, size_t len) {
+  size_t i = 0;
+  for (; i < len && (reinterpret_cast<uintptr_t>(p + i) & 7); ++i)
+    if (p[i]) return false;
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(p + i);
+  const size_t nw = (len - i) / 8;
+  size_t k = 0;
+  for (; k + 64 <= nw; k += 64) {
+    uint64_t acc = 0;
+    for (int j = 0; j < 64; ++j) acc |= w[k + j];
+    if (acc) return false;
+  }
+  for (; k < nw; ++k)
+    if (w[k]) return false;
+  for (i += nw * 8; i < len; ++i)
+    if (p[i]) return false;
+  return true;
+}
+
 int staged_copy(sscg_plan* p, char* dst, const char* src, size_t bytes, bool h2d) {
   if (bytes < STAGE_MIN || atoi(env_or("SSCG_STAGE_COPY", "1")) == 0) {
     CUDA_OK(cudaStreamSynchronize(p->stream));
@@ -1359,6 +1381,11 @@ int staged_copy(sscg_plan* p, char* dst, const char* src, size_t bytes, bool h2d
       const size_t len = std::min(C, b - off);
       const int sl = k & 1;
       if (h2d) {
+        if (all_zero(src + off, len)) {
+          e = cudaMemsetAsync(dst + off, 0, len, st);
+          --k;  // no staging slot used
+          continue;
+        }
         if (k >= 2) e = cudaEventSynchronize(ev[sl]);  // chunk k-2's DMA left this slot
         if (e != cudaSuccess) break;
         std::memcpy(pin[sl], src + off, len);
