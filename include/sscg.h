@@ -202,6 +202,12 @@ int sscg_solve(sscg_plan* plan, const sscg_config* cfg, const double* b, const d
 int sscg_load(sscg_plan* plan, const double* b, const double* x0);
 int sscg_run(sscg_plan* plan, const sscg_config* cfg, sscg_logs* logs);
 int sscg_fetch(sscg_plan* plan, double* x_out, sscg_logs* logs);
+/* Page-locked host memory for result vectors: an x_out inside such a block is
+ * written by one DMA (no staging through bounce buffers).  The Python drop-in
+ * keeps a small pool of them behind the arrays adaptive_solve returns (the
+ * reference returns a fresh numpy array: adaptive.py:268). */
+int sscg_host_alloc(void** out, int64_t bytes);
+int sscg_host_free(void* p);
 /* per-kernel-class device time of the last sscg_run with profiling enabled:
  * ms[0] mpk level kernels, ms[1] gram, ms[2] small, ms[3] recovery, ms[4] other;
  * counts[] launches of each class.  enable=1 makes the next runs record one

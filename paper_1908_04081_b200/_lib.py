@@ -44,7 +44,7 @@ EXPORTS = (
     "sscg_leja_points", "sscg_params_for", "sscg_ritz_sequence", "sscg_sym_eig",
     "sscg_nccl_unique_id", "sscg_plan_create_part", "sscg_vgroup_run",
     "sscg_plan_collectives", "sscg_group_create", "sscg_group_solve", "sscg_hscg_ex",
-    "sscg_vgroup_hscg",
+    "sscg_vgroup_hscg", "sscg_host_alloc", "sscg_host_free",
 )
 HSCG_MODES = {"reference": 0, "production": 1}
 
@@ -143,6 +143,8 @@ def _declare(lib):
         "sscg_hscg_ex": (C.c_int, [vp, _DP, _DP, dbl, i64, i32, _DP, C.POINTER(SscgLogs)]),
         "sscg_vgroup_hscg": (C.c_int, [C.POINTER(vp), i32, C.POINTER(_DP), C.POINTER(_DP), dbl,
                                        i64, i32, C.POINTER(SscgLogs)]),
+        "sscg_host_alloc": (C.c_int, [C.POINTER(vp), i64]),
+        "sscg_host_free": (C.c_int, [vp]),
         "sscg_group_create": (C.c_int, [C.POINTER(vp), i32, _IP, C.POINTER(SscgPart)]),
         "sscg_group_solve": (C.c_int, [C.POINTER(vp), i32, C.POINTER(SscgConfig), C.POINTER(_DP),
                                        C.POINTER(_DP), C.POINTER(_DP),
@@ -169,6 +171,79 @@ def load(path=LIB_PATH):
                 raise RuntimeError("libsscg ABI version mismatch")
             _lib = lib
     return _lib
+
+
+class _PinnedBlock:
+    """One page-locked host block behind a result vector; back to the pool when
+    the last array viewing it is gone."""
+
+    def __init__(self, pool, ptr, nbytes):
+        self._pool, self.ptr, self.nbytes = pool, ptr, nbytes
+        self.__array_interface__ = {"shape": (nbytes // 8,), "typestr": "<f8",
+                                    "data": (ptr, False), "version": 3}
+
+    def __del__(self):
+        pool = self._pool
+        if pool is not None:
+            pool._give_back(self.ptr, self.nbytes)
+
+
+class PinnedPool:
+    """Result vectors in page-locked host memory (sscg_host_alloc): the solve's
+    device-to-host copy of x is then one DMA instead of a staged copy into a
+    freshly faulted-in numpy array.  Blocks return to the pool when the arrays
+    handed out are garbage collected; at most `max_bytes` are ever pinned --
+    past that (or for small vectors) callers get a plain numpy array."""
+
+    def __init__(self, min_bytes=16 << 20, max_bytes=1 << 30):
+        self.min_bytes, self.max_bytes = min_bytes, max_bytes
+        self._free = {}  # nbytes -> [ptr]
+        self._pinned = 0
+        self._mu = threading.Lock()
+
+    def vector(self, n):
+        nbytes = 8 * int(n)
+        if nbytes < self.min_bytes:
+            return np.empty(n)
+        with self._mu:
+            lst = self._free.get(nbytes)
+            ptr = lst.pop() if lst else None
+            if ptr is None:
+                if self._pinned + nbytes > self.max_bytes:
+                    self._trim_locked()
+                if self._pinned + nbytes > self.max_bytes:
+                    return np.empty(n)
+                out = C.c_void_p()
+                if load().sscg_host_alloc(C.byref(out), nbytes) != OK or not out.value:
+                    return np.empty(n)
+                ptr = out.value
+                self._pinned += nbytes
+                # the first block of a size brings a spare: `x, tr, co = solve(...)`
+                # in a loop holds the last x while the next solve fills another
+                # block, and page-locking costs ~0.2 ms per MB -- not inside a solve
+                if lst is None and self._pinned + nbytes <= self.max_bytes:
+                    spare = C.c_void_p()
+                    if load().sscg_host_alloc(C.byref(spare), nbytes) == OK and spare.value:
+                        self._free.setdefault(nbytes, []).append(spare.value)
+                        self._pinned += nbytes
+        return np.asarray(_PinnedBlock(self, ptr, nbytes))
+
+    def _give_back(self, ptr, nbytes):
+        try:
+            with self._mu:
+                self._free.setdefault(nbytes, []).append(ptr)
+        except Exception:  # interpreter shutdown
+            pass
+
+    def _trim_locked(self):
+        lib = load()
+        for nbytes, lst in self._free.items():
+            while lst:
+                lib.sscg_host_free(lst.pop())
+                self._pinned -= nbytes
+
+
+result_pool = PinnedPool()
 
 
 def check(rc):

@@ -219,7 +219,7 @@ def adaptive_solve(problem, cfg, *, trace=None, device=0, devices=None, info=Non
     if b.shape != (a.n,) or x0.shape != (a.n,):
         raise ValueError("b / x0 do not match the matrix dimension")
     logs = LogBuffers(cfg)
-    x = np.empty(a.n)
+    x = L.result_pool.vector(a.n)  # page-locked for large n: one DMA brings x back
     L.check(L.load().sscg_solve(plan.handle, ccfg, L.dptr(b), L.dptr(x0), L.dptr(x), logs.s))
     tr, co = build_trace(cfg, logs, trace)
     tr.check_consistency()

@@ -82,7 +82,7 @@ def hscg_solve(problem, eps_star, max_iters=None, *, device=0, mode="reference",
         raise ValueError("b / x0 do not match the matrix dimension")
     plan = _plan(a, device)
     iters, logs = hscg_logs(max_iters)
-    x = np.empty(a.n)
+    x = L.result_pool.vector(a.n)
     L.check(L.load().sscg_hscg_ex(plan.handle, L.dptr(b), L.dptr(x0), float(eps_star),
                                   int(max_iters), L.HSCG_MODES[mode], L.dptr(x), logs))
     tr, co = hscg_trace(iters, logs)

@@ -1364,6 +1364,16 @@ int staged_copy(sscg_plan* p, char* dst, const char* src, size_t bytes, bool h2d
     CUDA_OK(cudaMemcpy(dst, src, bytes, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost));
     return SSCG_OK;
   }
+  {  // a page-locked host side (sscg_host_alloc) takes one DMA, no staging
+    cudaPointerAttributes at;
+    const void* host = h2d ? (const void*)src : (const void*)dst;
+    if (cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost) {
+      CUDA_OK(cudaStreamSynchronize(p->stream));
+      CUDA_OK(cudaMemcpy(dst, src, bytes, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost));
+      return SSCG_OK;
+    }
+    cudaGetLastError();  // an unregistered pointer may report an error on older drivers
+  }
   TRY(stage_init(p));
   CUDA_OK(cudaStreamSynchronize(p->stream));  // device buffers free / results complete
   const int T = p->st_threads;
@@ -1588,6 +1598,22 @@ int sscg_fetch(sscg_plan* p, double* x_out, sscg_logs* logs) {
     const int d = 2 * p->cfg.s_bar0 + 1;
     CUDA_OK(cudaMemcpy(logs->first_gram, p->d_fg, sizeof(double) * d * d, cudaMemcpyDeviceToHost));
   }
+  return SSCG_OK;
+}
+
+int sscg_host_alloc(void** out, int64_t bytes) {
+  if (!out || bytes < 1) return sscg_fail(SSCG_EINVAL, "bad host allocation request");
+  *out = nullptr;
+  cudaError_t e = cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return sscg_fail(SSCG_ENOMEM, "cudaHostAlloc(%lld bytes): %s", (long long)bytes, cudaGetErrorString(e));
+  }
+  return SSCG_OK;
+}
+int sscg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+  cudaGetLastError();
   return SSCG_OK;
 }
 

@@ -66,7 +66,7 @@ def sstep_solve(problem, s, eps_star, max_outer=None, params=None, basis_kind="m
         raise ValueError("b / x0 do not match the matrix dimension")
     shape = SimpleNamespace(sigma=s, s_bar0=s, max_outer=clamp_i32(max_outer))
     logs = LogBuffers(shape)
-    x = np.empty(a.n)
+    x = L.result_pool.vector(a.n)
     if params is not None:
         th, ga = L.f64(params.thetas), L.f64(params.gammas)
         mu = L.f64(params.mus) if len(params.mus) else np.zeros(1)

@@ -189,28 +189,52 @@ def test_value_stream_bit_identical_to_csr(gpu_ready, key, kw):
 
 def test_staged_host_copies_round_trip(gpu_ready):
     """Vectors of >= 16 MB move through the per-thread pinned chunk pipelines
-    (plan.cu staged_copy); the solve must be bit-identical to plain
-    cudaMemcpy transfers (SSCG_STAGE_COPY=0)."""
+    (plan.cu staged_copy; all-zero chunks of an upload are set on the device),
+    and x comes back into a page-locked block of the result pool by one DMA;
+    every combination must be bit-identical to plain cudaMemcpy transfers
+    (SSCG_STAGE_COPY=0) into a plain numpy array."""
+    import gc
+    from paper_1908_04081_b200 import _lib as L
     kw = dict(sigma=12, eps_star=1e-10, basis_kind="newton", max_outer=3)
 
-    def run(env):
+    def run(env, pool):
         old = os.environ.get("SSCG_STAGE_COPY")
+        old_pool = L.result_pool
         os.environ["SSCG_STAGE_COPY"] = env
+        L.result_pool = pool
         try:
             prob = problems.make_problem("c5", scale=136)  # 2.5 M rows: 20 MB vectors
-            prob.x0[:] = np.linspace(-1e-3, 1e-3, prob.a.n)  # a non-trivial x0 upload
+            n = prob.a.n
+            prob.x0[n // 2:] = np.linspace(-1e-3, 1e-3, n - n // 2)  # zero chunks, then data
             return adaptive_solve(prob, AdaptiveConfig(**kw), trace="fast")
         finally:
+            L.result_pool = old_pool
             if old is None:
                 os.environ.pop("SSCG_STAGE_COPY", None)
             else:
                 os.environ["SSCG_STAGE_COPY"] = old
 
-    ref = run("0")
-    got = run("1")
-    assert ref[0].nbytes >= 16 << 20
-    np.testing.assert_array_equal(got[0], ref[0])
-    np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
+    plain = L.PinnedPool(max_bytes=0)  # hands out numpy arrays only
+    ref = run("0", plain)
+    assert ref[0].nbytes >= 16 << 20 and ref[0].base is None
+    staged = run("1", plain)           # staged both ways
+    pool = L.PinnedPool()
+    pinned = run("1", pool)            # staged upload, x by one DMA into the pool's block
+    assert pinned[0].base is not None and pool._pinned == 2 * pinned[0].nbytes  # + the spare
+    for got in (staged, pinned):
+        np.testing.assert_array_equal(got[0], ref[0])
+        np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
+    # the block returns to the pool only when the last view of x is gone
+    del got
+    ptr = pinned[0].ctypes.data
+    view = pinned[0][5:10]
+    nb = pinned[0].nbytes
+    pinned = None
+    gc.collect()
+    assert pool._free[nb] and ptr not in pool._free[nb]  # only the spare is free
+    view = None
+    gc.collect()
+    assert ptr in pool._free[nb] and pool._pinned == 2 * nb
 
 
 @pytest.mark.parametrize("shape", [(17, 16, 5), (40, 9, 13), (33, 33, 3), (256, 1, 6),
