@@ -10,11 +10,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -602,6 +604,7 @@ namespace {
 // owned, n_local rows (>= n_rows) is the vector length; lvl[d] = rows with
 // ghost depth <= d (d = 0..depth)
 const char* env_or(const char* name, const char* dflt);
+int copy_h2d(sscg_plan* p, void* d, const void* h, size_t bytes);
 int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64_t n_local,
               int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx, const double* values,
               const int64_t* lvl, int depth) {
@@ -637,9 +640,13 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   CUDA_OK(cudaMemset(p->d_rp, 0, sizeof(int) * (n_rows + 1 + 8)));
   TRY(dalloc(p, &p->d_col, nnz + 4));
   TRY(dalloc(p, &p->d_val, nnz + 2));
-  CUDA_OK(cudaMemcpy(p->d_rp, rp32.data(), sizeof(int) * (n_rows + 1), cudaMemcpyHostToDevice));
-  if (nnz) CUDA_OK(cudaMemcpy(p->d_col, col_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice));
-  if (nnz) CUDA_OK(cudaMemcpy(p->d_val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  // the CSR arrays go up through the staged chunk pipelines (pageable host
+  // memory: a plain cudaMemcpy of c5w's 1.4 GB takes ~0.4 s)
+  CUDA_OK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  CUDA_OK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+  TRY(copy_h2d(p, p->d_rp, rp32.data(), sizeof(int) * (size_t)(n_rows + 1)));
+  if (nnz) TRY(copy_h2d(p, p->d_col, col_idx, sizeof(int) * (size_t)nnz));
+  if (nnz) TRY(copy_h2d(p, p->d_val, values, sizeof(double) * (size_t)nnz));
   for (double** v : {&p->d_x, &p->d_b, &p->d_x0, &p->d_xj, &p->d_rj}) {
     TRY(dalloc(p, v, p->ld));
     CUDA_OK(cudaMemset(*v, 0, sizeof(double) * p->ld));
@@ -653,8 +660,6 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   TRY(dalloc(p, &p->d_fg, CMAX * CMAX));
   TRY(dalloc(p, &p->d_red, GPACK + 2));
   CUDA_OK(cudaMemset(p->d_st, 0, sizeof(SolverState)));
-  CUDA_OK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-  CUDA_OK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
   CUDA_OK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
   for (int i = 0; i < SMAX; ++i) CUDA_OK(cudaEventCreateWithFlags(&p->ev_leja[i], cudaEventDisableTiming));
   CUDA_OK(cudaHostAlloc((void**)&p->h_done, 2 * sizeof(int), cudaHostAllocDefault));
@@ -721,56 +726,117 @@ constexpr int PAT_MAX_BYTES = 16 * 1024;
 // grows[row] (the slab's rows are translates in the GLOBAL grid even where the
 // local ordering -- owned rows, then ghost planes by depth -- is not).  false
 // when the table outgrows shared memory.
+// Pattern table of the rows [r0, r1): ids local to this table, in order of
+// first appearance.  ids32 receives one id per row (index i - r0).
+struct PatTable {
+  std::vector<int> ptr{0}, off;
+  std::vector<double> val;
+  std::unordered_map<uint64_t, std::vector<int>> buckets;
+  bool ok = true;
+  // id of the pattern (offsets o[0..m), values v[0..m)), added if new; -1: table full
+  int find_or_add(const int64_t* o, const double* v, int m) {
+    uint64_t h = 1469598103934665603ull ^ (uint64_t)m;
+    for (int j = 0; j < m; ++j) {
+      uint64_t vb;
+      std::memcpy(&vb, &v[j], 8);
+      h = (h ^ (uint64_t)o[j]) * 1099511628211ull;
+      h = (h ^ vb) * 1099511628211ull;
+    }
+    auto& cand = buckets[h];
+    for (int q : cand) {
+      const int pb = ptr[(size_t)q], pe = ptr[(size_t)q + 1];
+      if (pe - pb != m) continue;
+      bool same = true;
+      for (int j = 0; j < m && same; ++j)
+        same = off[(size_t)(pb + j)] == o[j] && std::memcmp(&val[(size_t)(pb + j)], &v[j], 8) == 0;
+      if (same) return q;
+    }
+    const int id = (int)ptr.size() - 1;
+    const size_t ne = off.size() + (size_t)m;
+    if (id >= 65535 || ne * 12 + (ptr.size() + 1) * 4 > (size_t)PAT_MAX_BYTES) return -1;
+    for (int j = 0; j < m; ++j) {
+      if (o[j] != (int64_t)(int)o[j]) return -1;
+      off.push_back((int)o[j]);
+      val.push_back(v[j]);
+    }
+    ptr.push_back((int)off.size());
+    cand.push_back(id);
+    return id;
+  }
+};
+
+// Rows that are translates of each other (same offsets, values, stored order)
+// share a pattern; ids in order of first appearance.  The scan runs on several
+// host threads over contiguous row ranges, each with its own table; the tables
+// are merged in range order, which keeps first-appearance order (a 256^3
+// operator: 1.7 s of plan creation on one thread).
 bool build_patterns(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
                     const double* values, const int64_t* grows, std::vector<int>& ptr,
                     std::vector<int>& off, std::vector<double>& val, std::vector<uint16_t>& ids) {
-  std::unordered_map<uint64_t, std::vector<int>> buckets;
-  ptr.assign(1, 0);
-  off.clear();
-  val.clear();
   ids.assign((size_t)n_rows, 0);
-  auto ofs = [&](int64_t i, int64_t j) -> int64_t {
-    return grows ? grows[col_idx[j]] - grows[i] : (int64_t)col_idx[j] - i;
+  int T = atoi(env_or("SSCG_SETUP_THREADS", "0"));
+  if (T <= 0) T = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+  T = (int)std::max<int64_t>(1, std::min<int64_t>(T, n_rows / 65536));
+  std::vector<PatTable> tabs((size_t)T);
+  std::vector<std::vector<uint16_t>> lid((size_t)T);
+  std::atomic<bool> fail{false};
+  auto scan = [&](int t) {
+    const int64_t r0 = n_rows * t / T, r1 = n_rows * (t + 1) / T;
+    PatTable& tb = tabs[(size_t)t];
+    std::vector<uint16_t>& li = lid[(size_t)t];
+    li.resize((size_t)(r1 - r0));
+    std::vector<int64_t> o;
+    for (int64_t i = r0; i < r1; ++i) {
+      if ((i & 4095) == 0 && fail.load(std::memory_order_relaxed)) return;
+      const int64_t b = row_ptr[i], e = row_ptr[i + 1];
+      o.resize((size_t)(e - b));
+      for (int64_t j = b; j < e; ++j)
+        o[(size_t)(j - b)] = grows ? grows[col_idx[j]] - grows[i] : (int64_t)col_idx[j] - i;
+      const int id = tb.find_or_add(o.data(), values + b, (int)(e - b));
+      if (id < 0) {
+        tb.ok = false;
+        fail.store(true, std::memory_order_relaxed);
+        return;
+      }
+      li[(size_t)(i - r0)] = (uint16_t)id;
+    }
   };
-  for (int64_t i = 0; i < n_rows; ++i) {
-    const int64_t b = row_ptr[i], e = row_ptr[i + 1];
-    uint64_t h = 1469598103934665603ull ^ (uint64_t)(e - b);
-    for (int64_t j = b; j < e; ++j) {
-      uint64_t vb;
-      std::memcpy(&vb, &values[j], 8);
-      h = (h ^ (uint64_t)ofs(i, j)) * 1099511628211ull;
-      h = (h ^ vb) * 1099511628211ull;
-    }
-    int id = -1;
-    auto& cand = buckets[h];
-    for (int q : cand) {
-      const int pb = ptr[q], pe = ptr[q + 1];
-      if (pe - pb != e - b) continue;
-      bool same = true;
-      for (int64_t j = b; j < e && same; ++j) {
-        const int k = pb + (int)(j - b);
-        same = off[k] == ofs(i, j) && std::memcmp(&val[k], &values[j], 8) == 0;
-      }
-      if (same) {
-        id = q;
-        break;
-      }
-    }
-    if (id < 0) {
-      id = (int)ptr.size() - 1;
-      const size_t ne = off.size() + (size_t)(e - b);
-      if (id >= 65535 || ne * 12 + (ptr.size() + 1) * 4 > (size_t)PAT_MAX_BYTES) return false;
-      for (int64_t j = b; j < e; ++j) {
-        const int64_t o = ofs(i, j);
-        if (o != (int64_t)(int)o) return false;
-        off.push_back((int)o);
-        val.push_back(values[j]);
-      }
-      ptr.push_back((int)off.size());
-      cand.push_back(id);
-    }
-    ids[(size_t)i] = (uint16_t)id;
+  {
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(scan, t);
+    scan(0);
+    for (auto& x : th) x.join();
   }
+  if (fail.load()) return false;
+  // merge in range order
+  PatTable g;
+  std::vector<std::vector<uint16_t>> remap((size_t)T);
+  std::vector<int64_t> o;
+  for (int t = 0; t < T; ++t) {
+    const PatTable& tb = tabs[(size_t)t];
+    const int np = (int)tb.ptr.size() - 1;
+    remap[(size_t)t].resize((size_t)np);
+    for (int q = 0; q < np; ++q) {
+      const int pb = tb.ptr[(size_t)q], m = tb.ptr[(size_t)q + 1] - pb;
+      o.assign(tb.off.begin() + pb, tb.off.begin() + pb + m);
+      const int id = g.find_or_add(o.data(), tb.val.data() + pb, m);
+      if (id < 0) return false;
+      remap[(size_t)t][(size_t)q] = (uint16_t)id;
+    }
+  }
+  auto apply = [&](int t) {
+    const int64_t r0 = n_rows * t / T, r1 = n_rows * (t + 1) / T;
+    for (int64_t i = r0; i < r1; ++i) ids[(size_t)i] = remap[(size_t)t][lid[(size_t)t][(size_t)(i - r0)]];
+  };
+  {
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(apply, t);
+    apply(0);
+    for (auto& x : th) x.join();
+  }
+  ptr.swap(g.ptr);
+  off.swap(g.off);
+  val.swap(g.val);
   return true;
 }
 
@@ -1020,20 +1086,55 @@ int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col
   auto ofs = [&](int64_t i, int64_t j) -> int64_t {
     return grows ? grows[col_idx[j]] - grows[i] : (int64_t)col_idx[j] - i;
   };
+  // the union of offsets, scanned on several host threads over contiguous row
+  // ranges (c4: 189 M nonzeros), each with its own sorted set
+  int T = atoi(env_or("SSCG_SETUP_THREADS", "0"));
+  if (T <= 0) T = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+  T = (int)std::max<int64_t>(1, std::min<int64_t>(T, n / 65536));
+  auto on_ranges = [&](auto&& fn) {
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(fn, t);
+    fn(0);
+    for (auto& x : th) x.join();
+  };
+  std::vector<std::vector<int64_t>> unis((size_t)T);
+  std::atomic<bool> bad{false};
+  on_ranges([&](int t) {
+    std::vector<int64_t>& u = unis[(size_t)t];
+    int64_t last = INT64_MIN;  // most rows repeat the previous offset set: skip the search
+    for (int64_t i = n * t / T; i < n * (t + 1) / T; ++i) {
+      if ((i & 4095) == 0 && bad.load(std::memory_order_relaxed)) return;
+      int64_t prev = INT64_MIN;
+      for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; ++j) {
+        const int64_t o = ofs(i, j);
+        if (o <= prev) {  // unsorted row
+          bad.store(true, std::memory_order_relaxed);
+          return;
+        }
+        prev = o;
+        if (o == last) continue;
+        last = o;
+        auto it = std::lower_bound(u.begin(), u.end(), o);
+        if (it == u.end() || *it != o) {
+          if ((int)u.size() >= VS_MAX_NE) {
+            bad.store(true, std::memory_order_relaxed);
+            return;
+          }
+          u.insert(it, o);
+        }
+      }
+    }
+  });
+  if (bad.load()) return SSCG_OK;
   std::vector<int64_t> uni;
-  for (int64_t i = 0; i < n; ++i) {
-    int64_t prev = INT64_MIN;
-    for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; ++j) {
-      const int64_t o = ofs(i, j);
-      if (o <= prev) return SSCG_OK;  // unsorted row
-      prev = o;
+  for (const auto& u : unis)
+    for (int64_t o : u) {
       auto it = std::lower_bound(uni.begin(), uni.end(), o);
       if (it == uni.end() || *it != o) {
         if ((int)uni.size() >= VS_MAX_NE) return SSCG_OK;
         uni.insert(it, o);
       }
     }
-  }
   const int ne = (int)uni.size();
   int occ[2] = {0, 0};
   if (ne < 3 || vs_ctas_per_sm(ne, grows != nullptr, occ) < 1) return SSCG_OK;
@@ -1069,25 +1170,31 @@ int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col
     }
   }
   // the kernels unroll over a bucket of slots (9 / 18 / 27 / 32): slots past the
-  // union exist and hold 0.0
+  // union exist and hold 0.0.  Each thread zeroes and fills its own row range.
   const int nb = ne <= 9 ? 9 : ne <= 18 ? 18 : ne <= 27 ? 27 : 32;
-  std::vector<double> sv((size_t)nb * (size_t)p->ld, 0.0);
-  for (int64_t i = 0; i < n; ++i) {
-    int k = 0;
-    for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; ++j) {
-      const int64_t o = ofs(i, j);
-      while (uni[(size_t)k] != o) ++k;  // rows are sorted subsequences of uni
-      sv[(size_t)k * (size_t)p->ld + (size_t)i] = values[j];
+  const size_t sv_len = (size_t)nb * (size_t)p->ld;
+  std::unique_ptr<double[]> sv(new double[sv_len]);
+  on_ranges([&](int t) {
+    const int64_t r0 = (int64_t)p->ld * t / T, r1 = (int64_t)p->ld * (t + 1) / T;  // incl. padding rows
+    for (int k = 0; k < nb; ++k)
+      std::memset(sv.get() + (size_t)k * (size_t)p->ld + (size_t)r0, 0, sizeof(double) * (size_t)(r1 - r0));
+    for (int64_t i = std::min<int64_t>(r0, n); i < std::min<int64_t>(r1, n); ++i) {
+      int k = 0;
+      for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; ++j) {
+        const int64_t o = ofs(i, j);
+        while (uni[(size_t)k] != o) ++k;  // rows are sorted subsequences of uni
+        sv[(size_t)k * (size_t)p->ld + (size_t)i] = values[j];
+      }
     }
-  }
+  });
   if (grows) {
     TRY(dalloc(p, &p->d_vs_geo, geo.size()));
     TRY(dalloc(p, &p->d_vs_base, base.size()));
     CUDA_OK(cudaMemcpy(p->d_vs_geo, geo.data(), 4 * geo.size(), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(p->d_vs_base, base.data(), 4 * base.size(), cudaMemcpyHostToDevice));
   }
-  TRY(dalloc(p, &p->d_vs_val, sv.size()));
-  CUDA_OK(cudaMemcpy(p->d_vs_val, sv.data(), 8 * sv.size(), cudaMemcpyHostToDevice));
+  TRY(dalloc(p, &p->d_vs_val, sv_len));
+  TRY(copy_h2d(p, p->d_vs_val, sv.get(), 8 * sv_len));
   p->vs_ne = ne;
   for (int k = 0; k < VS_MAX_NE; ++k) p->vs_off[k] = k < ne ? (int)uni[(size_t)k] : 0;  // (plain form)
   int sms = NUM_SMS;
@@ -1128,10 +1235,21 @@ int sscg_plan_create(sscg_plan** out, int32_t device, int64_t n, int64_t nnz,
     if (n < 1) return sscg_fail(SSCG_EINVAL, "n must be >= 1");
     int64_t lvl[SMAX + 1];
     for (int d = 0; d <= SMAX; ++d) lvl[d] = n;
+    // SSCG_SETUP_TIMING=1: where plan creation spends its time (stderr)
+    const bool timing = atoi(env_or("SSCG_SETUP_TIMING", "0")) != 0;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
     TRY(plan_init(p, device, n, n, n, nnz, row_ptr, col_idx, values, lvl, SMAX));
+    const auto t1 = now();
     TRY(pattern_setup(p, n, row_ptr, col_idx, values));
-    if (p->d_pid) return SSCG_OK;  // the pattern kernels replace the CSR staging
-    return vs_setup(p, n, row_ptr, col_idx, values);
+    const auto t2 = now();
+    int rc = SSCG_OK;
+    if (!p->d_pid) rc = vs_setup(p, n, row_ptr, col_idx, values);  // else the pattern kernels replace the CSR staging
+    if (timing)
+      fprintf(stderr, "[sscg] plan_create n=%lld nnz=%lld: init+upload %.1f ms, patterns %.1f ms, value stream %.1f ms\n",
+              (long long)n, (long long)nnz, ms(t0, t1), ms(t1, t2), ms(t2, now()));
+    return rc;
   });
 }
 
