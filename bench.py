@@ -274,7 +274,7 @@ def traffic_for(config, kname):
         return None
 
 
-def single_plan_line(prob, cfg_kw, steps, warmup, env=None, label=None):
+def single_plan_line(prob, cfg_kw, steps, warmup, env=None, label=None, traffic_config=None):
     """Device-time solves of one problem on a single-GPU plan (optionally under
     an environment override, e.g. SSCG_PATTERN=0 for the CSR kernels)."""
     from paper_1908_04081_b200 import AdaptiveConfig, _lib as L
@@ -311,7 +311,9 @@ def single_plan_line(prob, cfg_kw, steps, warmup, env=None, label=None):
     line = {"workload": label, "value": tot / (dev / 1e3), "unit": "iter/s", "ms_per_step": dev,
             "steps": steps, "syncs_to_tol": outer, "total_iters": tot,
             "converged": int(logs.s.status) == L.CONVERGED, "plan_create_s": round(t_plan, 2),
-            "roofline": roofline(n, nnz, cfg.sigma, cfg.basis_kind, sched, pms, pcnt, outer + 1)}
+            "roofline": roofline(n, nnz, cfg.sigma, cfg.basis_kind, sched, pms, pcnt, outer + 1,
+                                 traffic_for(traffic_config, kernel_name(sched))
+                                 if traffic_config else None)}
     plan.close()
     return line
 
@@ -406,12 +408,14 @@ def run_single(args):
         # the general CSR kernels on the same operator (no pattern compression)
         secondary.append(single_plan_line(
             prob, cfg_kw, min(args.steps, 3), 1, env={"SSCG_PATTERN": "0"},
-            label="c5w through the general CSR kernels (SSCG_PATTERN=0): " + desc))
+            label="c5w through the general CSR kernels (SSCG_PATTERN=0): " + desc,
+            traffic_config=None if args.scale else "c5w"))
         # the value-stream kernels on c4j (27-point, row-varying values)
         _, s4, b4, e4, _, d4 = CONFIGS["c4j"]
         p4 = problems.make_problem("c4j", scale=args.scale and max(16, args.scale * 3 // 4))
         secondary.append(single_plan_line(p4, dict(sigma=s4, eps_star=e4, basis_kind=b4),
-                                          min(args.steps, 3), 1, label=d4))
+                                          min(args.steps, 3), 1, label=d4,
+                                          traffic_config=None if args.scale else "c4j"))
         del p4
 
     line = {

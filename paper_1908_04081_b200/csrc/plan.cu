@@ -644,6 +644,9 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   // memory: a plain cudaMemcpy of c5w's 1.4 GB takes ~0.4 s)
   CUDA_OK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   CUDA_OK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+  // (the pipelines' streams do not order after the cudaMemset calls above,
+  // which run on the legacy stream and may still be in flight)
+  CUDA_OK(cudaDeviceSynchronize());
   TRY(copy_h2d(p, p->d_rp, rp32.data(), sizeof(int) * (size_t)(n_rows + 1)));
   if (nnz) TRY(copy_h2d(p, p->d_col, col_idx, sizeof(int) * (size_t)nnz));
   if (nnz) TRY(copy_h2d(p, p->d_val, values, sizeof(double) * (size_t)nnz));
@@ -1495,7 +1498,7 @@ int staged_copy(sscg_plan* p, char* dst, const char* src, size_t bytes, bool h2d
   TRY(stage_init(p));
   CUDA_OK(cudaStreamSynchronize(p->stream));  // device buffers free / results complete
   const int T = p->st_threads;
-  const size_t C = p->st_chunk, per = (bytes / T + 4095) & ~(size_t)4095;
+  const size_t C = p->st_chunk, per = ((bytes + T - 1) / T + 4095) & ~(size_t)4095;  // T * per >= bytes
   std::vector<cudaError_t> err((size_t)T, cudaSuccess);
   auto work = [&](int t) {
     cudaError_t e = cudaSetDevice(p->device);

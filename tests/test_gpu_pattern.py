@@ -237,6 +237,35 @@ def test_staged_host_copies_round_trip(gpu_ready):
     assert ptr in pool._free[nb] and pool._pinned == 2 * nb
 
 
+def test_staged_upload_covers_every_byte(gpu_ready):
+    """The CSR arrays of a plan go up through the staged chunk pipelines, one
+    contiguous range per copy thread.  4 (n + 1) bytes of row_ptr with n a
+    multiple of 8 * 4096 / 4 is the size whose last word falls off a partition
+    rounded down: the last row would end at 0 (found by bench.py's CSR line on
+    c5w).  A bidiagonal operator of 2^22 rows: y = A x must be right at the
+    last row."""
+    from paper_1908_04081_b200.kernels import spmv
+    n = 1 << 22
+    row_ptr = np.concatenate([[0], np.cumsum(np.r_[1, np.full(n - 1, 2)])]).astype(np.int64)
+    col = np.empty(2 * n - 1, dtype=np.int64)
+    col[0] = 0
+    col[1::2] = np.arange(n - 1)
+    col[2::2] = np.arange(1, n)
+    val = np.empty(2 * n - 1)
+    val[0] = 2.0
+    val[1::2] = -0.5
+    val[2::2] = 2.0
+    a = SparseMatrix(n=n, row_ptr=row_ptr, col_idx=col, values=val, n_a=2, is_symmetric=False)
+    assert 4 * (n + 1) >= 16 << 20  # staged
+    x = np.linspace(1.0, 2.0, n)
+    y = spmv(a, x)
+    ref = 2.0 * x
+    ref[1:] += -0.5 * x[:-1]
+    np.testing.assert_array_equal(y[-4:], ref[-4:])
+    np.testing.assert_array_equal(y[:4], ref[:4])
+    assert np.array_equal(y, ref)
+
+
 @pytest.mark.parametrize("shape", [(17, 16, 5), (40, 9, 13), (33, 33, 3), (256, 1, 6),
                                    (64, 8, 2), (32, 16, 40), (96, 24, 7)],
                          ids=lambda s: "x".join(map(str, s)))
