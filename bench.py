@@ -539,7 +539,7 @@ def run_partitioned(args, rank, world):
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     # end to end through the C ABI with host buffers, max over ranks
     b_loc, x0_loc = info["b"], info["x0"]
-    x_host = np.empty(hi - lo)
+    x_host = L.result_pool.vector(hi - lo)  # page-locked (sscg_host_alloc): x back by one DMA
     e2e = []
     for _ in range(max(1, min(args.steps, 3))):
         dist.barrier()
