@@ -60,7 +60,8 @@ __host__ __device__ constexpr uint32_t tm_tx_bytes(int nv, bool l0, bool mu) {
   return (uint32_t)(nv * TM_BOX * 8 + (l0 ? 2048 : mu ? nv * 2048 : 0) + 256);
 }
 __host__ __device__ inline size_t tm_head_bytes(int pat_np, int zm_np, bool table) {
-  const size_t a = (size_t)pat_np * SS_MAX_NE * 8 + (table ? 4 * (size_t)zm_np : 0);
+  // pattern values, then (plane-table plans) each plane's first local row and its plane index
+  const size_t a = (size_t)pat_np * SS_MAX_NE * 8 + (table ? 8 * (size_t)zm_np : 0);
   return (a + 127) / 128 * 128;
 }
 
@@ -139,6 +140,7 @@ struct TmShared {
   uint64_t* full;
   uint64_t* empty;
   int* sitem;
+  int* sbase;  // with sitem: the largest plane base of the item's planes (plane-table plans)
   double (*red)[8];
   const double* pval;
   const int* ptab;
@@ -207,10 +209,17 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
         const int s = k % RING;
         if (k >= RING) mbar_wait(&empty[s], ((k / RING) - 1) & 1);
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        if (zz == z0 - 1) sh.sitem[s] = it;
+        if (zz == z0 - 1) {
+          sh.sitem[s] = it;
+          if (table) {  // one thread looks the item's planes up for all 256 consumers
+            int mb = 0;
+            for (int z = z0; z < z1; ++z) mb = max(mb, sh.ptab[z]);
+            sh.sbase[s] = mb;
+          }
+        }
         // plane coordinate: geometric plane -> local block (plane table) or
         // itself; outside the walk -1 (zero fill)
-        const int pz = (zz >= 0 && zz < np) ? (table ? sh.ptab[zz] / S : zz) : -1;
+        const int pz = (zz >= 0 && zz < np) ? (table ? sh.ptab[np + zz] : zz) : -1;
         SSCG_CHECK(pz >= -1 && pz < np + (table ? 64 : 1));
         unsigned char* dst = stg + (size_t)s * SB;
         mbar_arrive_tx(&full[s], tm_tx_bytes(NV, L0, MU));
@@ -270,13 +279,18 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
   // arrivals per phase: no warp-level sync on the per-plane path).  CHECK:
   // the item may hold rows outside this level's range (tile past the last
   // line, ghost depth beyond the level) -- else every row computes.
+  // rb: first local row of plane z, carried from step to step -- the plane
+  // table (partitioned plans) is read one plane ahead, beside the row's work,
+  // not between the stage wait and the first store address
+  int rb = 0;
   auto step = [&](auto check, double (&p)[NV], double (&cc)[NV], double (&nn)[NV], int z,
                   int rel, int& sc) {
     constexpr bool CHECK = decltype(check)::value;
     tm_wait(full0 + 8u * s, ph);
 #pragma unroll
     for (int q = 0; q < NV; ++q) nn[q] = lds_f64(my0 + s * SB + q * TM_BOXB);
-    const int r = (table ? sh.ptab[z] : z * S) + rel;
+    const int r = rb + rel;
+    rb = table ? sh.ptab[min(z + 1, np - 1)] : rb + S;
     if (!CHECK || r < plim) {
       const uint32_t cur = my0 + sc * SB;  // this plane's centre
       const uint32_t pid = lds_u8(id0 + sc * SB);
@@ -327,14 +341,10 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
     const int x0 = (cb % ntx) * 32, y0 = (cb / ntx) * 8;
     const int line = y0 + warp;
     const int rel = line * o + x0 + lane;  // row within its plane
+    rb = table ? sh.ptab[z0] : z0 * S;
     // rows of this item: all below plim unless the tile passes the last line
     // or a plane lies at a ghost depth this level does not compute
-    bool all_in = line < lines;
-    if (table) {
-      for (int z = z0; z < z1 && all_in; ++z) all_in = sh.ptab[z] + rel < plim;
-    } else {
-      all_in = all_in && (z1 - 1) * S + rel < plim;
-    }
+    const bool all_in = line < lines && (table ? sh.sbase[s] : (z1 - 1) * S) + rel < plim;
     const bool live = line < lines;
     double pv[NV], cu[NV], nx[NV];
 #pragma unroll
@@ -400,15 +410,19 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB)
   extern __shared__ __align__(128) unsigned char tsm[];
   constexpr int RING = Ring<L0>::R;
   __shared__ __align__(8) uint64_t full[RING], empty[RING];
-  __shared__ int sitem[RING];
+  __shared__ int sitem[RING], sbase[RING];
   __shared__ double red[2][8];
   const int tid = threadIdx.x;
   const bool table = c.zm_base != nullptr;
   double* pval = reinterpret_cast<double*>(tsm);
   int* ptab = reinterpret_cast<int*>(tsm + (size_t)c.pat_np * SS_MAX_NE * 8);
   for (int j = tid; j < c.pat_np * SS_MAX_NE; j += blockDim.x) pval[j] = __ldg(c.ss_val + j);
-  if (table)
-    for (int j = tid; j < c.zm_np; j += blockDim.x) ptab[j] = __ldg(c.zm_base + j);
+  if (table)  // row base and plane index (the producer's TMA coordinate: no division per stage)
+    for (int j = tid; j < c.zm_np; j += blockDim.x) {
+      const int base = __ldg(c.zm_base + j);
+      ptab[j] = base;
+      ptab[c.zm_np + j] = base / (int)c.zm_S;
+    }
   if (tid == 0) {
     for (int s = 0; s < RING; ++s) {
       mbar_init(&full[s], 1);
@@ -417,7 +431,7 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  TmShared sh{full, empty, sitem, red, pval, ptab,
+  TmShared sh{full, empty, sitem, sbase, red, pval, ptab,
               tsm + tm_head_bytes(c.pat_np, c.zm_np, table)};
   TL_K(c, 0);
   TL_BEGIN(c, l);
