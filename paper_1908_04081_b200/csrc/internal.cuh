@@ -167,15 +167,16 @@ struct Ctx {
   // a row-partitioned value stream (vs_S > 0): local rows are whole global
   // planes of vs_S rows in a permuted order, so a slot's neighbour is found
   // through plane tables, not by adding the offset: union offset k = vs_dz[k]
-  // planes + vs_r[k] rows within the plane; local block b of vs_S rows is
-  // geometric plane vs_geo[b]; geometric plane z starts at local row
-  // vs_base[z] (-1: not held; only absent slots can point there)
+  // planes + vs_r[k] rows within the plane; for local block b of vs_S rows,
+  // vs_below[b] / vs_above[b] = first local row of the geometric plane below /
+  // above it (the block's own first row where that plane is not held -- only
+  // absent slots can point there)
   int64_t vs_S;
   int vs_np;
   signed char vs_dz[VS_MAX_NE];
   int vs_r[VS_MAX_NE];
-  const int* vs_geo;
-  const int* vs_base;
+  const int* vs_below;
+  const int* vs_above;
   int ss_ne;
   int ss_off[SS_MAX_NE];
   int hs_ss;         // HSCG row sums through the superset mask (SSCG_HS_SS)

@@ -692,12 +692,39 @@ __device__ __forceinline__ int vs_nbr(const Ctx& c, int i, int nm1, int k, const
 // are requested VS_DEPTH chunks before their use -- across rows too: vq holds
 // the next VS_DEPTH chunks (of this row, then of the row this thread handles
 // next, inext; < 0: none), a register queue the unrolled loop renames for free.
+// PL: the row is row `pin` of local block `blk` (the kernels carry both from
+// row to row: one division per thread, not per row).
 #ifndef VS_DEPTH
 #define VS_DEPTH 1
 #endif
 #ifndef VS_MINB
 #define VS_MINB 4  // CTAs per SM the register allocation must allow (64 registers)
 #endif
+// (block, row within the block) of a thread's rows i0, i0 + stride, ...
+template <bool PL>
+struct VsWalk {
+  int blk = 0, pin = 0, dblk = 0, dpin = 0, S = 1;
+  __device__ __forceinline__ VsWalk(const Ctx& c, int i0, int stride) {
+    if (PL) {
+      S = (int)c.vs_S;
+      blk = i0 / S;
+      pin = i0 - blk * S;
+      dblk = stride / S;
+      dpin = stride - dblk * S;
+    }
+  }
+  __device__ __forceinline__ void next() {
+    if (PL) {
+      blk += dblk;
+      pin += dpin;
+      if (pin >= S) {
+        pin -= S;
+        ++blk;
+      }
+    }
+  }
+};
+
 template <int NE>
 __device__ __forceinline__ void vs_request(const Ctx& c, int i, int chunk, double (&v)[VS_CHUNK]) {
   const double* vp = c.vs_val + i + (int64_t)(chunk * VS_CHUNK) * c.ld;
@@ -717,22 +744,17 @@ __device__ __forceinline__ void vs_first(const Ctx& c, int i, double (&vq)[VS_DE
 template <int NV, int NE, bool PL = false>
 __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
                                        const double* const* __restrict__ xs, double* acc,
-                                       double (&vq)[VS_DEPTH][VS_CHUNK], int inext) {
+                                       double (&vq)[VS_DEPTH][VS_CHUNK], int inext, int blk = 0,
+                                       int pin = 0) {
   constexpr int NCH = (NE + VS_CHUNK - 1) / VS_CHUNK;
   constexpr int D = VS_DEPTH < NCH ? VS_DEPTH : NCH;  // the queue reaches at most one row ahead
 #pragma unroll
   for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-  int pb[3] = {0, 0, 0}, pin = 0;
+  int pb[3] = {0, 0, 0};
   if (PL) {
-    const int S = (int)c.vs_S, blk = i / S;
-    const int zg = __ldg(c.vs_geo + blk);
-    pin = i - blk * S;
-    const int own = i - pin;
-    const int bm = zg > 0 ? __ldg(c.vs_base + zg - 1) : -1;
-    const int bp = zg + 1 < c.vs_np ? __ldg(c.vs_base + zg + 1) : -1;
-    pb[0] = bm >= 0 ? bm : own;
-    pb[1] = own;
-    pb[2] = bp >= 0 ? bp : own;
+    pb[0] = __ldg(c.vs_below + blk);
+    pb[1] = i - pin;
+    pb[2] = __ldg(c.vs_above + blk);
   }
 #pragma unroll
   for (int ch = 0; ch < NCH; ++ch) {
@@ -787,9 +809,10 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, VS_MINB) k_level0_vs(Ctx c, ZmPt
   double vn[VS_DEPTH][VS_CHUNK];
   if ((int)(blockIdx.x * blockDim.x + threadIdx.x) < plim)
     vs_first<NE>(c, blockIdx.x * blockDim.x + threadIdx.x, vn);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
+  VsWalk<PL> w(c, blockIdx.x * blockDim.x + threadIdx.x, stride);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride, w.next()) {
     double acc[3];
-    vs_row<3, NE, PL>(c, i, nm1, xs, acc, vn, i + stride < plim ? i + stride : -1);
+    vs_row<3, NE, PL>(c, i, nm1, xs, acc, vn, i + stride < plim ? i + stride : -1, w.blk, w.pin);
     const double p = xs[1][i], r = xs[2][i];
     if (i < n_own) {
       const double t = __dsub_rn(c.b[i], acc[0]);
@@ -832,14 +855,15 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, VS_MINB) k_level_vs(Ctx c, int l
   double vn[VS_DEPTH][VS_CHUNK];
   if ((int)(blockIdx.x * blockDim.x + threadIdx.x) < plim)
     vs_first<NE>(c, blockIdx.x * blockDim.x + threadIdx.x, vn);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride) {
+  VsWalk<PL> w(c, blockIdx.x * blockDim.x + threadIdx.x, stride);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride, w.next()) {
     double acc[2];
     const bool rrow = do_r && i < rlim;
     const int inext = i + stride < plim ? i + stride : -1;
     if (rrow)
-      vs_row<2, NE, PL>(c, i, nm1, xs, acc, vn, inext);
+      vs_row<2, NE, PL>(c, i, nm1, xs, acc, vn, inext, w.blk, w.pin);
     else
-      vs_row<1, NE, PL>(c, i, nm1, xs, acc, vn, inext);
+      vs_row<1, NE, PL>(c, i, nm1, xs, acc, vn, inext, w.blk, w.pin);
     const double wp = recur(acc[0], xs[0][i], use_mu ? zp.ym[0][i] : 0.0, th, ga, mu, use_mu);
     zp.yo[0][i] = wp;
     bad |= !finite(wp);

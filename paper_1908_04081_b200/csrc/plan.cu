@@ -159,8 +159,8 @@ struct sscg_plan {
   int vs_np = 0;
   signed char vs_dz[VS_MAX_NE] = {};
   int vs_r[VS_MAX_NE] = {};
-  int* d_vs_geo = nullptr;
-  int* d_vs_base = nullptr;
+  int* d_vs_geo = nullptr;   // vs_below
+  int* d_vs_base = nullptr;  // vs_above
   int ss_ne = 0;  // superset-mask form (superset_setup); 0: table-walking kernels
   int ss_off[SS_MAX_NE] = {};
   unsigned* d_ss_mask = nullptr;
@@ -320,8 +320,8 @@ Ctx make_ctx(sscg_plan* p) {
     c.vs_dz[k] = p->vs_dz[k];
     c.vs_r[k] = p->vs_r[k];
   }
-  c.vs_geo = p->d_vs_geo;
-  c.vs_base = p->d_vs_base;
+  c.vs_below = p->d_vs_geo;
+  c.vs_above = p->d_vs_base;
   c.ss_ne = p->ss_ne;
   c.hs_ss = p->hs_ss;
   for (int k = 0; k < SS_MAX_NE; ++k) c.ss_off[k] = p->ss_off[k];
@@ -1191,10 +1191,18 @@ int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col
     }
   });
   if (grows) {
-    TRY(dalloc(p, &p->d_vs_geo, geo.size()));
-    TRY(dalloc(p, &p->d_vs_base, base.size()));
-    CUDA_OK(cudaMemcpy(p->d_vs_geo, geo.data(), 4 * geo.size(), cudaMemcpyHostToDevice));
-    CUDA_OK(cudaMemcpy(p->d_vs_base, base.data(), 4 * base.size(), cudaMemcpyHostToDevice));
+    // per local block: first local rows of the geometric planes below / above
+    const size_t nblk = geo.size();
+    std::vector<int> below(nblk), above(nblk);
+    for (size_t bk = 0; bk < nblk; ++bk) {
+      const int zg = geo[bk], own = (int)(bk * (size_t)p->vs_S);
+      below[bk] = zg > 0 ? base[(size_t)zg - 1] : own;
+      above[bk] = zg + 1 < (int)base.size() ? base[(size_t)zg + 1] : own;
+    }
+    TRY(dalloc(p, &p->d_vs_geo, nblk));
+    TRY(dalloc(p, &p->d_vs_base, nblk));
+    CUDA_OK(cudaMemcpy(p->d_vs_geo, below.data(), 4 * nblk, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(p->d_vs_base, above.data(), 4 * nblk, cudaMemcpyHostToDevice));
   }
   TRY(dalloc(p, &p->d_vs_val, sv_len));
   TRY(copy_h2d(p, p->d_vs_val, sv.get(), 8 * sv_len));
