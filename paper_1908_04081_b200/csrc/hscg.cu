@@ -16,6 +16,8 @@
 //
 // Roofline (HBM): ~105 n bytes per iteration (p, ap, x, r, b passes, two
 // SpMV-shaped gathers), ids or CSR once per SpMV.
+#include <algorithm>
+
 #include "internal.cuh"
 #include "ritz.cuh"
 #include "rowops.cuh"
@@ -219,9 +221,28 @@ __global__ void __launch_bounds__(HS_T) k_hs_xr(Ctx c, const double* P, const do
   double rr = 0.0;
   if (out == SSCG_RUNNING) {
     const double alpha = st->hs_rr / pap;
-    const int64_t stride = (int64_t)gridDim.x * HS_T;
-    for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.n_own; i += stride) {
-      c.x[i] = __dadd_rn(c.x[i], __dmul_rn(alpha, P[i]));  // q = alpha*p; x = x + q
+    // two rows per thread and step (16-byte accesses; the columns are 16-byte
+    // aligned), two steps in flight: a pure stream of 48 bytes per row
+    const int64_t n2 = c.n_own & ~(int64_t)1;
+    const int64_t stride = (int64_t)gridDim.x * HS_T * 2;
+#pragma unroll 2
+    for (int64_t i = ((int64_t)blockIdx.x * HS_T + threadIdx.x) * 2; i < n2; i += stride) {
+      double2 xv = *reinterpret_cast<const double2*>(c.x + i);
+      const double2 pv = *reinterpret_cast<const double2*>(P + i);
+      double2 rv = *reinterpret_cast<const double2*>(R + i);
+      const double2 av = *reinterpret_cast<const double2*>(AP + i);
+      xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));  // q = alpha*p; x = x + q
+      xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+      rv.x = __dsub_rn(rv.x, __dmul_rn(alpha, av.x));
+      rv.y = __dsub_rn(rv.y, __dmul_rn(alpha, av.y));
+      *reinterpret_cast<double2*>(c.x + i) = xv;
+      *reinterpret_cast<double2*>(R + i) = rv;
+      rr = fma(rv.x, rv.x, rr);
+      rr = fma(rv.y, rv.y, rr);
+    }
+    if (n2 < c.n_own && blockIdx.x == 0 && threadIdx.x == 0) {  // odd row count: the last row
+      const int64_t i = n2;
+      c.x[i] = __dadd_rn(c.x[i], __dmul_rn(alpha, P[i]));
       const double r = __dsub_rn(R[i], __dmul_rn(alpha, AP[i]));
       R[i] = r;
       rr = fma(r, r, rr);
@@ -261,9 +282,18 @@ __global__ void __launch_bounds__(HS_T) k_hs_p(Ctx c, double* P, const double* R
   if (st->done) return;
   const double rr = c.red_buf[HS_RED_RRN];
   const double beta = rr / st->hs_rr;
-  const int64_t stride = (int64_t)gridDim.x * HS_T;
-  for (int64_t i = (int64_t)blockIdx.x * HS_T + threadIdx.x; i < c.n_own; i += stride)
-    P[i] = __dadd_rn(R[i], __dmul_rn(beta, P[i]));
+  const int64_t n2 = c.n_own & ~(int64_t)1;
+  const int64_t stride = (int64_t)gridDim.x * HS_T * 2;
+#pragma unroll 2
+  for (int64_t i = ((int64_t)blockIdx.x * HS_T + threadIdx.x) * 2; i < n2; i += stride) {
+    double2 pv = *reinterpret_cast<const double2*>(P + i);
+    const double2 rv = *reinterpret_cast<const double2*>(R + i);
+    pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
+    pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
+    *reinterpret_cast<double2*>(P + i) = pv;
+  }
+  if (n2 < c.n_own && blockIdx.x == 0 && threadIdx.x == 0)
+    P[n2] = __dadd_rn(R[n2], __dmul_rn(beta, P[n2]));
   if (!last_cta(&st->gram_count)) return;
   if (threadIdx.x == 0) {
     st->gram_count = 0;
@@ -339,10 +369,14 @@ void hs_launch_init(const Ctx& c, double* P, double* R, const double* x0, size_t
 template <int MODE>
 void hs_launch_ap(const Ctx& c, const double* P, double* AP, const double* R, bool tv, size_t smem,
                   cudaStream_t s) {
-  if (tv)
+  // as many CTAs as the partial-sum arrays hold (8 per SM): the row sums gather
+  // through L1 and want every warp slot, not the level kernels' grid
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((c.n_own + HS_T - 1) / HS_T, RED_BLOCKS));
+  if (tv)  // (two row sums per row, 78 registers: one wave of the plan's grid is faster)
     k_hs_ap<MODE, true><<<c.red_n, HS_T, smem, s>>>(c, P, AP, R);
   else
-    k_hs_ap<MODE, false><<<c.red_n, HS_T, smem, s>>>(c, P, AP, R);
+    k_hs_ap<MODE, false><<<grid, HS_T, smem, s>>>(c, P, AP, R);
 }
 template <int MODE>
 void hs_launch_final(const Ctx& c, const double* R, size_t smem, cudaStream_t s) {
@@ -395,11 +429,17 @@ void launch_hscg_ap(const Ctx& c, double* P, double* AP, const double* R, bool t
     default: hs_launch_ap<0>(c, P, AP, R, tv, 0, s); break;
   }
 }
+// the two streaming kernels: one wave of 8 CTAs per SM at most, a function of
+// the owned rows only (every plan form of an operator sums the same partials)
+static int hs_stream_grid(const Ctx& c) {
+  const int64_t g = (c.n_own + (int64_t)HS_T * 4 - 1) / ((int64_t)HS_T * 4);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, RED_BLOCKS));
+}
 void launch_hscg_xr(const Ctx& c, double* P, double* AP, double* R, bool prod, cudaStream_t s) {
-  k_hs_xr<<<c.red_n, HS_T, 0, s>>>(c, P, AP, R, prod ? 1 : 0);
+  k_hs_xr<<<hs_stream_grid(c), HS_T, 0, s>>>(c, P, AP, R, prod ? 1 : 0);
 }
 void launch_hscg_p(const Ctx& c, double* P, double* R, cudaStream_t s) {
-  k_hs_p<<<c.red_n, HS_T, 0, s>>>(c, P, R);
+  k_hs_p<<<hs_stream_grid(c), HS_T, 0, s>>>(c, P, R);
 }
 void launch_hscg_final(const Ctx& c, const double* R, cudaStream_t s) {
   const size_t smem = hs_smem(c);

@@ -101,7 +101,9 @@ def test_hscg_production_mode(gpu_ready):
     x2, t2, c2 = hscg_solve(prob, 1e-10, mode="production")
     assert t1.converged and t2.converged
     m = min(len(c1.alphas), len(c2.alphas))
-    np.testing.assert_array_equal(c2.alphas[:m], c1.alphas[:m])
+    # the production SpMV kernel runs a larger grid (one row sum per row), so its
+    # p.Ap partials group differently: the same coefficients to rounding
+    np.testing.assert_allclose(c2.alphas[:m], c1.alphas[:m], rtol=1e-11)
     assert abs(t2.total_iters - t1.total_iters) <= 2
     a = prob.a
     m_ = sp.csr_matrix((a.values, a.col_idx, a.row_ptr), shape=(a.n, a.n))
