@@ -490,6 +490,108 @@ __device__ void golden_refine(const double* pts_, int n, double lo, double hi, d
   *vo = leja_f(x, pts, n);
 }
 
+// The same maximisation, two golden-section steps per round (n <= 10, three
+// groups of 10 lanes).  A step's new point depends on the comparison before it
+// only through which of two formulas applies, so while group 0 evaluates the
+// objective at this step's new point, groups 1 and 2 evaluate it at the two
+// points the NEXT step could take; once this step's value is in, the next
+// comparison picks one of them.  Every quantity is formed by the expressions of
+// golden_refine on the same operands -- the iterates are bit-identical, the
+// dependent chain of logs is half as long.
+__device__ __forceinline__ double np_sum_group(double term, int n, int base) {
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = __shfl_sync(0xffffffffu, term, base + j);
+  double res;
+  if (n < 8) {
+    res = 0.0;
+    for (int j = 0; j < n; ++j) res += r[j];
+  } else {
+    res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (int j = 8; j < n; ++j) res += __shfl_sync(0xffffffffu, term, base + j);
+  }
+  return res;
+}
+__device__ void golden_refine2(const double* pts_, int n, double lo, double hi, double* xo,
+                               double* vo) {
+  constexpr int G = 10;
+  const int lane = threadIdx.x & 31, grp = lane / G, gl = lane - grp * G;
+  const int base = grp * G;
+  const double pl = gl < n ? pts_[gl] : 0.0;  // this lane's point (every group holds them all)
+  // objective at x0 / x1 / x2 in groups 0 / 1 / 2; every lane returns all three
+  auto eval3 = [&](double x0, double x1, double x2, double& f0, double& f1, double& f2) {
+    const double x = grp == 0 ? x0 : grp == 1 ? x1 : x2;
+    const double term = (gl < n && grp < 3) ? log(fabs(x - pl) + 1e-300) : 0.0;
+    const double res = np_sum_group(term, n, base);
+    f0 = __shfl_sync(0xffffffffu, res, 0);
+    f1 = __shfl_sync(0xffffffffu, res, G);
+    f2 = __shfl_sync(0xffffffffu, res, 2 * G);
+  };
+  const double ratio = (sqrt(5.0) - 1.0) / 2.0;
+  double a = lo, b = hi;
+  double c = b - ratio * (b - a);
+  double d = a + ratio * (b - a);
+  double fc, fd, unused;
+  eval3(c, d, d, fc, fd, unused);
+  int it = 0;
+  while (it < 80) {
+    if (b - a <= 1e-14 * py_max(py_max(fabs(a), fabs(b)), 1.0)) break;
+    // this step (comparison known): the new point x1
+    const bool up = fc > fd;
+    double a1 = a, b1 = b, c1, d1, x1;
+    if (up) {
+      b1 = d;
+      d1 = c;
+      c1 = b1 - ratio * (b1 - a1);
+      x1 = c1;
+    } else {
+      a1 = c;
+      c1 = d;
+      d1 = a1 + ratio * (b1 - a1);
+      x1 = d1;
+    }
+    // the next step's two possible new points (it runs if the loop goes on)
+    const bool more = it + 1 < 80 && !(b1 - a1 <= 1e-14 * py_max(py_max(fabs(a1), fabs(b1)), 1.0));
+    // comparison true: b2 = d1, c2 = b2 - ratio (b2 - a1); false: a2 = c1, d2 = a2 + ratio (b1 - a2)
+    const double xt = d1 - ratio * (d1 - a1);
+    const double xf = c1 + ratio * (b1 - c1);
+    double f1, ft, ff;
+    eval3(x1, xt, xf, f1, ft, ff);
+    a = a1;
+    b = b1;
+    c = c1;
+    d = d1;
+    if (up) {
+      fd = fc;
+      fc = f1;
+    } else {
+      fc = fd;
+      fd = f1;
+    }
+    ++it;
+    if (!more) continue;  // the loop's own test ends it (or the iteration cap)
+    if (fc > fd) {
+      b = d;
+      d = c;
+      fd = fc;
+      c = xt;
+      fc = ft;
+    } else {
+      a = c;
+      c = d;
+      fc = fd;
+      d = xf;
+      fd = ff;
+    }
+    ++it;
+  }
+  const double x = 0.5 * (a + b);
+  double v;
+  eval3(x, x, x, v, unused, unused);
+  *xo = x;
+  *vo = v;
+}
+
 struct LejaShared {
   double pts[SMAX];
   double rx[4], rv[4];
@@ -658,8 +760,12 @@ __device__ void cta_leja_point(double lo, double hi, int n, int grid, double* ob
     const int il = i - 1 > 0 ? i - 1 : 0;
     const int ih = i + 1 < grid - 1 ? i + 1 : grid - 1;
     double xr, vr;
-    golden_refine(L.pts, n, lin_x(il, grid, lo, hi, step, zero_step),
-                  lin_x(ih, grid, lo, hi, step, zero_step), &xr, &vr);
+    if (n <= 10)
+      golden_refine2(L.pts, n, lin_x(il, grid, lo, hi, step, zero_step),
+                     lin_x(ih, grid, lo, hi, step, zero_step), &xr, &vr);
+    else
+      golden_refine(L.pts, n, lin_x(il, grid, lo, hi, step, zero_step),
+                    lin_x(ih, grid, lo, hi, step, zero_step), &xr, &vr);
     if ((tid & 31) == 0) {
       L.rx[warp] = xr;
       L.rv[warp] = vr;

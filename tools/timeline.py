@@ -62,13 +62,18 @@ def main():
     names.update({16: "gram", 17: "small", 18: "recover", 19: "params"})
     names.update({20 + n: f"leja{n}" for n in range(2, 16)})
     lo, hi = args.lo, min(args.hi, outer - 2)
+    # reference node: level 0 of the TMA march, else (other level kernels are
+    # not instrumented) the parameter kernel that opens the outer loop
+    ref = 0 if valid[lo:hi, 0].any() else 19
+    valid[:, 19] = buf[:, 19, 0] != np.uint64(0xFFFFFFFFFFFFFFFF)
+    t1[:, 19] = np.where(buf[:, 19, 1] != 0, t1[:, 19], t0[:, 19])
     chain = [l for l in range(sigma)] + [16, 17, 18]
     rows = []
     for nd in sorted(names):
-        ks = [k for k in range(lo, hi) if valid[k, nd] and valid[k, 0]]
+        ks = [k for k in range(lo, hi) if valid[k, nd] and valid[k, ref]]
         if not ks:
             continue
-        st = np.mean([t0[k, nd] - t0[k, 0] for k in ks]) / 1e3
+        st = np.mean([t0[k, nd] - t0[k, ref] for k in ks]) / 1e3
         du = np.mean([t1[k, nd] - t0[k, nd] for k in ks]) / 1e3
         gap = None
         if nd in chain and chain.index(nd) > 0:
@@ -80,7 +85,7 @@ def main():
             gap = float(np.mean(g)) / 1e3 if g else None
         rows.append({"node": names[nd], "start_us": round(st, 1), "dur_us": round(du, 1),
                      "gap_before_us": None if gap is None else round(gap, 1), "n": len(ks)})
-    period = np.mean([t0[k + 1, 0] - t0[k, 0] for k in range(lo, hi) if valid[k, 0] and valid[k + 1, 0]]) / 1e3
+    period = np.mean([t0[k + 1, ref] - t0[k, ref] for k in range(lo, hi) if valid[k, ref] and valid[k + 1, ref]]) / 1e3
     print(json.dumps({"config": args.config, "device_ms": ms, "outer": outer,
                       "period_us": round(float(period), 1)}))
     for r in rows:
