@@ -16,6 +16,7 @@
 //   next-block parameters         adaptive.py:254-258 -> basis.py:58-177 (Leja grid
 //                                  objective in numpy's pairwise-sum order, golden
 //                                  refinement, 1e-12 tie rule; Chebyshev mu = w/8)
+#include <cstdio>
 #include <math.h>
 
 #include "internal.cuh"
@@ -27,6 +28,10 @@ constexpr int NT = SMALL_THREADS;  // 512
 constexpr int NW = NT / 32;        // 16 warps
 constexpr int JLD = CMAX;          // work matrix leading dimension (odd: conflict-free row access)
 constexpr int LEJA_CAND_CAP = 256;
+#ifndef SSCG_STURM_CHAINS
+#define SSCG_STURM_CHAINS 2
+#endif
+constexpr int STURM_CHAINS = SSCG_STURM_CHAINS;  // shifts per lane and multisection step
 constexpr int LEJA_SMEM_GRID = 16384;  // grid objective in shared memory up to this many points
 
 
@@ -155,13 +160,16 @@ __device__ void warp_jacobi(double* A, int n, double* rot /* 4*17 */) {
 //     multisection, 32 shifts per step (one per lane).
 // Cost O(n^3/32) per matrix instead of ~10 Jacobi sweeps of O(n^3).
 __device__ __forceinline__ double warp_sum_all(double v) {
-  // fixed-order tree into lane 0, then broadcast: every lane sees the same bits
-  v += __shfl_down_sync(0xffffffffu, v, 16);
-  v += __shfl_down_sync(0xffffffffu, v, 8);
-  v += __shfl_down_sync(0xffffffffu, v, 4);
-  v += __shfl_down_sync(0xffffffffu, v, 2);
-  v += __shfl_down_sync(0xffffffffu, v, 1);
-  return __shfl_sync(0xffffffffu, v, 0);
+  // fixed-order tree (offsets 16, 8, 4, 2, 1) as a butterfly: IEEE addition is
+  // commutative, so after each round the partial sums are periodic over the
+  // lanes and every lane ends with the bits the shfl_down tree leaves in lane 0
+  // -- without the closing broadcast
+  v += __shfl_xor_sync(0xffffffffu, v, 16);
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
 }
 __device__ __forceinline__ double warp_max_all(double v) {
 #pragma unroll
@@ -180,10 +188,12 @@ __device__ void warp_tridiag(double* A, int n, double* d, double* e, double* v, 
     const double alpha = A[(i + 1) * JLD + i];
     // xnorm = ||A[i+2:n, i]|| (dnrm2; scaled only when squares could over/underflow)
     const double xr = (lane >= 1 && lane < m) ? A[(i + 1 + lane) * JLD + i] : 0.0;
+    // the two reductions are independent chains (the sum is only used in range)
+    const double ss = warp_sum_all(xr * xr);
     const double amax = warp_max_all(fabs(xr));
     double xnorm;
     if (amax > 1e-140 && amax < 1e140) {
-      xnorm = sqrt(warp_sum_all(xr * xr));
+      xnorm = sqrt(ss);
     } else if (amax > 0.0) {
       const double inv = 1.0 / amax;
       const double t = xr * inv;
@@ -249,43 +259,110 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
   return cnt;
 }
 
-// Eigenvalue j (ascending, 0-based) of (d, e) inside [lo, hi] by multisection
-// with the G lanes of one lane group (group-uniform control flow).  Like
+// Sturm counts of C shifts at once: the recurrence is one dependent chain of
+// ~100 cycles per row (reciprocal + three fp64 operations), so C independent
+// chains per lane cost about the time of one.  Same arithmetic per shift as
+// sturm_count.
+template <int C>
+__device__ __forceinline__ void sturm_count_multi(const double* d, const double* e2, int n,
+                                                  const double (&sig)[C], double pivmin,
+                                                  int (&cnt)[C]) {
+  double q[C];
+  const double d0 = d[0];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    q[c] = d0 - sig[c];
+    cnt[c] = q[c] < 0.0;
+  }
+  for (int k = 1; k < n; ++k) {
+    const double dk = d[k], ek = e2[k - 1];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      if (fabs(q[c]) <= pivmin) q[c] = -pivmin;
+      q[c] = (dk - sig[c]) - ek * rcp_fast(q[c]);
+      cnt[c] += q[c] < 0.0;
+    }
+  }
+}
+
+// Eigenvalue j (ascending, 0-based) of (d, e) inside [lo, hi] by multisection.
+// The warp runs up to three searches at once, each on its own group of G lanes
+// (lanes base .. base+G-1, gl = lane - base; j, lo, hi, active are uniform
+// inside a group), C shifts per lane: G * C shifts per step, ascending with
+// t = gl * C + c.  All groups walk the same loop in lockstep (one instruction
+// stream; a finished group idles until the last one is done) -- the searches
+// used to sit in three divergent branches and ran one after the other.  Like
 // LAPACK's tridiagonal eigensolvers the result has an absolute accuracy floor
 // (abs_tol, see warp_cond_estimate): an exactly singular direction comes back at
 // LAPACK's noise level instead of being resolved to ~0, which would inflate the
 // cond estimate far beyond the reference's saturation level.  Shifts are
 // log-spaced while the bracket spans many binades on one side of 0.
-template <int G>
+template <int C>
 __device__ double group_eig_index(const double* d, const double* e2, int n, int j, double lo,
-                                  double hi, double pivmin, double abs_tol, int gl,
-                                  unsigned gmask) {
-  const int base = __ffs(gmask) - 1;
+                                  double hi, double pivmin, double abs_tol, bool active, int G,
+                                  int base, int gl) {
+  const bool member = gl >= 0 && gl < G;  // lanes outside every group only vote
+  const unsigned gmask = member ? (((G >= 32) ? 0xffffffffu : ((1u << G) - 1u)) << base) : 0u;
+  const int GT = G * C;
   for (int step = 0; step < 80; ++step) {
     const double w = hi - lo;
-    if (!(w > fmax(abs_tol, 1e-13 * fmax(fabs(lo), fabs(hi))))) break;
-    double sig;
-    const double fr = (double)(gl + 1) / (double)(G + 1);
+    const bool go = member && active && (w > fmax(abs_tol, 1e-13 * fmax(fabs(lo), fabs(hi))));
+    if (!__any_sync(0xffffffffu, go)) break;
+    if (!go) continue;  // group-uniform
+    double sig[C];
     const double l0 = fmax(lo, abs_tol);         // positive side: log-spaced above abs_tol
     const double h0 = fmin(hi, -abs_tol);        // negative side
     if (lo >= 0.0 && hi > 16.0 * l0) {
-      sig = l0 * exp2(log2(hi / l0) * fr);
-      if (lo == 0.0) sig = (gl == 0) ? l0 : l0 * exp2(log2(hi / l0) * (double)gl / (double)(G - 1));
+      const double lg = log2(hi / l0);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int t = gl * C + c;
+        sig[c] = (lo == 0.0) ? (t == 0 ? l0 : l0 * exp2(lg * (double)t / (double)(GT - 1)))
+                             : l0 * exp2(lg * ((double)(t + 1) / (double)(GT + 1)));
+      }
     } else if (hi <= 0.0 && lo < 16.0 * h0) {
-      sig = h0 * exp2(log2(lo / h0) * (1.0 - fr));
-      if (hi == 0.0)
-        sig = (gl == G - 1) ? h0 : h0 * exp2(log2(lo / h0) * (double)(G - 1 - gl) / (double)(G - 1));
+      const double lg = log2(lo / h0);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int t = gl * C + c;
+        sig[c] = (hi == 0.0)
+                     ? (t == GT - 1 ? h0 : h0 * exp2(lg * (double)(GT - 1 - t) / (double)(GT - 1)))
+                     : h0 * exp2(lg * (1.0 - (double)(t + 1) / (double)(GT + 1)));
+      }
     } else {
-      sig = lo + w * fr;
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        sig[c] = lo + w * ((double)(gl * C + c + 1) / (double)(GT + 1));
     }
-    const int cnt = sturm_count(d, e2, n, sig, pivmin);
-    const unsigned ok = __ballot_sync(gmask, cnt >= j + 1) >> base;  // lambda_j < sig
-    // shifts increase with gl: the first lane with cnt >= j+1 bounds from above
+    int cnt[C];
+    sturm_count_multi<C>(d, e2, n, sig, pivmin, cnt);
+    // shifts increase with t: the first one with cnt >= j+1 bounds lambda_j from
+    // above, the one before it from below
+    int fc = C;  // this lane's first bounding shift
+#pragma unroll
+    for (int c = C - 1; c >= 0; --c)
+      if (cnt[c] >= j + 1) fc = c;
+    double my_hi = sig[0], my_lo_in = sig[0];  // sig[fc], sig[fc - 1]
+#pragma unroll
+    for (int c = 1; c < C; ++c)
+      if (fc == c) {
+        my_hi = sig[c];
+        my_lo_in = sig[c - 1];
+      }
+    // the last shift of the lane before (the lower bound when fc == 0)
+    const double prev_last = __shfl_sync(gmask, sig[C - 1], base + (gl > 0 ? gl - 1 : 0));
+    const double my_lo = (fc > 0) ? my_lo_in : (gl > 0 ? prev_last : lo);
+    const unsigned ok = (__ballot_sync(gmask, fc < C) & gmask) >> base;
     const int k = ok ? __ffs(ok) - 1 : G;
-    const double s_hi = __shfl_sync(gmask, sig, base + (k < G ? k : 0));
-    const double s_lo = (k == 0) ? lo : __shfl_sync(gmask, sig, base + (k - 1));
-    if (k < G) hi = s_hi;
-    lo = s_lo;
+    const double s_hi = __shfl_sync(gmask, my_hi, base + (k < G ? k : 0));
+    const double s_lo = __shfl_sync(gmask, my_lo, base + (k < G ? k : 0));
+    const double top = __shfl_sync(gmask, sig[C - 1], base + G - 1);
+    if (k < G) {
+      hi = s_hi;
+      lo = s_lo;
+    } else {
+      lo = top;
+    }
   }
   return 0.5 * (lo + hi);
 }
@@ -302,7 +379,13 @@ __device__ double warp_cond_estimate(double* A, int n, double* scratch, bool dup
     const double a = A[0];
     return (a <= 0.0) ? INFINITY : (fabs(a) == 0.0 ? INFINITY : 1.0);
   }
+#ifdef SSCG_CONDTIME
+  const long long ct0 = clock64();
+#endif
   warp_tridiag(A, n, d, e, v, p);
+#ifdef SSCG_CONDTIME
+  const long long ct1 = clock64();
+#endif
   // squared off-diagonals and Gershgorin bounds
   double emax2 = 0.0;
   for (int k = lane; k < n - 1; k += 32) {
@@ -339,20 +422,47 @@ __device__ double warp_cond_estimate(double* A, int n, double* scratch, bool dup
   // make numerically rank-deficient blocks look admissible (measured on c4p).
   const double abs_tol = (dup_floor ? 8.673617379884035e-19 : 6.842277657836021e-49) * span;
   const double* e2 = v;
-  // three searches at once, 10 lanes each: lambda_max and the eigenvalues
-  // straddling 0 (lacore.py:111-117 needs lambda_max and the smallest |lambda|)
+  // the searches run at once, each on its own lane group: lambda_max and the
+  // eigenvalues straddling 0 (lacore.py:111-117 needs lambda_max and the smallest
+  // |lambda|).  A definite matrix has one of the two (the usual case: a Gram is
+  // positive semi-definite up to rounding): two groups of 16 lanes, else three of 10.
   const int neg = sturm_count(d, e2, n, 0.0, pivmin);  // eigenvalues < 0
-  const int grp = lane / 10, gl = lane % 10;
-  double res = NAN;
-  if (grp < 3) {
-    const unsigned gmask = 0x3FFu << (10 * grp);
-    if (grp == 0) res = group_eig_index<10>(d, e2, n, n - 1, gl_, gu_, pivmin, abs_tol, gl, gmask);
-    if (grp == 1 && neg < n) res = group_eig_index<10>(d, e2, n, neg, 0.0, gu_, pivmin, abs_tol, gl, gmask);
-    if (grp == 2 && neg > 0) res = group_eig_index<10>(d, e2, n, neg - 1, gl_, 0.0, pivmin, abs_tol, gl, gmask);
+  const bool three = neg > 0 && neg < n;
+  const int G = three ? 10 : 16;
+  const int grp = lane / G, gl = lane - grp * G;
+#ifdef SSCG_CONDTIME
+  const long long ct2 = clock64();
+#endif
+  // group 0: lambda_max; group 1: the smallest positive one (or, for a negative
+  // definite matrix, the negative one nearest 0); group 2: the negative one nearest 0
+  int sj = n - 1;
+  double slo = gl_, shi = gu_;
+  bool act = grp == 0;
+  if (grp == 1) {
+    act = true;
+    if (neg < n) { sj = neg; slo = 0.0; shi = gu_; }
+    else { sj = neg - 1; slo = gl_; shi = 0.0; }
+  } else if (grp == 2 && three) {
+    act = true;
+    sj = neg - 1; slo = gl_; shi = 0.0;
   }
+  const double res = group_eig_index<STURM_CHAINS>(d, e2, n, sj, slo, shi, pivmin, abs_tol, act, G,
+                                                   grp * G, (grp < (three ? 3 : 2)) ? gl : -1);
+#ifdef SSCG_CONDTIME
+  {
+    const long long ct3 = clock64();
+    __syncwarp();
+    const long long ct4 = clock64();
+    if (n >= 23 && (lane % 10) == 0 && lane < 30)
+      printf("cond n=%d grp=%d tridiag=%lld setup+count=%lld search=%lld all=%lld\n", n, grp,
+             ct1 - ct0, ct2 - ct1, ct3 - ct2, ct4 - ct0);
+  }
+#endif
   const double lmax = __shfl_sync(0xffffffffu, res, 0);
-  const double pos_small = __shfl_sync(0xffffffffu, res, 10);
-  const double neg_small = __shfl_sync(0xffffffffu, res, 20);
+  const double g1 = __shfl_sync(0xffffffffu, res, G);
+  const double g2 = __shfl_sync(0xffffffffu, res, three ? 2 * G : 0);
+  const double pos_small = g1;                    // used when neg < n
+  const double neg_small = three ? g2 : g1;       // used when neg > 0
   if (!(lmax > 0.0)) return INFINITY;
   double smallest = INFINITY;
   if (neg < n) smallest = pos_small;
@@ -1327,6 +1437,19 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
         }
       }
     }
+    // the record's per-column arrays, one lane per entry (lane 0 alone used to
+    // walk them: ~50 dependent global load -> store pairs)
+    const int rk = st->n_records;
+    __syncwarp();
+    if (rk < cf.cap_outer) {
+      for (int i = lane; i <= SMAX; i += 32)
+        c.rec_conds[(int64_t)rk * (SMAX + 1) + i] = (i <= sbar) ? S.conds[i] : NAN;
+      for (int i = lane; i < SMAX; i += 32) {
+        c.rec_th[(int64_t)rk * SMAX + i] = st->prm.th[i];
+        c.rec_ga[(int64_t)rk * SMAX + i] = st->prm.ga[i];
+        c.rec_mu[(int64_t)rk * SMAX + i] = st->prm.mu[i];
+      }
+    }
     if (lane == 0) {
       st->rz = R.rz[j_done];
       // trace.mark_outer + record (adaptive.py:178, 232-246)
@@ -1336,7 +1459,6 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
       st->diag_base = mark;
       st->diag_n = cf.trace_full ? j_done : 0;
       st->s_tilde = s_t;
-      const int rk = st->n_records;
       if (rk < cf.cap_outer) {
         int* ri = c.rec_i + (int64_t)rk * SSCG_REC_NI;
         double* rd = c.rec_d + (int64_t)rk * SSCG_RECD_ND;
@@ -1355,13 +1477,6 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
         rd[SSCG_RECD_TRUE] = S.sc[SC_TRUE];
         rd[SSCG_RECD_RREL] = S.sc[SC_RREL];
         rd[SSCG_RECD_C] = S.sc[SC_CSEL];
-        for (int i = 0; i <= SMAX; ++i)
-          c.rec_conds[(int64_t)rk * (SMAX + 1) + i] = (i <= sbar) ? S.conds[i] : NAN;
-        for (int i = 0; i < SMAX; ++i) {
-          c.rec_th[(int64_t)rk * SMAX + i] = st->prm.th[i];
-          c.rec_ga[(int64_t)rk * SMAX + i] = st->prm.ga[i];
-          c.rec_mu[(int64_t)rk * SMAX + i] = st->prm.mu[i];
-        }
       }
       st->n_records = rk + 1;
       if (diverged) {
