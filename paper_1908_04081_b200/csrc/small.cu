@@ -28,6 +28,13 @@ constexpr int NT = SMALL_THREADS;  // 512
 constexpr int NW = NT / 32;        // 16 warps
 constexpr int JLD = CMAX;          // work matrix leading dimension (odd: conflict-free row access)
 constexpr int LEJA_CAND_CAP = 256;
+#ifndef SSCG_CONDS_SPREAD
+#define SSCG_CONDS_SPREAD 1
+#endif
+#ifndef SSCG_TRIDIAG_BATCH
+#define SSCG_TRIDIAG_BATCH 8
+#endif
+constexpr int TB = SSCG_TRIDIAG_BATCH;  // rows per load batch in warp_tridiag
 #ifndef SSCG_STURM_CHAINS
 #define SSCG_STURM_CHAINS 2
 #endif
@@ -180,27 +187,44 @@ __device__ __forceinline__ double warp_max_all(double v) {
 // dsytd2 (lower) on the n x n symmetric matrix A (smem, ld JLD, full storage);
 // d[n], e[n-1], v/p scratch [CMAX] in smem.  Warp-collective; lane c owns
 // column c of the trailing block (A is symmetric, so column c = row c).
-__device__ void warp_tridiag(double* A, int n, double* d, double* e, double* v, double* p) {
+// v and w of the current reflector sit interleaved in vp (one 16-byte load per
+// row of the rank-2 update); the row loops run in batches whose loads are all
+// issued before the first dependent operation -- same operations, same order.
+__device__ __noinline__ void warp_tridiag(double* __restrict__ A, int n, double* __restrict__ d,
+                                          double* __restrict__ e, double2* __restrict__ vp) {
   const int lane = threadIdx.x & 31;
+#ifdef SSCG_CONDTIME
+  long long tseg[6] = {0, 0, 0, 0, 0, 0};
+  long long tc = clock64();
+#define TSEG(k) do { const long long t_ = clock64(); tseg[k] += t_ - tc; tc = t_; } while (0)
+#else
+#define TSEG(k)
+#endif
   for (int i = 0; i < n - 1; ++i) {
     const int m = n - i - 1;  // reflector length (rows i+1 .. n-1)
     double* A22 = A + (i + 1) * JLD + (i + 1);
     const double alpha = A[(i + 1) * JLD + i];
     // xnorm = ||A[i+2:n, i]|| (dnrm2; scaled only when squares could over/underflow)
     const double xr = (lane >= 1 && lane < m) ? A[(i + 1 + lane) * JLD + i] : 0.0;
-    // the two reductions are independent chains (the sum is only used in range)
+    // amax^2 <= ss <= 31 amax^2: a sum of squares inside (1e-270, 1e270) puts the
+    // largest entry inside dnrm2's unscaled range without reducing for it
     const double ss = warp_sum_all(xr * xr);
-    const double amax = warp_max_all(fabs(xr));
     double xnorm;
-    if (amax > 1e-140 && amax < 1e140) {
+    if (ss > 1e-270 && ss < 1e270) {
       xnorm = sqrt(ss);
-    } else if (amax > 0.0) {
-      const double inv = 1.0 / amax;
-      const double t = xr * inv;
-      xnorm = amax * sqrt(warp_sum_all(t * t));
     } else {
-      xnorm = 0.0;
+      const double amax = warp_max_all(fabs(xr));
+      if (amax > 1e-140 && amax < 1e140) {
+        xnorm = sqrt(ss);
+      } else if (amax > 0.0) {
+        const double inv = 1.0 / amax;
+        const double t = xr * inv;
+        xnorm = amax * sqrt(warp_sum_all(t * t));
+      } else {
+        xnorm = 0.0;
+      }
     }
+    TSEG(0);
     if (xnorm == 0.0) {  // H = I
       if (lane == 0) e[i] = alpha;
       continue;
@@ -208,31 +232,73 @@ __device__ void warp_tridiag(double* A, int n, double* d, double* e, double* v, 
     const double beta = -copysign(hypot(alpha, xnorm), alpha);
     const double tau = (beta - alpha) / beta;
     const double scal = 1.0 / (alpha - beta);
+    TSEG(1);
     const double vl = (lane == 0) ? 1.0 : xr * scal;  // v[lane], lane < m
-    if (lane < m) v[lane] = vl;
+    if (lane < m) vp[lane].x = vl;
     if (lane == 0) e[i] = beta;
     __syncwarp();
     // p = tau * A22 v  (lane c: column c of the symmetric A22)
     double acc = 0.0;
     if (lane < m) {
-#pragma unroll 4
-      for (int r = 0; r < m; ++r) acc = fma(A22[r * JLD + lane], v[r], acc);
+      const double* col = A22 + lane;
+      int r = 0;
+#pragma unroll 1
+      for (; r + TB <= m; r += TB) {
+        double a[TB], x[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          a[k] = col[(r + k) * JLD];
+          x[k] = vp[r + k].x;
+        }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) acc = fma(a[k], x[k], acc);
+      }
+      {
+        double a[TB], x[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          const bool in = r + k < m;
+          a[k] = in ? col[(r + k) * JLD] : 0.0;
+          x[k] = in ? vp[r + k].x : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < TB; ++k)
+          if (r + k < m) acc = fma(a[k], x[k], acc);
+      }
     }
+    TSEG(2);
     const double pl = tau * acc;
     const double alpha2 = -0.5 * tau * warp_sum_all(lane < m ? pl * vl : 0.0);
     const double wl = fma(alpha2, vl, pl);  // w[lane]
-    if (lane < m) p[lane] = wl;
+    if (lane < m) vp[lane].y = wl;
     __syncwarp();
+    TSEG(3);
     // A22 -= v w^T + w v^T (column `lane`, rows 0..m-1; elementwise symmetric)
     if (lane < m) {
-#pragma unroll 4
-      for (int r = 0; r < m; ++r) {
-        double* a = A22 + r * JLD + lane;
-        *a = *a - (v[r] * wl + p[r] * vl);
+      double* col = A22 + lane;
+#pragma unroll 1
+      for (int r = 0; r < m; r += TB) {
+        double a[TB];
+        double2 q[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          const bool in = r + k < m;
+          a[k] = in ? col[(r + k) * JLD] : 0.0;
+          q[k] = in ? vp[r + k] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) a[k] = a[k] - (q[k].x * wl + q[k].y * vl);
+#pragma unroll
+        for (int k = 0; k < TB; ++k)
+          if (r + k < m) col[(r + k) * JLD] = a[k];
       }
     }
     __syncwarp();
+    TSEG(4);
   }
+#ifdef SSCG_CONDTIME
+  if (n == 25 && lane == 0) printf("tridiag segs norm=%lld scal=%lld matvec=%lld red2=%lld upd=%lld\n", tseg[0], tseg[1], tseg[2], tseg[3], tseg[4]);
+#endif
   for (int r = lane; r < n; r += 32) d[r] = A[r * JLD + r];
   __syncwarp();
 }
@@ -371,10 +437,13 @@ __device__ double group_eig_index(const double* d, const double* e2, int n, int 
 // A is destroyed.  scratch: >= 4 * CMAX doubles.
 __device__ double warp_cond_estimate(double* A, int n, double* scratch, bool dup_floor) {
   const int lane = threadIdx.x & 31;
+  // d[33] | e[32] | (pad to 16 bytes) vp[33] as (v, w) pairs; v's storage holds
+  // the squared off-diagonals afterwards
   double* d = scratch;
   double* e = scratch + CMAX;
-  double* v = scratch + 2 * CMAX;
-  double* p = scratch + 3 * CMAX;
+  double* v = scratch + 2 * CMAX - 1;
+  if ((size_t)v & 15) v += 1;
+  double2* vp = reinterpret_cast<double2*>(v);
   if (n == 1) {
     const double a = A[0];
     return (a <= 0.0) ? INFINITY : (fabs(a) == 0.0 ? INFINITY : 1.0);
@@ -382,7 +451,7 @@ __device__ double warp_cond_estimate(double* A, int n, double* scratch, bool dup
 #ifdef SSCG_CONDTIME
   const long long ct0 = clock64();
 #endif
-  warp_tridiag(A, n, d, e, v, p);
+  warp_tridiag(A, n, d, e, vp);
 #ifdef SSCG_CONDTIME
   const long long ct1 = clock64();
 #endif
@@ -486,8 +555,21 @@ __device__ void cta_nested_conds_from(const double* G, int ldg, int s_bar, doubl
   double* A = jac + (size_t)warp * (CMAX * JLD + 4 * CMAX);
   double* rot = A + CMAX * JLD;
   if (warp == w0 && lane == 0) conds[0] = NAN;
-  // largest blocks first: they set the critical path
-  for (int i = s_bar - (warp - w0); i >= 1; i -= NW - w0) {
+  // largest blocks first: they set the critical path.  The estimates are bound
+  // by the fp64 pipe of the warp's SM sub-partition (warp & 3), which the warps
+  // of a sub-partition share: the three largest blocks each get a sub-partition
+  // (nearly) to themselves, the rest are dealt out by remaining work.
+#if SSCG_CONDS_SPREAD
+  int rank = warp - w0;
+  if (w0 == 1 && NW == 16) {
+    // rank (0 = largest block) of warps 1 .. 15
+    const int rk[16] = {0, 0, 1, 2, 3, 12, 7, 5, 4, 13, 9, 8, 6, 14, 10, 11};
+    rank = rk[warp];
+  }
+#else
+  const int rank = warp - w0;
+#endif
+  for (int i = s_bar - rank; i >= 1; i -= NW - w0) {
     const int n = 2 * i + 1;
     for (int e = lane; e < n * n; e += 32) {
       const int a = e / n, b = e % n;
@@ -1451,10 +1533,16 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
       }
     }
     if (lane == 0) {
+      // the state's scalars in one go (each load after a store would be its own
+      // round trip to L2)
+      const int k = st->k;
+      const int n_outer = st->total_outer;
+      const int pkind = st->prm.kind;
+      const bool pfrom = st->prm.has_from;
+      const double plo = st->prm.lo, phi_ = st->prm.hi;
       st->rz = R.rz[j_done];
       // trace.mark_outer + record (adaptive.py:178, 232-246)
-      const int k = st->k;
-      st->total_outer += 1;
+      st->total_outer = n_outer + 1;
       st->total_iters = mark + j_done;
       st->diag_base = mark;
       st->diag_n = cf.trace_full ? j_done : 0;
@@ -1468,12 +1556,12 @@ __global__ void __launch_bounds__(NT, 1) k_small(Ctx c) {
         ri[SSCG_REC_SACTUAL] = j_done;
         ri[SSCG_REC_BREAKJ] = brk_j;
         ri[SSCG_REC_MARK] = mark;
-        ri[SSCG_REC_PKIND] = st->prm.kind;
+        ri[SSCG_REC_PKIND] = pkind;
         rd[SSCG_RECD_PHI] = phi;
         rd[SSCG_RECD_BLHS] = brk_l;
         rd[SSCG_RECD_BRHS] = brk_r;
-        rd[SSCG_RECD_GEN_LO] = st->prm.has_from ? st->prm.lo : NAN;
-        rd[SSCG_RECD_GEN_HI] = st->prm.has_from ? st->prm.hi : NAN;
+        rd[SSCG_RECD_GEN_LO] = pfrom ? plo : NAN;
+        rd[SSCG_RECD_GEN_HI] = pfrom ? phi_ : NAN;
         rd[SSCG_RECD_TRUE] = S.sc[SC_TRUE];
         rd[SSCG_RECD_RREL] = S.sc[SC_RREL];
         rd[SSCG_RECD_C] = S.sc[SC_CSEL];
