@@ -121,8 +121,9 @@ struct Ctx {
   double* part_r;   // [RED_BLOCKS] ||r||^2 partials
   double* part_d;   // [3][RED_BLOCKS] full-trace partials
   double* part_g;   // [GRAM_BLOCKS][GPACK] Gram partials
-  double* leja_obj; // [4 leja_grid] grid objective + pairwise-sum state (small.cu leja_obj_point)
+  double* leja_obj; // [leja_scratch_doubles] grid objective (two copies) + pairwise-sum state + candidates (small.cu)
   int leja_grid_host;  // cfg->leja_grid as the host knew it at launch / capture
+  int leja_split;      // a Leja step as k_leja_grid + k_leja_pick (small operators) or one k_leja_point
   // logs (device)
   double* it_log;   // [cap_iters][SSCG_IT_N]
   int* rec_i;       // [cap_outer][SSCG_REC_NI]
@@ -389,6 +390,7 @@ void launch_hscg_p(const Ctx& c, double* P, double* R, cudaStream_t s);
 void launch_hscg_final(const Ctx& c, const double* R, cudaStream_t s);
 void launch_hscg_final_row(const Ctx& c, cudaStream_t s);
 void launch_leja_point(const Ctx& c, int n, cudaStream_t s);
+size_t leja_scratch_doubles(int grid);  // Ctx::leja_obj's size (zeroed at allocation)
 size_t small_smem_bytes();
 // dist.cu
 int nccl_load(const char* path);

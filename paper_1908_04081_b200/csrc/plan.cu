@@ -87,6 +87,7 @@ struct sscg_plan {
   cudaStream_t side = nullptr;  // Leja branch of the outer-loop graph
   cudaEvent_t ev_fork = nullptr;
   int leja_after0 = 1;  // the head chain forks after level 0
+  int leja_split = 0;   // small operators: a Leja step over many small CTAs (the chain is their critical path)
   int hs_ss = 1;        // HSCG row sums through the superset mask
   cudaEvent_t ev_leja[SMAX] = {};
   cudaGraphExec_t gexec = nullptr;
@@ -227,7 +228,8 @@ int ensure_work(sscg_plan* p, int sigma, int64_t max_outer, int leja_grid) {
     }
   }
   if (leja_grid > p->leja_cap) {
-    TRY(dalloc(p, &p->d_leja, 4 * (size_t)leja_grid));  // objective + pairwise-sum state
+    TRY(dalloc(p, &p->d_leja, leja_scratch_doubles(leja_grid)));  // objective + pairwise-sum state + candidates
+    CUDA_OK(cudaMemsetAsync(p->d_leja, 0, 8 * leja_scratch_doubles(leja_grid), p->stream));  // the candidate count
     p->leja_cap = leja_grid;
     if (p->gexec) {
       cudaGraphExecDestroy(p->gexec);
@@ -275,6 +277,7 @@ Ctx make_ctx(sscg_plan* p) {
   c.part_g = p->d_part_g;
   c.leja_obj = p->d_leja;
   c.leja_grid_host = p->cfg.leja_grid;
+  c.leja_split = p->leja_split;
   c.it_log = p->d_it;
   c.rec_i = p->d_ri;
   c.rec_d = p->d_rd;
@@ -709,6 +712,10 @@ int plan_init(sscg_plan* p, int32_t device, int64_t n_rows, int64_t n_own, int64
   // (c5w: 197.1 vs 198.6 ms; c1, whose levels are shorter than a Leja point,
   // is faster with the fork before level 0: 9.43 vs 9.58 ms)
   p->leja_after0 = atoi(env_or("SSCG_LEJA_AFTER0", n_rows >= ((int64_t)1 << 20) ? "1" : "0")) != 0;
+  // beside the level kernels of a large operator the many-CTA grid pass takes
+  // SM slots of the next level's single wave (c5w +3 %); there the chain is
+  // hidden behind the levels anyway
+  p->leja_split = atoi(env_or("SSCG_LEJA_SPLIT", n_rows >= ((int64_t)1 << 20) ? "0" : "1")) != 0;
   return rc;
 }
 

@@ -828,6 +828,9 @@ __device__ unsigned long long g_leja_dbg[8];
 // beside the running sum: A = r0+r1 (n = 2), then (r0+r1)+(r2+r3) (n = 4);
 // B = r4+r5 (n = 6); T = the odd term waiting for its pair (n = 3, 5, 7).
 // st = the grid point's slot in the state arrays [A | B | T], each `grid` long.
+// OWN = false: the value only (a neighbour CTA's copy of a point it does not
+// own, k_leja_grid) -- the same expressions, no state update.
+template <bool OWN = true>
 __device__ __forceinline__ double leja_obj_point(double x, double prev, int n, const double* pts,
                                                  double* st, int grid) {
   if (n == 2) {
@@ -835,22 +838,26 @@ __device__ __forceinline__ double leja_obj_point(double x, double prev, int n, c
     double o = 0.0;
     o += r0;
     o += r1;
-    st[0] = r0 + r1;
+    if (OWN) st[0] = r0 + r1;
     return o;
   }
   const double r = log(fabs(x - pts[n - 1]) + 1e-300);
-  switch (n) {
-    case 3:
-    case 5:
-    case 7: st[2 * grid] = r; break;
-    case 4: st[0] = st[0] + (st[2 * grid] + r); break;
-    case 6: st[grid] = st[2 * grid] + r; break;
-    case 8: return st[0] + (st[grid] + (st[2 * grid] + r));
-    default: break;
+  if (n == 8) return st[0] + (st[grid] + (st[2 * grid] + r));
+  if (OWN) {
+    switch (n) {
+      case 3:
+      case 5:
+      case 7: st[2 * grid] = r; break;
+      case 4: st[0] = st[0] + (st[2 * grid] + r); break;
+      case 6: st[grid] = st[2 * grid] + r; break;
+      default: break;
+    }
   }
   return prev + r;
 }
 
+__device__ void cta_leja_pick(double lo, double hi, int n, int grid, const double* ob,
+                              LejaShared& L);
 // sobj: the objective in shared memory as well (k_leja_point, grid <=
 // LEJA_SMEM_GRID) -- the scans then read no global memory; nullptr: global only
 __device__ void cta_leja_point(double lo, double hi, int n, int grid, double* obj,
@@ -901,6 +908,20 @@ __device__ void cta_leja_point(double lo, double hi, int n, int grid, double* ob
   }
   __syncthreads();
   LDBG(1);
+  cta_leja_pick(lo, hi, n, grid, ob, L);
+}
+
+// The second half of a greedy Leja step: the candidates (L.cand / L.cval /
+// L.ncand, any order) -> pts[n].  ob: the grid objective (read only when there
+// is no interior local maximum).  CTA-wide, at least 4 warps.
+__device__ void cta_leja_pick(double lo, double hi, int n, int grid, const double* ob,
+                              LejaShared& L) {
+#ifdef LEJA_DBG
+  long long t_prev__ = clock64();
+#endif
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const double step = (hi - lo) / (double)(grid - 1);
+  const bool zero_step = (step == 0.0);
   if (tid == 0) {
     int nc = L.ncand < LEJA_CAND_CAP ? L.ncand : LEJA_CAND_CAP;
     if (nc == 0) {  // np.argmax: first maximal index
@@ -1669,6 +1690,90 @@ __global__ void __launch_bounds__(NT) k_leja_point(Ctx c, int n) {
   TL_END(c, 20 + n);
 }
 
+// The same step as two launches (the outer-loop graph's form): the grid
+// objective and its local maxima over many small CTAs -- one grid point per
+// thread, so the step's 10^4 logs are one log deep instead of twenty -- then
+// one CTA that sorts the candidates and refines the best four.  Scratch layout
+// (doubles): [obj_a | A | B | T | obj_b | cand values | cand indices | count];
+// the objective ping-pongs between obj_a and obj_b from step to step: a CTA
+// also evaluates the two points beside its chunk (their values decide its edge
+// maxima), reading their previous objective while the owner writes the new one.
+constexpr int LG_T = 128;          // threads = points evaluated per CTA
+constexpr int LG_OWN = LG_T - 2;   // of which it owns (stores, scans) this many
+__device__ __forceinline__ double* leja_cand_val(double* base, int grid) { return base + 5 * (size_t)grid; }
+__device__ __forceinline__ int* leja_cand_idx(double* base, int grid) {
+  return reinterpret_cast<int*>(base + 5 * (size_t)grid + LEJA_CAND_CAP);
+}
+__device__ __forceinline__ int* leja_cand_count(double* base, int grid) {
+  return leja_cand_idx(base, grid) + LEJA_CAND_CAP;
+}
+__global__ void __launch_bounds__(LG_T) k_leja_grid(Ctx c, int n) {
+  __shared__ double so[LG_T];
+  __shared__ double pts[SMAX];
+  SolverState* st = c.st;
+  if (!st->leja_on || n >= c.cfg->sigma) return;
+  const int grid = c.cfg->leja_grid;
+  const int t = threadIdx.x;
+  if (t < n) pts[t] = st->prm.th[t];
+  __syncthreads();
+  const double lo = st->prm.lo, hi = st->prm.hi;
+  const double step = (hi - lo) / (double)(grid - 1);
+  const bool zero_step = (step == 0.0);
+  double* base = c.leja_obj;
+  const double* oin = base + ((n & 1) ? 4 * (size_t)grid : 0);
+  double* oout = base + ((n & 1) ? 0 : 4 * (size_t)grid);
+  const int c0 = blockIdx.x * LG_OWN;  // first owned point; slot t <-> point c0 - 1 + t
+  const int i = c0 - 1 + t;
+  const bool own = t >= 1 && t <= LG_OWN && i < grid;
+  if (i >= 0 && i < grid) {
+    const double prev = (n != 2 && n != 8) ? oin[i] : 0.0;  // n = 8 restarts from the tree
+    const double x = lin_x(i, grid, lo, hi, step, zero_step);
+    double o;
+    if (own) {
+      o = leja_obj_point<true>(x, prev, n, pts, base + grid + i, grid);
+      oout[i] = o;
+    } else {
+      o = leja_obj_point<false>(x, prev, n, pts, base + grid + i, grid);
+    }
+    so[t] = o;
+  }
+  __syncthreads();
+  // interior local maxima (>= both neighbours) among the owned points
+  if (own && i >= 1 && i < grid - 1) {
+    const double v = so[t];
+    if (v >= so[t - 1] && v >= so[t + 1]) {
+      const int slot = atomicAdd(leja_cand_count(base, grid), 1);
+      if (slot < LEJA_CAND_CAP) {
+        leja_cand_idx(base, grid)[slot] = i;
+        leja_cand_val(base, grid)[slot] = v;
+      }
+    }
+  }
+}
+__global__ void __launch_bounds__(128) k_leja_pick(Ctx c, int n) {
+  __shared__ LejaShared L;
+  SolverState* st = c.st;
+  if (!st->leja_on || n >= c.cfg->sigma) return;
+  TL_K(c, 0);
+  TL_BEGIN(c, 20 + n);
+  const int grid = c.cfg->leja_grid;
+  double* base = c.leja_obj;
+  int* cnt = leja_cand_count(base, grid);
+  const int nc_all = *cnt;
+  const int nc = nc_all < LEJA_CAND_CAP ? nc_all : LEJA_CAND_CAP;
+  if (threadIdx.x < n) L.pts[threadIdx.x] = st->prm.th[threadIdx.x];
+  for (int a = threadIdx.x; a < nc; a += blockDim.x) {
+    L.cand[a] = leja_cand_idx(base, grid)[a];
+    L.cval[a] = leja_cand_val(base, grid)[a];
+  }
+  if (threadIdx.x == 0) L.ncand = nc_all;
+  __syncthreads();
+  if (threadIdx.x == 0) *cnt = 0;  // for the next step's k_leja_grid
+  cta_leja_pick(st->prm.lo, st->prm.hi, n, grid, base + ((n & 1) ? 0 : 4 * (size_t)grid), L);
+  if (threadIdx.x == 0) st->prm.th[n] = L.pts[n];
+  TL_END(c, 20 + n);
+}
+
 // full trace: reduce the diag partials of inner iteration j into the log
 __global__ void __launch_bounds__(NT) k_diag_fin(Ctx c, int j) {
   __shared__ double red[NT];
@@ -1846,9 +1951,15 @@ void launch_leja_point(const Ctx& c, int n, cudaStream_t s) {
   // the grid objective in shared memory when it fits (sized from the host's
   // leja_grid, known at capture: the plan rebuilds its graph when it changes)
   const int grid = c.leja_grid_host;
-  const size_t bytes = grid <= LEJA_SMEM_GRID ? 8 * (size_t)grid : 0;
-  k_leja_point<<<1, NT, bytes, s>>>(c, n);
+  if (c.leja_split) {
+    k_leja_grid<<<(grid + LG_OWN - 1) / LG_OWN, LG_T, 0, s>>>(c, n);
+    k_leja_pick<<<1, 128, 0, s>>>(c, n);
+  } else {
+    const size_t bytes = grid <= LEJA_SMEM_GRID ? 8 * (size_t)grid : 0;
+    k_leja_point<<<1, NT, bytes, s>>>(c, n);
+  }
 }
+size_t leja_scratch_doubles(int grid) { return 5 * (size_t)grid + 2 * LEJA_CAND_CAP + 8; }
 
 // ---- unit entry helpers (synchronous, own allocations) ----------------------
 #define U_OK(expr)                                   \
