@@ -334,6 +334,8 @@ def run_single(args):
     prob = problems.make_problem(key, scale=args.scale)
     t_gen = time.perf_counter() - t0
     cfg_kw = dict(sigma=sigma, eps_star=eps, basis_kind=basis)
+    if os.environ.get("SSCG_BENCH_LEJA_GRID"):  # experiments only (another grid = other shifts)
+        cfg_kw["leja_grid"] = int(os.environ["SSCG_BENCH_LEJA_GRID"])
     n, nnz = prob.a.n, prob.a.nnz
     # first call through the public API on a matrix with no cached plan: plan
     # creation (upload, pattern compression) + the solve, host buffers in / out

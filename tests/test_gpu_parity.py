@@ -160,6 +160,28 @@ def test_leja_and_params(gpu_ready):
         np.testing.assert_array_equal(pr.mus, dp[f"c{i}_mus"])
 
 
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_graph_leja_forms_match_the_unit_entry(gpu_ready, split, monkeypatch):
+    """The outer-loop graph computes a Leja point either by one CTA (large
+    operators) or as k_leja_grid + k_leja_pick (small ones): both must return
+    the bits of the unit entry leja_points (basis.py:91-127) for the interval
+    each block's parameters were generated from."""
+    monkeypatch.setenv("SSCG_LEJA_SPLIT", split)  # read at plan creation
+    prob = problems.make_problem("c1", scale=24)   # a fresh matrix: a fresh plan
+    _, tr, _ = adaptive_solve(prob, AdaptiveConfig(sigma=8, eps_star=1e-10, basis_kind="newton"),
+                              trace="fast")
+    assert tr.converged
+    seen = 0
+    for rec in tr.outer_records:
+        bp = rec.basis_params_used
+        if bp.kind != "newton" or bp.generated_from is None:
+            continue
+        lo, hi = bp.generated_from
+        np.testing.assert_array_equal(np.asarray(bp.thetas), leja_points(lo, hi, 8))
+        seen += 1
+    assert seen >= 3
+
+
 def test_ritz_device_bitwise(gpu_ready):
     d = golden("ritz")
     for i in range(int(d["nseq"])):
