@@ -562,9 +562,9 @@ __device__ void cta_nested_conds_from(const double* G, int ldg, int s_bar, doubl
 #if SSCG_CONDS_SPREAD
   int rank = warp - w0;
   if (w0 == 1 && NW == 16) {
-    // rank (0 = largest block) of warps 1 .. 15
-    const int rk[16] = {0, 0, 1, 2, 3, 12, 7, 5, 4, 13, 9, 8, 6, 14, 10, 11};
-    rank = rk[warp];
+    // rank (0 = largest block) of warps 1 .. 15, a nibble per warp:
+    // {-, 0, 1, 2, 3, 12, 7, 5, 4, 13, 9, 8, 6, 14, 10, 11}
+    rank = (int)((0xbae689d457c32100ull >> (4 * warp)) & 15ull);
   }
 #else
   const int rank = warp - w0;
@@ -638,8 +638,12 @@ __device__ __forceinline__ double np_sum_warp(double term, int n) {
   for (int j = 0; j < 8; ++j) r[j] = __shfl_sync(0xffffffffu, term, j);
   double res;
   if (n < 8) {
+    // predicated adds on registers (a loop to n would index r[] dynamically and
+    // put it in local memory: eight stores and n dependent loads per call)
     res = 0.0;
-    for (int j = 0; j < n; ++j) res += r[j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < n) res += r[j];
   } else {
     res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
     for (int j = 8; j < n; ++j) res += __shfl_sync(0xffffffffu, term, j);
@@ -697,13 +701,18 @@ __device__ __forceinline__ double np_sum_group(double term, int n, int base) {
   double res;
   if (n < 8) {
     res = 0.0;
-    for (int j = 0; j < n; ++j) res += r[j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < n) res += r[j];
   } else {
     res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
     for (int j = 8; j < n; ++j) res += __shfl_sync(0xffffffffu, term, base + j);
   }
   return res;
 }
+#ifdef LEJA_DBG
+__device__ unsigned long long g_leja_dbg2[4];
+#endif
 __device__ void golden_refine2(const double* pts_, int n, double lo, double hi, double* xo,
                                double* vo) {
   constexpr int G = 10;
@@ -726,7 +735,14 @@ __device__ void golden_refine2(const double* pts_, int n, double lo, double hi, 
   double fc, fd, unused;
   eval3(c, d, d, fc, fd, unused);
   int it = 0;
+#ifdef LEJA_DBG
+  const long long tg0 = clock64();
+  int rounds = 0;
+#endif
   while (it < 80) {
+#ifdef LEJA_DBG
+    ++rounds;
+#endif
     if (b - a <= 1e-14 * py_max(py_max(fabs(a), fabs(b)), 1.0)) break;
     // this step (comparison known): the new point x1
     const bool up = fc > fd;
@@ -777,6 +793,13 @@ __device__ void golden_refine2(const double* pts_, int n, double lo, double hi, 
     }
     ++it;
   }
+#ifdef LEJA_DBG
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_leja_dbg2[0], (unsigned long long)(clock64() - tg0));
+    atomicAdd(&g_leja_dbg2[1], (unsigned long long)rounds);
+    atomicAdd(&g_leja_dbg2[2], 1ull);
+  }
+#endif
   const double x = 0.5 * (a + b);
   double v;
   eval3(x, x, x, v, unused, unused);
@@ -2073,6 +2096,14 @@ double sscg_host_c0() { return host_c0(); }
 extern "C" int sscg_debug_leja(unsigned long long* out8) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out8, g_leja_dbg, sizeof(unsigned long long) * 8);
+  {
+    unsigned long long g2[4];
+    cudaMemcpyFromSymbol(g2, g_leja_dbg2, sizeof(g2));
+    out8[5] = g2[0];  // cycles inside golden_refine2's loop (warp 0)
+    out8[6] = g2[1];  // its rounds
+    const unsigned long long z2[4] = {};
+    cudaMemcpyToSymbol(g_leja_dbg2, z2, sizeof(z2));
+  }
   const unsigned long long z[8] = {};
   cudaMemcpyToSymbol(g_leja_dbg, z, sizeof(z));
   return (int)cudaGetLastError();
