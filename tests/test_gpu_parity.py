@@ -160,6 +160,42 @@ def test_leja_and_params(gpu_ready):
         np.testing.assert_array_equal(pr.mus, dp[f"c{i}_mus"])
 
 
+def _cond_numpy(g, s_bar, i):
+    cols = list(range(i + 1)) + list(range(s_bar + 1, s_bar + 1 + i))
+    w = np.linalg.eigvalsh(g[np.ix_(cols, cols)])  # lacore.py:103-117
+    if w.max() <= 0 or np.min(np.abs(w)) == 0:
+        return np.inf
+    return np.sqrt(w.max() / np.min(np.abs(w)))
+
+
+@pytest.mark.parametrize("kind", ["definite", "indefinite", "negative"])
+def test_nested_conds_search_groups(gpu_ready, kind):
+    """The eigenvalue searches of a nested block run on lane groups in lockstep:
+    two groups of 16 lanes when the block is definite (lambda_max and one
+    eigenvalue next to 0), three of 10 when it has eigenvalues on both sides of
+    0.  Well-separated spectra, so the estimate is resolvable: 1e-9 against
+    eigvalsh (lacore.py:103-117, 135-148), inf where lambda_max <= 0."""
+    rng = np.random.default_rng(5)
+    for s_bar in (3, 8, 12, 16):
+        n = 2 * s_bar + 1
+        q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        lam = np.exp(rng.uniform(np.log(1e-3), np.log(10.0), n))
+        if kind == "indefinite":
+            lam[::3] *= -1.0
+        elif kind == "negative":
+            lam = -lam
+        g = (q * lam) @ q.T
+        g = 0.5 * (g + g.T)
+        got = nested_basis_conds(g, s_bar)
+        assert np.isnan(got[0])
+        for i in range(1, s_bar + 1):
+            ref = _cond_numpy(g, s_bar, i)
+            if np.isinf(ref):
+                assert np.isinf(got[i]), (kind, s_bar, i, got[i])
+            else:
+                assert abs(got[i] - ref) <= 1e-9 * ref, (kind, s_bar, i, got[i], ref)
+
+
 @pytest.mark.parametrize("split", ["0", "1"])
 def test_graph_leja_forms_match_the_unit_entry(gpu_ready, split, monkeypatch):
     """The outer-loop graph computes a Leja point either by one CTA (large
