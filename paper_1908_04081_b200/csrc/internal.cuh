@@ -196,6 +196,7 @@ struct Ctx {
   unsigned* zm_ctr;  // [2 (SMAX + 1)] per-level claim / done counters (levels >= 1), or NULL
   const int* zm_base;  // [zm_np] first local row of each plane (partitioned), or NULL (z * S)
   int zm_o;          // 2-D column tiles with line stride zm_o (0: 256 consecutive columns)
+  int tm_exact;      // every off-centre pattern value is 0 or +-1: v * x is exact, one fma per term gives the mul + add bits
   // TMA plane march (tmarch.cu; tm == nullptr: the register march): host
   // pointer to the plan's tensor maps (passed to the kernel by value)
   const TmMaps* tm;

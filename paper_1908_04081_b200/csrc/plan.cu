@@ -163,6 +163,7 @@ struct sscg_plan {
   int* d_vs_geo = nullptr;   // vs_below
   int* d_vs_base = nullptr;  // vs_above
   int ss_ne = 0;  // superset-mask form (superset_setup); 0: table-walking kernels
+  int ss_exact = 0;  // its off-centre values are all 0 or +-1 (products exact)
   int ss_off[SS_MAX_NE] = {};
   unsigned* d_ss_mask = nullptr;
   double* d_ss_val = nullptr;
@@ -314,6 +315,7 @@ Ctx make_ctx(sscg_plan* p) {
   c.zm_base = p->d_zm_base;
   c.zm_ctr = p->d_zm_ctr;
   c.zm_o = p->zm_o;
+  c.tm_exact = p->ss_exact;
   c.vs_ne = p->vs_ne;
   for (int k = 0; k < VS_MAX_NE; ++k) c.vs_off[k] = p->vs_off[k];
   c.vs_val = p->d_vs_val;
@@ -974,6 +976,14 @@ int pattern_setup(sscg_plan* p, int64_t n_rows, const int64_t* row_ptr, const in
       CUDA_OK(cudaMemcpy(p->d_ss_mask, mask.data(), 4 * mask.size(), cudaMemcpyHostToDevice));
       CUDA_OK(cudaMemcpy(p->d_ss_val, sval.data(), 8 * sval.size(), cudaMemcpyHostToDevice));
       p->ss_ne = (int)uni.size();
+      // Poisson-like operators: a product with 0 or +-1 is exact, so the march
+      // may fuse it into its add (same bits as csr_matvec's mul then add)
+      p->ss_exact = atoi(env_or("SSCG_TM_EXACT", "1")) != 0;
+      for (int q = 0; q < np && p->ss_exact; ++q)
+        for (int k = 0; k < (int)uni.size(); ++k) {
+          const double v = sval[(size_t)q * SS_MAX_NE + k];
+          if (uni[(size_t)k] != 0 && !(v == 0.0 || v == 1.0 || v == -1.0)) p->ss_exact = 0;
+        }
       for (int k = 0; k < SS_MAX_NE; ++k) p->ss_off[k] = k < p->ss_ne ? uni[(size_t)k] : 0;
       p->red_n = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms * socc[0], (int64_t)RED_BLOCKS, tiles}));
       p->pat_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * socc[1], tiles));

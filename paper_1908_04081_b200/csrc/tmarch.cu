@@ -156,7 +156,7 @@ __device__ __forceinline__ void tm_item(const Ctx& c, int it, int ncb, int& cb, 
   z1 = min(z0 + zcs, c.zm_np);
 }
 
-template <int NV, bool L0, int RK>
+template <int NV, bool L0, int RK, bool EX>
 __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, const TmMaps& maps,
                                         const TmShared& sh, bool dyn, bool do_r) {
   constexpr bool UNIT = (RK & 1) == 0, MU = (RK & 2) != 0 && !L0;
@@ -307,7 +307,14 @@ __device__ __forceinline__ void tm_body(const Ctx& c, int l, const ZmPtrs& zp, c
                               lds_f64(bx + 8), lds_f64(bx + 8 * TM_W), nn[q]};
         double a = 0.0;
 #pragma unroll
-        for (int kk = 0; kk < 7; ++kk) a = __dadd_rn(a, __dmul_rn(v[kk], xb[kk]));
+        for (int kk = 0; kk < 7; ++kk) {
+          // EX: the off-centre values are 0 or +-1 (Ctx::tm_exact), their
+          // products exact -- fma(v, x, a) is csr_matvec's a + v * x bit for bit
+          if (EX && kk != 3)
+            a = fma(v[kk], xb[kk], a);
+          else
+            a = __dadd_rn(a, __dmul_rn(v[kk], xb[kk]));
+        }
         acc[q] = a;
       }
       if (L0 && r < n_own) {
@@ -437,10 +444,17 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB)
   TL_BEGIN(c, l);
   if (L0) {
     const bool do_r = sbar >= 2;
-    if (st->prm.ga[0] == 1.0)
-      tm_body<3, true, 0>(c, 0, zp, maps, sh, false, do_r);
-    else
-      tm_body<3, true, 1>(c, 0, zp, maps, sh, false, do_r);
+    if (st->prm.ga[0] == 1.0) {
+      if (c.tm_exact)
+        tm_body<3, true, 0, true>(c, 0, zp, maps, sh, false, do_r);
+      else
+        tm_body<3, true, 0, false>(c, 0, zp, maps, sh, false, do_r);
+    } else {
+      if (c.tm_exact)
+        tm_body<3, true, 1, true>(c, 0, zp, maps, sh, false, do_r);
+      else
+        tm_body<3, true, 1, false>(c, 0, zp, maps, sh, false, do_r);
+    }
     TL_END(c, 0);
     return;
   }
@@ -449,17 +463,25 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB)
   const int rk = (ga == 1.0 ? 0 : 1) | (use_mu ? 2 : 0);
   const bool do_r = l < sbar - 1;
   const bool dyn = c.zm_ctr != nullptr && st->leja_on;
-#define TM_RK(NV)                                                      \
-  switch (rk) {                                                        \
-    case 0: tm_body<NV, false, 0>(c, l, zp, maps, sh, dyn, do_r); break; \
-    case 1: tm_body<NV, false, 1>(c, l, zp, maps, sh, dyn, do_r); break; \
-    case 2: tm_body<NV, false, 2>(c, l, zp, maps, sh, dyn, do_r); break; \
-    default: tm_body<NV, false, 3>(c, l, zp, maps, sh, dyn, do_r); break; \
+#define TM_RK(NV, EX)                                                      \
+  switch (rk) {                                                            \
+    case 0: tm_body<NV, false, 0, EX>(c, l, zp, maps, sh, dyn, do_r); break; \
+    case 1: tm_body<NV, false, 1, EX>(c, l, zp, maps, sh, dyn, do_r); break; \
+    case 2: tm_body<NV, false, 2, EX>(c, l, zp, maps, sh, dyn, do_r); break; \
+    default: tm_body<NV, false, 3, EX>(c, l, zp, maps, sh, dyn, do_r); break; \
   }
-  if (do_r) {
-    TM_RK(2)
+  if (c.tm_exact) {
+    if (do_r) {
+      TM_RK(2, true)
+    } else {
+      TM_RK(1, true)
+    }
   } else {
-    TM_RK(1)
+    if (do_r) {
+      TM_RK(2, false)
+    } else {
+      TM_RK(1, false)
+    }
   }
 #undef TM_RK
   TL_END(c, l);
