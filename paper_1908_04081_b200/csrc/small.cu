@@ -712,6 +712,7 @@ __device__ __forceinline__ double np_sum_group(double term, int n, int base) {
 }
 #ifdef LEJA_DBG
 __device__ unsigned long long g_leja_dbg2[4];
+__device__ unsigned long long g_leja_dbg[8];
 #endif
 __device__ void golden_refine2(const double* pts_, int n, double lo, double hi, double* xo,
                                double* vo) {
@@ -720,13 +721,25 @@ __device__ void golden_refine2(const double* pts_, int n, double lo, double hi, 
   const int base = grp * G;
   const double pl = gl < n ? pts_[gl] : 0.0;  // this lane's point (every group holds them all)
   // objective at x0 / x1 / x2 in groups 0 / 1 / 2; every lane returns all three
+#ifdef LEJA_DBG
+  long long tsec[4] = {0, 0, 0, 0};
+#define GSEC(k, t0_) do { const long long t1_ = clock64(); tsec[k] += t1_ - (t0_); (t0_) = t1_; } while (0)
+#else
+#define GSEC(k, t0_)
+#endif
   auto eval3 = [&](double x0, double x1, double x2, double& f0, double& f1, double& f2) {
+#ifdef LEJA_DBG
+    long long te = clock64();
+#endif
     const double x = grp == 0 ? x0 : grp == 1 ? x1 : x2;
     const double term = (gl < n && grp < 3) ? log(fabs(x - pl) + 1e-300) : 0.0;
+    GSEC(0, te);
     const double res = np_sum_group(term, n, base);
+    GSEC(1, te);
     f0 = __shfl_sync(0xffffffffu, res, 0);
     f1 = __shfl_sync(0xffffffffu, res, G);
     f2 = __shfl_sync(0xffffffffu, res, 2 * G);
+    GSEC(2, te);
   };
   const double ratio = (sqrt(5.0) - 1.0) / 2.0;
   double a = lo, b = hi;
@@ -798,6 +811,9 @@ __device__ void golden_refine2(const double* pts_, int n, double lo, double hi, 
     atomicAdd(&g_leja_dbg2[0], (unsigned long long)(clock64() - tg0));
     atomicAdd(&g_leja_dbg2[1], (unsigned long long)rounds);
     atomicAdd(&g_leja_dbg2[2], 1ull);
+    atomicAdd(&g_leja_dbg[0], (unsigned long long)tsec[0]);  // split builds leave slots 0, 1 free
+    atomicAdd(&g_leja_dbg[1], (unsigned long long)tsec[1]);
+    atomicAdd(&g_leja_dbg2[3], (unsigned long long)tsec[2]);
   }
 #endif
   const double x = 0.5 * (a + b);
@@ -830,7 +846,6 @@ __device__ __forceinline__ double lin_x(int i, int grid, double lo, double hi, d
 // scratch of 4 * grid doubles -- the objective and the pairwise-sum state of
 // leja_obj_point -- carried between calls), append pts[n].  CTA-wide.
 #ifdef LEJA_DBG
-__device__ unsigned long long g_leja_dbg[8];
 #define LDBG(i)                                                             \
   do {                                                                      \
     __syncthreads();                                                        \
@@ -2101,6 +2116,7 @@ extern "C" int sscg_debug_leja(unsigned long long* out8) {
     cudaMemcpyFromSymbol(g2, g_leja_dbg2, sizeof(g2));
     out8[5] = g2[0];  // cycles inside golden_refine2's loop (warp 0)
     out8[6] = g2[1];  // its rounds
+    out8[4] = g2[3];  // cycles in eval3's broadcasts (the tie phase's slot is overwritten)
     const unsigned long long z2[4] = {};
     cudaMemcpyToSymbol(g_leja_dbg2, z2, sizeof(z2));
   }

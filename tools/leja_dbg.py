@@ -12,3 +12,4 @@ print("points", n, "cycles/point:", {k: round(buf[i] / n) for i, k in enumerate(
 
 if buf[6]:
     print("golden_refine2 (warp 0): rounds", buf[6], "cycles per round", round(buf[5] / buf[6]))
+    print("per round: log", round(buf[0] / buf[6]), "group sum", round(buf[1] / buf[6]), "broadcasts", round(buf[4] / buf[6]))
