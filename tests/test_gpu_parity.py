@@ -196,16 +196,18 @@ def test_nested_conds_search_groups(gpu_ready, kind):
                 assert abs(got[i] - ref) <= 1e-9 * ref, (kind, s_bar, i, got[i], ref)
 
 
+@pytest.mark.parametrize("grid", [10_000, 257, 50])
 @pytest.mark.parametrize("split", ["0", "1"])
-def test_graph_leja_forms_match_the_unit_entry(gpu_ready, split, monkeypatch):
+def test_graph_leja_forms_match_the_unit_entry(gpu_ready, split, grid, monkeypatch):
     """The outer-loop graph computes a Leja point either by one CTA (large
     operators) or as k_leja_grid + k_leja_pick (small ones): both must return
     the bits of the unit entry leja_points (basis.py:91-127) for the interval
     each block's parameters were generated from."""
     monkeypatch.setenv("SSCG_LEJA_SPLIT", split)  # read at plan creation
     prob = problems.make_problem("c1", scale=24)   # a fresh matrix: a fresh plan
-    _, tr, _ = adaptive_solve(prob, AdaptiveConfig(sigma=8, eps_star=1e-10, basis_kind="newton"),
-                              trace="fast")
+    # grids that are not a multiple of a CTA's chunk, and one smaller than a chunk
+    _, tr, _ = adaptive_solve(prob, AdaptiveConfig(sigma=8, eps_star=1e-10, basis_kind="newton",
+                                                   leja_grid=grid), trace="fast")
     assert tr.converged
     seen = 0
     for rec in tr.outer_records:
@@ -213,7 +215,7 @@ def test_graph_leja_forms_match_the_unit_entry(gpu_ready, split, monkeypatch):
         if bp.kind != "newton" or bp.generated_from is None:
             continue
         lo, hi = bp.generated_from
-        np.testing.assert_array_equal(np.asarray(bp.thetas), leja_points(lo, hi, 8))
+        np.testing.assert_array_equal(np.asarray(bp.thetas), leja_points(lo, hi, 8, grid))
         seen += 1
     assert seen >= 3
 
