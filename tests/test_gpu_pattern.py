@@ -121,16 +121,17 @@ def test_pattern_kernel_forms(gpu_ready):
 
 @pytest.mark.parametrize("env", [{"SSCG_ZM": "0"}, {"SSCG_PAT_SS": "0"}, {"SSCG_ZM_ZC": "3"},
                                  {"SSCG_ZM_2D": "0"}, {"SSCG_ZM_DYN": "0"}, {"SSCG_TM": "0"},
-                                 {"SSCG_TM": "0", "SSCG_ZM_DYN": "0"}],
+                                 {"SSCG_TM": "0", "SSCG_ZM_DYN": "0"}, {"SSCG_TM_EXACT": "0"}],
                          ids=["superset", "table", "march_zc3", "march_1d", "static_items",
-                              "register_march", "register_march_static"])
+                              "register_march", "register_march_static", "tma_mul_then_add"])
 def test_pattern_forms_bit_identical(gpu_ready, env):
     """Plane march (default), its opt-in variants, superset mask and table
     walk run the same rounded operations in the same order: identical solves
     (Newton and Chebyshev bases, unit and non-unit gamma, mu != 0).  The 32^3
     grids give whole 32 x 8 column tiles: the default there is the TMA march,
     so the reference run and every variant compare the TMA-fed and register
-    marches too."""
+    marches too; the TMA march's exact-product form (one fma per 0 / +-1 entry,
+    the default on these Poisson operators) against its mul-then-add form."""
     for key, scale, kw in (("c5", 28, dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
                            ("c3", 24, dict(sigma=10, eps_star=1e-10, basis_kind="chebyshev")),
                            ("c5", 32, dict(sigma=12, eps_star=1e-10, basis_kind="newton")),
