@@ -17,10 +17,13 @@
 //                                  objective in numpy's pairwise-sum order, golden
 //                                  refinement, 1e-12 tie rule; Chebyshev mu = w/8)
 #include <cstdio>
+#include <cstdlib>
 #include <math.h>
 
 #include "internal.cuh"
 #include "ritz.cuh"
+
+void sync_golden_mode();  // SSCG_GOLDEN_SEQ -> the device flag (defined below)
 
 namespace {
 
@@ -823,6 +826,12 @@ __device__ void golden_refine2(const double* pts_, int n, double lo, double hi, 
   *vo = v;
 }
 
+// SSCG_GOLDEN_SEQ=1 (read when a plan is created / a unit entry runs): every
+// candidate is refined by golden_refine, one step at a time -- the form the
+// two-steps-per-round golden_refine2 is checked against bit for bit
+// (tests/test_gpu_parity.py)
+__device__ int g_golden_seq = 0;
+
 struct LejaShared {
   double pts[SMAX];
   double rx[4], rv[4];
@@ -1011,7 +1020,10 @@ __device__ void cta_leja_pick(double lo, double hi, int n, int grid, const doubl
     const int il = i - 1 > 0 ? i - 1 : 0;
     const int ih = i + 1 < grid - 1 ? i + 1 : grid - 1;
     double xr, vr;
-    if (n <= 10)
+    if (g_golden_seq)
+      golden_refine(L.pts, n, lin_x(il, grid, lo, hi, step, zero_step),
+                    lin_x(ih, grid, lo, hi, step, zero_step), &xr, &vr);
+    else if (n <= 10)
       golden_refine2(L.pts, n, lin_x(il, grid, lo, hi, step, zero_step),
                      lin_x(ih, grid, lo, hi, step, zero_step), &xr, &vr);
     else
@@ -1977,7 +1989,16 @@ double host_c0() { return pow(ldexp(1.0, -53), -0.5); }
 
 size_t small_smem_bytes() { return ((sizeof(SmallShared) + 7) / 8) * 8 + JAC_BYTES; }
 
-void small_prepare() { ensure_attr(); }
+// SSCG_GOLDEN_SEQ -> g_golden_seq on the current device
+void sync_golden_mode() {
+  const char* e = getenv("SSCG_GOLDEN_SEQ");
+  const int v = (e && atoi(e) != 0) ? 1 : 0;
+  cudaMemcpyToSymbol(g_golden_seq, &v, sizeof(int));
+}
+void small_prepare() {
+  ensure_attr();
+  sync_golden_mode();
+}
 
 void launch_state_init(const Ctx& c, cudaStream_t s) {
   k_state_init<<<1, NT, small_smem_bytes(), s>>>(c);
@@ -2034,6 +2055,7 @@ done:
 
 int unit_leja(double lo, double hi, int count, int grid, double* out) {
   ensure_attr();
+  sync_golden_mode();
   int rc = SSCG_OK;
   double *dout = nullptr, *obj = nullptr;
   U_OK(cudaMalloc(&dout, sizeof(double) * SMAX));
@@ -2050,6 +2072,7 @@ done:
 int unit_params_for(int kind, int s, int has, double lo, double hi, int grid, double* th,
                     double* ga, double* mu, int* kind_out) {
   ensure_attr();
+  sync_golden_mode();
   int rc = SSCG_OK;
   ParamsDev* dp = nullptr;
   double* obj = nullptr;

@@ -196,6 +196,27 @@ def test_nested_conds_search_groups(gpu_ready, kind):
                 assert abs(got[i] - ref) <= 1e-9 * ref, (kind, s_bar, i, got[i], ref)
 
 
+def test_golden_two_step_matches_sequential_golden_section(gpu_ready, monkeypatch):
+    """The refinement of a Leja candidate (basis.py:70-88) takes two
+    golden-section steps per round (three lane groups evaluate this step's point
+    and the next step's two possible points; up to 10 points);
+    SSCG_GOLDEN_SEQ=1 walks the same steps one by one.  Same iterates, bit for
+    bit: every point count up to the device limit, narrow and wide intervals."""
+    rng = np.random.default_rng(11)
+    cases = [(1.0, 3.0, 8, 10_000), (4.7e-3, 7.995, 12, 10_000), (1e-3, 1e2, 16, 10_000),
+             (0.0, 4.0, 4, 100_000), (2.0, 2.0 + 1e-9, 6, 1000)]
+    for _ in range(6):
+        lo = float(np.exp(rng.uniform(np.log(1e-4), np.log(10.0))))
+        cases.append((lo, lo * float(np.exp(rng.uniform(0.1, 9.0))), int(rng.integers(3, 17)),
+                      int(rng.integers(60, 20_000))))
+    for lo, hi, count, grid in cases:
+        monkeypatch.setenv("SSCG_GOLDEN_SEQ", "1")
+        seq = leja_points(lo, hi, count, grid)
+        monkeypatch.setenv("SSCG_GOLDEN_SEQ", "0")
+        two = leja_points(lo, hi, count, grid)
+        np.testing.assert_array_equal(two, seq, err_msg=str((lo, hi, count, grid)))
+
+
 @pytest.mark.parametrize("grid", [10_000, 257, 50])
 @pytest.mark.parametrize("split", ["0", "1"])
 def test_graph_leja_forms_match_the_unit_entry(gpu_ready, split, grid, monkeypatch):
