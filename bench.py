@@ -136,11 +136,12 @@ def a_bytes_per_level(n, nnz, sched):
     """Bytes of the operator one matrix-powers level must stream: CSR
     (12 nnz + 4 (n+1)) or, for a pattern-compressed plan, the
     1- or 2-byte row ids (the pattern table lives in shared memory), or the
-    value stream's 8 bytes per union slot and row."""
+    value stream's 8 bytes per stored plane and row (every union slot, or the
+    diagonal and the upper offsets of a bitwise symmetric operator)."""
     if sched and sched.get("kind") == "pattern":
         return (1 if sched["patterns"] <= 256 else 2) * n
     if sched and sched.get("kind") == "stencil values":
-        return 8 * sched["slots"] * n
+        return 8 * sched.get("planes", sched["slots"]) * n  # symmetric form: half the planes
     return 12 * nnz + 4 * (n + 1)
 
 

@@ -333,13 +333,19 @@ def plan_mpk_schedule(lib, handle, sigma):
     """sscg_plan_mpk_schedule of a plan handle:
     {"kind": "csr"|"pattern"|"stencil values", "form": pattern kernel form ("table" walk,
     "superset" mask, plane "march", TMA-fed "tma march") or None, "ctas": G, "patterns": P (pattern),
-    "slots": union size (stencil values), "passes": [(1, 0)] * sigma (one launch per level)}."""
+    "slots": union size (stencil values), "planes": value planes streamed per level (the
+    symmetric form stores the diagonal and the upper offsets only), "passes": [(1, 0)] * sigma
+    (one launch per level)}."""
     out = np.zeros(4 + 2 * 16, dtype=np.int32)
     check(lib.sscg_plan_mpk_schedule(handle, int(sigma), iptr(out)))
     npass = int(out[3])
     kind = ("csr", "csr", "pattern", "stencil values")[int(out[0])]
     form = ("table", "superset", "march", "tma march")[int(out[-1])] if kind == "pattern" else None
+    slots = int(out[2]) if kind == "stencil values" else 0
+    if kind == "stencil values" and int(out[-1]) == 1:
+        form = "symmetric"  # the diagonal's and the upper offsets' planes only
     return {"kind": kind, "form": form, "ctas": int(out[1]),
             "patterns": int(out[2]) if kind == "pattern" else 0,
-            "slots": int(out[2]) if kind == "stencil values" else 0,
+            "slots": slots,
+            "planes": (slots + 1) // 2 if form == "symmetric" else slots,
             "passes": [(int(out[4 + 2 * q]), int(out[5 + 2 * q])) for q in range(npass)]}

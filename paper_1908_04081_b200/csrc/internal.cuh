@@ -165,6 +165,7 @@ struct Ctx {
   int vs_ne;
   int vs_off[VS_MAX_NE];
   const double* vs_val;
+  int vs_sym;  // symmetric form: planes of the diagonal and the upper offsets only (mpk.cu vs_request)
   // a row-partitioned value stream (vs_S > 0): local rows are whole global
   // planes of vs_S rows in a permuted order, so a slot's neighbour is found
   // through plane tables, not by adding the offset: union offset k = vs_dz[k]

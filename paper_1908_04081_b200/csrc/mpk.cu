@@ -725,23 +725,46 @@ struct VsWalk {
   }
 };
 
-template <int NE>
+// SYM (Ctx::vs_sym: a bitwise symmetric operator whose union is NE offsets,
+// NE odd): only the diagonal's and the upper offsets' planes are stored
+// (vs_val[(k - NE/2) * ld + row], k >= NE/2).  The value of a lower offset -o
+// at row i is A[i][i - o] = A[i - o][i]: the upper plane of +o at row i - o --
+// the same coalesced stream, o rows earlier (0.0 where i - o < 0: no such
+// neighbour).  An element is read as an upper value by row i and as a lower one
+// by row i + o, at most vs_off[NE - 1] rows later: the second read comes from
+// L2, the DRAM stream is (NE + 1) / 2 planes instead of NE.
+template <int NE, bool SYM = false>
 __device__ __forceinline__ void vs_request(const Ctx& c, int i, int chunk, double (&v)[VS_CHUNK]) {
-  const double* vp = c.vs_val + i + (int64_t)(chunk * VS_CHUNK) * c.ld;
+  if (!SYM) {
+    const double* vp = c.vs_val + i + (int64_t)(chunk * VS_CHUNK) * c.ld;
 #pragma unroll
-  for (int kk = 0; kk < VS_CHUNK; ++kk)
-    if (chunk * VS_CHUNK + kk < NE) v[kk] = __ldg(vp + (int64_t)kk * c.ld);
+    for (int kk = 0; kk < VS_CHUNK; ++kk)
+      if (chunk * VS_CHUNK + kk < NE) v[kk] = __ldg(vp + (int64_t)kk * c.ld);
+  } else {
+    constexpr int MID = NE / 2;
+#pragma unroll
+    for (int kk = 0; kk < VS_CHUNK; ++kk) {
+      const int k = chunk * VS_CHUNK + kk;
+      if (k >= NE) continue;
+      if (k >= MID) {
+        v[kk] = __ldg(c.vs_val + i + (int64_t)(k - MID) * c.ld);
+      } else {
+        const int j = i + c.vs_off[k];  // the row that stores this entry
+        v[kk] = j >= 0 ? __ldg(c.vs_val + j + (int64_t)(NE - 1 - k - MID) * c.ld) : 0.0;
+      }
+    }
+  }
 }
 // the first row's first VS_DEPTH chunks
-template <int NE>
+template <int NE, bool SYM = false>
 __device__ __forceinline__ void vs_first(const Ctx& c, int i, double (&vq)[VS_DEPTH][VS_CHUNK]) {
 #pragma unroll
   constexpr int NCH = (NE + VS_CHUNK - 1) / VS_CHUNK;
 #pragma unroll
-  for (int d = 0; d < (VS_DEPTH < NCH ? VS_DEPTH : NCH); ++d) vs_request<NE>(c, i, d, vq[d]);
+  for (int d = 0; d < (VS_DEPTH < NCH ? VS_DEPTH : NCH); ++d) vs_request<NE, SYM>(c, i, d, vq[d]);
 }
 
-template <int NV, int NE, bool PL = false>
+template <int NV, int NE, bool PL = false, bool SYM = false>
 __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
                                        const double* const* __restrict__ xs, double* acc,
                                        double (&vq)[VS_DEPTH][VS_CHUNK], int inext, int blk = 0,
@@ -767,9 +790,9 @@ __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
 #pragma unroll
       for (int kk = 0; kk < VS_CHUNK; ++kk) vq[d][kk] = vq[d + 1][kk];
     if (ch + D < NCH)
-      vs_request<NE>(c, i, ch + D, vq[D - 1]);
+      vs_request<NE, SYM>(c, i, ch + D, vq[D - 1]);
     else if (inext >= 0)
-      vs_request<NE>(c, inext, ch + D - NCH, vq[D - 1]);
+      vs_request<NE, SYM>(c, inext, ch + D - NCH, vq[D - 1]);
 #pragma unroll
     for (int kk = 0; kk < VS_CHUNK; ++kk) {
       const int k = k0 + kk;
@@ -790,7 +813,7 @@ __device__ __forceinline__ void vs_row(const Ctx& c, int i, int nm1,
   }
 }
 
-template <int NE, bool PL>
+template <int NE, bool PL, bool SYM = false>
 __global__ void __launch_bounds__(ROWS_PER_CTA, VS_MINB) k_level0_vs(Ctx c, ZmPtrs zp) {
   __shared__ double sm[ROWS_PER_CTA / 32];
   const SolverState* st = c.st;
@@ -808,11 +831,11 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, VS_MINB) k_level0_vs(Ctx c, ZmPt
   const int stride = gridDim.x * blockDim.x;
   double vn[VS_DEPTH][VS_CHUNK];
   if ((int)(blockIdx.x * blockDim.x + threadIdx.x) < plim)
-    vs_first<NE>(c, blockIdx.x * blockDim.x + threadIdx.x, vn);
+    vs_first<NE, SYM>(c, blockIdx.x * blockDim.x + threadIdx.x, vn);
   VsWalk<PL> w(c, blockIdx.x * blockDim.x + threadIdx.x, stride);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride, w.next()) {
     double acc[3];
-    vs_row<3, NE, PL>(c, i, nm1, xs, acc, vn, i + stride < plim ? i + stride : -1, w.blk, w.pin);
+    vs_row<3, NE, PL, SYM>(c, i, nm1, xs, acc, vn, i + stride < plim ? i + stride : -1, w.blk, w.pin);
     const double p = xs[1][i], r = xs[2][i];
     if (i < n_own) {
       const double t = __dsub_rn(c.b[i], acc[0]);
@@ -837,7 +860,7 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, VS_MINB) k_level0_vs(Ctx c, ZmPt
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&c.st->breakdown, 1);
 }
 
-template <int NE, bool PL>
+template <int NE, bool PL, bool SYM = false>
 __global__ void __launch_bounds__(ROWS_PER_CTA, VS_MINB) k_level_vs(Ctx c, int l, ZmPtrs zp) {
   const SolverState* st = c.st;
   if (st->done) return;
@@ -854,16 +877,16 @@ __global__ void __launch_bounds__(ROWS_PER_CTA, VS_MINB) k_level_vs(Ctx c, int l
   const double* xs[2] = {zp.xs[0], zp.xs[1]};
   double vn[VS_DEPTH][VS_CHUNK];
   if ((int)(blockIdx.x * blockDim.x + threadIdx.x) < plim)
-    vs_first<NE>(c, blockIdx.x * blockDim.x + threadIdx.x, vn);
+    vs_first<NE, SYM>(c, blockIdx.x * blockDim.x + threadIdx.x, vn);
   VsWalk<PL> w(c, blockIdx.x * blockDim.x + threadIdx.x, stride);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < plim; i += stride, w.next()) {
     double acc[2];
     const bool rrow = do_r && i < rlim;
     const int inext = i + stride < plim ? i + stride : -1;
     if (rrow)
-      vs_row<2, NE, PL>(c, i, nm1, xs, acc, vn, inext, w.blk, w.pin);
+      vs_row<2, NE, PL, SYM>(c, i, nm1, xs, acc, vn, inext, w.blk, w.pin);
     else
-      vs_row<1, NE, PL>(c, i, nm1, xs, acc, vn, inext, w.blk, w.pin);
+      vs_row<1, NE, PL, SYM>(c, i, nm1, xs, acc, vn, inext, w.blk, w.pin);
     const double wp = recur(acc[0], xs[0][i], use_mu ? zp.ym[0][i] : 0.0, th, ga, mu, use_mu);
     zp.yo[0][i] = wp;
     bad |= !finite(wp);
@@ -1235,6 +1258,20 @@ void launch_level(const Ctx& c, int level, int sigma, cudaStream_t s) {
     k_level_vs<NE, true><<<c.pat_grid, ROWS_PER_CTA, 0, s>>>(c, level, zp);  \
   else                                                                       \
     k_level_vs<NE, false><<<c.pat_grid, ROWS_PER_CTA, 0, s>>>(c, level, zp);
+#define VS_LAUNCH_SYM(NE)                                                          \
+  if (level == 0)                                                                  \
+    k_level0_vs<NE, false, true><<<c.red_n, ROWS_PER_CTA, 0, s>>>(c, zp);          \
+  else                                                                             \
+    k_level_vs<NE, false, true><<<c.pat_grid, ROWS_PER_CTA, 0, s>>>(c, level, zp);
+    if (c.vs_sym && !c.vs_S && (c.vs_ne == 9 || c.vs_ne == 27)) {
+      if (c.vs_ne == 9) {
+        VS_LAUNCH_SYM(9)
+      } else {
+        VS_LAUNCH_SYM(27)
+      }
+      return;
+    }
+#undef VS_LAUNCH_SYM
     switch (ne) {
       case 9: VS_LAUNCH(9) break;
       case 18: VS_LAUNCH(18) break;

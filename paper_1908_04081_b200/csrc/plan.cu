@@ -156,6 +156,7 @@ struct sscg_plan {
   int vs_ne = 0;  // value-stream stencil form (vs_setup); 0: not used
   int vs_off[VS_MAX_NE] = {};
   double* d_vs_val = nullptr;
+  int vs_sym = 0;  // the value stream holds the diagonal's and the upper offsets' planes only
   int64_t vs_S = 0;  // partitioned value stream: plane size (0: plain offsets)
   int vs_np = 0;
   signed char vs_dz[VS_MAX_NE] = {};
@@ -319,6 +320,7 @@ Ctx make_ctx(sscg_plan* p) {
   c.vs_ne = p->vs_ne;
   for (int k = 0; k < VS_MAX_NE; ++k) c.vs_off[k] = p->vs_off[k];
   c.vs_val = p->d_vs_val;
+  c.vs_sym = p->vs_sym;
   c.vs_S = p->vs_S;
   c.vs_np = p->vs_np;
   for (int k = 0; k < VS_MAX_NE; ++k) {
@@ -1221,8 +1223,42 @@ int vs_setup(sscg_plan* p, int64_t n, const int64_t* row_ptr, const int32_t* col
     CUDA_OK(cudaMemcpy(p->d_vs_geo, below.data(), 4 * nblk, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(p->d_vs_base, above.data(), 4 * nblk, cudaMemcpyHostToDevice));
   }
-  TRY(dalloc(p, &p->d_vs_val, sv_len));
-  TRY(copy_h2d(p, p->d_vs_val, sv.get(), 8 * sv_len));
+  // A bitwise symmetric operator (every A[i][i - o] equals A[i - o][i] bit for
+  // bit, the union symmetric, no bucket padding) streams half of its planes:
+  // the lower offsets read the upper planes o rows earlier (vs_request)
+  p->vs_sym = 0;
+  if (!grows && ne == nb && (ne & 1) && atoi(env_or("SSCG_VS_SYM", "1")) != 0) {
+    const int mid = ne / 2;
+    bool sym = uni[(size_t)mid] == 0;
+    for (int k = 0; k < mid && sym; ++k) sym = uni[(size_t)k] == -uni[(size_t)(ne - 1 - k)];
+    std::atomic<bool> asym{!sym};
+    if (sym)
+      on_ranges([&](int t) {
+        for (int k = 0; k < mid; ++k) {
+          const int64_t o = uni[(size_t)k];  // < 0
+          const double* lo_p = sv.get() + (size_t)k * (size_t)p->ld;
+          const double* up_p = sv.get() + (size_t)(ne - 1 - k) * (size_t)p->ld;
+          for (int64_t i = n * t / T; i < n * (t + 1) / T; ++i) {
+            const int64_t j = i + o;
+            const double want = j >= 0 ? up_p[j] : 0.0;
+            if (std::memcmp(&lo_p[i], &want, sizeof(double)) != 0) {
+              asym.store(true, std::memory_order_relaxed);
+              return;
+            }
+          }
+          if (asym.load(std::memory_order_relaxed)) return;
+        }
+      });
+    p->vs_sym = asym.load() ? 0 : 1;
+  }
+  if (p->vs_sym) {
+    const size_t half = (size_t)(ne - ne / 2) * (size_t)p->ld;
+    TRY(dalloc(p, &p->d_vs_val, half));
+    TRY(copy_h2d(p, p->d_vs_val, sv.get() + (size_t)(ne / 2) * (size_t)p->ld, 8 * half));
+  } else {
+    TRY(dalloc(p, &p->d_vs_val, sv_len));
+    TRY(copy_h2d(p, p->d_vs_val, sv.get(), 8 * sv_len));
+  }
   p->vs_ne = ne;
   for (int k = 0; k < VS_MAX_NE; ++k) p->vs_off[k] = k < ne ? (int)uni[(size_t)k] : 0;  // (plain form)
   int sms = NUM_SMS;
@@ -1788,6 +1824,7 @@ int sscg_plan_mpk_schedule(sscg_plan* p, int32_t sigma, int32_t* out) {
   // last slot: pattern kernel form (0 table walk, 1 superset mask, 2 plane
   // march, 3 the TMA plane march)
   if (p->d_pid) out[3 + 2 * SMAX] = p->zm_S > 0 ? (p->tm_on ? 3 : 2) : p->ss_ne > 0 ? 1 : 0;
+  if (!p->d_pid && p->vs_ne) out[3 + 2 * SMAX] = p->vs_sym;  // value stream: 1 = symmetric form (half the planes)
   if (p->tm_on) out[1] = p->tm_grid;
   out[3] = sigma;
   for (int q = 0; q < sigma; ++q) out[4 + 2 * q] = 1;
