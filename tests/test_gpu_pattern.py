@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 
 _KEYS = ("SSCG_PATTERN", "SSCG_PAT_SS", "SSCG_ZM", "SSCG_ZM_ZC", "SSCG_ZM_2D", "SSCG_VS",
-         "SSCG_ZM_DYN", "SSCG_TM")
+         "SSCG_ZM_DYN", "SSCG_TM", "SSCG_TM_EXACT", "SSCG_VS_SYM")
 
 
 def _with_env(env, fn):
@@ -185,6 +185,36 @@ def test_value_stream_bit_identical_to_csr(gpu_ready, key, kw):
     np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
     np.testing.assert_array_equal(got[0], ref[0])
     assert got[1].total_outer == ref[1].total_outer
+    # these operators are bitwise symmetric: the default streams the diagonal's
+    # and the upper offsets' planes only; the full-plane form must agree too
+    assert s1["form"] == "symmetric" and s1["planes"] == 14, s1
+    s2, full = _with_env({"SSCG_VS_SYM": "0"}, run)
+    assert s2["form"] is None and s2["planes"] == 27, s2
+    np.testing.assert_array_equal(full[2].alphas, ref[2].alphas)
+    np.testing.assert_array_equal(full[0], ref[0])
+
+
+def test_value_stream_symmetric_form_needs_bitwise_symmetry(gpu_ready):
+    """One entry one ulp away from its mirror image: the plan must keep every
+    plane (the symmetric form would read the mirror's bits), and the solve
+    stays the CSR kernels'."""
+    cfg = AdaptiveConfig(sigma=8, eps_star=1e-8, basis_kind="newton", max_outer=12)
+
+    def run():
+        prob = problems.make_problem("c4j", scale=16)
+        a = prob.a
+        a.values = np.array(a.values, copy=True)
+        i = a.n // 2
+        j = int(a.row_ptr[i])  # the row's first (a lower) entry
+        assert a.col_idx[j] < i
+        a.values[j] = np.nextafter(a.values[j], np.inf)
+        return _plan(a).mpk_schedule(cfg.sigma), adaptive_solve(prob, cfg, trace="fast")
+
+    s0, ref = _with_env({"SSCG_VS": "0"}, run)
+    s1, got = _with_env({}, run)
+    assert s1["kind"] == "stencil values" and s1["form"] is None and s1["planes"] == 27, s1
+    np.testing.assert_array_equal(got[2].alphas, ref[2].alphas)
+    np.testing.assert_array_equal(got[0], ref[0])
 
 
 
